@@ -1,0 +1,349 @@
+#!/usr/bin/env python3
+"""Headline benchmark: BASELINE.json config 1 — batched objective evaluation, fp64, D=1000,
+pop=1024 (seed 7), on 1 B200 (N>1: independent replicas, weak scaling).
+
+One step = the three config-1 objectives (elliptic, Rastrigin, Ackley; shared o and M)
+evaluated over the 1024-point population through ``evaluate_batch`` — 3 launches of the fused
+TMA + DMMA kernel, 3072 objective evaluations.  The reference arm (``--impl reference``) does the
+identical work through the reference's own ``problems::evaluate_batch`` (compiled from
+/root/reference by oracle/Makefile into oracle/_ref) on all host cores.
+
+Timing: W warm-up steps, then K steps each bracketed by CUDA events on the launching stream; L2
+is flushed (256 MiB write) between steps outside the events; barrier + synchronize on both
+sides; max over ranks.  ``e2e`` repeats the step through the C-ABI host-buffer entry point
+(evb_evaluate_batch_host: pinned X in, fitness out, inside the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "oracle"))
+
+D, P, SEED = 1000, 1024, 7
+KINDS = ("elliptic", "rastrigin", "ackley")
+METRIC = "objective evals/sec (D=1000, pop 1024, fp64) and % of FP64/HBM roofline, 1 B200"
+UNIT = "evals/s"
+CONFIG = {
+    "workload": "config1: batched shifted-rotated evaluation, fp64, D=1000, pop=1024, seed 7; "
+                "one step = elliptic + Rastrigin + Ackley over the population (3 x evaluate_batch)",
+    "dim": D,
+    "pop": P,
+    "objectives_per_step": 3,
+    "evals_per_step": 3 * P,
+    "l2": "flushed between steps (256 MiB write outside the timed events)",
+    "parallelism": "replicas",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="evb", choices=["evb", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """NVML sampling of SM clocks and throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def make_inputs():
+    import oracle as O  # seeded input generator (restated draw_shift / random_rotation / init_population)
+
+    o, m = O.shift_rotation(SEED, D)
+    X = O.population(SEED, P, D)
+    return o, m, X
+
+
+def cpu_baseline_reference(o, m, X, budget_s: float = 10.0):
+    """The reference's own evaluate_batch (oracle/_ref, -O3 -march, all host threads)."""
+    import numpy as np
+
+    import oracle as O
+
+    L = O.REF_FAST()
+    threads = os.cpu_count() or 1
+    n = P
+    jobs = []
+    keep = []
+    for kind in KINDS:
+        kid = {"elliptic": 1, "rastrigin": 5, "ackley": 6}[kind]
+        mr = np.ascontiguousarray(m.ravel())
+        keep.append(mr)
+        jobs.append(L.ref_batch_job_create(1, kid, D, O.ptr(o), O.ptr(mr), 0.0, n, O.ptr(X)))
+    L.ref_batch_job_run(jobs[0], threads, None)  # warm-up
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        for j in jobs:
+            L.ref_batch_job_run(j, threads, None)
+        reps += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    el = time.perf_counter() - t0
+    for j in jobs:
+        L.ref_batch_job_destroy(j)
+    return {
+        "value": reps * 3 * n / el,
+        "unit": UNIT,
+        "cores": threads,
+        "kind": "reference",
+        "sample": f"{reps} full config-1 steps (3 x evaluate_batch of {n} points, D={D}, fp64) in {el:.1f} s, "
+                  f"batch split into {threads} contiguous slices; {L._evb_name}",
+    }
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference CPU implementation on the host cores, same metric."""
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle as O
+
+    o, m, X = make_inputs()
+    L = O.REF_FAST()
+    threads = os.cpu_count() or 1
+    sample = 128  # points per objective per step: a bounded sample of the 1024-point step
+    jobs, keep = [], []
+    for kind in KINDS:
+        kid = {"elliptic": 1, "rastrigin": 5, "ackley": 6}[kind]
+        mr = np.ascontiguousarray(m.ravel())
+        keep.append(mr)
+        jobs.append(L.ref_batch_job_create(1, kid, D, O.ptr(o), O.ptr(mr), 0.0, sample, O.ptr(X)))
+    for _ in range(args.warmup):
+        for j in jobs:
+            L.ref_batch_job_run(j, threads, None)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        for j in jobs:
+            L.ref_batch_job_run(j, threads, None)
+        times.append(time.perf_counter() - t0)
+    for j in jobs:
+        L.ref_batch_job_destroy(j)
+    total = sum(times)
+    value = args.steps * 3 * sample / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": dict(CONFIG, reference_sample_points_per_objective=sample),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"3 x evaluate_batch of {sample} of the {P} points per step, {threads} threads, "
+                                   f"{L._evb_name} (reference headers, -O3 -march)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_evb(args, rank, world, local):
+    import numpy as np
+    import torch
+
+    import paper_2505_17430_b200 as evb
+    from paper_2505_17430_b200 import _lib
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist = None
+
+    o, m, X = make_inputs()
+    kinds = [getattr(evb.BaseKind, k) for k in KINDS]
+    probs = [evb.ProblemInstance.base(k, o, m, 0.0) for k in kinds]
+    sc = evb.EvalScratch()
+    Xd = torch.from_numpy(X).to(dev)
+    outs = [torch.empty(P, dtype=torch.float64, device=dev) for _ in kinds]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(evs=None):
+        for i, p in enumerate(probs):
+            if evs is not None:
+                evs[2 * i].record(stream)
+            evb.evaluate_batch(p, Xd, sc, outs[i], stream)
+            if evs is not None:
+                evs[2 * i + 1].record(stream)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * len(probs))] for _ in range(args.steps)]
+    launches0 = evb.launch_count()
+    sampler = ClockSampler(local)
+    with sampler:
+        for s in range(args.steps):
+            flush.zero_()  # L2 flush outside the timed events
+            step(ev[s])
+        torch.cuda.synchronize()
+    launches = evb.launch_count() - launches0
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    launch_ms = [e[2 * i].elapsed_time(e[2 * i + 1]) for e in ev for i in range(len(probs))]
+    step_ms = [sum(e[2 * i].elapsed_time(e[2 * i + 1]) for i in range(len(probs))) for e in ev]
+    total_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * args.steps * 3 * P / (total_ms * 1e-3)
+
+    # ---- roofline (dominant kernel: the fused DMMA evaluation) ----
+    flops_per_launch = 2.0 * D * D * P  # algorithmic: the z = M(x - o) contraction
+    avg_launch_s = statistics.mean(launch_ms) * 1e-3
+    achieved = flops_per_launch / avg_launch_s / 1e12
+    peak = _lib.probe_peak_tflops(0)
+    traffic = None
+    tfile = ROOT / "profiles" / "traffic.json"
+    if tfile.exists():
+        try:
+            traffic = json.loads(tfile.read_text()).get("eval_f64_dmma_kernel")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": traffic,
+                "peak_source": "measured in-run: DMMA m8n8k4 throughput kernel over all SMs "
+                               "(MEASURED_PEAKS.json has no FP64 figure)",
+                "algorithmic": f"2*D^2*P = {flops_per_launch:.4g} flop per launch; compulsory bytes "
+                               f"8*(D^2+P*D+D+P) = {8 * (D * D + P * D + D + P) / 1e6:.2f} MB"}
+
+    # ---- e2e: host buffers through the C ABI (pinned X in, fitness out) ----
+    Xh = torch.from_numpy(X).pin_memory()
+    outh = [torch.empty(P, dtype=torch.float64).pin_memory() for _ in kinds]
+    import ctypes
+
+    L = _lib.lib()
+
+    def e2e_step():
+        for i, p in enumerate(probs):
+            _lib.check(L.evb_evaluate_batch_host(p.handle, sc.handle, ctypes.c_void_p(Xh.data_ptr()), P, D,
+                                                 ctypes.c_void_p(outh[i].data_ptr())), "e2e")
+
+    for _ in range(max(3, args.warmup // 2)):
+        e2e_step()
+    e2e_steps = max(10, min(args.steps, 100))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": world * e2e_steps * 3 * P / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 3 * P * D * 8,
+           "d2h_bytes_per_step": 3 * P * 8,
+           "how": "3 x evb_evaluate_batch_host per step (C ABI, pinned host X copied in per call, fitness copied out), "
+                  "wall clock with device sync, max over ranks"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded draw_shift / random_rotation / "
+                                                     "init_population, seed 7)",
+        "config": CONFIG, "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
+        "clocks": sampler.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline_reference(o, m, X)
+        except Exception as exc:  # the checker is test infrastructure; report, do not crash the bench
+            line["cpu_baseline"] = {"value": None, "unavailable": str(exc)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_evb(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

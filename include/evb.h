@@ -1,0 +1,139 @@
+/*
+ * evb.h — C ABI of the B200-native SEvoBench hot path (libevb.so).
+ *
+ * Plain C: opaque handles, plain pointers and sizes, integer status codes,
+ * a thread-local last-error string, and an explicit cudaStream_t (passed as
+ * void*) on every device call. No exception crosses this boundary and no
+ * torch type appears in it. Status codes map onto the reference's error
+ * conventions:
+ *
+ *   EVB_ERR_INVALID_ARGUMENT  -> std::invalid_argument  (problems/instance.hpp:222-223,
+ *                                                       problems/batch.hpp:250-252)
+ *   EVB_ERR_CONFIG            -> evobench::config_error (common.hpp:12-15, 25-28)
+ *   EVB_ERR_LOGIC             -> std::logic_error       (de/engine.hpp:32-33)
+ *   EVB_ERR_RUNTIME           -> std::runtime_error     (CUDA / allocation failures)
+ *
+ * All file:line citations point into the reference tree
+ * (/root/reference/proj/include/evobench/...).  There is no CPU fallback:
+ * every compute entry point launches sm_100a kernels or fails.
+ */
+#ifndef EVB_H_
+#define EVB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EVB_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define EVB_API __attribute__((visibility("default")))
+#else
+#define EVB_API
+#endif
+
+enum evb_status {
+  EVB_OK = 0,
+  EVB_ERR_INVALID_ARGUMENT = 1,
+  EVB_ERR_CONFIG = 2,
+  EVB_ERR_LOGIC = 3,
+  EVB_ERR_RUNTIME = 4
+};
+
+/* Arithmetic type of a problem / engine: the reference's template parameter T. */
+enum evb_dtype { EVB_F32 = 0, EVB_F64 = 1 };
+
+/* Same order as evobench::problems::base_kind (problems/functions.hpp:15-26). */
+enum evb_base_kind {
+  EVB_SPHERE = 0,
+  EVB_ELLIPTIC = 1,
+  EVB_BENT_CIGAR = 2,
+  EVB_DISCUS = 3,
+  EVB_ROSENBROCK = 4,
+  EVB_RASTRIGIN = 5,
+  EVB_ACKLEY = 6,
+  EVB_GRIEWANK = 7,
+  EVB_SCHWEFEL_12 = 8,
+  EVB_EXPANDED_SCHAFFER_F6 = 9
+};
+
+typedef struct evb_problem_s* evb_problem; /* immutable device-resident problem_instance */
+typedef struct evb_scratch_s* evb_scratch; /* per-task evaluation scratch (eval_scratch)   */
+
+/* ---- library ---------------------------------------------------------------------- */
+
+EVB_API int evb_abi_version(void);
+/* Message of the last failing call on this thread ("" if none). */
+EVB_API const char* evb_last_error(void);
+/* Device properties the kernels size themselves by (SM count, smem/SM, L2 bytes). */
+EVB_API int evb_device_info(int device, int* sm_count, int* smem_per_sm, int* l2_bytes, int* cc_major,
+                    int* cc_minor);
+
+/* ---- problems (problems/instance.hpp:180-252) -------------------------------------- */
+
+/* Shifted-rotated base problem: value(x) = base(M (x - o)) + bias, rosenbrock on z + 1
+ * (problems/instance.hpp:221-228, 82-91). shift (dim) and rotation (dim*dim, row-major)
+ * are HOST pointers of the problem dtype; they are copied to the device once. */
+EVB_API int evb_problem_create_base(int dtype, int dim, int kind, const void* shift,
+                            const void* rotation, double bias, evb_problem* out);
+
+/* Hybrid problem (problems/instance.hpp:97-112, 229-231): z = M (x - o), permute, split into
+ * chunks, sum per-chunk base values, plus bias. */
+EVB_API int evb_problem_create_hybrid(int dtype, int dim, const void* shift, const void* rotation,
+                              double bias, int n_chunks, const int* sub_kinds,
+                              const int* chunk_sizes, const int* permutation, evb_problem* out);
+
+/* Composition problem (problems/instance.hpp:116-174, 232): n_comp components, each with its
+ * own shift (n_comp*dim) and rotation (n_comp*dim*dim), sigma, lambda and bias. */
+EVB_API int evb_problem_create_composition(int dtype, int dim, int n_comp, const int* kinds,
+                                   const void* shifts, const void* rotations,
+                                   const double* sigma, const double* lambda,
+                                   const double* comp_bias, double bias, evb_problem* out);
+
+EVB_API int evb_problem_destroy(evb_problem p);
+EVB_API int evb_problem_dim(evb_problem p);
+EVB_API int evb_problem_dtype(evb_problem p);
+
+/* ---- scratch (problems/instance.hpp:45-56) ----------------------------------------- */
+
+EVB_API int evb_scratch_create(evb_scratch* out);
+EVB_API int evb_scratch_destroy(evb_scratch s);
+
+/* ---- batched evaluation (problems/batch.hpp:243-278) ------------------------------- */
+
+/* out[b] = problem.evaluate(X[b]) for b < n_points.  X and out are DEVICE pointers of the
+ * problem dtype; X is row-major with row stride ldx elements (ldx >= dim).  n_points == 0
+ * is valid and launches nothing (problems/batch.hpp:247-249).  ldx < dim is the analogue of
+ * the reference's dimension mismatch -> EVB_ERR_INVALID_ARGUMENT. */
+EVB_API int evb_evaluate_batch(evb_problem p, evb_scratch s, const void* X, int64_t n_points,
+                       int64_t ldx, void* out, void* stream);
+
+/* Several base kinds on ONE z = M (x - o) (BASELINE config 1: "three transforms are
+ * evaluated on the same z").  Base problems only; kinds[k] in {sphere, elliptic, bent_cigar,
+ * discus, rastrigin, ackley, griewank}; out[k*ldo + b] = base_k(z_b) + biases[k]. */
+EVB_API int evb_evaluate_batch_multi(evb_problem p, evb_scratch s, int n_kinds, const int* kinds,
+                             const double* biases, const void* X, int64_t n_points,
+                             int64_t ldx, void* out, int64_t ldo, void* stream);
+
+/* Host-buffer form (batched_evaluate, problems/batch.hpp:281-288): X_host (n_points*ldx) and
+ * out_host (n_points) are host memory; the call copies in, evaluates and copies out on the
+ * scratch's own stream and returns when out_host is filled. */
+EVB_API int evb_evaluate_batch_host(evb_problem p, evb_scratch s, const void* X_host, int64_t n_points,
+                            int64_t ldx, void* out_host);
+
+/* Kernel launches this library has issued on the calling thread (monotonic counter; used by
+ * bench.py to report gpu_launches inside its timed region). */
+EVB_API int evb_launch_count(void);
+
+/* Live roofline denominator: which = 0 -> FP64 tensor (DMMA m8n8k4) TFLOP/s, which = 1 -> FP32
+ * FFMA TFLOP/s, measured by a throughput kernel over every SM (best of 3 launches). */
+EVB_API int evb_probe_peak_tflops(int which, int iters, double* tflops);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* EVB_H_ */

@@ -1,0 +1,399 @@
+// capi.cu — the extern "C" boundary of libevb (include/evb.h).
+//
+// Host C++ owns the problem/scratch objects; every entry point converts internal exceptions
+// into status codes plus a thread-local message, so no exception crosses the ABI.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "evb_internal.cuh"
+
+namespace evb {
+
+namespace {
+thread_local std::string g_last_error;
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    g_last_error.clear();
+    return EVB_OK;
+  } catch (const invalid_argument& e) {
+    g_last_error = e.what();
+    return EVB_ERR_INVALID_ARGUMENT;
+  } catch (const config_error& e) {
+    g_last_error = e.what();
+    return EVB_ERR_CONFIG;
+  } catch (const logic_error& e) {
+    g_last_error = e.what();
+    return EVB_ERR_LOGIC;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return EVB_ERR_RUNTIME;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return EVB_ERR_RUNTIME;
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+size_t elem_size(int dtype) { return dtype == EVB_F64 ? 8 : 4; }
+
+void check_dtype(int dtype) {
+  require(dtype == EVB_F32 || dtype == EVB_F64, "problem: dtype must be EVB_F32 or EVB_F64");
+}
+void check_kind(int kind) {
+  require(kind >= EVB_SPHERE && kind <= EVB_EXPANDED_SCHAFFER_F6, "problem: unknown base kind");
+}
+
+template <typename T>
+std::vector<T> elliptic_weights(int len) {
+  // pow(T(10), T(6) * T(i) / T(max(len - 1, 1))) in T, as problems/functions.hpp:57-60 and
+  // problems/batch.hpp:109-111 compute it.
+  std::vector<T> w(std::max(len, 1));
+  const T denom = T(std::max(len - 1, 1));
+  for (int i = 0; i < len; ++i) w[i] = std::pow(T(10), T(6) * T(i) / denom);
+  return w;
+}
+
+void* upload(const void* host, size_t bytes) {
+  void* d = nullptr;
+  EVB_CUDA(cudaMalloc(&d, std::max<size_t>(bytes, 16)));
+  if (bytes) EVB_CUDA(cudaMemcpy(d, host, bytes, cudaMemcpyHostToDevice));
+  return d;
+}
+
+// rows x dim (stride src_ld) -> device rows x ld, zero padded, plus `extra` zero elements
+void* upload_padded(const void* host, int rows, int dim, int ld, int extra, size_t es) {
+  std::vector<uint8_t> buf(size_t(rows) * ld * es + size_t(extra) * es, 0);
+  for (int r = 0; r < rows; ++r)
+    std::memcpy(buf.data() + size_t(r) * ld * es, static_cast<const uint8_t*>(host) + size_t(r) * dim * es,
+                size_t(dim) * es);
+  return upload(buf.data(), buf.size());
+}
+
+template <typename T>
+void* upload_weights(const std::vector<T>& w) {
+  return upload(w.data(), w.size() * sizeof(T));
+}
+
+void fill_weights(device_problem& p) {
+  if (p.dtype == EVB_F64) p.ell_w = upload_weights(elliptic_weights<double>(p.dim));
+  else p.ell_w = upload_weights(elliptic_weights<float>(p.dim));
+}
+
+void free_problem(device_problem& p) {
+  void* ptrs[] = {p.shift, p.rotation, p.ell_w, p.hyb_w, p.perm, p.sub_kinds, p.chunk_sizes, p.comp_kinds,
+                  p.comp_shift, p.comp_rot, p.comp_sigma, p.comp_lambda, p.comp_bias};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+}
+
+}  // namespace
+
+bool make_tma_2d(CUtensorMap* map, const void* base, int dtype, uint64_t inner_elems, uint64_t outer_rows,
+                 uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {inner_elems, outer_rows};
+  const cuuint64_t strides[1] = {row_stride_bytes};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = enc(map, dtype == EVB_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                         const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace evb
+
+using namespace evb;
+
+extern "C" {
+
+int evb_abi_version(void) { return EVB_ABI_VERSION; }
+
+const char* evb_last_error(void) { return g_last_error.c_str(); }
+
+int evb_device_info(int device, int* sm_count, int* smem_per_sm, int* l2_bytes, int* cc_major, int* cc_minor) {
+  return guarded([&] {
+    cudaDeviceProp pr;
+    EVB_CUDA(cudaGetDeviceProperties(&pr, device));
+    if (sm_count) *sm_count = pr.multiProcessorCount;
+    if (smem_per_sm) *smem_per_sm = int(pr.sharedMemPerMultiprocessor);
+    if (l2_bytes) *l2_bytes = pr.l2CacheSize;
+    if (cc_major) *cc_major = pr.major;
+    if (cc_minor) *cc_minor = pr.minor;
+  });
+}
+
+int evb_problem_create_base(int dtype, int dim, int kind, const void* shift, const void* rotation, double bias,
+                            evb_problem* out) {
+  return guarded([&] {
+    check_dtype(dtype);
+    check_kind(kind);
+    require(dim >= 1, "problem: dim must be positive");
+    require(shift && rotation && out, "problem: null shift, rotation or output handle");
+    auto* h = new evb_problem_s();
+    device_problem& p = h->p;
+    try {
+      p.dtype = dtype;
+      p.dim = dim;
+      p.ld = int(round_up(dim, kLdAlign));
+      p.spec = SPEC_BASE;
+      p.kind = kind;
+      p.bias = bias;
+      const size_t es = elem_size(dtype);
+      p.shift = upload_padded(shift, 1, dim, p.ld, 64, es);
+      p.rotation = upload_padded(rotation, dim, dim, p.ld, 0, es);
+      fill_weights(p);
+    } catch (...) {
+      free_problem(p);
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int evb_problem_create_hybrid(int dtype, int dim, const void* shift, const void* rotation, double bias, int n_chunks,
+                              const int* sub_kinds, const int* chunk_sizes, const int* permutation, evb_problem* out) {
+  return guarded([&] {
+    check_dtype(dtype);
+    require(dim >= 1, "problem: dim must be positive");
+    require(shift && rotation && out && sub_kinds && chunk_sizes && permutation,
+            "hybrid: null input pointer");
+    require(n_chunks >= 1, "hybrid: at least one chunk");
+    int total = 0;
+    for (int c = 0; c < n_chunks; ++c) {
+      check_kind(sub_kinds[c]);
+      require(chunk_sizes[c] >= 1, "hybrid: every chunk needs at least one dimension");
+      total += chunk_sizes[c];
+    }
+    require(total == dim, "hybrid: chunk sizes must sum to dim");
+    std::vector<int> seen(dim, 0);
+    for (int i = 0; i < dim; ++i) {
+      require(permutation[i] >= 0 && permutation[i] < dim && !seen[permutation[i]],
+              "hybrid: permutation must use every dimension once");
+      seen[permutation[i]] = 1;
+    }
+    auto* h = new evb_problem_s();
+    device_problem& p = h->p;
+    try {
+      p.dtype = dtype;
+      p.dim = dim;
+      p.ld = int(round_up(dim, kLdAlign));
+      p.spec = SPEC_HYBRID;
+      p.bias = bias;
+      const size_t es = elem_size(dtype);
+      p.shift = upload_padded(shift, 1, dim, p.ld, 64, es);
+      p.rotation = upload_padded(rotation, dim, dim, p.ld, 0, es);
+      fill_weights(p);
+      p.n_chunks = n_chunks;
+      p.perm = static_cast<int*>(upload(permutation, sizeof(int) * dim));
+      p.sub_kinds = static_cast<int*>(upload(sub_kinds, sizeof(int) * n_chunks));
+      p.chunk_sizes = static_cast<int*>(upload(chunk_sizes, sizeof(int) * n_chunks));
+      // per-chunk elliptic weights: kernels::elliptic sees only the chunk (len - 1 denominator)
+      if (dtype == EVB_F64) {
+        std::vector<double> w;
+        for (int c = 0; c < n_chunks; ++c) {
+          auto wc = elliptic_weights<double>(chunk_sizes[c]);
+          w.insert(w.end(), wc.begin(), wc.begin() + chunk_sizes[c]);
+        }
+        p.hyb_w = upload_weights(w);
+      } else {
+        std::vector<float> w;
+        for (int c = 0; c < n_chunks; ++c) {
+          auto wc = elliptic_weights<float>(chunk_sizes[c]);
+          w.insert(w.end(), wc.begin(), wc.begin() + chunk_sizes[c]);
+        }
+        p.hyb_w = upload_weights(w);
+      }
+    } catch (...) {
+      free_problem(p);
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int evb_problem_create_composition(int dtype, int dim, int n_comp, const int* kinds, const void* shifts,
+                                   const void* rotations, const double* sigma, const double* lambda,
+                                   const double* comp_bias, double bias, evb_problem* out) {
+  return guarded([&] {
+    check_dtype(dtype);
+    require(dim >= 1, "problem: dim must be positive");
+    require(n_comp >= 1 && n_comp <= 8, "composition: 1 to 8 components supported");
+    require(kinds && shifts && rotations && sigma && lambda && comp_bias && out, "composition: null input pointer");
+    for (int c = 0; c < n_comp; ++c) check_kind(kinds[c]);
+    auto* h = new evb_problem_s();
+    device_problem& p = h->p;
+    try {
+      p.dtype = dtype;
+      p.dim = dim;
+      p.ld = int(round_up(dim, kLdAlign));
+      p.spec = SPEC_COMPOSITION;
+      p.bias = bias;
+      const size_t es = elem_size(dtype);
+      fill_weights(p);
+      p.n_comp = n_comp;
+      p.comp_kinds = static_cast<int*>(upload(kinds, sizeof(int) * n_comp));
+      p.comp_shift = upload_padded(shifts, n_comp, dim, p.ld, 64, es);
+      // rotations: n_comp blocks of dim rows
+      p.comp_rot = upload_padded(rotations, n_comp * dim, dim, p.ld, 0, es);
+      p.comp_sigma = static_cast<double*>(upload(sigma, sizeof(double) * n_comp));
+      p.comp_lambda = static_cast<double*>(upload(lambda, sizeof(double) * n_comp));
+      p.comp_bias = static_cast<double*>(upload(comp_bias, sizeof(double) * n_comp));
+    } catch (...) {
+      free_problem(p);
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int evb_problem_destroy(evb_problem p) {
+  return guarded([&] {
+    if (!p) return;
+    free_problem(p->p);
+    delete p;
+  });
+}
+
+int evb_problem_dim(evb_problem p) { return p ? p->p.dim : -1; }
+int evb_problem_dtype(evb_problem p) { return p ? p->p.dtype : -1; }
+
+int evb_scratch_create(evb_scratch* out) {
+  return guarded([&] {
+    require(out != nullptr, "scratch: null output handle");
+    *out = new evb_scratch_s();
+  });
+}
+
+int evb_scratch_destroy(evb_scratch s) {
+  return guarded([&] {
+    if (!s) return;
+    void* ptrs[] = {s->partial, s->counters, s->zbuf, s->xpad, s->dx, s->dout, s->acc};
+    for (void* q : ptrs)
+      if (q) cudaFree(q);
+    if (s->own_stream) cudaStreamDestroy(s->own_stream);
+    delete s;
+  });
+}
+
+static void validate_eval(evb_problem p, evb_scratch s, int64_t n, int64_t ldx) {
+  if (!p || !s) throw config_error("evaluate_batch: null problem or scratch");
+  if (n < 0) throw invalid_argument("evaluate_batch: negative point count");
+  if (n > 0 && ldx < p->p.dim) throw invalid_argument("evaluate_batch: point dimension mismatch");
+  if (n > (int64_t(1) << 30)) throw invalid_argument("evaluate_batch: batch too large");
+}
+
+int evb_evaluate_batch(evb_problem p, evb_scratch s, const void* X, int64_t n_points, int64_t ldx, void* out,
+                       void* stream) {
+  return guarded([&] {
+    validate_eval(p, s, n_points, ldx);
+    if (n_points == 0) return;
+    if (!X || !out) throw config_error("evaluate_batch: null X or out");
+    eval_request rq{};
+    rq.prob = &p->p;
+    rq.scratch = s;
+    rq.X = X;
+    rq.n = n_points;
+    rq.ldx = ldx;
+    rq.out = out;
+    rq.ldo = n_points;
+    rq.n_out = 1;
+    rq.kinds[0] = p->p.kind;
+    rq.biases[0] = p->p.bias;
+    rq.stream = static_cast<cudaStream_t>(stream);
+    eval_dispatch(rq);
+  });
+}
+
+int evb_evaluate_batch_multi(evb_problem p, evb_scratch s, int n_kinds, const int* kinds, const double* biases,
+                             const void* X, int64_t n_points, int64_t ldx, void* out, int64_t ldo, void* stream) {
+  return guarded([&] {
+    validate_eval(p, s, n_points, ldx);
+    if (p->p.spec != SPEC_BASE) throw config_error("evaluate_batch_multi: base problems only");
+    if (n_kinds < 1 || n_kinds > 4) throw config_error("evaluate_batch_multi: 1 to 4 kinds");
+    if (!kinds || !biases) throw config_error("evaluate_batch_multi: null kinds or biases");
+    for (int k = 0; k < n_kinds; ++k) check_kind(kinds[k]);
+    if (n_points == 0) return;
+    if (!X || !out) throw config_error("evaluate_batch_multi: null X or out");
+    if (ldo < n_points) throw invalid_argument("evaluate_batch_multi: ldo < n_points");
+    eval_request rq{};
+    rq.prob = &p->p;
+    rq.scratch = s;
+    rq.X = X;
+    rq.n = n_points;
+    rq.ldx = ldx;
+    rq.out = out;
+    rq.ldo = ldo;
+    rq.n_out = n_kinds;
+    for (int k = 0; k < n_kinds; ++k) {
+      rq.kinds[k] = kinds[k];
+      rq.biases[k] = biases[k];
+    }
+    rq.stream = static_cast<cudaStream_t>(stream);
+    eval_dispatch(rq);
+  });
+}
+
+int evb_evaluate_batch_host(evb_problem p, evb_scratch s, const void* X_host, int64_t n_points, int64_t ldx,
+                            void* out_host) {
+  return guarded([&] {
+    validate_eval(p, s, n_points, ldx);
+    if (n_points == 0) return;
+    if (!X_host || !out_host) throw config_error("evaluate_batch_host: null X or out");
+    if (!s->own_stream) EVB_CUDA(cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking));
+    cudaStream_t st = s->own_stream;
+    const size_t es = elem_size(p->p.dtype);
+    const int64_t D = p->p.dim;
+    const int64_t ldd = round_up(D, 16 / int64_t(es));
+    ensure_buffer(&s->dx, &s->dx_bytes, size_t(ldd) * n_points * es, st);
+    ensure_buffer(&s->dout, &s->dout_bytes, size_t(n_points) * es, st);
+    EVB_CUDA(cudaMemcpy2DAsync(s->dx, ldd * es, X_host, ldx * es, D * es, n_points, cudaMemcpyHostToDevice, st));
+    eval_request rq{};
+    rq.prob = &p->p;
+    rq.scratch = s;
+    rq.X = s->dx;
+    rq.n = n_points;
+    rq.ldx = ldd;
+    rq.out = s->dout;
+    rq.ldo = n_points;
+    rq.n_out = 1;
+    rq.kinds[0] = p->p.kind;
+    rq.biases[0] = p->p.bias;
+    rq.stream = st;
+    eval_dispatch(rq);
+    EVB_CUDA(cudaMemcpyAsync(out_host, s->dout, size_t(n_points) * es, cudaMemcpyDeviceToHost, st));
+    EVB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int evb_launch_count(void) { return last_launch_count(); }
+
+}  // extern "C"

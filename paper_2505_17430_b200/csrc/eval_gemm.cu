@@ -1,0 +1,618 @@
+// eval_gemm.cu — large-dimension batched objective evaluation (K1 fp64 / K2 fp32).
+//
+// Replaces problems/batch.hpp:40-235 (transform_batch + base_kernel_batch) for base problems.
+//   z[b][i] = sum_k M[i][k] * (x_b[k] - o[k])        an NT GEMM: both operands K-contiguous
+//   f[b]    = base(z[b]) + bias                        fused epilogue + deterministic row sum
+//
+// Structure (one CTA per BM x BN output tile, warp-specialised):
+//   * producer warp: TMA (cp.async.bulk.tensor, SWIZZLE_128B) streams 16-double (fp64) or
+//     32-float (fp32) K-slices of X and M into a STAGES-deep mbarrier ring; the matching slice
+//     of the shift o rides along as a 128-byte bulk copy on the same barrier;
+//   * consumer warps: the shift is applied while fragments are loaded from shared memory
+//     (x - o rounded in T exactly like problems/batch.hpp:50), then
+//       fp64: DMMA m8n8k4 tensor-core tiles (the only FP64 tensor route on sm_100a;
+//             tcgen05 has no f64 kind),
+//       fp32: FFMA register-tiled outer products (1xTF32 fails the 1e-4 tolerance);
+//   * epilogue: per-element transform terms (elliptic / rastrigin / ackley / sphere /
+//     bent-cigar / discus / griewank) are reduced per row inside the CTA, written as per-N-tile
+//     partials, and the last CTA of each row block (ticket counter) sums the partials in fixed
+//     N-tile order and applies the final formula + bias.  No float atomics: results are
+//     deterministic run to run.
+//   * z-store mode writes z in the reference's SoA layout (soa_z[i*ldz + b]) for the kinds
+//     whose epilogue needs neighbours or prefixes (rosenbrock, schwefel_1.2, schaffer F6,
+//     hybrids); eval_rows.cu finishes those.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <type_traits>
+
+#include "evb_internal.cuh"
+#include "evb_math.cuh"
+#include "ptx.cuh"
+
+namespace evb {
+
+// ---------------------------------------------------------------------------------------
+// channel terms of the fused epilogue
+enum term_id {
+  TERM_SQ = 0,    // v*v
+  TERM_WSQ = 1,   // (w_i*v)*v                      elliptic
+  TERM_RAST = 2,  // v*v - 10 cos(2 pi v) + 10      rastrigin
+  TERM_COS = 3,   // cos(2 pi v)                    ackley
+  TERM_TAIL = 4,  // v*v for i >= 1                 bent cigar / discus
+  TERM_HEAD = 5,  // v at i == 0 (raw z0)           bent cigar / discus
+  TERM_GCOS = 6   // product of cos(v / sqrt(i+1))  griewank
+};
+
+constexpr int kMaxCh = 6;
+constexpr int kMaxOut = 4;
+
+template <typename T>
+struct fused_params {
+  int P, D;
+  const T* ell_w;  // elliptic weights (length D), may be null
+  int n_ch;
+  int ch_term[kMaxCh];
+  int n_out;
+  int out_kind[kMaxOut];
+  double out_bias[kMaxOut];
+  int out_ch0[kMaxOut], out_ch1[kMaxOut];
+  T* out;
+  int64_t ldo;
+  T* partial;          // [n_ch][n_ntiles][P]
+  unsigned* counters;  // [n_mtiles]
+  int n_ntiles;
+  T* zbuf;  // non-null: z-store mode, zbuf[i*ldz + b]
+  int64_t ldz;
+  const T* shift;  // padded with zeros beyond D
+};
+
+template <typename T>
+__device__ __forceinline__ T term_value(int term, T v, int col, const T* ell_w) {
+  using F = fop<T>;
+  switch (term) {
+    case TERM_SQ: return F::mul(v, v);
+    case TERM_WSQ: return elliptic_term<T>(ell_w[col], v);
+    case TERM_RAST: return rastrigin_term<T, true>(v);
+    case TERM_COS: return trig<T, true>::cos_(F::mul(two_pi_v<T>(), v));
+    case TERM_TAIL: return col >= 1 ? F::mul(v, v) : T(0);
+    case TERM_HEAD: return col == 0 ? v : T(0);
+    case TERM_GCOS: return trig<T, true>::cos_(F::div(v, F::sqrt_(T(col + 1))));
+  }
+  return T(0);
+}
+__device__ __forceinline__ bool term_is_product(int term) { return term == TERM_GCOS; }
+
+// Final formula per base kind from its channel sums (problems/batch.hpp:96-233).
+template <typename T>
+__device__ __forceinline__ T finalize(int kind, T s0, T s1, int D, T bias) {
+  using F = fop<T>;
+  T v;
+  switch (kind) {
+    case EVB_SPHERE:
+    case EVB_ELLIPTIC:
+    case EVB_RASTRIGIN: v = s0; break;
+    case EVB_BENT_CIGAR: v = F::add(F::mul(s1, s1), F::mul(T(1e6), s0)); break;  // s0 tail, s1 z0
+    case EVB_DISCUS: v = F::add(F::mul(F::mul(T(1e6), s1), s1), s0); break;
+    case EVB_ACKLEY: v = ackley_final<T>(s0, s1, D); break;  // s0 sum sq, s1 sum cos
+    case EVB_GRIEWANK: v = F::add(F::sub(F::div(s0, T(4000)), s1), T(1)); break;
+    default: v = T(0);
+  }
+  return F::add(v, bias);
+}
+
+// Shared tail of both kernels.  The accumulator tile has been parked in shared memory
+// (zt[r * ldt + c], reusing the drained pipeline buffers) so the transcendental-heavy epilogue
+// runs with the mainloop registers released.  Per channel: each consumer warp owns rows, lanes
+// stride over the tile's columns, a shuffle tree gives the row sum of this N-tile; the last CTA
+// of the row block (ticket counter) combines the N-tile partials in fixed order and applies
+// the final formula.  Deterministic: fixed reduction trees, no float atomics.
+struct epilogue_flag {
+  int last;
+};
+
+template <typename T, int BM, int BN>
+__device__ void tile_epilogue(const fused_params<T>& p, const T* zt, int ldt, int m0, int n0, int tid, int nthreads,
+                              int* last_flag) {
+  using F = fop<T>;
+  const int warp = tid >> 5, lane = tid & 31, nwarps = nthreads >> 5;
+  if (p.zbuf) {
+    // z-store: SoA z[i*ldz + b]; lanes over rows -> coalesced along b
+    for (int c = warp; c < BN; c += nwarps) {
+      const int col = n0 + c;
+      if (col >= p.D) break;
+      for (int r = lane; r < BM; r += 32) {
+        const int row = m0 + r;
+        if (row < p.P) p.zbuf[size_t(col) * p.ldz + row] = zt[r * ldt + c];
+      }
+    }
+    return;
+  }
+  for (int r = warp; r < BM; r += nwarps) {
+    const int row = m0 + r;
+    for (int ch = 0; ch < p.n_ch; ++ch) {
+      const int term = p.ch_term[ch];
+      const bool prod = term_is_product(term);
+      const T ident = prod ? T(1) : T(0);
+      T s = ident;
+      for (int c = lane; c < BN; c += 32) {
+        const int col = n0 + c;
+        const T v = col < p.D ? term_value<T>(term, zt[r * ldt + c], col, p.ell_w) : ident;
+        s = prod ? F::mul(s, v) : F::add(s, v);
+      }
+      for (int off = 16; off > 0; off >>= 1) {
+        const T o = __shfl_xor_sync(0xffffffffu, s, off);
+        s = prod ? F::mul(s, o) : F::add(s, o);
+      }
+      if (lane == 0 && row < p.P) p.partial[(size_t(ch) * p.n_ntiles + blockIdx.y) * p.P + row] = s;
+    }
+  }
+  __threadfence();
+  ptx::named_bar_sync(1, nthreads);
+  if (tid == 0) {
+    const unsigned ticket = atomicAdd(&p.counters[blockIdx.x], 1u);
+    *last_flag = (ticket == unsigned(p.n_ntiles - 1)) ? 1 : 0;
+  }
+  ptx::named_bar_sync(1, nthreads);
+  if (!*last_flag) return;
+  __threadfence();
+  for (int r = tid; r < BM; r += nthreads) {
+    const int row = m0 + r;
+    if (row >= p.P) continue;
+    T chv[kMaxCh];
+    for (int ch = 0; ch < p.n_ch; ++ch) {
+      const bool prod = term_is_product(p.ch_term[ch]);
+      const T* src = p.partial + size_t(ch) * p.n_ntiles * p.P + row;
+      T v = __ldcg(src);
+      for (int t = 1; t < p.n_ntiles; ++t) {
+        const T x = __ldcg(src + size_t(t) * p.P);
+        v = prod ? F::mul(v, x) : F::add(v, x);
+      }
+      chv[ch] = v;
+    }
+    for (int o = 0; o < p.n_out; ++o) {
+      const T s0 = chv[p.out_ch0[o]];
+      const T s1 = p.out_ch1[o] >= 0 ? chv[p.out_ch1[o]] : T(0);
+      p.out[o * p.ldo + row] = finalize<T>(p.out_kind[o], s0, s1, p.D, T(p.out_bias[o]));
+    }
+  }
+  if (tid == 0) p.counters[blockIdx.x] = 0u;  // re-arm for the next launch
+}
+
+// byte offset of element (r, kk) inside a SWIZZLE_128B tile whose rows are 128 bytes
+template <int ELEM>
+__device__ __forceinline__ uint32_t swz(int r, int kk) {
+  constexpr int per_chunk = 16 / ELEM;
+  return uint32_t(r * 128 + ((((kk / per_chunk) ^ (r & 7))) << 4) + (kk % per_chunk) * ELEM);
+}
+
+// ---------------------------------------------------------------------------------------
+// K1: FP64 DMMA kernel
+template <int BM, int BN, int WM, int WN, int STAGES>
+struct f64_cfg {
+  static constexpr int KB = 16;  // doubles per K-slice (one 128-byte swizzle row)
+  static constexpr int NCW = WM * WN;
+  static constexpr int THREADS = (NCW + 1) * 32;
+  static constexpr int WTM = BM / WM, WTN = BN / WN;
+  static constexpr int TM = WTM / 8, TN = WTN / 8;
+  static constexpr int A_BYTES = BM * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int O_BYTES = 128;
+  static constexpr int STAGE_BYTES = ((A_BYTES + B_BYTES + O_BYTES + 1023) / 1024) * 1024;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 2 * STAGES * 8 + 64;
+  static_assert(WTM % 8 == 0 && WTN % 8 == 0, "warp tile must be a multiple of 8");
+  static_assert(BM * (BN + 1) * 8 <= STAGES * STAGE_BYTES, "epilogue tile must fit the stage ring");
+};
+
+template <int BM, int BN, int WM, int WN, int STAGES>
+__global__ void __launch_bounds__(f64_cfg<BM, BN, WM, WN, STAGES>::THREADS, 1)
+    eval_f64_dmma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmM,
+                         const fused_params<double> p) {
+  using C = f64_cfg<BM, BN, WM, WN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  int* last_flag = reinterpret_cast<int*>(empty + STAGES);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int KT = (p.D + C::KB - 1) / C::KB;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], C::NCW);
+    }
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == C::NCW) {
+    // ---------------- producer ----------------
+    if (lane == 0) {
+      ptx::prefetch_tma(&tmX);
+      ptx::prefetch_tma(&tmM);
+      for (int kb = 0; kb < KT; ++kb) {
+        const int s = kb % STAGES;
+        if (kb >= STAGES) ptx::mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
+        uint8_t* st = smem + s * C::STAGE_BYTES;
+        ptx::mbar_arrive_expect_tx(&full[s], C::A_BYTES + C::B_BYTES + C::O_BYTES);
+        ptx::tma_load_2d(st, &tmX, &full[s], kb * C::KB, m0);
+        ptx::tma_load_2d(st + C::A_BYTES, &tmM, &full[s], kb * C::KB, n0);
+        ptx::bulk_load(st + C::A_BYTES + C::B_BYTES, p.shift + size_t(kb) * C::KB, C::O_BYTES, &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int wm = warp / WN, wn = warp % WN;
+  const int g = lane >> 2, t = lane & 3;
+  const int rA = wm * C::WTM, rB = wn * C::WTN;
+  double acc[C::TM][C::TN][2];
+#pragma unroll
+  for (int i = 0; i < C::TM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  for (int kb = 0; kb < KT; ++kb) {
+    const int s = kb % STAGES;
+    ptx::mbar_wait(&full[s], (kb / STAGES) & 1);
+    const uint8_t* st = smem + s * C::STAGE_BYTES;
+    const uint8_t* sA = st;
+    const uint8_t* sB = st + C::A_BYTES;
+    const double* sO = reinterpret_cast<const double*>(st + C::A_BYTES + C::B_BYTES);
+#pragma unroll
+    for (int ks = 0; ks < C::KB / 4; ++ks) {
+      const int kk = ks * 4 + t;
+      const double o = sO[kk];
+      double a[C::TM], b[C::TN];
+#pragma unroll
+      for (int i = 0; i < C::TM; ++i) {
+        const int r = rA + i * 8 + g;
+        a[i] = __dsub_rn(*reinterpret_cast<const double*>(sA + swz<8>(r, kk)), o);
+      }
+#pragma unroll
+      for (int j = 0; j < C::TN; ++j) {
+        const int r = rB + j * 8 + g;
+        b[j] = *reinterpret_cast<const double*>(sB + swz<8>(r, kk));
+      }
+#pragma unroll
+      for (int i = 0; i < C::TM; ++i)
+#pragma unroll
+        for (int j = 0; j < C::TN; ++j) ptx::dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&empty[s]);
+  }
+
+  // park the accumulator tile in the (drained) stage ring, then run the epilogue from smem
+  ptx::named_bar_sync(1, C::NCW * 32);
+  double* zt = reinterpret_cast<double*>(smem);
+  constexpr int LDT = BN + 1;
+#pragma unroll
+  for (int i = 0; i < C::TM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::TN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) zt[(rA + i * 8 + g) * LDT + rB + j * 8 + 2 * t + h] = acc[i][j][h];
+  ptx::named_bar_sync(1, C::NCW * 32);
+  tile_epilogue<double, BM, BN>(p, zt, LDT, m0, n0, threadIdx.x, C::NCW * 32, last_flag);
+}
+
+// ---------------------------------------------------------------------------------------
+// K2: FP32 FFMA kernel.  Each consumer thread owns an 8x8 register tile; rows and columns
+// are interleaved with stride 8 (rows ty + 8*i, cols tx + 8*j) so the float4 fragment loads
+// of a warp hit 8 distinct 16-byte swizzle chunks (conflict free).
+template <int BM, int BN, int STAGES>
+struct f32_cfg {
+  static constexpr int KB = 32;  // floats per K-slice (128-byte swizzle row)
+  static constexpr int TY = BM / 8, TX = BN / 8;
+  static constexpr int NCT = TY * TX;  // consumer threads
+  static constexpr int NCW = NCT / 32;
+  static constexpr int WN = 1;  // row sums reduced across all threads of a row via smem
+  static constexpr int THREADS = NCT + 32;
+  static constexpr int A_BYTES = BM * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int O_BYTES = 128;
+  static constexpr int STAGE_BYTES = ((A_BYTES + B_BYTES + O_BYTES + 1023) / 1024) * 1024;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 2 * STAGES * 8 + 64;
+  static_assert(NCT % 32 == 0, "consumer threads must be whole warps");
+  static_assert(BM * (BN + 1) * 4 <= STAGES * STAGE_BYTES, "epilogue tile must fit the stage ring");
+};
+
+template <int BM, int BN, int STAGES>
+__global__ void __launch_bounds__(f32_cfg<BM, BN, STAGES>::THREADS, 1)
+    eval_f32_ffma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmM,
+                         const fused_params<float> p) {
+  using C = f32_cfg<BM, BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  int* last_flag = reinterpret_cast<int*>(empty + STAGES);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int KT = (p.D + C::KB - 1) / C::KB;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], C::NCW);
+    }
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == C::NCW) {
+    if (lane == 0) {
+      ptx::prefetch_tma(&tmX);
+      ptx::prefetch_tma(&tmM);
+      for (int kb = 0; kb < KT; ++kb) {
+        const int s = kb % STAGES;
+        if (kb >= STAGES) ptx::mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
+        uint8_t* st = smem + s * C::STAGE_BYTES;
+        ptx::mbar_arrive_expect_tx(&full[s], C::A_BYTES + C::B_BYTES + C::O_BYTES);
+        ptx::tma_load_2d(st, &tmX, &full[s], kb * C::KB, m0);
+        ptx::tma_load_2d(st + C::A_BYTES, &tmM, &full[s], kb * C::KB, n0);
+        ptx::bulk_load(st + C::A_BYTES + C::B_BYTES, p.shift + size_t(kb) * C::KB, C::O_BYTES, &full[s]);
+      }
+    }
+    return;
+  }
+
+  const int tid = threadIdx.x;
+  const int ty = tid / C::TX, tx = tid % C::TX;  // rows ty + TY*i? no: rows ty*1 + TY*i
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+  for (int kb = 0; kb < KT; ++kb) {
+    const int s = kb % STAGES;
+    ptx::mbar_wait(&full[s], (kb / STAGES) & 1);
+    const uint8_t* st = smem + s * C::STAGE_BYTES;
+    const uint8_t* sA = st;
+    const uint8_t* sB = st + C::A_BYTES;
+    const float* sO = reinterpret_cast<const float*>(st + C::A_BYTES + C::B_BYTES);
+#pragma unroll 2
+    for (int kc = 0; kc < C::KB / 4; ++kc) {
+      const float4 o = *reinterpret_cast<const float4*>(sO + kc * 4);
+      float4 a[8], b[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int r = ty + C::TY * i;
+        float4 x = *reinterpret_cast<const float4*>(sA + swz<4>(r, kc * 4));
+        a[i] = make_float4(__fsub_rn(x.x, o.x), __fsub_rn(x.y, o.y), __fsub_rn(x.z, o.z), __fsub_rn(x.w, o.w));
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int r = tx + C::TX * j;
+        b[j] = *reinterpret_cast<const float4*>(sB + swz<4>(r, kc * 4));
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          acc[i][j] = fmaf(a[i].x, b[j].x, acc[i][j]);
+          acc[i][j] = fmaf(a[i].y, b[j].y, acc[i][j]);
+          acc[i][j] = fmaf(a[i].z, b[j].z, acc[i][j]);
+          acc[i][j] = fmaf(a[i].w, b[j].w, acc[i][j]);
+        }
+    }
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&empty[s]);
+  }
+
+  ptx::named_bar_sync(1, C::NCT);
+  float* zt = reinterpret_cast<float*>(smem);
+  constexpr int LDT = BN + 1;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) zt[(ty + C::TY * i) * LDT + tx + C::TX * j] = acc[i][j];
+  ptx::named_bar_sync(1, C::NCT);
+  tile_epilogue<float, BM, BN>(p, zt, LDT, m0, n0, tid, C::NCT, last_flag);
+}
+
+// ---------------------------------------------------------------------------------------
+// host side
+
+namespace {
+
+struct kind_channels {
+  int n;
+  int term[2];
+};
+kind_channels channels_for(int kind) {
+  switch (kind) {
+    case EVB_SPHERE: return {1, {TERM_SQ, -1}};
+    case EVB_ELLIPTIC: return {1, {TERM_WSQ, -1}};
+    case EVB_BENT_CIGAR:
+    case EVB_DISCUS: return {2, {TERM_TAIL, TERM_HEAD}};
+    case EVB_RASTRIGIN: return {1, {TERM_RAST, -1}};
+    case EVB_ACKLEY: return {2, {TERM_SQ, TERM_COS}};
+    case EVB_GRIEWANK: return {2, {TERM_SQ, TERM_GCOS}};
+  }
+  return {0, {-1, -1}};
+}
+
+template <typename T>
+bool build_plan(fused_params<T>& fp, int n_out, const int* kinds, const double* biases) {
+  fp.n_ch = 0;
+  fp.n_out = n_out;
+  for (int o = 0; o < n_out; ++o) {
+    const kind_channels kc = channels_for(kinds[o]);
+    if (kc.n == 0) return false;
+    int idx[2] = {-1, -1};
+    for (int c = 0; c < kc.n; ++c) {
+      int found = -1;
+      for (int q = 0; q < fp.n_ch; ++q)
+        if (fp.ch_term[q] == kc.term[c]) found = q;
+      if (found < 0) {
+        if (fp.n_ch == kMaxCh) return false;
+        found = fp.n_ch;
+        fp.ch_term[fp.n_ch++] = kc.term[c];
+      }
+      idx[c] = found;
+    }
+    fp.out_kind[o] = kinds[o];
+    fp.out_bias[o] = biases[o];
+    fp.out_ch0[o] = idx[0];
+    fp.out_ch1[o] = idx[1];
+  }
+  return true;
+}
+
+// Tile configurations, chosen per problem shape to minimise wave quantisation on the SMs.
+// fp64: (BM, BN, WM, WN); warp tile (BM/WM) x (BN/WN).
+constexpr int kStages64 = 6;
+constexpr int kStages32 = 4;
+
+template <int BM, int BN, int WM, int WN>
+void launch_f64(const CUtensorMap& tmX, const CUtensorMap& tmM, const fused_params<double>& fp, cudaStream_t st) {
+  using C = f64_cfg<BM, BN, WM, WN, kStages64>;
+  auto kern = eval_f64_dmma_kernel<BM, BN, WM, WN, kStages64>;
+  static bool attr = false;
+  if (!attr) {
+    EVB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  dim3 grid((fp.P + BM - 1) / BM, (fp.D + BN - 1) / BN);
+  kern<<<grid, C::THREADS, C::SMEM, st>>>(tmX, tmM, fp);
+  EVB_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+template <int BM, int BN>
+void launch_f32(const CUtensorMap& tmX, const CUtensorMap& tmM, const fused_params<float>& fp, cudaStream_t st) {
+  using C = f32_cfg<BM, BN, kStages32>;
+  auto kern = eval_f32_ffma_kernel<BM, BN, kStages32>;
+  static bool attr = false;
+  if (!attr) {
+    EVB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  dim3 grid((fp.P + BM - 1) / BM, (fp.D + BN - 1) / BN);
+  kern<<<grid, C::THREADS, C::SMEM, st>>>(tmX, tmM, fp);
+  EVB_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    EVB_CUDA(cudaGetDevice(&dev));
+    EVB_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
+// cost model: waves * tile area (one CTA per SM for every config)
+double tile_cost(int64_t P, int D, int BM, int BN) {
+  const int64_t ctas = ((P + BM - 1) / BM) * ((D + BN - 1) / BN);
+  const int64_t waves = (ctas + sm_count() - 1) / sm_count();
+  return double(waves) * BM * BN;
+}
+
+}  // namespace
+
+// Fused (or z-store) GEMM evaluation of a base problem on device-resident X.
+template <typename T>
+void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, T* zbuf, int64_t ldz,
+               const T* shift, const void* rotation, int ldm, int P, int D) {
+  fused_params<T> fp{};
+  fp.P = P;
+  fp.D = D;
+  fp.ell_w = static_cast<const T*>(rq.prob->ell_w);
+  fp.shift = shift;
+  fp.out = static_cast<T*>(rq.out);
+  fp.ldo = rq.ldo;
+  if (zstore) {
+    fp.zbuf = zbuf;
+    fp.ldz = ldz;
+  } else if (!build_plan<T>(fp, rq.n_out, rq.kinds, rq.biases)) {
+    throw logic_error("gemm_eval: kind set has no fused epilogue");
+  }
+  evb_scratch_s* sc = rq.scratch;
+  constexpr int dtype = std::is_same<T, double>::value ? EVB_F64 : EVB_F32;
+  constexpr int KB = std::is_same<T, double>::value ? 16 : 32;
+
+  int BM, BN;
+  if constexpr (std::is_same<T, double>::value) {
+    // pick the tile with the least wave-quantised cost
+    const int cands[3][2] = {{64, 112}, {64, 128}, {32, 128}};
+    int best = 0;
+    double bc = 1e300;
+    for (int c = 0; c < 3; ++c) {
+      const double v = tile_cost(P, D, cands[c][0], cands[c][1]) * (cands[c][0] == 32 ? 1.08 : 1.0);
+      if (v < bc) {
+        bc = v;
+        best = c;
+      }
+    }
+    BM = cands[best][0];
+    BN = cands[best][1];
+  } else {
+    BM = 64;
+    BN = 128;
+  }
+  CUtensorMap tmX, tmM;
+  if (!make_tma_2d(&tmX, X, dtype, uint64_t(D), uint64_t(P), uint64_t(ldx) * sizeof(T), KB, BM))
+    throw runtime_error("gemm_eval: cannot encode the TMA descriptor of X");
+  if (!make_tma_2d(&tmM, rotation, dtype, uint64_t(ldm), uint64_t(D), uint64_t(ldm) * sizeof(T), KB, BN))
+    throw runtime_error("gemm_eval: cannot encode the TMA descriptor of M");
+  fp.n_ntiles = (D + BN - 1) / BN;
+  const int n_mtiles = (P + BM - 1) / BM;
+  if (!zstore) {
+    ensure_buffer(&sc->partial, &sc->partial_bytes, size_t(fp.n_ch) * fp.n_ntiles * P * sizeof(T), rq.stream);
+    if (sc->counters_n < size_t(n_mtiles)) {
+      size_t cap = sc->counters_n * sizeof(unsigned);
+      void* ptr = sc->counters;
+      ensure_buffer(&ptr, &cap, size_t(n_mtiles) * sizeof(unsigned), rq.stream);
+      sc->counters = static_cast<unsigned*>(ptr);
+      sc->counters_n = cap / sizeof(unsigned);
+      EVB_CUDA(cudaMemsetAsync(sc->counters, 0, cap, rq.stream));
+    }
+    fp.partial = static_cast<T*>(sc->partial);
+    fp.counters = sc->counters;
+  }
+  if constexpr (std::is_same<T, double>::value) {
+    if (BM == 64 && BN == 112) launch_f64<64, 112, 2, 2>(tmX, tmM, fp, rq.stream);
+    else if (BM == 64 && BN == 128) launch_f64<64, 128, 2, 2>(tmX, tmM, fp, rq.stream);
+    else launch_f64<32, 128, 1, 4>(tmX, tmM, fp, rq.stream);
+  } else {
+    launch_f32<64, 128>(tmX, tmM, fp, rq.stream);
+  }
+}
+
+template void gemm_eval<double>(const eval_request&, const void*, int64_t, bool, double*, int64_t, const double*,
+                                const void*, int, int, int);
+template void gemm_eval<float>(const eval_request&, const void*, int64_t, bool, float*, int64_t, const float*,
+                               const void*, int, int, int);
+
+bool fused_kinds_ok(int n, const int* kinds) {
+  int terms[kMaxCh];
+  int nt = 0;
+  for (int o = 0; o < n; ++o) {
+    const kind_channels kc = channels_for(kinds[o]);
+    if (kc.n == 0) return false;
+    for (int c = 0; c < kc.n; ++c) {
+      bool f = false;
+      for (int q = 0; q < nt; ++q) f = f || terms[q] == kc.term[c];
+      if (!f) {
+        if (nt == kMaxCh) return false;
+        terms[nt++] = kc.term[c];
+      }
+    }
+  }
+  return n <= kMaxOut;
+}
+
+}  // namespace evb

@@ -1,0 +1,150 @@
+// evb_internal.cuh — shared host/device definitions of libevb (not part of the ABI).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "evb.h"
+
+namespace evb {
+
+// ---- error plumbing --------------------------------------------------------------------
+// Internal code throws these; the C ABI layer converts them to status codes.
+struct invalid_argument : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct config_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct logic_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct runtime_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define EVB_CUDA(x) ::evb::cuda_check((x), #x)
+
+inline void require(bool c, const std::string& msg) {
+  if (!c) throw config_error(msg);
+}
+
+inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+// ---- problem representation ------------------------------------------------------------
+enum spec_kind { SPEC_BASE = 0, SPEC_HYBRID = 1, SPEC_COMPOSITION = 2 };
+
+// Leading dimension of every device matrix/vector the problem owns: a multiple of 16
+// elements so TMA boxes of one 128-byte swizzle atom tile it, and the tail [dim, ld) is
+// zero so out-of-range K contributes exactly 0 to z.
+constexpr int kLdAlign = 16;
+
+struct device_problem {
+  int dtype = EVB_F64;
+  int dim = 0;
+  int ld = 0;  // padded leading dimension (elements)
+  int spec = SPEC_BASE;
+  int kind = EVB_SPHERE;
+  double bias = 0.0;
+  // base / hybrid
+  void* shift = nullptr;     // ld + 16 elements, zero padded
+  void* rotation = nullptr;  // dim rows x ld (row-major, zero padded columns)
+  void* ell_w = nullptr;     // elliptic weights pow(10, 6 i/(D-1)) in T, computed on the host
+  // hybrid (problems/instance.hpp:24-30, 97-112)
+  int n_chunks = 0;
+  int* perm = nullptr;
+  int* sub_kinds = nullptr;
+  int* chunk_sizes = nullptr;
+  // composition (problems/instance.hpp:33-41, 116-174)
+  int n_comp = 0;
+  int* comp_kinds = nullptr;
+  void* comp_shift = nullptr;  // n_comp x ld
+  void* comp_rot = nullptr;    // n_comp x dim x ld
+  double* comp_sigma = nullptr;
+  double* comp_lambda = nullptr;
+  double* comp_bias = nullptr;
+  void* hyb_w = nullptr;      // hybrid: per-chunk elliptic weights, chunk c at its offset
+};
+
+}  // namespace evb
+
+struct evb_problem_s {
+  evb::device_problem p;
+};
+
+struct evb_scratch_s {
+  cudaStream_t own_stream = nullptr;
+  // large-D fused path: per (channel, n-tile, point) partial sums + per m-block counters
+  void* partial = nullptr;
+  size_t partial_bytes = 0;
+  unsigned* counters = nullptr;
+  size_t counters_n = 0;
+  // materialised z (SoA: z[i * ldp + b], the reference's soa_z layout, problems/batch.hpp:44-45)
+  void* zbuf = nullptr;
+  size_t zbuf_bytes = 0;
+  // re-pitched copy of X when the caller's rows are not TMA-legal
+  void* xpad = nullptr;
+  size_t xpad_bytes = 0;
+  // host-buffer path
+  void* dx = nullptr;
+  size_t dx_bytes = 0;
+  void* dout = nullptr;
+  size_t dout_bytes = 0;
+  // composition: value accumulators (double) per point
+  double* acc = nullptr;
+  size_t acc_bytes = 0;
+};
+
+namespace evb {
+
+// Grow-only device buffer; synchronises `stream` before releasing an old allocation.
+inline void ensure_buffer(void** ptr, size_t* cap, size_t need, cudaStream_t stream) {
+  if (*cap >= need && *ptr) return;
+  if (*ptr) {
+    EVB_CUDA(cudaStreamSynchronize(stream));
+    EVB_CUDA(cudaFree(*ptr));
+    *ptr = nullptr;
+    *cap = 0;
+  }
+  size_t bytes = need < 256 ? 256 : need;
+  EVB_CUDA(cudaMalloc(ptr, bytes));
+  *cap = bytes;
+}
+
+// TMA descriptor helpers (driver entry point fetched through the runtime; no -lcuda).
+bool make_tma_2d(CUtensorMap* map, const void* base, int dtype, uint64_t inner_elems,
+                 uint64_t outer_rows, uint64_t row_stride_bytes, uint32_t box_inner,
+                 uint32_t box_outer);
+
+// ---- evaluation entry points (eval_*.cu) -------------------------------------------------
+struct eval_request {
+  const device_problem* prob;
+  evb_scratch_s* scratch;
+  const void* X;
+  int64_t n;
+  int64_t ldx;
+  void* out;
+  int64_t ldo;
+  int n_out;        // number of output kinds (multi); 1 for evaluate_batch
+  int kinds[4];     // base kinds per output
+  double biases[4]; // additive bias per output
+  cudaStream_t stream;
+};
+
+void eval_dispatch(const eval_request& rq);
+
+// Number of kernel launches issued by the last eval_dispatch on this thread (bench accounting).
+int last_launch_count();
+void count_launch(int n = 1);
+
+}  // namespace evb

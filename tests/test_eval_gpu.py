@@ -1,0 +1,217 @@
+"""GPU parity of batched evaluation (K1 fp64 / K2 fp32 / small-D / z-store / hybrid / composition)
+against the C oracle (itself pinned to the reference, tests/test_oracle.py).
+
+Tolerances (north_star): fitness within 1e-10 relative (fp64) and 1e-4 relative (fp32), with
+the reference's own convention |d| <= tol * max(1, |ref|) (tests/test_problems.cpp:310, 328-329).
+Small-D paths accumulate in the reference's exact order, so transcendental-free kinds are
+required to be bit-identical there.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+
+torch = pytest.importorskip("torch")
+import paper_2505_17430_b200 as evb  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+K = evb.BaseKind
+ALL_KINDS = list(K)
+NO_TRIG = [K.sphere, K.elliptic, K.bent_cigar, K.discus, K.rosenbrock, K.schwefel_12]
+
+
+def rel_err(got, ref):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    return float(np.max(np.abs(got - ref) / np.maximum(1.0, np.abs(ref)))) if ref.size else 0.0
+
+
+def gpu_eval(problem, X, dev):
+    sc = evb.EvalScratch()
+    Xd = torch.from_numpy(np.ascontiguousarray(X)).to(dev)
+    out = torch.empty(X.shape[0], dtype=Xd.dtype, device=dev)
+    evb.evaluate_batch(problem, Xd, sc, out)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+@pytest.fixture(scope="module")
+def config1():
+    # BASELINE config 1: D=1000, pop=1024, seed 7 (SURVEY §8(d) stream assignment)
+    o, m = O.shift_rotation(7, 1000)
+    X = O.population(7, 1024, 1000)
+    return o, m, X
+
+
+@pytest.mark.parametrize("kind", [K.elliptic, K.rastrigin, K.ackley])
+def test_config1_fp64(config1, dev, kind):
+    o, m, X = config1
+    p = evb.ProblemInstance.base(kind, o, m, 0.0)
+    got = gpu_eval(p, X, dev)
+    ref = O.eval_batch(int(kind), o, m, 0.0, X)
+    assert rel_err(got, ref) <= 1e-10
+
+
+@pytest.mark.parametrize("kind", [K.elliptic, K.rastrigin, K.ackley])
+def test_config1_fp32(config1, dev, kind):
+    o, m, X = config1
+    o32, m32, X32 = o.astype(np.float32), m.astype(np.float32), X.astype(np.float32)
+    p = evb.ProblemInstance.base(kind, o32, m32, 0.0, dtype=evb.EVB_F32)
+    got = gpu_eval(p, X32, dev)
+    ref = O.eval_batch(int(kind), o32, m32, 0.0, X32)
+    assert rel_err(got, ref) <= 1e-4
+
+
+def test_config1_three_on_one_z(config1, dev):
+    o, m, X = config1
+    kinds = [K.elliptic, K.rastrigin, K.ackley]
+    p = evb.ProblemInstance.base(K.elliptic, o, m, 0.0)
+    sc = evb.EvalScratch()
+    Xd = torch.from_numpy(X).to(dev)
+    out = torch.empty((3, X.shape[0]), dtype=torch.float64, device=dev)
+    evb.evaluate_batch_multi(p, kinds, [0.0, 100.0, 200.0], Xd, sc, out)
+    got = out.cpu().numpy()
+    for k, kind in enumerate(kinds):
+        ref = O.eval_batch(int(kind), o, m, 100.0 * k, X)
+        assert rel_err(got[k], ref) <= 1e-10, kind
+
+
+@pytest.mark.parametrize("dtype", [evb.EVB_F64, evb.EVB_F32])
+@pytest.mark.parametrize("kind", ALL_KINDS)
+def test_all_kinds_large_dim(dev, kind, dtype):
+    # D=1000 (1000-D parity of every base kind, tests/test_problems.cpp:370-401) with a ragged
+    # batch; rosenbrock / schwefel / schaffer take the z-store + row path
+    o, m = O.shift_rotation(64, 1000)
+    X = O.population(65, 37, 1000)
+    nd = np.float64 if dtype == evb.EVB_F64 else np.float32
+    o, m, X = o.astype(nd), m.astype(nd), X.astype(nd)
+    p = evb.ProblemInstance.base(kind, o, m, 100.0, dtype=dtype)
+    got = gpu_eval(p, X, dev)
+    ref = O.eval_batch(int(kind), o, m, 100.0, X)
+    assert rel_err(got, ref) <= (1e-10 if dtype == evb.EVB_F64 else 1e-4)
+
+
+@pytest.mark.parametrize("dim", [1, 2, 10, 30, 50, 100])
+@pytest.mark.parametrize("dtype", [evb.EVB_F64, evb.EVB_F32])
+def test_small_dim_exact_order(dev, dim, dtype):
+    o, m = O.shift_rotation(3 + dim, dim)
+    X = O.population(4 + dim, 13, dim)
+    nd = np.float64 if dtype == evb.EVB_F64 else np.float32
+    o, m, X = o.astype(nd), m.astype(nd), X.astype(nd)
+    for kind in ALL_KINDS:
+        p = evb.ProblemInstance.base(kind, o, m, 100.0 * (int(kind) + 1), dtype=dtype)
+        got = gpu_eval(p, X, dev)
+        ref = O.eval_batch(int(kind), o, m, 100.0 * (int(kind) + 1), X)
+        if kind in NO_TRIG:
+            assert np.array_equal(got, ref), (kind, dim)
+        else:
+            assert rel_err(got, ref) <= (1e-12 if dtype == evb.EVB_F64 else 1e-6), (kind, dim)
+
+
+def test_evaluate_at_shift_is_bias(dev):
+    # tests/test_problems.cpp:124-130
+    for dim in (10, 1000):
+        o, m = O.shift_rotation(99, dim)
+        for kind in ALL_KINDS:
+            p = evb.ProblemInstance.base(kind, o, m, 100.0 * (int(kind) + 1))
+            got = gpu_eval(p, o.reshape(1, -1), dev)
+            assert abs(got[0] - 100.0 * (int(kind) + 1)) <= 1e-10 * 100.0 * (int(kind) + 1), (kind, dim)
+
+
+def test_identity_sphere_114(dev):
+    # tests/test_problems.cpp:132-139: identity sphere at (1,2,3) with bias 100 is exactly 114
+    p = evb.ProblemInstance.base(K.sphere, np.zeros(3), np.eye(3), 100.0)
+    got = gpu_eval(p, np.array([[1.0, 2.0, 3.0]]), dev)
+    assert got[0] == 114.0
+
+
+@pytest.mark.parametrize("dim", [10, 100, 1000])
+def test_hybrid(dev, dim):
+    o, m = O.shift_rotation(11, dim)
+    X = O.population(12, 21, dim)
+    rng = np.random.default_rng(dim)
+    perm = rng.permutation(dim).astype(np.int32)
+    for kinds, props in (([K.schwefel_12, K.rastrigin, K.elliptic], [0.3, 0.3, 0.4]),
+                         ([K.discus, K.griewank, K.rosenbrock, K.sphere], [0.2, 0.2, 0.3, 0.3])):
+        sizes = []
+        used = 0
+        for c, pr in enumerate(props[:-1]):  # problems/instance.hpp:300-313
+            s = int(np.ceil(pr * dim))
+            s = max(1, min(s, dim - used - (len(props) - 1 - c)))
+            sizes.append(s)
+            used += s
+        sizes.append(dim - used)
+        p = evb.ProblemInstance.hybrid(o, m, [int(k) for k in kinds], sizes, perm, 900.0)
+        got = gpu_eval(p, X, dev)
+        ref = O.eval_hybrid(o, m, 900.0, [int(k) for k in kinds], sizes, perm, X)
+        assert rel_err(got, ref) <= 1e-10
+
+
+@pytest.mark.parametrize("dim", [10, 50, 200])
+@pytest.mark.parametrize("dtype", [evb.EVB_F64, evb.EVB_F32])
+def test_composition(dev, dim, dtype):
+    # BASELINE config 4 composition: rastrigin / elliptic / ackley, sigma (10,20,30),
+    # lambda (1, 1e-6, 1), bias (0, 100, 200)
+    nd = np.float64 if dtype == evb.EVB_F64 else np.float32
+    shifts, rots = [], []
+    for c in range(3):
+        o, m = O.shift_rotation(1000 + c, dim)
+        shifts.append(o)
+        rots.append(m)
+    shifts = np.stack(shifts).astype(nd)
+    rots = np.stack(rots).astype(nd)
+    kinds = [int(K.rastrigin), int(K.elliptic), int(K.ackley)]
+    sigma, lam, cb = [10.0, 20.0, 30.0], [1.0, 1e-6, 1.0], [0.0, 100.0, 200.0]
+    X = O.population(5, 33, dim).astype(nd)
+    X[0] = shifts[1]  # zero-distance collapse onto component 1 (problems/instance.hpp:135-149)
+    p = evb.ProblemInstance.composition(kinds, shifts, rots, sigma, lam, cb, 0.0, dtype=dtype)
+    got = gpu_eval(p, X, dev)
+    ref = O.eval_composition(kinds, shifts, rots, sigma, lam, cb, 0.0, X)
+    assert rel_err(got, ref) <= (1e-10 if dtype == evb.EVB_F64 else 1e-4)
+    assert abs(float(got[0]) - 100.0) <= 1e-6  # lambda_1 * f(0) + bias_1
+
+
+def test_edge_cases(dev):
+    o, m = O.shift_rotation(21, 1000)
+    p = evb.ProblemInstance.base(K.rastrigin, o, m, 0.0)
+    sc = evb.EvalScratch()
+    # empty batch gives empty output (tests/test_problems.cpp:289-292)
+    X0 = torch.empty((0, 1000), dtype=torch.float64, device=dev)
+    out0 = torch.empty(0, dtype=torch.float64, device=dev)
+    evb.evaluate_batch(p, X0, sc, out0)
+    # single point, odd row pitch (not TMA-legal -> re-pitched), padded rows
+    X = O.population(22, 5, 1000)
+    ref = O.eval_batch(int(K.rastrigin), o, m, 0.0, X)
+    for pad in (0, 1, 3, 24):
+        Xp = np.zeros((5, 1000 + pad))
+        Xp[:, :1000] = X
+        Xd = torch.from_numpy(Xp).to(dev)[:, :1000]
+        out = torch.empty(5, dtype=torch.float64, device=dev)
+        evb.evaluate_batch(p, Xd, sc, out)
+        assert rel_err(out.cpu().numpy(), ref) <= 1e-10, pad
+    got1 = gpu_eval(p, X[:1], dev)
+    assert rel_err(got1, ref[:1]) <= 1e-10
+    # dimension mismatch -> std::invalid_argument analogue
+    with pytest.raises(evb.InvalidArgument):
+        evb.evaluate_batch(p, torch.zeros((3, 999), dtype=torch.float64, device=dev), sc,
+                           torch.empty(3, dtype=torch.float64, device=dev))
+
+
+def test_deterministic(config1, dev):
+    o, m, X = config1
+    p = evb.ProblemInstance.base(K.ackley, o, m, 0.0)
+    a = gpu_eval(p, X, dev)
+    b = gpu_eval(p, X, dev)
+    assert np.array_equal(a, b)
+
+
+def test_host_path(config1):
+    o, m, X = config1
+    p = evb.ProblemInstance.base(K.elliptic, o, m, 200.0)
+    got = evb.batched_evaluate(p, X[:100])
+    ref = O.eval_batch(int(K.elliptic), o, m, 200.0, X[:100])
+    assert rel_err(got, ref) <= 1e-10
+    assert evb.batched_evaluate(p, np.zeros((0, 1000))).size == 0
+    with pytest.raises(evb.InvalidArgument):
+        evb.batched_evaluate(p, np.zeros((2, 7)))
