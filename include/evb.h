@@ -124,6 +124,81 @@ EVB_API int evb_evaluate_batch_multi(evb_problem p, evb_scratch s, int n_kinds, 
 EVB_API int evb_evaluate_batch_host(evb_problem p, evb_scratch s, const void* X_host, int64_t n_points,
                             int64_t ldx, void* out_host);
 
+/* ---- random words (core/rng.hpp:37-121) --------------------------------------------- */
+
+/* PHILOX: counter-based Philox4x32-10 words.  word(key, ctr_hi, n) = lanes (2(n&1), 2(n&1)+1)
+ * of block n>>1 under counter (lo(n>>1), hi(n>>1), lo(ctr_hi), hi(ctr_hi)).  Engines give each
+ * (generation g, individual i) its own sub-stream ctr_hi = (g << 32) | i (archive victims:
+ * sub 0xFFFFFFFF, init_population: 0xFFFFFFF0), so every individual draws in parallel; the words
+ * each individual consumed are exported (evb_de_last_draws) so the reference engine can replay
+ * them in its own sequential order through rng_stream::scripted (core/rng.hpp:54-58).
+ * WORDS: oracle mode — a caller-supplied word list consumed strictly in the reference's order
+ * (e.g. the raw words of rng_stream(42, 0)), reproducing the reference run exactly. */
+enum evb_rng_mode { EVB_RNG_PHILOX = 0, EVB_RNG_WORDS = 1 };
+typedef struct evb_rng_s* evb_rng;
+
+EVB_API int evb_rng_create_philox(uint64_t key, evb_rng* out);
+EVB_API int evb_rng_create_words(const uint64_t* words_host, int64_t n_words, evb_rng* out);
+EVB_API int evb_rng_destroy(evb_rng r);
+/* Synchronous: WORDS cursor (next unread word), PHILOX generation counter, overflow flag. */
+EVB_API int evb_rng_state(evb_rng r, int64_t* cursor, uint32_t* generation, int* overflow);
+EVB_API int evb_rng_set_generation(evb_rng r, uint32_t generation);
+/* n device-generated Philox words (key, ctr_hi, start..start+n) into host memory. */
+EVB_API int evb_philox_words(uint64_t key, uint64_t ctr_hi, uint64_t start, int64_t n, uint64_t* out_host);
+
+/* ---- DE engine (de/engine.hpp:51-173, de/builder.hpp:16-78) --------------------------- */
+
+/* strategy slots, by the reference's names (de/strategy.hpp, de/parameter.hpp) */
+enum evb_de_mutation { EVB_MUT_RAND1 = 0 /* "rand_1" */, EVB_MUT_BEST1 = 1 /* "best_1" */,
+                       EVB_MUT_TTPB1 = 2 /* "ttpb_1" */ };
+enum evb_de_crossover { EVB_CX_BINOMIAL = 0 /* "binomial" */ };
+enum evb_de_repair { EVB_REP_CLIP = 0 /* "clip" */, EVB_REP_REFLECT = 1 /* "reflect" */,
+                     EVB_REP_MIDPOINT_TARGET = 2 /* "midpoint_target" */ };
+enum evb_de_parameter { EVB_PAR_FIXED = 0 /* "fixed" */, EVB_PAR_JADE = 1 /* "jade" */,
+                        EVB_PAR_SHADE = 2 /* "shade" */ };
+
+typedef struct {
+  int mutation, crossover, repair, parameter;
+  double f, cr;        /* fixed_parameter(F, CR)                 de/parameter.hpp:79-97   */
+  double p_best;       /* ttpb1_mutation(p, use_archive)         de/strategy.hpp:124-165  */
+  int use_archive;
+  int memory_size;     /* shade_parameter(H)                     de/parameter.hpp:149-213 */
+  double jade_c;       /* jade_parameter(c)                      de/parameter.hpp:99-147  */
+  double archive_rate; /* de_builder::archive_rate               de/builder.hpp:44-48     */
+} evb_de_config;
+
+typedef struct evb_de_s* evb_de;
+
+/* Validates like de_builder::build + de_engine::validate_run; unknown slots -> EVB_ERR_CONFIG
+ * (there is no CPU fallback for a strategy without a GPU kernel). */
+EVB_API int evb_de_create(int dtype, const evb_de_config* cfg, int pop_size, int dim, evb_de* out);
+EVB_API int evb_de_destroy(evb_de e);
+/* de_engine::reset (de/engine.hpp:142-145): adapter to its initial state, archive emptied. */
+EVB_API int evb_de_reset(evb_de e);
+EVB_API int evb_de_archive_capacity(evb_de e);
+EVB_API int evb_de_p_count(evb_de e);
+/* de_engine::generation(pop, st, objective, lb, ub, rng) (de/engine.hpp:71-102) on a device
+ * population (pop_size x ldp, row-major) and fitness vector; `objective` is evaluated with
+ * problem_instance::evaluate semantics.  s may be NULL (engine-owned scratch). */
+EVB_API int evb_de_generation(evb_de e, evb_problem objective, evb_scratch s, void* pop, int64_t ldp,
+                              void* fitness, double lb, double ub, evb_rng rng, void* stream);
+/* init_population (core/population.hpp:88-98) from the rng. */
+EVB_API int evb_de_init_population(evb_de e, void* pop, int64_t ldp, double lb, double ub, evb_rng rng,
+                                   void* stream);
+/* de_engine::optimize (de/engine.hpp:107-133): init, evaluate, generations until max_fes. */
+EVB_API int evb_de_optimize(evb_de e, evb_problem objective, evb_scratch s, void* pop, int64_t ldp,
+                            void* fitness, double lb, double ub, int64_t max_fes, evb_rng rng,
+                            int* best_index, double* best_fitness, int* generations, void* stream);
+/* Engine state (archive members row-major cap x dim, size; SHADE/JADE memories; write index). */
+EVB_API int evb_de_get_state(evb_de e, void* archive_host, int* archive_size, void* mem_f_host,
+                             void* mem_cr_host, int* write_index);
+EVB_API int evb_de_set_state(evb_de e, const void* archive_host, int archive_size,
+                             const void* mem_f_host, const void* mem_cr_host, int write_index);
+/* Draws of the last generation: words consumed per individual, archive-victim words, the
+ * Philox generation id, per-individual F, CR, donor indices (4 per individual) and jrand. */
+EVB_API int evb_de_last_draws(evb_de e, int64_t* word_counts, int64_t* archive_words, uint32_t* generation,
+                              void* F_host, void* CR_host, int* idx_host, int* jrand_host);
+
 /* Kernel launches this library has issued on the calling thread (monotonic counter; used by
  * bench.py to report gpu_launches inside its timed region). */
 EVB_API int evb_launch_count(void);

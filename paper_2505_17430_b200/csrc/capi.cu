@@ -20,30 +20,6 @@ namespace evb {
 namespace {
 thread_local std::string g_last_error;
 
-template <typename Fn>
-int guarded(Fn&& fn) {
-  try {
-    fn();
-    g_last_error.clear();
-    return EVB_OK;
-  } catch (const invalid_argument& e) {
-    g_last_error = e.what();
-    return EVB_ERR_INVALID_ARGUMENT;
-  } catch (const config_error& e) {
-    g_last_error = e.what();
-    return EVB_ERR_CONFIG;
-  } catch (const logic_error& e) {
-    g_last_error = e.what();
-    return EVB_ERR_LOGIC;
-  } catch (const std::exception& e) {
-    g_last_error = e.what();
-    return EVB_ERR_RUNTIME;
-  } catch (...) {
-    g_last_error = "unknown error";
-    return EVB_ERR_RUNTIME;
-  }
-}
-
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -110,6 +86,8 @@ void free_problem(device_problem& p) {
 }
 
 }  // namespace
+
+void set_last_error(const char* msg) { g_last_error = msg; }
 
 bool make_tma_2d(CUtensorMap* map, const void* base, int dtype, uint64_t inner_elems, uint64_t outer_rows,
                  uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer) {

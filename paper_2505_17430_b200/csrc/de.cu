@@ -1,0 +1,903 @@
+// de.cu — DE per-generation update on the device (K4 mutation+crossover+repair, K5 selection +
+// archive + SHADE update, K6 top-p order) behind the reference's engine semantics.
+//
+// Reference: de/engine.hpp:71-102 (generation), de/strategy.hpp (rand/1 :80-94, best/1 :104-118,
+// current-to-pbest/1 :138-160, binomial :184-194, clip :234-240, midpoint-target :268-276,
+// archive :18-54), de/parameter.hpp (fixed :79-97, SHADE :149-213, sampling :28-43),
+// core/population.hpp:70-77 (stable fitness order).
+//
+// Per generation (one stream, no host sync):
+//   1. order     stable (fitness, index) ranks -> the first p_count entries      (ttpb/1, best/1)
+//   2. draws     per-individual scalar draws: adapter (slot, F, CR), donor indices, jrand.
+//                PHILOX: thread per individual, each on its own sub-stream (gen<<32 | i).
+//                WORDS : one thread walks the caller's word list in the reference's exact order
+//                        (rejection loops, Cauchy resampling) and records every offset.
+//   3. trial     block per individual, threads over genes: donor, binomial mask, repair.
+//   4. evaluate  the trial matrix through eval_dispatch (scalar-path trig, problem.evaluate).
+//   5. select    one CTA: greedy <= replacement in i order, success lists, archive slot
+//                assignment with last-writer-wins victims, SHADE memory update (double sums in
+//                the reference's sequential order).
+//   6. apply     block per replaced individual: parent -> archive slot, trial -> population.
+// Arithmetic uses explicitly rounded intrinsics (no FMA contraction), so with the same draws the
+// trial vectors are bit-identical to the reference's.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "evb_internal.cuh"
+#include "evb_math.cuh"
+#include "rng.cuh"
+
+namespace evb {
+
+struct de_conf {
+  int mutation;   // EVB_MUT_*
+  int crossover;  // EVB_CX_*
+  int repair;     // EVB_REP_*
+  int parameter;  // EVB_PAR_*
+  double f, cr;   // fixed adapter (stored in T, de/parameter.hpp:81-82)
+  double p_best;  // ttpb/1 p (stored in T, de/strategy.hpp:127-131)
+  int use_archive;
+  int memory_size;
+  double jade_c;  // JADE learning rate c (de/parameter.hpp:94-97)
+  double archive_rate;
+};
+
+}  // namespace evb
+
+struct evb_rng_s {
+  int mode = evb::RNG_PHILOX;
+  uint64_t key = 0;
+  uint64_t* d_words = nullptr;
+  int64_t n_words = 0;
+  int64_t* d_cursor = nullptr;  // WORDS: next unread word (device-resident)
+  uint32_t gen = 0;             // PHILOX: generation counter (host)
+  int* d_overflow = nullptr;
+};
+
+struct evb_de_s {
+  int dtype = EVB_F64;
+  int P = 0, D = 0;
+  evb::de_conf cfg{};
+  int p_count = 0;
+  int archive_cap = 0;
+  int64_t ldt = 0;
+  void* trial = nullptr;      // P x ldt
+  void* trial_fit = nullptr;  // P
+  void* F = nullptr;          // P (T)
+  void* CR = nullptr;         // P (T)
+  int* slot = nullptr;        // P
+  int* idx = nullptr;         // P x 4 (r1, r2, r3 | pbest, r1, r2)
+  int* jrand = nullptr;       // P
+  int64_t* woff = nullptr;    // P: first gene-uniform word (WORDS) / scalar word count (PHILOX)
+  int64_t* wcount = nullptr;  // P: words consumed by individual i
+  int* order = nullptr;       // p_count
+  int* win = nullptr;         // P
+  int* arch_slot = nullptr;   // P: archive slot written by i's push (-1: none / overwritten)
+  int* owner = nullptr;       // archive_cap
+  int* succ = nullptr;        // P success list (indices)
+  void* archive = nullptr;    // archive_cap x ldt
+  int* d_arch_size = nullptr;
+  int* d_write_index = nullptr;
+  int64_t* d_arch_words = nullptr;  // archive-victim words consumed by the last generation
+  void* mem_f = nullptr;            // H
+  void* mem_cr = nullptr;           // H
+  evb_scratch_s* eval_scratch = nullptr;
+  uint32_t last_gen = 0;
+};
+
+namespace evb {
+
+namespace {
+
+template <typename T>
+struct de_dev {
+  int P, D;
+  de_conf cfg;
+  int p_count;
+  int archive_cap;
+  T* pop;
+  int64_t ldp;
+  T* fit;
+  T* trial;
+  int64_t ldt;
+  T* trial_fit;
+  T* F;
+  T* CR;
+  int* slot;
+  int* idx;
+  int* jrand;
+  int64_t* woff;
+  int64_t* wcount;
+  int* order;
+  int* win;
+  int* arch_slot;
+  int* owner;
+  int* succ;
+  T* archive;
+  int* arch_size;
+  int* write_index;
+  int64_t* arch_words;
+  T* mem_f;
+  T* mem_cr;
+  T lb, ub;
+  word_source src;
+  uint32_t gen;
+  int64_t* cursor;
+  int* overflow;
+};
+
+// fitness order (core/population.hpp:70-77): rank = #{j : f_j < f_i or (f_j == f_i and j < i)}
+template <typename T>
+__global__ void de_order_kernel(const de_dev<T> d) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  T* sf = reinterpret_cast<T*>(smem_raw);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const T fi = i < d.P ? d.fit[i] : T(0);
+  int rank = 0;
+  for (int base = 0; base < d.P; base += blockDim.x) {
+    const int j = base + threadIdx.x;
+    sf[threadIdx.x] = j < d.P ? d.fit[j] : T(0);
+    __syncthreads();
+    const int n = min(int(blockDim.x), d.P - base);
+    if (i < d.P)
+      for (int q = 0; q < n; ++q) {
+        const T fj = sf[q];
+        const int jj = base + q;
+        rank += (fj < fi || (!(fi < fj) && !(fj < fi) && jj < i)) ? 1 : 0;
+      }
+    __syncthreads();
+  }
+  if (i < d.P && rank < d.p_count) d.order[rank] = i;
+}
+
+// de/parameter.hpp:28-38
+template <typename R>
+__device__ double sample_scale_factor(R& r, double mu) {
+  double f = 0.0;
+  for (int attempt = 0; attempt < 100; ++attempt) {
+    f = draw_cauchy(r, mu, 0.1);
+    if (f > 0.0) break;
+  }
+  if (f <= 0.0) f = 0.1;
+  return fmin(f, 1.0);
+}
+// de/parameter.hpp:41-43
+template <typename R>
+__device__ double sample_crossover_rate(R& r, double mu) {
+  const double v = draw_normal(r, mu, 0.1);
+  return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+}
+
+// Scalar draws of individual i in the reference's order (de/engine.hpp:88-92):
+// adapter sample, mutation indices, crossover jrand.  Returns via the de_dev arrays.
+template <typename T, typename R>
+__device__ void draw_scalars(const de_dev<T>& d, int i, int arch_size, R& r) {
+  // adapter
+  T F, CR;
+  int slot = -1;
+  if (d.cfg.parameter == EVB_PAR_SHADE) {
+    slot = draw_int(r, d.cfg.memory_size);
+    F = T(sample_scale_factor(r, double(d.mem_f[slot])));
+    CR = T(sample_crossover_rate(r, double(d.mem_cr[slot])));
+  } else if (d.cfg.parameter == EVB_PAR_JADE) {
+    F = T(sample_scale_factor(r, double(d.mem_f[0])));
+    CR = T(sample_crossover_rate(r, double(d.mem_cr[0])));
+  } else {
+    F = T(d.cfg.f);
+    CR = T(d.cfg.cr);
+  }
+  // mutation
+  const int ps = d.P;
+  int a = 0, b = 0, c = 0;
+  if (d.cfg.mutation == EVB_MUT_RAND1) {  // de/strategy.hpp:84-86
+    do { a = draw_int(r, ps); } while (a == i);
+    do { b = draw_int(r, ps); } while (b == i || b == a);
+    do { c = draw_int(r, ps); } while (c == i || c == a || c == b);
+  } else if (d.cfg.mutation == EVB_MUT_BEST1) {  // de/strategy.hpp:107-110
+    a = d.order[0];
+    do { b = draw_int(r, ps); } while (b == i);
+    do { c = draw_int(r, ps); } while (c == i || c == b);
+  } else {  // ttpb/1, de/strategy.hpp:143-152
+    a = d.order[draw_int(r, d.p_count)];
+    do { b = draw_int(r, ps); } while (b == i);
+    const int pool = ps + (d.cfg.use_archive ? arch_size : 0);
+    do { c = draw_int(r, pool); } while (c == i || c == b);
+  }
+  const int jr = draw_int(r, d.D);  // de/strategy.hpp:187
+  d.F[i] = F;
+  d.CR[i] = CR;
+  d.slot[i] = slot;
+  d.idx[4 * i + 0] = a;
+  d.idx[4 * i + 1] = b;
+  d.idx[4 * i + 2] = c;
+  d.jrand[i] = jr;
+}
+
+template <typename T>
+__global__ void de_draw_philox_kernel(const de_dev<T> d) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= d.P) return;
+  const int arch_size = *d.arch_size;
+  word_reader r{&d.src, (uint64_t(d.gen) << 32) | uint32_t(i), 0, 0, d.overflow};
+  draw_scalars<T>(d, i, arch_size, r);
+  d.woff[i] = r.count;  // gene uniforms start after the scalar words
+  d.wcount[i] = r.count + d.D;
+}
+
+template <typename T>
+__global__ void de_draw_words_kernel(const de_dev<T> d) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int arch_size = *d.arch_size;
+  int64_t pos = *d.cursor;
+  for (int i = 0; i < d.P; ++i) {
+    word_reader r{&d.src, 0, pos, 0, d.overflow};
+    draw_scalars<T>(d, i, arch_size, r);
+    d.woff[i] = r.pos;
+    d.wcount[i] = r.count + d.D;
+    pos = r.pos + d.D;
+  }
+  *d.cursor = pos;
+  if (pos > d.src.n_words) *d.overflow = 1;
+}
+
+// K4: donor + binomial crossover + repair.  Block per individual; each thread owns one Philox
+// block (two consecutive stream words) and so up to two genes.
+template <typename T>
+__global__ void de_trial_kernel(const de_dev<T> d) {
+  using F_ = fop<T>;
+  const int i = blockIdx.x;
+  const int D = d.D;
+  const T Fi = d.F[i];
+  const double cr = double(d.CR[i]);
+  const int jr = d.jrand[i];
+  const int a = d.idx[4 * i + 0], b = d.idx[4 * i + 1], c = d.idx[4 * i + 2];
+  const T* xi = d.pop + size_t(i) * d.ldp;
+  const T* xa = d.pop + size_t(a) * d.ldp;
+  const T* xb = d.pop + size_t(b) * d.ldp;
+  const T* xc = (d.cfg.mutation == EVB_MUT_TTPB1 && c >= d.P) ? d.archive + size_t(c - d.P) * d.ldt
+                                                                : d.pop + size_t(c) * d.ldp;
+  T* out = d.trial + size_t(i) * d.ldt;
+  const int64_t s0 = d.woff[i];  // stream index of gene 0's uniform
+  const uint64_t ctr_hi = (uint64_t(d.gen) << 32) | uint32_t(i);
+  const T lb = d.lb, ub = d.ub;
+  // Philox blocks covering stream words [s0, s0 + D)
+  const int64_t blk0 = s0 >> 1;
+  const int64_t nblk = ((s0 + D + 1) >> 1) - blk0;
+  for (int64_t q = threadIdx.x; q < nblk; q += blockDim.x) {
+    uint64_t w[2];
+    const int64_t n0 = (blk0 + q) * 2;
+    if (d.src.mode == RNG_PHILOX) {
+      philox_pair(d.src.key, ctr_hi, uint64_t(blk0 + q), w[0], w[1]);
+    } else {
+      // WORDS: s0 is the absolute list position of gene 0
+      w[0] = (n0 >= s0 && n0 < s0 + D && n0 < d.src.n_words) ? d.src.words[n0] : 0;
+      w[1] = (n0 + 1 >= s0 && n0 + 1 < s0 + D && n0 + 1 < d.src.n_words) ? d.src.words[n0 + 1] : 0;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t j64 = n0 + h - s0;
+      if (j64 < 0 || j64 >= D) continue;
+      const int j = int(j64);
+      const double u = u01_of(w[h]);
+      T v;
+      if (u < cr || j == jr) {
+        if (d.cfg.mutation == EVB_MUT_TTPB1)  // x_i + F(x_pb - x_i) + F(x_r1 - x~_r2), de/strategy.hpp:159
+          v = F_::add(F_::add(xi[j], F_::mul(Fi, F_::sub(xa[j], xi[j]))), F_::mul(Fi, F_::sub(xb[j], xc[j])));
+        else  // x_a + F(x_b - x_c), de/strategy.hpp:93 / :117
+          v = F_::add(xa[j], F_::mul(Fi, F_::sub(xb[j], xc[j])));
+      } else {
+        v = xi[j];
+      }
+      if (d.cfg.repair == EVB_REP_CLIP) {  // de/strategy.hpp:236-239
+        if (v < lb) v = lb;
+        if (v > ub) v = ub;
+      } else if (d.cfg.repair == EVB_REP_MIDPOINT_TARGET) {  // de/strategy.hpp:270-275
+        if (v < lb) v = F_::div(F_::add(lb, xi[j]), T(2));
+        else if (v > ub) v = F_::div(F_::add(ub, xi[j]), T(2));
+      } else if (d.cfg.repair == EVB_REP_REFLECT) {  // de/strategy.hpp:250-257
+        for (int fold = 0; (v < lb || v > ub) && fold < 100; ++fold) {
+          if (v < lb) v = F_::add(lb, F_::sub(lb, v));
+          if (v > ub) v = F_::sub(ub, F_::sub(v, ub));
+        }
+        if (v < lb) v = lb;
+        if (v > ub) v = ub;
+      }
+      out[j] = v;
+    }
+  }
+}
+
+// K5a: sequential selection bookkeeping (de/engine.hpp:27-47, de/strategy.hpp:29-37,
+// de/parameter.hpp:166-184).  One CTA; the O(P) sequential part runs in thread 0 because the
+// reference's archive victims and SHADE sums are order-dependent.
+template <typename T>
+__global__ void de_select_scan_kernel(const de_dev<T> d) {
+  for (int s = threadIdx.x; s < d.archive_cap; s += blockDim.x) d.owner[s] = -1;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  int size = *d.arch_size;
+  int n_succ = 0;
+  int64_t q = 0;  // archive-victim words consumed
+  int64_t wpos = d.src.mode == RNG_WORDS ? *d.cursor : 0;
+  const uint64_t ctr_hi = (uint64_t(d.gen) << 32) | kSubArchive;
+  for (int i = 0; i < d.P; ++i) {
+    const T ft = d.trial_fit[i], fp = d.fit[i];
+    const int w = (ft <= fp) ? 1 : 0;
+    d.win[i] = w;
+    d.arch_slot[i] = -1;
+    if (!w) continue;
+    const T gain = fop<T>::sub(fp, ft);
+    if (gain > T(0)) d.succ[n_succ++] = i;
+    if (d.archive_cap > 0) {
+      int sl;
+      if (size < d.archive_cap) {
+        sl = size++;
+      } else {
+        const uint64_t word = word_at(d.src, ctr_hi, d.src.mode == RNG_WORDS ? wpos + q : q, d.overflow);
+        ++q;
+        sl = uint_of(word, size);
+      }
+      const int prev = d.owner[sl];
+      if (prev >= 0) d.arch_slot[prev] = -1;  // last writer wins (members_[v] = genome)
+      d.owner[sl] = i;
+      d.arch_slot[i] = sl;
+    }
+  }
+  *d.arch_size = size;
+  *d.arch_words = q;
+  if (d.src.mode == RNG_WORDS) *d.cursor = wpos + q;
+  // adapter update
+  if (n_succ == 0) return;
+  if (d.cfg.parameter == EVB_PAR_SHADE) {
+    double gain_sum = 0.0;
+    for (int s = 0; s < n_succ; ++s) {
+      const int i = d.succ[s];
+      gain_sum = __dadd_rn(gain_sum, double(fop<T>::sub(d.fit[i], d.trial_fit[i])));
+    }
+    double f_num = 0.0, f_den = 0.0, cr_acc = 0.0;
+    for (int s = 0; s < n_succ; ++s) {
+      const int i = d.succ[s];
+      const double w = __ddiv_rn(double(fop<T>::sub(d.fit[i], d.trial_fit[i])), gain_sum);
+      const double f = double(d.F[i]);
+      f_num = __dadd_rn(f_num, __dmul_rn(__dmul_rn(w, f), f));
+      f_den = __dadd_rn(f_den, __dmul_rn(w, f));
+      cr_acc = __dadd_rn(cr_acc, __dmul_rn(w, double(d.CR[i])));
+    }
+    const int k = *d.write_index;
+    d.mem_f[k] = T(__ddiv_rn(f_num, f_den));
+    d.mem_cr[k] = T(cr_acc);
+    *d.write_index = (k + 1) % d.cfg.memory_size;
+  } else if (d.cfg.parameter == EVB_PAR_JADE) {  // de/parameter.hpp:107-120
+    double num = 0.0, den = 0.0, crm = 0.0;
+    for (int s = 0; s < n_succ; ++s) {  // lehmer_mean, de/parameter.hpp:45-52
+      const double v = double(d.F[d.succ[s]]);
+      num = __dadd_rn(num, __dmul_rn(v, v));
+      den = __dadd_rn(den, v);
+    }
+    const double lehmer = __ddiv_rn(num, den);
+    for (int s = 0; s < n_succ; ++s) crm = __dadd_rn(crm, double(d.CR[d.succ[s]]));
+    crm = __ddiv_rn(crm, double(n_succ));
+    const double c = double(T(d.cfg.jade_c));
+    d.mem_f[0] = T(__dadd_rn(__dmul_rn(__dsub_rn(1.0, c), double(d.mem_f[0])), __dmul_rn(c, lehmer)));
+    d.mem_cr[0] = T(__dadd_rn(__dmul_rn(__dsub_rn(1.0, c), double(d.mem_cr[0])), __dmul_rn(c, crm)));
+  }
+}
+
+// K5b: replaced parent -> archive slot, trial -> population (std::swap(pop[i], trial)).
+template <typename T>
+__global__ void de_select_apply_kernel(const de_dev<T> d) {
+  const int i = blockIdx.x;
+  if (!d.win[i]) return;
+  const int sl = d.arch_slot[i];
+  T* x = d.pop + size_t(i) * d.ldp;
+  const T* t = d.trial + size_t(i) * d.ldt;
+  T* a = sl >= 0 ? d.archive + size_t(sl) * d.ldt : nullptr;
+  for (int j = threadIdx.x; j < d.D; j += blockDim.x) {
+    const T old = x[j];
+    if (a) a[j] = old;
+    x[j] = t[j];
+  }
+  if (threadIdx.x == 0) d.fit[i] = d.trial_fit[i];
+}
+
+// init_population (core/population.hpp:88-98): P*D uniforms, individual-major
+template <typename T>
+__global__ void init_population_kernel(T* pop, int64_t ldp, int P, int D, double lb, double ub, word_source src,
+                                       uint64_t ctr_hi, int64_t base, int* overflow) {
+  const int64_t n = int64_t(P) * D;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t pos = base + e;
+    const uint64_t w = word_at(src, ctr_hi, pos, overflow);
+    const double u = u01_of(w);
+    pop[(e / D) * ldp + (e % D)] = T(__dadd_rn(lb, __dmul_rn(__dsub_rn(ub, lb), u)));
+  }
+}
+
+template <typename T>
+de_dev<T> make_dev(evb_de_s* e, void* pop, int64_t ldp, void* fit, double lb, double ub, evb_rng_s* r) {
+  de_dev<T> d{};
+  d.P = e->P;
+  d.D = e->D;
+  d.cfg = e->cfg;
+  d.p_count = e->p_count;
+  d.archive_cap = e->archive_cap;
+  d.pop = static_cast<T*>(pop);
+  d.ldp = ldp;
+  d.fit = static_cast<T*>(fit);
+  d.trial = static_cast<T*>(e->trial);
+  d.ldt = e->ldt;
+  d.trial_fit = static_cast<T*>(e->trial_fit);
+  d.F = static_cast<T*>(e->F);
+  d.CR = static_cast<T*>(e->CR);
+  d.slot = e->slot;
+  d.idx = e->idx;
+  d.jrand = e->jrand;
+  d.woff = e->woff;
+  d.wcount = e->wcount;
+  d.order = e->order;
+  d.win = e->win;
+  d.arch_slot = e->arch_slot;
+  d.owner = e->owner;
+  d.succ = e->succ;
+  d.archive = static_cast<T*>(e->archive);
+  d.arch_size = e->d_arch_size;
+  d.write_index = e->d_write_index;
+  d.arch_words = e->d_arch_words;
+  d.mem_f = static_cast<T*>(e->mem_f);
+  d.mem_cr = static_cast<T*>(e->mem_cr);
+  d.lb = T(lb);
+  d.ub = T(ub);
+  d.src.mode = r->mode;
+  d.src.key = r->key;
+  d.src.words = r->d_words;
+  d.src.n_words = r->n_words;
+  d.gen = r->gen;
+  d.cursor = r->d_cursor;
+  d.overflow = r->d_overflow;
+  return d;
+}
+
+template <typename T>
+void generation_t(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, void* pop, int64_t ldp, void* fit,
+                  double lb, double ub, evb_rng_s* r, cudaStream_t st) {
+  de_dev<T> d = make_dev<T>(e, pop, ldp, fit, lb, ub, r);
+  if (e->cfg.mutation == EVB_MUT_TTPB1 || e->cfg.mutation == EVB_MUT_BEST1) {
+    const int th = 256;
+    de_order_kernel<T><<<(e->P + th - 1) / th, th, th * sizeof(T), st>>>(d);
+    count_launch();
+  }
+  if (r->mode == RNG_PHILOX) {
+    de_draw_philox_kernel<T><<<(e->P + 127) / 128, 128, 0, st>>>(d);
+  } else {
+    de_draw_words_kernel<T><<<1, 32, 0, st>>>(d);
+  }
+  count_launch();
+  {
+    const int th = std::min(256, int(round_up((e->D + 2) / 2 + 1, 32)));
+    de_trial_kernel<T><<<e->P, th, 0, st>>>(d);
+    count_launch();
+  }
+  EVB_CUDA(cudaGetLastError());
+  // evaluate the trials with the scalar path's semantics (problem.evaluate via individual::evaluate)
+  eval_request rq{};
+  rq.prob = prob;
+  rq.scratch = sc;
+  rq.X = e->trial;
+  rq.n = e->P;
+  rq.ldx = e->ldt;
+  rq.out = e->trial_fit;
+  rq.ldo = e->P;
+  rq.n_out = 1;
+  rq.kinds[0] = prob->kind;
+  rq.biases[0] = prob->bias;
+  rq.stream = st;
+  rq.scalar_trig = true;
+  eval_dispatch(rq);
+  de_select_scan_kernel<T><<<1, 256, 0, st>>>(d);
+  count_launch();
+  {
+    const int th = std::min(256, int(round_up(e->D, 32)));
+    de_select_apply_kernel<T><<<e->P, th, 0, st>>>(d);
+    count_launch();
+  }
+  EVB_CUDA(cudaGetLastError());
+  e->last_gen = r->gen;
+  r->gen++;
+}
+
+template <typename T>
+void init_population_t(evb_de_s* e, void* pop, int64_t ldp, double lb, double ub, evb_rng_s* r, cudaStream_t st) {
+  word_source src{r->mode, r->key, r->d_words, r->n_words};
+  int64_t base = 0;
+  if (r->mode == RNG_WORDS) {
+    EVB_CUDA(cudaMemcpyAsync(&base, r->d_cursor, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    EVB_CUDA(cudaStreamSynchronize(st));
+  }
+  const uint64_t ctr_hi = (uint64_t(r->gen) << 32) | kSubInit;
+  init_population_kernel<T><<<std::min<int64_t>(4096, (int64_t(e->P) * e->D + 255) / 256), 256, 0, st>>>(
+      static_cast<T*>(pop), ldp, e->P, e->D, lb, ub, src, ctr_hi, base, r->d_overflow);
+  count_launch();
+  EVB_CUDA(cudaGetLastError());
+  if (r->mode == RNG_WORDS) {
+    const int64_t nb = base + int64_t(e->P) * e->D;
+    EVB_CUDA(cudaMemcpyAsync(r->d_cursor, &nb, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    EVB_CUDA(cudaStreamSynchronize(st));
+  } else {
+    r->gen++;
+  }
+}
+
+}  // namespace
+
+void de_generation(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, void* pop, int64_t ldp, void* fit,
+                   double lb, double ub, evb_rng_s* r, cudaStream_t st) {
+  if (e->dtype == EVB_F64) generation_t<double>(e, prob, sc, pop, ldp, fit, lb, ub, r, st);
+  else generation_t<float>(e, prob, sc, pop, ldp, fit, lb, ub, r, st);
+}
+
+void de_init_population(evb_de_s* e, void* pop, int64_t ldp, double lb, double ub, evb_rng_s* r, cudaStream_t st) {
+  if (e->dtype == EVB_F64) init_population_t<double>(e, pop, ldp, lb, ub, r, st);
+  else init_population_t<float>(e, pop, ldp, lb, ub, r, st);
+}
+
+}  // namespace evb
+
+// =============================================================================================
+// C ABI: random words + DE engine
+// =============================================================================================
+namespace evb {
+namespace {
+
+template <typename T>
+void* dalloc(size_t n) {
+  void* p = nullptr;
+  EVB_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+  EVB_CUDA(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(T)));
+  return p;
+}
+
+void free_de(evb_de_s* e) {
+  void* ptrs[] = {e->trial, e->trial_fit, e->F, e->CR, e->slot, e->idx, e->jrand, e->woff, e->wcount, e->order,
+                  e->win, e->arch_slot, e->owner, e->succ, e->archive, e->d_arch_size, e->d_write_index,
+                  e->d_arch_words, e->mem_f, e->mem_cr};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (e->eval_scratch) evb_scratch_destroy(e->eval_scratch);
+}
+
+const char* mutation_name(int m) {
+  return m == EVB_MUT_RAND1 ? "rand_1" : m == EVB_MUT_BEST1 ? "best_1" : m == EVB_MUT_TTPB1 ? "ttpb_1" : "?";
+}
+
+template <typename T>
+void reset_adapter(evb_de_s* e) {
+  const int H = std::max(1, e->cfg.memory_size);
+  std::vector<T> half(H, T(0.5));
+  EVB_CUDA(cudaMemcpy(e->mem_f, half.data(), sizeof(T) * H, cudaMemcpyHostToDevice));
+  EVB_CUDA(cudaMemcpy(e->mem_cr, half.data(), sizeof(T) * H, cudaMemcpyHostToDevice));
+  EVB_CUDA(cudaMemset(e->d_write_index, 0, sizeof(int)));
+}
+
+}  // namespace
+}  // namespace evb
+
+using namespace evb;
+
+extern "C" {
+
+int evb_rng_create_philox(uint64_t key, evb_rng* out) {
+  return guarded([&] {
+    require(out != nullptr, "rng: null output handle");
+    auto* r = new evb_rng_s();
+    r->mode = RNG_PHILOX;
+    r->key = key;
+    EVB_CUDA(cudaMalloc(&r->d_overflow, sizeof(int)));
+    EVB_CUDA(cudaMemset(r->d_overflow, 0, sizeof(int)));
+    EVB_CUDA(cudaMalloc(&r->d_cursor, sizeof(int64_t)));
+    EVB_CUDA(cudaMemset(r->d_cursor, 0, sizeof(int64_t)));
+    *out = r;
+  });
+}
+
+int evb_rng_create_words(const uint64_t* words, int64_t n_words, evb_rng* out) {
+  return guarded([&] {
+    require(out != nullptr && (words != nullptr || n_words == 0), "rng: null words or output handle");
+    require(n_words >= 0, "rng: negative word count");
+    auto* r = new evb_rng_s();
+    r->mode = RNG_WORDS;
+    r->n_words = n_words;
+    EVB_CUDA(cudaMalloc(&r->d_words, std::max<int64_t>(n_words, 1) * sizeof(uint64_t)));
+    if (n_words) EVB_CUDA(cudaMemcpy(r->d_words, words, n_words * sizeof(uint64_t), cudaMemcpyHostToDevice));
+    EVB_CUDA(cudaMalloc(&r->d_overflow, sizeof(int)));
+    EVB_CUDA(cudaMemset(r->d_overflow, 0, sizeof(int)));
+    EVB_CUDA(cudaMalloc(&r->d_cursor, sizeof(int64_t)));
+    EVB_CUDA(cudaMemset(r->d_cursor, 0, sizeof(int64_t)));
+    *out = r;
+  });
+}
+
+int evb_rng_destroy(evb_rng r) {
+  return guarded([&] {
+    if (!r) return;
+    if (r->d_words) cudaFree(r->d_words);
+    if (r->d_cursor) cudaFree(r->d_cursor);
+    if (r->d_overflow) cudaFree(r->d_overflow);
+    delete r;
+  });
+}
+
+int evb_rng_state(evb_rng r, int64_t* cursor, uint32_t* generation, int* overflow) {
+  return guarded([&] {
+    require(r != nullptr, "rng: null handle");
+    EVB_CUDA(cudaDeviceSynchronize());
+    int64_t c = 0;
+    int o = 0;
+    EVB_CUDA(cudaMemcpy(&c, r->d_cursor, sizeof(c), cudaMemcpyDeviceToHost));
+    EVB_CUDA(cudaMemcpy(&o, r->d_overflow, sizeof(o), cudaMemcpyDeviceToHost));
+    if (cursor) *cursor = c;
+    if (generation) *generation = r->gen;
+    if (overflow) *overflow = o;
+  });
+}
+
+int evb_rng_set_generation(evb_rng r, uint32_t generation) {
+  return guarded([&] {
+    require(r != nullptr, "rng: null handle");
+    r->gen = generation;
+  });
+}
+
+int evb_de_create(int dtype, const evb_de_config* c, int pop_size, int dim, evb_de* out) {
+  return guarded([&] {
+    require(dtype == EVB_F32 || dtype == EVB_F64, "de: dtype must be EVB_F32 or EVB_F64");
+    require(c != nullptr && out != nullptr, "de: null config or output handle");
+    require(c->mutation == EVB_MUT_RAND1 || c->mutation == EVB_MUT_BEST1 || c->mutation == EVB_MUT_TTPB1,
+            "de builder: unknown mutation strategy (GPU kernels: rand_1, best_1, ttpb_1)");
+    require(c->crossover == EVB_CX_BINOMIAL, "de builder: unknown crossover strategy (GPU kernels: binomial)");
+    require(c->repair == EVB_REP_CLIP || c->repair == EVB_REP_REFLECT || c->repair == EVB_REP_MIDPOINT_TARGET,
+            "de builder: unknown repair strategy (GPU kernels: clip, reflect, midpoint_target)");
+    require(c->parameter == EVB_PAR_FIXED || c->parameter == EVB_PAR_JADE || c->parameter == EVB_PAR_SHADE,
+            "de builder: unknown parameter adapter (GPU kernels: fixed, jade, shade)");
+    if (c->parameter == EVB_PAR_FIXED) {  // de/parameter.hpp:81-84
+      require(c->f > 0.0 && c->f <= 1.0, "fixed_parameter: F must be in (0,1]");
+      require(c->cr >= 0.0 && c->cr <= 1.0, "fixed_parameter: CR must be in [0,1]");
+    }
+    if (c->parameter == EVB_PAR_SHADE) require(c->memory_size >= 1, "shade_parameter: memory size must be >= 1");
+    if (c->parameter == EVB_PAR_JADE)
+      require(c->jade_c > 0.0 && c->jade_c <= 1.0, "jade_parameter: learning rate must be in (0,1]");
+    if (c->mutation == EVB_MUT_TTPB1)
+      require(c->p_best > 0.0 && c->p_best <= 1.0, "ttpb1_mutation: p-best fraction must be in (0,1]");
+    require(c->archive_rate >= 0.0, "de builder: archive rate must be >= 0");
+    const int min_pop = c->mutation == EVB_MUT_RAND1 ? 4 : 3;  // de/strategy.hpp:78, 102, 134
+    require(pop_size >= min_pop,
+            std::string("de_engine: population too small for mutation ") + mutation_name(c->mutation));
+    require(dim >= 1, "de: dim must be positive");
+
+    auto* e = new evb_de_s();
+    try {
+      e->dtype = dtype;
+      e->P = pop_size;
+      e->D = dim;
+      e->cfg.mutation = c->mutation;
+      e->cfg.crossover = c->crossover;
+      e->cfg.repair = c->repair;
+      e->cfg.parameter = c->parameter;
+      e->cfg.f = c->f;
+      e->cfg.cr = c->cr;
+      e->cfg.p_best = c->p_best;
+      e->cfg.use_archive = c->use_archive;
+      e->cfg.memory_size = c->parameter == EVB_PAR_SHADE ? c->memory_size : 1;
+      e->cfg.jade_c = c->jade_c;
+      e->cfg.archive_rate = c->archive_rate;
+      const size_t es = dtype == EVB_F64 ? 8 : 4;
+      // p_count = min(P, max(2, ceil(p * P))) with p stored in T (de/strategy.hpp:143)
+      const double p_t = dtype == EVB_F64 ? c->p_best : double(float(c->p_best));
+      e->p_count = c->mutation == EVB_MUT_TTPB1 ? std::min(pop_size, std::max(2, int(std::ceil(p_t * pop_size))))
+                                                : (c->mutation == EVB_MUT_BEST1 ? 1 : 0);
+      // archive_capacity_for (de/engine.hpp:137-139), archive_rate stored in T
+      const double rate_t = dtype == EVB_F64 ? c->archive_rate : double(float(c->archive_rate));
+      e->archive_cap = int(std::ceil(rate_t * double(pop_size)));
+      e->ldt = round_up(dim, 16 / int64_t(es));
+      auto bytes = [&](size_t n) { return n * es; };
+      EVB_CUDA(cudaMalloc(&e->trial, bytes(size_t(pop_size) * e->ldt)));
+      EVB_CUDA(cudaMemset(e->trial, 0, bytes(size_t(pop_size) * e->ldt)));
+      EVB_CUDA(cudaMalloc(&e->trial_fit, bytes(pop_size)));
+      EVB_CUDA(cudaMalloc(&e->F, bytes(pop_size)));
+      EVB_CUDA(cudaMalloc(&e->CR, bytes(pop_size)));
+      e->slot = static_cast<int*>(dalloc<int>(pop_size));
+      e->idx = static_cast<int*>(dalloc<int>(size_t(pop_size) * 4));
+      e->jrand = static_cast<int*>(dalloc<int>(pop_size));
+      e->woff = static_cast<int64_t*>(dalloc<int64_t>(pop_size));
+      e->wcount = static_cast<int64_t*>(dalloc<int64_t>(pop_size));
+      e->order = static_cast<int*>(dalloc<int>(std::max(1, e->p_count)));
+      e->win = static_cast<int*>(dalloc<int>(pop_size));
+      e->arch_slot = static_cast<int*>(dalloc<int>(pop_size));
+      e->owner = static_cast<int*>(dalloc<int>(std::max(1, e->archive_cap)));
+      e->succ = static_cast<int*>(dalloc<int>(pop_size));
+      EVB_CUDA(cudaMalloc(&e->archive, bytes(size_t(std::max(1, e->archive_cap)) * e->ldt)));
+      EVB_CUDA(cudaMemset(e->archive, 0, bytes(size_t(std::max(1, e->archive_cap)) * e->ldt)));
+      e->d_arch_size = static_cast<int*>(dalloc<int>(1));
+      e->d_write_index = static_cast<int*>(dalloc<int>(1));
+      e->d_arch_words = static_cast<int64_t*>(dalloc<int64_t>(1));
+      EVB_CUDA(cudaMalloc(&e->mem_f, bytes(e->cfg.memory_size)));
+      EVB_CUDA(cudaMalloc(&e->mem_cr, bytes(e->cfg.memory_size)));
+      if (dtype == EVB_F64) reset_adapter<double>(e);
+      else reset_adapter<float>(e);
+      EVB_CUDA(evb_scratch_create(&e->eval_scratch) == EVB_OK ? cudaSuccess : cudaErrorUnknown);
+    } catch (...) {
+      free_de(e);
+      delete e;
+      throw;
+    }
+    *out = e;
+  });
+}
+
+int evb_de_destroy(evb_de e) {
+  return guarded([&] {
+    if (!e) return;
+    free_de(e);
+    delete e;
+  });
+}
+
+int evb_de_reset(evb_de e) {
+  return guarded([&] {
+    require(e != nullptr, "de: null handle");
+    if (e->dtype == EVB_F64) reset_adapter<double>(e);
+    else reset_adapter<float>(e);
+    EVB_CUDA(cudaMemset(e->d_arch_size, 0, sizeof(int)));
+  });
+}
+
+int evb_de_archive_capacity(evb_de e) { return e ? e->archive_cap : -1; }
+int evb_de_p_count(evb_de e) { return e ? e->p_count : -1; }
+
+int evb_de_generation(evb_de e, evb_problem objective, evb_scratch s, void* pop, int64_t ldp, void* fitness,
+                      double lb, double ub, evb_rng rng, void* stream) {
+  return guarded([&] {
+    require(e && objective && rng && pop && fitness, "de_generation: null argument");
+    if (objective->p.dim != e->D) throw invalid_argument("de_generation: problem dimension mismatch");
+    if (objective->p.dtype != e->dtype) throw config_error("de_generation: problem dtype differs from engine");
+    if (ldp < e->D) throw invalid_argument("de_generation: ldp < dim");
+    de_generation(e, &objective->p, s ? s : e->eval_scratch, pop, ldp, fitness, lb, ub, rng,
+                  static_cast<cudaStream_t>(stream));
+  });
+}
+
+int evb_de_init_population(evb_de e, void* pop, int64_t ldp, double lb, double ub, evb_rng rng, void* stream) {
+  return guarded([&] {
+    require(e && rng && pop, "de_init_population: null argument");
+    require(lb < ub, "init_population: lb must be less than ub");
+    if (ldp < e->D) throw invalid_argument("de_init_population: ldp < dim");
+    de_init_population(e, pop, ldp, lb, ub, rng, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int evb_de_get_state(evb_de e, void* archive_host, int* archive_size, void* mem_f_host, void* mem_cr_host,
+                     int* write_index) {
+  return guarded([&] {
+    require(e != nullptr, "de: null handle");
+    EVB_CUDA(cudaDeviceSynchronize());
+    const size_t es = e->dtype == EVB_F64 ? 8 : 4;
+    int sz = 0;
+    EVB_CUDA(cudaMemcpy(&sz, e->d_arch_size, sizeof(int), cudaMemcpyDeviceToHost));
+    if (archive_size) *archive_size = sz;
+    if (archive_host && e->archive_cap > 0)
+      EVB_CUDA(cudaMemcpy2D(archive_host, e->D * es, e->archive, e->ldt * es, e->D * es, e->archive_cap,
+                            cudaMemcpyDeviceToHost));
+    if (mem_f_host) EVB_CUDA(cudaMemcpy(mem_f_host, e->mem_f, es * e->cfg.memory_size, cudaMemcpyDeviceToHost));
+    if (mem_cr_host) EVB_CUDA(cudaMemcpy(mem_cr_host, e->mem_cr, es * e->cfg.memory_size, cudaMemcpyDeviceToHost));
+    if (write_index) EVB_CUDA(cudaMemcpy(write_index, e->d_write_index, sizeof(int), cudaMemcpyDeviceToHost));
+  });
+}
+
+int evb_de_set_state(evb_de e, const void* archive_host, int archive_size, const void* mem_f_host,
+                     const void* mem_cr_host, int write_index) {
+  return guarded([&] {
+    require(e != nullptr, "de: null handle");
+    require(archive_size >= 0 && archive_size <= e->archive_cap, "de_set_state: archive size exceeds capacity");
+    const size_t es = e->dtype == EVB_F64 ? 8 : 4;
+    EVB_CUDA(cudaDeviceSynchronize());
+    if (archive_host && archive_size > 0)
+      EVB_CUDA(cudaMemcpy2D(e->archive, e->ldt * es, archive_host, e->D * es, e->D * es, archive_size,
+                            cudaMemcpyHostToDevice));
+    EVB_CUDA(cudaMemcpy(e->d_arch_size, &archive_size, sizeof(int), cudaMemcpyHostToDevice));
+    if (mem_f_host) EVB_CUDA(cudaMemcpy(e->mem_f, mem_f_host, es * e->cfg.memory_size, cudaMemcpyHostToDevice));
+    if (mem_cr_host) EVB_CUDA(cudaMemcpy(e->mem_cr, mem_cr_host, es * e->cfg.memory_size, cudaMemcpyHostToDevice));
+    require(write_index >= 0 && write_index < e->cfg.memory_size, "de_set_state: write index out of range");
+    EVB_CUDA(cudaMemcpy(e->d_write_index, &write_index, sizeof(int), cudaMemcpyHostToDevice));
+  });
+}
+
+int evb_de_last_draws(evb_de e, int64_t* word_counts, int64_t* archive_words, uint32_t* generation, void* F_host,
+                      void* CR_host, int* idx_host, int* jrand_host) {
+  return guarded([&] {
+    require(e != nullptr, "de: null handle");
+    EVB_CUDA(cudaDeviceSynchronize());
+    const size_t es = e->dtype == EVB_F64 ? 8 : 4;
+    if (word_counts) EVB_CUDA(cudaMemcpy(word_counts, e->wcount, sizeof(int64_t) * e->P, cudaMemcpyDeviceToHost));
+    if (archive_words) EVB_CUDA(cudaMemcpy(archive_words, e->d_arch_words, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    if (generation) *generation = e->last_gen;
+    if (F_host) EVB_CUDA(cudaMemcpy(F_host, e->F, es * e->P, cudaMemcpyDeviceToHost));
+    if (CR_host) EVB_CUDA(cudaMemcpy(CR_host, e->CR, es * e->P, cudaMemcpyDeviceToHost));
+    if (idx_host) EVB_CUDA(cudaMemcpy(idx_host, e->idx, sizeof(int) * 4 * e->P, cudaMemcpyDeviceToHost));
+    if (jrand_host) EVB_CUDA(cudaMemcpy(jrand_host, e->jrand, sizeof(int) * e->P, cudaMemcpyDeviceToHost));
+  });
+}
+
+int evb_de_optimize(evb_de e, evb_problem objective, evb_scratch s, void* pop, int64_t ldp, void* fitness, double lb,
+                    double ub, int64_t max_fes, evb_rng rng, int* best_index, double* best_fitness, int* generations,
+                    void* stream) {
+  return guarded([&] {
+    // de/engine.hpp:107-133
+    require(e && objective && rng && pop && fitness, "de_optimize: null argument");
+    require(max_fes > 0, "evolution_state: max_fes must be positive");
+    require(e->P >= 4, "init_population: pop_size must be at least 4");
+    if (objective->p.dim != e->D) throw invalid_argument("de_optimize: problem dimension mismatch");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    evb_scratch_s* sc = s ? s : e->eval_scratch;
+    de_init_population(e, pop, ldp, lb, ub, rng, st);
+    eval_request rq{};
+    rq.prob = &objective->p;
+    rq.scratch = sc;
+    rq.X = pop;
+    rq.n = e->P;
+    rq.ldx = ldp;
+    rq.out = fitness;
+    rq.ldo = e->P;
+    rq.n_out = 1;
+    rq.kinds[0] = objective->p.kind;
+    rq.biases[0] = objective->p.bias;
+    rq.stream = st;
+    rq.scalar_trig = true;
+    eval_dispatch(rq);
+    int64_t fes = e->P;
+    int gens = 0;
+    while (fes < max_fes) {
+      de_generation(e, &objective->p, sc, pop, ldp, fitness, lb, ub, rng, st);
+      fes += e->P;
+      ++gens;
+    }
+    // best (core/population.hpp:59-65): lowest fitness, ties to the lowest index
+    const size_t es = e->dtype == EVB_F64 ? 8 : 4;
+    std::vector<uint8_t> f(es * e->P);
+    EVB_CUDA(cudaMemcpyAsync(f.data(), fitness, es * e->P, cudaMemcpyDeviceToHost, st));
+    EVB_CUDA(cudaStreamSynchronize(st));
+    int best = 0;
+    auto val = [&](int i) {
+      return e->dtype == EVB_F64 ? reinterpret_cast<double*>(f.data())[i] : double(reinterpret_cast<float*>(f.data())[i]);
+    };
+    for (int i = 1; i < e->P; ++i)
+      if (val(i) < val(best)) best = i;
+    if (best_index) *best_index = best;
+    if (best_fitness) *best_fitness = val(best);
+    if (generations) *generations = gens;
+  });
+}
+
+}  // extern "C"
+
+namespace {
+__global__ void philox_words_kernel(uint64_t key, uint64_t ctr_hi, uint64_t start, int64_t n, uint64_t* out) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] = evb::philox_word(key, ctr_hi, start + uint64_t(i));
+}
+}  // namespace
+
+extern "C" int evb_philox_words(uint64_t key, uint64_t ctr_hi, uint64_t start, int64_t n, uint64_t* out_host) {
+  return guarded([&] {
+    require(n >= 0 && (out_host || n == 0), "philox_words: bad output");
+    if (n == 0) return;
+    uint64_t* d = nullptr;
+    EVB_CUDA(cudaMalloc(&d, n * sizeof(uint64_t)));
+    philox_words_kernel<<<(n + 255) / 256, 256>>>(key, ctr_hi, start, n, d);
+    evb::count_launch();
+    cudaError_t e = cudaMemcpy(out_host, d, n * sizeof(uint64_t), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    EVB_CUDA(e);
+  });
+}

@@ -258,28 +258,22 @@ __global__ void __launch_bounds__(f64_cfg<BM, BN, WM, WN, STAGES>::THREADS, 1)
 #pragma unroll
     for (int j = 0; j < C::TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+  const uint32_t smem_base = ptx::smem_u32(smem);
   for (int kb = 0; kb < KT; ++kb) {
     const int s = kb % STAGES;
     ptx::mbar_wait(&full[s], (kb / STAGES) & 1);
-    const uint8_t* st = smem + s * C::STAGE_BYTES;
-    const uint8_t* sA = st;
-    const uint8_t* sB = st + C::A_BYTES;
-    const double* sO = reinterpret_cast<const double*>(st + C::A_BYTES + C::B_BYTES);
+    const uint32_t sA = smem_base + s * C::STAGE_BYTES;
+    const uint32_t sB = sA + C::A_BYTES;
+    const uint32_t sO = sB + C::B_BYTES;
 #pragma unroll
     for (int ks = 0; ks < C::KB / 4; ++ks) {
       const int kk = ks * 4 + t;
-      const double o = sO[kk];
+      const double o = ptx::lds_f64(sO + kk * 8);
       double a[C::TM], b[C::TN];
 #pragma unroll
-      for (int i = 0; i < C::TM; ++i) {
-        const int r = rA + i * 8 + g;
-        a[i] = __dsub_rn(*reinterpret_cast<const double*>(sA + swz<8>(r, kk)), o);
-      }
+      for (int i = 0; i < C::TM; ++i) a[i] = __dsub_rn(ptx::lds_f64(sA + swz<8>(rA + i * 8 + g, kk)), o);
 #pragma unroll
-      for (int j = 0; j < C::TN; ++j) {
-        const int r = rB + j * 8 + g;
-        b[j] = *reinterpret_cast<const double*>(sB + swz<8>(r, kk));
-      }
+      for (int j = 0; j < C::TN; ++j) b[j] = ptx::lds_f64(sB + swz<8>(rB + j * 8 + g, kk));
 #pragma unroll
       for (int i = 0; i < C::TM; ++i)
 #pragma unroll
@@ -373,28 +367,24 @@ __global__ void __launch_bounds__(f32_cfg<BM, BN, STAGES>::THREADS, 1)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
 
+  const uint32_t smem_base = ptx::smem_u32(smem);
   for (int kb = 0; kb < KT; ++kb) {
     const int s = kb % STAGES;
     ptx::mbar_wait(&full[s], (kb / STAGES) & 1);
-    const uint8_t* st = smem + s * C::STAGE_BYTES;
-    const uint8_t* sA = st;
-    const uint8_t* sB = st + C::A_BYTES;
-    const float* sO = reinterpret_cast<const float*>(st + C::A_BYTES + C::B_BYTES);
+    const uint32_t sA = smem_base + s * C::STAGE_BYTES;
+    const uint32_t sB = sA + C::A_BYTES;
+    const uint32_t sO = sB + C::B_BYTES;
 #pragma unroll 2
     for (int kc = 0; kc < C::KB / 4; ++kc) {
-      const float4 o = *reinterpret_cast<const float4*>(sO + kc * 4);
+      const float4 o = ptx::lds_f32x4(sO + kc * 16);
       float4 a[8], b[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const int r = ty + C::TY * i;
-        float4 x = *reinterpret_cast<const float4*>(sA + swz<4>(r, kc * 4));
+        const float4 x = ptx::lds_f32x4(sA + swz<4>(ty + C::TY * i, kc * 4));
         a[i] = make_float4(__fsub_rn(x.x, o.x), __fsub_rn(x.y, o.y), __fsub_rn(x.z, o.z), __fsub_rn(x.w, o.w));
       }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int r = tx + C::TX * j;
-        b[j] = *reinterpret_cast<const float4*>(sB + swz<4>(r, kc * 4));
-      }
+      for (int j = 0; j < 8; ++j) b[j] = ptx::lds_f32x4(sB + swz<4>(tx + C::TX * j, kc * 4));
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -584,9 +574,9 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
     fp.counters = sc->counters;
   }
   if constexpr (std::is_same<T, double>::value) {
-    if (BM == 64 && BN == 112) launch_f64<64, 112, 2, 2>(tmX, tmM, fp, rq.stream);
-    else if (BM == 64 && BN == 128) launch_f64<64, 128, 2, 2>(tmX, tmM, fp, rq.stream);
-    else launch_f64<32, 128, 1, 4>(tmX, tmM, fp, rq.stream);
+    if (BM == 64 && BN == 112) launch_f64<64, 112, 4, 2>(tmX, tmM, fp, rq.stream);
+    else if (BM == 64 && BN == 128) launch_f64<64, 128, 4, 2>(tmX, tmM, fp, rq.stream);
+    else launch_f64<32, 128, 2, 4>(tmX, tmM, fp, rq.stream);
   } else {
     launch_f32<64, 128>(tmX, tmM, fp, rq.stream);
   }

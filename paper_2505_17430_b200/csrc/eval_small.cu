@@ -49,6 +49,7 @@ struct small_args {
   double biases[4];
   T* out;
   int64_t ldo;
+  int scalar_trig;
 };
 
 template <typename T>
@@ -106,7 +107,8 @@ __global__ void eval_small_kernel(const small_args<T> a) {
       a.out[b] = fop<T>::add(v, a.bias);
     } else {
       auto z = [&](int i) { return zrow[i]; };
-      const T v = base_value_seq<T, true>(a.kinds[o], D, z, a.ell_w);
+      const T v = a.scalar_trig ? base_value_seq<T, false>(a.kinds[o], D, z, a.ell_w)
+                                : base_value_seq<T, true>(a.kinds[o], D, z, a.ell_w);
       a.out[o * a.ldo + b] = fop<T>::add(v, T(a.biases[o]));
     }
   }
@@ -265,8 +267,11 @@ __global__ void eval_rows_kernel(const rows_args<T> a) {
     a.out[b] = base_value_seq<T, false>(a.kinds[0], a.D, z, a.ell_w);
     return;
   }
-  for (int o = 0; o < a.n_out; ++o)
-    a.out[o * a.ldo + b] = fop<T>::add(base_value_seq<T, true>(a.kinds[o], a.D, z, a.ell_w), T(a.biases[o]));
+  for (int o = 0; o < a.n_out; ++o) {
+    const T v = a.scalar_trig ? base_value_seq<T, false>(a.kinds[o], a.D, z, a.ell_w)
+                              : base_value_seq<T, true>(a.kinds[o], a.D, z, a.ell_w);
+    a.out[o * a.ldo + b] = fop<T>::add(v, T(a.biases[o]));
+  }
 }
 
 template <typename T>
@@ -366,7 +371,7 @@ void dispatch_t(const eval_request& rq) {
       a.perm = pr.perm; a.sub_kinds = pr.sub_kinds; a.chunk_sizes = pr.chunk_sizes; a.n_chunks = pr.n_chunks;
       a.bias = T(pr.bias); a.n_out = rq.n_out;
       for (int o = 0; o < rq.n_out; ++o) { a.kinds[o] = rq.kinds[o]; a.biases[o] = rq.biases[o]; }
-      a.out = static_cast<T*>(rq.out); a.ldo = rq.ldo;
+      a.out = static_cast<T*>(rq.out); a.ldo = rq.ldo; a.scalar_trig = rq.scalar_trig ? 1 : 0;
       set_smem_attr<T>(reinterpret_cast<const void*>(eval_small_kernel<T>), smem);
       eval_small_kernel<T><<<blocks, threads, smem, rq.stream>>>(a);
     }
@@ -395,7 +400,7 @@ void dispatch_t(const eval_request& rq) {
     for (int o = 0; o < rq.n_out; ++o) { a.kinds[o] = rq.kinds[o]; a.biases[o] = rq.biases[o]; }
     a.ell_w = static_cast<const T*>(pr.ell_w); a.hyb_w = static_cast<const T*>(pr.hyb_w);
     a.perm = pr.perm; a.sub_kinds = pr.sub_kinds; a.chunk_sizes = pr.chunk_sizes; a.n_chunks = pr.n_chunks;
-    a.bias = T(pr.bias); a.out = static_cast<T*>(rq.out); a.ldo = rq.ldo;
+    a.bias = T(pr.bias); a.out = static_cast<T*>(rq.out); a.ldo = rq.ldo; a.scalar_trig = rq.scalar_trig ? 1 : 0;
     eval_rows_kernel<T><<<rows_blocks, rows_threads, 0, rq.stream>>>(a);
     EVB_CUDA(cudaGetLastError());
     count_launch();

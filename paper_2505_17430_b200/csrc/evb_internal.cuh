@@ -41,6 +41,34 @@ inline void require(bool c, const std::string& msg) {
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
+// thread-local message behind evb_last_error (capi.cu)
+void set_last_error(const char* msg);
+
+// Run `fn`, mapping internal exceptions onto C status codes + evb_last_error.
+template <typename Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    set_last_error("");
+    return EVB_OK;
+  } catch (const invalid_argument& e) {
+    set_last_error(e.what());
+    return EVB_ERR_INVALID_ARGUMENT;
+  } catch (const config_error& e) {
+    set_last_error(e.what());
+    return EVB_ERR_CONFIG;
+  } catch (const logic_error& e) {
+    set_last_error(e.what());
+    return EVB_ERR_LOGIC;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return EVB_ERR_RUNTIME;
+  } catch (...) {
+    set_last_error("unknown error");
+    return EVB_ERR_RUNTIME;
+  }
+}
+
 // ---- problem representation ------------------------------------------------------------
 enum spec_kind { SPEC_BASE = 0, SPEC_HYBRID = 1, SPEC_COMPOSITION = 2 };
 
@@ -139,6 +167,9 @@ struct eval_request {
   int kinds[4];     // base kinds per output
   double biases[4]; // additive bias per output
   cudaStream_t stream;
+  bool scalar_trig = false;  // true: problem_instance::evaluate semantics (libm trig also for
+                             // float, problems/functions.hpp); false: evaluate_batch semantics
+                             // (fast_cos/fast_sin for float, problems/batch.hpp:17-33)
 };
 
 void eval_dispatch(const eval_request& rq);
