@@ -250,6 +250,7 @@ struct rows_args {
   T bias;
   T* out;
   int64_t ldo;
+  int scalar_trig;
 };
 
 template <typename T>
