@@ -881,12 +881,12 @@ int evb_de_optimize(evb_de e, evb_problem objective, evb_scratch s, void* pop, i
 
 }  // extern "C"
 
-namespace {
+namespace evb {
 __global__ void philox_words_kernel(uint64_t key, uint64_t ctr_hi, uint64_t start, int64_t n, uint64_t* out) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (i < n) out[i] = evb::philox_word(key, ctr_hi, start + uint64_t(i));
+  if (i < n) out[i] = philox_word(key, ctr_hi, start + uint64_t(i));
 }
-}  // namespace
+}  // namespace evb
 
 extern "C" int evb_philox_words(uint64_t key, uint64_t ctr_hi, uint64_t start, int64_t n, uint64_t* out_host) {
   return guarded([&] {
@@ -894,7 +894,7 @@ extern "C" int evb_philox_words(uint64_t key, uint64_t ctr_hi, uint64_t start, i
     if (n == 0) return;
     uint64_t* d = nullptr;
     EVB_CUDA(cudaMalloc(&d, n * sizeof(uint64_t)));
-    philox_words_kernel<<<(n + 255) / 256, 256>>>(key, ctr_hi, start, n, d);
+    evb::philox_words_kernel<<<(n + 255) / 256, 256>>>(key, ctr_hi, start, n, d);
     evb::count_launch();
     cudaError_t e = cudaMemcpy(out_host, d, n * sizeof(uint64_t), cudaMemcpyDeviceToHost);
     cudaFree(d);
