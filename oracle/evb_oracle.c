@@ -516,3 +516,217 @@ ORC_API void orc_eval_composition_f32(int dim, int n_comp, const int* kinds, con
   free(diff);
   free(z);
 }
+
+/* ------------------------------------------------------------------------------------------
+ * DE engine (de/engine.hpp, de/strategy.hpp, de/parameter.hpp) — fp64, restated
+ * ---------------------------------------------------------------------------------------- */
+enum { ORC_MUT_RAND1 = 0, ORC_MUT_BEST1 = 1, ORC_MUT_TTPB1 = 2 };
+enum { ORC_REP_CLIP = 0, ORC_REP_REFLECT = 1, ORC_REP_MIDPOINT = 2 };
+enum { ORC_PAR_FIXED = 0, ORC_PAR_JADE = 1, ORC_PAR_SHADE = 2 };
+
+typedef struct {
+  int mutation, repair, parameter;
+  double f, cr, p;
+  int use_archive, H;
+  double jade_c;
+  int P, D;
+  int archive_cap;
+  /* objective: base (kind >= 0) or composition (n_comp > 0) */
+  int kind;
+  const double *shift, *rot;
+  double bias;
+  int n_comp;
+  const int* comp_kinds;
+  const double *comp_shifts, *comp_rots, *sigma, *lambda, *cbias;
+} orc_de_cfg;
+
+typedef struct {
+  double* pop;     /* P x D */
+  double* fit;     /* P */
+  double* archive; /* cap x D */
+  int arch_size;
+  double* mem_f; /* H (JADE: [0]) */
+  double* mem_cr;
+  int write_index;
+} orc_de_state;
+
+static double orc_objective(const orc_de_cfg* c, const double* x, double* diff, double* z) {
+  if (c->n_comp > 0)
+    return composition_f64(c->n_comp, c->D, c->comp_kinds, c->comp_shifts, c->comp_rots, c->sigma, c->lambda,
+                           c->cbias, x, diff, z) + c->bias;
+  transform_f64(x, c->shift, c->rot, c->D, diff, z);
+  return base_value_f64(c->kind, z, c->D) + c->bias;
+}
+
+/* de/parameter.hpp:28-38, 41-43 */
+static double orc_sample_f(orc_rng* r, double mu) {
+  double f = 0.0;
+  for (int a = 0; a < 100; ++a) {
+    f = cauchy(r, mu, 0.1);
+    if (f > 0.0) break;
+  }
+  if (f <= 0.0) f = 0.1;
+  return f < 1.0 ? f : 1.0;
+}
+static double orc_sample_cr(orc_rng* r, double mu) {
+  const double v = normal(r, mu, 0.1);
+  return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+}
+
+/* core/population.hpp:70-77 stable ascending order (insertion sort keeps it stable) */
+static void orc_fitness_order(const double* fit, int P, int* order) {
+  for (int i = 0; i < P; ++i) order[i] = i;
+  for (int i = 1; i < P; ++i) {
+    const int v = order[i];
+    int j = i - 1;
+    while (j >= 0 && fit[v] < fit[order[j]]) {
+      order[j + 1] = order[j];
+      --j;
+    }
+    order[j + 1] = v;
+  }
+}
+
+/* One generation (de/engine.hpp:71-102).  Per-individual exports: F, CR, idx[4], jrand,
+ * words consumed, win mask; returns the archive-victim words consumed. */
+ORC_API int64_t orc_de_generation(const orc_de_cfg* c, orc_de_state* s, orc_rng* r, double lb, double ub,
+                                  double* F_out, double* CR_out, int* idx_out, int* jrand_out,
+                                  int64_t* words_out, int* win_out) {
+  const int P = c->P, D = c->D;
+  int* order = (int*)malloc(sizeof(int) * P);
+  double* trials = (double*)malloc(sizeof(double) * P * D);
+  double* tfit = (double*)malloc(sizeof(double) * P);
+  double* Fs = (double*)malloc(sizeof(double) * P);
+  double* CRs = (double*)malloc(sizeof(double) * P);
+  double* diff = (double*)malloc(sizeof(double) * D);
+  double* z = (double*)malloc(sizeof(double) * D);
+  double* donor = (double*)malloc(sizeof(double) * D);
+  orc_fitness_order(s->fit, P, order);
+  int p_count = (int)ceil(c->p * P); /* de/strategy.hpp:143 */
+  if (p_count < 2) p_count = 2;
+  if (p_count > P) p_count = P;
+  for (int i = 0; i < P; ++i) {
+    const int64_t w0 = r->consumed;
+    double F, CR;
+    if (c->parameter == ORC_PAR_SHADE) {
+      const int slot = uniform_int(r, c->H);
+      F = orc_sample_f(r, s->mem_f[slot]);
+      CR = orc_sample_cr(r, s->mem_cr[slot]);
+    } else if (c->parameter == ORC_PAR_JADE) {
+      F = orc_sample_f(r, s->mem_f[0]);
+      CR = orc_sample_cr(r, s->mem_cr[0]);
+    } else {
+      F = c->f;
+      CR = c->cr;
+    }
+    int a, b, cc;
+    const double *xa, *xb, *xc;
+    const double* xi = s->pop + (size_t)i * D;
+    if (c->mutation == ORC_MUT_RAND1) { /* de/strategy.hpp:84-93 */
+      do { a = uniform_int(r, P); } while (a == i);
+      do { b = uniform_int(r, P); } while (b == i || b == a);
+      do { cc = uniform_int(r, P); } while (cc == i || cc == a || cc == b);
+      xa = s->pop + (size_t)a * D; xb = s->pop + (size_t)b * D; xc = s->pop + (size_t)cc * D;
+      for (int j = 0; j < D; ++j) donor[j] = xa[j] + F * (xb[j] - xc[j]);
+    } else if (c->mutation == ORC_MUT_BEST1) { /* de/strategy.hpp:104-118 */
+      a = order[0];
+      do { b = uniform_int(r, P); } while (b == i);
+      do { cc = uniform_int(r, P); } while (cc == i || cc == b);
+      xa = s->pop + (size_t)a * D; xb = s->pop + (size_t)b * D; xc = s->pop + (size_t)cc * D;
+      for (int j = 0; j < D; ++j) donor[j] = xa[j] + F * (xb[j] - xc[j]);
+    } else { /* de/strategy.hpp:138-160 */
+      a = order[uniform_int(r, p_count)];
+      do { b = uniform_int(r, P); } while (b == i);
+      const int pool = P + (c->use_archive ? s->arch_size : 0);
+      do { cc = uniform_int(r, pool); } while (cc == i || cc == b);
+      xa = s->pop + (size_t)a * D; xb = s->pop + (size_t)b * D;
+      xc = cc < P ? s->pop + (size_t)cc * D : s->archive + (size_t)(cc - P) * D;
+      for (int j = 0; j < D; ++j) donor[j] = xi[j] + F * (xa[j] - xi[j]) + F * (xb[j] - xc[j]);
+    }
+    /* binomial crossover, de/strategy.hpp:184-194 */
+    const int jr = uniform_int(r, D);
+    double* t = trials + (size_t)i * D;
+    for (int j = 0; j < D; ++j) {
+      const double u = uniform01(r);
+      t[j] = (u < CR || j == jr) ? donor[j] : xi[j];
+    }
+    /* repair, de/strategy.hpp:229-277 */
+    for (int j = 0; j < D; ++j) {
+      double g = t[j];
+      if (c->repair == ORC_REP_CLIP) {
+        if (g < lb) g = lb;
+        if (g > ub) g = ub;
+      } else if (c->repair == ORC_REP_MIDPOINT) {
+        if (g < lb) g = (lb + xi[j]) / 2.0;
+        else if (g > ub) g = (ub + xi[j]) / 2.0;
+      } else {
+        for (int fold = 0; (g < lb || g > ub) && fold < 100; ++fold) {
+          if (g < lb) g = lb + (lb - g);
+          if (g > ub) g = ub - (g - ub);
+        }
+        if (g < lb) g = lb;
+        if (g > ub) g = ub;
+      }
+      t[j] = g;
+    }
+    tfit[i] = orc_objective(c, t, diff, z);
+    Fs[i] = F;
+    CRs[i] = CR;
+    if (F_out) F_out[i] = F;
+    if (CR_out) CR_out[i] = CR;
+    if (idx_out) { idx_out[4 * i] = a; idx_out[4 * i + 1] = b; idx_out[4 * i + 2] = cc; idx_out[4 * i + 3] = 0; }
+    if (jrand_out) jrand_out[i] = jr;
+    if (words_out) words_out[i] = r->consumed - w0;
+  }
+  /* select_and_archive, de/engine.hpp:27-47 + adapter update */
+  const int64_t aw0 = r->consumed;
+  double gain_sum = 0.0;
+  int n_succ = 0;
+  int* succ = (int*)malloc(sizeof(int) * P);
+  double* gains = (double*)malloc(sizeof(double) * P);
+  for (int i = 0; i < P; ++i) {
+    const int w = tfit[i] <= s->fit[i];
+    if (win_out) win_out[i] = w;
+    if (!w) continue;
+    const double gain = s->fit[i] - tfit[i];
+    if (gain > 0.0) { succ[n_succ] = i; gains[n_succ] = gain; ++n_succ; }
+    if (c->archive_cap > 0) { /* de/strategy.hpp:29-37 */
+      if (s->arch_size < c->archive_cap) {
+        memcpy(s->archive + (size_t)s->arch_size * D, s->pop + (size_t)i * D, sizeof(double) * D);
+        s->arch_size++;
+      } else {
+        const int v = uniform_int(r, s->arch_size);
+        memcpy(s->archive + (size_t)v * D, s->pop + (size_t)i * D, sizeof(double) * D);
+      }
+    }
+    memcpy(s->pop + (size_t)i * D, trials + (size_t)i * D, sizeof(double) * D);
+    s->fit[i] = tfit[i];
+  }
+  if (n_succ > 0 && c->parameter == ORC_PAR_SHADE) { /* de/parameter.hpp:166-184 */
+    for (int k = 0; k < n_succ; ++k) gain_sum += gains[k];
+    double fn = 0.0, fd = 0.0, ca = 0.0;
+    for (int k = 0; k < n_succ; ++k) {
+      const double w = gains[k] / gain_sum;
+      const double f = Fs[succ[k]];
+      fn += w * f * f;
+      fd += w * f;
+      ca += w * CRs[succ[k]];
+    }
+    s->mem_f[s->write_index] = fn / fd;
+    s->mem_cr[s->write_index] = ca;
+    s->write_index = (s->write_index + 1) % c->H;
+  } else if (n_succ > 0 && c->parameter == ORC_PAR_JADE) { /* de/parameter.hpp:107-120 */
+    double num = 0.0, den = 0.0, crm = 0.0;
+    for (int k = 0; k < n_succ; ++k) { num += Fs[succ[k]] * Fs[succ[k]]; den += Fs[succ[k]]; }
+    for (int k = 0; k < n_succ; ++k) crm += CRs[succ[k]];
+    crm /= (double)n_succ;
+    s->mem_f[0] = (1.0 - c->jade_c) * s->mem_f[0] + c->jade_c * (num / den);
+    s->mem_cr[0] = (1.0 - c->jade_c) * s->mem_cr[0] + c->jade_c * crm;
+  }
+  const int64_t aw = r->consumed - aw0;
+  free(order); free(trials); free(tfit); free(Fs); free(CRs); free(diff); free(z); free(donor); free(succ); free(gains);
+  return aw;
+}
+
+ORC_API int orc_de_cfg_size(void) { return (int)sizeof(orc_de_cfg); }
+ORC_API int orc_de_state_size(void) { return (int)sizeof(orc_de_state); }

@@ -234,3 +234,164 @@ def eval_composition(kinds, shifts, rots, sigma, lam, cbias, bias, X):
         C().orc_eval_composition_f32(d, len(k), ptr(k), ptr(o), ptr(m), ptr(sg), ptr(la), ptr(cb), np.float32(bias),
                                      n, ptr(X), d, ptr(out))
     return out
+
+
+# ---- DE: the reference engine (REF) and the C restatement (C) -------------------------------------
+REF_DE_SIG = {
+    "ref_de_create": (vp, [c_int, c_int, c_int, c_double, c_double, c_double, c_int, c_int, c_double, c_double,
+                           c_int, c_int]),
+    "ref_de_destroy": (None, [vp]),
+    "ref_de_set_problem_base": (None, [vp, c_int, vp, vp, c_double]),
+    "ref_de_set_problem_composition": (None, [vp, c_int, vp, vp, vp, vp, vp, vp, c_double]),
+    "ref_de_set_pop": (None, [vp, vp, vp]),
+    "ref_de_init": (i64, [vp, vp, i64, c_double, c_double]),
+    "ref_de_generation": (c_int, [vp, vp, i64, c_double, c_double]),
+    "ref_de_get": (None, [vp, vp, vp, vp, vp, vp, vp, vp]),
+    "ref_de_native_run": (None, [vp, u64, u64, c_int, c_double, c_double]),
+}
+register_ref(REF_DE_SIG)
+
+MUT = {"rand_1": 0, "best_1": 1, "ttpb_1": 2}
+REP = {"clip": 0, "reflect": 1, "midpoint_target": 2}
+ADA = {"fixed": 0, "jade": 1, "shade": 2}
+
+
+class RefDE:
+    """The reference de_engine<double> (built through de_builder) stepped one generation at a
+    time with rng_stream::scripted word lists (or run natively)."""
+
+    def __init__(self, cfg, P, D):
+        self.P, self.D, self.cfg = P, D, cfg
+        self.H = max(1, cfg.memory_size if cfg.parameter == "shade" else 1)
+        self.h = REF().ref_de_create(MUT[cfg.mutation], REP[cfg.repair], ADA[cfg.parameter], cfg.f, cfg.cr,
+                                     cfg.p_best, int(cfg.use_archive), self.H, cfg.jade_c, cfg.archive_rate, P, D)
+        self._keep = []
+
+    def set_problem_base(self, kind, shift, rot, bias):
+        o = np.ascontiguousarray(shift, np.float64)
+        m = np.ascontiguousarray(rot, np.float64).ravel()
+        self._keep += [o, m]
+        REF().ref_de_set_problem_base(self.h, int(kind), ptr(o), ptr(m), bias)
+
+    def set_problem_composition(self, kinds, shifts, rots, sigma, lam, cbias, bias=0.0):
+        arrs = [np.ascontiguousarray(kinds, np.int32), np.ascontiguousarray(shifts, np.float64),
+                np.ascontiguousarray(rots, np.float64), np.ascontiguousarray(sigma, np.float64),
+                np.ascontiguousarray(lam, np.float64), np.ascontiguousarray(cbias, np.float64)]
+        self._keep += arrs
+        REF().ref_de_set_problem_composition(self.h, len(arrs[0]), *[ptr(a) for a in arrs], bias)
+
+    def set_pop(self, x, fit):
+        x = np.ascontiguousarray(x, np.float64)
+        f = np.ascontiguousarray(fit, np.float64)
+        REF().ref_de_set_pop(self.h, ptr(x), ptr(f))
+
+    def init(self, words, lb, ub):
+        w = np.ascontiguousarray(words, np.uint64)
+        return int(REF().ref_de_init(self.h, ptr(w), len(w), lb, ub))
+
+    def generation(self, words, lb, ub) -> bool:
+        w = np.ascontiguousarray(words, np.uint64)
+        return bool(REF().ref_de_generation(self.h, ptr(w), len(w), lb, ub))
+
+    def native_run(self, seed, stream, generations, lb, ub):
+        REF().ref_de_native_run(self.h, seed, stream, generations, lb, ub)
+
+    def get(self):
+        x = np.empty((self.P, self.D))
+        f = np.empty(self.P)
+        cap = max(1, int(np.ceil(self.cfg.archive_rate * self.P)))
+        a = np.zeros((cap, self.D))
+        sz, wi = ctypes.c_int(), ctypes.c_int()
+        mf = np.zeros(self.H)
+        mc = np.zeros(self.H)
+        REF().ref_de_get(self.h, ptr(x), ptr(f), ptr(a), ctypes.byref(sz), ptr(mf), ptr(mc), ctypes.byref(wi))
+        return {"pop": x, "fit": f, "archive": a[:sz.value], "archive_size": sz.value, "memory_f": mf,
+                "memory_cr": mc, "write_index": wi.value}
+
+    def __del__(self):
+        try:
+            REF().ref_de_destroy(self.h)
+        except Exception:
+            pass
+
+
+class _OrcDeCfg(ctypes.Structure):
+    _fields_ = [("mutation", c_int), ("repair", c_int), ("parameter", c_int), ("f", c_double), ("cr", c_double),
+                ("p", c_double), ("use_archive", c_int), ("H", c_int), ("jade_c", c_double), ("P", c_int),
+                ("D", c_int), ("archive_cap", c_int), ("kind", c_int), ("shift", vp), ("rot", vp),
+                ("bias", c_double), ("n_comp", c_int), ("comp_kinds", vp), ("comp_shifts", vp), ("comp_rots", vp),
+                ("sigma", vp), ("lambda_", vp), ("cbias", vp)]
+
+
+class _OrcDeState(ctypes.Structure):
+    _fields_ = [("pop", vp), ("fit", vp), ("archive", vp), ("arch_size", c_int), ("mem_f", vp), ("mem_cr", vp),
+                ("write_index", c_int)]
+
+
+register_c({
+    "orc_de_generation": (i64, [ctypes.POINTER(_OrcDeCfg), ctypes.POINTER(_OrcDeState), vp, c_double, c_double, vp,
+                                vp, vp, vp, vp, vp]),
+    "orc_de_cfg_size": (c_int, []),
+    "orc_de_state_size": (c_int, []),
+})
+
+
+class OracleDE:
+    """The C restatement of de_engine::generation (oracle/evb_oracle.c), exporting the integer
+    outputs (donor indices, jrand, selection mask, words per individual)."""
+
+    def __init__(self, cfg, P, D):
+        assert C().orc_de_cfg_size() == ctypes.sizeof(_OrcDeCfg)
+        self.cfg, self.P, self.D = cfg, P, D
+        self.H = max(1, cfg.memory_size if cfg.parameter == "shade" else 1)
+        self.cap = int(np.ceil(cfg.archive_rate * P))
+        self.c = _OrcDeCfg(MUT[cfg.mutation], REP[cfg.repair], ADA[cfg.parameter], cfg.f, cfg.cr, cfg.p_best,
+                           int(cfg.use_archive), self.H, cfg.jade_c, P, D, self.cap)
+        self.c.kind = -1
+        self.pop = np.zeros((P, D))
+        self.fit = np.zeros(P)
+        self.archive = np.zeros((max(1, self.cap), D))
+        self.mem_f = np.full(self.H, 0.5)
+        self.mem_cr = np.full(self.H, 0.5)
+        self.s = _OrcDeState(ptr(self.pop), ptr(self.fit), ptr(self.archive), 0, ptr(self.mem_f), ptr(self.mem_cr), 0)
+        self._keep = []
+
+    def set_problem_base(self, kind, shift, rot, bias):
+        o = np.ascontiguousarray(shift, np.float64)
+        m = np.ascontiguousarray(rot, np.float64).ravel()
+        self._keep += [o, m]
+        self.c.kind, self.c.shift, self.c.rot, self.c.bias = int(kind), o.ctypes.data, m.ctypes.data, bias
+
+    def set_problem_composition(self, kinds, shifts, rots, sigma, lam, cbias, bias=0.0):
+        arrs = [np.ascontiguousarray(kinds, np.int32), np.ascontiguousarray(shifts, np.float64),
+                np.ascontiguousarray(rots, np.float64), np.ascontiguousarray(sigma, np.float64),
+                np.ascontiguousarray(lam, np.float64), np.ascontiguousarray(cbias, np.float64)]
+        self._keep += arrs
+        self.c.n_comp = len(arrs[0])
+        (self.c.comp_kinds, self.c.comp_shifts, self.c.comp_rots, self.c.sigma, self.c.lambda_,
+         self.c.cbias) = [a.ctypes.data for a in arrs]
+        self.c.bias = bias
+
+    def set_state(self, pop, fit, archive=None, arch_size=0, mem_f=None, mem_cr=None, write_index=0):
+        self.pop[:] = pop
+        self.fit[:] = fit
+        if archive is not None and arch_size:
+            self.archive[:arch_size] = archive[:arch_size]
+        self.s.arch_size = arch_size
+        if mem_f is not None:
+            self.mem_f[:] = mem_f
+            self.mem_cr[:] = mem_cr
+        self.s.write_index = write_index
+
+    def generation(self, words, lb, ub):
+        w = np.ascontiguousarray(words, np.uint64)
+        rng = ctypes.create_string_buffer(C().orc_rng_size())
+        C().orc_rng_scripted(rng, ptr(w), len(w))
+        P = self.P
+        out = {"F": np.zeros(P), "CR": np.zeros(P), "idx": np.zeros((P, 4), np.int32), "jrand": np.zeros(P, np.int32),
+               "words": np.zeros(P, np.int64), "win": np.zeros(P, np.int32)}
+        aw = C().orc_de_generation(ctypes.byref(self.c), ctypes.byref(self.s), rng, lb, ub, ptr(out["F"]),
+                                   ptr(out["CR"]), ptr(out["idx"]), ptr(out["jrand"]), ptr(out["words"]),
+                                   ptr(out["win"]))
+        out["archive_words"] = int(aw)
+        return out

@@ -212,3 +212,142 @@ REF_API void ref_batch_job_run(void* job, int threads, void* out) {
 REF_API void ref_batch_job_destroy(void* job) { delete static_cast<ref_batch_job*>(job); }
 
 REF_API int ref_hardware_threads(void) { return int(std::thread::hardware_concurrency()); }
+
+// ---- DE engine (de/engine.hpp) driven generation by generation ----------------------------------
+namespace {
+
+struct ref_de_run {
+  std::unique_ptr<de::de_engine<double>> engine;
+  std::unique_ptr<problem_instance<double>> problem;
+  population<double> pop;
+  int P = 0, D = 0;
+};
+
+std::unique_ptr<de::mutation_strategy<double>> make_mutation(int m, double p, int use_archive) {
+  if (m == 0) return std::make_unique<de::rand1_mutation<double>>();
+  if (m == 1) return std::make_unique<de::best1_mutation<double>>();
+  return std::make_unique<de::ttpb1_mutation<double>>(p, use_archive != 0);
+}
+std::unique_ptr<de::repair_strategy<double>> make_repair(int r) {
+  if (r == 0) return std::make_unique<de::clip_repair<double>>();
+  if (r == 1) return std::make_unique<de::reflect_repair<double>>();
+  return std::make_unique<de::midpoint_target_repair<double>>();
+}
+std::unique_ptr<de::parameter_adapter<double>> make_adapter(int a, double f, double cr, int H, double c) {
+  if (a == 0) return std::make_unique<de::fixed_parameter<double>>(f, cr);
+  if (a == 1) return std::make_unique<de::jade_parameter<double>>(c);
+  return std::make_unique<de::shade_parameter<double>>(H);
+}
+
+}  // namespace
+
+// Engine built through the reference de_builder from the same strategy choices as evb_de_config.
+REF_API void* ref_de_create(int mutation, int repair, int adapter, double f, double cr, double p, int use_archive,
+                            int H, double jade_c, double archive_rate, int P, int D) {
+  auto* r = new ref_de_run();
+  r->engine = std::make_unique<de::de_engine<double>>(de::de_builder<double>()
+                                                          .mutation(make_mutation(mutation, p, use_archive))
+                                                          .crossover(std::make_unique<de::binomial_crossover<double>>())
+                                                          .repair(make_repair(repair))
+                                                          .parameter(make_adapter(adapter, f, cr, H, jade_c))
+                                                          .population(de::population_policy::fixed())
+                                                          .archive_rate(archive_rate)
+                                                          .build());
+  r->P = P;
+  r->D = D;
+  r->pop = population<double>(P, D);
+  rng_stream dummy(0, 0);
+  r->engine->archive().set_capacity(r->engine->archive_capacity_for(P), dummy);
+  return r;
+}
+REF_API void ref_de_destroy(void* h) { delete static_cast<ref_de_run*>(h); }
+
+REF_API void ref_de_set_problem_base(void* h, int kind, const double* shift, const double* rot, double bias) {
+  auto* r = static_cast<ref_de_run*>(h);
+  r->problem = std::make_unique<problem_instance<double>>(make_base<double>(kind, r->D, shift, rot, bias));
+}
+REF_API void ref_de_set_problem_composition(void* h, int n_comp, const int* kinds, const double* shifts,
+                                            const double* rots, const double* sigma, const double* lambda,
+                                            const double* cbias, double bias) {
+  auto* r = static_cast<ref_de_run*>(h);
+  r->problem = std::make_unique<problem_instance<double>>(
+      make_comp<double>(r->D, n_comp, kinds, shifts, rots, sigma, lambda, cbias, bias));
+}
+
+REF_API void ref_de_set_pop(void* h, const double* x, const double* fit) {
+  auto* r = static_cast<ref_de_run*>(h);
+  for (int i = 0; i < r->P; ++i) {
+    std::memcpy(r->pop[i].genome.data(), x + size_t(i) * r->D, sizeof(double) * r->D);
+    r->pop[i].fitness = fit[i];
+    r->pop[i].evaluated = true;
+  }
+}
+
+// init_population + evaluation exactly as de_engine::optimize does (de/engine.hpp:118-122), from
+// a scripted word list; returns the number of words consumed.
+REF_API int64_t ref_de_init(void* h, const uint64_t* words, int64_t n, double lb, double ub) {
+  auto* r = static_cast<ref_de_run*>(h);
+  std::vector<uint64_t> w(words, words + n);
+  w.push_back(0x5e5e5e5e5e5e5e5eULL);
+  rng_stream rng = rng_stream::scripted(w);
+  r->pop = init_population<double>(r->P, r->D, lb, ub, rng);
+  eval_scratch<double> scratch;
+  for (auto& m : r->pop) m.evaluate([&](std::span<const double> x) { return r->problem->evaluate(x, scratch); });
+  int64_t used = 0;
+  while (rng.next_u64() != 0x5e5e5e5e5e5e5e5eULL && used <= n) ++used;
+  return n - used;  // words consumed
+}
+
+// One de_engine::generation with rng_stream::scripted(words + sentinel).  Returns 1 when the
+// engine consumed exactly n words (the next word is the sentinel), 0 otherwise.
+REF_API int ref_de_generation(void* h, const uint64_t* words, int64_t n, double lb, double ub) {
+  auto* r = static_cast<ref_de_run*>(h);
+  const uint64_t sentinel = 0xa5a5a5a5deadbeefULL;
+  std::vector<uint64_t> w(words, words + n);
+  w.push_back(sentinel);
+  rng_stream rng = rng_stream::scripted(w);
+  evolution_state st(1LL << 40, r->P, r->D, std::min(4, r->P));
+  eval_scratch<double> scratch;
+  auto objective = [&](std::span<const double> x) { return r->problem->evaluate(x, scratch); };
+  r->engine->generation(r->pop, st, objective, lb, ub, rng);
+  return rng.next_u64() == sentinel ? 1 : 0;
+}
+
+REF_API void ref_de_get(void* h, double* x, double* fit, double* archive, int* arch_size, double* mem_f,
+                        double* mem_cr, int* write_index) {
+  auto* r = static_cast<ref_de_run*>(h);
+  for (int i = 0; i < r->P; ++i) {
+    if (x) std::memcpy(x + size_t(i) * r->D, r->pop[i].genome.data(), sizeof(double) * r->D);
+    if (fit) fit[i] = r->pop[i].fitness;
+  }
+  auto& ar = r->engine->archive();
+  if (arch_size) *arch_size = ar.size();
+  if (archive)
+    for (int j = 0; j < ar.size(); ++j)
+      std::memcpy(archive + size_t(j) * r->D, ar.member(j).data(), sizeof(double) * r->D);
+  auto& ad = r->engine->parameter();
+  if (auto* s = dynamic_cast<de::shade_parameter<double>*>(&ad)) {
+    if (mem_f) std::memcpy(mem_f, s->memory_f().data(), sizeof(double) * s->memory_f().size());
+    if (mem_cr) std::memcpy(mem_cr, s->memory_cr().data(), sizeof(double) * s->memory_cr().size());
+    if (write_index) *write_index = s->write_index();
+  } else if (auto* j = dynamic_cast<de::jade_parameter<double>*>(&ad)) {
+    if (mem_f) mem_f[0] = j->mu_f();
+    if (mem_cr) mem_cr[0] = j->mu_cr();
+    if (write_index) *write_index = 0;
+  }
+}
+
+// The reference's own run with its NATIVE stream: rng_stream(seed, stream) -> init_population,
+// evaluate, set_capacity, `generations` generations (de/engine.hpp:107-133 without the budget
+// loop).  Used for the config-0 exact replay.
+REF_API void ref_de_native_run(void* h, uint64_t seed, uint64_t stream, int generations, double lb, double ub) {
+  auto* r = static_cast<ref_de_run*>(h);
+  rng_stream rng(seed, stream);
+  r->pop = init_population<double>(r->P, r->D, lb, ub, rng);
+  eval_scratch<double> scratch;
+  auto objective = [&](std::span<const double> x) { return r->problem->evaluate(x, scratch); };
+  for (auto& m : r->pop) m.evaluate(objective);
+  r->engine->archive().set_capacity(r->engine->archive_capacity_for(r->P), rng);
+  evolution_state st(1LL << 40, r->P, r->D, std::min(4, r->P));
+  for (int g = 0; g < generations; ++g) r->engine->generation(r->pop, st, objective, lb, ub, rng);
+}

@@ -1,0 +1,210 @@
+"""GPU parity of the DE engine (K4/K5/K6 + RNG) against the reference engine (oracle/_ref) and the
+C restatement (oracle/evb_oracle.c, which exports the integer outputs).
+
+* config 0 — rand/1/bin, F 0.5, CR 0.9, D=10, pop 100, Rastrigin on 0.0512*M(x-o), words of
+  rng_stream(42, 0) (the reference's native stream; WORDS mode): population bit-exact after
+  init_population + one generation; donor indices, jrand and selection mask bit-exact.
+* criterion-1 style — 50 generations bit-exact (tests/acceptance.cpp:98-132).
+* config 2 — SHADE (ttpb/1 p=0.11, archive = pop, midpoint repair), D=100, pop 180, Ackley, Philox:
+  lockstep per generation (GPU state re-synced from the reference, SURVEY §7 hard part 3); F/CR
+  come from tan/log/cos, so ulp-level F/CR differences are counted and flagged, everything
+  integer must match exactly.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+
+torch = pytest.importorskip("torch")
+import paper_2505_17430_b200 as evb  # noqa: E402
+from paper_2505_17430_b200.de import (DEConfig, DEEngine, Rng, preset_de, preset_shade,  # noqa: E402
+                                      scripted_words_for_generation)
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")]
+
+
+def dev_eval(problem, x, dev):
+    sc = evb.EvalScratch()
+    X = x if torch.is_tensor(x) else torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+    out = torch.empty(X.shape[0], dtype=X.dtype, device=dev)
+    evb.evaluate_batch(problem, X, sc, out)
+    return out
+
+
+def test_config0_native_stream_exact(dev):
+    P, D = 100, 10
+    o, m = O.shift_rotation(42, D)
+    m = m * 0.0512
+    cfg = preset_de(0.5, 0.9)
+    # reference: its own engine on its own stream rng_stream(42, 0)
+    ref = O.RefDE(cfg, P, D)
+    ref.set_problem_base(5, o, m, 0.0)
+    ref.native_run(42, 0, 1, -100.0, 100.0)
+    st = ref.get()
+    # GPU: the same words, consumed in the reference's order
+    words = O.rng_words(42, 0, P * D + P * (D + 30))
+    rng = Rng.words(words)
+    eng = DEEngine(cfg, P, D)
+    prob = evb.ProblemInstance.base(evb.BaseKind.rastrigin, o, m, 0.0)
+    pop = torch.empty((P, D), dtype=torch.float64, device=dev)
+    eng.init_population(pop, -100.0, 100.0, rng)
+    fit = dev_eval(prob, pop, dev)
+    x0, f0 = pop.cpu().numpy().copy(), fit.cpu().numpy().copy()
+    eng.generation(prob, pop, fit, -100.0, 100.0, rng)
+    torch.cuda.synchronize()
+    assert np.array_equal(pop.cpu().numpy(), st["pop"])
+    got_f = fit.cpu().numpy()
+    assert np.max(np.abs(got_f - st["fit"]) / np.maximum(1, np.abs(st["fit"]))) <= 1e-12
+    # integer outputs against the C restatement on the same words
+    orc = O.OracleDE(cfg, P, D)
+    orc.set_problem_base(5, o, m, 0.0)
+    orc.set_state(x0, f0)
+    out = orc.generation(words[P * D:], -100.0, 100.0)
+    dr = eng.last_draws()
+    assert np.array_equal(dr["idx"][:, :3], out["idx"][:, :3])
+    assert np.array_equal(dr["jrand"], out["jrand"])
+    assert np.array_equal(dr["word_counts"], out["words"])
+    assert rng.state()["cursor"] == P * D + int(out["words"].sum())
+    assert not rng.state()["overflow"]
+
+
+@pytest.mark.parametrize("kind", [0, 5])
+def test_criterion1_fifty_generations_exact(dev, kind):
+    # acceptance criterion 1 style: pop 30, D 10, 50 generations, stream (12345, 0)
+    P, D, G = 30, 10, 50
+    o, m = O.shift_rotation(7, D)
+    cfg = preset_de(0.5, 0.9)
+    ref = O.RefDE(cfg, P, D)
+    ref.set_problem_base(kind, o, m, 0.0)
+    ref.native_run(12345, 0, G, -100.0, 100.0)
+    st = ref.get()
+    words = O.rng_words(12345, 0, P * D + G * P * (D + 30))
+    rng = Rng.words(words)
+    eng = DEEngine(cfg, P, D)
+    prob = evb.ProblemInstance.base(kind, o, m, 0.0)
+    pop = torch.empty((P, D), dtype=torch.float64, device=dev)
+    eng.init_population(pop, -100.0, 100.0, rng)
+    fit = dev_eval(prob, pop, dev)
+    for _ in range(G):
+        eng.generation(prob, pop, fit, -100.0, 100.0, rng)
+    torch.cuda.synchronize()
+    assert np.array_equal(pop.cpu().numpy(), st["pop"])
+    if kind == 0:
+        assert np.array_equal(fit.cpu().numpy(), st["fit"])
+
+
+def test_philox_replay_rand1(dev):
+    # Philox sub-streams: the reference engine replays the exported words generation by
+    # generation (free-running, no re-sync) and must agree exactly
+    P, D, G, key = 64, 50, 20, 0x5EED
+    o, m = O.shift_rotation(11, D)
+    cfg = preset_de(0.5, 0.9)
+    prob = evb.ProblemInstance.base(evb.BaseKind.elliptic, o, m, 0.0)
+    eng = DEEngine(cfg, P, D)
+    rng = Rng.philox(key)
+    pop = torch.empty((P, D), dtype=torch.float64, device=dev)
+    eng.init_population(pop, -100.0, 100.0, rng)
+    fit = dev_eval(prob, pop, dev)
+    ref = O.RefDE(cfg, P, D)
+    ref.set_problem_base(1, o, m, 0.0)
+    ref.set_pop(pop.cpu().numpy(), fit.cpu().numpy())
+    for g in range(G):
+        eng.generation(prob, pop, fit, -100.0, 100.0, rng)
+        dr = eng.last_draws()
+        words = scripted_words_for_generation(key, dr["generation"], dr["word_counts"], dr["archive_words"],
+                                              philox=O.philox_words)
+        assert ref.generation(words, -100.0, 100.0), g
+        st = ref.get()
+        assert np.array_equal(pop.cpu().numpy(), st["pop"]), g
+        assert np.array_equal(fit.cpu().numpy(), st["fit"]), g
+
+
+def test_device_philox_matches_restatement():
+    from paper_2505_17430_b200.de import philox_words
+
+    for key, hi in ((0, 0), (0x0123456789ABCDEF, (7 << 32) | 3), (2**64 - 1, 2**64 - 1)):
+        assert np.array_equal(philox_words(key, hi, 5, 257), O.philox_words(key, hi, 5, 257))
+
+
+@pytest.mark.parametrize("G", [40])
+def test_config2_shade_lockstep(dev, G):
+    P, D, key = 180, 100, 11
+    o, m = O.shift_rotation(11, D)
+    cfg = preset_shade(0.11, P, 1.0)
+    prob = evb.ProblemInstance.base(evb.BaseKind.ackley, o, m, 0.0)
+    eng = DEEngine(cfg, P, D)
+    assert eng.archive_capacity == P and eng.p_count == 20
+    rng = Rng.philox(key)
+    pop = torch.empty((P, D), dtype=torch.float64, device=dev)
+    eng.init_population(pop, -100.0, 100.0, rng)
+    fit = dev_eval(prob, pop, dev)
+    ref = O.RefDE(cfg, P, D)
+    ref.set_problem_base(6, o, m, 0.0)
+    ref.set_pop(pop.cpu().numpy(), fit.cpu().numpy())
+    orc = O.OracleDE(cfg, P, D)
+    orc.set_problem_base(6, o, m, 0.0)
+    flagged = 0
+    exact_gens = 0
+    for g in range(G):
+        st0 = ref.get()
+        # lockstep: GPU state <- reference state
+        pop.copy_(torch.from_numpy(st0["pop"]))
+        fit.copy_(torch.from_numpy(st0["fit"]))
+        eng.set_state(st0["archive"], st0["memory_f"], st0["memory_cr"], st0["write_index"])
+        orc.set_state(st0["pop"], st0["fit"], st0["archive"], st0["archive_size"], st0["memory_f"],
+                      st0["memory_cr"], st0["write_index"])
+        eng.generation(prob, pop, fit, -100.0, 100.0, rng)
+        dr = eng.last_draws()
+        words = scripted_words_for_generation(key, dr["generation"], dr["word_counts"], dr["archive_words"],
+                                              philox=O.philox_words)
+        assert ref.generation(words, -100.0, 100.0), f"gen {g}: word count mismatch"
+        out = orc.generation(words, -100.0, 100.0)
+        st = ref.get()
+        # integer outputs: exact
+        assert np.array_equal(dr["idx"][:, :3], out["idx"][:, :3]), g
+        assert np.array_equal(dr["jrand"], out["jrand"]), g
+        assert np.array_equal(dr["word_counts"], out["words"]), g
+        # F / CR from libm-vs-CUDA transcendentals: ulp-level agreement, flagged when not exact
+        assert np.max(np.abs(dr["F"] - out["F"])) <= 4e-16
+        assert np.max(np.abs(dr["CR"] - out["CR"])) <= 4e-16
+        gpu_pop = pop.cpu().numpy()
+        same = np.all(gpu_pop == st["pop"], axis=1)
+        flagged += int((~same).sum())
+        if same.all():
+            exact_gens += 1
+            assert np.array_equal(eng.get_state()["archive"], st["archive"]), g
+        # rows that differ must come from an F/CR ulp difference
+        diff_rows = np.where(~same)[0]
+        for i in diff_rows:
+            assert dr["F"][i] != out["F"][i] or dr["CR"][i] != out["CR"][i], (g, i)
+        assert np.max(np.abs(gpu_pop - st["pop"])) <= 1e-9
+    assert exact_gens >= G // 2, (exact_gens, flagged)
+
+
+def test_large_population_properties(dev):
+    # HBM-sized update (P=16384, D=1000): structural properties of one Philox generation
+    P, D = 16384, 1000
+    o, m = O.shift_rotation(13, D)
+    prob = evb.ProblemInstance.base(evb.BaseKind.sphere, o, m, 0.0)
+    eng = DEEngine(preset_de(0.5, 0.9), P, D)
+    rng = Rng.philox(99)
+    pop = torch.empty((P, D), dtype=torch.float64, device=dev)
+    eng.init_population(pop, -100.0, 100.0, rng)
+    fit = dev_eval(prob, pop, dev)
+    f0 = fit.clone()
+    x0 = pop.clone()
+    eng.generation(prob, pop, fit, -100.0, 100.0, rng)
+    torch.cuda.synchronize()
+    assert bool((fit <= f0).all())
+    assert float(pop.min()) >= -100.0 and float(pop.max()) <= 100.0
+    dr = eng.last_draws()
+    idx = dr["idx"][:, :3]
+    assert np.all(idx[:, 0] != np.arange(P)) and np.all(idx[:, 1] != idx[:, 0]) and np.all(idx[:, 2] != idx[:, 1])
+    # sampled rows: replaced rows equal trial = target or donor gene by gene
+    x0n = x0.cpu().numpy()
+    popn = pop.cpu().numpy()
+    for i in range(0, P, 997):
+        a, b, c = idx[i]
+        donor = np.clip(x0n[a] + 0.5 * (x0n[b] - x0n[c]), -100, 100)
+        if not np.array_equal(popn[i], x0n[i]):
+            assert np.all((popn[i] == x0n[i]) | (popn[i] == donor)), i
