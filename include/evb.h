@@ -199,6 +199,35 @@ EVB_API int evb_de_set_state(evb_de e, const void* archive_host, int archive_siz
 EVB_API int evb_de_last_draws(evb_de e, int64_t* word_counts, int64_t* archive_words, uint32_t* generation,
                               void* F_host, void* CR_host, int* idx_host, int* jrand_host);
 
+/* ---- PSO engine (pso/engine.hpp:33-153, pso/topology.hpp, pso/update.hpp) ------------------ */
+
+enum evb_pso_topology { EVB_TOPO_GBEST = 0 /* "gbest" */, EVB_TOPO_LBEST_RING = 1 /* "lbest_ring" */ };
+enum evb_pso_update { EVB_UPD_STANDARD = 0 /* "standard" */ };
+
+typedef struct {
+  int topology, update;
+  double inertia, cognitive, social; /* swarm_params (pso/update.hpp:16-22) */
+  double vmax;                       /* > 0: clamp |v| <= vmax after the velocity rule (config 3) */
+} evb_pso_config;
+
+typedef struct evb_pso_s* evb_pso;
+
+EVB_API int evb_pso_create(int dtype, const evb_pso_config* cfg, int pop_size, int dim, evb_pso* out);
+EVB_API int evb_pso_destroy(evb_pso s);
+/* pso_engine::prepare, first call (pso/engine.hpp:40-50): personal bests <- population. */
+EVB_API int evb_pso_prepare(evb_pso s, const void* X, int64_t ldx, const void* fitness, void* stream);
+/* One SYNCHRONOUS generation: neighbourhood from start-of-generation pbests, velocity rule,
+ * optional clamp, move + bound rule, batched evaluation, strict-< pbest update.  The stock
+ * reference engine is asynchronous (pso/engine.hpp:52-82); see DESIGN.md. */
+EVB_API int evb_pso_generation(evb_pso s, evb_problem objective, evb_scratch sc, void* X, int64_t ldx,
+                               void* V, int64_t ldv, void* fitness, double lb, double ub, evb_rng rng,
+                               void* stream);
+/* A (pop_size x lda) <- U[lo, hi) from the rng (positions: init_population order; velocities). */
+EVB_API int evb_pso_init_uniform(evb_pso s, void* A, int64_t lda, double lo, double hi, evb_rng rng,
+                                 void* stream);
+EVB_API int evb_pso_get(evb_pso s, void* pbest_host, void* pbest_fit_host, int* nb_host, uint32_t* generation);
+EVB_API int evb_pso_set_pbest(evb_pso s, const void* pbest_host, const void* pbest_fit_host);
+
 /* Kernel launches this library has issued on the calling thread (monotonic counter; used by
  * bench.py to report gpu_launches inside its timed region). */
 EVB_API int evb_launch_count(void);

@@ -730,3 +730,66 @@ ORC_API int64_t orc_de_generation(const orc_de_cfg* c, orc_de_state* s, orc_rng*
 
 ORC_API int orc_de_cfg_size(void) { return (int)sizeof(orc_de_cfg); }
 ORC_API int orc_de_state_size(void) { return (int)sizeof(orc_de_state); }
+
+/* ------------------------------------------------------------------------------------------
+ * Synchronous PSO generation (config 3), restated from pso/topology.hpp:28-54,
+ * pso/update.hpp:66-74, pso/engine.hpp:66-79 plus the config's velocity clamp.
+ * ---------------------------------------------------------------------------------------- */
+#define DEFINE_PSO(T, SUF)                                                                              \
+  ORC_API void orc_pso_step_##SUF(int topology, double w_, double c1_, double c2_, double vmax_, int P, int D, \
+                                  int kind, const T* shift, const T* rot, T bias, T* x, T* v, T* fit, T* pb,   \
+                                  T* pbf, const uint64_t* words, int64_t n_words, T lb, T ub, int* nb_out) {   \
+    orc_rng r;                                                                                          \
+    orc_rng_scripted(&r, words, n_words);                                                               \
+    const T w = (T)w_, c1 = (T)c1_, c2 = (T)c2_, vmax = (T)vmax_;                                       \
+    int* nb = (int*)malloc(sizeof(int) * P);                                                            \
+    for (int i = 0; i < P; ++i) {                                                                       \
+      int best = -1;                                                                                    \
+      if (topology == 0) {                                                                              \
+        best = 0;                                                                                       \
+        for (int k = 1; k < P; ++k)                                                                     \
+          if (pbf[k] < pbf[best]) best = k;                                                             \
+      } else {                                                                                          \
+        for (int off = -1; off <= 1; ++off) {                                                           \
+          const int c = ((i + off) % P + P) % P;                                                        \
+          if (best < 0 || pbf[c] < pbf[best] || (pbf[c] == pbf[best] && c < best)) best = c;           \
+        }                                                                                               \
+      }                                                                                                 \
+      nb[i] = best;                                                                                     \
+      if (nb_out) nb_out[i] = best;                                                                     \
+    }                                                                                                   \
+    for (int i = 0; i < P; ++i) {                                                                       \
+      T* xi = x + (size_t)i * D;                                                                        \
+      T* vi = v + (size_t)i * D;                                                                        \
+      const T* p = pb + (size_t)i * D;                                                                  \
+      const T* l = pb + (size_t)nb[i] * D;                                                              \
+      for (int j = 0; j < D; ++j) {                                                                     \
+        const T r1 = (T)uniform01(&r);                                                                  \
+        const T r2 = (T)uniform01(&r);                                                                  \
+        vi[j] = w * vi[j] + c1 * r1 * (p[j] - xi[j]) + c2 * r2 * (l[j] - xi[j]);                        \
+      }                                                                                                 \
+      for (int j = 0; j < D; ++j) {                                                                     \
+        if (vmax > (T)0) {                                                                              \
+          if (vi[j] > vmax) vi[j] = vmax;                                                               \
+          if (vi[j] < -vmax) vi[j] = -vmax;                                                             \
+        }                                                                                               \
+        xi[j] += vi[j];                                                                                 \
+        if (xi[j] < lb) { xi[j] = lb; vi[j] = (T)(-0.5) * vi[j]; }                                      \
+        else if (xi[j] > ub) { xi[j] = ub; vi[j] = (T)(-0.5) * vi[j]; }                                 \
+      }                                                                                                 \
+    }                                                                                                   \
+    /* pbest snapshot semantics: all moves use the start-of-generation pbests (read above) */           \
+    T* diff = (T*)malloc(sizeof(T) * D);                                                                \
+    T* z = (T*)malloc(sizeof(T) * D);                                                                   \
+    for (int i = 0; i < P; ++i) {                                                                       \
+      transform_##SUF(x + (size_t)i * D, shift, rot, D, diff, z);                                      \
+      fit[i] = base_value_##SUF(kind, z, D) + bias;                                                     \
+      if (fit[i] < pbf[i]) {                                                                            \
+        memcpy(pb + (size_t)i * D, x + (size_t)i * D, sizeof(T) * D);                                   \
+        pbf[i] = fit[i];                                                                                \
+      }                                                                                                 \
+    }                                                                                                   \
+    free(diff); free(z); free(nb);                                                                      \
+  }
+DEFINE_PSO(double, f64)
+DEFINE_PSO(float, f32)

@@ -395,3 +395,66 @@ class OracleDE:
                                    ptr(out["win"]))
         out["archive_words"] = int(aw)
         return out
+
+
+# ---- PSO: synchronous driver over the reference pieces (REF) and the C restatement (C) ------------
+register_ref({
+    "ref_pso_create": (vp, [c_int, c_int, c_double, c_double, c_double, c_double, c_int, c_int, c_int, vp, vp,
+                            c_double]),
+    "ref_pso_set": (None, [c_int, vp, vp, vp, vp]),
+    "ref_pso_step": (c_int, [c_int, vp, vp, i64, c_double, c_double]),
+    "ref_pso_get": (None, [c_int, vp, vp, vp, vp, vp, vp]),
+    "ref_pso_destroy": (None, [c_int, vp]),
+})
+_PSO_C = {"orc_pso_step_f64": (None, [c_int, c_double, c_double, c_double, c_double, c_int, c_int, c_int, vp, vp,
+                                      c_double, vp, vp, vp, vp, vp, vp, i64, c_double, c_double, vp]),
+          "orc_pso_step_f32": (None, [c_int, c_double, c_double, c_double, c_double, c_int, c_int, c_int, vp, vp,
+                                      c_float, vp, vp, vp, vp, vp, vp, i64, c_float, c_float, vp])}
+register_c(_PSO_C)
+
+
+class RefPSO:
+    def __init__(self, dtype_np, topology, w, c1, c2, vmax, P, D, kind, shift, rot, bias=0.0):
+        self.nd = dtype_np
+        self.dt = 1 if dtype_np == np.float64 else 0
+        self.P, self.D = P, D
+        self._o = np.ascontiguousarray(shift, dtype_np)
+        self._m = np.ascontiguousarray(rot, dtype_np).ravel()
+        self.h = REF().ref_pso_create(self.dt, topology, w, c1, c2, vmax, P, D, kind, ptr(self._o), ptr(self._m), bias)
+
+    def set(self, x, v, fit):
+        x, v, f = (np.ascontiguousarray(a, self.nd) for a in (x, v, fit))
+        REF().ref_pso_set(self.dt, self.h, ptr(x), ptr(v), ptr(f))
+
+    def step(self, words, lb, ub) -> bool:
+        w = np.ascontiguousarray(words, np.uint64)
+        return bool(REF().ref_pso_step(self.dt, self.h, ptr(w), len(w), lb, ub))
+
+    def get(self):
+        P, D = self.P, self.D
+        out = {k: np.zeros((P, D), self.nd) for k in ("x", "v", "pbest")}
+        out["fit"] = np.zeros(P, self.nd)
+        out["pbest_fit"] = np.zeros(P, self.nd)
+        REF().ref_pso_get(self.dt, self.h, ptr(out["x"]), ptr(out["v"]), ptr(out["fit"]), ptr(out["pbest"]),
+                          ptr(out["pbest_fit"]))
+        return out
+
+    def __del__(self):
+        try:
+            REF().ref_pso_destroy(self.dt, self.h)
+        except Exception:
+            pass
+
+
+def pso_step_c(topology, w, c1, c2, vmax, kind, shift, rot, bias, x, v, fit, pb, pbf, words, lb, ub):
+    """C restatement, in place on numpy arrays; returns the neighbour index of every particle."""
+    nd = x.dtype
+    P, D = x.shape
+    o = np.ascontiguousarray(shift, nd)
+    m = np.ascontiguousarray(rot, nd).ravel()
+    w_ = np.ascontiguousarray(words, np.uint64)
+    nb = np.zeros(P, np.int32)
+    fn = C().orc_pso_step_f64 if nd == np.float64 else C().orc_pso_step_f32
+    fn(topology, w, c1, c2, vmax, P, D, kind, ptr(o), ptr(m), bias, ptr(x), ptr(v), ptr(fit), ptr(pb), ptr(pbf),
+       ptr(w_), len(w_), lb, ub, ptr(nb))
+    return nb

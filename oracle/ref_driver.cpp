@@ -351,3 +351,132 @@ REF_API void ref_de_native_run(void* h, uint64_t seed, uint64_t stream, int gene
   evolution_state st(1LL << 40, r->P, r->D, std::min(4, r->P));
   for (int g = 0; g < generations; ++g) r->engine->generation(r->pop, st, objective, lb, ub, rng);
 }
+
+// ---- synchronous PSO driver built from the reference's own pieces --------
+// gbest_topology / lbest_topology::neighbor_best on the start-of-generation pbests,
+// standard_update::apply (pso/update.hpp:66-74) followed by the config's velocity clamp, the move
+// and bound rule of pso/engine.hpp:66-75, problem_instance::evaluate, strict-< pbest
+// (pso/engine.hpp:78-79).  The stock pso_engine is asynchronous; this driver is the synchronous
+// variant BASELINE config 3 specifies.
+namespace {
+template <typename T>
+struct ref_pso_run {
+  std::unique_ptr<pso::topology_strategy<T>> topo;
+  pso::standard_update<T> upd;
+  pso::swarm_params<T> params;
+  T vmax;
+  std::unique_ptr<problem_instance<T>> problem;
+  std::vector<std::vector<T>> x, v;
+  std::vector<individual<T>> pb;
+  std::vector<T> fit;
+  int P, D;
+
+  int step(const uint64_t* words, int64_t n, T lb, T ub) {
+    const uint64_t sentinel = 0x0badc0ffee0ddf00ULL;
+    std::vector<uint64_t> w(words, words + n);
+    w.push_back(sentinel);
+    rng_stream rng = rng_stream::scripted(w);
+    std::vector<int> nb(static_cast<size_t>(P));
+    for (int i = 0; i < P; ++i) nb[size_t(i)] = topo->neighbor_best(pb, i);
+    const auto snapshot = pb;  // start-of-generation personal bests (synchronous)
+    for (int i = 0; i < P; ++i) {
+      auto& xi = x[size_t(i)];
+      auto& vi = v[size_t(i)];
+      upd.apply(xi, vi, snapshot[size_t(i)].genome, snapshot[size_t(nb[size_t(i)])].genome, nb[size_t(i)] == i,
+                params, rng);
+      for (int j = 0; j < D; ++j) {
+        if (vmax > T(0)) {
+          if (vi[size_t(j)] > vmax) vi[size_t(j)] = vmax;
+          if (vi[size_t(j)] < -vmax) vi[size_t(j)] = -vmax;
+        }
+        xi[size_t(j)] += vi[size_t(j)];  // pso/engine.hpp:66-75
+        if (xi[size_t(j)] < lb) {
+          xi[size_t(j)] = lb;
+          vi[size_t(j)] = T(-0.5) * vi[size_t(j)];
+        } else if (xi[size_t(j)] > ub) {
+          xi[size_t(j)] = ub;
+          vi[size_t(j)] = T(-0.5) * vi[size_t(j)];
+        }
+      }
+    }
+    eval_scratch<T> scratch;
+    for (int i = 0; i < P; ++i) {
+      fit[size_t(i)] = problem->evaluate(x[size_t(i)], scratch);
+      if (fit[size_t(i)] < pb[size_t(i)].fitness) {
+        pb[size_t(i)].genome = x[size_t(i)];
+        pb[size_t(i)].fitness = fit[size_t(i)];
+      }
+    }
+    return rng.next_u64() == sentinel ? 1 : 0;
+  }
+};
+
+template <typename T>
+void* pso_create(int topology, double w, double c1, double c2, double vmax, int P, int D, int kind, const void* shift,
+                 const void* rot, double bias) {
+  auto* r = new ref_pso_run<T>();
+  if (topology == 0) r->topo = std::make_unique<pso::gbest_topology<T>>();
+  else r->topo = std::make_unique<pso::lbest_topology<T>>();
+  r->params.inertia = T(w);
+  r->params.cognitive = T(c1);
+  r->params.social = T(c2);
+  r->vmax = T(vmax);
+  r->P = P;
+  r->D = D;
+  r->problem = std::make_unique<problem_instance<T>>(
+      make_base<T>(kind, D, static_cast<const T*>(shift), static_cast<const T*>(rot), bias));
+  return r;
+}
+
+template <typename T>
+void pso_set(void* h, const void* x, const void* v, const void* fit) {
+  auto* r = static_cast<ref_pso_run<T>*>(h);
+  const T* X = static_cast<const T*>(x);
+  const T* V = static_cast<const T*>(v);
+  const T* F = static_cast<const T*>(fit);
+  r->x.assign(size_t(r->P), std::vector<T>(size_t(r->D)));
+  r->v.assign(size_t(r->P), std::vector<T>(size_t(r->D)));
+  r->pb.assign(size_t(r->P), individual<T>(r->D));
+  r->fit.assign(size_t(r->P), T(0));
+  for (int i = 0; i < r->P; ++i) {
+    std::memcpy(r->x[size_t(i)].data(), X + size_t(i) * r->D, sizeof(T) * r->D);
+    std::memcpy(r->v[size_t(i)].data(), V + size_t(i) * r->D, sizeof(T) * r->D);
+    r->fit[size_t(i)] = F[i];
+    r->pb[size_t(i)].genome = r->x[size_t(i)];  // prepare(), first call (pso/engine.hpp:40-45)
+    r->pb[size_t(i)].fitness = F[i];
+    r->pb[size_t(i)].evaluated = true;
+  }
+}
+
+template <typename T>
+void pso_get(void* h, void* x, void* v, void* fit, void* pb, void* pbf) {
+  auto* r = static_cast<ref_pso_run<T>*>(h);
+  for (int i = 0; i < r->P; ++i) {
+    if (x) std::memcpy(static_cast<T*>(x) + size_t(i) * r->D, r->x[size_t(i)].data(), sizeof(T) * r->D);
+    if (v) std::memcpy(static_cast<T*>(v) + size_t(i) * r->D, r->v[size_t(i)].data(), sizeof(T) * r->D);
+    if (pb) std::memcpy(static_cast<T*>(pb) + size_t(i) * r->D, r->pb[size_t(i)].genome.data(), sizeof(T) * r->D);
+    if (fit) static_cast<T*>(fit)[i] = r->fit[size_t(i)];
+    if (pbf) static_cast<T*>(pbf)[i] = r->pb[size_t(i)].fitness;
+  }
+}
+}  // namespace
+
+REF_API void* ref_pso_create(int dtype, int topology, double w, double c1, double c2, double vmax, int P, int D,
+                             int kind, const void* shift, const void* rot, double bias) {
+  return dtype == 1 ? pso_create<double>(topology, w, c1, c2, vmax, P, D, kind, shift, rot, bias)
+                    : pso_create<float>(topology, w, c1, c2, vmax, P, D, kind, shift, rot, bias);
+}
+REF_API void ref_pso_set(int dtype, void* h, const void* x, const void* v, const void* fit) {
+  dtype == 1 ? pso_set<double>(h, x, v, fit) : pso_set<float>(h, x, v, fit);
+}
+REF_API int ref_pso_step(int dtype, void* h, const uint64_t* words, int64_t n, double lb, double ub) {
+  return dtype == 1 ? static_cast<ref_pso_run<double>*>(h)->step(words, n, lb, ub)
+                    : static_cast<ref_pso_run<float>*>(h)->step(words, n, float(lb), float(ub));
+}
+REF_API void ref_pso_get(int dtype, void* h, void* x, void* v, void* fit, void* pb, void* pbf) {
+  dtype == 1 ? pso_get<double>(h, x, v, fit, pb, pbf) : pso_get<float>(h, x, v, fit, pb, pbf);
+}
+REF_API void ref_pso_destroy(int dtype, void* h) {
+  if (dtype == 1) delete static_cast<ref_pso_run<double>*>(h);
+  else delete static_cast<ref_pso_run<float>*>(h);
+}

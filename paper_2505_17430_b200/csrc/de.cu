@@ -47,16 +47,6 @@ struct de_conf {
 
 }  // namespace evb
 
-struct evb_rng_s {
-  int mode = evb::RNG_PHILOX;
-  uint64_t key = 0;
-  uint64_t* d_words = nullptr;
-  int64_t n_words = 0;
-  int64_t* d_cursor = nullptr;  // WORDS: next unread word (device-resident)
-  uint32_t gen = 0;             // PHILOX: generation counter (host)
-  int* d_overflow = nullptr;
-};
-
 struct evb_de_s {
   int dtype = EVB_F64;
   int P = 0, D = 0;

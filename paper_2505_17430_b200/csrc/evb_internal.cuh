@@ -110,6 +110,17 @@ struct evb_problem_s {
   evb::device_problem p;
 };
 
+// device word source (rng.cuh): PHILOX (mode 0) or WORDS (mode 1)
+struct evb_rng_s {
+  int mode = 0;
+  uint64_t key = 0;
+  uint64_t* d_words = nullptr;
+  int64_t n_words = 0;
+  int64_t* d_cursor = nullptr;  // WORDS: next unread word (device-resident)
+  uint32_t gen = 0;             // PHILOX: generation counter (host)
+  int* d_overflow = nullptr;
+};
+
 struct evb_scratch_s {
   cudaStream_t own_stream = nullptr;
   // large-D fused path: per (channel, n-tile, point) partial sums + per m-block counters

@@ -1,0 +1,407 @@
+// pso.cu — synchronous PSO generation on the device (K7): neighbourhood argmin, velocity / position
+// update with bound handling, batched evaluation (K1/K2) and strict-< personal-best update.
+//
+// Reference pieces (pso/): gbest_topology::neighbor_best pso/topology.hpp:28-34 (strict <, ties to
+// the lowest index), lbest_topology::neighbor_best :44-54 (ring {i-1, i, i+1}, ties to the lowest
+// index), standard_update::apply pso/update.hpp:66-74 (r1, r2 drawn per gene, interleaved), move
+// and bound rule pso/engine.hpp:66-75, pbest update :78-79.
+//
+// Deviation: the stock pso_engine is asynchronous — particle i sees pbests already
+// updated by particles < i in the same generation.  A data-parallel GPU generation is
+// synchronous: every particle reads the start-of-generation pbests.  BASELINE config 3 asks for
+// this synchronous variant with a velocity clamp (|v| <= vmax, applied after the velocity rule,
+// before the move); the CPU oracle is the synchronous driver built from the same reference pieces.
+//
+// Draws: particle i of generation g uses Philox sub-stream (g << 32) | i; gene j takes words 2j
+// (r1) and 2j+1 (r2) — exactly one Philox block per gene.  WORDS mode consumes the list
+// particle-major, gene-minor, r1 before r2 (the reference's per-particle order).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "evb_internal.cuh"
+#include "evb_math.cuh"
+#include "rng.cuh"
+
+struct evb_pso_s {
+  int dtype = EVB_F64;
+  int P = 0, D = 0;
+  int topology = EVB_TOPO_GBEST;
+  int update = EVB_UPD_STANDARD;
+  double w = 0, c1 = 0, c2 = 0, vmax = 0;
+  int64_t ldb = 0;
+  void* pbest = nullptr;      // P x ldb
+  void* pbest_fit = nullptr;  // P
+  void* fit_new = nullptr;    // P (evaluation of the moved swarm)
+  int* nb = nullptr;          // P
+  int prepared = 0;
+  uint32_t last_gen = 0;
+  evb_scratch_s* eval_scratch = nullptr;
+};
+
+namespace evb {
+namespace {
+
+// (fitness, index) lexicographic minimum — strict <, ties to the lower index
+template <typename T>
+__device__ __forceinline__ void argmin_merge(T& f, int& i, T f2, int i2) {
+  if (f2 < f || (!(f < f2) && !(f2 < f) && i2 < i) || (i < 0 && i2 >= 0)) {
+    f = f2;
+    i = i2;
+  }
+}
+
+// gbest: one block reduces all pbests (pso/topology.hpp:28-34 semantics: index of the first
+// strict minimum == lexicographic (f, i) minimum); writes nb[i] = best for all i.
+template <typename T>
+__global__ void pso_gbest_kernel(const T* __restrict__ pf, int P, int* nb) {
+  __shared__ T sf[32];
+  __shared__ int si[32];
+  T bf = T(0);
+  int bi = -1;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) argmin_merge(bf, bi, pf[i], i);
+  for (int off = 16; off > 0; off >>= 1) {
+    const T of = __shfl_xor_sync(0xffffffffu, bf, off);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+    if (oi >= 0) argmin_merge(bf, bi, of, oi);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+    sf[w] = bf;
+    si[w] = bi;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    bf = l < nw ? sf[l] : T(0);
+    bi = l < nw ? si[l] : -1;
+    for (int off = 16; off > 0; off >>= 1) {
+      const T of = __shfl_xor_sync(0xffffffffu, bf, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (oi >= 0) argmin_merge(bf, bi, of, oi);
+    }
+    if (l == 0) si[0] = bi;
+  }
+  __syncthreads();
+  const int best = si[0];
+  for (int i = threadIdx.x; i < P; i += blockDim.x) nb[i] = best;
+}
+
+// ring of width one (pso/topology.hpp:44-54), offsets -1, 0, +1 in that order
+template <typename T>
+__global__ void pso_ring_kernel(const T* __restrict__ pf, int P, int* nb) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  int best = -1;
+  for (int off = -1; off <= 1; ++off) {
+    const int c = ((i + off) % P + P) % P;
+    if (best < 0 || pf[c] < pf[best] || (pf[c] == pf[best] && c < best)) best = c;
+  }
+  nb[i] = best;
+}
+
+template <typename T>
+struct pso_dev {
+  int P, D;
+  T* x;
+  int64_t ldx;
+  T* v;
+  int64_t ldv;
+  const T* pb;
+  int64_t ldb;
+  const int* nb;
+  T w, c1, c2, vmax;
+  int clamp;
+  T lb, ub;
+  word_source src;
+  uint32_t gen;
+  int64_t base;  // WORDS: list position of this generation's first word
+  int* overflow;
+};
+
+// K7 update: grid (gene blocks, particles); one Philox block per gene gives (r1, r2).
+// v = w v + c1 r1 (p - x) + c2 r2 (l - x)  evaluated left to right (pso/update.hpp:71-72),
+// clamp, move, bound rule (pso/engine.hpp:66-75).  Pure streaming: 5 s P D bytes.
+template <typename T>
+__global__ void __launch_bounds__(256) pso_update_kernel(const pso_dev<T> d) {
+  using F = fop<T>;
+  const int i = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= d.D) return;
+  uint64_t w0, w1;
+  if (d.src.mode == RNG_PHILOX) {
+    philox_pair(d.src.key, (uint64_t(d.gen) << 32) | uint32_t(i), uint64_t(j), w0, w1);
+  } else {
+    const int64_t n = d.base + (int64_t(i) * d.D + j) * 2;
+    w0 = word_at(d.src, 0, n, d.overflow);
+    w1 = word_at(d.src, 0, n + 1, d.overflow);
+  }
+  const T r1 = T(u01_of(w0)), r2 = T(u01_of(w1));
+  T* xr = d.x + size_t(i) * d.ldx;
+  T* vr = d.v + size_t(i) * d.ldv;
+  const T x = xr[j];
+  const T p = d.pb[size_t(i) * d.ldb + j];
+  const T l = d.pb[size_t(d.nb[i]) * d.ldb + j];
+  T v = F::add(F::add(F::mul(d.w, vr[j]), F::mul(F::mul(d.c1, r1), F::sub(p, x))),
+               F::mul(F::mul(d.c2, r2), F::sub(l, x)));
+  if (d.clamp) {
+    if (v > d.vmax) v = d.vmax;
+    if (v < -d.vmax) v = -d.vmax;
+  }
+  T xn = F::add(x, v);
+  if (xn < d.lb) {
+    xn = d.lb;
+    v = F::mul(T(-0.5), v);
+  } else if (xn > d.ub) {
+    xn = d.ub;
+    v = F::mul(T(-0.5), v);
+  }
+  xr[j] = xn;
+  vr[j] = v;
+}
+
+// pbest update (pso/engine.hpp:78-79): strict <, copy the moved particle; also publishes the
+// particle's fitness into the caller's fitness vector.
+template <typename T>
+__global__ void pso_pbest_kernel(const T* __restrict__ x, int64_t ldx, const T* __restrict__ fnew, T* fit, T* pb,
+                                 int64_t ldb, T* pbf, int D) {
+  const int i = blockIdx.x;
+  const T f = fnew[i];
+  if (threadIdx.x == 0) fit[i] = f;
+  if (!(f < pbf[i])) return;
+  for (int j = threadIdx.x; j < D; j += blockDim.x) pb[size_t(i) * ldb + j] = x[size_t(i) * ldx + j];
+  __syncthreads();
+  if (threadIdx.x == 0) pbf[i] = f;
+}
+
+template <typename T>
+__global__ void copy_rows_kernel(const T* src, int64_t lds, T* dst, int64_t ldd, int D) {
+  const int i = blockIdx.x;
+  for (int j = threadIdx.x; j < D; j += blockDim.x) dst[size_t(i) * ldd + j] = src[size_t(i) * lds + j];
+}
+
+// velocities ~ U[lo, hi]: gene-positional words (sub-stream kSubInit + 1 of the current generation)
+template <typename T>
+__global__ void init_uniform_kernel(T* a, int64_t lda, int P, int D, double lo, double hi, word_source src,
+                                    uint64_t ctr_hi, int64_t base, int* overflow) {
+  const int64_t n = int64_t(P) * D;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t w = word_at(src, ctr_hi, base + e, overflow);
+    a[(e / D) * lda + (e % D)] = T(__dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), u01_of(w))));
+  }
+}
+
+}  // namespace
+int64_t words_cursor(evb_rng_s* r, cudaStream_t st);
+void words_advance(evb_rng_s* r, int64_t to, cudaStream_t st);
+namespace {
+
+template <typename T>
+void generation_t(evb_pso_s* s, const device_problem* prob, evb_scratch_s* sc, void* X, int64_t ldx, void* V,
+                  int64_t ldv, void* fit, double lb, double ub, evb_rng_s* r, cudaStream_t st) {
+  const T* pf = static_cast<const T*>(s->pbest_fit);
+  if (s->topology == EVB_TOPO_GBEST) pso_gbest_kernel<T><<<1, 1024, 0, st>>>(pf, s->P, s->nb);
+  else pso_ring_kernel<T><<<(s->P + 255) / 256, 256, 0, st>>>(pf, s->P, s->nb);
+  count_launch();
+  pso_dev<T> d{};
+  d.P = s->P;
+  d.D = s->D;
+  d.x = static_cast<T*>(X);
+  d.ldx = ldx;
+  d.v = static_cast<T*>(V);
+  d.ldv = ldv;
+  d.pb = static_cast<const T*>(s->pbest);
+  d.ldb = s->ldb;
+  d.nb = s->nb;
+  d.w = T(s->w);
+  d.c1 = T(s->c1);
+  d.c2 = T(s->c2);
+  d.vmax = T(s->vmax);
+  d.clamp = s->vmax > 0 ? 1 : 0;
+  d.lb = T(lb);
+  d.ub = T(ub);
+  d.src = word_source{r->mode, r->key, r->d_words, r->n_words};
+  d.gen = r->gen;
+  d.overflow = r->d_overflow;
+  if (r->mode == RNG_WORDS) d.base = words_cursor(r, st);
+  dim3 grid((s->D + 255) / 256, s->P);
+  pso_update_kernel<T><<<grid, 256, 0, st>>>(d);
+  count_launch();
+  EVB_CUDA(cudaGetLastError());
+  if (r->mode == RNG_WORDS) words_advance(r, d.base + int64_t(s->P) * s->D * 2, st);
+  eval_request rq{};
+  rq.prob = prob;
+  rq.scratch = sc;
+  rq.X = X;
+  rq.n = s->P;
+  rq.ldx = ldx;
+  rq.out = s->fit_new;
+  rq.ldo = s->P;
+  rq.n_out = 1;
+  rq.kinds[0] = prob->kind;
+  rq.biases[0] = prob->bias;
+  rq.stream = st;
+  rq.scalar_trig = true;
+  eval_dispatch(rq);
+  pso_pbest_kernel<T><<<s->P, std::min(256, int(round_up(s->D, 32))), 0, st>>>(
+      static_cast<const T*>(X), ldx, static_cast<const T*>(s->fit_new), static_cast<T*>(fit),
+      static_cast<T*>(s->pbest), s->ldb, static_cast<T*>(s->pbest_fit), s->D);
+  count_launch();
+  EVB_CUDA(cudaGetLastError());
+  s->last_gen = r->gen;
+  r->gen++;
+}
+
+}  // namespace
+
+int64_t words_cursor(evb_rng_s* r, cudaStream_t st) {
+  int64_t c = 0;
+  EVB_CUDA(cudaMemcpyAsync(&c, r->d_cursor, sizeof(c), cudaMemcpyDeviceToHost, st));
+  EVB_CUDA(cudaStreamSynchronize(st));
+  return c;
+}
+void words_advance(evb_rng_s* r, int64_t to, cudaStream_t st) {
+  EVB_CUDA(cudaMemcpyAsync(r->d_cursor, &to, sizeof(to), cudaMemcpyHostToDevice, st));
+  EVB_CUDA(cudaStreamSynchronize(st));
+  if (to > r->n_words) {
+    int one = 1;
+    EVB_CUDA(cudaMemcpy(r->d_overflow, &one, sizeof(int), cudaMemcpyHostToDevice));
+  }
+}
+
+}  // namespace evb
+
+using namespace evb;
+
+extern "C" {
+
+int evb_pso_create(int dtype, const evb_pso_config* c, int pop_size, int dim, evb_pso* out) {
+  return guarded([&] {
+    require(dtype == EVB_F32 || dtype == EVB_F64, "pso: dtype must be EVB_F32 or EVB_F64");
+    require(c != nullptr && out != nullptr, "pso: null config or output handle");
+    require(c->topology == EVB_TOPO_GBEST || c->topology == EVB_TOPO_LBEST_RING,
+            "pso builder: unknown topology strategy (GPU kernels: gbest, lbest_ring)");
+    require(c->update == EVB_UPD_STANDARD, "pso builder: unknown update strategy (GPU kernels: standard)");
+    require(pop_size >= 1 && dim >= 1, "pso: pop_size and dim must be positive");
+    auto* s = new evb_pso_s();
+    try {
+      s->dtype = dtype;
+      s->P = pop_size;
+      s->D = dim;
+      s->topology = c->topology;
+      s->update = c->update;
+      s->w = c->inertia;
+      s->c1 = c->cognitive;
+      s->c2 = c->social;
+      s->vmax = c->vmax;
+      const size_t es = dtype == EVB_F64 ? 8 : 4;
+      s->ldb = round_up(dim, 16 / int64_t(es));
+      EVB_CUDA(cudaMalloc(&s->pbest, es * s->ldb * pop_size));
+      EVB_CUDA(cudaMalloc(&s->pbest_fit, es * pop_size));
+      EVB_CUDA(cudaMalloc(&s->fit_new, es * pop_size));
+      EVB_CUDA(cudaMalloc(&s->nb, sizeof(int) * pop_size));
+      require(evb_scratch_create(&s->eval_scratch) == EVB_OK, "pso: scratch allocation failed");
+    } catch (...) {
+      void* ptrs[] = {s->pbest, s->pbest_fit, s->fit_new, s->nb};
+      for (void* p : ptrs)
+        if (p) cudaFree(p);
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
+int evb_pso_destroy(evb_pso s) {
+  return guarded([&] {
+    if (!s) return;
+    void* ptrs[] = {s->pbest, s->pbest_fit, s->fit_new, s->nb};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    if (s->eval_scratch) evb_scratch_destroy(s->eval_scratch);
+    delete s;
+  });
+}
+
+// pso_engine::prepare first call (pso/engine.hpp:40-50): pbests <- population
+int evb_pso_prepare(evb_pso s, const void* X, int64_t ldx, const void* fitness, void* stream) {
+  return guarded([&] {
+    require(s && X && fitness, "pso_prepare: null argument");
+    if (ldx < s->D) throw invalid_argument("pso_prepare: ldx < dim");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t es = s->dtype == EVB_F64 ? 8 : 4;
+    if (s->dtype == EVB_F64)
+      copy_rows_kernel<double><<<s->P, 128, 0, st>>>(static_cast<const double*>(X), ldx,
+                                                     static_cast<double*>(s->pbest), s->ldb, s->D);
+    else
+      copy_rows_kernel<float><<<s->P, 128, 0, st>>>(static_cast<const float*>(X), ldx, static_cast<float*>(s->pbest),
+                                                    s->ldb, s->D);
+    count_launch();
+    EVB_CUDA(cudaMemcpyAsync(s->pbest_fit, fitness, es * s->P, cudaMemcpyDeviceToDevice, st));
+    s->prepared = 1;
+  });
+}
+
+int evb_pso_generation(evb_pso s, evb_problem objective, evb_scratch sc, void* X, int64_t ldx, void* V, int64_t ldv,
+                       void* fitness, double lb, double ub, evb_rng rng, void* stream) {
+  return guarded([&] {
+    require(s && objective && X && V && fitness && rng, "pso_generation: null argument");
+    require(s->prepared, "pso_generation: prepare() must run first (pso/engine.hpp:40-50)");
+    if (objective->p.dim != s->D) throw invalid_argument("pso_generation: problem dimension mismatch");
+    if (objective->p.dtype != s->dtype) throw config_error("pso_generation: problem dtype differs from engine");
+    if (ldx < s->D || ldv < s->D) throw invalid_argument("pso_generation: leading dimension < dim");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    evb_scratch_s* scr = sc ? sc : s->eval_scratch;
+    if (s->dtype == EVB_F64) generation_t<double>(s, &objective->p, scr, X, ldx, V, ldv, fitness, lb, ub, rng, st);
+    else generation_t<float>(s, &objective->p, scr, X, ldx, V, ldv, fitness, lb, ub, rng, st);
+  });
+}
+
+int evb_pso_init_uniform(evb_pso s, void* A, int64_t lda, double lo, double hi, evb_rng r, void* stream) {
+  return guarded([&] {
+    require(s && A && r, "pso_init_uniform: null argument");
+    require(lo < hi, "pso_init_uniform: lo must be less than hi");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    word_source src{r->mode, r->key, r->d_words, r->n_words};
+    int64_t base = r->mode == RNG_WORDS ? words_cursor(r, st) : 0;
+    const uint64_t ctr_hi = (uint64_t(r->gen) << 32) | kSubInit;
+    const int blocks = int(std::min<int64_t>(4096, (int64_t(s->P) * s->D + 255) / 256));
+    if (s->dtype == EVB_F64)
+      init_uniform_kernel<double><<<blocks, 256, 0, st>>>(static_cast<double*>(A), lda, s->P, s->D, lo, hi, src,
+                                                          ctr_hi, base, r->d_overflow);
+    else
+      init_uniform_kernel<float><<<blocks, 256, 0, st>>>(static_cast<float*>(A), lda, s->P, s->D, lo, hi, src, ctr_hi,
+                                                         base, r->d_overflow);
+    count_launch();
+    EVB_CUDA(cudaGetLastError());
+    if (r->mode == RNG_WORDS) words_advance(r, base + int64_t(s->P) * s->D, st);
+    else r->gen++;
+  });
+}
+
+int evb_pso_get(evb_pso s, void* pbest_host, void* pbest_fit_host, int* nb_host, uint32_t* generation) {
+  return guarded([&] {
+    require(s != nullptr, "pso: null handle");
+    EVB_CUDA(cudaDeviceSynchronize());
+    const size_t es = s->dtype == EVB_F64 ? 8 : 4;
+    if (pbest_host)
+      EVB_CUDA(cudaMemcpy2D(pbest_host, s->D * es, s->pbest, s->ldb * es, s->D * es, s->P, cudaMemcpyDeviceToHost));
+    if (pbest_fit_host) EVB_CUDA(cudaMemcpy(pbest_fit_host, s->pbest_fit, es * s->P, cudaMemcpyDeviceToHost));
+    if (nb_host) EVB_CUDA(cudaMemcpy(nb_host, s->nb, sizeof(int) * s->P, cudaMemcpyDeviceToHost));
+    if (generation) *generation = s->last_gen;
+  });
+}
+
+int evb_pso_set_pbest(evb_pso s, const void* pbest_host, const void* pbest_fit_host) {
+  return guarded([&] {
+    require(s && pbest_host && pbest_fit_host, "pso_set_pbest: null argument");
+    const size_t es = s->dtype == EVB_F64 ? 8 : 4;
+    EVB_CUDA(cudaDeviceSynchronize());
+    EVB_CUDA(cudaMemcpy2D(s->pbest, s->ldb * es, pbest_host, s->D * es, s->D * es, s->P, cudaMemcpyHostToDevice));
+    EVB_CUDA(cudaMemcpy(s->pbest_fit, pbest_fit_host, es * s->P, cudaMemcpyHostToDevice));
+    s->prepared = 1;
+  });
+}
+
+}  // extern "C"
