@@ -199,6 +199,18 @@ EVB_API int evb_de_set_state(evb_de e, const void* archive_host, int archive_siz
 EVB_API int evb_de_last_draws(evb_de e, int64_t* word_counts, int64_t* archive_words, uint32_t* generation,
                               void* F_host, void* CR_host, int* idx_host, int* jrand_host);
 
+/* K8: n_runs independent DE runs in ONE persistent launch (one CTA per run, every generation
+ * inside the kernel; experiment/runner.hpp:101-160 evo_bench over a suite).  Run r evaluates
+ * problems[r] (base or composition, fp64) and draws from Philox key keys[r]; pops / fits are
+ * device arrays (n_runs x pop_size x dim, n_runs x pop_size).  init != 0: draw and evaluate the
+ * initial populations first (generation id gen0), then run `generations` generations (ids
+ * gen0+1 ...); otherwise continue from the given populations (ids gen0 ...).  Supports the `de`
+ * preset family: rand_1 / best_1, binomial, clip / midpoint_target, fixed F, CR, no archive;
+ * the run state must fit in shared memory (else use evb_de_generation per run). */
+EVB_API int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int pop_size, int dim,
+                        const evb_problem* problems, const uint64_t* keys, int generations, double lb,
+                        double ub, void* pops, void* fits, int init, uint32_t gen0, void* stream);
+
 /* ---- PSO engine (pso/engine.hpp:33-153, pso/topology.hpp, pso/update.hpp) ------------------ */
 
 enum evb_pso_topology { EVB_TOPO_GBEST = 0 /* "gbest" */, EVB_TOPO_LBEST_RING = 1 /* "lbest_ring" */ };

@@ -793,3 +793,40 @@ ORC_API int orc_de_state_size(void) { return (int)sizeof(orc_de_state); }
   }
 DEFINE_PSO(double, f64)
 DEFINE_PSO(float, f32)
+
+/* The sequential word list one rand/1 (mutation 0) or best/1 (mutation 1) + binomial generation
+ * consumes when individual i draws from Philox sub-stream (gen << 32) | i: the rejection loops
+ * of de/strategy.hpp:84-86 / 109-110 decide how many index words precede jrand and the D gene
+ * uniforms.  Fitness-independent, so the oracle can rebuild it.  Returns the word count. */
+ORC_API int64_t orc_de_fixed_generation_words(int mutation, uint64_t key, uint32_t gen, int P, int D, uint64_t* out,
+                                              int64_t cap) {
+  int64_t n = 0;
+  for (int i = 0; i < P; ++i) {
+    const uint64_t hi = ((uint64_t)gen << 32) | (uint32_t)i;
+    uint64_t pos = 0;
+    int a = -1, b, c;
+    if (mutation == 0) {
+      do { a = orc_uniform_int_word(orc_philox_word(key, hi, pos++), P); } while (a == i);
+    }
+    do { b = orc_uniform_int_word(orc_philox_word(key, hi, pos++), P); } while (b == i || (mutation == 0 && b == a));
+    do { c = orc_uniform_int_word(orc_philox_word(key, hi, pos++), P); } while (c == i || c == b || (mutation == 0 && c == a));
+    pos += 1 + (uint64_t)D; /* jrand + gene uniforms */
+    for (uint64_t q = 0; q < pos; ++q) {
+      if (n < cap) out[n] = orc_philox_word(key, hi, q);
+      ++n;
+    }
+  }
+  return n;
+}
+
+/* A composition instance's components drawn like make_instance does for compositions
+ * (problems/suite.hpp:134-143): one stream, per component draw_shift then draw_rotation. */
+ORC_API void orc_make_composition(uint64_t seed, uint64_t stream_id, int dim, int n_comp, double* shifts,
+                                  double* rots) {
+  orc_rng r;
+  orc_rng_init(&r, seed, stream_id);
+  for (int c = 0; c < n_comp; ++c) {
+    orc_draw_shift(&r, dim, -100.0, 100.0, shifts + (size_t)c * dim);
+    orc_random_rotation(&r, dim, rots + (size_t)c * dim * dim);
+  }
+}

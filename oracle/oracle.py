@@ -458,3 +458,31 @@ def pso_step_c(topology, w, c1, c2, vmax, kind, shift, rot, bias, x, v, fit, pb,
     fn(topology, w, c1, c2, vmax, P, D, kind, ptr(o), ptr(m), bias, ptr(x), ptr(v), ptr(fit), ptr(pb), ptr(pbf),
        ptr(w_), len(w_), lb, ub, ptr(nb))
     return nb
+
+
+register_c({"orc_de_fixed_generation_words": (i64, [c_int, u64, ctypes.c_uint32, c_int, c_int, vp, i64])})
+
+
+def de_fixed_generation_words(mutation: int, key: int, gen: int, P: int, D: int) -> np.ndarray:
+    cap = P * (D + 64)
+    out = np.empty(cap, np.uint64)
+    n = C().orc_de_fixed_generation_words(mutation, key, gen, P, D, ptr(out), cap)
+    assert n <= cap
+    return out[:n].copy()
+
+
+register_c({"orc_make_composition": (None, [u64, u64, c_int, c_int, vp, vp])})
+register_ref({"ref_make_composition": (None, [u64, u64, c_int, c_int, vp, vp])})
+
+# BASELINE config 4 composition recipe (component order: Rastrigin, elliptic, Ackley)
+CONFIG4_KINDS = [5, 1, 6]
+CONFIG4_SIGMA = [10.0, 20.0, 30.0]
+CONFIG4_LAMBDA = [1.0, 1e-6, 1.0]
+CONFIG4_BIAS = [0.0, 100.0, 200.0]
+
+
+def composition_components(seed: int, dim: int, n_comp: int = 3, stream: int = 1):
+    s = np.empty((n_comp, dim))
+    m = np.empty((n_comp, dim, dim))
+    C().orc_make_composition(seed, stream, dim, n_comp, ptr(s), ptr(m))
+    return s, m

@@ -480,3 +480,14 @@ REF_API void ref_pso_destroy(int dtype, void* h) {
   if (dtype == 1) delete static_cast<ref_pso_run<double>*>(h);
   else delete static_cast<ref_pso_run<float>*>(h);
 }
+
+REF_API void ref_make_composition(uint64_t seed, uint64_t stream, int dim, int n_comp, double* shifts, double* rots) {
+  rng_stream r = derive_stream(seed, stream);
+  std::vector<double> scratch;
+  for (int c = 0; c < n_comp; ++c) {
+    auto o = problems::detail::draw_shift<double>(dim, -100.0, 100.0, r);
+    auto m = problems::detail::draw_rotation<double>(dim, r, scratch);
+    std::memcpy(shifts + size_t(c) * dim, o.data(), sizeof(double) * dim);
+    std::memcpy(rots + size_t(c) * dim * dim, m.data(), sizeof(double) * size_t(dim) * dim);
+  }
+}

@@ -1,0 +1,324 @@
+// runs.cu — K8: many independent DE runs in ONE persistent launch (BASELINE config 4).
+//
+// Replaces the reference's thread pool over independent runs (experiment/runner.hpp:101-160,
+// evo_bench) for small problems: one CTA owns one run for ALL its generations, with the
+// population, the trial vectors, the run's rotation(s) and shift(s) resident in shared memory.
+// Per generation, inside the CTA (de/engine.hpp:71-102 semantics):
+//   draws     thread per individual, Philox sub-stream (g << 32) | i of the run's key: donor
+//             indices with the reference's rejection loops, jrand (de/strategy.hpp:84-86, 187)
+//   trial     thread per gene: binomial mask from the gene's word, donor x_r1 + F (x_r2 - x_r3),
+//             clip / midpoint repair (de/strategy.hpp:93, 189-193, 234-276)
+//   evaluate  the run's problem on every trial: z = M_k (t - o_k) accumulated in the reference's
+//             order (separate mul / add), base values, composition weights and weighted sum in
+//             double (problems/instance.hpp:60-76, 116-174)
+//   select    trial replaces parent when f_trial <= f_parent (de/engine.hpp:36)
+// Supported here: rand/1 or best/1 with a fixed adapter and no archive (the `de` preset,
+// presets.hpp:59-69) on base or composition problems whose data fit in shared memory.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "evb_internal.cuh"
+#include "evb_math.cuh"
+#include "rng.cuh"
+
+namespace evb {
+namespace {
+
+constexpr int kRunsMaxComp = 4;
+
+struct run_problem {
+  const double* shift[kRunsMaxComp];  // per component (base problem: component 0)
+  const double* rot[kRunsMaxComp];
+  int kind[kRunsMaxComp];
+  double sigma[kRunsMaxComp], lambda[kRunsMaxComp], cbias[kRunsMaxComp];
+  int n_comp;  // 0: base problem (shift[0], rot[0], kind[0])
+  int ld;      // row stride of the rotations
+  double bias;
+  const double* ell_w;
+};
+
+struct runs_args {
+  int P, D, G, ld;
+  int mutation, repair;
+  double F, CR, lb, ub;
+  const run_problem* probs;
+  const uint64_t* keys;
+  uint32_t gen0;
+  double* pop;  // n_runs x P x D
+  double* fit;  // n_runs x P
+  int init;
+};
+
+__device__ __forceinline__ double clip_or_mid(double v, double target, double lb, double ub, int repair) {
+  if (repair == EVB_REP_CLIP) {
+    if (v < lb) v = lb;
+    if (v > ub) v = ub;
+  } else if (repair == EVB_REP_MIDPOINT_TARGET) {
+    if (v < lb) v = __ddiv_rn(__dadd_rn(lb, target), 2.0);
+    else if (v > ub) v = __ddiv_rn(__dadd_rn(ub, target), 2.0);
+  }
+  return v;
+}
+
+// Evaluate the P rows of `X` (smem, stride D) into f (smem).  Composition components are done one
+// after another through `sZ` (P x D) with the component rotation in sM (D x S, S odd).
+__device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int D, int S, double* sM, double* sZ,
+                              double* sO, double* sFk, double* sDist, double* f) {
+  const int ncomp = pr.n_comp > 0 ? pr.n_comp : 1;
+  for (int c = 0; c < ncomp; ++c) {
+    for (int e = threadIdx.x; e < D * D; e += blockDim.x) sM[(e / D) * S + (e % D)] = pr.rot[c][(e / D) * pr.ld + (e % D)];
+    for (int e = threadIdx.x; e < D; e += blockDim.x) sO[e] = pr.shift[c][e];
+    __syncthreads();
+    if (pr.n_comp > 0)
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {  // dist^2 in double (problems/instance.hpp:127-134)
+        double d2 = 0.0;
+        for (int j = 0; j < D; ++j) {
+          const double dj = __dsub_rn(X[i * D + j], sO[j]);
+          d2 = __dadd_rn(d2, __dmul_rn(dj, dj));
+        }
+        sDist[i * kRunsMaxComp + c] = d2;
+      }
+    for (int e = threadIdx.x; e < P * D; e += blockDim.x) {  // z = M (x - o), reference order
+      const int i = e / D, r = e % D;
+      const double* m = sM + r * S;
+      const double* x = X + i * D;
+      double acc = 0.0;
+      for (int k = 0; k < D; ++k) acc = __dadd_rn(acc, __dmul_rn(m[k], __dsub_rn(x[k], sO[k])));
+      sZ[e] = acc;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+      const double* zr = sZ + i * D;
+      auto z = [&](int q) { return zr[q]; };
+      sFk[i * kRunsMaxComp + c] = base_value_seq<double, false>(pr.kind[c], D, z, pr.ell_w);
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    if (pr.n_comp == 0) {
+      f[i] = __dadd_rn(sFk[i * kRunsMaxComp], pr.bias);
+      continue;
+    }
+    // weights exactly as problems/instance.hpp:135-171
+    const double* dist = sDist + i * kRunsMaxComp;
+    double w[kRunsMaxComp];
+    int zero_count = 0;
+    for (int k = 0; k < pr.n_comp; ++k) {
+      if (dist[k] == 0.0) {
+        ++zero_count;
+        w[k] = -1.0;
+      } else {
+        w[k] = __dmul_rn(__ddiv_rn(1.0, __dsqrt_rn(dist[k])),
+                         exp(__ddiv_rn(-dist[k], __dmul_rn(__dmul_rn(__dmul_rn(2.0, double(D)), pr.sigma[k]), pr.sigma[k]))));
+      }
+    }
+    double wsum = 0.0;
+    if (zero_count > 0) {
+      for (int k = 0; k < pr.n_comp; ++k) w[k] = w[k] < 0.0 ? 1.0 : 0.0;
+      wsum = double(zero_count);
+    } else {
+      for (int k = 0; k < pr.n_comp; ++k) wsum = __dadd_rn(wsum, w[k]);
+      if (wsum == 0.0) {
+        int nearest = 0;
+        for (int k = 1; k < pr.n_comp; ++k)
+          if (dist[k] < dist[nearest]) nearest = k;
+        w[nearest] = 1.0;
+        wsum = 1.0;
+      }
+    }
+    double value = 0.0;
+    for (int k = 0; k < pr.n_comp; ++k) {
+      const double wk = __ddiv_rn(w[k], wsum);
+      if (wk == 0.0) continue;
+      value = __dadd_rn(value, __dmul_rn(wk, __dadd_rn(__dmul_rn(pr.lambda[k], sFk[i * kRunsMaxComp + k]), pr.cbias[k])));
+    }
+    f[i] = __dadd_rn(value, pr.bias);
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
+  extern __shared__ __align__(16) double sm[];
+  const int P = a.P, D = a.D, S = (D % 2 == 1) ? D : D + 1;
+  const int run = blockIdx.x;
+  double* sPop = sm;                           // P x D
+  double* sTrial = sPop + P * D;               // P x D
+  double* sM = sTrial + P * D;                 // D x S
+  double* sZ = sM + D * S;                     // P x D
+  double* sO = sZ + P * D;                     // D
+  double* sFit = sO + D;                       // P
+  double* sTfit = sFit + P;                    // P
+  double* sFk = sTfit + P;                     // P x 4
+  double* sDist = sFk + P * kRunsMaxComp;      // P x 4
+  int* sIdx = reinterpret_cast<int*>(sDist + P * kRunsMaxComp);  // P x 4 (a, b, c, word offset)
+  const run_problem pr = a.probs[run];
+  const uint64_t key = a.keys[run];
+  double* gpop = a.pop + size_t(run) * P * D;
+  double* gfit = a.fit + size_t(run) * P;
+  word_source src{RNG_PHILOX, key, nullptr, 0};
+
+  if (a.init) {  // init_population (core/population.hpp:88-98), sub-stream kSubInit of gen0
+    const uint64_t ctr = (uint64_t(a.gen0) << 32) | kSubInit;
+    for (int e = threadIdx.x; e < P * D; e += blockDim.x)
+      sPop[e] = __dadd_rn(a.lb, __dmul_rn(__dsub_rn(a.ub, a.lb), u01_of(philox_word(key, ctr, uint64_t(e)))));
+    __syncthreads();
+    runs_evaluate(pr, sPop, P, D, S, sM, sZ, sO, sFk, sDist, sFit);
+  } else {
+    for (int e = threadIdx.x; e < P * D; e += blockDim.x) sPop[e] = gpop[e];
+    for (int i = threadIdx.x; i < P; i += blockDim.x) sFit[i] = gfit[i];
+    __syncthreads();
+  }
+  const uint32_t g_first = a.gen0 + (a.init ? 1u : 0u);
+  for (int g = 0; g < a.G; ++g) {
+    const uint32_t gen = g_first + uint32_t(g);
+    // draws (thread per individual)
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+      word_reader r{&src, (uint64_t(gen) << 32) | uint32_t(i), 0, 0, nullptr};
+      int x1, x2, x3;
+      if (a.mutation == EVB_MUT_RAND1) {
+        do { x1 = draw_int(r, P); } while (x1 == i);
+        do { x2 = draw_int(r, P); } while (x2 == i || x2 == x1);
+        do { x3 = draw_int(r, P); } while (x3 == i || x3 == x1 || x3 == x2);
+      } else {  // best/1: best = first strict minimum (fitness_order[0])
+        int best = 0;
+        for (int q = 1; q < P; ++q)
+          if (sFit[q] < sFit[best]) best = q;
+        x1 = best;
+        do { x2 = draw_int(r, P); } while (x2 == i);
+        do { x3 = draw_int(r, P); } while (x3 == i || x3 == x2);
+      }
+      const int jr = draw_int(r, D);
+      sIdx[4 * i + 0] = x1;
+      sIdx[4 * i + 1] = x2;
+      sIdx[4 * i + 2] = x3;
+      sIdx[4 * i + 3] = (int(r.count) << 16) | jr;  // gene words start after the scalar words
+    }
+    __syncthreads();
+    // trial (thread per gene)
+    for (int e = threadIdx.x; e < P * D; e += blockDim.x) {
+      const int i = e / D, j = e % D;
+      const int packed = sIdx[4 * i + 3];
+      const int s0 = packed >> 16, jr = packed & 0xFFFF;
+      const uint64_t w = philox_word(key, (uint64_t(gen) << 32) | uint32_t(i), uint64_t(s0 + j));
+      const double u = u01_of(w);
+      const double xi = sPop[i * D + j];
+      double v = xi;
+      if (u < a.CR || j == jr) {
+        const double xa = sPop[sIdx[4 * i] * D + j], xb = sPop[sIdx[4 * i + 1] * D + j], xc = sPop[sIdx[4 * i + 2] * D + j];
+        v = __dadd_rn(xa, __dmul_rn(a.F, __dsub_rn(xb, xc)));
+      }
+      sTrial[e] = clip_or_mid(v, xi, a.lb, a.ub, a.repair);
+    }
+    __syncthreads();
+    runs_evaluate(pr, sTrial, P, D, S, sM, sZ, sO, sFk, sDist, sTfit);
+    // selection
+    for (int e = threadIdx.x; e < P * D; e += blockDim.x) {
+      const int i = e / D;
+      if (sTfit[i] <= sFit[i]) sPop[e] = sTrial[e];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < P; i += blockDim.x)
+      if (sTfit[i] <= sFit[i]) sFit[i] = sTfit[i];
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < P * D; e += blockDim.x) gpop[e] = sPop[e];
+  for (int i = threadIdx.x; i < P; i += blockDim.x) gfit[i] = sFit[i];
+}
+
+size_t runs_smem(int P, int D) {
+  const int S = (D % 2 == 1) ? D : D + 1;
+  return sizeof(double) * (size_t(3) * P * D + size_t(D) * S + D + 2 * P + 2 * P * kRunsMaxComp) +
+         sizeof(int) * 4 * P + 64;
+}
+
+}  // namespace
+}  // namespace evb
+
+using namespace evb;
+
+extern "C" int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int pop_size, int dim,
+                           const evb_problem* problems, const uint64_t* keys, int generations, double lb, double ub,
+                           void* pops, void* fits, int init, uint32_t gen0, void* stream) {
+  return guarded([&] {
+    require(dtype == EVB_F64, "de_runs: the persistent runs kernel is fp64");
+    require(cfg && problems && keys && pops && fits, "de_runs: null argument");
+    require(cfg->mutation == EVB_MUT_RAND1 || cfg->mutation == EVB_MUT_BEST1,
+            "de_runs: persistent kernel supports rand_1 / best_1 mutation");
+    require(cfg->parameter == EVB_PAR_FIXED, "de_runs: persistent kernel supports the fixed adapter");
+    require(cfg->archive_rate == 0.0, "de_runs: persistent kernel runs without an archive");
+    require(cfg->repair == EVB_REP_CLIP || cfg->repair == EVB_REP_MIDPOINT_TARGET, "de_runs: clip or midpoint repair");
+    require(cfg->crossover == EVB_CX_BINOMIAL, "de_runs: binomial crossover");
+    require(cfg->f > 0.0 && cfg->f <= 1.0, "fixed_parameter: F must be in (0,1]");
+    require(cfg->cr >= 0.0 && cfg->cr <= 1.0, "fixed_parameter: CR must be in [0,1]");
+    require(pop_size >= (cfg->mutation == EVB_MUT_RAND1 ? 4 : 3), "de_engine: population too small for mutation");
+    require(n_runs >= 1 && dim >= 1 && dim < 65536 && generations >= 0, "de_runs: bad sizes");
+    const size_t smem = runs_smem(pop_size, dim);
+    require(smem <= 227 * 1024, "de_runs: run state does not fit in shared memory (use evb_de_generation)");
+    std::vector<run_problem> rp(n_runs);
+    for (int r = 0; r < n_runs; ++r) {
+      const device_problem& p = problems[r]->p;
+      require(p.dtype == EVB_F64 && p.dim == dim, "de_runs: problem dtype / dim mismatch");
+      require(p.spec != SPEC_HYBRID, "de_runs: hybrid problems are not supported by the persistent kernel");
+      run_problem& q = rp[r];
+      q.bias = p.bias;
+      q.ld = p.ld;
+      q.ell_w = static_cast<const double*>(p.ell_w);
+      if (p.spec == SPEC_BASE) {
+        q.n_comp = 0;
+        q.shift[0] = static_cast<const double*>(p.shift);
+        q.rot[0] = static_cast<const double*>(p.rotation);
+        q.kind[0] = p.kind;
+      } else {
+        require(p.n_comp <= kRunsMaxComp, "de_runs: at most 4 composition components");
+        q.n_comp = p.n_comp;
+        std::vector<int> kinds(p.n_comp);
+        std::vector<double> sg(p.n_comp), la(p.n_comp), cb(p.n_comp);
+        EVB_CUDA(cudaMemcpy(kinds.data(), p.comp_kinds, sizeof(int) * p.n_comp, cudaMemcpyDeviceToHost));
+        EVB_CUDA(cudaMemcpy(sg.data(), p.comp_sigma, sizeof(double) * p.n_comp, cudaMemcpyDeviceToHost));
+        EVB_CUDA(cudaMemcpy(la.data(), p.comp_lambda, sizeof(double) * p.n_comp, cudaMemcpyDeviceToHost));
+        EVB_CUDA(cudaMemcpy(cb.data(), p.comp_bias, sizeof(double) * p.n_comp, cudaMemcpyDeviceToHost));
+        for (int c = 0; c < p.n_comp; ++c) {
+          q.shift[c] = static_cast<const double*>(p.comp_shift) + size_t(c) * p.ld;
+          q.rot[c] = static_cast<const double*>(p.comp_rot) + size_t(c) * dim * p.ld;
+          q.kind[c] = kinds[c];
+          q.sigma[c] = sg[c];
+          q.lambda[c] = la[c];
+          q.cbias[c] = cb[c];
+        }
+      }
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    run_problem* dprobs = nullptr;
+    uint64_t* dkeys = nullptr;
+    EVB_CUDA(cudaMalloc(&dprobs, sizeof(run_problem) * n_runs));
+    EVB_CUDA(cudaMalloc(&dkeys, sizeof(uint64_t) * n_runs));
+    EVB_CUDA(cudaMemcpyAsync(dprobs, rp.data(), sizeof(run_problem) * n_runs, cudaMemcpyHostToDevice, st));
+    EVB_CUDA(cudaMemcpyAsync(dkeys, keys, sizeof(uint64_t) * n_runs, cudaMemcpyHostToDevice, st));
+    runs_args a{};
+    a.P = pop_size;
+    a.D = dim;
+    a.G = generations;
+    a.mutation = cfg->mutation;
+    a.repair = cfg->repair;
+    a.F = cfg->f;
+    a.CR = cfg->cr;
+    a.lb = lb;
+    a.ub = ub;
+    a.probs = dprobs;
+    a.keys = dkeys;
+    a.gen0 = gen0;
+    a.pop = static_cast<double*>(pops);
+    a.fit = static_cast<double*>(fits);
+    a.init = init;
+    EVB_CUDA(cudaFuncSetAttribute(de_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    de_runs_kernel<<<n_runs, 512, smem, st>>>(a);
+    count_launch();
+    const cudaError_t err = cudaGetLastError();
+    EVB_CUDA(cudaStreamSynchronize(st));
+    cudaFree(dprobs);
+    cudaFree(dkeys);
+    EVB_CUDA(err);
+  });
+}
