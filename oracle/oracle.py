@@ -486,3 +486,10 @@ def composition_components(seed: int, dim: int, n_comp: int = 3, stream: int = 1
     m = np.empty((n_comp, dim, dim))
     C().orc_make_composition(seed, stream, dim, n_comp, ptr(s), ptr(m))
     return s, m
+
+
+register_ref({
+    "ref_pso_set_threads": (None, [c_int, vp, c_int]),
+    "ref_bench_config4": (c_double, [c_int, c_int, c_int, c_int, c_int, vp, vp, vp, vp, vp, vp]),
+    "ref_bench_de": (c_double, [c_int, c_int, c_int, c_int, c_int, vp, vp, u64]),
+})

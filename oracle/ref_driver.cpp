@@ -370,6 +370,7 @@ struct ref_pso_run {
   std::vector<individual<T>> pb;
   std::vector<T> fit;
   int P, D;
+  int threads = 1;
 
   int step(const uint64_t* words, int64_t n, T lb, T ub) {
     const uint64_t sentinel = 0x0badc0ffee0ddf00ULL;
@@ -399,9 +400,15 @@ struct ref_pso_run {
         }
       }
     }
-    eval_scratch<T> scratch;
+    const int nt = std::max(1, std::min(threads, P));
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nt; ++t)
+      pool.emplace_back([&, t] {
+        eval_scratch<T> scratch;
+        for (int i = P * t / nt; i < P * (t + 1) / nt; ++i) fit[size_t(i)] = problem->evaluate(x[size_t(i)], scratch);
+      });
+    for (auto& th : pool) th.join();
     for (int i = 0; i < P; ++i) {
-      fit[size_t(i)] = problem->evaluate(x[size_t(i)], scratch);
       if (fit[size_t(i)] < pb[size_t(i)].fitness) {
         pb[size_t(i)].genome = x[size_t(i)];
         pb[size_t(i)].fitness = fit[size_t(i)];
@@ -490,4 +497,63 @@ REF_API void ref_make_composition(uint64_t seed, uint64_t stream, int dim, int n
     std::memcpy(shifts + size_t(c) * dim, o.data(), sizeof(double) * dim);
     std::memcpy(rots + size_t(c) * dim * dim, m.data(), sizeof(double) * size_t(dim) * dim);
   }
+}
+
+REF_API void ref_pso_set_threads(int dtype, void* h, int threads) {
+  if (dtype == 1) static_cast<ref_pso_run<double>*>(h)->threads = threads;
+  else static_cast<ref_pso_run<float>*>(h)->threads = threads;
+}
+
+// ---- CPU baselines through the reference's own harness (bench_configs.py) ------------------------
+#include <chrono>
+
+namespace {
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace
+
+// Config 4: evo_bench (experiment/runner.hpp:101-160) with the `de` preset (presets.hpp:621-628)
+// over a suite of n_runs composition instances, `threads` workers; max_fes covers init + gens.
+REF_API double ref_bench_config4(int n_runs, int P, int D, int gens, int threads, const double* shifts,
+                                 const double* rots, const int* kinds, const double* sigma, const double* lambda,
+                                 const double* cbias) {
+  std::vector<problem_instance<double>> inst;
+  for (int r = 0; r < n_runs; ++r)
+    inst.push_back(make_comp<double>(D, 3, kinds, shifts + size_t(r) * 3 * D, rots + size_t(r) * 3 * D * D, sigma,
+                                     lambda, cbias, 0.0));
+  problems::suite<double> su("config4", D, {11}, n_runs, 64, std::move(inst));
+  experiment::observer<double> obs;
+  experiment::bench_options opt;
+  opt.independent_runs = 1;
+  opt.max_fes = (long long)P * (gens + 1);
+  opt.parallel = threads > 1;
+  opt.threads = threads;
+  opt.master_seed = 64;
+  presets::algorithm_options ao;
+  ao.name = "de";
+  ao.pop_size = P;
+  auto alg = presets::make_algorithm<double>(ao);
+  const double t0 = now_s();
+  experiment::evo_bench(alg, su, obs, opt);
+  return now_s() - t0;
+}
+
+// Configs 0 / 2: one de_engine run on its native stream; returns seconds for `gens` generations
+// (init + evaluation excluded).  preset 0: build_de_fixed(0.5, 0.9); 1: build_shade(0.11, P, 1.0).
+REF_API double ref_bench_de(int preset, int P, int D, int gens, int kind, const double* shift, const double* rot,
+                            uint64_t seed) {
+  auto engine = preset == 0 ? presets::detail::build_de_fixed<double>(0.5, 0.9)
+                            : presets::detail::build_shade<double>(0.11, P, 1.0, de::population_policy::fixed());
+  auto prob = make_base<double>(kind, D, shift, rot, 0.0);
+  rng_stream rng(seed, 0);
+  auto pop = init_population<double>(P, D, -100.0, 100.0, rng);
+  eval_scratch<double> scratch;
+  auto objective = [&](std::span<const double> x) { return prob.evaluate(x, scratch); };
+  for (auto& m : pop) m.evaluate(objective);
+  engine.archive().set_capacity(engine.archive_capacity_for(P), rng);
+  evolution_state st(1LL << 40, P, D, std::min(4, P));
+  const double t0 = now_s();
+  for (int g = 0; g < gens; ++g) engine.generation(pop, st, objective, -100.0, 100.0, rng);
+  return now_s() - t0;
 }
