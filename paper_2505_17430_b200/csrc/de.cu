@@ -300,47 +300,113 @@ __global__ void de_trial_kernel(const de_dev<T> d) {
   }
 }
 
-// K5a: sequential selection bookkeeping (de/engine.hpp:27-47, de/strategy.hpp:29-37,
-// de/parameter.hpp:166-184).  One CTA; the O(P) sequential part runs in thread 0 because the
-// reference's archive victims and SHADE sums are order-dependent.
+// K5a: selection bookkeeping (de/engine.hpp:27-47, de/strategy.hpp:29-37, de/parameter.hpp:166-184)
+// in one CTA, parallel where the reference's sequential semantics allow it:
+//   * win / success flags per individual, stable compaction of pushes and successes by block
+//     prefix sums (i order preserved);
+//   * archive slots: push q appends while the archive has room (slot size+q); once full the size
+//     stays at capacity, so each later push's victim uniform_int(cap) depends only on its own word
+//     (the (q - room)-th archive word) -> computed in parallel; last writer wins per slot via an
+//     atomicMax on the push index;
+//   * SHADE / JADE sums stay sequential (one thread, successes staged in order) so the memory
+//     update rounds exactly like the reference's loops.
+constexpr int kSelThreads = 1024;
+
 template <typename T>
-__global__ void de_select_scan_kernel(const de_dev<T> d) {
-  for (int s = threadIdx.x; s < d.archive_cap; s += blockDim.x) d.owner[s] = -1;
-  __syncthreads();
-  if (threadIdx.x != 0) return;
-  int size = *d.arch_size;
-  int n_succ = 0;
-  int64_t q = 0;  // archive-victim words consumed
-  int64_t wpos = d.src.mode == RNG_WORDS ? *d.cursor : 0;
+__global__ void __launch_bounds__(kSelThreads) de_select_scan_kernel(const de_dev<T> d) {
+  __shared__ int warp_sum[2][kSelThreads / 32];
+  __shared__ int carry[2];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int s = tid; s < d.archive_cap; s += blockDim.x) d.owner[s] = -1;
+  const int size0 = *d.arch_size;
+  const int room = d.archive_cap - size0;
+  const int64_t wpos = d.src.mode == RNG_WORDS ? *d.cursor : 0;
   const uint64_t ctr_hi = (uint64_t(d.gen) << 32) | kSubArchive;
-  for (int i = 0; i < d.P; ++i) {
-    const T ft = d.trial_fit[i], fp = d.fit[i];
-    const int w = (ft <= fp) ? 1 : 0;
-    d.win[i] = w;
-    d.arch_slot[i] = -1;
-    if (!w) continue;
-    const T gain = fop<T>::sub(fp, ft);
-    if (gain > T(0)) d.succ[n_succ++] = i;
-    if (d.archive_cap > 0) {
-      int sl;
-      if (size < d.archive_cap) {
-        sl = size++;
-      } else {
-        const uint64_t word = word_at(d.src, ctr_hi, d.src.mode == RNG_WORDS ? wpos + q : q, d.overflow);
-        ++q;
-        sl = uint_of(word, size);
+  if (tid == 0) carry[0] = carry[1] = 0;
+  __syncthreads();
+  // pass 1: flags, exclusive prefix sums (pushes, successes), slot assignment
+  for (int base = 0; base < d.P; base += blockDim.x) {
+    const int i = base + tid;
+    int w = 0, s = 0;
+    if (i < d.P) {
+      const T ft = d.trial_fit[i], fp = d.fit[i];
+      w = (ft <= fp) ? 1 : 0;
+      s = (w && fop<T>::sub(fp, ft) > T(0)) ? 1 : 0;
+      d.arch_slot[i] = -1;
+    }
+    // block-wide exclusive scans of (w, s)
+    int iw = w, is = s;
+    for (int off = 1; off < 32; off <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, iw, off), b = __shfl_up_sync(0xffffffffu, is, off);
+      if (lane >= off) {
+        iw += a;
+        is += b;
       }
-      const int prev = d.owner[sl];
-      if (prev >= 0) d.arch_slot[prev] = -1;  // last writer wins (members_[v] = genome)
-      d.owner[sl] = i;
-      d.arch_slot[i] = sl;
+    }
+    if (lane == 31) {
+      warp_sum[0][wid] = iw;
+      warp_sum[1][wid] = is;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      const int nw = blockDim.x >> 5;
+      int a = lane < nw ? warp_sum[0][lane] : 0, b = lane < nw ? warp_sum[1][lane] : 0;
+      for (int off = 1; off < 32; off <<= 1) {
+        const int x = __shfl_up_sync(0xffffffffu, a, off), y = __shfl_up_sync(0xffffffffu, b, off);
+        if (lane >= off) {
+          a += x;
+          b += y;
+        }
+      }
+      if (lane < nw) {
+        warp_sum[0][lane] = a;
+        warp_sum[1][lane] = b;
+      }
+    }
+    __syncthreads();
+    const int q = carry[0] + (wid > 0 ? warp_sum[0][wid - 1] : 0) + iw - w;  // push index
+    const int k = carry[1] + (wid > 0 ? warp_sum[1][wid - 1] : 0) + is - s;  // success index
+    if (i < d.P) {
+      d.win[i] = w ? q + 1 : 0;  // winner flag carrying its push index
+      if (s) d.succ[k] = i;
+      if (w && d.archive_cap > 0) {
+        int sl;
+        if (q < room) {
+          sl = size0 + q;
+        } else {
+          const int64_t v = q - room;
+          sl = uint_of(word_at(d.src, ctr_hi, d.src.mode == RNG_WORDS ? wpos + v : v, d.overflow), d.archive_cap);
+        }
+        d.arch_slot[i] = sl;  // provisional; resolved below
+        atomicMax(&d.owner[sl], q);
+      }
+    }
+    __syncthreads();
+    if (tid == blockDim.x - 1) {
+      carry[0] = q + w;
+      carry[1] = k + s;
+    }
+    __syncthreads();
+  }
+  const int n_push = carry[0], n_succ = carry[1];
+  // pass 2: last writer wins (members_[victim] = genome, in push order)
+  for (int base = 0; base < d.P; base += blockDim.x) {
+    const int i = base + tid;
+    if (i < d.P && d.win[i] && d.archive_cap > 0) {
+      const int sl = d.arch_slot[i];
+      if (d.owner[sl] != d.win[i] - 1) d.arch_slot[i] = -1;  // overwritten by a later push
     }
   }
-  *d.arch_size = size;
-  *d.arch_words = q;
-  if (d.src.mode == RNG_WORDS) *d.cursor = wpos + q;
+  __syncthreads();
+  if (tid == 0) {
+    const int new_size = min(d.archive_cap, size0 + n_push);
+    const int64_t nv = d.archive_cap > 0 ? max(0, n_push - room) : 0;
+    *d.arch_size = new_size;
+    *d.arch_words = nv;
+    if (d.src.mode == RNG_WORDS) *d.cursor = wpos + nv;
+  }
   // adapter update
-  if (n_succ == 0) return;
+  if (tid != 0 || n_succ == 0) return;
   if (d.cfg.parameter == EVB_PAR_SHADE) {
     double gain_sum = 0.0;
     for (int s = 0; s < n_succ; ++s) {
@@ -486,7 +552,7 @@ void generation_t(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, vo
   rq.stream = st;
   rq.scalar_trig = true;
   eval_dispatch(rq);
-  de_select_scan_kernel<T><<<1, 256, 0, st>>>(d);
+  de_select_scan_kernel<T><<<1, kSelThreads, 0, st>>>(d);
   count_launch();
   {
     const int th = std::min(256, int(round_up(e->D, 32)));
