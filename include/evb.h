@@ -72,6 +72,13 @@ EVB_API const char* evb_last_error(void);
 EVB_API int evb_device_info(int device, int* sm_count, int* smem_per_sm, int* l2_bytes, int* cc_major,
                     int* cc_minor);
 
+/* Device memory helpers for hosts without a CUDA toolchain (FFI bindings, the C++ wrapper). */
+EVB_API int evb_device_alloc(size_t bytes, void** out);
+EVB_API int evb_device_free(void* ptr);
+EVB_API int evb_copy_to_device(void* dst, const void* src_host, size_t bytes);
+EVB_API int evb_copy_to_host(void* dst_host, const void* src, size_t bytes);
+EVB_API int evb_synchronize(void);
+
 /* ---- problems (problems/instance.hpp:180-252) -------------------------------------- */
 
 /* Shifted-rotated base problem: value(x) = base(M (x - o)) + bias, rosenbrock on z + 1

@@ -126,6 +126,27 @@ int evb_device_info(int device, int* sm_count, int* smem_per_sm, int* l2_bytes, 
   });
 }
 
+int evb_device_alloc(size_t bytes, void** out) {
+  return guarded([&] {
+    require(out != nullptr, "device_alloc: null output");
+    EVB_CUDA(cudaMalloc(out, bytes ? bytes : 1));
+  });
+}
+int evb_device_free(void* ptr) {
+  return guarded([&] {
+    if (ptr) EVB_CUDA(cudaFree(ptr));
+  });
+}
+int evb_copy_to_device(void* dst, const void* src, size_t bytes) {
+  return guarded([&] { EVB_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice)); });
+}
+int evb_copy_to_host(void* dst, const void* src, size_t bytes) {
+  return guarded([&] { EVB_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost)); });
+}
+int evb_synchronize(void) {
+  return guarded([&] { EVB_CUDA(cudaDeviceSynchronize()); });
+}
+
 int evb_problem_create_base(int dtype, int dim, int kind, const void* shift, const void* rotation, double bias,
                             evb_problem* out) {
   return guarded([&] {

@@ -62,31 +62,55 @@ __device__ __forceinline__ double clip_or_mid(double v, double target, double lb
   return v;
 }
 
-// Evaluate the P rows of `X` (smem, stride D) into f (smem).  Composition components are done one
-// after another through `sZ` (P x D) with the component rotation in sM (D x S, S odd).
+// Evaluate the P rows of `X` (smem, stride D) into f (smem).  Per component: s = x - o is staged
+// once (rounded like transform_input's diff, problems/instance.hpp:66-67), then z = M s with each
+// z[i][r] accumulated over k in the reference's order (separate mul and add).  Register blocking:
+// lane r owns one row of M (conflict-free, odd stride) and up to 8 individuals of its group, whose
+// s[i][k] are warp-broadcast loads — ~8x fewer shared-memory wavefronts per MAC than one dot per
+// thread.  Base values and composition weights are sequential per individual (exact order).
 __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int D, int S, double* sM, double* sZ,
-                              double* sO, double* sFk, double* sDist, double* f) {
+                              double* sS, double* sO, double* sFk, double* sDist, double* f) {
   const int ncomp = pr.n_comp > 0 ? pr.n_comp : 1;
+  const int RP = (D + 31) / 32 * 32;           // threads per row group
+  const int NG = max(1, int(blockDim.x) / RP);  // individual groups
   for (int c = 0; c < ncomp; ++c) {
     for (int e = threadIdx.x; e < D * D; e += blockDim.x) sM[(e / D) * S + (e % D)] = pr.rot[c][(e / D) * pr.ld + (e % D)];
     for (int e = threadIdx.x; e < D; e += blockDim.x) sO[e] = pr.shift[c][e];
     __syncthreads();
+    for (int e = threadIdx.x; e < P * D; e += blockDim.x) sS[e] = __dsub_rn(X[e], sO[e % D]);
+    __syncthreads();
     if (pr.n_comp > 0)
       for (int i = threadIdx.x; i < P; i += blockDim.x) {  // dist^2 in double (problems/instance.hpp:127-134)
         double d2 = 0.0;
-        for (int j = 0; j < D; ++j) {
-          const double dj = __dsub_rn(X[i * D + j], sO[j]);
-          d2 = __dadd_rn(d2, __dmul_rn(dj, dj));
-        }
+        const double* si = sS + i * D;
+        for (int j = 0; j < D; ++j) d2 = __dadd_rn(d2, __dmul_rn(si[j], si[j]));
         sDist[i * kRunsMaxComp + c] = d2;
       }
-    for (int e = threadIdx.x; e < P * D; e += blockDim.x) {  // z = M (x - o), reference order
-      const int i = e / D, r = e % D;
-      const double* m = sM + r * S;
-      const double* x = X + i * D;
-      double acc = 0.0;
-      for (int k = 0; k < D; ++k) acc = __dadd_rn(acc, __dmul_rn(m[k], __dsub_rn(x[k], sO[k])));
-      sZ[e] = acc;
+    {
+      const int r = int(threadIdx.x) % RP, g = int(threadIdx.x) / RP;
+      if (r < D && g < NG) {
+        const double* m = sM + r * S;
+        for (int i0 = g; i0 < P; i0 += 8 * NG) {
+          double acc[8];
+          const double* sp[8];
+          int n = 0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int i = i0 + q * NG;
+            acc[q] = 0.0;
+            sp[q] = sS + min(i, P - 1) * D;
+            n += i < P ? 1 : 0;
+          }
+          for (int k = 0; k < D; ++k) {
+            const double mk = m[k];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(mk, sp[q][k]));
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (q < n) sZ[(i0 + q * NG) * D + r] = acc[q];
+        }
+      }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < P; i += blockDim.x) {
@@ -147,7 +171,8 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
   double* sTrial = sPop + P * D;               // P x D
   double* sM = sTrial + P * D;                 // D x S
   double* sZ = sM + D * S;                     // P x D
-  double* sO = sZ + P * D;                     // D
+  double* sS = sZ + P * D;                     // P x D  (x - o of the current component)
+  double* sO = sS + P * D;                     // D
   double* sFit = sO + D;                       // P
   double* sTfit = sFit + P;                    // P
   double* sFk = sTfit + P;                     // P x 4
@@ -164,7 +189,7 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
     for (int e = threadIdx.x; e < P * D; e += blockDim.x)
       sPop[e] = __dadd_rn(a.lb, __dmul_rn(__dsub_rn(a.ub, a.lb), u01_of(philox_word(key, ctr, uint64_t(e)))));
     __syncthreads();
-    runs_evaluate(pr, sPop, P, D, S, sM, sZ, sO, sFk, sDist, sFit);
+    runs_evaluate(pr, sPop, P, D, S, sM, sZ, sS, sO, sFk, sDist, sFit);
   } else {
     for (int e = threadIdx.x; e < P * D; e += blockDim.x) sPop[e] = gpop[e];
     for (int i = threadIdx.x; i < P; i += blockDim.x) sFit[i] = gfit[i];
@@ -212,7 +237,7 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
       sTrial[e] = clip_or_mid(v, xi, a.lb, a.ub, a.repair);
     }
     __syncthreads();
-    runs_evaluate(pr, sTrial, P, D, S, sM, sZ, sO, sFk, sDist, sTfit);
+    runs_evaluate(pr, sTrial, P, D, S, sM, sZ, sS, sO, sFk, sDist, sTfit);
     // selection
     for (int e = threadIdx.x; e < P * D; e += blockDim.x) {
       const int i = e / D;
@@ -229,7 +254,7 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
 
 size_t runs_smem(int P, int D) {
   const int S = (D % 2 == 1) ? D : D + 1;
-  return sizeof(double) * (size_t(3) * P * D + size_t(D) * S + D + 2 * P + 2 * P * kRunsMaxComp) +
+  return sizeof(double) * (size_t(4) * P * D + size_t(D) * S + D + 2 * P + 2 * P * kRunsMaxComp) +
          sizeof(int) * 4 * P + 64;
 }
 
