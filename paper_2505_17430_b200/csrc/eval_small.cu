@@ -96,21 +96,37 @@ __global__ void eval_small_kernel(const small_args<T> a) {
     sZ[idx] = acc;
   }
   __syncthreads();
-  const int nwork = a.PB * (a.spec == SPEC_HYBRID ? 1 : a.n_out);
-  for (int idx = threadIdx.x; idx < nwork; idx += blockDim.x) {
-    const int pb = idx % a.PB, o = idx / a.PB;
-    const int b = b0 + pb;
-    if (b >= a.P) continue;
-    const T* zrow = sZ + pb * D;
-    if (a.spec == SPEC_HYBRID) {
-      const T v = hybrid_value<T>(a.perm, a.sub_kinds, a.chunk_sizes, a.n_chunks, a.hyb_w, zrow, 1);
+  if (a.spec == SPEC_HYBRID) {
+    for (int pb = threadIdx.x; pb < a.PB; pb += blockDim.x) {
+      const int b = b0 + pb;
+      if (b >= a.P) continue;
+      const T v = hybrid_value<T>(a.perm, a.sub_kinds, a.chunk_sizes, a.n_chunks, a.hyb_w, sZ + pb * D, 1);
       a.out[b] = fop<T>::add(v, a.bias);
-    } else {
+    }
+    return;
+  }
+  for (int o = 0; o < a.n_out; ++o) {
+    const int kind = a.kinds[o];
+    if (kind_has_pre(kind)) {  // transcendental terms of every element in parallel (into sS)
+      for (int e = threadIdx.x; e < a.PB * D; e += blockDim.x) {
+        const T* zr = sZ + (e / D) * D;
+        auto z = [&](int q) { return zr[q]; };
+        sS[e] = a.scalar_trig ? base_pre_term<T, false>(kind, D, z, e % D) : base_pre_term<T, true>(kind, D, z, e % D);
+      }
+      __syncthreads();
+    }
+    for (int pb = threadIdx.x; pb < a.PB; pb += blockDim.x) {
+      const int b = b0 + pb;
+      if (b >= a.P) continue;
+      const T* zrow = sZ + pb * D;
+      const T* pe = sS + pb * D;
       auto z = [&](int i) { return zrow[i]; };
-      const T v = a.scalar_trig ? base_value_seq<T, false>(a.kinds[o], D, z, a.ell_w)
-                                : base_value_seq<T, true>(a.kinds[o], D, z, a.ell_w);
+      auto pre = [&](int i) { return pe[i]; };
+      const T v = a.scalar_trig ? base_value_pre<T, false>(kind, D, z, pre, a.ell_w)
+                                : base_value_pre<T, true>(kind, D, z, pre, a.ell_w);
       a.out[o * a.ldo + b] = fop<T>::add(v, T(a.biases[o]));
     }
+    __syncthreads();
   }
 }
 
@@ -215,10 +231,21 @@ __global__ void eval_comp_small_kernel(const comp_args<T> a) {
       sZ[idx] = acc;
     }
     __syncthreads();
+    const int kind = a.kinds[c];
+    if (kind_has_pre(kind)) {
+      for (int e = threadIdx.x; e < a.PB * D; e += blockDim.x) {
+        const T* zr = sZ + (e / D) * D;
+        auto z = [&](int q) { return zr[q]; };
+        sS[e] = base_pre_term<T, false>(kind, D, z, e % D);
+      }
+      __syncthreads();
+    }
     for (int pb = threadIdx.x; pb < a.PB; pb += blockDim.x) {
       const T* zrow = sZ + pb * D;
+      const T* pe = sS + pb * D;
       auto z = [&](int i) { return zrow[i]; };
-      sF[pb * kMaxComp + c] = base_value_seq<T, false>(a.kinds[c], D, z, a.ell_w);
+      auto pre = [&](int i) { return pe[i]; };
+      sF[pb * kMaxComp + c] = base_value_pre<T, false>(kind, D, z, pre, a.ell_w);
     }
     __syncthreads();
   }

@@ -216,3 +216,67 @@ __device__ T base_value_seq(int kind, int n, const Z& z, const T* w) {
 }
 
 }  // namespace evb
+
+namespace evb {
+
+// ---- split form of base_value_seq for latency hiding ---------------------------------------------
+// The transcendental part of each element (the whole Rastrigin / Schaffer term, the cosine of
+// Ackley / Griewank) is independent across elements, so a whole CTA can compute it in parallel
+// into `pre`; the reference's sequential accumulation then runs over `pre` with cheap ops only.
+// base_value_pre(kind, n, z, pre, w) == base_value_seq(kind, n, z, w) bit for bit.
+__host__ __device__ inline bool kind_has_pre(int kind) {
+  return kind == EVB_RASTRIGIN || kind == EVB_ACKLEY || kind == EVB_GRIEWANK || kind == EVB_EXPANDED_SCHAFFER_F6;
+}
+
+template <typename T, bool kBatchTrig, typename Z>
+__device__ __forceinline__ T base_pre_term(int kind, int n, const Z& z, int i) {
+  using F = fop<T>;
+  switch (kind) {
+    case EVB_RASTRIGIN: return rastrigin_term<T, kBatchTrig>(z(i));
+    case EVB_ACKLEY: return trig<T, kBatchTrig>::cos_(F::mul(two_pi_v<T>(), z(i)));
+    case EVB_GRIEWANK: return trig<T, kBatchTrig>::cos_(F::div(z(i), F::sqrt_(T(i + 1))));
+    case EVB_EXPANDED_SCHAFFER_F6: return n == 1 ? schaffer_term<T, kBatchTrig>(z(0), z(0))
+                                                 : schaffer_term<T, kBatchTrig>(z(i), z((i + 1) % n));
+  }
+  return T(0);
+}
+
+template <typename T, bool kBatchTrig, typename Z, typename PRE>
+__device__ T base_value_pre(int kind, int n, const Z& z, const PRE& pre, const T* w) {
+  using F = fop<T>;
+  switch (kind) {
+    case EVB_RASTRIGIN: {
+      T acc = T(0);
+      for (int i = 0; i < n; ++i) acc = F::add(acc, pre(i));
+      return acc;
+    }
+    case EVB_ACKLEY: {
+      T ssq = T(0), scos = T(0);
+      for (int i = 0; i < n; ++i) {
+        const T v = z(i);
+        ssq = F::add(ssq, F::mul(v, v));
+        scos = F::add(scos, pre(i));
+      }
+      return ackley_final<T>(ssq, scos, n);
+    }
+    case EVB_GRIEWANK: {
+      T sum = T(0), prod = T(1);
+      for (int i = 0; i < n; ++i) {
+        const T v = z(i);
+        sum = F::add(sum, F::mul(v, v));
+        prod = F::mul(prod, pre(i));
+      }
+      return F::add(F::sub(F::div(sum, T(4000)), prod), T(1));
+    }
+    case EVB_EXPANDED_SCHAFFER_F6: {
+      if (n == 1) return pre(0);
+      T acc = T(0);
+      for (int i = 0; i < n; ++i) acc = F::add(acc, pre(i));
+      return acc;
+    }
+    default:
+      return base_value_seq<T, kBatchTrig>(kind, n, z, w);
+  }
+}
+
+}  // namespace evb

@@ -113,10 +113,21 @@ __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int
       }
     }
     __syncthreads();
+    const int kind = pr.kind[c];
+    if (kind_has_pre(kind)) {  // transcendental terms in parallel over all P*D elements (into sS)
+      for (int e = threadIdx.x; e < P * D; e += blockDim.x) {
+        const double* zr = sZ + (e / D) * D;
+        auto z = [&](int q) { return zr[q]; };
+        sS[e] = base_pre_term<double, false>(kind, D, z, e % D);
+      }
+      __syncthreads();
+    }
     for (int i = threadIdx.x; i < P; i += blockDim.x) {
       const double* zr = sZ + i * D;
+      const double* pe = sS + i * D;
       auto z = [&](int q) { return zr[q]; };
-      sFk[i * kRunsMaxComp + c] = base_value_seq<double, false>(pr.kind[c], D, z, pr.ell_w);
+      auto pre = [&](int q) { return pe[q]; };
+      sFk[i * kRunsMaxComp + c] = base_value_pre<double, false>(kind, D, z, pre, pr.ell_w);
     }
     __syncthreads();
   }
