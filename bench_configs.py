@@ -95,6 +95,14 @@ def cfg0(out):
     fit = torch.empty(P, dtype=torch.float64, device=DEV)
     evb.evaluate_batch(prob, pop, evb.EvalScratch(), fit)
     ms = timed(lambda: eng.generation(prob, pop, fit, -100.0, 100.0, rng), 200)
+    a, b = ev(), ev()
+    eng.generations(prob, pop, fit, -100.0, 100.0, rng, 10)
+    torch.cuda.synchronize()
+    a.record()
+    eng.generations(prob, pop, fit, -100.0, 100.0, rng, 1000)
+    b.record()
+    torch.cuda.synchronize()
+    ms_graph = a.elapsed_time(b) / 1000
     # end to end: one generation from host state, result read back
     t0 = time.perf_counter()
     for _ in range(20):
@@ -103,6 +111,7 @@ def cfg0(out):
     e2e_ms = (time.perf_counter() - t0) / 20 * 1e3
     cpu_s = O.REF_FAST().ref_bench_de(0, P, D, 2000, 5, O.ptr(o), O.ptr(np.ascontiguousarray(m)), 42)
     out["config0"] = {"gpu_ms_per_generation": ms, "gpu_generations_per_s": 1e3 / ms,
+                      "gpu_graph_ms_per_generation": ms_graph, "gpu_graph_generations_per_s": 1e3 / ms_graph,
                       "gpu_e2e_ms_per_generation": e2e_ms, "kernels_per_generation": 5,
                       "cpu_reference_ms_per_generation": cpu_s / 2000 * 1e3, "cpu_cores": 1,
                       "cpu_sample": "build_de_fixed(0.5,0.9), 2000 generations, native stream"}
@@ -121,8 +130,7 @@ def cfg2(out):
         eng.reset()
         eng.init_population(pop, -100.0, 100.0, rng)
         evb.evaluate_batch(prob, pop, evb.EvalScratch(), fit)
-        for _ in range(G):
-            eng.generation(prob, pop, fit, -100.0, 100.0, rng)
+        eng.generations(prob, pop, fit, -100.0, 100.0, rng, G)
 
     run()
     torch.cuda.synchronize()

@@ -189,6 +189,11 @@ EVB_API int evb_de_p_count(evb_de e);
  * problem_instance::evaluate semantics.  s may be NULL (engine-owned scratch). */
 EVB_API int evb_de_generation(evb_de e, evb_problem objective, evb_scratch s, void* pop, int64_t ldp,
                               void* fitness, double lb, double ub, evb_rng rng, void* stream);
+/* n consecutive generations (identical to n evb_de_generation calls): the first runs eagerly,
+ * the rest replay a CUDA graph of one generation (the generation id and the word cursor are
+ * device-resident), removing per-kernel launch overhead for small populations. */
+EVB_API int evb_de_generations(evb_de e, evb_problem objective, evb_scratch s, void* pop, int64_t ldp,
+                               void* fitness, double lb, double ub, evb_rng rng, int n, void* stream);
 /* init_population (core/population.hpp:88-98) from the rng. */
 EVB_API int evb_de_init_population(evb_de e, void* pop, int64_t ldp, double lb, double ub, evb_rng rng,
                                    void* stream);

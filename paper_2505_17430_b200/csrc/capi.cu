@@ -259,6 +259,7 @@ int evb_problem_create_composition(int dtype, int dim, int n_comp, const int* ki
       fill_weights(p);
       p.n_comp = n_comp;
       p.comp_kinds = static_cast<int*>(upload(kinds, sizeof(int) * n_comp));
+      p.h_comp_kinds.assign(kinds, kinds + n_comp);
       p.comp_shift = upload_padded(shifts, n_comp, dim, p.ld, 64, es);
       // rotations: n_comp blocks of dim rows
       p.comp_rot = upload_padded(rotations, n_comp * dim, dim, p.ld, 0, es);

@@ -76,9 +76,21 @@ struct evb_de_s {
   void* mem_cr = nullptr;           // H
   evb_scratch_s* eval_scratch = nullptr;
   uint32_t last_gen = 0;
+  // CUDA graph of one generation (evb_de_generations), keyed by its arguments
+  cudaGraphExec_t graph = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  const void* g_key[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  double g_bounds[2] = {0, 0};
+  int g_kernels = 0;
 };
 
 namespace evb {
+
+__global__ void set_gen_kernel(uint32_t* p, uint32_t v) { *p = v; }
+void set_device_gen(evb_rng_s* r, cudaStream_t st) {
+  set_gen_kernel<<<1, 1, 0, st>>>(r->d_gen, r->gen);
+  count_launch();
+}
 
 namespace {
 
@@ -114,7 +126,7 @@ struct de_dev {
   T* mem_cr;
   T lb, ub;
   word_source src;
-  uint32_t gen;
+  uint32_t* gen_ptr;  // device generation counter (incremented by the apply kernel)
   int64_t* cursor;
   int* overflow;
 };
@@ -211,7 +223,8 @@ __global__ void de_draw_philox_kernel(const de_dev<T> d) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= d.P) return;
   const int arch_size = *d.arch_size;
-  word_reader r{&d.src, (uint64_t(d.gen) << 32) | uint32_t(i), 0, 0, d.overflow};
+  const uint32_t gen = *d.gen_ptr;
+  word_reader r{&d.src, (uint64_t(gen) << 32) | uint32_t(i), 0, 0, d.overflow};
   draw_scalars<T>(d, i, arch_size, r);
   d.woff[i] = r.count;  // gene uniforms start after the scalar words
   d.wcount[i] = r.count + d.D;
@@ -251,7 +264,7 @@ __global__ void de_trial_kernel(const de_dev<T> d) {
                                                                 : d.pop + size_t(c) * d.ldp;
   T* out = d.trial + size_t(i) * d.ldt;
   const int64_t s0 = d.woff[i];  // stream index of gene 0's uniform
-  const uint64_t ctr_hi = (uint64_t(d.gen) << 32) | uint32_t(i);
+  const uint64_t ctr_hi = (uint64_t(*d.gen_ptr) << 32) | uint32_t(i);
   const T lb = d.lb, ub = d.ub;
   // Philox blocks covering stream words [s0, s0 + D)
   const int64_t blk0 = s0 >> 1;
@@ -321,7 +334,7 @@ __global__ void __launch_bounds__(kSelThreads) de_select_scan_kernel(const de_de
   const int size0 = *d.arch_size;
   const int room = d.archive_cap - size0;
   const int64_t wpos = d.src.mode == RNG_WORDS ? *d.cursor : 0;
-  const uint64_t ctr_hi = (uint64_t(d.gen) << 32) | kSubArchive;
+  const uint64_t ctr_hi = (uint64_t(*d.gen_ptr) << 32) | kSubArchive;
   if (tid == 0) carry[0] = carry[1] = 0;
   __syncthreads();
   // pass 1: flags, exclusive prefix sums (pushes, successes), slot assignment
@@ -446,6 +459,7 @@ __global__ void __launch_bounds__(kSelThreads) de_select_scan_kernel(const de_de
 template <typename T>
 __global__ void de_select_apply_kernel(const de_dev<T> d) {
   const int i = blockIdx.x;
+  if (i == 0 && threadIdx.x == 0) *d.gen_ptr += 1u;  // last reader of this generation's id is done
   if (!d.win[i]) return;
   const int sl = d.arch_slot[i];
   T* x = d.pop + size_t(i) * d.ldp;
@@ -510,7 +524,7 @@ de_dev<T> make_dev(evb_de_s* e, void* pop, int64_t ldp, void* fit, double lb, do
   d.src.key = r->key;
   d.src.words = r->d_words;
   d.src.n_words = r->n_words;
-  d.gen = r->gen;
+  d.gen_ptr = r->d_gen;
   d.cursor = r->d_cursor;
   d.overflow = r->d_overflow;
   return d;
@@ -583,6 +597,7 @@ void init_population_t(evb_de_s* e, void* pop, int64_t ldp, double lb, double ub
     EVB_CUDA(cudaStreamSynchronize(st));
   } else {
     r->gen++;
+    set_device_gen(r, st);
   }
 }
 
@@ -616,6 +631,8 @@ void* dalloc(size_t n) {
 }
 
 void free_de(evb_de_s* e) {
+  if (e->graph) cudaGraphExecDestroy(e->graph);
+  if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
   void* ptrs[] = {e->trial, e->trial_fit, e->F, e->CR, e->slot, e->idx, e->jrand, e->woff, e->wcount, e->order,
                   e->win, e->arch_slot, e->owner, e->succ, e->archive, e->d_arch_size, e->d_write_index,
                   e->d_arch_words, e->mem_f, e->mem_cr};
@@ -650,6 +667,8 @@ int evb_rng_create_philox(uint64_t key, evb_rng* out) {
     auto* r = new evb_rng_s();
     r->mode = RNG_PHILOX;
     r->key = key;
+    EVB_CUDA(cudaMalloc(&r->d_gen, sizeof(uint32_t)));
+    EVB_CUDA(cudaMemset(r->d_gen, 0, sizeof(uint32_t)));
     EVB_CUDA(cudaMalloc(&r->d_overflow, sizeof(int)));
     EVB_CUDA(cudaMemset(r->d_overflow, 0, sizeof(int)));
     EVB_CUDA(cudaMalloc(&r->d_cursor, sizeof(int64_t)));
@@ -665,6 +684,8 @@ int evb_rng_create_words(const uint64_t* words, int64_t n_words, evb_rng* out) {
     auto* r = new evb_rng_s();
     r->mode = RNG_WORDS;
     r->n_words = n_words;
+    EVB_CUDA(cudaMalloc(&r->d_gen, sizeof(uint32_t)));
+    EVB_CUDA(cudaMemset(r->d_gen, 0, sizeof(uint32_t)));
     EVB_CUDA(cudaMalloc(&r->d_words, std::max<int64_t>(n_words, 1) * sizeof(uint64_t)));
     if (n_words) EVB_CUDA(cudaMemcpy(r->d_words, words, n_words * sizeof(uint64_t), cudaMemcpyHostToDevice));
     EVB_CUDA(cudaMalloc(&r->d_overflow, sizeof(int)));
@@ -681,6 +702,7 @@ int evb_rng_destroy(evb_rng r) {
     if (r->d_words) cudaFree(r->d_words);
     if (r->d_cursor) cudaFree(r->d_cursor);
     if (r->d_overflow) cudaFree(r->d_overflow);
+    if (r->d_gen) cudaFree(r->d_gen);
     delete r;
   });
 }
@@ -703,6 +725,8 @@ int evb_rng_set_generation(evb_rng r, uint32_t generation) {
   return guarded([&] {
     require(r != nullptr, "rng: null handle");
     r->gen = generation;
+    EVB_CUDA(cudaDeviceSynchronize());
+    EVB_CUDA(cudaMemcpy(r->d_gen, &generation, sizeof(uint32_t), cudaMemcpyHostToDevice));
   });
 }
 
@@ -821,6 +845,64 @@ int evb_de_generation(evb_de e, evb_problem objective, evb_scratch s, void* pop,
     if (ldp < e->D) throw invalid_argument("de_generation: ldp < dim");
     de_generation(e, &objective->p, s ? s : e->eval_scratch, pop, ldp, fitness, lb, ub, rng,
                   static_cast<cudaStream_t>(stream));
+  });
+}
+
+// n generations; after the first (which also sizes every buffer) one generation is captured into
+// a CUDA graph and replayed — the generation id and the WORDS cursor live on the device, so the
+// replays are exact continuations (identical to n calls of evb_de_generation).
+int evb_de_generations(evb_de e, evb_problem objective, evb_scratch s, void* pop, int64_t ldp, void* fitness,
+                       double lb, double ub, evb_rng rng, int n, void* stream) {
+  return guarded([&] {
+    require(e && objective && rng && pop && fitness, "de_generations: null argument");
+    require(n >= 0, "de_generations: negative count");
+    if (objective->p.dim != e->D) throw invalid_argument("de_generations: problem dimension mismatch");
+    if (objective->p.dtype != e->dtype) throw config_error("de_generations: problem dtype differs from engine");
+    if (ldp < e->D) throw invalid_argument("de_generations: ldp < dim");
+    if (n == 0) return;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    evb_scratch_s* sc = s ? s : e->eval_scratch;
+    de_generation(e, &objective->p, sc, pop, ldp, fitness, lb, ub, rng, st);
+    if (--n == 0) return;
+    const void* key[6] = {pop, fitness, objective, sc, rng, reinterpret_cast<const void*>(ldp)};
+    bool same = e->graph != nullptr && e->g_bounds[0] == lb && e->g_bounds[1] == ub;
+    for (int k = 0; k < 6 && same; ++k) same = e->g_key[k] == key[k];
+    if (!same) {
+      if (e->graph) {
+        EVB_CUDA(cudaGraphExecDestroy(e->graph));
+        e->graph = nullptr;
+      }
+      if (!e->cap_stream) EVB_CUDA(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
+      EVB_CUDA(cudaStreamSynchronize(st));
+      const uint32_t host_gen = rng->gen, host_last = e->last_gen;
+      const int k0 = last_launch_count();
+      cudaGraph_t g = nullptr;
+      EVB_CUDA(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        de_generation(e, &objective->p, sc, pop, ldp, fitness, lb, ub, rng, e->cap_stream);
+      } catch (...) {
+        cudaStreamEndCapture(e->cap_stream, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      EVB_CUDA(cudaStreamEndCapture(e->cap_stream, &g));
+      e->g_kernels = last_launch_count() - k0;
+      count_launch(-e->g_kernels);  // captured, not launched
+      rng->gen = host_gen;
+      e->last_gen = host_last;
+      const cudaError_t ie = cudaGraphInstantiate(&e->graph, g, 0);
+      cudaGraphDestroy(g);
+      EVB_CUDA(ie);
+      for (int k = 0; k < 6; ++k) e->g_key[k] = key[k];
+      e->g_bounds[0] = lb;
+      e->g_bounds[1] = ub;
+    }
+    for (int i = 0; i < n; ++i) {
+      EVB_CUDA(cudaGraphLaunch(e->graph, st));
+      e->last_gen = rng->gen;
+      rng->gen++;
+      count_launch(e->g_kernels);
+    }
   });
 }
 

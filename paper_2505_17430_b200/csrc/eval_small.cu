@@ -437,8 +437,7 @@ void dispatch_t(const eval_request& rq) {
   // composition, large D: per component z-store GEMM + component values, then combine
   ensure_buffer(reinterpret_cast<void**>(&sc->acc), &sc->acc_bytes, size_t(pr.n_comp) * P * sizeof(T), rq.stream);
   T* fk = reinterpret_cast<T*>(sc->acc);
-  std::vector<int> kinds(pr.n_comp);
-  EVB_CUDA(cudaMemcpy(kinds.data(), pr.comp_kinds, sizeof(int) * pr.n_comp, cudaMemcpyDeviceToHost));
+  const std::vector<int>& kinds = pr.h_comp_kinds;
   for (int c = 0; c < pr.n_comp; ++c) {
     const T* shift = static_cast<const T*>(pr.comp_shift) + size_t(c) * pr.ld;
     const T* rot = static_cast<const T*>(pr.comp_rot) + size_t(c) * D * pr.ld;

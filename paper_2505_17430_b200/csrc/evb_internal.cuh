@@ -96,6 +96,7 @@ struct device_problem {
   // composition (problems/instance.hpp:33-41, 116-174)
   int n_comp = 0;
   int* comp_kinds = nullptr;
+  std::vector<int> h_comp_kinds;  // host copy (no device->host read on the evaluation path)
   void* comp_shift = nullptr;  // n_comp x ld
   void* comp_rot = nullptr;    // n_comp x dim x ld
   double* comp_sigma = nullptr;
@@ -117,7 +118,8 @@ struct evb_rng_s {
   uint64_t* d_words = nullptr;
   int64_t n_words = 0;
   int64_t* d_cursor = nullptr;  // WORDS: next unread word (device-resident)
-  uint32_t gen = 0;             // PHILOX: generation counter (host)
+  uint32_t gen = 0;             // PHILOX: generation counter (host mirror)
+  uint32_t* d_gen = nullptr;    // PHILOX: generation counter read by the kernels (graph-replayable)
   int* d_overflow = nullptr;
 };
 
@@ -184,6 +186,9 @@ struct eval_request {
 };
 
 void eval_dispatch(const eval_request& rq);
+
+// device generation counter <- host mirror (after host-side Philox consumers such as init)
+void set_device_gen(evb_rng_s* r, cudaStream_t st);
 
 // Number of kernel launches issued by the last eval_dispatch on this thread (bench accounting).
 int last_launch_count();

@@ -115,7 +115,7 @@ struct pso_dev {
   int clamp;
   T lb, ub;
   word_source src;
-  uint32_t gen;
+  const uint32_t* gen_ptr;
   int64_t base;  // WORDS: list position of this generation's first word
   int* overflow;
 };
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(256) pso_update_kernel(const pso_dev<T> d) {
   if (j >= d.D) return;
   uint64_t w0, w1;
   if (d.src.mode == RNG_PHILOX) {
-    philox_pair(d.src.key, (uint64_t(d.gen) << 32) | uint32_t(i), uint64_t(j), w0, w1);
+    philox_pair(d.src.key, (uint64_t(*d.gen_ptr) << 32) | uint32_t(i), uint64_t(j), w0, w1);
   } else {
     const int64_t n = d.base + (int64_t(i) * d.D + j) * 2;
     w0 = word_at(d.src, 0, n, d.overflow);
@@ -165,8 +165,9 @@ __global__ void __launch_bounds__(256) pso_update_kernel(const pso_dev<T> d) {
 // particle's fitness into the caller's fitness vector.
 template <typename T>
 __global__ void pso_pbest_kernel(const T* __restrict__ x, int64_t ldx, const T* __restrict__ fnew, T* fit, T* pb,
-                                 int64_t ldb, T* pbf, int D) {
+                                 int64_t ldb, T* pbf, int D, uint32_t* gen) {
   const int i = blockIdx.x;
+  if (i == 0 && threadIdx.x == 0) *gen += 1u;  // the update kernel (last reader) has finished
   const T f = fnew[i];
   if (threadIdx.x == 0) fit[i] = f;
   if (!(f < pbf[i])) return;
@@ -222,7 +223,7 @@ void generation_t(evb_pso_s* s, const device_problem* prob, evb_scratch_s* sc, v
   d.lb = T(lb);
   d.ub = T(ub);
   d.src = word_source{r->mode, r->key, r->d_words, r->n_words};
-  d.gen = r->gen;
+  d.gen_ptr = r->d_gen;
   d.overflow = r->d_overflow;
   if (r->mode == RNG_WORDS) d.base = words_cursor(r, st);
   dim3 grid((s->D + 255) / 256, s->P);
@@ -246,7 +247,7 @@ void generation_t(evb_pso_s* s, const device_problem* prob, evb_scratch_s* sc, v
   eval_dispatch(rq);
   pso_pbest_kernel<T><<<s->P, std::min(256, int(round_up(s->D, 32))), 0, st>>>(
       static_cast<const T*>(X), ldx, static_cast<const T*>(s->fit_new), static_cast<T*>(fit),
-      static_cast<T*>(s->pbest), s->ldb, static_cast<T*>(s->pbest_fit), s->D);
+      static_cast<T*>(s->pbest), s->ldb, static_cast<T*>(s->pbest_fit), s->D, r->d_gen);
   count_launch();
   EVB_CUDA(cudaGetLastError());
   s->last_gen = r->gen;
@@ -375,8 +376,12 @@ int evb_pso_init_uniform(evb_pso s, void* A, int64_t lda, double lo, double hi, 
                                                          base, r->d_overflow);
     count_launch();
     EVB_CUDA(cudaGetLastError());
-    if (r->mode == RNG_WORDS) words_advance(r, base + int64_t(s->P) * s->D, st);
-    else r->gen++;
+    if (r->mode == RNG_WORDS) {
+      words_advance(r, base + int64_t(s->P) * s->D, st);
+    } else {
+      r->gen++;
+      set_device_gen(r, st);
+    }
   });
 }
 

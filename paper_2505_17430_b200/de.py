@@ -96,6 +96,7 @@ def _sigs():
         "evb_de_p_count": (c_int, [vp]),
         "evb_de_generation": (c_int, [vp, vp, vp, vp, i64, vp, c_double, c_double, vp, vp]),
         "evb_de_init_population": (c_int, [vp, vp, i64, c_double, c_double, vp, vp]),
+        "evb_de_generations": (c_int, [vp, vp, vp, vp, i64, vp, c_double, c_double, vp, c_int, vp]),
         "evb_de_optimize": (c_int, [vp, vp, vp, vp, i64, vp, c_double, c_double, i64, vp, P(c_int), P(c_double),
                                     P(c_int), vp]),
         "evb_de_get_state": (c_int, [vp, vp, P(c_int), vp, vp, P(c_int)]),
@@ -200,6 +201,13 @@ class DEEngine:
         p, ld, f = self._pop(pop, fitness)
         check(_lib.lib().evb_de_generation(self._h, problem.handle, scratch.handle if scratch else None, p, ld, f,
                                            lb, ub, rng.handle, _stream_ptr(stream)), "de_generation")
+
+    def generations(self, problem: ProblemInstance, pop, fitness, lb: float, ub: float, rng: Rng, n: int,
+                    scratch: EvalScratch | None = None, stream=None) -> None:
+        """n consecutive generations; after the first, a CUDA graph of one generation is replayed."""
+        p, ld, f = self._pop(pop, fitness)
+        check(_lib.lib().evb_de_generations(self._h, problem.handle, scratch.handle if scratch else None, p, ld, f,
+                                            lb, ub, rng.handle, n, _stream_ptr(stream)), "de_generations")
 
     def init_population(self, pop, lb: float, ub: float, rng: Rng, stream=None) -> None:
         check(_lib.lib().evb_de_init_population(self._h, ctypes.c_void_p(pop.data_ptr()), pop.stride(0), lb, ub,

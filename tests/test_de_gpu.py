@@ -208,3 +208,30 @@ def test_large_population_properties(dev):
         donor = np.clip(x0n[a] + 0.5 * (x0n[b] - x0n[c]), -100, 100)
         if not np.array_equal(popn[i], x0n[i]):
             assert np.all((popn[i] == x0n[i]) | (popn[i] == donor)), i
+
+
+@pytest.mark.parametrize("mode", ["philox", "words"])
+def test_graph_generations_equal_eager(dev, mode):
+    # evb_de_generations (CUDA-graph replay) == the same number of eager generations, bit for bit
+    P, D, G = 180, 100, 25
+    o, m = O.shift_rotation(11, D)
+    prob = evb.ProblemInstance.base(evb.BaseKind.ackley, o, m, 0.0)
+    words = O.rng_words(11, 0, P * D + G * P * (D + 40) * 2)
+    results = []
+    for use_graph in (False, True):
+        eng = DEEngine(preset_shade(0.11, P, 1.0), P, D)
+        rng = Rng.philox(11) if mode == "philox" else Rng.words(words)
+        pop = torch.empty((P, D), dtype=torch.float64, device=dev)
+        eng.init_population(pop, -100.0, 100.0, rng)
+        fit = dev_eval(prob, pop, dev)
+        if use_graph:
+            eng.generations(prob, pop, fit, -100.0, 100.0, rng, G)
+        else:
+            for _ in range(G):
+                eng.generation(prob, pop, fit, -100.0, 100.0, rng)
+        torch.cuda.synchronize()
+        results.append((pop.cpu().numpy(), fit.cpu().numpy(), eng.get_state(), rng.state()))
+    (p0, f0, s0, r0), (p1, f1, s1, r1) = results
+    assert np.array_equal(p0, p1) and np.array_equal(f0, f1)
+    assert np.array_equal(s0["archive"], s1["archive"]) and np.array_equal(s0["memory_f"], s1["memory_f"])
+    assert r0["cursor"] == r1["cursor"] and r0["generation"] == r1["generation"]
