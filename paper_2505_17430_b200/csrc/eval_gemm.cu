@@ -26,6 +26,8 @@
 
 #include <algorithm>
 #include <cstring>
+#include <cstdlib>
+#include <string>
 #include <type_traits>
 
 #include "evb_internal.cuh"
@@ -115,7 +117,7 @@ struct epilogue_flag {
 
 template <typename T, int BM, int BN>
 __device__ void tile_epilogue(const fused_params<T>& p, const T* zt, int ldt, int m0, int n0, int tid, int nthreads,
-                              int* last_flag) {
+                              int* last_flag, int mtile, int ntile, int bar_id) {
   using F = fop<T>;
   const int warp = tid >> 5, lane = tid & 31, nwarps = nthreads >> 5;
   if (p.zbuf) {
@@ -146,16 +148,16 @@ __device__ void tile_epilogue(const fused_params<T>& p, const T* zt, int ldt, in
         const T o = __shfl_xor_sync(0xffffffffu, s, off);
         s = prod ? F::mul(s, o) : F::add(s, o);
       }
-      if (lane == 0 && row < p.P) p.partial[(size_t(ch) * p.n_ntiles + blockIdx.y) * p.P + row] = s;
+      if (lane == 0 && row < p.P) p.partial[(size_t(ch) * p.n_ntiles + ntile) * p.P + row] = s;
     }
   }
   __threadfence();
-  ptx::named_bar_sync(1, nthreads);
+  ptx::named_bar_sync(bar_id, nthreads);
   if (tid == 0) {
-    const unsigned ticket = atomicAdd(&p.counters[blockIdx.x], 1u);
+    const unsigned ticket = atomicAdd(&p.counters[mtile], 1u);
     *last_flag = (ticket == unsigned(p.n_ntiles - 1)) ? 1 : 0;
   }
-  ptx::named_bar_sync(1, nthreads);
+  ptx::named_bar_sync(bar_id, nthreads);
   if (!*last_flag) return;
   __threadfence();
   for (int r = tid; r < BM; r += nthreads) {
@@ -178,7 +180,7 @@ __device__ void tile_epilogue(const fused_params<T>& p, const T* zt, int ldt, in
       p.out[o * p.ldo + row] = finalize<T>(p.out_kind[o], s0, s1, p.D, T(p.out_bias[o]));
     }
   }
-  if (tid == 0) p.counters[blockIdx.x] = 0u;  // re-arm for the next launch
+  if (tid == 0) p.counters[mtile] = 0u;  // re-arm for the next launch
 }
 
 // byte offset of element (r, kk) inside a SWIZZLE_128B tile whose rows are 128 bytes
@@ -294,7 +296,149 @@ __global__ void __launch_bounds__(f64_cfg<BM, BN, WM, WN, STAGES>::THREADS, 1)
 #pragma unroll
       for (int h = 0; h < 2; ++h) zt[(rA + i * 8 + g) * LDT + rB + j * 8 + 2 * t + h] = acc[i][j][h];
   ptx::named_bar_sync(1, C::NCW * 32);
-  tile_epilogue<double, BM, BN>(p, zt, LDT, m0, n0, threadIdx.x, C::NCW * 32, last_flag);
+  tile_epilogue<double, BM, BN>(p, zt, LDT, m0, n0, threadIdx.x, C::NCW * 32, last_flag, blockIdx.x, blockIdx.y, 1);
+}
+
+// ---------------------------------------------------------------------------------------
+// K1 (persistent): one CTA per SM walks a static list of BM x BN tiles.  Warp roles:
+//   warps 0-3  MMA      (warp tile 16 x 56: 14 DMMA m8n8k4 per k4 step, 1 per SMSP)
+//   warps 4-7  epilogue (transform terms + row sums of the previous tile, from smem)
+//   warp  8    producer (TMA ring of 16-double K-slices, continuous across tiles)
+// The accumulator tile is handed to the epilogue warps through one of two smem buffers
+// (acc_full / acc_empty mbarriers), so a tile's epilogue overlaps the next tile's mainloop and
+// only the CTA's last epilogue is exposed.  With 64 x 56 tiles, D = 1000 and P = 1024 give 288
+// tiles = 2 per SM (140 SMs) — the same per-SM work as one 64 x 112 tile, minus the epilogue.
+template <int BM, int BN, int STAGES>
+struct f64p_cfg {
+  static constexpr int KB = 16;
+  static constexpr int NMW = 4;  // MMA warps, stacked along M
+  static constexpr int NEW = 4;  // epilogue warps
+  static constexpr int THREADS = (NMW + NEW + 1) * 32;
+  static constexpr int WTM = BM / NMW;
+  static constexpr int TM = WTM / 8, TN = BN / 8;
+  static constexpr int A_BYTES = BM * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int O_BYTES = 128;
+  static constexpr int STAGE_BYTES = ((A_BYTES + B_BYTES + O_BYTES + 1023) / 1024) * 1024;
+  static constexpr int LDT = BN + 1;
+  static constexpr int EBUF_BYTES = BM * LDT * 8;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * EBUF_BYTES + 1024 + (2 * STAGES + 4) * 8 + 64;
+  static_assert(WTM % 8 == 0 && BN % 8 == 0, "tile must be a multiple of 8");
+};
+
+template <int BM, int BN, int STAGES>
+__global__ void __launch_bounds__(f64p_cfg<BM, BN, STAGES>::THREADS, 1)
+    eval_f64_dmma_persistent(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmM,
+                             const fused_params<double> p, int n_mtiles, int n_tiles) {
+  using C = f64p_cfg<BM, BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  double* ebuf = reinterpret_cast<double*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES + 2 * C::EBUF_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;  // [2]
+  uint64_t* acc_empty = acc_full + 2;   // [2]
+  int* last_flag = reinterpret_cast<int*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int KT = (p.D + C::KB - 1) / C::KB;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], C::NMW);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&acc_full[b], C::NMW * 32);
+      ptx::mbar_init(&acc_empty[b], C::NEW * 32);
+    }
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == C::NMW + C::NEW) {
+    // ---------------- producer ----------------
+    if (lane == 0) {
+      ptx::prefetch_tma(&tmX);
+      ptx::prefetch_tma(&tmM);
+      int it = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int m0 = (tile % n_mtiles) * BM, n0 = (tile / n_mtiles) * BN;
+        for (int kb = 0; kb < KT; ++kb, ++it) {
+          const int s = it % STAGES;
+          if (it >= STAGES) ptx::mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+          uint8_t* st = smem + s * C::STAGE_BYTES;
+          ptx::mbar_arrive_expect_tx(&full[s], C::A_BYTES + C::B_BYTES + C::O_BYTES);
+          ptx::tma_load_2d(st, &tmX, &full[s], kb * C::KB, m0);
+          ptx::tma_load_2d(st + C::A_BYTES, &tmM, &full[s], kb * C::KB, n0);
+          ptx::bulk_load(st + C::A_BYTES + C::B_BYTES, p.shift + size_t(kb) * C::KB, C::O_BYTES, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  if (warp >= C::NMW) {
+    // ---------------- epilogue warps ----------------
+    const int etid = threadIdx.x - C::NMW * 32;
+    int local = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++local) {
+      const int b = local & 1;
+      ptx::mbar_wait(&acc_full[b], (local >> 1) & 1);
+      const int mt = tile % n_mtiles, nt = tile / n_mtiles;
+      tile_epilogue<double, BM, BN>(p, ebuf + b * (BM * C::LDT), C::LDT, mt * BM, nt * BN, etid, C::NEW * 32,
+                                    last_flag, mt, nt, 2);
+      ptx::mbar_arrive(&acc_empty[b]);
+    }
+    return;
+  }
+
+  // ---------------- MMA warps ----------------
+  const int g = lane >> 2, t = lane & 3;
+  const int rA = warp * C::WTM;
+  const uint32_t smem_base = ptx::smem_u32(smem);
+  int it = 0, local = 0;
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++local) {
+    double acc[C::TM][C::TN][2];
+#pragma unroll
+    for (int i = 0; i < C::TM; ++i)
+#pragma unroll
+      for (int j = 0; j < C::TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int kb = 0; kb < KT; ++kb, ++it) {
+      const int s = it % STAGES;
+      ptx::mbar_wait(&full[s], (it / STAGES) & 1);
+      const uint32_t sA = smem_base + s * C::STAGE_BYTES;
+      const uint32_t sB = sA + C::A_BYTES;
+      const uint32_t sO = sB + C::B_BYTES;
+#pragma unroll
+      for (int ks = 0; ks < C::KB / 4; ++ks) {
+        const int kk = ks * 4 + t;
+        const double o = ptx::lds_f64(sO + kk * 8);
+        double a[C::TM], bf[C::TN];
+#pragma unroll
+        for (int i = 0; i < C::TM; ++i) a[i] = __dsub_rn(ptx::lds_f64(sA + swz<8>(rA + i * 8 + g, kk)), o);
+#pragma unroll
+        for (int j = 0; j < C::TN; ++j) bf[j] = ptx::lds_f64(sB + swz<8>(j * 8 + g, kk));
+#pragma unroll
+        for (int i = 0; i < C::TM; ++i)
+#pragma unroll
+          for (int j = 0; j < C::TN; ++j) ptx::dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], bf[j]);
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&empty[s]);
+    }
+    // hand the tile to the epilogue warps
+    const int b = local & 1;
+    if (local >= 2) ptx::mbar_wait(&acc_empty[b], ((local >> 1) - 1) & 1);
+    double* zt = ebuf + b * (BM * C::LDT);
+#pragma unroll
+    for (int i = 0; i < C::TM; ++i)
+#pragma unroll
+      for (int j = 0; j < C::TN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) zt[(rA + i * 8 + g) * C::LDT + j * 8 + 2 * t + h] = acc[i][j][h];
+    ptx::mbar_arrive(&acc_full[b]);
+  }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -407,7 +551,7 @@ __global__ void __launch_bounds__(f32_cfg<BM, BN, STAGES>::THREADS, 1)
 #pragma unroll
     for (int j = 0; j < 8; ++j) zt[(ty + C::TY * i) * LDT + tx + C::TX * j] = acc[i][j];
   ptx::named_bar_sync(1, C::NCT);
-  tile_epilogue<float, BM, BN>(p, zt, LDT, m0, n0, tid, C::NCT, last_flag);
+  tile_epilogue<float, BM, BN>(p, zt, LDT, m0, n0, tid, C::NCT, last_flag, blockIdx.x, blockIdx.y, 1);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -459,6 +603,16 @@ bool build_plan(fused_params<T>& fp, int n_out, const int* kinds, const double* 
   return true;
 }
 
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    EVB_CUDA(cudaGetDevice(&dev));
+    EVB_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
 // Tile configurations, chosen per problem shape to minimise wave quantisation on the SMs.
 // fp64: (BM, BN, WM, WN); warp tile (BM/WM) x (BN/WN).
 constexpr int kStages64 = 6;
@@ -480,6 +634,25 @@ void launch_f64(const CUtensorMap& tmX, const CUtensorMap& tmM, const fused_para
 }
 
 template <int BM, int BN>
+void launch_f64_persistent(const CUtensorMap& tmX, const CUtensorMap& tmM, const fused_params<double>& fp,
+                           cudaStream_t st) {
+  constexpr int STAGES = 8;
+  using C = f64p_cfg<BM, BN, STAGES>;
+  auto kern = eval_f64_dmma_persistent<BM, BN, STAGES>;
+  static bool attr = false;
+  if (!attr) {
+    EVB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  const int n_mtiles = (fp.P + BM - 1) / BM;
+  const int n_tiles = n_mtiles * ((fp.D + BN - 1) / BN);
+  const int grid = std::min(n_tiles, sm_count());
+  kern<<<grid, C::THREADS, C::SMEM, st>>>(tmX, tmM, fp, n_mtiles, n_tiles);
+  EVB_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+template <int BM, int BN>
 void launch_f32(const CUtensorMap& tmX, const CUtensorMap& tmM, const fused_params<float>& fp, cudaStream_t st) {
   using C = f32_cfg<BM, BN, kStages32>;
   auto kern = eval_f32_ffma_kernel<BM, BN, kStages32>;
@@ -494,15 +667,6 @@ void launch_f32(const CUtensorMap& tmX, const CUtensorMap& tmM, const fused_para
   count_launch();
 }
 
-int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    EVB_CUDA(cudaGetDevice(&dev));
-    EVB_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
-  }
-  return n;
-}
 
 // cost model: waves * tile area (one CTA per SM for every config)
 double tile_cost(int64_t P, int D, int BM, int BN) {
@@ -535,6 +699,13 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
   constexpr int KB = std::is_same<T, double>::value ? 16 : 32;
 
   int BM, BN;
+  bool use_persistent = false;
+  if constexpr (std::is_same<T, double>::value) {
+    // persistent overlapped-epilogue kernel once there are at least as many 64 x 56 tiles as SMs
+    static const char* force = std::getenv("EVB_F64_KERNEL");
+    const int ptiles = int(((P + 63) / 64) * ((D + 55) / 56));
+    use_persistent = force ? std::string(force) == "persistent" : ptiles >= sm_count();
+  }
   if constexpr (std::is_same<T, double>::value) {
     // pick the tile with the least wave-quantised cost
     const int cands[3][2] = {{64, 112}, {64, 128}, {32, 128}};
@@ -549,6 +720,10 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
     }
     BM = cands[best][0];
     BN = cands[best][1];
+    if (use_persistent) {
+      BM = 64;
+      BN = 56;
+    }
   } else {
     BM = 64;
     BN = 128;
@@ -574,6 +749,10 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
     fp.counters = sc->counters;
   }
   if constexpr (std::is_same<T, double>::value) {
+    if (use_persistent) {
+      launch_f64_persistent<64, 56>(tmX, tmM, fp, rq.stream);
+      return;
+    }
     if (BM == 64 && BN == 112) launch_f64<64, 112, 4, 2>(tmX, tmM, fp, rq.stream);
     else if (BM == 64 && BN == 128) launch_f64<64, 128, 4, 2>(tmX, tmM, fp, rq.stream);
     else launch_f64<32, 128, 2, 4>(tmX, tmM, fp, rq.stream);
