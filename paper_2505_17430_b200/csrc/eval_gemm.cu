@@ -132,23 +132,44 @@ __device__ void tile_epilogue(const fused_params<T>& p, const T* zt, int ldt, in
     }
     return;
   }
-  for (int r = warp; r < BM; r += nwarps) {
-    const int row = m0 + r;
-    for (int ch = 0; ch < p.n_ch; ++ch) {
-      const int term = p.ch_term[ch];
-      const bool prod = term_is_product(term);
-      const T ident = prod ? T(1) : T(0);
-      T s = ident;
-      for (int c = lane; c < BN; c += 32) {
-        const int col = n0 + c;
-        const T v = col < p.D ? term_value<T>(term, zt[r * ldt + c], col, p.ell_w) : ident;
-        s = prod ? F::mul(s, v) : F::add(s, v);
+  // Each warp owns rows warp, warp + nwarps, ...; per channel every lane evaluates all of its
+  // (row, column) terms before any shuffle, so the transcendental chains of up to 4 x RPW elements
+  // are independent (ILP) instead of one row at a time.
+  constexpr int CPL = (BN + 31) / 32;  // columns per lane
+  const int rpw = (BM + nwarps - 1) / nwarps;
+  for (int ch = 0; ch < p.n_ch; ++ch) {
+    const int term = p.ch_term[ch];
+    const bool prod = term_is_product(term);
+    const T ident = prod ? T(1) : T(0);
+    for (int r0 = 0; r0 < rpw; r0 += 8) {
+      T s[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int r = warp + (r0 + q) * nwarps;
+        s[q] = ident;
+        if (r0 + q < rpw && r < BM) {
+#pragma unroll
+          for (int cc = 0; cc < CPL; ++cc) {
+            const int c = lane + 32 * cc;
+            const int col = n0 + c;
+            if (c < BN) {
+              const T v = col < p.D ? term_value<T>(term, zt[r * ldt + c], col, p.ell_w) : ident;
+              s[q] = prod ? F::mul(s[q], v) : F::add(s[q], v);
+            }
+          }
+        }
       }
-      for (int off = 16; off > 0; off >>= 1) {
-        const T o = __shfl_xor_sync(0xffffffffu, s, off);
-        s = prod ? F::mul(s, o) : F::add(s, o);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        for (int off = 16; off > 0; off >>= 1) {
+          const T o = __shfl_xor_sync(0xffffffffu, s[q], off);
+          s[q] = prod ? F::mul(s[q], o) : F::add(s[q], o);
+        }
+        const int r = warp + (r0 + q) * nwarps;
+        const int row = m0 + r;
+        if (lane == 0 && r0 + q < rpw && r < BM && row < p.P)
+          p.partial[(size_t(ch) * p.n_ntiles + ntile) * p.P + row] = s[q];
       }
-      if (lane == 0 && row < p.P) p.partial[(size_t(ch) * p.n_ntiles + ntile) * p.P + row] = s;
     }
   }
   __threadfence();
@@ -208,8 +229,8 @@ struct f64_cfg {
   static_assert(BM * (BN + 1) * 8 <= STAGES * STAGE_BYTES, "epilogue tile must fit the stage ring");
 };
 
-template <int BM, int BN, int WM, int WN, int STAGES>
-__global__ void __launch_bounds__(f64_cfg<BM, BN, WM, WN, STAGES>::THREADS, 1)
+template <int BM, int BN, int WM, int WN, int STAGES, int MINB = 1>
+__global__ void __launch_bounds__(f64_cfg<BM, BN, WM, WN, STAGES>::THREADS, MINB)
     eval_f64_dmma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmM,
                          const fused_params<double> p) {
   using C = f64_cfg<BM, BN, WM, WN, STAGES>;
@@ -301,17 +322,17 @@ __global__ void __launch_bounds__(f64_cfg<BM, BN, WM, WN, STAGES>::THREADS, 1)
 
 // ---------------------------------------------------------------------------------------
 // K1 (persistent): one CTA per SM walks a static list of BM x BN tiles.  Warp roles:
-//   warps 0-3  MMA      (warp tile 16 x 56: 14 DMMA m8n8k4 per k4 step, 1 per SMSP)
-//   warps 4-7  epilogue (transform terms + row sums of the previous tile, from smem)
-//   warp  8    producer (TMA ring of 16-double K-slices, continuous across tiles)
+//   warps 0-7   MMA      (warp tile 8 x 56: 7 DMMA m8n8k4 per k4 step, 2 warps per SMSP)
+//   warps 8-11  epilogue (transform terms + row sums of the previous tile, from smem)
+//   warp  12    producer (TMA ring of 16-double K-slices, continuous across tiles)
 // The accumulator tile is handed to the epilogue warps through one of two smem buffers
 // (acc_full / acc_empty mbarriers), so a tile's epilogue overlaps the next tile's mainloop and
 // only the CTA's last epilogue is exposed.  With 64 x 56 tiles, D = 1000 and P = 1024 give 288
 // tiles = 2 per SM (140 SMs) — the same per-SM work as one 64 x 112 tile, minus the epilogue.
-template <int BM, int BN, int STAGES>
+template <int BM, int BN, int STAGES, int NMW_ = 8>
 struct f64p_cfg {
   static constexpr int KB = 16;
-  static constexpr int NMW = 4;  // MMA warps, stacked along M
+  static constexpr int NMW = NMW_;  // MMA warps, stacked along M (2 per SMSP by default)
   static constexpr int NEW = 4;  // epilogue warps
   static constexpr int THREADS = (NMW + NEW + 1) * 32;
   static constexpr int WTM = BM / NMW;
@@ -618,10 +639,10 @@ int sm_count() {
 constexpr int kStages64 = 6;
 constexpr int kStages32 = 4;
 
-template <int BM, int BN, int WM, int WN>
+template <int BM, int BN, int WM, int WN, int STAGES = kStages64, int MINB = 1>
 void launch_f64(const CUtensorMap& tmX, const CUtensorMap& tmM, const fused_params<double>& fp, cudaStream_t st) {
-  using C = f64_cfg<BM, BN, WM, WN, kStages64>;
-  auto kern = eval_f64_dmma_kernel<BM, BN, WM, WN, kStages64>;
+  using C = f64_cfg<BM, BN, WM, WN, STAGES>;
+  auto kern = eval_f64_dmma_kernel<BM, BN, WM, WN, STAGES, MINB>;
   static bool attr = false;
   if (!attr) {
     EVB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -700,24 +721,29 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
 
   int BM, BN;
   bool use_persistent = false;
+  // EVB_F64_KERNEL=persistent|pair|classic overrides the shape choice (A/B measurements)
+  static const char* force = std::getenv("EVB_F64_KERNEL");
+  if constexpr (std::is_same<T, double>::value) use_persistent = force && std::string(force) == "persistent";
   if constexpr (std::is_same<T, double>::value) {
-    // persistent overlapped-epilogue kernel once there are at least as many 64 x 56 tiles as SMs
-    static const char* force = std::getenv("EVB_F64_KERNEL");
-    const int ptiles = int(((P + 63) / 64) * ((D + 55) / 56));
-    use_persistent = force ? std::string(force) == "persistent" : ptiles >= sm_count();
-  }
-  if constexpr (std::is_same<T, double>::value) {
-    // pick the tile with the least wave-quantised cost
-    const int cands[3][2] = {{64, 112}, {64, 128}, {32, 128}};
+    // pick the tile with the least wave-quantised cost; {64, 56} runs 2 CTAs per SM so one CTA's
+    // epilogue overlaps the other's DMMA mainloop (preferred on ties)
+    const int cands[4][2] = {{64, 56}, {64, 112}, {64, 128}, {32, 128}};
+    const int per_sm[4] = {2, 1, 1, 1};
     int best = 0;
     double bc = 1e300;
-    for (int c = 0; c < 3; ++c) {
-      const double v = tile_cost(P, D, cands[c][0], cands[c][1]) * (cands[c][0] == 32 ? 1.08 : 1.0);
+    for (int c = 0; c < 4; ++c) {
+      const int64_t ctas = ((P + cands[c][0] - 1) / cands[c][0]) * ((D + cands[c][1] - 1) / cands[c][1]);
+      const int64_t waves = (ctas + int64_t(sm_count()) * per_sm[c] - 1) / (int64_t(sm_count()) * per_sm[c]);
+      double v = double(waves) * per_sm[c] * cands[c][0] * cands[c][1];
+      if (cands[c][0] == 32) v *= 1.08;
+      if (per_sm[c] == 2) v *= 0.97;  // overlap bonus
       if (v < bc) {
         bc = v;
         best = c;
       }
     }
+    if (force && std::string(force) == "classic" && best == 0) best = 1;
+    if (force && std::string(force) == "pair") best = 0;
     BM = cands[best][0];
     BN = cands[best][1];
     if (use_persistent) {
@@ -753,7 +779,8 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
       launch_f64_persistent<64, 56>(tmX, tmM, fp, rq.stream);
       return;
     }
-    if (BM == 64 && BN == 112) launch_f64<64, 112, 4, 2>(tmX, tmM, fp, rq.stream);
+    if (BM == 64 && BN == 56) launch_f64<64, 56, 4, 1, 6, 2>(tmX, tmM, fp, rq.stream);
+    else if (BM == 64 && BN == 112) launch_f64<64, 112, 4, 2>(tmX, tmM, fp, rq.stream);
     else if (BM == 64 && BN == 128) launch_f64<64, 128, 4, 2>(tmX, tmM, fp, rq.stream);
     else launch_f64<32, 128, 2, 4>(tmX, tmM, fp, rq.stream);
   } else {
