@@ -80,7 +80,7 @@ void fill_weights(device_problem& p) {
 
 void free_problem(device_problem& p) {
   void* ptrs[] = {p.shift, p.rotation, p.ell_w, p.hyb_w, p.perm, p.sub_kinds, p.chunk_sizes, p.comp_kinds,
-                  p.comp_shift, p.comp_rot, p.comp_sigma, p.comp_lambda, p.comp_bias};
+                  p.comp_shift, p.comp_rot, p.comp_sigma, p.comp_lambda, p.comp_bias, p.rot_hi, p.rot_lo};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -296,7 +296,7 @@ int evb_scratch_create(evb_scratch* out) {
 int evb_scratch_destroy(evb_scratch s) {
   return guarded([&] {
     if (!s) return;
-    void* ptrs[] = {s->partial, s->counters, s->zbuf, s->xpad, s->dx, s->dout, s->acc};
+    void* ptrs[] = {s->partial, s->counters, s->zbuf, s->xpad, s->dx, s->dout, s->acc, s->s_hi, s->s_lo};
     for (void* q : ptrs)
       if (q) cudaFree(q);
     if (s->own_stream) cudaStreamDestroy(s->own_stream);

@@ -33,6 +33,7 @@
 #include "evb_internal.cuh"
 #include "evb_math.cuh"
 #include "ptx.cuh"
+#include "umma.cuh"
 
 namespace evb {
 
@@ -463,6 +464,167 @@ __global__ void __launch_bounds__(f64p_cfg<BM, BN, STAGES>::THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------------------
+// K2 on tcgen05 (see umma.cuh): 3xTF32, 128 x BN tile per CTA, accumulator in TMEM.
+template <int BN>
+struct umma_cfg {
+  static constexpr int BM = 128;
+  static constexpr int KB = 32;  // floats per K-slice (one 128-byte swizzle row)
+  static constexpr int STAGES = 4;
+  static constexpr int A_BYTES = BM * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // hi + lo of both operands
+  static constexpr int THREADS = 6 * 32;
+  static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + (2 * STAGES + 1) * 8 + 64;
+  static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
+};
+
+template <int BN>
+__global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
+    eval_f32_umma_kernel(const __grid_constant__ CUtensorMap tmShi, const __grid_constant__ CUtensorMap tmSlo,
+                         const __grid_constant__ CUtensorMap tmMhi, const __grid_constant__ CUtensorMap tmMlo,
+                         const fused_params<float> p) {
+  using C = umma_cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* accfull = empty + C::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accfull + 1);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * C::BM, n0 = blockIdx.y * BN;
+  const int KT = (p.D + C::KB - 1) / C::KB;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    ptx::mbar_init(accfull, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) umma::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer ----------------
+      ptx::prefetch_tma(&tmShi);
+      ptx::prefetch_tma(&tmSlo);
+      ptx::prefetch_tma(&tmMhi);
+      ptx::prefetch_tma(&tmMlo);
+      for (int kb = 0; kb < KT; ++kb) {
+        const int s = kb % C::STAGES;
+        if (kb >= C::STAGES) ptx::mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
+        uint8_t* st = smem + s * C::STAGE_BYTES;
+        ptx::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
+        ptx::tma_load_2d(st, &tmShi, &full[s], kb * C::KB, m0);
+        ptx::tma_load_2d(st + C::A_BYTES, &tmSlo, &full[s], kb * C::KB, m0);
+        ptx::tma_load_2d(st + 2 * C::A_BYTES, &tmMhi, &full[s], kb * C::KB, n0);
+        ptx::tma_load_2d(st + 2 * C::A_BYTES + C::B_BYTES, &tmMlo, &full[s], kb * C::KB, n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- single-thread MMA issuer ----------------
+      constexpr uint32_t idesc = umma::idesc_tf32(C::BM, BN);
+      const uint32_t base = ptx::smem_u32(smem);
+      for (int kb = 0; kb < KT; ++kb) {
+        const int s = kb % C::STAGES;
+        ptx::mbar_wait(&full[s], (kb / C::STAGES) & 1);
+        umma::fence_after();
+        const uint32_t sa_hi = base + s * C::STAGE_BYTES, sa_lo = sa_hi + C::A_BYTES;
+        const uint32_t sb_hi = sa_hi + 2 * C::A_BYTES, sb_lo = sb_hi + C::B_BYTES;
+#pragma unroll
+        for (int k = 0; k < C::KB / 8; ++k) {  // K = 8 tf32 = 32 bytes per instruction
+          const uint32_t off = k * 32;
+          const uint32_t acc0 = (kb | k) ? 1u : 0u;
+          umma::mma_tf32(tmem, umma::smem_desc(sa_lo + off), umma::smem_desc(sb_hi + off), idesc, acc0);
+          umma::mma_tf32(tmem, umma::smem_desc(sa_hi + off), umma::smem_desc(sb_lo + off), idesc, 1u);
+          umma::mma_tf32(tmem, umma::smem_desc(sa_hi + off), umma::smem_desc(sb_hi + off), idesc, 1u);
+        }
+        umma::commit(&empty[s]);  // frees the stage when these MMAs have read it
+      }
+      umma::commit(accfull);  // accumulator complete
+    }
+  } else {
+    // ---------------- epilogue warps 2..5: one output row per thread ----------------
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int r = quarter * 32 + lane;
+    const int row = m0 + r;
+    ptx::mbar_wait(accfull, 0);
+    umma::fence_after();
+    const uint32_t taddr = tmem + (uint32_t(quarter * 32) << 16);
+    if (p.zbuf) {
+#pragma unroll
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        float v[16];
+        umma::tmem_ld16(taddr + c0, v);
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          if (row < p.P && n0 + c0 + q < p.D) p.zbuf[size_t(n0 + c0 + q) * p.ldz + row] = v[q];
+      }
+    } else {
+      for (int ch = 0; ch < p.n_ch; ++ch) {
+        const int term = p.ch_term[ch];
+        const bool prod = term_is_product(term);
+        float acc = prod ? 1.f : 0.f;
+#pragma unroll
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          float v[16];
+          umma::tmem_ld16(taddr + c0, v);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const int col = n0 + c0 + q;
+            if (col < p.D) {
+              const float t = term_value<float>(term, v[q], col, p.ell_w);
+              acc = prod ? __fmul_rn(acc, t) : __fadd_rn(acc, t);
+            }
+          }
+        }
+        if (row < p.P) p.partial[(size_t(ch) * p.n_ntiles + blockIdx.y) * p.P + row] = acc;
+      }
+      __threadfence();
+      ptx::named_bar_sync(1, 128);
+      const int etid = threadIdx.x - 64;
+      if (etid == 0) {
+        const unsigned ticket = atomicAdd(&p.counters[blockIdx.x], 1u);
+        *last_flag = (ticket == unsigned(p.n_ntiles - 1)) ? 1 : 0;
+      }
+      ptx::named_bar_sync(1, 128);
+      if (*last_flag) {
+        __threadfence();
+        if (row < p.P) {
+          float chv[kMaxCh];
+          for (int ch = 0; ch < p.n_ch; ++ch) {
+            const bool prod = term_is_product(p.ch_term[ch]);
+            const float* src = p.partial + size_t(ch) * p.n_ntiles * p.P + row;
+            float v = __ldcg(src);
+            for (int t = 1; t < p.n_ntiles; ++t) {
+              const float x = __ldcg(src + size_t(t) * p.P);
+              v = prod ? __fmul_rn(v, x) : __fadd_rn(v, x);
+            }
+            chv[ch] = v;
+          }
+          for (int o = 0; o < p.n_out; ++o) {
+            const float s0 = chv[p.out_ch0[o]];
+            const float s1 = p.out_ch1[o] >= 0 ? chv[p.out_ch1[o]] : 0.f;
+            p.out[o * p.ldo + row] = finalize<float>(p.out_kind[o], s0, s1, p.D, float(p.out_bias[o]));
+          }
+        }
+        if (etid == 0) p.counters[blockIdx.x] = 0u;
+      }
+    }
+  }
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 1) umma::tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
+// ---------------------------------------------------------------------------------------
 // K2: FP32 FFMA kernel.  Each consumer thread owns an 8x8 register tile; rows and columns
 // are interleaved with stride 8 (rows ty + 8*i, cols tx + 8*j) so the float4 fragment loads
 // of a warp hit 8 distinct 16-byte swizzle chunks (conflict free).
@@ -673,6 +835,22 @@ void launch_f64_persistent(const CUtensorMap& tmX, const CUtensorMap& tmM, const
   count_launch();
 }
 
+template <int BN>
+void launch_f32_umma(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUtensorMap& b_hi, const CUtensorMap& b_lo,
+                     const fused_params<float>& fp, cudaStream_t st) {
+  using C = umma_cfg<BN>;
+  auto kern = eval_f32_umma_kernel<BN>;
+  static bool attr = false;
+  if (!attr) {
+    EVB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  dim3 grid((fp.P + C::BM - 1) / C::BM, (fp.D + BN - 1) / BN);
+  kern<<<grid, C::THREADS, C::SMEM, st>>>(a_hi, a_lo, b_hi, b_lo, fp);
+  EVB_CUDA(cudaGetLastError());
+  count_launch();
+}
+
 template <int BM, int BN>
 void launch_f32(const CUtensorMap& tmX, const CUtensorMap& tmM, const fused_params<float>& fp, cudaStream_t st) {
   using C = f32_cfg<BM, BN, kStages32>;
@@ -689,12 +867,6 @@ void launch_f32(const CUtensorMap& tmX, const CUtensorMap& tmM, const fused_para
 }
 
 
-// cost model: waves * tile area (one CTA per SM for every config)
-double tile_cost(int64_t P, int D, int BM, int BN) {
-  const int64_t ctas = ((P + BM - 1) / BM) * ((D + BN - 1) / BN);
-  const int64_t waves = (ctas + sm_count() - 1) / sm_count();
-  return double(waves) * BM * BN;
-}
 
 }  // namespace
 
@@ -753,6 +925,68 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
   } else {
     BM = 64;
     BN = 128;
+  }
+  static const char* force32 = std::getenv("EVB_F32_KERNEL");
+  const bool umma32 = !std::is_same<T, double>::value && !(force32 && std::string(force32) == "ffma");
+  if constexpr (!std::is_same<T, double>::value) {
+    if (umma32) {
+      // ---- fp32 on tcgen05: 3xTF32, 128 x 64 tiles ----
+      constexpr int UBN = 64;
+      device_problem* pr = const_cast<device_problem*>(rq.prob);
+      const bool own_rot = rotation == pr->rotation;  // composition components pass their own rotation
+      const int64_t mel = int64_t(D) * ldm;
+      void* rhi = nullptr;
+      void* rlo = nullptr;
+      if (own_rot && pr->rot_hi) {
+        rhi = pr->rot_hi;
+        rlo = pr->rot_lo;
+      } else {
+        EVB_CUDA(cudaMalloc(&rhi, mel * sizeof(float)));
+        EVB_CUDA(cudaMalloc(&rlo, mel * sizeof(float)));
+        split_plain_kernel<<<int(std::min<int64_t>(2048, (mel + 255) / 256)), 256, 0, rq.stream>>>(
+            static_cast<const float*>(rotation), mel, static_cast<float*>(rhi), static_cast<float*>(rlo));
+        count_launch();
+        if (own_rot) {
+          pr->rot_hi = rhi;
+          pr->rot_lo = rlo;
+        }
+      }
+      const int64_t lds = round_up(D, 32);
+      ensure_buffer(&sc->s_hi, &sc->s_hi_bytes, size_t(lds) * P * sizeof(float), rq.stream);
+      ensure_buffer(&sc->s_lo, &sc->s_lo_bytes, size_t(lds) * P * sizeof(float), rq.stream);
+      split_tf32_kernel<<<dim3(unsigned((lds + 255) / 256), unsigned(P)), 256, 0, rq.stream>>>(
+          static_cast<const float*>(X), ldx, shift, P, D, static_cast<float*>(sc->s_hi), static_cast<float*>(sc->s_lo),
+          lds);
+      count_launch();
+      CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
+      bool ok = make_tma_2d(&ta_hi, sc->s_hi, EVB_F32, uint64_t(lds), uint64_t(P), uint64_t(lds) * 4, 32, 128) &&
+                make_tma_2d(&ta_lo, sc->s_lo, EVB_F32, uint64_t(lds), uint64_t(P), uint64_t(lds) * 4, 32, 128) &&
+                make_tma_2d(&tb_hi, rhi, EVB_F32, uint64_t(ldm), uint64_t(D), uint64_t(ldm) * 4, 32, UBN) &&
+                make_tma_2d(&tb_lo, rlo, EVB_F32, uint64_t(ldm), uint64_t(D), uint64_t(ldm) * 4, 32, UBN);
+      if (!ok) throw runtime_error("gemm_eval: cannot encode the TMA descriptors of the tf32 split");
+      fp.n_ntiles = (D + UBN - 1) / UBN;
+      const int n_mtiles = (P + 127) / 128;
+      if (!zstore) {
+        ensure_buffer(&sc->partial, &sc->partial_bytes, size_t(fp.n_ch) * fp.n_ntiles * P * sizeof(T), rq.stream);
+        if (sc->counters_n < size_t(n_mtiles)) {
+          size_t cap = sc->counters_n * sizeof(unsigned);
+          void* ptr = sc->counters;
+          ensure_buffer(&ptr, &cap, size_t(n_mtiles) * sizeof(unsigned), rq.stream);
+          sc->counters = static_cast<unsigned*>(ptr);
+          sc->counters_n = cap / sizeof(unsigned);
+          EVB_CUDA(cudaMemsetAsync(sc->counters, 0, cap, rq.stream));
+        }
+        fp.partial = static_cast<T*>(sc->partial);
+        fp.counters = sc->counters;
+      }
+      launch_f32_umma<UBN>(ta_hi, ta_lo, tb_hi, tb_lo, fp, rq.stream);
+      if (!own_rot) {
+        EVB_CUDA(cudaStreamSynchronize(rq.stream));
+        cudaFree(rhi);
+        cudaFree(rlo);
+      }
+      return;
+    }
   }
   CUtensorMap tmX, tmM;
   if (!make_tma_2d(&tmX, X, dtype, uint64_t(D), uint64_t(P), uint64_t(ldx) * sizeof(T), KB, BM))

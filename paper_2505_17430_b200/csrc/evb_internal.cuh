@@ -103,6 +103,9 @@ struct device_problem {
   double* comp_lambda = nullptr;
   double* comp_bias = nullptr;
   void* hyb_w = nullptr;      // hybrid: per-chunk elliptic weights, chunk c at its offset
+  // fp32 tensor-core path: TF32 head / remainder split of the rotation (made on first use)
+  void* rot_hi = nullptr;
+  void* rot_lo = nullptr;
 };
 
 }  // namespace evb
@@ -144,6 +147,11 @@ struct evb_scratch_s {
   // composition: value accumulators (double) per point
   double* acc = nullptr;
   size_t acc_bytes = 0;
+  // fp32 tensor-core path: TF32 split of S = X - o
+  void* s_hi = nullptr;
+  size_t s_hi_bytes = 0;
+  void* s_lo = nullptr;
+  size_t s_lo_bytes = 0;
 };
 
 namespace evb {

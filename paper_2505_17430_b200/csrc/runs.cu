@@ -74,10 +74,13 @@ __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int
   const int RP = (D + 31) / 32 * 32;           // threads per row group
   const int NG = max(1, int(blockDim.x) / RP);  // individual groups
   for (int c = 0; c < ncomp; ++c) {
-    for (int e = threadIdx.x; e < D * D; e += blockDim.x) sM[(e / D) * S + (e % D)] = pr.rot[c][(e / D) * pr.ld + (e % D)];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    for (int r = warp; r < D; r += nwarps)
+      for (int k = lane; k < D; k += 32) sM[r * S + k] = pr.rot[c][r * pr.ld + k];
     for (int e = threadIdx.x; e < D; e += blockDim.x) sO[e] = pr.shift[c][e];
     __syncthreads();
-    for (int e = threadIdx.x; e < P * D; e += blockDim.x) sS[e] = __dsub_rn(X[e], sO[e % D]);
+    for (int i = warp; i < P; i += nwarps)
+      for (int k = lane; k < D; k += 32) sS[i * D + k] = __dsub_rn(X[i * D + k], sO[k]);
     __syncthreads();
     if (pr.n_comp > 0)
       for (int i = threadIdx.x; i < P; i += blockDim.x) {  // dist^2 in double (problems/instance.hpp:127-134)
@@ -115,10 +118,10 @@ __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int
     __syncthreads();
     const int kind = pr.kind[c];
     if (kind_has_pre(kind)) {  // transcendental terms in parallel over all P*D elements (into sS)
-      for (int e = threadIdx.x; e < P * D; e += blockDim.x) {
-        const double* zr = sZ + (e / D) * D;
+      for (int i = warp; i < P; i += nwarps) {
+        const double* zr = sZ + i * D;
         auto z = [&](int q) { return zr[q]; };
-        sS[e] = base_pre_term<double, false>(kind, D, z, e % D);
+        for (int k = lane; k < D; k += 32) sS[i * D + k] = base_pre_term<double, false>(kind, D, z, k);
       }
       __syncthreads();
     }
@@ -198,7 +201,7 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
   if (a.init) {  // init_population (core/population.hpp:88-98), sub-stream kSubInit of gen0
     const uint64_t ctr = (uint64_t(a.gen0) << 32) | kSubInit;
     for (int e = threadIdx.x; e < P * D; e += blockDim.x)
-      sPop[e] = __dadd_rn(a.lb, __dmul_rn(__dsub_rn(a.ub, a.lb), u01_of(philox_word(key, ctr, uint64_t(e)))));
+      sPop[e] = __dadd_rn(a.lb, __dmul_rn(__dsub_rn(a.ub, a.lb), u01_of(philox_word(key, ctr, uint64_t(e)))));  // once
     __syncthreads();
     runs_evaluate(pr, sPop, P, D, S, sM, sZ, sS, sO, sFk, sDist, sFit);
   } else {
@@ -232,27 +235,33 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
       sIdx[4 * i + 3] = (int(r.count) << 16) | jr;  // gene words start after the scalar words
     }
     __syncthreads();
-    // trial (thread per gene)
-    for (int e = threadIdx.x; e < P * D; e += blockDim.x) {
-      const int i = e / D, j = e % D;
-      const int packed = sIdx[4 * i + 3];
-      const int s0 = packed >> 16, jr = packed & 0xFFFF;
-      const uint64_t w = philox_word(key, (uint64_t(gen) << 32) | uint32_t(i), uint64_t(s0 + j));
-      const double u = u01_of(w);
-      const double xi = sPop[i * D + j];
-      double v = xi;
-      if (u < a.CR || j == jr) {
-        const double xa = sPop[sIdx[4 * i] * D + j], xb = sPop[sIdx[4 * i + 1] * D + j], xc = sPop[sIdx[4 * i + 2] * D + j];
-        v = __dadd_rn(xa, __dmul_rn(a.F, __dsub_rn(xb, xc)));
+    // trial (warp per individual, lanes over genes)
+    {
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+      for (int i = warp; i < P; i += nwarps) {
+        const int packed = sIdx[4 * i + 3];
+        const int s0 = packed >> 16, jr = packed & 0xFFFF;
+        const double* xa = sPop + sIdx[4 * i] * D;
+        const double* xb = sPop + sIdx[4 * i + 1] * D;
+        const double* xc = sPop + sIdx[4 * i + 2] * D;
+        const uint64_t ctr = (uint64_t(gen) << 32) | uint32_t(i);
+        for (int j = lane; j < D; j += 32) {
+          const double u = u01_of(philox_word(key, ctr, uint64_t(s0 + j)));
+          const double xi = sPop[i * D + j];
+          double v = xi;
+          if (u < a.CR || j == jr) v = __dadd_rn(xa[j], __dmul_rn(a.F, __dsub_rn(xb[j], xc[j])));
+          sTrial[i * D + j] = clip_or_mid(v, xi, a.lb, a.ub, a.repair);
+        }
       }
-      sTrial[e] = clip_or_mid(v, xi, a.lb, a.ub, a.repair);
     }
     __syncthreads();
     runs_evaluate(pr, sTrial, P, D, S, sM, sZ, sS, sO, sFk, sDist, sTfit);
     // selection
-    for (int e = threadIdx.x; e < P * D; e += blockDim.x) {
-      const int i = e / D;
-      if (sTfit[i] <= sFit[i]) sPop[e] = sTrial[e];
+    {
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+      for (int i = warp; i < P; i += nwarps)
+        if (sTfit[i] <= sFit[i])
+          for (int j = lane; j < D; j += 32) sPop[i * D + j] = sTrial[i * D + j];
     }
     __syncthreads();
     for (int i = threadIdx.x; i < P; i += blockDim.x)
