@@ -70,6 +70,8 @@ struct fused_params {
   T* zbuf;  // non-null: z-store mode, zbuf[i*ldz + b]
   int64_t ldz;
   const T* shift;  // padded with zeros beyond D
+  int umma_variant;  // tf32 path: 0 = 3 products in one accumulator, 1 = + lo*lo, 2 = hi*hi and
+                     // corrections in separate TMEM accumulators (summed in the epilogue)
 };
 
 template <typename T>
@@ -474,7 +476,7 @@ struct umma_cfg {
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // hi + lo of both operands
   static constexpr int THREADS = 6 * 32;
-  static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // [0,BN): main, [BN,2BN): corrections
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + (2 * STAGES + 1) * 8 + 64;
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
 };
@@ -538,13 +540,17 @@ __global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
         umma::fence_after();
         const uint32_t sa_hi = base + s * C::STAGE_BYTES, sa_lo = sa_hi + C::A_BYTES;
         const uint32_t sb_hi = sa_hi + 2 * C::A_BYTES, sb_lo = sb_hi + C::B_BYTES;
+        const uint32_t tcorr = p.umma_variant == 2 ? tmem + BN : tmem;
 #pragma unroll
         for (int k = 0; k < C::KB / 8; ++k) {  // K = 8 tf32 = 32 bytes per instruction
           const uint32_t off = k * 32;
           const uint32_t acc0 = (kb | k) ? 1u : 0u;
-          umma::mma_tf32(tmem, umma::smem_desc(sa_lo + off), umma::smem_desc(sb_hi + off), idesc, acc0);
-          umma::mma_tf32(tmem, umma::smem_desc(sa_hi + off), umma::smem_desc(sb_lo + off), idesc, 1u);
-          umma::mma_tf32(tmem, umma::smem_desc(sa_hi + off), umma::smem_desc(sb_hi + off), idesc, 1u);
+          umma::mma_tf32(tcorr, umma::smem_desc(sa_lo + off), umma::smem_desc(sb_hi + off), idesc, acc0);
+          umma::mma_tf32(tcorr, umma::smem_desc(sa_hi + off), umma::smem_desc(sb_lo + off), idesc, 1u);
+          if (p.umma_variant == 1)
+            umma::mma_tf32(tcorr, umma::smem_desc(sa_lo + off), umma::smem_desc(sb_lo + off), idesc, 1u);
+          umma::mma_tf32(tmem, umma::smem_desc(sa_hi + off), umma::smem_desc(sb_hi + off), idesc,
+                         p.umma_variant == 2 ? acc0 : 1u);
         }
         umma::commit(&empty[s]);  // frees the stage when these MMAs have read it
       }
@@ -563,6 +569,12 @@ __global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
       for (int c0 = 0; c0 < BN; c0 += 16) {
         float v[16];
         umma::tmem_ld16(taddr + c0, v);
+        if (p.umma_variant == 2) {
+          float w[16];
+          umma::tmem_ld16(taddr + BN + c0, w);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) v[q] = __fadd_rn(v[q], w[q]);
+        }
 #pragma unroll
         for (int q = 0; q < 16; ++q)
           if (row < p.P && n0 + c0 + q < p.D) p.zbuf[size_t(n0 + c0 + q) * p.ldz + row] = v[q];
@@ -576,6 +588,12 @@ __global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
         for (int c0 = 0; c0 < BN; c0 += 16) {
           float v[16];
           umma::tmem_ld16(taddr + c0, v);
+          if (p.umma_variant == 2) {
+            float w[16];
+            umma::tmem_ld16(taddr + BN + c0, w);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] = __fadd_rn(v[q], w[q]);
+          }
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             const int col = n0 + c0 + q;
@@ -926,8 +944,14 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
     BM = 64;
     BN = 128;
   }
+  // fp32 tensor-core path (3xTF32, main product and corrections in separate TMEM accumulators):
+  // measured fitness error <= 1e-5 relative for every base kind except discus, whose value is
+  // dominated by 1e6 * z0^2 and amplifies the tensor-core accumulation error to ~1e-4; discus,
+  // hybrids (chunks may be discus) and compositions stay on the FFMA kernel.
   static const char* force32 = std::getenv("EVB_F32_KERNEL");
-  const bool umma32 = !std::is_same<T, double>::value && !(force32 && std::string(force32) == "ffma");
+  bool umma32 = !std::is_same<T, double>::value && rq.prob->spec == SPEC_BASE;
+  for (int o = 0; o < rq.n_out && umma32; ++o) umma32 = rq.kinds[o] != EVB_DISCUS;
+  if (force32) umma32 = std::string(force32) == "umma" && !std::is_same<T, double>::value;
   if constexpr (!std::is_same<T, double>::value) {
     if (umma32) {
       // ---- fp32 on tcgen05: 3xTF32, 128 x 64 tiles ----
@@ -979,6 +1003,8 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
         fp.partial = static_cast<T*>(sc->partial);
         fp.counters = sc->counters;
       }
+      static const char* var = std::getenv("EVB_UMMA_VARIANT");
+      fp.umma_variant = var ? std::atoi(var) : 2;
       launch_f32_umma<UBN>(ta_hi, ta_lo, tb_hi, tb_lo, fp, rq.stream);
       if (!own_rot) {
         EVB_CUDA(cudaStreamSynchronize(rq.stream));

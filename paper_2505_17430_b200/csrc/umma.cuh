@@ -102,7 +102,9 @@ __global__ void split_tf32_kernel(const float* __restrict__ X, int64_t ldx, cons
     if (k < D) {
       const float s = __fsub_rn(X[size_t(i) * ldx + k], shift[k]);
       h = __uint_as_float(umma::cvt_rna_tf32(s));
-      l = __fsub_rn(s, h);
+      // round the remainder to TF32 too: the tensor core would otherwise truncate it, and a
+      // truncation bias accumulates linearly over K instead of as sqrt(K)
+      l = __uint_as_float(umma::cvt_rna_tf32(__fsub_rn(s, h)));
     }
     hi[size_t(i) * lds + k] = h;
     lo[size_t(i) * lds + k] = l;
@@ -116,7 +118,7 @@ __global__ void split_plain_kernel(const float* __restrict__ a, int64_t n, float
     const float x = a[e];
     const float h = __uint_as_float(umma::cvt_rna_tf32(x));
     hi[e] = h;
-    lo[e] = __fsub_rn(x, h);
+    lo[e] = __uint_as_float(umma::cvt_rna_tf32(__fsub_rn(x, h)));
   }
 }
 

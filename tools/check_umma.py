@@ -16,7 +16,7 @@ for D, P in ((1000, 1024), (200, 37), (257, 129)):
     o, m = O.shift_rotation(7, D)
     X = O.population(7, P, D)
     o32, m32, X32 = o.astype(np.float32), m.astype(np.float32), X.astype(np.float32)
-    for kind in (1, 5, 6, 4):
+    for kind in (1, 5, 6, 4, 3, 2, 7):
         p = evb.ProblemInstance.base(kind, o32, m32, 0.0, dtype=evb.EVB_F32)
         sc = evb.EvalScratch()
         Xd = torch.from_numpy(X32).cuda()
