@@ -212,11 +212,11 @@ def run_evb(args, rank, world, local):
     import paper_2505_17430_b200 as evb
     from paper_2505_17430_b200 import _lib
 
-    from paper_2505_17430_b200 import dist as D
+    from paper_2505_17430_b200 import dist as pdist
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist = D.init("nccl", device=dev)  # replicas: barrier + max-over-ranks only
+    dist = pdist.init("nccl", device=dev)  # replicas: barrier + max-over-ranks only
 
     o, m, X = make_inputs()
     kinds = [getattr(evb.BaseKind, k) for k in KINDS]
@@ -258,7 +258,7 @@ def run_evb(args, rank, world, local):
 
     launch_ms = [e[2 * i].elapsed_time(e[2 * i + 1]) for e in ev for i in range(len(probs))]
     step_ms = [sum(e[2 * i].elapsed_time(e[2 * i + 1]) for i in range(len(probs))) for e in ev]
-    total_ms = D.max_over_ranks(sum(step_ms), dist, dev)
+    total_ms = pdist.max_over_ranks(sum(step_ms), dist, dev)
     value = world * args.steps * 3 * P / (total_ms * 1e-3)
 
     # ---- roofline (dominant kernel: the fused DMMA evaluation) ----
@@ -300,7 +300,7 @@ def run_evb(args, rank, world, local):
     for _ in range(e2e_steps):
         e2e_step()
     torch.cuda.synchronize()
-    e2e_s = D.max_over_ranks(time.perf_counter() - t0, dist, dev)
+    e2e_s = pdist.max_over_ranks(time.perf_counter() - t0, dist, dev)
     e2e = {"value": world * e2e_steps * 3 * P / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 3 * P * D * 8,
            "d2h_bytes_per_step": 3 * P * 8,
            "how": "3 x evb_evaluate_batch_host per step (C ABI, pinned host X copied in per call, fitness copied out), "

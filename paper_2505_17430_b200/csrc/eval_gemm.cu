@@ -90,6 +90,35 @@ __device__ __forceinline__ T term_value(int term, T v, int col, const T* ell_w) 
 }
 __device__ __forceinline__ bool term_is_product(int term) { return term == TERM_GCOS; }
 
+// Channel accumulation over 16 columns with the term fixed at compile time (keeps the unrolled
+// epilogue free of per-element switches: one specialised loop per term instead of a 7-way
+// switch replicated per unrolled element, which blew the instruction cache).
+template <int TERM, typename T>
+__device__ __forceinline__ T accumulate16(T acc, const T (&v)[16], int col0, int D, const T* ell_w) {
+  constexpr bool prod = TERM == TERM_GCOS;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int col = col0 + q;
+    if (col < D) {
+      const T t = term_value<T>(TERM, v[q], col, ell_w);
+      acc = prod ? fop<T>::mul(acc, t) : fop<T>::add(acc, t);
+    }
+  }
+  return acc;
+}
+template <typename T>
+__device__ __forceinline__ T accumulate16_rt(int term, T acc, const T (&v)[16], int col0, int D, const T* ell_w) {
+  switch (term) {
+    case TERM_SQ: return accumulate16<TERM_SQ>(acc, v, col0, D, ell_w);
+    case TERM_WSQ: return accumulate16<TERM_WSQ>(acc, v, col0, D, ell_w);
+    case TERM_RAST: return accumulate16<TERM_RAST>(acc, v, col0, D, ell_w);
+    case TERM_COS: return accumulate16<TERM_COS>(acc, v, col0, D, ell_w);
+    case TERM_TAIL: return accumulate16<TERM_TAIL>(acc, v, col0, D, ell_w);
+    case TERM_HEAD: return accumulate16<TERM_HEAD>(acc, v, col0, D, ell_w);
+    default: return accumulate16<TERM_GCOS>(acc, v, col0, D, ell_w);
+  }
+}
+
 // Final formula per base kind from its channel sums (problems/batch.hpp:96-233).
 template <typename T>
 __device__ __forceinline__ T finalize(int kind, T s0, T s1, int D, T bias) {
@@ -118,6 +147,46 @@ struct epilogue_flag {
   int last;
 };
 
+// Per channel: each warp owns rows warp, warp + nwarps, ...; every lane evaluates all of its
+// (row, column) terms of up to 8 rows before any shuffle (independent transcendental chains).
+template <int TERM, typename T, int BM, int BN>
+__device__ __forceinline__ void epilogue_rows(const fused_params<T>& p, const T* zt, int ldt, int m0, int n0, int warp,
+                                              int lane, int nwarps, int rpw, int ch, int ntile) {
+  using F = fop<T>;
+  constexpr int CPL = (BN + 31) / 32;  // columns per lane
+  constexpr bool prod = TERM == TERM_GCOS;
+  const T ident = prod ? T(1) : T(0);
+  for (int r0 = 0; r0 < rpw; r0 += 8) {
+    T s[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int r = warp + (r0 + q) * nwarps;
+      s[q] = ident;
+      if (r0 + q < rpw && r < BM) {
+#pragma unroll
+        for (int cc = 0; cc < CPL; ++cc) {
+          const int c = lane + 32 * cc;
+          const int col = n0 + c;
+          if (c < BN && col < p.D) {
+            const T v = term_value<T>(TERM, zt[r * ldt + c], col, p.ell_w);
+            s[q] = prod ? F::mul(s[q], v) : F::add(s[q], v);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      for (int off = 16; off > 0; off >>= 1) {
+        const T o = __shfl_xor_sync(0xffffffffu, s[q], off);
+        s[q] = prod ? F::mul(s[q], o) : F::add(s[q], o);
+      }
+      const int r = warp + (r0 + q) * nwarps;
+      const int row = m0 + r;
+      if (lane == 0 && r0 + q < rpw && r < BM && row < p.P) p.partial[(size_t(ch) * p.n_ntiles + ntile) * p.P + row] = s[q];
+    }
+  }
+}
+
 template <typename T, int BM, int BN>
 __device__ void tile_epilogue(const fused_params<T>& p, const T* zt, int ldt, int m0, int n0, int tid, int nthreads,
                               int* last_flag, int mtile, int ntile, int bar_id) {
@@ -138,41 +207,16 @@ __device__ void tile_epilogue(const fused_params<T>& p, const T* zt, int ldt, in
   // Each warp owns rows warp, warp + nwarps, ...; per channel every lane evaluates all of its
   // (row, column) terms before any shuffle, so the transcendental chains of up to 4 x RPW elements
   // are independent (ILP) instead of one row at a time.
-  constexpr int CPL = (BN + 31) / 32;  // columns per lane
   const int rpw = (BM + nwarps - 1) / nwarps;
   for (int ch = 0; ch < p.n_ch; ++ch) {
-    const int term = p.ch_term[ch];
-    const bool prod = term_is_product(term);
-    const T ident = prod ? T(1) : T(0);
-    for (int r0 = 0; r0 < rpw; r0 += 8) {
-      T s[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int r = warp + (r0 + q) * nwarps;
-        s[q] = ident;
-        if (r0 + q < rpw && r < BM) {
-#pragma unroll
-          for (int cc = 0; cc < CPL; ++cc) {
-            const int c = lane + 32 * cc;
-            const int col = n0 + c;
-            if (c < BN) {
-              const T v = col < p.D ? term_value<T>(term, zt[r * ldt + c], col, p.ell_w) : ident;
-              s[q] = prod ? F::mul(s[q], v) : F::add(s[q], v);
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        for (int off = 16; off > 0; off >>= 1) {
-          const T o = __shfl_xor_sync(0xffffffffu, s[q], off);
-          s[q] = prod ? F::mul(s[q], o) : F::add(s[q], o);
-        }
-        const int r = warp + (r0 + q) * nwarps;
-        const int row = m0 + r;
-        if (lane == 0 && r0 + q < rpw && r < BM && row < p.P)
-          p.partial[(size_t(ch) * p.n_ntiles + ntile) * p.P + row] = s[q];
-      }
+    switch (p.ch_term[ch]) {  // one specialised loop nest per term (no per-element switch)
+      case TERM_SQ: epilogue_rows<TERM_SQ, T, BM, BN>(p, zt, ldt, m0, n0, warp, lane, nwarps, rpw, ch, ntile); break;
+      case TERM_WSQ: epilogue_rows<TERM_WSQ, T, BM, BN>(p, zt, ldt, m0, n0, warp, lane, nwarps, rpw, ch, ntile); break;
+      case TERM_RAST: epilogue_rows<TERM_RAST, T, BM, BN>(p, zt, ldt, m0, n0, warp, lane, nwarps, rpw, ch, ntile); break;
+      case TERM_COS: epilogue_rows<TERM_COS, T, BM, BN>(p, zt, ldt, m0, n0, warp, lane, nwarps, rpw, ch, ntile); break;
+      case TERM_TAIL: epilogue_rows<TERM_TAIL, T, BM, BN>(p, zt, ldt, m0, n0, warp, lane, nwarps, rpw, ch, ntile); break;
+      case TERM_HEAD: epilogue_rows<TERM_HEAD, T, BM, BN>(p, zt, ldt, m0, n0, warp, lane, nwarps, rpw, ch, ntile); break;
+      default: epilogue_rows<TERM_GCOS, T, BM, BN>(p, zt, ldt, m0, n0, warp, lane, nwarps, rpw, ch, ntile); break;
     }
   }
   __threadfence();
@@ -471,10 +515,10 @@ template <int BN>
 struct umma_cfg {
   static constexpr int BM = 128;
   static constexpr int KB = 32;  // floats per K-slice (one 128-byte swizzle row)
-  static constexpr int STAGES = 4;
   static constexpr int A_BYTES = BM * 128;
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // hi + lo of both operands
+  static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) < 4 ? (200 * 1024 / STAGE_BYTES) : 4;
   static constexpr int THREADS = 6 * 32;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // [0,BN): main, [BN,2BN): corrections
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + (2 * STAGES + 1) * 8 + 64;
@@ -523,6 +567,10 @@ __global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
         const int s = kb % C::STAGES;
         if (kb >= C::STAGES) ptx::mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
         uint8_t* st = smem + s * C::STAGE_BYTES;
+        if (p.umma_variant >= 20) {  // debug: no loads
+          ptx::mbar_arrive(&full[s]);
+          continue;
+        }
         ptx::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
         ptx::tma_load_2d(st, &tmShi, &full[s], kb * C::KB, m0);
         ptx::tma_load_2d(st + C::A_BYTES, &tmSlo, &full[s], kb * C::KB, m0);
@@ -537,31 +585,37 @@ __global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
       for (int kb = 0; kb < KT; ++kb) {
         const int s = kb % C::STAGES;
         ptx::mbar_wait(&full[s], (kb / C::STAGES) & 1);
-        umma::fence_after();
+        if (p.umma_variant < 40) umma::fence_after();
+        if (p.umma_variant >= 10 && p.umma_variant < 20) {  // debug: no MMA
+          ptx::mbar_arrive(&empty[s]);
+          continue;
+        }
         const uint32_t sa_hi = base + s * C::STAGE_BYTES, sa_lo = sa_hi + C::A_BYTES;
         const uint32_t sb_hi = sa_hi + 2 * C::A_BYTES, sb_lo = sb_hi + C::B_BYTES;
-        const uint32_t tcorr = p.umma_variant == 2 ? tmem + BN : tmem;
+        const uint32_t tcorr = (p.umma_variant % 10) == 2 ? tmem + BN : tmem;
 #pragma unroll
         for (int k = 0; k < C::KB / 8; ++k) {  // K = 8 tf32 = 32 bytes per instruction
           const uint32_t off = k * 32;
           const uint32_t acc0 = (kb | k) ? 1u : 0u;
           umma::mma_tf32(tcorr, umma::smem_desc(sa_lo + off), umma::smem_desc(sb_hi + off), idesc, acc0);
           umma::mma_tf32(tcorr, umma::smem_desc(sa_hi + off), umma::smem_desc(sb_lo + off), idesc, 1u);
-          if (p.umma_variant == 1)
+          if ((p.umma_variant % 10) == 1)
             umma::mma_tf32(tcorr, umma::smem_desc(sa_lo + off), umma::smem_desc(sb_lo + off), idesc, 1u);
           umma::mma_tf32(tmem, umma::smem_desc(sa_hi + off), umma::smem_desc(sb_hi + off), idesc,
-                         p.umma_variant == 2 ? acc0 : 1u);
+                         (p.umma_variant % 10) == 2 ? acc0 : 1u);
         }
-        umma::commit(&empty[s]);  // frees the stage when these MMAs have read it
+        if (p.umma_variant >= 50 && p.umma_variant < 60 && kb + C::STAGES < KT) ptx::mbar_arrive(&empty[s]);  // debug
+        else umma::commit(&empty[s]);  // frees the stage when these MMAs have read it
       }
-      umma::commit(accfull);  // accumulator complete
+      if (p.umma_variant >= 10 && p.umma_variant < 20) ptx::mbar_arrive(accfull);
+      else umma::commit(accfull);  // accumulator complete
     }
   } else {
     // ---------------- epilogue warps 2..5: one output row per thread ----------------
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int r = quarter * 32 + lane;
     const int row = m0 + r;
-    ptx::mbar_wait(accfull, 0);
+    ptx::mbar_wait_sleep(accfull, 0);
     umma::fence_after();
     const uint32_t taddr = tmem + (uint32_t(quarter * 32) << 16);
     if (p.zbuf) {
@@ -569,7 +623,7 @@ __global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
       for (int c0 = 0; c0 < BN; c0 += 16) {
         float v[16];
         umma::tmem_ld16(taddr + c0, v);
-        if (p.umma_variant == 2) {
+        if ((p.umma_variant % 10) == 2) {
           float w[16];
           umma::tmem_ld16(taddr + BN + c0, w);
 #pragma unroll
@@ -584,24 +638,17 @@ __global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
         const int term = p.ch_term[ch];
         const bool prod = term_is_product(term);
         float acc = prod ? 1.f : 0.f;
-#pragma unroll
+#pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 16) {
           float v[16];
           umma::tmem_ld16(taddr + c0, v);
-          if (p.umma_variant == 2) {
+          if ((p.umma_variant % 10) == 2) {
             float w[16];
             umma::tmem_ld16(taddr + BN + c0, w);
 #pragma unroll
             for (int q = 0; q < 16; ++q) v[q] = __fadd_rn(v[q], w[q]);
           }
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int col = n0 + c0 + q;
-            if (col < p.D) {
-              const float t = term_value<float>(term, v[q], col, p.ell_w);
-              acc = prod ? __fmul_rn(acc, t) : __fadd_rn(acc, t);
-            }
-          }
+          acc = accumulate16_rt<float>(term, acc, v, n0 + c0, p.D, p.ell_w);
         }
         if (row < p.P) p.partial[(size_t(ch) * p.n_ntiles + blockIdx.y) * p.P + row] = acc;
       }
@@ -954,8 +1001,9 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
   if (force32) umma32 = std::string(force32) == "umma" && !std::is_same<T, double>::value;
   if constexpr (!std::is_same<T, double>::value) {
     if (umma32) {
-      // ---- fp32 on tcgen05: 3xTF32, 128 x 64 tiles ----
-      constexpr int UBN = 64;
+      // ---- fp32 on tcgen05: 3xTF32, 128 x UBN tiles ----
+      static const char* ubn_env = std::getenv("EVB_UMMA_BN");
+      const int UBN = ubn_env ? std::atoi(ubn_env) : 64;
       device_problem* pr = const_cast<device_problem*>(rq.prob);
       const bool own_rot = rotation == pr->rotation;  // composition components pass their own rotation
       const int64_t mel = int64_t(D) * ldm;
@@ -985,8 +1033,8 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
       CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
       bool ok = make_tma_2d(&ta_hi, sc->s_hi, EVB_F32, uint64_t(lds), uint64_t(P), uint64_t(lds) * 4, 32, 128) &&
                 make_tma_2d(&ta_lo, sc->s_lo, EVB_F32, uint64_t(lds), uint64_t(P), uint64_t(lds) * 4, 32, 128) &&
-                make_tma_2d(&tb_hi, rhi, EVB_F32, uint64_t(ldm), uint64_t(D), uint64_t(ldm) * 4, 32, UBN) &&
-                make_tma_2d(&tb_lo, rlo, EVB_F32, uint64_t(ldm), uint64_t(D), uint64_t(ldm) * 4, 32, UBN);
+                make_tma_2d(&tb_hi, rhi, EVB_F32, uint64_t(ldm), uint64_t(D), uint64_t(ldm) * 4, 32, uint32_t(UBN)) &&
+                make_tma_2d(&tb_lo, rlo, EVB_F32, uint64_t(ldm), uint64_t(D), uint64_t(ldm) * 4, 32, uint32_t(UBN));
       if (!ok) throw runtime_error("gemm_eval: cannot encode the TMA descriptors of the tf32 split");
       fp.n_ntiles = (D + UBN - 1) / UBN;
       const int n_mtiles = (P + 127) / 128;
@@ -1005,7 +1053,9 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
       }
       static const char* var = std::getenv("EVB_UMMA_VARIANT");
       fp.umma_variant = var ? std::atoi(var) : 2;
-      launch_f32_umma<UBN>(ta_hi, ta_lo, tb_hi, tb_lo, fp, rq.stream);
+      if (UBN == 256) launch_f32_umma<256>(ta_hi, ta_lo, tb_hi, tb_lo, fp, rq.stream);
+      else if (UBN == 128) launch_f32_umma<128>(ta_hi, ta_lo, tb_hi, tb_lo, fp, rq.stream);
+      else launch_f32_umma<64>(ta_hi, ta_lo, tb_hi, tb_lo, fp, rq.stream);
       if (!own_rot) {
         EVB_CUDA(cudaStreamSynchronize(rq.stream));
         cudaFree(rhi);
