@@ -153,6 +153,25 @@ EVB_API int evb_rng_set_generation(evb_rng r, uint32_t generation);
 /* n device-generated Philox words (key, ctr_hi, start..start+n) into host memory. */
 EVB_API int evb_philox_words(uint64_t key, uint64_t ctr_hi, uint64_t start, int64_t n, uint64_t* out_host);
 
+/* ---- best-so-far recorder (experiment/recorder.hpp:35-155) ------------------------------ */
+
+/* Device-resident best_so_far_record: n_runs x (max_fes / interval) checkpoints; slot k holds the
+ * running minimum after exactly (k+1)*interval evaluations; finish() fills a stopped run's tail. */
+typedef struct evb_recorder_s* evb_recorder;
+EVB_API int evb_recorder_create(int dtype, int n_runs, int64_t max_fes, int64_t interval, evb_recorder* out);
+EVB_API int evb_recorder_destroy(evb_recorder r);
+EVB_API int evb_recorder_checkpoints(evb_recorder r);
+/* on_evaluate for n device values of `run`, in FE order */
+EVB_API int evb_recorder_observe(evb_recorder r, int run, const void* values, int64_t n, void* stream);
+/* on_run_end for runs [run0, run0 + n) */
+EVB_API int evb_recorder_finish(evb_recorder r, int run0, int n, void* stream);
+EVB_API int evb_recorder_grid(evb_recorder r, void* grid_host, int64_t* fes_host);
+/* to_csv (recorder.hpp:103-121) for runs laid out problem x instance x run (run fastest); call
+ * with buf = NULL to get the length in *len. */
+EVB_API int evb_recorder_csv(evb_recorder r, const char* suite_name, int dim, int n_problems,
+                             const int* problem_ids, int instances, int runs, char* buf, int64_t cap,
+                             int64_t* len);
+
 /* ---- DE engine (de/engine.hpp:51-173, de/builder.hpp:16-78) --------------------------- */
 
 /* strategy slots, by the reference's names (de/strategy.hpp, de/parameter.hpp) */
@@ -208,6 +227,10 @@ EVB_API int evb_de_set_state(evb_de e, const void* archive_host, int archive_siz
                              const void* mem_f_host, const void* mem_cr_host, int write_index);
 /* Draws of the last generation: words consumed per individual, archive-victim words, the
  * Philox generation id, per-individual F, CR, donor indices (4 per individual) and jrand. */
+/* Every evaluation the engine makes (init in evb_de_optimize, trials in each generation) is
+ * reported, in FE order, to recorder run `run` (run_handle::evaluate -> on_evaluate,
+ * experiment/runner.hpp:38-45); r = NULL detaches. */
+EVB_API int evb_de_attach_recorder(evb_de e, evb_recorder r, int run);
 EVB_API int evb_de_last_draws(evb_de e, int64_t* word_counts, int64_t* archive_words, uint32_t* generation,
                               void* F_host, void* CR_host, int* idx_host, int* jrand_host);
 
@@ -218,10 +241,12 @@ EVB_API int evb_de_last_draws(evb_de e, int64_t* word_counts, int64_t* archive_w
  * initial populations first (generation id gen0), then run `generations` generations (ids
  * gen0+1 ...); otherwise continue from the given populations (ids gen0 ...).  Supports the `de`
  * preset family: rand_1 / best_1, binomial, clip / midpoint_target, fixed F, CR, no archive;
- * the run state must fit in shared memory (else use evb_de_generation per run). */
+ * the run state must fit in shared memory (else use evb_de_generation per run).  rec (may be
+ * NULL): run r's evaluations are recorded into recorder run r, in FE order. */
 EVB_API int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int pop_size, int dim,
                         const evb_problem* problems, const uint64_t* keys, int generations, double lb,
-                        double ub, void* pops, void* fits, int init, uint32_t gen0, void* stream);
+                        double ub, void* pops, void* fits, int init, uint32_t gen0, evb_recorder rec,
+                        void* stream);
 
 /* ---- PSO engine (pso/engine.hpp:33-153, pso/topology.hpp, pso/update.hpp) ------------------ */
 

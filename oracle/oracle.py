@@ -493,3 +493,48 @@ register_ref({
     "ref_bench_config4": (c_double, [c_int, c_int, c_int, c_int, c_int, vp, vp, vp, vp, vp, vp]),
     "ref_bench_de": (c_double, [c_int, c_int, c_int, c_int, c_int, vp, vp, u64]),
 })
+
+
+register_ref({
+    "ref_record": (i64, [vp, c_int, vp, c_int, c_int, ctypes.c_longlong, ctypes.c_longlong, vp, vp, i64]),
+    "ref_de_generation_trace": (c_int, [vp, vp, i64, c_double, c_double, vp]),
+})
+
+
+def ref_record(values_per_run, dim: int, max_fes: int, interval: int):
+    """The reference best_so_far_record fed with each run's values in FE order (+ on_run_end);
+    returns (grid, csv)."""
+    runs = len(values_per_run)
+    n = max(1, max(len(v) for v in values_per_run))
+    vals = np.full((runs, n), np.nan)
+    for r, v in enumerate(values_per_run):
+        vals[r, :len(v)] = v
+    counts = np.array([len(v) for v in values_per_run], np.int32)
+    ck = max_fes // interval
+    grid = np.zeros((runs, ck))
+    ln = REF().ref_record(ptr(vals), n, ptr(counts), runs, dim, max_fes, interval, ptr(grid), None, 0)
+    buf = ctypes.create_string_buffer(int(ln) + 1)
+    REF().ref_record(ptr(vals), n, ptr(counts), runs, dim, max_fes, interval, ptr(grid), buf, int(ln))
+    return grid, buf.raw[:ln].decode()
+
+
+def _refde_generation_trace(self, words, lb, ub):
+    w = np.ascontiguousarray(words, np.uint64)
+    vals = np.empty(self.P)
+    ok = bool(REF().ref_de_generation_trace(self.h, ptr(w), len(w), lb, ub, ptr(vals)))
+    return ok, vals
+
+
+RefDE.generation_trace = _refde_generation_trace
+
+
+register_ref({"ref_de_native_trace": (None, [vp, ctypes.c_uint64, ctypes.c_uint64, c_int, c_double, c_double, vp])})
+
+
+def _refde_native_trace(self, seed, stream, generations, lb, ub):
+    vals = np.empty(self.P * (generations + 1))
+    REF().ref_de_native_trace(self.h, seed, stream, generations, lb, ub, ptr(vals))
+    return vals
+
+
+RefDE.native_trace = _refde_native_trace

@@ -557,3 +557,66 @@ REF_API double ref_bench_de(int preset, int P, int D, int gens, int kind, const 
   for (int g = 0; g < gens; ++g) engine.generation(pop, st, objective, -100.0, 100.0, rng);
   return now_s() - t0;
 }
+
+// ---- best_so_far_record (experiment/recorder.hpp) fed with given value sequences ----------------
+#include "evobench/experiment/recorder.hpp"
+
+// values: runs x n (row per run); counts[r] values of run r are observed (then on_run_end).
+// Writes the grid (runs x checkpoints) and the CSV (returns its length; csv may be null).
+REF_API int64_t ref_record(const double* values, int n, const int* counts, int runs, int dim, long long max_fes,
+                           long long interval, double* grid, char* csv, int64_t cap) {
+  std::vector<problem_instance<double>> inst;
+  inst.push_back(make_instance<double>(1, dim, 1, 0));
+  problems::suite<double> su("gpu", dim, {1}, 1, 0, std::move(inst));
+  experiment::best_so_far_record<double> rec(su, runs, max_fes, interval);
+  for (int r = 0; r < runs; ++r) {
+    experiment::run_key key{1, 1, 0, 0, r};
+    for (int q = 0; q < counts[r]; ++q) rec.on_evaluate(key, q + 1, values[size_t(r) * n + q]);
+    rec.on_run_end(key);
+  }
+  for (int r = 0; r < runs; ++r)
+    for (int c = 0; c < rec.checkpoint_count(); ++c) grid[size_t(r) * rec.checkpoint_count() + c] = rec.at(0, 0, r, c);
+  const std::string s = rec.to_csv();
+  if (csv) std::memcpy(csv, s.data(), std::min<size_t>(size_t(cap), s.size()));
+  return int64_t(s.size());
+}
+
+// one generation like ref_de_generation, additionally returning every objective value in call
+// (FE) order
+REF_API int ref_de_generation_trace(void* h, const uint64_t* words, int64_t n, double lb, double ub, double* values) {
+  auto* r = static_cast<ref_de_run*>(h);
+  const uint64_t sentinel = 0xa5a5a5a5deadbeefULL;
+  std::vector<uint64_t> w(words, words + n);
+  w.push_back(sentinel);
+  rng_stream rng = rng_stream::scripted(w);
+  evolution_state st(1LL << 40, r->P, r->D, std::min(4, r->P));
+  eval_scratch<double> scratch;
+  int q = 0;
+  auto objective = [&](std::span<const double> x) {
+    const double v = r->problem->evaluate(x, scratch);
+    values[q++] = v;
+    return v;
+  };
+  r->engine->generation(r->pop, st, objective, lb, ub, rng);
+  return rng.next_u64() == sentinel ? 1 : 0;
+}
+
+// ref_de_native_run that also returns every objective value in call (FE) order:
+// P initial evaluations, then P trials per generation
+REF_API void ref_de_native_trace(void* h, uint64_t seed, uint64_t stream, int generations, double lb, double ub,
+                                 double* values) {
+  auto* r = static_cast<ref_de_run*>(h);
+  rng_stream rng(seed, stream);
+  r->pop = init_population<double>(r->P, r->D, lb, ub, rng);
+  eval_scratch<double> scratch;
+  int64_t q = 0;
+  auto objective = [&](std::span<const double> x) {
+    const double v = r->problem->evaluate(x, scratch);
+    values[q++] = v;
+    return v;
+  };
+  for (auto& m : r->pop) m.evaluate(objective);
+  r->engine->archive().set_capacity(r->engine->archive_capacity_for(r->P), rng);
+  evolution_state st(1LL << 40, r->P, r->D, std::min(4, r->P));
+  for (int g = 0; g < generations; ++g) r->engine->generation(r->pop, st, objective, lb, ub, rng);
+}

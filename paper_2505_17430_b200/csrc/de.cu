@@ -82,6 +82,8 @@ struct evb_de_s {
   const void* g_key[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   double g_bounds[2] = {0, 0};
   int g_kernels = 0;
+  evb_recorder_s* rec = nullptr;  // attached best-so-far recorder (may be null)
+  int rec_run = 0;
 };
 
 namespace evb {
@@ -566,6 +568,7 @@ void generation_t(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, vo
   rq.stream = st;
   rq.scalar_trig = true;
   eval_dispatch(rq);
+  if (e->rec) recorder_observe(e->rec, e->rec_run, e->trial_fit, e->P, st);  // trials in FE (i) order
   de_select_scan_kernel<T><<<1, kSelThreads, 0, st>>>(d);
   count_launch();
   {
@@ -951,6 +954,22 @@ int evb_de_set_state(evb_de e, const void* archive_host, int archive_size, const
   });
 }
 
+int evb_de_attach_recorder(evb_de e, evb_recorder r, int run) {
+  return guarded([&] {
+    require(e != nullptr, "de: null handle");
+    if (r) {
+      require(recorder_dtype(r) == e->dtype, "de_attach_recorder: dtype mismatch");
+      require(run >= 0 && run < recorder_runs(r), "de_attach_recorder: run out of range");
+    }
+    e->rec = r;
+    e->rec_run = run;
+    if (e->graph) {  // the captured generation does not contain the recorder call
+      EVB_CUDA(cudaGraphExecDestroy(e->graph));
+      e->graph = nullptr;
+    }
+  });
+}
+
 int evb_de_last_draws(evb_de e, int64_t* word_counts, int64_t* archive_words, uint32_t* generation, void* F_host,
                       void* CR_host, int* idx_host, int* jrand_host) {
   return guarded([&] {
@@ -993,6 +1012,7 @@ int evb_de_optimize(evb_de e, evb_problem objective, evb_scratch s, void* pop, i
     rq.stream = st;
     rq.scalar_trig = true;
     eval_dispatch(rq);
+    if (e->rec) recorder_observe(e->rec, e->rec_run, fitness, e->P, st);  // initial evaluations
     int64_t fes = e->P;
     int gens = 0;
     while (fes < max_fes) {

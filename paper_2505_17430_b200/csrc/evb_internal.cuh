@@ -195,6 +195,12 @@ struct eval_request {
 
 void eval_dispatch(const eval_request& rq);
 
+// best-so-far recorder (recorder.cu)
+void recorder_observe(evb_recorder_s* rec, int run, const void* values, int64_t n, cudaStream_t st);
+void* recorder_view(evb_recorder_s* rec, int* n_ckpt, int64_t* interval, void** running, int** next, int64_t** fes);
+int recorder_dtype(evb_recorder_s* rec);
+int recorder_runs(evb_recorder_s* rec);
+
 // device generation counter <- host mirror (after host-side Philox consumers such as init)
 void set_device_gen(evb_rng_s* r, cudaStream_t st);
 

@@ -22,6 +22,7 @@
 #include "evb_internal.cuh"
 #include "evb_math.cuh"
 #include "rng.cuh"
+#include "recorder.cuh"
 
 namespace evb {
 namespace {
@@ -49,6 +50,8 @@ struct runs_args {
   double* pop;  // n_runs x P x D
   double* fit;  // n_runs x P
   int init;
+  int rec_on;
+  rec_view<double> rec;  // best-so-far recorder, run r -> recorder run r
 };
 
 __device__ __forceinline__ double clip_or_mid(double v, double target, double lb, double ub, int repair) {
@@ -204,6 +207,7 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
       sPop[e] = __dadd_rn(a.lb, __dmul_rn(__dsub_rn(a.ub, a.lb), u01_of(philox_word(key, ctr, uint64_t(e)))));  // once
     __syncthreads();
     runs_evaluate(pr, sPop, P, D, S, sM, sZ, sS, sO, sFk, sDist, sFit);
+    if (a.rec_on && threadIdx.x == 0) rec_observe_seq<double>(a.rec, run, sFit, P);
   } else {
     for (int e = threadIdx.x; e < P * D; e += blockDim.x) sPop[e] = gpop[e];
     for (int i = threadIdx.x; i < P; i += blockDim.x) sFit[i] = gfit[i];
@@ -256,6 +260,7 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
     }
     __syncthreads();
     runs_evaluate(pr, sTrial, P, D, S, sM, sZ, sS, sO, sFk, sDist, sTfit);
+    if (a.rec_on && threadIdx.x == 0) rec_observe_seq<double>(a.rec, run, sTfit, P);  // trials, i order
     // selection
     {
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
@@ -285,7 +290,7 @@ using namespace evb;
 
 extern "C" int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int pop_size, int dim,
                            const evb_problem* problems, const uint64_t* keys, int generations, double lb, double ub,
-                           void* pops, void* fits, int init, uint32_t gen0, void* stream) {
+                           void* pops, void* fits, int init, uint32_t gen0, evb_recorder rec, void* stream) {
   return guarded([&] {
     require(dtype == EVB_F64, "de_runs: the persistent runs kernel is fp64");
     require(cfg && problems && keys && pops && fits, "de_runs: null argument");
@@ -357,6 +362,17 @@ extern "C" int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int 
     a.pop = static_cast<double*>(pops);
     a.fit = static_cast<double*>(fits);
     a.init = init;
+    if (rec) {
+      require(recorder_dtype(rec) == EVB_F64 && recorder_runs(rec) >= n_runs, "de_runs: recorder dtype / runs mismatch");
+      void* running;
+      int* next;
+      int64_t* fes;
+      int nck;
+      int64_t itv;
+      void* grid = recorder_view(rec, &nck, &itv, &running, &next, &fes);
+      a.rec_on = 1;
+      a.rec = rec_view<double>{static_cast<double*>(grid), static_cast<double*>(running), next, fes, nck, itv};
+    }
     EVB_CUDA(cudaFuncSetAttribute(de_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     de_runs_kernel<<<n_runs, 512, smem, st>>>(a);
     count_launch();

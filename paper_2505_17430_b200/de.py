@@ -209,6 +209,15 @@ class DEEngine:
         check(_lib.lib().evb_de_generations(self._h, problem.handle, scratch.handle if scratch else None, p, ld, f,
                                             lb, ub, rng.handle, n, _stream_ptr(stream)), "de_generations")
 
+    def attach_recorder(self, recorder, run: int = 0) -> None:
+        """Report every later evaluation (init inside optimize, each generation's trials, FE order)
+        to `recorder` as run `run` (experiment/runner.hpp:38-52 run_handle). None detaches."""
+        from .recorder import _sigs as _rec_sigs
+        _rec_sigs()
+        check(_lib.lib().evb_de_attach_recorder(self._h, recorder.handle if recorder is not None else None, run),
+              "de_attach_recorder")
+        self._recorder = recorder  # keep the device arrays alive while attached
+
     def init_population(self, pop, lb: float, ub: float, rng: Rng, stream=None) -> None:
         check(_lib.lib().evb_de_init_population(self._h, ctypes.c_void_p(pop.data_ptr()), pop.stride(0), lb, ub,
                                                 rng.handle, _stream_ptr(stream)), "de_init_population")

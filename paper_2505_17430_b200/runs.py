@@ -24,7 +24,7 @@ def _sigs():
     vp, i64, c_int, c_double, u32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_uint32
     _lib.register_signatures({
         "evb_de_runs": (c_int, [c_int, ctypes.POINTER(_Cfg), c_int, c_int, c_int, vp, vp, c_int, c_double, c_double,
-                                vp, vp, c_int, u32, vp]),
+                                vp, vp, c_int, u32, vp, vp]),
     })
     _REG = True
 
@@ -43,7 +43,7 @@ def run_keys(master_seed: int, n_runs: int) -> np.ndarray:
 
 
 def de_runs(cfg: DEConfig, problems: Sequence[ProblemInstance], keys, pops, fits, generations: int, lb: float,
-            ub: float, init: bool = True, gen0: int = 0, stream=None) -> None:
+            ub: float, init: bool = True, gen0: int = 0, recorder=None, stream=None) -> None:
     """Run len(problems) independent DE runs for `generations` generations in one launch.
     pops: (n_runs, pop_size, dim) float64 CUDA tensor; fits: (n_runs, pop_size)."""
     _sigs()
@@ -53,4 +53,5 @@ def de_runs(cfg: DEConfig, problems: Sequence[ProblemInstance], keys, pops, fits
     k = np.ascontiguousarray(keys, np.uint64)
     check(_lib.lib().evb_de_runs(EVB_F64, ctypes.byref(c), n_runs, P, D, handles, ctypes.c_void_p(k.ctypes.data),
                                  generations, lb, ub, ctypes.c_void_p(pops.data_ptr()),
-                                 ctypes.c_void_p(fits.data_ptr()), int(init), gen0, _stream_ptr(stream)), "de_runs")
+                                 ctypes.c_void_p(fits.data_ptr()), int(init), gen0,
+                                 recorder.handle if recorder is not None else None, _stream_ptr(stream)), "de_runs")

@@ -1,0 +1,151 @@
+"""GPU parity of the device best-so-far recorder (csrc/recorder.cu) against the reference's
+experiment::best_so_far_record (experiment/recorder.hpp:35-155, driven through oracle/_ref's
+ref_record): the checkpoint grid bit for bit and the CSV byte for byte, on raw value sequences
+(ties, NaN, early-stopping runs, partial last interval) and on the FE sequences that the DE
+engine and the batched-runs kernel report while they run."""
+import numpy as np
+import pytest
+
+import oracle as O
+
+torch = pytest.importorskip("torch")
+import paper_2505_17430_b200 as evb  # noqa: E402
+from paper_2505_17430_b200.de import DEEngine, Rng, preset_de  # noqa: E402
+from paper_2505_17430_b200.recorder import BestSoFarRecorder  # noqa: E402
+from paper_2505_17430_b200.runs import de_runs, run_keys  # noqa: E402
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")]
+
+
+def same_grid(a, b):
+    return np.array_equal(a, b, equal_nan=True)
+
+
+@pytest.mark.parametrize("max_fes,interval", [(1000, 100), (1000, 7), (999, 1000 // 3), (50, 50)])
+def test_raw_sequences_match_reference(dev, max_fes, interval):
+    rs = np.random.default_rng(max_fes + interval)
+    runs = 6
+    seqs = []
+    for r in range(runs):
+        n = [max_fes, max_fes // 2, 3, 0, max_fes + 37, interval - 1][r]  # full, early stop, overrun
+        v = np.round(rs.standard_normal(n) * 1e3, 1)  # rounding makes ties
+        if n > 5:
+            v[rs.integers(0, n, 3)] = np.nan
+            v[0] = np.nan if r == 1 else v[0]
+        seqs.append(v)
+    ref_grid, ref_csv = O.ref_record(seqs, 10, max_fes, interval)
+    rec = BestSoFarRecorder(runs, max_fes, interval)
+    for r, v in enumerate(seqs):
+        if len(v):
+            # split into uneven chunks: observe is incremental across calls
+            cuts = sorted(set([0, len(v)] + list(rs.integers(0, len(v), 3))))
+            for a, b in zip(cuts[:-1], cuts[1:]):
+                rec.observe(r, torch.from_numpy(v[a:b].copy()).to(dev))
+    rec.finish()
+    grid, fes = rec.grid()
+    assert same_grid(grid, ref_grid)
+    assert list(fes) == [len(v) for v in seqs]
+    assert rec.to_csv("gpu", 10, [1], 1, runs) == ref_csv
+
+
+def test_csv_layout_problems_instances(dev):
+    # run index = (problem * instances + instance) * runs + run, as recorder.hpp:103-121 orders rows
+    rec = BestSoFarRecorder(2 * 3 * 2, 40, 10)
+    for r in range(12):
+        rec.observe(r, torch.arange(40, 0, -1, dtype=torch.float64, device=dev) * (r + 1))
+    rec.finish()
+    csv = rec.to_csv("cec", 30, [4, 9], 3, 2).splitlines()
+    assert csv[0] == "suite,problem,instance,dim,run,fes,best_so_far"
+    assert len(csv) == 1 + 12 * 4
+    assert csv[1] == "cec,4,1,30,1,10,31"
+    assert csv[-1] == "cec,9,3,30,2,40,12"
+
+
+@pytest.mark.parametrize("interval", [50, 64, 2100])
+def test_de_engine_recording_matches_reference(dev, interval):
+    # config-0 problem on the reference's native stream rng_stream(42, 0): the engine reports the
+    # P initial evaluations and every generation's P trials in FE order; the reference engine's
+    # objective-call trace fed to its own best_so_far_record must give the same grid and CSV
+    P, D, G = 100, 10, 20
+    o, m = O.shift_rotation(42, D)
+    m = m * 0.0512
+    cfg = preset_de(0.5, 0.9)
+    prob = evb.ProblemInstance.base(evb.BaseKind.rastrigin, o, m, 0.0)
+    max_fes = P * (G + 1)
+    words = O.rng_words(42, 0, P * D + G * P * (D + 40))
+    rec = BestSoFarRecorder(1, max_fes, interval)
+    eng = DEEngine(cfg, P, D)
+    eng.attach_recorder(rec, 0)
+    pop = torch.empty((P, D), dtype=torch.float64, device=dev)
+    fit = torch.empty(P, dtype=torch.float64, device=dev)
+    res = eng.optimize(prob, pop, fit, -100.0, 100.0, max_fes, Rng.words(words))
+    rec.finish()
+    assert res["generations"] == G
+    ref = O.RefDE(cfg, P, D)
+    ref.set_problem_base(5, o, m, 0.0)
+    trace = ref.native_trace(42, 0, G, -100.0, 100.0)
+    ref_grid, ref_csv = O.ref_record([trace], D, max_fes, interval)
+    grid, fes = rec.grid()
+    assert fes[0] == max_fes
+    assert same_grid(grid, ref_grid)
+    assert rec.to_csv("gpu", D, [1], 1, 1) == ref_csv
+    assert grid[0, -1] == fit.min().item()
+
+
+def test_graph_replay_detached_recorder(dev):
+    # attaching drops the cached graph (it does not contain the recorder call); later eager
+    # generations keep recording, and detaching stops it
+    P, D = 64, 20
+    o, m = O.shift_rotation(5, D)
+    prob = evb.ProblemInstance.base(evb.BaseKind.ackley, o, m, 0.0)
+    eng = DEEngine(preset_de(0.5, 0.9), P, D)
+    rng = Rng.philox(5)
+    pop = torch.empty((P, D), dtype=torch.float64, device=dev)
+    eng.init_population(pop, -32.0, 32.0, rng)
+    fit = torch.empty(P, dtype=torch.float64, device=dev)
+    evb.evaluate_batch(prob, pop, evb.EvalScratch(), fit)
+    eng.generations(prob, pop, fit, -32.0, 32.0, rng, 4)  # graph captured, no recorder
+    rec = BestSoFarRecorder(1, 10 * P, P)
+    eng.attach_recorder(rec, 0)
+    eng.generations(prob, pop, fit, -32.0, 32.0, rng, 6)
+    eng.attach_recorder(None)
+    eng.generations(prob, pop, fit, -32.0, 32.0, rng, 3)
+    grid, fes = rec.grid()
+    assert fes[0] == 6 * P
+    assert np.all(np.diff(grid[0, :6]) <= 0) and np.isnan(grid[0, 6:]).all()
+
+
+def test_batched_runs_recording(dev):
+    # K8 reports init + every generation's trials per run; the reference engine replays run 0's
+    # Philox words and its objective trace through best_so_far_record
+    from test_runs_gpu import D as D8, P as P8, make_runs
+    n_runs, gens, interval = 6, 40, 250
+    probs, comps = make_runs(n_runs)
+    keys = run_keys(64, n_runs)
+    pops = torch.empty((n_runs, P8, D8), dtype=torch.float64, device=dev)
+    fits = torch.empty((n_runs, P8), dtype=torch.float64, device=dev)
+    max_fes = P8 * (gens + 1)
+    rec = BestSoFarRecorder(n_runs, max_fes, interval)
+    de_runs(preset_de(0.5, 0.9), probs, keys, pops, fits, gens, -100.0, 100.0, init=True, gen0=0, recorder=rec)
+    rec.finish()
+    grid, fes = rec.grid()
+    assert list(fes) == [max_fes] * n_runs
+    f = fits.cpu().numpy()
+    for r in range(n_runs):
+        assert np.all(np.diff(grid[r]) <= 0)
+        assert grid[r, -1] == f[r].min()
+    s, mm = comps[0]
+    ref = O.RefDE(preset_de(0.5, 0.9), P8, D8)
+    ref.set_problem_composition(O.CONFIG4_KINDS, s, mm, O.CONFIG4_SIGMA, O.CONFIG4_LAMBDA, O.CONFIG4_BIAS, 0.0)
+    init_words = O.philox_words(int(keys[0]), (0 << 32) | 0xFFFFFFF0, 0, P8 * D8)
+    assert ref.init(init_words, -100.0, 100.0) == P8 * D8
+    trace = [ref.get()["fit"].copy()]
+    for g in range(1, gens + 1):
+        ok, vals = ref.generation_trace(O.de_fixed_generation_words(0, int(keys[0]), g, P8, D8), -100.0, 100.0)
+        assert ok
+        trace.append(vals)
+    trace = np.concatenate(trace)
+    ref_grid, _ = O.ref_record([trace], D8, max_fes, interval)
+    # exact-order arithmetic: identical unless a libm-vs-CUDA ulp flipped a near-tie selection
+    rel = np.abs(grid[0] - ref_grid[0]) / np.maximum(1.0, np.abs(ref_grid[0]))
+    assert rel.max() <= 1e-10
