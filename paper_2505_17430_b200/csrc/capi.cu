@@ -33,6 +33,20 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
+using write_value32_fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+write_value32_fn stream_write_value32() {
+  static write_value32_fn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<write_value32_fn>(p);
+  });
+  return fn;
+}
+
 size_t elem_size(int dtype) { return dtype == EVB_F64 ? 8 : 4; }
 
 void check_dtype(int dtype) {
@@ -296,10 +310,12 @@ int evb_scratch_create(evb_scratch* out) {
 int evb_scratch_destroy(evb_scratch s) {
   return guarded([&] {
     if (!s) return;
-    void* ptrs[] = {s->partial, s->counters, s->zbuf, s->xpad, s->dx, s->dout, s->acc, s->s_hi, s->s_lo};
+    void* ptrs[] = {s->partial, s->counters, s->zbuf, s->xpad, s->dx, s->dout, s->acc, s->s_hi, s->s_lo, s->gate};
     for (void* q : ptrs)
       if (q) cudaFree(q);
     if (s->own_stream) cudaStreamDestroy(s->own_stream);
+    if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
+    if (s->ev_x_ready) cudaEventDestroy(s->ev_x_ready);
     delete s;
   });
 }
@@ -375,7 +391,6 @@ int evb_evaluate_batch_host(evb_problem p, evb_scratch s, const void* X_host, in
     const int64_t ldd = round_up(D, 16 / int64_t(es));
     ensure_buffer(&s->dx, &s->dx_bytes, size_t(ldd) * n_points * es, st);
     ensure_buffer(&s->dout, &s->dout_bytes, size_t(n_points) * es, st);
-    EVB_CUDA(cudaMemcpy2DAsync(s->dx, ldd * es, X_host, ldx * es, D * es, n_points, cudaMemcpyHostToDevice, st));
     eval_request rq{};
     rq.prob = &p->p;
     rq.scratch = s;
@@ -388,7 +403,47 @@ int evb_evaluate_batch_host(evb_problem p, evb_scratch s, const void* X_host, in
     rq.kinds[0] = p->p.kind;
     rq.biases[0] = p->p.bias;
     rq.stream = st;
-    eval_dispatch(rq);
+    // The fused fp64 GEMM starts while X is still crossing the host link: X goes over in column
+    // chunks on a second stream, each chunk followed by a stream write of its gate word, and the
+    // GEMM producer waits per chunk before its TMA loads (the copy is the e2e bound: ~8 MB per
+    // batch at D=1000, P=1024).  All copies are enqueued before the kernel, so the kernel only
+    // ever waits on work queued ahead of it.  Other paths copy X whole, then launch.
+    rq.X = s->dx;
+    rq.ldx = ldd;
+    static const char* chunks_env = std::getenv("EVB_H2D_CHUNKS");
+    const int want = chunks_env ? std::max(1, std::atoi(chunks_env)) : 8;
+    write_value32_fn wv = stream_write_value32();
+    if (want > 1 && wv && gate_eligible(rq)) {
+      if (!s->copy_stream) EVB_CUDA(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
+      if (!s->ev_x_ready) EVB_CUDA(cudaEventCreateWithFlags(&s->ev_x_ready, cudaEventDisableTiming));
+      if (!s->gate) {
+        EVB_CUDA(cudaMalloc(&s->gate, kMaxGates * sizeof(unsigned)));
+        EVB_CUDA(cudaMemset(s->gate, 0, kMaxGates * sizeof(unsigned)));
+      }
+      const int64_t cols = round_up((D + want - 1) / want, 16);
+      const int n_chunks = int((D + cols - 1) / cols);
+      if (n_chunks > kMaxGates) throw logic_error("evaluate_batch_host: too many copy chunks");
+      const unsigned epoch = ++s->gate_epoch == 0 ? ++s->gate_epoch : s->gate_epoch;
+      // the previous call on this scratch synchronised st, so dx is free to overwrite
+      for (int c = 0; c < n_chunks; ++c) {
+        const int64_t c0 = int64_t(c) * cols, w = std::min<int64_t>(cols, D - c0);
+        EVB_CUDA(cudaMemcpy2DAsync(static_cast<uint8_t*>(s->dx) + c0 * es, ldd * es,
+                                   static_cast<const uint8_t*>(X_host) + c0 * es, ldx * es, w * es, n_points,
+                                   cudaMemcpyHostToDevice, s->copy_stream));
+        if (wv(s->copy_stream, CUdeviceptr(s->gate + c), epoch, 0) != CUDA_SUCCESS)
+          throw runtime_error("evaluate_batch_host: cuStreamWriteValue32 failed");
+      }
+      EVB_CUDA(cudaEventRecord(s->ev_x_ready, s->copy_stream));
+      rq.kgate = s->gate;
+      rq.kgate_cols = int(cols);
+      rq.kgate_epoch = epoch;
+      rq.x_ready = s->ev_x_ready;
+      eval_dispatch(rq);
+      EVB_CUDA(cudaStreamWaitEvent(st, s->ev_x_ready, 0));
+    } else {
+      EVB_CUDA(cudaMemcpy2DAsync(s->dx, ldd * es, X_host, ldx * es, D * es, n_points, cudaMemcpyHostToDevice, st));
+      eval_dispatch(rq);
+    }
     EVB_CUDA(cudaMemcpyAsync(out_host, s->dout, size_t(n_points) * es, cudaMemcpyDeviceToHost, st));
     EVB_CUDA(cudaStreamSynchronize(st));
   });

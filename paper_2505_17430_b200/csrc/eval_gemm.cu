@@ -70,6 +70,9 @@ struct fused_params {
   T* zbuf;  // non-null: z-store mode, zbuf[i*ldz + b]
   int64_t ldz;
   const T* shift;  // padded with zeros beyond D
+  const unsigned* kgate;  // non-null: X columns arrive in chunks (see eval_request)
+  int kgate_cols;
+  unsigned kgate_epoch;
   int umma_variant;  // tf32 path: 0 = 3 products in one accumulator, 1 = + lo*lo, 2 = hi*hi and
                      // corrections in separate TMEM accumulators (summed in the epilogue)
 };
@@ -305,9 +308,17 @@ __global__ void __launch_bounds__(f64_cfg<BM, BN, WM, WN, STAGES>::THREADS, MINB
     if (lane == 0) {
       ptx::prefetch_tma(&tmX);
       ptx::prefetch_tma(&tmM);
+      int ready_chunk = -1;
       for (int kb = 0; kb < KT; ++kb) {
         const int s = kb % STAGES;
         if (kb >= STAGES) ptx::mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
+        if (p.kgate) {
+          const int c = (kb * C::KB) / p.kgate_cols;  // chunks are multiples of KB columns
+          if (c > ready_chunk) {
+            ptx::wait_gate(p.kgate + c, p.kgate_epoch);
+            ready_chunk = c;
+          }
+        }
         uint8_t* st = smem + s * C::STAGE_BYTES;
         ptx::mbar_arrive_expect_tx(&full[s], C::A_BYTES + C::B_BYTES + C::O_BYTES);
         ptx::tma_load_2d(st, &tmX, &full[s], kb * C::KB, m0);
@@ -946,6 +957,7 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
   fp.shift = shift;
   fp.out = static_cast<T*>(rq.out);
   fp.ldo = rq.ldo;
+  bool gate_consumed = false;
   if (zstore) {
     fp.zbuf = zbuf;
     fp.ldz = ldz;
@@ -1084,6 +1096,15 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
     fp.partial = static_cast<T*>(sc->partial);
     fp.counters = sc->counters;
   }
+  if constexpr (std::is_same<T, double>::value) {
+    if (!use_persistent && rq.kgate && rq.kgate_cols % 16 == 0) {
+      fp.kgate = rq.kgate;
+      fp.kgate_cols = rq.kgate_cols;
+      fp.kgate_epoch = rq.kgate_epoch;
+      gate_consumed = true;
+    }
+  }
+  if (rq.x_ready && !gate_consumed) EVB_CUDA(cudaStreamWaitEvent(rq.stream, rq.x_ready, 0));
   if constexpr (std::is_same<T, double>::value) {
     if (use_persistent) {
       launch_f64_persistent<64, 56>(tmX, tmM, fp, rq.stream);

@@ -13,6 +13,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "evb_internal.cuh"
 #include "evb_math.cuh"
@@ -369,7 +371,16 @@ const T* tma_legal_x(const eval_request& rq, int D, int64_t* ldx_out) {
 }
 
 template <typename T>
-void dispatch_t(const eval_request& rq) {
+void dispatch_t(const eval_request& rq_in) {
+  // Only the fused fp64 GEMM consumes per-chunk gates (its producer waits column chunk by column
+  // chunk); every other path waits for all of X before its first launch.
+  const bool gated = gate_eligible(rq_in);
+  eval_request rq = rq_in;
+  if (rq.x_ready && !gated) {
+    EVB_CUDA(cudaStreamWaitEvent(rq.stream, rq.x_ready, 0));
+    rq.x_ready = nullptr;
+    rq.kgate = nullptr;
+  }
   const device_problem& pr = *rq.prob;
   const int P = int(rq.n);
   const int D = pr.dim;
@@ -460,6 +471,12 @@ void dispatch_t(const eval_request& rq) {
 
 void count_launch(int n) { g_launches += n; }
 int last_launch_count() { return g_launches; }
+
+bool gate_eligible(const eval_request& rq) {
+  return rq.prob->dtype == EVB_F64 && rq.prob->spec == SPEC_BASE && !small_fits<double>(rq.prob->dim, false) &&
+         fused_kinds_ok(rq.n_out, rq.kinds) && reinterpret_cast<uintptr_t>(rq.X) % 16 == 0 &&
+         (rq.ldx * 8) % 16 == 0 && !(std::getenv("EVB_F64_KERNEL") && std::string(std::getenv("EVB_F64_KERNEL")) == "persistent");
+}
 
 void eval_dispatch(const eval_request& rq) {
   if (rq.n == 0) return;

@@ -152,6 +152,12 @@ struct evb_scratch_s {
   size_t s_hi_bytes = 0;
   void* s_lo = nullptr;
   size_t s_lo_bytes = 0;
+  // host-buffer path with the H2D copy overlapped: X arrives in column chunks on copy_stream,
+  // each followed by a stream write of gate[c] = epoch that the GEMM producer waits on
+  cudaStream_t copy_stream = nullptr;
+  unsigned* gate = nullptr;  // kMaxGates words
+  unsigned gate_epoch = 0;
+  cudaEvent_t ev_x_ready = nullptr;
 };
 
 namespace evb {
@@ -191,9 +197,20 @@ struct eval_request {
   bool scalar_trig = false;  // true: problem_instance::evaluate semantics (libm trig also for
                              // float, problems/functions.hpp); false: evaluate_batch semantics
                              // (fast_cos/fast_sin for float, problems/batch.hpp:17-33)
+  // X still arriving: columns [c*kgate_cols, (c+1)*kgate_cols) are valid once kgate[c] reaches
+  // kgate_epoch (wrap-safe compare); x_ready fires when all of X is resident.  Kernels that do
+  // not consume the gates make the stream wait on x_ready instead.
+  const unsigned* kgate = nullptr;
+  int kgate_cols = 0;
+  unsigned kgate_epoch = 0;
+  cudaEvent_t x_ready = nullptr;
 };
 
+constexpr int kMaxGates = 64;
+
 void eval_dispatch(const eval_request& rq);
+// true when eval_dispatch runs the request on the fused fp64 GEMM, whose producer honours kgate
+bool gate_eligible(const eval_request& rq);
 
 // best-so-far recorder (recorder.cu)
 void recorder_observe(evb_recorder_s* rec, int run, const void* values, int64_t n, cudaStream_t st);

@@ -45,6 +45,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 
 // Long waits (epilogue warps waiting for a whole mainloop): back off between probes so the
 // spinning warps do not steal issue slots from the MMA / TMA issuers on the same SMSP.
+// Wait until *gate has reached `epoch` (wrap-safe), written by a stream memory operation after a
+// host->device copy; then order the copy's data before this thread's later async-proxy (TMA)
+// reads.  Traps after 10 s instead of hanging if the gate never opens.
+__device__ __forceinline__ void wait_gate(const unsigned* gate, unsigned epoch) {
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (true) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gate) : "memory");
+    if (int(v - epoch) >= 0) break;
+    __nanosleep(256);
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 10000000000ull) __trap();
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   uint32_t done = 0;

@@ -21,6 +21,21 @@ def same_grid(a, b):
     return np.array_equal(a, b, equal_nan=True)
 
 
+def close_grid(a, b, tol):
+    return a.shape == b.shape and bool(np.all(np.abs(a - b) <= tol * np.maximum(1.0, np.abs(b))))
+
+
+def csv_close(a, b, tol):
+    ra, rb = a.splitlines(), b.splitlines()
+    if len(ra) != len(rb) or ra[0] != rb[0] or not a.endswith("\n"):
+        return False
+    for x, y in zip(ra[1:], rb[1:]):
+        fx, fy = x.split(","), y.split(",")
+        if fx[:-1] != fy[:-1] or abs(float(fx[-1]) - float(fy[-1])) > tol * max(1.0, abs(float(fy[-1]))):
+            return False
+    return True
+
+
 @pytest.mark.parametrize("max_fes,interval", [(1000, 100), (1000, 7), (999, 1000 // 3), (50, 50)])
 def test_raw_sequences_match_reference(dev, max_fes, interval):
     rs = np.random.default_rng(max_fes + interval)
@@ -87,8 +102,10 @@ def test_de_engine_recording_matches_reference(dev, interval):
     ref_grid, ref_csv = O.ref_record([trace], D, max_fes, interval)
     grid, fes = rec.grid()
     assert fes[0] == max_fes
-    assert same_grid(grid, ref_grid)
-    assert rec.to_csv("gpu", D, [1], 1, 1) == ref_csv
+    # populations are bit-exact (test_de_gpu); fitness values agree to 1e-12 (CUDA vs libm cos),
+    # so the recorded minima do too and the CSV rows match field by field
+    assert close_grid(grid, ref_grid, 1e-12)
+    assert csv_close(rec.to_csv("gpu", D, [1], 1, 1), ref_csv, 1e-12)
     assert grid[0, -1] == fit.min().item()
 
 
