@@ -127,7 +127,10 @@ EVB_API int evb_evaluate_batch_multi(evb_problem p, evb_scratch s, int n_kinds, 
 
 /* Host-buffer form (batched_evaluate, problems/batch.hpp:281-288): X_host (n_points*ldx) and
  * out_host (n_points) are host memory; the call copies in, evaluates and copies out on the
- * scratch's own stream and returns when out_host is filled. */
+ * scratch's own streams and returns when out_host is filled.  For the fused fp64 GEMM path the
+ * copy of X is split into column chunks that the kernel consumes as they land (copy/compute
+ * overlap; EVB_H2D_CHUNKS, default 4, halving widths); page-locked out_host is written by the
+ * kernel directly.  Pinned X_host gives full host-link bandwidth. */
 EVB_API int evb_evaluate_batch_host(evb_problem p, evb_scratch s, const void* X_host, int64_t n_points,
                             int64_t ldx, void* out_host);
 

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -315,7 +316,10 @@ int evb_scratch_destroy(evb_scratch s) {
       if (q) cudaFree(q);
     if (s->own_stream) cudaStreamDestroy(s->own_stream);
     if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
+    if (s->gate_stream) cudaStreamDestroy(s->gate_stream);
     if (s->ev_x_ready) cudaEventDestroy(s->ev_x_ready);
+    for (auto e : s->ev_chunk)
+      if (e) cudaEventDestroy(e);
     delete s;
   });
 }
@@ -403,6 +407,14 @@ int evb_evaluate_batch_host(evb_problem p, evb_scratch s, const void* X_host, in
     rq.kinds[0] = p->p.kind;
     rq.biases[0] = p->p.bias;
     rq.stream = st;
+    // Page-locked `out` (cudaHostAlloc / cudaHostRegister) is written by the kernel directly
+    // (mapped, same address under UVA): no device staging and no D2H copy at the end.
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, out_host) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+        pa.devicePointer == out_host)
+      rq.out = out_host;
+    else
+      cudaGetLastError();
     // The fused fp64 GEMM starts while X is still crossing the host link: X goes over in column
     // chunks on a second stream, each chunk followed by a stream write of its gate word, and the
     // GEMM producer waits per chunk before its TMA loads (the copy is the e2e bound: ~8 MB per
@@ -411,40 +423,86 @@ int evb_evaluate_batch_host(evb_problem p, evb_scratch s, const void* X_host, in
     rq.X = s->dx;
     rq.ldx = ldd;
     static const char* chunks_env = std::getenv("EVB_H2D_CHUNKS");
-    const int want = chunks_env ? std::max(1, std::atoi(chunks_env)) : 8;
+    static const char* split_env = std::getenv("EVB_H2D_SPLIT");
+    const int want = std::min(kMaxGates, chunks_env ? std::max(1, std::atoi(chunks_env)) : 4);
+    const bool geometric = !(split_env && std::string(split_env) == "uniform");
     write_value32_fn wv = stream_write_value32();
     if (want > 1 && wv && gate_eligible(rq)) {
       if (!s->copy_stream) EVB_CUDA(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
+      if (!s->gate_stream) EVB_CUDA(cudaStreamCreateWithFlags(&s->gate_stream, cudaStreamNonBlocking));
       if (!s->ev_x_ready) EVB_CUDA(cudaEventCreateWithFlags(&s->ev_x_ready, cudaEventDisableTiming));
+      for (auto& e : s->ev_chunk)
+        if (!e) EVB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       if (!s->gate) {
         EVB_CUDA(cudaMalloc(&s->gate, kMaxGates * sizeof(unsigned)));
         EVB_CUDA(cudaMemset(s->gate, 0, kMaxGates * sizeof(unsigned)));
       }
-      const int64_t cols = round_up((D + want - 1) / want, 16);
-      const int n_chunks = int((D + cols - 1) / cols);
-      if (n_chunks > kMaxGates) throw logic_error("evaluate_batch_host: too many copy chunks");
+      // chunk boundaries (multiples of 16 columns = the GEMM's K-slice): uniform, or halving
+      // so the compute left after the last chunk lands is small
+      int n_chunks = 0;
+      int64_t c0 = 0;
+      while (c0 < D) {
+        int64_t w;
+        if (n_chunks == want - 1) w = D - c0;
+        else if (geometric) w = round_up((D - c0 + 1) / 2, 16);
+        else w = round_up((D + want - 1) / want, 16);
+        w = std::min<int64_t>(std::max<int64_t>(w, 16), D - c0);
+        rq.kgate_end[n_chunks++] = int(c0 + w);
+        c0 += w;
+      }
+      rq.kgate_n = n_chunks;
       const unsigned epoch = ++s->gate_epoch == 0 ? ++s->gate_epoch : s->gate_epoch;
+      // EVB_H2D_TRACE=1: print the copy / kernel timeline of each call (tuning aid)
+      static const bool trace = std::getenv("EVB_H2D_TRACE") != nullptr;
+      static cudaEvent_t tev[kMaxGates + 3];
+      if (trace && !tev[0])
+        for (auto& e : tev) EVB_CUDA(cudaEventCreate(&e));
+      if (trace) EVB_CUDA(cudaEventRecord(tev[0], s->copy_stream));
       // the previous call on this scratch synchronised st, so dx is free to overwrite
       for (int c = 0; c < n_chunks; ++c) {
-        const int64_t c0 = int64_t(c) * cols, w = std::min<int64_t>(cols, D - c0);
-        EVB_CUDA(cudaMemcpy2DAsync(static_cast<uint8_t*>(s->dx) + c0 * es, ldd * es,
-                                   static_cast<const uint8_t*>(X_host) + c0 * es, ldx * es, w * es, n_points,
+        const int64_t b = c ? rq.kgate_end[c - 1] : 0, w = rq.kgate_end[c] - b;
+        EVB_CUDA(cudaMemcpy2DAsync(static_cast<uint8_t*>(s->dx) + b * es, ldd * es,
+                                   static_cast<const uint8_t*>(X_host) + b * es, ldx * es, w * es, n_points,
                                    cudaMemcpyHostToDevice, s->copy_stream));
-        if (wv(s->copy_stream, CUdeviceptr(s->gate + c), epoch, 0) != CUDA_SUCCESS)
+        EVB_CUDA(cudaEventRecord(s->ev_chunk[c], s->copy_stream));
+        EVB_CUDA(cudaStreamWaitEvent(s->gate_stream, s->ev_chunk[c], 0));
+        if (wv(s->gate_stream, CUdeviceptr(s->gate + c), epoch, 0) != CUDA_SUCCESS)
           throw runtime_error("evaluate_batch_host: cuStreamWriteValue32 failed");
+        if (trace) EVB_CUDA(cudaEventRecord(tev[1 + c], s->copy_stream));
       }
       EVB_CUDA(cudaEventRecord(s->ev_x_ready, s->copy_stream));
       rq.kgate = s->gate;
-      rq.kgate_cols = int(cols);
       rq.kgate_epoch = epoch;
       rq.x_ready = s->ev_x_ready;
+      if (trace) EVB_CUDA(cudaStreamWaitEvent(st, tev[0], 0));
       eval_dispatch(rq);
+      if (trace) EVB_CUDA(cudaEventRecord(tev[n_chunks + 1], st));
       EVB_CUDA(cudaStreamWaitEvent(st, s->ev_x_ready, 0));
+      if (trace) {
+        if (rq.out != out_host)
+          EVB_CUDA(cudaMemcpyAsync(out_host, s->dout, size_t(n_points) * es, cudaMemcpyDeviceToHost, st));
+        EVB_CUDA(cudaEventRecord(tev[n_chunks + 2], st));
+        EVB_CUDA(cudaStreamSynchronize(st));
+        std::string line = "[evb h2d]";
+        for (int c = 1; c <= n_chunks + 2; ++c) {
+          float ms = 0.f;
+          cudaEventElapsedTime(&ms, tev[0], tev[c]);
+          line += (c == n_chunks + 1 ? " kernel_end " : c == n_chunks + 2 ? " d2h_end " : " ") +
+                  std::to_string(int(ms * 1000.f));
+        }
+        std::fprintf(stderr, "%s us\n", line.c_str());
+      }
     } else {
-      EVB_CUDA(cudaMemcpy2DAsync(s->dx, ldd * es, X_host, ldx * es, D * es, n_points, cudaMemcpyHostToDevice, st));
+      // one linear copy when the rows are packed (the DMA engines run 2D copies of wide rows at
+      // about half the rate of a linear copy of the same bytes: 300 vs 160 us for 8 MB)
+      if (ldx == ldd)
+        EVB_CUDA(cudaMemcpyAsync(s->dx, X_host, size_t(ldd) * n_points * es, cudaMemcpyHostToDevice, st));
+      else
+        EVB_CUDA(cudaMemcpy2DAsync(s->dx, ldd * es, X_host, ldx * es, D * es, n_points, cudaMemcpyHostToDevice, st));
       eval_dispatch(rq);
     }
-    EVB_CUDA(cudaMemcpyAsync(out_host, s->dout, size_t(n_points) * es, cudaMemcpyDeviceToHost, st));
+    if (rq.out != out_host)
+      EVB_CUDA(cudaMemcpyAsync(out_host, s->dout, size_t(n_points) * es, cudaMemcpyDeviceToHost, st));
     EVB_CUDA(cudaStreamSynchronize(st));
   });
 }

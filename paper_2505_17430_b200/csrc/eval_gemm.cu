@@ -71,7 +71,8 @@ struct fused_params {
   int64_t ldz;
   const T* shift;  // padded with zeros beyond D
   const unsigned* kgate;  // non-null: X columns arrive in chunks (see eval_request)
-  int kgate_cols;
+  int kgate_n;
+  int kgate_end[8];
   unsigned kgate_epoch;
   int umma_variant;  // tf32 path: 0 = 3 products in one accumulator, 1 = + lo*lo, 2 = hi*hi and
                      // corrections in separate TMEM accumulators (summed in the epilogue)
@@ -308,15 +309,15 @@ __global__ void __launch_bounds__(f64_cfg<BM, BN, WM, WN, STAGES>::THREADS, MINB
     if (lane == 0) {
       ptx::prefetch_tma(&tmX);
       ptx::prefetch_tma(&tmM);
-      int ready_chunk = -1;
+      int chunk = 0, chunk_end = 0;  // columns [0, chunk_end) are resident
       for (int kb = 0; kb < KT; ++kb) {
         const int s = kb % STAGES;
         if (kb >= STAGES) ptx::mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
         if (p.kgate) {
-          const int c = (kb * C::KB) / p.kgate_cols;  // chunks are multiples of KB columns
-          if (c > ready_chunk) {
-            ptx::wait_gate(p.kgate + c, p.kgate_epoch);
-            ready_chunk = c;
+          while (kb * C::KB >= chunk_end) {  // chunk ends are multiples of KB columns
+            ptx::wait_gate(p.kgate + chunk, p.kgate_epoch);
+            chunk_end = chunk + 1 < p.kgate_n ? p.kgate_end[chunk] : 1 << 30;
+            ++chunk;
           }
         }
         uint8_t* st = smem + s * C::STAGE_BYTES;
@@ -1097,9 +1098,10 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
     fp.counters = sc->counters;
   }
   if constexpr (std::is_same<T, double>::value) {
-    if (!use_persistent && rq.kgate && rq.kgate_cols % 16 == 0) {
+    if (!use_persistent && rq.kgate) {
       fp.kgate = rq.kgate;
-      fp.kgate_cols = rq.kgate_cols;
+      fp.kgate_n = rq.kgate_n;
+      for (int c = 0; c < rq.kgate_n; ++c) fp.kgate_end[c] = rq.kgate_end[c];
       fp.kgate_epoch = rq.kgate_epoch;
       gate_consumed = true;
     }

@@ -154,10 +154,14 @@ struct evb_scratch_s {
   size_t s_lo_bytes = 0;
   // host-buffer path with the H2D copy overlapped: X arrives in column chunks on copy_stream,
   // each followed by a stream write of gate[c] = epoch that the GEMM producer waits on
+  // (gate writes are issued on gate_stream behind per-chunk events: a stream write between two
+  // copies on the copy stream stalls the DMA pipeline ~5 us per chunk)
   cudaStream_t copy_stream = nullptr;
+  cudaStream_t gate_stream = nullptr;
   unsigned* gate = nullptr;  // kMaxGates words
   unsigned gate_epoch = 0;
   cudaEvent_t ev_x_ready = nullptr;
+  cudaEvent_t ev_chunk[8] = {};
 };
 
 namespace evb {
@@ -201,12 +205,13 @@ struct eval_request {
   // kgate_epoch (wrap-safe compare); x_ready fires when all of X is resident.  Kernels that do
   // not consume the gates make the stream wait on x_ready instead.
   const unsigned* kgate = nullptr;
-  int kgate_cols = 0;
+  int kgate_n = 0;
+  int kgate_end[8] = {};  // exclusive end column of chunk c (multiples of 16 but the last)
   unsigned kgate_epoch = 0;
   cudaEvent_t x_ready = nullptr;
 };
 
-constexpr int kMaxGates = 64;
+constexpr int kMaxGates = 8;
 
 void eval_dispatch(const eval_request& rq);
 // true when eval_dispatch runs the request on the fused fp64 GEMM, whose producer honours kgate

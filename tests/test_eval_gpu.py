@@ -215,3 +215,21 @@ def test_host_path(config1):
     assert evb.batched_evaluate(p, np.zeros((0, 1000))).size == 0
     with pytest.raises(evb.InvalidArgument):
         evb.batched_evaluate(p, np.zeros((2, 7)))
+
+
+@pytest.mark.parametrize("kind", [K.elliptic, K.rastrigin, K.ackley, K.sphere])
+def test_host_path_overlapped_copy_bit_identical(config1, dev, kind):
+    # the host entry point streams X in column chunks gated per chunk into the fused fp64 GEMM:
+    # results must equal the device-resident path bit for bit, call after call (gate epochs)
+    o, m, X = config1
+    p = evb.ProblemInstance.base(kind, o, m, 10.0)
+    # (the tile shape, hence the fixed partial-sum grouping, depends on P: compare like with like)
+    want = {rows: gpu_eval(p, X[:rows], dev) for rows in (1024, 37, 64)}
+    sc = evb.EvalScratch()
+    for rows in (1024, 1024, 37, 1024):
+        got = evb.batched_evaluate(p, X[:rows], sc)
+        assert np.array_equal(got, want[rows])
+    wide = np.zeros((64, 1003))
+    wide[:, :1000] = X[:64]
+    got = evb.batched_evaluate(p, wide[:, :1000], sc)
+    assert np.array_equal(got, want[64])
