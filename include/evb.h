@@ -251,6 +251,25 @@ EVB_API int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int pop
                         double ub, void* pops, void* fits, int init, uint32_t gen0, evb_recorder rec,
                         void* stream);
 
+/* ---- suite-level grouped launch (experiment/runner.hpp:101-160 evo_bench) ----------------- */
+
+/* Philox key of task t: splitmix64(master_seed ^ t), the positional analogue of
+ * derive_stream(master_seed, t) (runner.hpp:119-120). */
+EVB_API uint64_t evb_task_key(uint64_t master_seed, uint64_t task_index);
+
+enum { EVB_BENCH_FORCE_ENGINE = 1 /* run every task through the per-generation engine */ };
+
+/* evo_bench(alg = DE config `cfg` with pop_size, suite, recorder, {runs, max_fes, master_seed}):
+ * problems[(p * instance_count) + i] is instance i of problem p (suite::at(p, i)); task
+ * t = ((p * instance_count) + i) * runs + r runs de_engine::optimize(max_fes) from Philox key
+ * evb_task_key(master_seed, t) and reports its evaluations, in FE order, to recorder run t (may
+ * be NULL), then on_run_end.  best_host (may be NULL): each task's best fitness.  *path_used:
+ * 1 = all tasks in one persistent launch (evb_de_runs), 2 = per-task engines. */
+EVB_API int evb_evo_bench_de(int dtype, const evb_de_config* cfg, int pop_size, int dim,
+                             const evb_problem* problems, int problem_count, int instance_count, int runs,
+                             int64_t max_fes, uint64_t master_seed, double lb, double ub, evb_recorder rec,
+                             double* best_host, int flags, int* path_used, void* stream);
+
 /* ---- PSO engine (pso/engine.hpp:33-153, pso/topology.hpp, pso/update.hpp) ------------------ */
 
 enum evb_pso_topology { EVB_TOPO_GBEST = 0 /* "gbest" */, EVB_TOPO_LBEST_RING = 1 /* "lbest_ring" */ };

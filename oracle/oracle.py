@@ -538,3 +538,38 @@ def _refde_native_trace(self, seed, stream, generations, lb, ub):
 
 
 RefDE.native_trace = _refde_native_trace
+
+
+register_ref({"ref_evo_bench_de": (i64, [c_double, c_double, c_int, c_int, c_int, vp, c_int, c_int, ctypes.c_longlong,
+                                         ctypes.c_longlong, vp, vp, vp, c_double, vp, vp, c_double, c_double, c_int,
+                                         vp, i64, vp])})
+
+
+def de_task_words(key: int, P: int, D: int, generations: int, mutation: int = 0) -> np.ndarray:
+    """The words a task's positional Philox stream yields in the reference's consumption order:
+    init_population (sub-stream 0xFFFFFFF0 of generation 0), then generations 1..G."""
+    parts = [philox_words(key, 0xFFFFFFF0, 0, P * D)]
+    for g in range(1, generations + 1):
+        parts.append(de_fixed_generation_words(mutation, key, g, P, D))
+    return np.concatenate(parts)
+
+
+def ref_evo_bench_de(f, cr, P, D, problem_ids, instances, runs, max_fes, interval, kinds, shifts, rots, bias,
+                     task_words, lb=-100.0, ub=100.0, threads=0):
+    """experiment::evo_bench with the `de` preset over a suite of base problems, the reference's
+    recorder attached; task t replays task_words[t].  Returns (csv, best per task)."""
+    n_problems = len(problem_ids)
+    ids = np.ascontiguousarray(problem_ids, np.int32)
+    k = np.ascontiguousarray(kinds, np.int32)
+    sh = np.ascontiguousarray(shifts, np.float64)
+    ro = np.ascontiguousarray(rots, np.float64)
+    words = np.ascontiguousarray(np.concatenate(task_words), np.uint64)
+    off = np.zeros(len(task_words) + 1, np.int64)
+    off[1:] = np.cumsum([len(w) for w in task_words])
+    best = np.zeros(len(task_words))
+    args = (f, cr, P, D, n_problems, ptr(ids), instances, runs, max_fes, interval, ptr(k), ptr(sh), ptr(ro), bias,
+            ptr(words), ptr(off), lb, ub, threads)
+    n = REF().ref_evo_bench_de(*args, None, 0, ptr(best))
+    buf = ctypes.create_string_buffer(int(n) + 1)
+    REF().ref_evo_bench_de(*args, buf, int(n), ptr(best))
+    return buf.raw[:n].decode(), best

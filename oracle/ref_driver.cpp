@@ -620,3 +620,37 @@ REF_API void ref_de_native_trace(void* h, uint64_t seed, uint64_t stream, int ge
   evolution_state st(1LL << 40, r->P, r->D, std::min(4, r->P));
   for (int g = 0; g < generations; ++g) r->engine->generation(r->pop, st, objective, lb, ub, rng);
 }
+
+// ---- evo_bench (experiment/runner.hpp:101-160) over a suite of base problems, `de` preset ------
+// The reference's own evo_bench + run_handle + best_so_far_record + de_engine::optimize; only the
+// random words are substituted: task t draws from rng_stream::scripted(words[off[t], off[t+1])),
+// the words the GPU's positional Philox stream of that task produces.  Returns the CSV length.
+REF_API int64_t ref_evo_bench_de(double f, double cr, int P, int D, int n_problems, const int* problem_ids,
+                                 int instances, int runs, long long max_fes, long long interval, const int* kinds,
+                                 const double* shifts, const double* rots, double bias, const uint64_t* words,
+                                 const int64_t* off, double lb, double ub, int threads, char* csv, int64_t cap,
+                                 double* best) {
+  std::vector<problem_instance<double>> inst;
+  for (int q = 0; q < n_problems * instances; ++q)
+    inst.push_back(make_base<double>(kinds[q], D, shifts + size_t(q) * D, rots + size_t(q) * D * D, bias));
+  problems::suite<double> su("gpu", D, std::vector<int>(problem_ids, problem_ids + n_problems), instances, 0,
+                             std::move(inst));
+  experiment::best_so_far_record<double> rec(su, runs, max_fes, interval);
+  experiment::bench_options opt;
+  opt.independent_runs = runs;
+  opt.max_fes = max_fes;
+  opt.threads = threads;
+  opt.parallel = threads != 1;
+  auto alg = [&](experiment::run_handle<double>& h) {
+    const auto& k = h.key();
+    const int64_t t = (int64_t(k.problem_ordinal) * instances + k.instance_ordinal) * runs + k.run_index;
+    rng_stream rng = rng_stream::scripted(std::vector<uint64_t>(words + off[t], words + off[t + 1]));
+    auto engine = presets::detail::build_de_fixed<double>(f, cr);
+    const auto b = engine.optimize(h, lb, ub, P, D, max_fes, rng, [](int, auto) {});
+    best[t] = b.fitness;
+  };
+  experiment::evo_bench<double>(alg, su, rec, opt);
+  const std::string s = rec.to_csv();
+  if (csv) std::memcpy(csv, s.data(), std::min<size_t>(size_t(cap), s.size()));
+  return int64_t(s.size());
+}

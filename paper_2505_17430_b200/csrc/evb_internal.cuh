@@ -223,6 +223,10 @@ void* recorder_view(evb_recorder_s* rec, int* n_ckpt, int64_t* interval, void** 
 int recorder_dtype(evb_recorder_s* rec);
 int recorder_runs(evb_recorder_s* rec);
 
+// batched-runs kernel eligibility (runs.cu): empty when supported, else the reason
+std::string runs_kernel_unsupported(int dtype, const evb_de_config* cfg, int pop_size, int dim,
+                                    const evb_problem* problems, int n_runs);
+
 // device generation counter <- host mirror (after host-side Philox consumers such as init)
 void set_device_gen(evb_rng_s* r, cudaStream_t st);
 

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <string>
 #include <vector>
 
 #include "evb_internal.cuh"
@@ -286,31 +287,47 @@ size_t runs_smem(int P, int D) {
 }  // namespace
 }  // namespace evb
 
+namespace evb {
+// Empty when the persistent runs kernel can execute this configuration, else the reason.
+std::string runs_kernel_unsupported(int dtype, const evb_de_config* cfg, int pop_size, int dim,
+                                    const evb_problem* problems, int n_runs) {
+  if (dtype != EVB_F64) return "de_runs: the persistent runs kernel is fp64";
+  if (cfg->mutation != EVB_MUT_RAND1 && cfg->mutation != EVB_MUT_BEST1)
+    return "de_runs: persistent kernel supports rand_1 / best_1 mutation";
+  if (cfg->parameter != EVB_PAR_FIXED) return "de_runs: persistent kernel supports the fixed adapter";
+  if (cfg->archive_rate != 0.0) return "de_runs: persistent kernel runs without an archive";
+  if (cfg->repair != EVB_REP_CLIP && cfg->repair != EVB_REP_MIDPOINT_TARGET) return "de_runs: clip or midpoint repair";
+  if (cfg->crossover != EVB_CX_BINOMIAL) return "de_runs: binomial crossover";
+  if (!(cfg->f > 0.0 && cfg->f <= 1.0)) return "fixed_parameter: F must be in (0,1]";
+  if (!(cfg->cr >= 0.0 && cfg->cr <= 1.0)) return "fixed_parameter: CR must be in [0,1]";
+  if (pop_size < (cfg->mutation == EVB_MUT_RAND1 ? 4 : 3)) return "de_engine: population too small for mutation";
+  if (dim < 1 || dim >= 65536) return "de_runs: bad sizes";
+  if (runs_smem(pop_size, dim) > 227 * 1024)
+    return "de_runs: run state does not fit in shared memory (use evb_de_generation)";
+  for (int r = 0; r < n_runs; ++r) {
+    const device_problem& p = problems[r]->p;
+    if (p.dtype != EVB_F64 || p.dim != dim) return "de_runs: problem dtype / dim mismatch";
+    if (p.spec == SPEC_HYBRID) return "de_runs: hybrid problems are not supported by the persistent kernel";
+    if (p.spec == SPEC_COMPOSITION && p.n_comp > kRunsMaxComp) return "de_runs: at most 4 composition components";
+  }
+  return {};
+}
+}  // namespace evb
+
 using namespace evb;
 
 extern "C" int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int pop_size, int dim,
                            const evb_problem* problems, const uint64_t* keys, int generations, double lb, double ub,
                            void* pops, void* fits, int init, uint32_t gen0, evb_recorder rec, void* stream) {
   return guarded([&] {
-    require(dtype == EVB_F64, "de_runs: the persistent runs kernel is fp64");
     require(cfg && problems && keys && pops && fits, "de_runs: null argument");
-    require(cfg->mutation == EVB_MUT_RAND1 || cfg->mutation == EVB_MUT_BEST1,
-            "de_runs: persistent kernel supports rand_1 / best_1 mutation");
-    require(cfg->parameter == EVB_PAR_FIXED, "de_runs: persistent kernel supports the fixed adapter");
-    require(cfg->archive_rate == 0.0, "de_runs: persistent kernel runs without an archive");
-    require(cfg->repair == EVB_REP_CLIP || cfg->repair == EVB_REP_MIDPOINT_TARGET, "de_runs: clip or midpoint repair");
-    require(cfg->crossover == EVB_CX_BINOMIAL, "de_runs: binomial crossover");
-    require(cfg->f > 0.0 && cfg->f <= 1.0, "fixed_parameter: F must be in (0,1]");
-    require(cfg->cr >= 0.0 && cfg->cr <= 1.0, "fixed_parameter: CR must be in [0,1]");
-    require(pop_size >= (cfg->mutation == EVB_MUT_RAND1 ? 4 : 3), "de_engine: population too small for mutation");
     require(n_runs >= 1 && dim >= 1 && dim < 65536 && generations >= 0, "de_runs: bad sizes");
+    const std::string why = runs_kernel_unsupported(dtype, cfg, pop_size, dim, problems, n_runs);
+    if (!why.empty()) throw config_error(why);
     const size_t smem = runs_smem(pop_size, dim);
-    require(smem <= 227 * 1024, "de_runs: run state does not fit in shared memory (use evb_de_generation)");
     std::vector<run_problem> rp(n_runs);
     for (int r = 0; r < n_runs; ++r) {
       const device_problem& p = problems[r]->p;
-      require(p.dtype == EVB_F64 && p.dim == dim, "de_runs: problem dtype / dim mismatch");
-      require(p.spec != SPEC_HYBRID, "de_runs: hybrid problems are not supported by the persistent kernel");
       run_problem& q = rp[r];
       q.bias = p.bias;
       q.ld = p.ld;
@@ -321,7 +338,6 @@ extern "C" int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int 
         q.rot[0] = static_cast<const double*>(p.rotation);
         q.kind[0] = p.kind;
       } else {
-        require(p.n_comp <= kRunsMaxComp, "de_runs: at most 4 composition components");
         q.n_comp = p.n_comp;
         std::vector<int> kinds(p.n_comp);
         std::vector<double> sg(p.n_comp), la(p.n_comp), cb(p.n_comp);

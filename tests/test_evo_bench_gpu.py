@@ -1,0 +1,108 @@
+"""GPU parity of the suite-level grouped launch (csrc/evo_bench.cu) against the
+reference's own experiment::evo_bench (experiment/runner.hpp:101-160) with its
+best_so_far_record and de_engine::optimize (oracle/_ref ref_evo_bench_de): the same suite, the
+`de` preset, each task replaying the words of the GPU task's positional Philox stream.  The CSV
+(experiment/recorder.hpp:103-121) produced on the GPU must match the reference's row for row."""
+import numpy as np
+import pytest
+
+import oracle as O
+
+torch = pytest.importorskip("torch")
+import paper_2505_17430_b200 as evb  # noqa: E402
+from paper_2505_17430_b200.de import preset_de, preset_shade  # noqa: E402
+from paper_2505_17430_b200.experiment import evo_bench_de, task_key  # noqa: E402
+from paper_2505_17430_b200.recorder import BestSoFarRecorder  # noqa: E402
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")]
+
+K = evb.BaseKind
+
+
+def csv_close(a, b, tol):
+    ra, rb = a.splitlines(), b.splitlines()
+    assert len(ra) == len(rb) and ra[0] == rb[0] and a.endswith("\n")
+    worst = 0.0
+    for x, y in zip(ra[1:], rb[1:]):
+        fx, fy = x.split(","), y.split(",")
+        assert fx[:-1] == fy[:-1], (x, y)
+        worst = max(worst, abs(float(fx[-1]) - float(fy[-1])) / max(1.0, abs(float(fy[-1]))))
+    return worst <= tol
+
+
+def make_suite(D, kinds, instances):
+    suite, flat = [], []
+    for p, kind in enumerate(kinds):
+        row = []
+        for i in range(instances):
+            o, m = O.shift_rotation(500 + 10 * p + i, D)
+            row.append(evb.ProblemInstance.base(kind, o, m, 0.0))
+            flat.append((int(kind), o, m))
+        suite.append(row)
+    return suite, flat
+
+
+@pytest.mark.parametrize("D,P,max_fes,interval", [(10, 20, 20 * 25 + 7, 50), (30, 24, 24 * 40, 96)])
+def test_evo_bench_matches_reference(dev, D, P, max_fes, interval):
+    kinds, ids, instances, runs, seed = [K.rastrigin, K.ackley], [5, 6], 2, 3, 99
+    suite, flat = make_suite(D, kinds, instances)
+    tasks = len(kinds) * instances * runs
+    rec = BestSoFarRecorder(tasks, max_fes, interval)
+    res = evo_bench_de(preset_de(0.5, 0.9), P, suite, runs, max_fes, master_seed=seed, recorder=rec)
+    assert res["path"] == "batched"
+    gpu_csv = rec.to_csv("gpu", D, ids, instances, runs)
+    gens = max(0, -(-(max_fes - P) // P))
+    words = [O.de_task_words(task_key(seed, t), P, D, gens) for t in range(tasks)]
+    ref_csv, ref_best = O.ref_evo_bench_de(0.5, 0.9, P, D, ids, instances, runs, max_fes, interval,
+                                           [k for k, _, _ in flat], np.stack([o for _, o, _ in flat]),
+                                           np.stack([m for _, _, m in flat]), 0.0, words)
+    # exact-order arithmetic; fitness differs from libm only in cos/exp ulps
+    assert csv_close(gpu_csv, ref_csv, 1e-10)
+    assert np.all(np.abs(res["best"] - ref_best) <= 1e-10 * np.maximum(1.0, np.abs(ref_best)))
+    grid, fes = rec.grid()
+    assert list(fes) == [P * (gens + 1)] * tasks
+    # the last checkpoint is at (max_fes // interval) * interval FEs; trials past it can still improve
+    if (max_fes // interval) * interval == P * (gens + 1):
+        assert np.array_equal(grid[:, -1], res["best"])
+    else:
+        assert np.all(grid[:, -1] >= res["best"])
+
+
+def test_batched_and_engine_paths_agree(dev):
+    # the persistent kernel and the per-generation engine consume the same positional stream
+    D, P, max_fes, interval, runs = 12, 16, 16 * 20, 32, 2
+    suite, _ = make_suite(D, [K.ackley, K.rastrigin], 2)
+    grids = []
+    for force in (False, True):
+        rec = BestSoFarRecorder(8, max_fes, interval)
+        res = evo_bench_de(preset_de(0.5, 0.9), P, suite, runs, max_fes, master_seed=3, recorder=rec,
+                           force_engine=force)
+        assert res["path"] == ("engine" if force else "batched")
+        grids.append((rec.grid()[0], res["best"]))
+    (g0, b0), (g1, b1) = grids
+    assert np.allclose(g0, g1, rtol=1e-12, atol=0) and np.allclose(b0, b1, rtol=1e-12, atol=0)
+
+
+def test_engine_path_shade(dev):
+    # configurations outside the persistent kernel (SHADE + archive) run per task on the engine
+    D, P, max_fes, runs = 20, 30, 30 * 12, 2
+    suite, _ = make_suite(D, [K.elliptic], 3)
+    rec = BestSoFarRecorder(6, max_fes, 30)
+    res = evo_bench_de(preset_shade(0.11, P, 1.0), P, suite, runs, max_fes, master_seed=5, recorder=rec)
+    assert res["path"] == "engine"
+    grid, fes = rec.grid()
+    assert np.all(fes == max_fes)
+    assert np.all(np.diff(grid, axis=1) <= 0)
+    assert np.array_equal(grid[:, -1], res["best"])
+    csv = rec.to_csv("cec", D, [2], 3, runs)
+    assert csv.count("\n") == 1 + 6 * 12
+
+
+def test_evo_bench_errors(dev):
+    suite, _ = make_suite(10, [K.sphere], 1)
+    with pytest.raises(evb.ConfigError):
+        evo_bench_de(preset_de(), 20, suite, 0, 100)
+    with pytest.raises(evb.ConfigError):
+        evo_bench_de(preset_de(), 20, suite, 1, 0)
+    with pytest.raises(evb.ConfigError):
+        evo_bench_de(preset_de(), 3, suite, 1, 100)
