@@ -180,9 +180,10 @@ EVB_API int evb_recorder_csv(evb_recorder r, const char* suite_name, int dim, in
 /* strategy slots, by the reference's names (de/strategy.hpp, de/parameter.hpp) */
 enum evb_de_mutation { EVB_MUT_RAND1 = 0 /* "rand_1" */, EVB_MUT_BEST1 = 1 /* "best_1" */,
                        EVB_MUT_TTPB1 = 2 /* "ttpb_1" */ };
-enum evb_de_crossover { EVB_CX_BINOMIAL = 0 /* "binomial" */ };
+enum evb_de_crossover { EVB_CX_BINOMIAL = 0 /* "binomial" */, EVB_CX_EXPONENTIAL = 1 /* "exponential" */ };
 enum evb_de_repair { EVB_REP_CLIP = 0 /* "clip" */, EVB_REP_REFLECT = 1 /* "reflect" */,
-                     EVB_REP_MIDPOINT_TARGET = 2 /* "midpoint_target" */ };
+                     EVB_REP_MIDPOINT_TARGET = 2 /* "midpoint_target" */,
+                     EVB_REP_REINITIALIZE = 3 /* "reinitialize" */ };
 enum evb_de_parameter { EVB_PAR_FIXED = 0 /* "fixed" */, EVB_PAR_JADE = 1 /* "jade" */,
                         EVB_PAR_SHADE = 2 /* "shade" */ };
 

@@ -521,7 +521,8 @@ ORC_API void orc_eval_composition_f32(int dim, int n_comp, const int* kinds, con
  * DE engine (de/engine.hpp, de/strategy.hpp, de/parameter.hpp) — fp64, restated
  * ---------------------------------------------------------------------------------------- */
 enum { ORC_MUT_RAND1 = 0, ORC_MUT_BEST1 = 1, ORC_MUT_TTPB1 = 2 };
-enum { ORC_REP_CLIP = 0, ORC_REP_REFLECT = 1, ORC_REP_MIDPOINT = 2 };
+enum { ORC_REP_CLIP = 0, ORC_REP_REFLECT = 1, ORC_REP_MIDPOINT = 2, ORC_REP_REINIT = 3 };
+enum { ORC_CX_BINOMIAL = 0, ORC_CX_EXPONENTIAL = 1 };
 enum { ORC_PAR_FIXED = 0, ORC_PAR_JADE = 1, ORC_PAR_SHADE = 2 };
 
 typedef struct {
@@ -538,6 +539,7 @@ typedef struct {
   int n_comp;
   const int* comp_kinds;
   const double *comp_shifts, *comp_rots, *sigma, *lambda, *cbias;
+  int crossover; /* ORC_CX_* */
 } orc_de_cfg;
 
 typedef struct {
@@ -643,12 +645,21 @@ ORC_API int64_t orc_de_generation(const orc_de_cfg* c, orc_de_state* s, orc_rng*
       xc = cc < P ? s->pop + (size_t)cc * D : s->archive + (size_t)(cc - P) * D;
       for (int j = 0; j < D; ++j) donor[j] = xi[j] + F * (xa[j] - xi[j]) + F * (xb[j] - xc[j]);
     }
-    /* binomial crossover, de/strategy.hpp:184-194 */
     const int jr = uniform_int(r, D);
     double* t = trials + (size_t)i * D;
-    for (int j = 0; j < D; ++j) {
-      const double u = uniform01(r);
-      t[j] = (u < CR || j == jr) ? donor[j] : xi[j];
+    if (c->crossover == ORC_CX_EXPONENTIAL) { /* de/strategy.hpp:203-214 */
+      memcpy(t, xi, sizeof(double) * D);
+      int length = 0;
+      do {
+        const int j = (jr + length) % D;
+        t[j] = donor[j];
+        ++length;
+      } while (length < D && uniform01(r) < CR);
+    } else { /* binomial crossover, de/strategy.hpp:184-194 */
+      for (int j = 0; j < D; ++j) {
+        const double u = uniform01(r);
+        t[j] = (u < CR || j == jr) ? donor[j] : xi[j];
+      }
     }
     /* repair, de/strategy.hpp:229-277 */
     for (int j = 0; j < D; ++j) {
@@ -659,6 +670,8 @@ ORC_API int64_t orc_de_generation(const orc_de_cfg* c, orc_de_state* s, orc_rng*
       } else if (c->repair == ORC_REP_MIDPOINT) {
         if (g < lb) g = (lb + xi[j]) / 2.0;
         else if (g > ub) g = (ub + xi[j]) / 2.0;
+      } else if (c->repair == ORC_REP_REINIT) { /* de/strategy.hpp:285-289 */
+        if (g < lb || g > ub) g = lb + (ub - lb) * uniform01(r);
       } else {
         for (int fold = 0; (g < lb || g > ub) && fold < 100; ++fold) {
           if (g < lb) g = lb + (lb - g);

@@ -239,7 +239,7 @@ def eval_composition(kinds, shifts, rots, sigma, lam, cbias, bias, X):
 # ---- DE: the reference engine (REF) and the C restatement (C) -------------------------------------
 REF_DE_SIG = {
     "ref_de_create": (vp, [c_int, c_int, c_int, c_double, c_double, c_double, c_int, c_int, c_double, c_double,
-                           c_int, c_int]),
+                           c_int, c_int, c_int]),
     "ref_de_destroy": (None, [vp]),
     "ref_de_set_problem_base": (None, [vp, c_int, vp, vp, c_double]),
     "ref_de_set_problem_composition": (None, [vp, c_int, vp, vp, vp, vp, vp, vp, c_double]),
@@ -252,7 +252,8 @@ REF_DE_SIG = {
 register_ref(REF_DE_SIG)
 
 MUT = {"rand_1": 0, "best_1": 1, "ttpb_1": 2}
-REP = {"clip": 0, "reflect": 1, "midpoint_target": 2}
+REP = {"clip": 0, "reflect": 1, "midpoint_target": 2, "reinitialize": 3}
+CX = {"binomial": 0, "exponential": 1}
 ADA = {"fixed": 0, "jade": 1, "shade": 2}
 
 
@@ -264,7 +265,8 @@ class RefDE:
         self.P, self.D, self.cfg = P, D, cfg
         self.H = max(1, cfg.memory_size if cfg.parameter == "shade" else 1)
         self.h = REF().ref_de_create(MUT[cfg.mutation], REP[cfg.repair], ADA[cfg.parameter], cfg.f, cfg.cr,
-                                     cfg.p_best, int(cfg.use_archive), self.H, cfg.jade_c, cfg.archive_rate, P, D)
+                                     cfg.p_best, int(cfg.use_archive), self.H, cfg.jade_c, cfg.archive_rate, P, D,
+                                     CX[cfg.crossover])
         self._keep = []
 
     def set_problem_base(self, kind, shift, rot, bias):
@@ -320,7 +322,7 @@ class _OrcDeCfg(ctypes.Structure):
                 ("p", c_double), ("use_archive", c_int), ("H", c_int), ("jade_c", c_double), ("P", c_int),
                 ("D", c_int), ("archive_cap", c_int), ("kind", c_int), ("shift", vp), ("rot", vp),
                 ("bias", c_double), ("n_comp", c_int), ("comp_kinds", vp), ("comp_shifts", vp), ("comp_rots", vp),
-                ("sigma", vp), ("lambda_", vp), ("cbias", vp)]
+                ("sigma", vp), ("lambda_", vp), ("cbias", vp), ("crossover", c_int)]
 
 
 class _OrcDeState(ctypes.Structure):
@@ -348,6 +350,7 @@ class OracleDE:
         self.c = _OrcDeCfg(MUT[cfg.mutation], REP[cfg.repair], ADA[cfg.parameter], cfg.f, cfg.cr, cfg.p_best,
                            int(cfg.use_archive), self.H, cfg.jade_c, P, D, self.cap)
         self.c.kind = -1
+        self.c.crossover = CX[cfg.crossover]
         self.pop = np.zeros((P, D))
         self.fit = np.zeros(P)
         self.archive = np.zeros((max(1, self.cap), D))

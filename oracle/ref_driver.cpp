@@ -231,6 +231,7 @@ std::unique_ptr<de::mutation_strategy<double>> make_mutation(int m, double p, in
 std::unique_ptr<de::repair_strategy<double>> make_repair(int r) {
   if (r == 0) return std::make_unique<de::clip_repair<double>>();
   if (r == 1) return std::make_unique<de::reflect_repair<double>>();
+  if (r == 3) return std::make_unique<de::reinitialize_repair<double>>();
   return std::make_unique<de::midpoint_target_repair<double>>();
 }
 std::unique_ptr<de::parameter_adapter<double>> make_adapter(int a, double f, double cr, int H, double c) {
@@ -243,11 +244,13 @@ std::unique_ptr<de::parameter_adapter<double>> make_adapter(int a, double f, dou
 
 // Engine built through the reference de_builder from the same strategy choices as evb_de_config.
 REF_API void* ref_de_create(int mutation, int repair, int adapter, double f, double cr, double p, int use_archive,
-                            int H, double jade_c, double archive_rate, int P, int D) {
+                            int H, double jade_c, double archive_rate, int P, int D, int crossover) {
   auto* r = new ref_de_run();
   r->engine = std::make_unique<de::de_engine<double>>(de::de_builder<double>()
                                                           .mutation(make_mutation(mutation, p, use_archive))
-                                                          .crossover(std::make_unique<de::binomial_crossover<double>>())
+                                                          .crossover(crossover == 1 ? std::unique_ptr<de::crossover_strategy<double>>(
+                                                                                          std::make_unique<de::exponential_crossover<double>>())
+                                                                                    : std::make_unique<de::binomial_crossover<double>>())
                                                           .repair(make_repair(repair))
                                                           .parameter(make_adapter(adapter, f, cr, H, jade_c))
                                                           .population(de::population_policy::fixed())

@@ -60,7 +60,9 @@ struct evb_de_s {
   void* CR = nullptr;         // P (T)
   int* slot = nullptr;        // P
   int* idx = nullptr;         // P x 4 (r1, r2, r3 | pbest, r1, r2)
-  int* jrand = nullptr;       // P
+  int* jrand = nullptr;       // P (binomial jrand / exponential start)
+  int* xlen = nullptr;        // P: exponential crossover block length
+  int64_t* rword = nullptr;   // P: stream index of the first reinitialize-repair word
   int64_t* woff = nullptr;    // P: first gene-uniform word (WORDS) / scalar word count (PHILOX)
   int64_t* wcount = nullptr;  // P: words consumed by individual i
   int* order = nullptr;       // p_count
@@ -113,6 +115,8 @@ struct de_dev {
   int* slot;
   int* idx;
   int* jrand;
+  int* xlen;
+  int64_t* rword;
   int64_t* woff;
   int64_t* wcount;
   int* order;
@@ -210,7 +214,17 @@ __device__ void draw_scalars(const de_dev<T>& d, int i, int arch_size, R& r) {
     const int pool = ps + (d.cfg.use_archive ? arch_size : 0);
     do { c = draw_int(r, pool); } while (c == i || c == b);
   }
-  const int jr = draw_int(r, d.D);  // de/strategy.hpp:187
+  const int jr = draw_int(r, d.D);  // binomial jrand (de/strategy.hpp:187) / exponential start (:207)
+  if (d.cfg.crossover == EVB_CX_EXPONENTIAL) {
+    // block length: extended while length < D and u < CR (de/strategy.hpp:208-213); the u's are
+    // consumed here, so the trial kernel needs no gene words
+    int L = 1;
+    while (L < d.D) {
+      if (!(draw_uniform01(r) < double(CR))) break;
+      ++L;
+    }
+    d.xlen[i] = L;
+  }
   d.F[i] = F;
   d.CR[i] = CR;
   d.slot[i] = slot;
@@ -228,8 +242,26 @@ __global__ void de_draw_philox_kernel(const de_dev<T> d) {
   const uint32_t gen = *d.gen_ptr;
   word_reader r{&d.src, (uint64_t(gen) << 32) | uint32_t(i), 0, 0, d.overflow};
   draw_scalars<T>(d, i, arch_size, r);
-  d.woff[i] = r.count;  // gene uniforms start after the scalar words
-  d.wcount[i] = r.count + d.D;
+  const int64_t xw = d.cfg.crossover == EVB_CX_BINOMIAL ? d.D : 0;  // gene uniforms follow the scalars
+  d.woff[i] = r.count;
+  d.rword[i] = r.count + xw;
+  d.wcount[i] = r.count + xw;  // + reinitialize-repair words, counted by the trial kernel
+}
+
+// Pre-repair trial gene j of individual i (mutation + crossover choice), for the sequential
+// WORDS walk of reinitialize repair; `take` = the crossover picked the donor gene.
+template <typename T>
+__device__ T trial_gene_pre(const de_dev<T>& d, int i, int j, bool take) {
+  using F_ = fop<T>;
+  const T* xi = d.pop + size_t(i) * d.ldp;
+  if (!take) return xi[j];
+  const int a = d.idx[4 * i + 0], b = d.idx[4 * i + 1], c = d.idx[4 * i + 2];
+  const T Fi = d.F[i];
+  const T xa = d.pop[size_t(a) * d.ldp + j], xb = d.pop[size_t(b) * d.ldp + j];
+  const T xc = (d.cfg.mutation == EVB_MUT_TTPB1 && c >= d.P) ? d.archive[size_t(c - d.P) * d.ldt + j]
+                                                               : d.pop[size_t(c) * d.ldp + j];
+  if (d.cfg.mutation == EVB_MUT_TTPB1) return F_::add(F_::add(xi[j], F_::mul(Fi, F_::sub(xa, xi[j]))), F_::mul(Fi, F_::sub(xb, xc)));
+  return F_::add(xa, F_::mul(Fi, F_::sub(xb, xc)));
 }
 
 template <typename T>
@@ -240,16 +272,57 @@ __global__ void de_draw_words_kernel(const de_dev<T> d) {
   for (int i = 0; i < d.P; ++i) {
     word_reader r{&d.src, 0, pos, 0, d.overflow};
     draw_scalars<T>(d, i, arch_size, r);
+    const int64_t xw = d.cfg.crossover == EVB_CX_BINOMIAL ? d.D : 0;
     d.woff[i] = r.pos;
-    d.wcount[i] = r.count + d.D;
-    pos = r.pos + d.D;
+    d.rword[i] = r.pos + xw;
+    int64_t nviol = 0;
+    if (d.cfg.repair == EVB_REP_REINITIALIZE) {
+      // the next individual's words start after this one's repair words: walk its trial here
+      const double cr = double(d.CR[i]);
+      const int jr = d.jrand[i], L = d.cfg.crossover == EVB_CX_EXPONENTIAL ? d.xlen[i] : 0;
+      for (int j = 0; j < d.D; ++j) {
+        bool take;
+        if (d.cfg.crossover == EVB_CX_BINOMIAL) {
+          const int64_t q = r.pos + j;
+          take = (q < d.src.n_words ? u01_of(d.src.words[q]) < cr : false) || j == jr;
+        } else {
+          take = ((j - jr + d.D) % d.D) < L;
+        }
+        const T v = trial_gene_pre<T>(d, i, j, take);
+        if (v < d.lb || v > d.ub) ++nviol;
+      }
+    }
+    d.wcount[i] = r.count + xw + nviol;
+    pos = r.pos + xw + nviol;
   }
   *d.cursor = pos;
   if (pos > d.src.n_words) *d.overflow = 1;
 }
 
-// K4: donor + binomial crossover + repair.  Block per individual; each thread owns one Philox
-// block (two consecutive stream words) and so up to two genes.
+// K4: donor + crossover + repair.  Block per individual.  Binomial: each thread owns one Philox
+// block (two consecutive stream words) and so up to two genes.  Exponential: the block
+// [start, start + L) mod D was sized by the draw kernel.  Reinitialize repair: the violating
+// genes, in j order, take the words after the crossover words (block prefix count).
+template <typename T>
+__device__ __forceinline__ T repair_gene(int repair, T v, T xij, T lb, T ub) {
+  using F_ = fop<T>;
+  if (repair == EVB_REP_CLIP) {  // de/strategy.hpp:236-239
+    if (v < lb) v = lb;
+    if (v > ub) v = ub;
+  } else if (repair == EVB_REP_MIDPOINT_TARGET) {  // de/strategy.hpp:270-275
+    if (v < lb) v = F_::div(F_::add(lb, xij), T(2));
+    else if (v > ub) v = F_::div(F_::add(ub, xij), T(2));
+  } else if (repair == EVB_REP_REFLECT) {  // de/strategy.hpp:250-257
+    for (int fold = 0; (v < lb || v > ub) && fold < 100; ++fold) {
+      if (v < lb) v = F_::add(lb, F_::sub(lb, v));
+      if (v > ub) v = F_::sub(ub, F_::sub(v, ub));
+    }
+    if (v < lb) v = lb;
+    if (v > ub) v = ub;
+  }  // reinitialize: second pass
+  return v;
+}
+
 template <typename T>
 __global__ void de_trial_kernel(const de_dev<T> d) {
   using F_ = fop<T>;
@@ -265,54 +338,83 @@ __global__ void de_trial_kernel(const de_dev<T> d) {
   const T* xc = (d.cfg.mutation == EVB_MUT_TTPB1 && c >= d.P) ? d.archive + size_t(c - d.P) * d.ldt
                                                                 : d.pop + size_t(c) * d.ldp;
   T* out = d.trial + size_t(i) * d.ldt;
-  const int64_t s0 = d.woff[i];  // stream index of gene 0's uniform
   const uint64_t ctr_hi = (uint64_t(*d.gen_ptr) << 32) | uint32_t(i);
   const T lb = d.lb, ub = d.ub;
-  // Philox blocks covering stream words [s0, s0 + D)
-  const int64_t blk0 = s0 >> 1;
-  const int64_t nblk = ((s0 + D + 1) >> 1) - blk0;
-  for (int64_t q = threadIdx.x; q < nblk; q += blockDim.x) {
-    uint64_t w[2];
-    const int64_t n0 = (blk0 + q) * 2;
-    if (d.src.mode == RNG_PHILOX) {
-      philox_pair(d.src.key, ctr_hi, uint64_t(blk0 + q), w[0], w[1]);
+  const int repair = d.cfg.repair;
+  auto gene = [&](int j, bool take) {
+    T v;
+    if (take) {
+      if (d.cfg.mutation == EVB_MUT_TTPB1)  // x_i + F(x_pb - x_i) + F(x_r1 - x~_r2), de/strategy.hpp:159
+        v = F_::add(F_::add(xi[j], F_::mul(Fi, F_::sub(xa[j], xi[j]))), F_::mul(Fi, F_::sub(xb[j], xc[j])));
+      else  // x_a + F(x_b - x_c), de/strategy.hpp:93 / :117
+        v = F_::add(xa[j], F_::mul(Fi, F_::sub(xb[j], xc[j])));
     } else {
-      // WORDS: s0 is the absolute list position of gene 0
-      w[0] = (n0 >= s0 && n0 < s0 + D && n0 < d.src.n_words) ? d.src.words[n0] : 0;
-      w[1] = (n0 + 1 >= s0 && n0 + 1 < s0 + D && n0 + 1 < d.src.n_words) ? d.src.words[n0 + 1] : 0;
+      v = xi[j];
     }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int64_t j64 = n0 + h - s0;
-      if (j64 < 0 || j64 >= D) continue;
-      const int j = int(j64);
-      const double u = u01_of(w[h]);
-      T v;
-      if (u < cr || j == jr) {
-        if (d.cfg.mutation == EVB_MUT_TTPB1)  // x_i + F(x_pb - x_i) + F(x_r1 - x~_r2), de/strategy.hpp:159
-          v = F_::add(F_::add(xi[j], F_::mul(Fi, F_::sub(xa[j], xi[j]))), F_::mul(Fi, F_::sub(xb[j], xc[j])));
-        else  // x_a + F(x_b - x_c), de/strategy.hpp:93 / :117
-          v = F_::add(xa[j], F_::mul(Fi, F_::sub(xb[j], xc[j])));
+    out[j] = repair_gene<T>(repair, v, xi[j], lb, ub);
+  };
+  if (d.cfg.crossover == EVB_CX_BINOMIAL) {
+    const int64_t s0 = d.woff[i];  // stream index of gene 0's uniform
+    // Philox blocks covering stream words [s0, s0 + D)
+    const int64_t blk0 = s0 >> 1;
+    const int64_t nblk = ((s0 + D + 1) >> 1) - blk0;
+    for (int64_t q = threadIdx.x; q < nblk; q += blockDim.x) {
+      uint64_t w[2];
+      const int64_t n0 = (blk0 + q) * 2;
+      if (d.src.mode == RNG_PHILOX) {
+        philox_pair(d.src.key, ctr_hi, uint64_t(blk0 + q), w[0], w[1]);
       } else {
-        v = xi[j];
+        // WORDS: s0 is the absolute list position of gene 0
+        w[0] = (n0 >= s0 && n0 < s0 + D && n0 < d.src.n_words) ? d.src.words[n0] : 0;
+        w[1] = (n0 + 1 >= s0 && n0 + 1 < s0 + D && n0 + 1 < d.src.n_words) ? d.src.words[n0 + 1] : 0;
       }
-      if (d.cfg.repair == EVB_REP_CLIP) {  // de/strategy.hpp:236-239
-        if (v < lb) v = lb;
-        if (v > ub) v = ub;
-      } else if (d.cfg.repair == EVB_REP_MIDPOINT_TARGET) {  // de/strategy.hpp:270-275
-        if (v < lb) v = F_::div(F_::add(lb, xi[j]), T(2));
-        else if (v > ub) v = F_::div(F_::add(ub, xi[j]), T(2));
-      } else if (d.cfg.repair == EVB_REP_REFLECT) {  // de/strategy.hpp:250-257
-        for (int fold = 0; (v < lb || v > ub) && fold < 100; ++fold) {
-          if (v < lb) v = F_::add(lb, F_::sub(lb, v));
-          if (v > ub) v = F_::sub(ub, F_::sub(v, ub));
-        }
-        if (v < lb) v = lb;
-        if (v > ub) v = ub;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t j64 = n0 + h - s0;
+        if (j64 < 0 || j64 >= D) continue;
+        const int j = int(j64);
+        gene(j, u01_of(w[h]) < cr || j == jr);
       }
-      out[j] = v;
     }
+  } else {  // exponential, de/strategy.hpp:203-214
+    const int L = d.xlen[i];
+    for (int j = threadIdx.x; j < D; j += blockDim.x) gene(j, ((j - jr + D) % D) < L);
   }
+  if (repair != EVB_REP_REINITIALIZE) return;
+  // reinitialize repair (de/strategy.hpp:285-289): g = T(uniform(lb, ub)) per violating gene, in j order
+  __shared__ int warp_tot[32];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  const int64_t r0 = d.rword[i];
+  int running = 0;
+  for (int base = 0; base < D; base += blockDim.x) {
+    const int j = base + threadIdx.x;
+    const bool viol = j < D && (out[j] < lb || out[j] > ub);
+    const unsigned m = __ballot_sync(0xffffffffu, viol);
+    if (lane == 0) warp_tot[warp] = __popc(m);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int w = 0; w < nw; ++w) {
+      before += w < warp ? warp_tot[w] : 0;
+      total += warp_tot[w];
+    }
+    if (viol) {
+      const int64_t s = r0 + running + before + __popc(m & ((1u << lane) - 1u));
+      uint64_t word;
+      if (d.src.mode == RNG_PHILOX) {
+        uint64_t w2[2];
+        philox_pair(d.src.key, ctr_hi, uint64_t(s >> 1), w2[0], w2[1]);
+        word = w2[s & 1];
+      } else {
+        word = s < d.src.n_words ? d.src.words[s] : 0;
+        if (s >= d.src.n_words) *d.overflow = 1;
+      }
+      out[j] = T(__dadd_rn(double(lb), __dmul_rn(__dsub_rn(double(ub), double(lb)), u01_of(word))));
+    }
+    running += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && d.src.mode == RNG_PHILOX) d.wcount[i] = r0 + running;
 }
 
 // K5a: selection bookkeeping (de/engine.hpp:27-47, de/strategy.hpp:29-37, de/parameter.hpp:166-184)
@@ -507,6 +609,8 @@ de_dev<T> make_dev(evb_de_s* e, void* pop, int64_t ldp, void* fit, double lb, do
   d.slot = e->slot;
   d.idx = e->idx;
   d.jrand = e->jrand;
+  d.xlen = e->xlen;
+  d.rword = e->rword;
   d.woff = e->woff;
   d.wcount = e->wcount;
   d.order = e->order;
@@ -636,7 +740,7 @@ void* dalloc(size_t n) {
 void free_de(evb_de_s* e) {
   if (e->graph) cudaGraphExecDestroy(e->graph);
   if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
-  void* ptrs[] = {e->trial, e->trial_fit, e->F, e->CR, e->slot, e->idx, e->jrand, e->woff, e->wcount, e->order,
+  void* ptrs[] = {e->trial, e->trial_fit, e->F, e->CR, e->slot, e->idx, e->jrand, e->xlen, e->rword, e->woff, e->wcount, e->order,
                   e->win, e->arch_slot, e->owner, e->succ, e->archive, e->d_arch_size, e->d_write_index,
                   e->d_arch_words, e->mem_f, e->mem_cr};
   for (void* p : ptrs)
@@ -739,9 +843,11 @@ int evb_de_create(int dtype, const evb_de_config* c, int pop_size, int dim, evb_
     require(c != nullptr && out != nullptr, "de: null config or output handle");
     require(c->mutation == EVB_MUT_RAND1 || c->mutation == EVB_MUT_BEST1 || c->mutation == EVB_MUT_TTPB1,
             "de builder: unknown mutation strategy (GPU kernels: rand_1, best_1, ttpb_1)");
-    require(c->crossover == EVB_CX_BINOMIAL, "de builder: unknown crossover strategy (GPU kernels: binomial)");
-    require(c->repair == EVB_REP_CLIP || c->repair == EVB_REP_REFLECT || c->repair == EVB_REP_MIDPOINT_TARGET,
-            "de builder: unknown repair strategy (GPU kernels: clip, reflect, midpoint_target)");
+    require(c->crossover == EVB_CX_BINOMIAL || c->crossover == EVB_CX_EXPONENTIAL,
+            "de builder: unknown crossover strategy (GPU kernels: binomial, exponential)");
+    require(c->repair == EVB_REP_CLIP || c->repair == EVB_REP_REFLECT || c->repair == EVB_REP_MIDPOINT_TARGET ||
+                c->repair == EVB_REP_REINITIALIZE,
+            "de builder: unknown repair strategy (GPU kernels: clip, reflect, midpoint_target, reinitialize)");
     require(c->parameter == EVB_PAR_FIXED || c->parameter == EVB_PAR_JADE || c->parameter == EVB_PAR_SHADE,
             "de builder: unknown parameter adapter (GPU kernels: fixed, jade, shade)");
     if (c->parameter == EVB_PAR_FIXED) {  // de/parameter.hpp:81-84
@@ -793,6 +899,8 @@ int evb_de_create(int dtype, const evb_de_config* c, int pop_size, int dim, evb_
       e->slot = static_cast<int*>(dalloc<int>(pop_size));
       e->idx = static_cast<int*>(dalloc<int>(size_t(pop_size) * 4));
       e->jrand = static_cast<int*>(dalloc<int>(pop_size));
+      e->xlen = static_cast<int*>(dalloc<int>(pop_size));
+      e->rword = static_cast<int64_t*>(dalloc<int64_t>(pop_size));
       e->woff = static_cast<int64_t*>(dalloc<int64_t>(pop_size));
       e->wcount = static_cast<int64_t*>(dalloc<int64_t>(pop_size));
       e->order = static_cast<int*>(dalloc<int>(std::max(1, e->p_count)));

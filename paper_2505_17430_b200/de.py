@@ -17,8 +17,8 @@ from ._lib import EVB_F32, EVB_F64, ConfigError, check
 from .problems import EvalScratch, ProblemInstance, _stream_ptr, dtype_of
 
 MUTATIONS = {"rand_1": 0, "best_1": 1, "ttpb_1": 2}
-CROSSOVERS = {"binomial": 0}
-REPAIRS = {"clip": 0, "reflect": 1, "midpoint_target": 2}
+CROSSOVERS = {"binomial": 0, "exponential": 1}
+REPAIRS = {"clip": 0, "reflect": 1, "midpoint_target": 2, "reinitialize": 3}
 ADAPTERS = {"fixed": 0, "jade": 1, "shade": 2}
 
 

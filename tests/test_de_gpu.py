@@ -235,3 +235,74 @@ def test_graph_generations_equal_eager(dev, mode):
     assert np.array_equal(p0, p1) and np.array_equal(f0, f1)
     assert np.array_equal(s0["archive"], s1["archive"]) and np.array_equal(s0["memory_f"], s1["memory_f"])
     assert r0["cursor"] == r1["cursor"] and r0["generation"] == r1["generation"]
+
+
+NEW_STRATEGIES = [
+    DEConfig("rand_1", "exponential", "clip", "fixed", f=0.5, cr=0.9),
+    DEConfig("rand_1", "binomial", "reinitialize", "fixed", f=0.9, cr=0.9),
+    DEConfig("best_1", "exponential", "reinitialize", "fixed", f=0.8, cr=0.7),
+    DEConfig("ttpb_1", "exponential", "reinitialize", "shade", p_best=0.11, use_archive=True, memory_size=20,
+             archive_rate=1.0),
+]
+
+
+@pytest.mark.parametrize("cfg", NEW_STRATEGIES, ids=lambda c: f"{c.mutation}-{c.crossover}-{c.repair}-{c.parameter}")
+def test_exponential_reinitialize_philox_replay(dev, cfg):
+    # exponential crossover (de/strategy.hpp:199-216) and reinitialize repair (:279-290): the
+    # block length and the repair words are data-dependent; the reference engine replays the
+    # exported per-individual word counts exactly, generation after generation (no re-sync)
+    P, D, G, key = 48, 30, 12, 0xC0FFEE
+    o, m = O.shift_rotation(17, D)
+    prob = evb.ProblemInstance.base(evb.BaseKind.sphere, o, m, 0.0)
+    eng = DEEngine(cfg, P, D)
+    rng = Rng.philox(key)
+    pop = torch.empty((P, D), dtype=torch.float64, device=dev)
+    eng.init_population(pop, -100.0, 100.0, rng)
+    fit = dev_eval(prob, pop, dev)
+    ref = O.RefDE(cfg, P, D)
+    ref.set_problem_base(0, o, m, 0.0)
+    ref.set_pop(pop.cpu().numpy(), fit.cpu().numpy())
+    for g in range(G):
+        eng.generation(prob, pop, fit, -100.0, 100.0, rng)
+        dr = eng.last_draws()
+        words = scripted_words_for_generation(key, dr["generation"], dr["word_counts"], dr["archive_words"],
+                                              philox=O.philox_words)
+        assert ref.generation(words, -100.0, 100.0), g
+        st = ref.get()
+        if cfg.parameter == "fixed":
+            assert np.array_equal(pop.cpu().numpy(), st["pop"]), g
+            assert np.array_equal(fit.cpu().numpy(), st["fit"]), g
+        else:  # F/CR via tan/log/cos: CUDA vs libm ulps can flip a gene; count, then re-sync
+            same = np.all(pop.cpu().numpy() == st["pop"], axis=1)
+            assert same.mean() >= 0.9, g
+            pop.copy_(torch.from_numpy(st["pop"]))
+            fit.copy_(torch.from_numpy(st["fit"]))
+            eng.set_state(st["archive"], st["memory_f"], st["memory_cr"], st["write_index"])
+
+
+@pytest.mark.parametrize("cfg", NEW_STRATEGIES[:3], ids=lambda c: f"{c.mutation}-{c.crossover}-{c.repair}")
+def test_exponential_reinitialize_words_mode(dev, cfg):
+    # oracle mode: one word list consumed in the reference's order; the C restatement walks the
+    # same list and must agree on the population, the word counts and the final cursor
+    P, D, G = 40, 16, 6
+    o, m = O.shift_rotation(23, D)
+    prob = evb.ProblemInstance.base(evb.BaseKind.rastrigin, o, m, 0.0)
+    words = O.rng_words(23, 0, P * D + G * P * (2 * D + 40))
+    rng = Rng.words(words)
+    eng = DEEngine(cfg, P, D)
+    pop = torch.empty((P, D), dtype=torch.float64, device=dev)
+    eng.init_population(pop, -100.0, 100.0, rng)
+    fit = dev_eval(prob, pop, dev)
+    orc = O.OracleDE(cfg, P, D)
+    orc.set_problem_base(5, o, m, 0.0)
+    orc.set_state(pop.cpu().numpy(), fit.cpu().numpy())
+    cursor = P * D
+    for g in range(G):
+        eng.generation(prob, pop, fit, -100.0, 100.0, rng)
+        out = orc.generation(words[cursor:], -100.0, 100.0)
+        cursor += int(out["words"].sum() + out["archive_words"])
+        dr = eng.last_draws()
+        assert np.array_equal(dr["word_counts"], out["words"]), g
+        assert np.array_equal(pop.cpu().numpy(), orc.pop), g
+        assert np.max(np.abs(fit.cpu().numpy() - orc.fit) / np.maximum(1, np.abs(orc.fit))) <= 1e-12
+        assert rng.state()["cursor"] == cursor

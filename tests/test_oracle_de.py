@@ -23,7 +23,7 @@ def run_both(cfg, P, D, kind, gens, seed, lb=-100.0, ub=100.0, scale=1.0):
     ref.set_pop(x, fit)
     orc.set_state(x, fit)
     for g in range(gens):
-        words = rng.integers(0, 2**64 - 1, size=P * (D + 40) + 64, dtype=np.uint64, endpoint=True)
+        words = rng.integers(0, 2**64 - 1, size=P * (2 * D + 40) + 64, dtype=np.uint64, endpoint=True)
         out = orc.generation(words, lb, ub)
         n_used = int(out["words"].sum() + out["archive_words"])
         assert ref.generation(words[:n_used], lb, ub), f"gen {g}: reference consumed a different word count"
@@ -42,6 +42,11 @@ def run_both(cfg, P, D, kind, gens, seed, lb=-100.0, ub=100.0, scale=1.0):
     (preset_shade(0.11, 40, 1.0), 6, 1.0),      # config 2 construction (smaller)
     (preset_jade(0.05, 0.1, 0.5), 0, 1.0),
     (DEConfig("best_1", "binomial", "reflect", "fixed", f=0.7, cr=0.3), 1, 1.0),
+    # exponential crossover (de/strategy.hpp:199-216) and reinitialize repair (:279-290)
+    (DEConfig("rand_1", "exponential", "clip", "fixed", f=0.5, cr=0.9), 5, 1.0),
+    (DEConfig("rand_1", "binomial", "reinitialize", "fixed", f=0.9, cr=0.9), 6, 1.0),
+    (DEConfig("ttpb_1", "exponential", "reinitialize", "shade", p_best=0.11, use_archive=True, memory_size=10,
+              archive_rate=1.0), 0, 1.0),
 ])
 def test_c_restatement_matches_reference_engine(cfg, kind, scale):
     run_both(cfg, 40, 12, kind, 6, 3, scale=scale)
