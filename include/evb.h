@@ -195,7 +195,12 @@ typedef struct {
   int memory_size;     /* shade_parameter(H)                     de/parameter.hpp:149-213 */
   double jade_c;       /* jade_parameter(c)                      de/parameter.hpp:99-147  */
   double archive_rate; /* de_builder::archive_rate               de/builder.hpp:44-48     */
+  int reduction;       /* population_policy: 0 fixed, 1 linear_reduction(N_init = pop_size, n_min)
+                          de/policy.hpp:14-60 (L-SHADE)                                       */
+  int n_min;
 } evb_de_config;
+
+enum evb_de_policy { EVB_POP_FIXED = 0 /* "fixed" */, EVB_POP_LINEAR_REDUCTION = 1 /* "linear_reduction" */ };
 
 typedef struct evb_de_s* evb_de;
 
@@ -231,6 +236,17 @@ EVB_API int evb_de_set_state(evb_de e, const void* archive_host, int archive_siz
                              const void* mem_f_host, const void* mem_cr_host, int write_index);
 /* Draws of the last generation: words consumed per individual, archive-victim words, the
  * Philox generation id, per-individual F, CR, donor indices (4 per individual) and jrand. */
+/* evolution_state of generation-level use (core/state.hpp:10-53): budget and evaluations so far.
+ * Needed before evb_de_generation when the population policy is linear_reduction (the schedule
+ * reads fes / max_fes); evb_de_optimize sets it itself.  Each generation adds its trials. */
+EVB_API int evb_de_set_budget(evb_de e, int64_t max_fes, int64_t fes);
+/* Current population size (shrinks under linear_reduction; rows [0, size) of the caller's
+ * population are the members, in the reference's order after erase_member). */
+EVB_API int evb_de_pop_size(evb_de e);
+/* The last generation's population size (its trial count; evb_de_last_draws reports that many
+ * individuals), the size after its reduction, and the archive-shrink words consumed by
+ * de_archive::set_capacity (de/strategy.hpp:40-47; Philox sub-stream 0xFFFFFFFE). */
+EVB_API int evb_de_last_reduction(evb_de e, int* pop_before, int* pop_after, int64_t* shrink_words);
 /* Every evaluation the engine makes (init in evb_de_optimize, trials in each generation) is
  * reported, in FE order, to recorder run `run` (run_handle::evaluate -> on_evaluate,
  * experiment/runner.hpp:38-45); r = NULL detaches. */

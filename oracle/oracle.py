@@ -239,7 +239,9 @@ def eval_composition(kinds, shifts, rots, sigma, lam, cbias, bias, X):
 # ---- DE: the reference engine (REF) and the C restatement (C) -------------------------------------
 REF_DE_SIG = {
     "ref_de_create": (vp, [c_int, c_int, c_int, c_double, c_double, c_double, c_int, c_int, c_double, c_double,
-                           c_int, c_int, c_int]),
+                           c_int, c_int, c_int, c_int, c_int]),
+    "ref_de_set_budget": (None, [vp, ctypes.c_longlong, ctypes.c_longlong]),
+    "ref_de_pop_size": (c_int, [vp]),
     "ref_de_destroy": (None, [vp]),
     "ref_de_set_problem_base": (None, [vp, c_int, vp, vp, c_double]),
     "ref_de_set_problem_composition": (None, [vp, c_int, vp, vp, vp, vp, vp, vp, c_double]),
@@ -266,7 +268,7 @@ class RefDE:
         self.H = max(1, cfg.memory_size if cfg.parameter == "shade" else 1)
         self.h = REF().ref_de_create(MUT[cfg.mutation], REP[cfg.repair], ADA[cfg.parameter], cfg.f, cfg.cr,
                                      cfg.p_best, int(cfg.use_archive), self.H, cfg.jade_c, cfg.archive_rate, P, D,
-                                     CX[cfg.crossover])
+                                     CX[cfg.crossover], int(cfg.reduction == "linear_reduction"), cfg.n_min)
         self._keep = []
 
     def set_problem_base(self, kind, shift, rot, bias):
@@ -298,9 +300,16 @@ class RefDE:
     def native_run(self, seed, stream, generations, lb, ub):
         REF().ref_de_native_run(self.h, seed, stream, generations, lb, ub)
 
+    def set_budget(self, max_fes, fes):
+        REF().ref_de_set_budget(self.h, max_fes, fes)
+
+    def pop_size(self):
+        return int(REF().ref_de_pop_size(self.h))
+
     def get(self):
-        x = np.empty((self.P, self.D))
-        f = np.empty(self.P)
+        n = self.pop_size()
+        x = np.empty((n, self.D))
+        f = np.empty(n)
         cap = max(1, int(np.ceil(self.cfg.archive_rate * self.P)))
         a = np.zeros((cap, self.D))
         sz, wi = ctypes.c_int(), ctypes.c_int()

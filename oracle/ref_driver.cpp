@@ -221,6 +221,8 @@ struct ref_de_run {
   std::unique_ptr<problem_instance<double>> problem;
   population<double> pop;
   int P = 0, D = 0;
+  int n_min = 4;
+  std::unique_ptr<evolution_state> st;  // persistent budget (L-SHADE schedules read it)
 };
 
 std::unique_ptr<de::mutation_strategy<double>> make_mutation(int m, double p, int use_archive) {
@@ -244,7 +246,8 @@ std::unique_ptr<de::parameter_adapter<double>> make_adapter(int a, double f, dou
 
 // Engine built through the reference de_builder from the same strategy choices as evb_de_config.
 REF_API void* ref_de_create(int mutation, int repair, int adapter, double f, double cr, double p, int use_archive,
-                            int H, double jade_c, double archive_rate, int P, int D, int crossover) {
+                            int H, double jade_c, double archive_rate, int P, int D, int crossover, int reduction,
+                            int n_min) {
   auto* r = new ref_de_run();
   r->engine = std::make_unique<de::de_engine<double>>(de::de_builder<double>()
                                                           .mutation(make_mutation(mutation, p, use_archive))
@@ -253,9 +256,11 @@ REF_API void* ref_de_create(int mutation, int repair, int adapter, double f, dou
                                                                                     : std::make_unique<de::binomial_crossover<double>>())
                                                           .repair(make_repair(repair))
                                                           .parameter(make_adapter(adapter, f, cr, H, jade_c))
-                                                          .population(de::population_policy::fixed())
+                                                          .population(reduction ? de::population_policy::linear_reduction(P, n_min)
+                                                                                : de::population_policy::fixed())
                                                           .archive_rate(archive_rate)
                                                           .build());
+  r->n_min = reduction ? n_min : std::min(4, P);
   r->P = P;
   r->D = D;
   r->pop = population<double>(P, D);
@@ -309,17 +314,27 @@ REF_API int ref_de_generation(void* h, const uint64_t* words, int64_t n, double 
   std::vector<uint64_t> w(words, words + n);
   w.push_back(sentinel);
   rng_stream rng = rng_stream::scripted(w);
-  evolution_state st(1LL << 40, r->P, r->D, std::min(4, r->P));
+  evolution_state tmp(1LL << 40, r->P, r->D, std::min(4, r->P));
+  evolution_state& st = r->st ? *r->st : tmp;
   eval_scratch<double> scratch;
   auto objective = [&](std::span<const double> x) { return r->problem->evaluate(x, scratch); };
   r->engine->generation(r->pop, st, objective, lb, ub, rng);
   return rng.next_u64() == sentinel ? 1 : 0;
 }
 
+// evolution_state(max_fes, P, D, n_min) with `fes` evaluations done, kept across generations
+REF_API void ref_de_set_budget(void* h, long long max_fes, long long fes) {
+  auto* r = static_cast<ref_de_run*>(h);
+  r->st = std::make_unique<evolution_state>(max_fes, r->P, r->D, r->n_min);
+  r->st->add_fes(fes);
+}
+
+REF_API int ref_de_pop_size(void* h) { return static_cast<ref_de_run*>(h)->pop.pop_size(); }
+
 REF_API void ref_de_get(void* h, double* x, double* fit, double* archive, int* arch_size, double* mem_f,
                         double* mem_cr, int* write_index) {
   auto* r = static_cast<ref_de_run*>(h);
-  for (int i = 0; i < r->P; ++i) {
+  for (int i = 0; i < r->pop.pop_size(); ++i) {
     if (x) std::memcpy(x + size_t(i) * r->D, r->pop[i].genome.data(), sizeof(double) * r->D);
     if (fit) fit[i] = r->pop[i].fitness;
   }

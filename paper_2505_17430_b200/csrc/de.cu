@@ -86,6 +86,16 @@ struct evb_de_s {
   int g_kernels = 0;
   evb_recorder_s* rec = nullptr;  // attached best-so-far recorder (may be null)
   int rec_run = 0;
+  // population policy (de/policy.hpp): P is the current size, P_alloc the initial one
+  int P_alloc = 0;
+  int reduction = 0;
+  int n_min = 4;
+  double p_t = 0.0, rate_t = 0.0;  // p and archive_rate as stored in T
+  int64_t fes = 0, max_fes = 0;    // evolution_state (core/state.hpp)
+  int* rank = nullptr;             // P_alloc: reduction ranks
+  int64_t* d_shrink_words = nullptr;
+  int last_shrink_valid = 0;
+  int gen_P = 0;  // population size at the start of the last generation (its trial count)
 };
 
 namespace evb {
@@ -637,9 +647,13 @@ de_dev<T> make_dev(evb_de_s* e, void* pop, int64_t ldp, void* fit, double lb, do
 }
 
 template <typename T>
+void reduce_t(evb_de_s* e, void* pop, int64_t ldp, void* fit, evb_rng_s* r, cudaStream_t st);
+
+template <typename T>
 void generation_t(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, void* pop, int64_t ldp, void* fit,
                   double lb, double ub, evb_rng_s* r, cudaStream_t st) {
   de_dev<T> d = make_dev<T>(e, pop, ldp, fit, lb, ub, r);
+  e->gen_P = e->P;
   if (e->cfg.mutation == EVB_MUT_TTPB1 || e->cfg.mutation == EVB_MUT_BEST1) {
     const int th = 256;
     de_order_kernel<T><<<(e->P + th - 1) / th, th, th * sizeof(T), st>>>(d);
@@ -681,8 +695,135 @@ void generation_t(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, vo
     count_launch();
   }
   EVB_CUDA(cudaGetLastError());
+  e->fes += e->P;  // st.add_fes(1) per trial (de/engine.hpp:88)
+  reduce_t<T>(e, pop, ldp, fit, r, st);
   e->last_gen = r->gen;
   r->gen++;
+}
+
+// ---- population reduction (L-SHADE, de/policy.hpp:40-60) + archive shrink ------------------
+// reduce_population removes the worst member (fitness >=, so ties remove the higher index) until
+// the scheduled size: the survivors are exactly the members of (fitness, index) rank < target,
+// kept in their order (erase_member).
+template <typename T>
+__global__ void de_reduce_rank_kernel(const T* fit, int P, int* rank) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  T* sf = reinterpret_cast<T*>(smem_raw);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const T fi = i < P ? fit[i] : T(0);
+  int rk = 0;
+  for (int base = 0; base < P; base += blockDim.x) {
+    const int j = base + threadIdx.x;
+    sf[threadIdx.x] = j < P ? fit[j] : T(0);
+    __syncthreads();
+    const int n = min(int(blockDim.x), P - base);
+    if (i < P)
+      for (int q = 0; q < n; ++q) {
+        const T fj = sf[q];
+        const int jj = base + q;
+        rk += (fj < fi || (!(fi < fj) && !(fj < fi) && jj < i)) ? 1 : 0;
+      }
+    __syncthreads();
+  }
+  if (i < P) rank[i] = rk;
+}
+
+// block i: survivor i moves to position #{j < i : survivor} of the staging rows
+template <typename T>
+__global__ void de_reduce_gather_kernel(const T* pop, int64_t ldp, const T* fit, int P, int D, const int* rank,
+                                        int target, T* stage, int64_t lds, T* stage_fit) {
+  const int i = blockIdx.x;
+  if (rank[i] >= target) return;
+  __shared__ int part[32];
+  int c = 0;
+  for (int j = threadIdx.x; j < i; j += blockDim.x) c += rank[j] < target ? 1 : 0;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
+  __syncthreads();
+  int pos = 0;
+  for (int w = 0; w < int(blockDim.x + 31) / 32; ++w) pos += part[w];
+  for (int j = threadIdx.x; j < D; j += blockDim.x) stage[size_t(pos) * lds + j] = pop[size_t(i) * ldp + j];
+  if (threadIdx.x == 0) stage_fit[pos] = fit[i];
+}
+
+template <typename T>
+__global__ void de_reduce_scatter_kernel(T* pop, int64_t ldp, T* fit, int D, const T* stage, int64_t lds,
+                                         const T* stage_fit) {
+  const int i = blockIdx.x;
+  for (int j = threadIdx.x; j < D; j += blockDim.x) pop[size_t(i) * ldp + j] = stage[size_t(i) * lds + j];
+  if (threadIdx.x == 0) fit[i] = stage_fit[i];
+}
+
+// de_archive::set_capacity (de/strategy.hpp:40-47): while size > cap, victim = uniform_int(size),
+// swap with the last member, drop it.  Words: Philox sub-stream 0xFFFFFFFE of this generation, or
+// the WORDS cursor.
+template <typename T>
+__global__ void de_archive_shrink_kernel(T* archive, int64_t ldt, int D, int* arch_size, int cap, word_source src,
+                                         uint64_t ctr_hi, int64_t* cursor, int* overflow, int64_t* used) {
+  __shared__ int victim, size;
+  __shared__ int64_t pos0;
+  if (threadIdx.x == 0) {
+    size = *arch_size;
+    pos0 = src.mode == RNG_WORDS ? *cursor : 0;
+  }
+  __syncthreads();
+  int64_t n = 0;
+  while (size > cap) {
+    if (threadIdx.x == 0) {
+      word_reader r{&src, ctr_hi, pos0 + n, 0, overflow};
+      victim = draw_int(r, size);
+    }
+    ++n;
+    __syncthreads();
+    const int last = size - 1;
+    if (victim != last)
+      for (int j = threadIdx.x; j < D; j += blockDim.x) archive[size_t(victim) * ldt + j] = archive[size_t(last) * ldt + j];
+    __syncthreads();
+    if (threadIdx.x == 0) size = last;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *arch_size = size;
+    *used = n;
+    if (src.mode == RNG_WORDS) {
+      *cursor = pos0 + n;
+      if (pos0 + n > src.n_words) *overflow = 1;
+    }
+  }
+}
+
+int ttpb_p_count(double p_t, int P) { return std::min(P, std::max(2, int(std::ceil(p_t * P)))); }
+
+// after the generation's selection: evolution_state::add_fes(P) has happened; shrink if scheduled
+template <typename T>
+void reduce_t(evb_de_s* e, void* pop, int64_t ldp, void* fit, evb_rng_s* r, cudaStream_t st) {
+  e->last_shrink_valid = 0;
+  if (!e->reduction) return;
+  const double frac = double(e->fes) / double(e->max_fes);
+  const int target = std::clamp(int(std::lround(e->P_alloc + (e->n_min - e->P_alloc) * frac)), e->n_min, e->P_alloc);
+  if (target >= e->P) return;  // policy.hpp:49: no-op when the schedule allows the current size
+  const int P = e->P, D = e->D;
+  const int th = 256;
+  de_reduce_rank_kernel<T><<<(P + th - 1) / th, th, th * sizeof(T), st>>>(static_cast<const T*>(fit), P, e->rank);
+  de_reduce_gather_kernel<T><<<P, 128, 0, st>>>(static_cast<const T*>(pop), ldp, static_cast<const T*>(fit), P, D,
+                                                 e->rank, target, static_cast<T*>(e->trial), e->ldt,
+                                                 static_cast<T*>(e->trial_fit));
+  de_reduce_scatter_kernel<T><<<target, 128, 0, st>>>(static_cast<T*>(pop), ldp, static_cast<T*>(fit), D,
+                                                      static_cast<const T*>(e->trial), e->ldt,
+                                                      static_cast<const T*>(e->trial_fit));
+  count_launch(3);
+  // archive.set_capacity(archive_capacity_for(new size), rng)  (de/engine.hpp:97-100)
+  const int cap = int(std::ceil(e->rate_t * double(target)));
+  word_source src{r->mode, r->key, r->d_words, r->n_words};
+  de_archive_shrink_kernel<T><<<1, 128, 0, st>>>(static_cast<T*>(e->archive), e->ldt, D, e->d_arch_size, cap, src,
+                                                 (uint64_t(r->gen) << 32) | kSubShrink, r->d_cursor, r->d_overflow,
+                                                 e->d_shrink_words);
+  count_launch();
+  EVB_CUDA(cudaGetLastError());
+  e->P = target;
+  e->archive_cap = cap;
+  if (e->cfg.mutation == EVB_MUT_TTPB1) e->p_count = ttpb_p_count(e->p_t, target);
+  e->last_shrink_valid = 1;
 }
 
 template <typename T>
@@ -742,7 +883,7 @@ void free_de(evb_de_s* e) {
   if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
   void* ptrs[] = {e->trial, e->trial_fit, e->F, e->CR, e->slot, e->idx, e->jrand, e->xlen, e->rword, e->woff, e->wcount, e->order,
                   e->win, e->arch_slot, e->owner, e->succ, e->archive, e->d_arch_size, e->d_write_index,
-                  e->d_arch_words, e->mem_f, e->mem_cr};
+                  e->d_arch_words, e->mem_f, e->mem_cr, e->rank, e->d_shrink_words};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (e->eval_scratch) evb_scratch_destroy(e->eval_scratch);
@@ -750,6 +891,13 @@ void free_de(evb_de_s* e) {
 
 const char* mutation_name(int m) {
   return m == EVB_MUT_RAND1 ? "rand_1" : m == EVB_MUT_BEST1 ? "best_1" : m == EVB_MUT_TTPB1 ? "ttpb_1" : "?";
+}
+
+// back to the initial population size (a new optimize() run starts from pop_size members)
+void restore_size(evb_de_s* e) {
+  e->P = e->P_alloc;
+  e->archive_cap = int(std::ceil(e->rate_t * double(e->P_alloc)));
+  if (e->cfg.mutation == EVB_MUT_TTPB1) e->p_count = ttpb_p_count(e->p_t, e->P_alloc);
 }
 
 template <typename T>
@@ -864,6 +1012,12 @@ int evb_de_create(int dtype, const evb_de_config* c, int pop_size, int dim, evb_
     require(pop_size >= min_pop,
             std::string("de_engine: population too small for mutation ") + mutation_name(c->mutation));
     require(dim >= 1, "de: dim must be positive");
+    require(c->reduction == EVB_POP_FIXED || c->reduction == EVB_POP_LINEAR_REDUCTION,
+            "de builder: unknown population policy");
+    if (c->reduction == EVB_POP_LINEAR_REDUCTION) {  // de/policy.hpp:24-28
+      require(c->n_min >= 4, "population_policy: N_min must be at least 4");
+      require(c->n_min <= pop_size, "population_policy: N_min must not exceed N_init");
+    }
 
     auto* e = new evb_de_s();
     try {
@@ -889,6 +1043,11 @@ int evb_de_create(int dtype, const evb_de_config* c, int pop_size, int dim, evb_
       // archive_capacity_for (de/engine.hpp:137-139), archive_rate stored in T
       const double rate_t = dtype == EVB_F64 ? c->archive_rate : double(float(c->archive_rate));
       e->archive_cap = int(std::ceil(rate_t * double(pop_size)));
+      e->P_alloc = pop_size;
+      e->p_t = p_t;
+      e->rate_t = rate_t;
+      e->reduction = c->reduction;
+      e->n_min = c->reduction == EVB_POP_LINEAR_REDUCTION ? c->n_min : std::min(4, pop_size);
       e->ldt = round_up(dim, 16 / int64_t(es));
       auto bytes = [&](size_t n) { return n * es; };
       EVB_CUDA(cudaMalloc(&e->trial, bytes(size_t(pop_size) * e->ldt)));
@@ -913,6 +1072,8 @@ int evb_de_create(int dtype, const evb_de_config* c, int pop_size, int dim, evb_
       e->d_arch_size = static_cast<int*>(dalloc<int>(1));
       e->d_write_index = static_cast<int*>(dalloc<int>(1));
       e->d_arch_words = static_cast<int64_t*>(dalloc<int64_t>(1));
+      e->rank = static_cast<int*>(dalloc<int>(pop_size));
+      e->d_shrink_words = static_cast<int64_t*>(dalloc<int64_t>(1));
       EVB_CUDA(cudaMalloc(&e->mem_f, bytes(e->cfg.memory_size)));
       EVB_CUDA(cudaMalloc(&e->mem_cr, bytes(e->cfg.memory_size)));
       if (dtype == EVB_F64) reset_adapter<double>(e);
@@ -941,6 +1102,33 @@ int evb_de_reset(evb_de e) {
     if (e->dtype == EVB_F64) reset_adapter<double>(e);
     else reset_adapter<float>(e);
     EVB_CUDA(cudaMemset(e->d_arch_size, 0, sizeof(int)));
+    restore_size(e);
+  });
+}
+
+int evb_de_set_budget(evb_de e, int64_t max_fes, int64_t fes) {
+  return guarded([&] {
+    require(e != nullptr, "de: null handle");
+    require(max_fes > 0, "evolution_state: max_fes must be positive");
+    require(fes >= 0, "evolution_state: add_fes requires n >= 0");
+    e->max_fes = max_fes;
+    e->fes = fes;
+  });
+}
+
+int evb_de_pop_size(evb_de e) { return e ? e->P : -1; }
+
+int evb_de_last_reduction(evb_de e, int* pop_before, int* pop_after, int64_t* shrink_words) {
+  return guarded([&] {
+    require(e != nullptr, "de: null handle");
+    if (pop_before) *pop_before = e->gen_P;
+    if (pop_after) *pop_after = e->P;
+    int64_t n = 0;
+    if (e->last_shrink_valid) {
+      EVB_CUDA(cudaDeviceSynchronize());
+      EVB_CUDA(cudaMemcpy(&n, e->d_shrink_words, sizeof(n), cudaMemcpyDeviceToHost));
+    }
+    if (shrink_words) *shrink_words = n;
   });
 }
 
@@ -954,6 +1142,8 @@ int evb_de_generation(evb_de e, evb_problem objective, evb_scratch s, void* pop,
     if (objective->p.dim != e->D) throw invalid_argument("de_generation: problem dimension mismatch");
     if (objective->p.dtype != e->dtype) throw config_error("de_generation: problem dtype differs from engine");
     if (ldp < e->D) throw invalid_argument("de_generation: ldp < dim");
+    if (e->reduction && e->max_fes <= 0)
+      throw config_error("de_generation: linear population reduction needs a budget (evb_de_set_budget)");
     de_generation(e, &objective->p, s ? s : e->eval_scratch, pop, ldp, fitness, lb, ub, rng,
                   static_cast<cudaStream_t>(stream));
   });
@@ -971,8 +1161,14 @@ int evb_de_generations(evb_de e, evb_problem objective, evb_scratch s, void* pop
     if (objective->p.dtype != e->dtype) throw config_error("de_generations: problem dtype differs from engine");
     if (ldp < e->D) throw invalid_argument("de_generations: ldp < dim");
     if (n == 0) return;
+    if (e->reduction && e->max_fes <= 0)
+      throw config_error("de_generations: linear population reduction needs a budget (evb_de_set_budget)");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     evb_scratch_s* sc = s ? s : e->eval_scratch;
+    if (e->reduction) {  // the population size changes between generations: no graph replay
+      for (int g = 0; g < n; ++g) de_generation(e, &objective->p, sc, pop, ldp, fitness, lb, ub, rng, st);
+      return;
+    }
     de_generation(e, &objective->p, sc, pop, ldp, fitness, lb, ub, rng, st);
     if (--n == 0) return;
     const void* key[6] = {pop, fitness, objective, sc, rng, reinterpret_cast<const void*>(ldp)};
@@ -1084,13 +1280,13 @@ int evb_de_last_draws(evb_de e, int64_t* word_counts, int64_t* archive_words, ui
     require(e != nullptr, "de: null handle");
     EVB_CUDA(cudaDeviceSynchronize());
     const size_t es = e->dtype == EVB_F64 ? 8 : 4;
-    if (word_counts) EVB_CUDA(cudaMemcpy(word_counts, e->wcount, sizeof(int64_t) * e->P, cudaMemcpyDeviceToHost));
+    if (word_counts) EVB_CUDA(cudaMemcpy(word_counts, e->wcount, sizeof(int64_t) * e->gen_P, cudaMemcpyDeviceToHost));
     if (archive_words) EVB_CUDA(cudaMemcpy(archive_words, e->d_arch_words, sizeof(int64_t), cudaMemcpyDeviceToHost));
     if (generation) *generation = e->last_gen;
-    if (F_host) EVB_CUDA(cudaMemcpy(F_host, e->F, es * e->P, cudaMemcpyDeviceToHost));
-    if (CR_host) EVB_CUDA(cudaMemcpy(CR_host, e->CR, es * e->P, cudaMemcpyDeviceToHost));
-    if (idx_host) EVB_CUDA(cudaMemcpy(idx_host, e->idx, sizeof(int) * 4 * e->P, cudaMemcpyDeviceToHost));
-    if (jrand_host) EVB_CUDA(cudaMemcpy(jrand_host, e->jrand, sizeof(int) * e->P, cudaMemcpyDeviceToHost));
+    if (F_host) EVB_CUDA(cudaMemcpy(F_host, e->F, es * e->gen_P, cudaMemcpyDeviceToHost));
+    if (CR_host) EVB_CUDA(cudaMemcpy(CR_host, e->CR, es * e->gen_P, cudaMemcpyDeviceToHost));
+    if (idx_host) EVB_CUDA(cudaMemcpy(idx_host, e->idx, sizeof(int) * 4 * e->gen_P, cudaMemcpyDeviceToHost));
+    if (jrand_host) EVB_CUDA(cudaMemcpy(jrand_host, e->jrand, sizeof(int) * e->gen_P, cudaMemcpyDeviceToHost));
   });
 }
 
@@ -1105,6 +1301,7 @@ int evb_de_optimize(evb_de e, evb_problem objective, evb_scratch s, void* pop, i
     if (objective->p.dim != e->D) throw invalid_argument("de_optimize: problem dimension mismatch");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     evb_scratch_s* sc = s ? s : e->eval_scratch;
+    restore_size(e);
     de_init_population(e, pop, ldp, lb, ub, rng, st);
     eval_request rq{};
     rq.prob = &objective->p;
@@ -1121,11 +1318,11 @@ int evb_de_optimize(evb_de e, evb_problem objective, evb_scratch s, void* pop, i
     rq.scalar_trig = true;
     eval_dispatch(rq);
     if (e->rec) recorder_observe(e->rec, e->rec_run, fitness, e->P, st);  // initial evaluations
-    int64_t fes = e->P;
+    e->max_fes = max_fes;  // evolution_state st(max_fes, ...); st.add_fes(P) for the initial members
+    e->fes = e->P;
     int gens = 0;
-    while (fes < max_fes) {
+    while (e->fes < max_fes) {
       de_generation(e, &objective->p, sc, pop, ldp, fitness, lb, ub, rng, st);
-      fes += e->P;
       ++gens;
     }
     // best (core/population.hpp:59-65): lowest fitness, ties to the lowest index

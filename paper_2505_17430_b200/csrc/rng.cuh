@@ -22,6 +22,7 @@ enum rng_mode { RNG_PHILOX = 0, RNG_WORDS = 1 };
 
 constexpr uint32_t kSubArchive = 0xFFFFFFFFu;  // archive-victim draws of a generation
 constexpr uint32_t kSubInit = 0xFFFFFFF0u;     // init_population draws
+constexpr uint32_t kSubShrink = 0xFFFFFFFEu;   // archive set_capacity victims after a population reduction
 constexpr uint32_t kSubEngine = 0xFFFFFFE0u;   // engine-level draws (archive shrink, restarts)
 
 __host__ __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {

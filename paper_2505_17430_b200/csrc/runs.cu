@@ -296,6 +296,7 @@ std::string runs_kernel_unsupported(int dtype, const evb_de_config* cfg, int pop
     return "de_runs: persistent kernel supports rand_1 / best_1 mutation";
   if (cfg->parameter != EVB_PAR_FIXED) return "de_runs: persistent kernel supports the fixed adapter";
   if (cfg->archive_rate != 0.0) return "de_runs: persistent kernel runs without an archive";
+  if (cfg->reduction != EVB_POP_FIXED) return "de_runs: persistent kernel runs a fixed population size";
   if (cfg->repair != EVB_REP_CLIP && cfg->repair != EVB_REP_MIDPOINT_TARGET) return "de_runs: clip or midpoint repair";
   if (cfg->crossover != EVB_CX_BINOMIAL) return "de_runs: binomial crossover";
   if (!(cfg->f > 0.0 && cfg->f <= 1.0)) return "fixed_parameter: F must be in (0,1]";

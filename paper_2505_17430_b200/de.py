@@ -19,6 +19,7 @@ from .problems import EvalScratch, ProblemInstance, _stream_ptr, dtype_of
 MUTATIONS = {"rand_1": 0, "best_1": 1, "ttpb_1": 2}
 CROSSOVERS = {"binomial": 0, "exponential": 1}
 REPAIRS = {"clip": 0, "reflect": 1, "midpoint_target": 2, "reinitialize": 3}
+POLICIES = {"fixed": 0, "linear_reduction": 1}
 ADAPTERS = {"fixed": 0, "jade": 1, "shade": 2}
 
 
@@ -26,7 +27,8 @@ class _Cfg(ctypes.Structure):
     _fields_ = [("mutation", ctypes.c_int), ("crossover", ctypes.c_int), ("repair", ctypes.c_int),
                 ("parameter", ctypes.c_int), ("f", ctypes.c_double), ("cr", ctypes.c_double),
                 ("p_best", ctypes.c_double), ("use_archive", ctypes.c_int), ("memory_size", ctypes.c_int),
-                ("jade_c", ctypes.c_double), ("archive_rate", ctypes.c_double)]
+                ("jade_c", ctypes.c_double), ("archive_rate", ctypes.c_double), ("reduction", ctypes.c_int),
+                ("n_min", ctypes.c_int)]
 
 
 @dataclass
@@ -44,15 +46,19 @@ class DEConfig:
     memory_size: int = 1
     jade_c: float = 0.1
     archive_rate: float = 0.0
+    reduction: str = "fixed"  # population_policy (de/policy.hpp): "fixed" | "linear_reduction"
+    n_min: int = 4
 
     def to_c(self) -> _Cfg:
         for name, table, what in ((self.mutation, MUTATIONS, "mutation"), (self.crossover, CROSSOVERS, "crossover"),
                                   (self.repair, REPAIRS, "repair"), (self.parameter, ADAPTERS, "parameter adapter")):
             if name not in table:
                 raise ConfigError(f"de builder: unknown {what} strategy '{name}' (no GPU kernel)")
+        if self.reduction not in POLICIES:
+            raise ConfigError(f"de builder: unknown population policy '{self.reduction}'")
         return _Cfg(MUTATIONS[self.mutation], CROSSOVERS[self.crossover], REPAIRS[self.repair],
                     ADAPTERS[self.parameter], self.f, self.cr, self.p_best, int(self.use_archive),
-                    self.memory_size, self.jade_c, self.archive_rate)
+                    self.memory_size, self.jade_c, self.archive_rate, POLICIES[self.reduction], self.n_min)
 
 
 def preset_de(f: float = 0.5, cr: float = 0.9) -> DEConfig:
@@ -64,6 +70,12 @@ def preset_shade(p: float = 0.11, memory_size: int = 100, archive_rate: float = 
     """presets.hpp:83-94 build_shade: ttpb/1(p, archive), binomial, midpoint_target, shade(H)."""
     return DEConfig("ttpb_1", "binomial", "midpoint_target", "shade", p_best=p, use_archive=archive_rate > 0,
                     memory_size=memory_size, archive_rate=archive_rate)
+
+
+def preset_lshade(p: float = 0.11, memory_size: int = 100, archive_rate: float = 1.0, n_min: int = 4) -> DEConfig:
+    """presets.hpp:150-162 "lshade": build_shade with population_policy::linear_reduction(pop, n_min)."""
+    return DEConfig("ttpb_1", "binomial", "midpoint_target", "shade", p_best=p, use_archive=archive_rate > 0,
+                    memory_size=memory_size, archive_rate=archive_rate, reduction="linear_reduction", n_min=n_min)
 
 
 def preset_jade(p: float = 0.05, c: float = 0.1, archive_rate: float = 0.0) -> DEConfig:
@@ -94,6 +106,9 @@ def _sigs():
         "evb_de_reset": (c_int, [vp]),
         "evb_de_archive_capacity": (c_int, [vp]),
         "evb_de_p_count": (c_int, [vp]),
+        "evb_de_pop_size": (c_int, [vp]),
+        "evb_de_set_budget": (c_int, [vp, i64, i64]),
+        "evb_de_last_reduction": (c_int, [vp, P(c_int), P(c_int), P(i64)]),
         "evb_de_generation": (c_int, [vp, vp, vp, vp, i64, vp, c_double, c_double, vp, vp]),
         "evb_de_init_population": (c_int, [vp, vp, i64, c_double, c_double, vp, vp]),
         "evb_de_generations": (c_int, [vp, vp, vp, vp, i64, vp, c_double, c_double, vp, c_int, vp]),
@@ -192,7 +207,7 @@ class DEEngine:
     def _pop(self, pop, fitness):
         if dtype_of(pop) != self.dtype or dtype_of(fitness) != self.dtype:
             raise ConfigError("de: tensor dtype differs from the engine dtype")
-        if tuple(pop.shape) != (self.pop_size, self.dim) or pop.stride(1) != 1:
+        if pop.dim() != 2 or pop.shape[0] < self.current_pop_size or pop.shape[1] != self.dim or pop.stride(1) != 1:
             raise ConfigError("de: population must be a (pop_size, dim) row-major CUDA tensor")
         return ctypes.c_void_p(pop.data_ptr()), pop.stride(0), ctypes.c_void_p(fitness.data_ptr())
 
@@ -208,6 +223,21 @@ class DEEngine:
         p, ld, f = self._pop(pop, fitness)
         check(_lib.lib().evb_de_generations(self._h, problem.handle, scratch.handle if scratch else None, p, ld, f,
                                             lb, ub, rng.handle, n, _stream_ptr(stream)), "de_generations")
+
+    @property
+    def current_pop_size(self) -> int:
+        """Members after the last reduction (de/policy.hpp); rows [0, n) of the population."""
+        return int(_lib.lib().evb_de_pop_size(self._h))
+
+    def set_budget(self, max_fes: int, fes: int) -> None:
+        """evolution_state(max_fes) with `fes` evaluations done (needed by linear_reduction)."""
+        check(_lib.lib().evb_de_set_budget(self._h, max_fes, fes), "de_set_budget")
+
+    def last_reduction(self):
+        b, a, w = ctypes.c_int(), ctypes.c_int(), ctypes.c_int64()
+        check(_lib.lib().evb_de_last_reduction(self._h, ctypes.byref(b), ctypes.byref(a), ctypes.byref(w)),
+              "de_last_reduction")
+        return {"pop_before": b.value, "pop_after": a.value, "shrink_words": w.value}
 
     def attach_recorder(self, recorder, run: int = 0) -> None:
         """Report every later evaluation (init inside optimize, each generation's trials, FE order)
@@ -268,8 +298,9 @@ class DEEngine:
                                            ctypes.byref(gen), ctypes.c_void_p(F.ctypes.data),
                                            ctypes.c_void_p(CR.ctypes.data), ctypes.c_void_p(idx.ctypes.data),
                                            ctypes.c_void_p(jr.ctypes.data)), "de_last_draws")
-        return {"word_counts": wc, "archive_words": aw.value, "generation": gen.value, "F": F, "CR": CR,
-                "idx": idx, "jrand": jr}
+        n = self.last_reduction()["pop_before"] or P
+        return {"word_counts": wc[:n], "archive_words": aw.value, "generation": gen.value, "F": F[:n], "CR": CR[:n],
+                "idx": idx[:n], "jrand": jr[:n]}
 
     def close(self):
         if self._h:
@@ -283,12 +314,16 @@ class DEEngine:
             pass
 
 
-def scripted_words_for_generation(key: int, generation: int, word_counts, archive_words: int, philox=None):
+def scripted_words_for_generation(key: int, generation: int, word_counts, archive_words: int, philox=None,
+                                  shrink_words: int = 0):
     """The sequential word list the reference engine consumes for one Philox-mode generation:
     individual i's sub-stream prefix (word_counts[i] words) in i order, then the archive-victim
-    words.  ``philox(key, ctr_hi, start, n)`` generates words (default: the device generator)."""
+    words, then (population reduction) the archive-shrink words.  ``philox(key, ctr_hi, start,
+    n)`` generates words (default: the device generator)."""
     gen_words = philox or philox_words
     parts = [gen_words(key, (generation << 32) | i, 0, int(c)) for i, c in enumerate(word_counts)]
     if archive_words:
         parts.append(gen_words(key, (generation << 32) | 0xFFFFFFFF, 0, int(archive_words)))
+    if shrink_words:
+        parts.append(gen_words(key, (generation << 32) | 0xFFFFFFFE, 0, int(shrink_words)))
     return np.concatenate(parts) if parts else np.zeros(0, np.uint64)

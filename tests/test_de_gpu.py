@@ -306,3 +306,59 @@ def test_exponential_reinitialize_words_mode(dev, cfg):
         assert np.array_equal(pop.cpu().numpy(), orc.pop), g
         assert np.max(np.abs(fit.cpu().numpy() - orc.fit) / np.maximum(1, np.abs(orc.fit))) <= 1e-12
         assert rng.state()["cursor"] == cursor
+
+
+@pytest.mark.parametrize("rate", [1.0, 0.5])
+def test_lshade_reduction_lockstep(dev, rate):
+    # L-SHADE (presets.hpp "lshade": shade + population_policy::linear_reduction, de/policy.hpp):
+    # after each generation the worst members (ties: higher index first) are removed down to
+    # round(N_init + (N_min - N_init) * fes / max_fes) and the archive shrinks to ceil(rate * N)
+    # by random swap-with-last evictions.  The reference engine, with a persistent
+    # evolution_state, replays the exported words generation by generation.
+    from paper_2505_17430_b200.de import preset_lshade
+    P, D, key = 60, 20, 0xD1CE
+    max_fes = P * 14
+    o, m = O.shift_rotation(29, D)
+    cfg = preset_lshade(0.11, P, rate, n_min=4)
+    prob = evb.ProblemInstance.base(evb.BaseKind.rastrigin, o, m, 0.0)
+    eng = DEEngine(cfg, P, D)
+    rng = Rng.philox(key)
+    pop = torch.empty((P, D), dtype=torch.float64, device=dev)
+    eng.init_population(pop, -100.0, 100.0, rng)
+    fit = dev_eval(prob, pop, dev)
+    eng.set_budget(max_fes, P)
+    ref = O.RefDE(cfg, P, D)
+    ref.set_problem_base(5, o, m, 0.0)
+    ref.set_pop(pop.cpu().numpy(), fit.cpu().numpy())
+    ref.set_budget(max_fes, P)
+    fes, sizes, flips, shrunk = P, [P], 0, 0
+    while fes < max_fes:
+        eng.generation(prob, pop, fit, -100.0, 100.0, rng)
+        fes += sizes[-1]
+        dr, red = eng.last_draws(), eng.last_reduction()
+        assert red["pop_before"] == sizes[-1] == len(dr["word_counts"])
+        shrunk += red["shrink_words"]
+        words = scripted_words_for_generation(key, dr["generation"], dr["word_counts"], dr["archive_words"],
+                                              philox=O.philox_words, shrink_words=red["shrink_words"])
+        assert ref.generation(words, -100.0, 100.0), len(sizes)
+        n = red["pop_after"]
+        assert ref.pop_size() == n == eng.current_pop_size
+        target = int(np.clip(np.round(P + (4 - P) * fes / max_fes), 4, P))  # lround on exact halves aside
+        assert n == min(sizes[-1], target)
+        sizes.append(n)
+        st = ref.get()
+        got = pop[:n].cpu().numpy()
+        # F/CR from tan/log/cos: CUDA vs libm ulps perturb a row by ulps (flagged), and at worst
+        # flip a near-tie selection; everything integer (sizes, word counts) matched exactly above
+        close = np.all(np.abs(got - st["pop"]) <= 1e-9 * np.maximum(1.0, np.abs(st["pop"])), axis=1)
+        flips += int((~close).sum())
+        assert close.mean() >= 0.9
+        assert eng.get_state()["archive_size"] == st["archive_size"]
+        # F/CR come from tan/log/cos (ulps, flagged): re-sync to the reference
+        pop[:n].copy_(torch.from_numpy(st["pop"]))
+        fit[:n].copy_(torch.from_numpy(st["fit"]))
+        eng.set_state(st["archive"], st["memory_f"], st["memory_cr"], st["write_index"])
+    assert sizes[-1] < P // 2
+    assert flips <= 3
+    if rate < 1.0:
+        assert shrunk > 0

@@ -106,3 +106,18 @@ def test_evo_bench_errors(dev):
         evo_bench_de(preset_de(), 20, suite, 1, 0)
     with pytest.raises(evb.ConfigError):
         evo_bench_de(preset_de(), 3, suite, 1, 100)
+
+
+def test_engine_path_lshade(dev):
+    # L-SHADE through optimize(): the population shrinks on schedule; the FE count stops at the
+    # first generation boundary at or past max_fes (de/engine.hpp:124, core/state.hpp:40)
+    from paper_2505_17430_b200.de import preset_lshade
+    D, P, max_fes, runs = 10, 40, 40 * 10, 2
+    suite, _ = make_suite(D, [K.rastrigin], 2)
+    rec = BestSoFarRecorder(4, max_fes, 40)
+    res = evo_bench_de(preset_lshade(0.11, P, 1.0, n_min=4), P, suite, runs, max_fes, master_seed=8, recorder=rec)
+    assert res["path"] == "engine"
+    grid, fes = rec.grid()
+    assert np.all(fes >= max_fes) and np.all(fes < max_fes + P)
+    assert np.all(fes != P * (max_fes // P))  # sizes shrank, so the count is not a multiple of P
+    assert np.all(np.diff(grid, axis=1) <= 0)
