@@ -268,6 +268,27 @@ EVB_API int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int pop
                         double ub, void* pops, void* fits, int init, uint32_t gen0, evb_recorder rec,
                         void* stream);
 
+/* ---- Competitive Swarm Optimizer (pso/cso.hpp:19-99, cso_optimizer<T>) ----------------------- */
+
+typedef struct evb_cso_s* evb_cso;
+
+/* cso_optimizer(phi): phi finite and >= 0, pop_size even (cso.hpp:25-27, 34). */
+EVB_API int evb_cso_create(int dtype, double phi, int pop_size, int dim, evb_cso* out);
+EVB_API int evb_cso_destroy(evb_cso c);
+/* cso_optimizer::generation (cso.hpp:31-72) — exactly the reference's generation (it is
+ * data-parallel: mean of the pre-update swarm, disjoint pairs, losers read only winners).
+ * X, V: pop_size x ld row-major device arrays; fitness: current fitness (losers updated). */
+EVB_API int evb_cso_generation(evb_cso c, evb_problem objective, evb_scratch s, void* X, int64_t ldx, void* V,
+                               int64_t ldv, void* fitness, double lb, double ub, evb_rng rng, void* stream);
+/* cso_optimizer::optimize (cso.hpp:74-91): init_population, evaluate, zero velocities,
+ * generations (pop_size / 2 evaluations each) while fes < max_fes; best = population::best. */
+EVB_API int evb_cso_optimize(evb_cso c, evb_problem objective, evb_scratch s, void* X, int64_t ldx, void* V,
+                             int64_t ldv, void* fitness, double lb, double ub, int64_t max_fes, evb_rng rng,
+                             int* best_index, double* best_fitness, int* generations, void* stream);
+/* Report the optimizer's evaluations (initial P in optimize, each generation's losers in pair
+ * order) to recorder run `run`; r = NULL detaches. */
+EVB_API int evb_cso_attach_recorder(evb_cso c, evb_recorder r, int run);
+
 /* ---- suite-level grouped launch (experiment/runner.hpp:101-160 evo_bench) ----------------- */
 
 /* Philox key of task t: splitmix64(master_seed ^ t), the positional analogue of

@@ -585,3 +585,52 @@ def ref_evo_bench_de(f, cr, P, D, problem_ids, instances, runs, max_fes, interva
     buf = ctypes.create_string_buffer(int(n) + 1)
     REF().ref_evo_bench_de(*args, buf, int(n), ptr(best))
     return buf.raw[:n].decode(), best
+
+
+register_ref({
+    "ref_cso_create": (vp, [c_int, c_double, c_int, c_int, c_int, vp, vp, c_double]),
+    "ref_cso_set": (None, [c_int, vp, vp, vp, vp]),
+    "ref_cso_step": (c_int, [c_int, vp, vp, i64, c_double, c_double]),
+    "ref_cso_get": (None, [c_int, vp, vp, vp, vp]),
+    "ref_cso_native_optimize": (c_double, [c_int, vp, ctypes.c_uint64, ctypes.c_uint64, c_double, c_double,
+                                           ctypes.c_longlong]),
+    "ref_cso_destroy": (None, [c_int, vp]),
+})
+
+
+class RefCSO:
+    """The reference's cso_optimizer<T> (pso/cso.hpp) stepped with scripted words."""
+
+    def __init__(self, phi, P, D, kind, shift, rot, bias=0.0, dtype=np.float64):
+        self.nd = np.dtype(dtype)
+        self.dt = 1 if self.nd == np.float64 else 0
+        self.P, self.D = P, D
+        self._o = np.ascontiguousarray(shift, self.nd)
+        self._m = np.ascontiguousarray(rot, self.nd).ravel()
+        self.h = REF().ref_cso_create(self.dt, phi, P, D, kind, ptr(self._o), ptr(self._m), bias)
+
+    def set(self, x, v, fit):
+        x = np.ascontiguousarray(x, self.nd)
+        v = np.ascontiguousarray(v, self.nd)
+        f = np.ascontiguousarray(fit, self.nd)
+        REF().ref_cso_set(self.dt, self.h, ptr(x), ptr(v), ptr(f))
+
+    def step(self, words, lb, ub) -> bool:
+        w = np.ascontiguousarray(words, np.uint64)
+        return bool(REF().ref_cso_step(self.dt, self.h, ptr(w), len(w), lb, ub))
+
+    def get(self):
+        x = np.zeros((self.P, self.D), self.nd)
+        v = np.zeros((self.P, self.D), self.nd)
+        f = np.zeros(self.P, self.nd)
+        REF().ref_cso_get(self.dt, self.h, ptr(x), ptr(v), ptr(f))
+        return {"x": x, "v": v, "fit": f}
+
+    def native_optimize(self, seed, stream, lb, ub, max_fes):
+        return float(REF().ref_cso_native_optimize(self.dt, self.h, seed, stream, lb, ub, max_fes))
+
+    def __del__(self):
+        try:
+            REF().ref_cso_destroy(self.dt, self.h)
+        except Exception:
+            pass

@@ -672,3 +672,100 @@ REF_API int64_t ref_evo_bench_de(double f, double cr, int P, int D, int n_proble
   if (csv) std::memcpy(csv, s.data(), std::min<size_t>(size_t(cap), s.size()));
   return int64_t(s.size());
 }
+
+// ---- CSO (pso/cso.hpp): the UNMODIFIED cso_optimizer stepped generation by generation ----------
+#include "evobench/pso/cso.hpp"
+
+namespace {
+template <typename T>
+struct ref_cso_run {
+  std::unique_ptr<pso::cso_optimizer<T>> opt;
+  std::unique_ptr<problem_instance<T>> problem;
+  population<T> pop;
+  std::vector<std::vector<T>> v;
+  int P = 0, D = 0;
+};
+
+template <typename T>
+void* cso_create(double phi, int P, int D, int kind, const void* shift, const void* rot, double bias) {
+  auto* r = new ref_cso_run<T>();
+  r->opt = std::make_unique<pso::cso_optimizer<T>>(T(phi));
+  r->P = P;
+  r->D = D;
+  r->pop = population<T>(P, D);
+  r->v.assign(size_t(P), std::vector<T>(size_t(D), T(0)));
+  r->problem = std::make_unique<problem_instance<T>>(
+      make_base<T>(kind, D, static_cast<const T*>(shift), static_cast<const T*>(rot), bias));
+  return r;
+}
+
+template <typename T>
+void cso_set(void* h, const void* x, const void* v, const void* fit) {
+  auto* r = static_cast<ref_cso_run<T>*>(h);
+  for (int i = 0; i < r->P; ++i) {
+    std::memcpy(r->pop[i].genome.data(), static_cast<const T*>(x) + size_t(i) * r->D, sizeof(T) * r->D);
+    std::memcpy(r->v[size_t(i)].data(), static_cast<const T*>(v) + size_t(i) * r->D, sizeof(T) * r->D);
+    r->pop[i].fitness = static_cast<const T*>(fit)[i];
+    r->pop[i].evaluated = true;
+  }
+}
+
+template <typename T>
+int cso_step(void* h, const uint64_t* words, int64_t n, T lb, T ub) {
+  auto* r = static_cast<ref_cso_run<T>*>(h);
+  const uint64_t sentinel = 0x0c50c50c50c50c50ULL;
+  std::vector<uint64_t> w(words, words + n);
+  w.push_back(sentinel);
+  rng_stream rng = rng_stream::scripted(w);
+  evolution_state st(1LL << 40, r->P, r->D, std::min(4, r->P));
+  eval_scratch<T> scratch;
+  auto objective = [&](std::span<const T> x) { return r->problem->evaluate(x, scratch); };
+  r->opt->generation(r->pop, r->v, st, objective, lb, ub, rng);
+  return rng.next_u64() == sentinel ? 1 : 0;
+}
+
+template <typename T>
+void cso_get(void* h, void* x, void* v, void* fit) {
+  auto* r = static_cast<ref_cso_run<T>*>(h);
+  for (int i = 0; i < r->P; ++i) {
+    if (x) std::memcpy(static_cast<T*>(x) + size_t(i) * r->D, r->pop[i].genome.data(), sizeof(T) * r->D);
+    if (v) std::memcpy(static_cast<T*>(v) + size_t(i) * r->D, r->v[size_t(i)].data(), sizeof(T) * r->D);
+    if (fit) static_cast<T*>(fit)[i] = r->pop[i].fitness;
+  }
+}
+
+template <typename T>
+double cso_native(void* h, uint64_t seed, uint64_t stream, double lb, double ub, long long max_fes) {
+  auto* r = static_cast<ref_cso_run<T>*>(h);
+  rng_stream rng(seed, stream);
+  eval_scratch<T> scratch;
+  auto objective = [&](std::span<const T> x) { return r->problem->evaluate(x, scratch); };
+  const auto best = r->opt->optimize(objective, T(lb), T(ub), r->P, r->D, max_fes, rng);
+  return double(best.fitness);
+}
+}  // namespace
+
+REF_API void* ref_cso_create(int dtype, double phi, int P, int D, int kind, const void* shift, const void* rot,
+                             double bias) {
+  return dtype == 1 ? cso_create<double>(phi, P, D, kind, shift, rot, bias)
+                    : cso_create<float>(phi, P, D, kind, shift, rot, bias);
+}
+REF_API void ref_cso_set(int dtype, void* h, const void* x, const void* v, const void* fit) {
+  dtype == 1 ? cso_set<double>(h, x, v, fit) : cso_set<float>(h, x, v, fit);
+}
+REF_API int ref_cso_step(int dtype, void* h, const uint64_t* words, int64_t n, double lb, double ub) {
+  return dtype == 1 ? cso_step<double>(h, words, n, lb, ub) : cso_step<float>(h, words, n, float(lb), float(ub));
+}
+REF_API void ref_cso_get(int dtype, void* h, void* x, void* v, void* fit) {
+  dtype == 1 ? cso_get<double>(h, x, v, fit) : cso_get<float>(h, x, v, fit);
+}
+// cso_optimizer::optimize on the reference's NATIVE stream rng_stream(seed, stream); returns the best fitness
+REF_API double ref_cso_native_optimize(int dtype, void* h, uint64_t seed, uint64_t stream, double lb, double ub,
+                                       long long max_fes) {
+  return dtype == 1 ? cso_native<double>(h, seed, stream, lb, ub, max_fes)
+                    : cso_native<float>(h, seed, stream, lb, ub, max_fes);
+}
+REF_API void ref_cso_destroy(int dtype, void* h) {
+  if (dtype == 1) delete static_cast<ref_cso_run<double>*>(h);
+  else delete static_cast<ref_cso_run<float>*>(h);
+}

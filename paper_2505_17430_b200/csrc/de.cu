@@ -827,7 +827,7 @@ void reduce_t(evb_de_s* e, void* pop, int64_t ldp, void* fit, evb_rng_s* r, cuda
 }
 
 template <typename T>
-void init_population_t(evb_de_s* e, void* pop, int64_t ldp, double lb, double ub, evb_rng_s* r, cudaStream_t st) {
+void init_population_t(int P, int D, void* pop, int64_t ldp, double lb, double ub, evb_rng_s* r, cudaStream_t st) {
   word_source src{r->mode, r->key, r->d_words, r->n_words};
   int64_t base = 0;
   if (r->mode == RNG_WORDS) {
@@ -835,12 +835,12 @@ void init_population_t(evb_de_s* e, void* pop, int64_t ldp, double lb, double ub
     EVB_CUDA(cudaStreamSynchronize(st));
   }
   const uint64_t ctr_hi = (uint64_t(r->gen) << 32) | kSubInit;
-  init_population_kernel<T><<<std::min<int64_t>(4096, (int64_t(e->P) * e->D + 255) / 256), 256, 0, st>>>(
-      static_cast<T*>(pop), ldp, e->P, e->D, lb, ub, src, ctr_hi, base, r->d_overflow);
+  init_population_kernel<T><<<std::min<int64_t>(4096, (int64_t(P) * D + 255) / 256), 256, 0, st>>>(
+      static_cast<T*>(pop), ldp, P, D, lb, ub, src, ctr_hi, base, r->d_overflow);
   count_launch();
   EVB_CUDA(cudaGetLastError());
   if (r->mode == RNG_WORDS) {
-    const int64_t nb = base + int64_t(e->P) * e->D;
+    const int64_t nb = base + int64_t(P) * D;
     EVB_CUDA(cudaMemcpyAsync(r->d_cursor, &nb, sizeof(int64_t), cudaMemcpyHostToDevice, st));
     EVB_CUDA(cudaStreamSynchronize(st));
   } else {
@@ -857,9 +857,15 @@ void de_generation(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, v
   else generation_t<float>(e, prob, sc, pop, ldp, fit, lb, ub, r, st);
 }
 
+// init_population (core/population.hpp:88-98): P x D uniforms in [lb, ub], individual-major
+void population_init(int dtype, int P, int D, void* pop, int64_t ldp, double lb, double ub, evb_rng_s* r,
+                     cudaStream_t st) {
+  if (dtype == EVB_F64) init_population_t<double>(P, D, pop, ldp, lb, ub, r, st);
+  else init_population_t<float>(P, D, pop, ldp, lb, ub, r, st);
+}
+
 void de_init_population(evb_de_s* e, void* pop, int64_t ldp, double lb, double ub, evb_rng_s* r, cudaStream_t st) {
-  if (e->dtype == EVB_F64) init_population_t<double>(e, pop, ldp, lb, ub, r, st);
-  else init_population_t<float>(e, pop, ldp, lb, ub, r, st);
+  population_init(e->dtype, e->P, e->D, pop, ldp, lb, ub, r, st);
 }
 
 }  // namespace evb

@@ -227,6 +227,11 @@ int recorder_runs(evb_recorder_s* rec);
 std::string runs_kernel_unsupported(int dtype, const evb_de_config* cfg, int pop_size, int dim,
                                     const evb_problem* problems, int n_runs);
 
+// init_population (de.cu): P x D uniforms in [lb, ub] from the rng (Philox sub-stream kSubInit of
+// the current generation, or the WORDS cursor); advances the rng like the reference's stream
+void population_init(int dtype, int P, int D, void* pop, int64_t ldp, double lb, double ub, evb_rng_s* r,
+                     cudaStream_t st);
+
 // device generation counter <- host mirror (after host-side Philox consumers such as init)
 void set_device_gen(evb_rng_s* r, cudaStream_t st);
 
