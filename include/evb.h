@@ -311,12 +311,13 @@ EVB_API int evb_evo_bench_de(int dtype, const evb_de_config* cfg, int pop_size, 
 /* ---- PSO engine (pso/engine.hpp:33-153, pso/topology.hpp, pso/update.hpp) ------------------ */
 
 enum evb_pso_topology { EVB_TOPO_GBEST = 0 /* "gbest" */, EVB_TOPO_LBEST_RING = 1 /* "lbest_ring" */ };
-enum evb_pso_update { EVB_UPD_STANDARD = 0 /* "standard" */ };
+enum evb_pso_update { EVB_UPD_STANDARD = 0 /* "standard" */, EVB_UPD_SPHERICAL = 1 /* "spherical" (SPSO2011) */ };
 
 typedef struct {
   int topology, update;
   double inertia, cognitive, social; /* swarm_params (pso/update.hpp:16-22) */
   double vmax;                       /* > 0: clamp |v| <= vmax after the velocity rule (config 3) */
+  double attraction;                 /* swarm_params::attraction c of the spherical rule        */
 } evb_pso_config;
 
 typedef struct evb_pso_s* evb_pso;

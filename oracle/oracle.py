@@ -412,7 +412,7 @@ class OracleDE:
 # ---- PSO: synchronous driver over the reference pieces (REF) and the C restatement (C) ------------
 register_ref({
     "ref_pso_create": (vp, [c_int, c_int, c_double, c_double, c_double, c_double, c_int, c_int, c_int, vp, vp,
-                            c_double]),
+                            c_double, c_int, c_double]),
     "ref_pso_set": (None, [c_int, vp, vp, vp, vp]),
     "ref_pso_step": (c_int, [c_int, vp, vp, i64, c_double, c_double]),
     "ref_pso_get": (None, [c_int, vp, vp, vp, vp, vp, vp]),
@@ -426,13 +426,15 @@ register_c(_PSO_C)
 
 
 class RefPSO:
-    def __init__(self, dtype_np, topology, w, c1, c2, vmax, P, D, kind, shift, rot, bias=0.0):
+    def __init__(self, dtype_np, topology, w, c1, c2, vmax, P, D, kind, shift, rot, bias=0.0, update=0,
+                 attraction=0.0):
         self.nd = dtype_np
         self.dt = 1 if dtype_np == np.float64 else 0
         self.P, self.D = P, D
         self._o = np.ascontiguousarray(shift, dtype_np)
         self._m = np.ascontiguousarray(rot, dtype_np).ravel()
-        self.h = REF().ref_pso_create(self.dt, topology, w, c1, c2, vmax, P, D, kind, ptr(self._o), ptr(self._m), bias)
+        self.h = REF().ref_pso_create(self.dt, topology, w, c1, c2, vmax, P, D, kind, ptr(self._o), ptr(self._m), bias,
+                                      update, attraction)
 
     def set(self, x, v, fit):
         x, v, f = (np.ascontiguousarray(a, self.nd) for a in (x, v, fit))

@@ -380,7 +380,7 @@ namespace {
 template <typename T>
 struct ref_pso_run {
   std::unique_ptr<pso::topology_strategy<T>> topo;
-  pso::standard_update<T> upd;
+  std::unique_ptr<pso::velocity_update_strategy<T>> upd;
   pso::swarm_params<T> params;
   T vmax;
   std::unique_ptr<problem_instance<T>> problem;
@@ -401,7 +401,7 @@ struct ref_pso_run {
     for (int i = 0; i < P; ++i) {
       auto& xi = x[size_t(i)];
       auto& vi = v[size_t(i)];
-      upd.apply(xi, vi, snapshot[size_t(i)].genome, snapshot[size_t(nb[size_t(i)])].genome, nb[size_t(i)] == i,
+      upd->apply(xi, vi, snapshot[size_t(i)].genome, snapshot[size_t(nb[size_t(i)])].genome, nb[size_t(i)] == i,
                 params, rng);
       for (int j = 0; j < D; ++j) {
         if (vmax > T(0)) {
@@ -438,10 +438,13 @@ struct ref_pso_run {
 
 template <typename T>
 void* pso_create(int topology, double w, double c1, double c2, double vmax, int P, int D, int kind, const void* shift,
-                 const void* rot, double bias) {
+                 const void* rot, double bias, int update, double attraction) {
   auto* r = new ref_pso_run<T>();
   if (topology == 0) r->topo = std::make_unique<pso::gbest_topology<T>>();
   else r->topo = std::make_unique<pso::lbest_topology<T>>();
+  if (update == 1) r->upd = std::make_unique<pso::spherical_update<T>>();
+  else r->upd = std::make_unique<pso::standard_update<T>>();
+  r->params.attraction = T(attraction);
   r->params.inertia = T(w);
   r->params.cognitive = T(c1);
   r->params.social = T(c2);
@@ -487,9 +490,9 @@ void pso_get(void* h, void* x, void* v, void* fit, void* pb, void* pbf) {
 }  // namespace
 
 REF_API void* ref_pso_create(int dtype, int topology, double w, double c1, double c2, double vmax, int P, int D,
-                             int kind, const void* shift, const void* rot, double bias) {
-  return dtype == 1 ? pso_create<double>(topology, w, c1, c2, vmax, P, D, kind, shift, rot, bias)
-                    : pso_create<float>(topology, w, c1, c2, vmax, P, D, kind, shift, rot, bias);
+                             int kind, const void* shift, const void* rot, double bias, int update, double attraction) {
+  return dtype == 1 ? pso_create<double>(topology, w, c1, c2, vmax, P, D, kind, shift, rot, bias, update, attraction)
+                    : pso_create<float>(topology, w, c1, c2, vmax, P, D, kind, shift, rot, bias, update, attraction);
 }
 REF_API void ref_pso_set(int dtype, void* h, const void* x, const void* v, const void* fit) {
   dtype == 1 ? pso_set<double>(h, x, v, fit) : pso_set<float>(h, x, v, fit);

@@ -29,7 +29,7 @@ struct evb_pso_s {
   int P = 0, D = 0;
   int topology = EVB_TOPO_GBEST;
   int update = EVB_UPD_STANDARD;
-  double w = 0, c1 = 0, c2 = 0, vmax = 0;
+  double w = 0, c1 = 0, c2 = 0, vmax = 0, attraction = 0;
   int64_t ldb = 0;
   void* pbest = nullptr;      // P x ldb
   void* pbest_fit = nullptr;  // P
@@ -111,7 +111,7 @@ struct pso_dev {
   const T* pb;
   int64_t ldb;
   const int* nb;
-  T w, c1, c2, vmax;
+  T w, c1, c2, vmax, c;
   int clamp;
   T lb, ub;
   word_source src;
@@ -159,6 +159,96 @@ __global__ void __launch_bounds__(256) pso_update_kernel(const pso_dev<T> d) {
   }
   xr[j] = xn;
   vr[j] = v;
+}
+
+// SPSO2011 spherical rule (pso/update.hpp:81-114, sample_in_ball :24-43), one block per particle.
+// Per gene (parallel): p* = x + c (p - x), l* = x + c (l - x), centre G = (x + p* [+ l*]) / 2|3,
+// the normal g_j (Box-Muller on words 2j, 2j+1); then the two double sums |G - x|^2 and |g|^2 in
+// increasing j (sequential, the reference's order), u = word 2D, scale = r u^(1/D) / |g|, and
+// v = w v + (G + T(scale g_j) - x).  Draws: 2D + 1 words per particle.
+template <typename T>
+__global__ void pso_spherical_kernel(const pso_dev<T> d) {
+  using F = fop<T>;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  double* rad = reinterpret_cast<double*>(smem_raw);  // D
+  double* nrm = rad + d.D;                            // D
+  T* cen = reinterpret_cast<T*>(nrm + d.D);           // D
+  T* gt = cen + d.D;                                  // D: T(g_j)
+  __shared__ double s_scale;
+  __shared__ double s_sum[2];
+  const int i = blockIdx.x;
+  const int nbi = d.nb[i];
+  const bool self = nbi == i;
+  const T* xr = d.x + size_t(i) * d.ldx;
+  const T* pr = d.pb + size_t(i) * d.ldb;
+  const T* lr = d.pb + size_t(nbi) * d.ldb;
+  const uint64_t ctr_hi = (uint64_t(*d.gen_ptr) << 32) | uint32_t(i);
+  const int64_t base = d.base + int64_t(i) * (2 * int64_t(d.D) + 1);  // WORDS
+  for (int j = threadIdx.x; j < d.D; j += blockDim.x) {
+    const T x = xr[j];
+    const T ps = F::add(x, F::mul(d.c, F::sub(pr[j], x)));
+    T g;
+    if (self) {
+      g = F::div(F::add(x, ps), T(2));
+    } else {
+      const T ls = F::add(x, F::mul(d.c, F::sub(lr[j], x)));
+      g = F::div(F::add(F::add(x, ps), ls), T(3));
+    }
+    cen[j] = g;
+    const double dd = double(F::sub(g, x));
+    rad[j] = __dmul_rn(dd, dd);
+    uint64_t w0, w1;
+    if (d.src.mode == RNG_PHILOX) {
+      philox_pair(d.src.key, ctr_hi, uint64_t(j), w0, w1);
+    } else {
+      w0 = word_at(d.src, 0, base + 2 * j, d.overflow);
+      w1 = word_at(d.src, 0, base + 2 * j + 1, d.overflow);
+    }
+    // rng_stream::normal(0, 1) (core/rng.hpp:96-101)
+    const double r = __dsqrt_rn(__dmul_rn(-2.0, log(u01pos_of(w0))));
+    const double gn = __dadd_rn(0.0, __dmul_rn(__dmul_rn(1.0, r), cos(__dmul_rn(2.0 * 3.14159265358979323846, u01_of(w1)))));
+    gt[j] = T(gn);
+    nrm[j] = __dmul_rn(gn, gn);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 || threadIdx.x == 32) {  // two sequential sums, one per warp
+    const double* a = threadIdx.x == 0 ? rad : nrm;
+    double acc = 0.0;
+    for (int j = 0; j < d.D; ++j) acc = __dadd_rn(acc, a[j]);
+    s_sum[threadIdx.x == 0 ? 0 : 1] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint64_t wu = d.src.mode == RNG_PHILOX ? philox_word(d.src.key, ctr_hi, uint64_t(2 * d.D))
+                                                 : word_at(d.src, 0, base + 2 * d.D, d.overflow);
+    const double u = u01_of(wu);
+    const double norm = __dsqrt_rn(s_sum[1]);
+    const double radius = __dsqrt_rn(s_sum[0]);
+    s_scale = norm > 0.0 ? __ddiv_rn(__dmul_rn(radius, pow(u, __ddiv_rn(1.0, double(d.D)))), norm) : 0.0;
+  }
+  __syncthreads();
+  const double scale = s_scale;
+  T* xw = d.x + size_t(i) * d.ldx;
+  T* vw = d.v + size_t(i) * d.ldv;
+  for (int j = threadIdx.x; j < d.D; j += blockDim.x) {
+    const T x = xw[j];
+    const T sample = F::add(cen[j], T(__dmul_rn(scale, double(gt[j]))));
+    T v = F::add(F::mul(d.w, vw[j]), F::sub(sample, x));
+    if (d.clamp) {
+      if (v > d.vmax) v = d.vmax;
+      if (v < -d.vmax) v = -d.vmax;
+    }
+    T xn = F::add(x, v);
+    if (xn < d.lb) {
+      xn = d.lb;
+      v = F::mul(T(-0.5), v);
+    } else if (xn > d.ub) {
+      xn = d.ub;
+      v = F::mul(T(-0.5), v);
+    }
+    xw[j] = xn;
+    vw[j] = v;
+  }
 }
 
 // pbest update (pso/engine.hpp:78-79): strict <, copy the moved particle; also publishes the
@@ -219,6 +309,7 @@ void generation_t(evb_pso_s* s, const device_problem* prob, evb_scratch_s* sc, v
   d.c1 = T(s->c1);
   d.c2 = T(s->c2);
   d.vmax = T(s->vmax);
+  d.c = T(s->attraction);
   d.clamp = s->vmax > 0 ? 1 : 0;
   d.lb = T(lb);
   d.ub = T(ub);
@@ -226,11 +317,24 @@ void generation_t(evb_pso_s* s, const device_problem* prob, evb_scratch_s* sc, v
   d.gen_ptr = r->d_gen;
   d.overflow = r->d_overflow;
   if (r->mode == RNG_WORDS) d.base = words_cursor(r, st);
-  dim3 grid((s->D + 255) / 256, s->P);
-  pso_update_kernel<T><<<grid, 256, 0, st>>>(d);
+  int64_t words_per_particle = 2 * int64_t(s->D);
+  if (s->update == EVB_UPD_SPHERICAL) {
+    const size_t smem = size_t(s->D) * (2 * sizeof(double) + 2 * sizeof(T));
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+      EVB_CUDA(cudaFuncSetAttribute(pso_spherical_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      attr = smem;
+    }
+    const int threads = std::max(64, std::min(256, int(round_up(s->D, 32))));  // warps 0 and 1 run the two sums
+    pso_spherical_kernel<T><<<s->P, threads, smem, st>>>(d);
+    words_per_particle += 1;
+  } else {
+    dim3 grid((s->D + 255) / 256, s->P);
+    pso_update_kernel<T><<<grid, 256, 0, st>>>(d);
+  }
   count_launch();
   EVB_CUDA(cudaGetLastError());
-  if (r->mode == RNG_WORDS) words_advance(r, d.base + int64_t(s->P) * s->D * 2, st);
+  if (r->mode == RNG_WORDS) words_advance(r, d.base + int64_t(s->P) * words_per_particle, st);
   eval_request rq{};
   rq.prob = prob;
   rq.scratch = sc;
@@ -283,7 +387,11 @@ int evb_pso_create(int dtype, const evb_pso_config* c, int pop_size, int dim, ev
     require(c != nullptr && out != nullptr, "pso: null config or output handle");
     require(c->topology == EVB_TOPO_GBEST || c->topology == EVB_TOPO_LBEST_RING,
             "pso builder: unknown topology strategy (GPU kernels: gbest, lbest_ring)");
-    require(c->update == EVB_UPD_STANDARD, "pso builder: unknown update strategy (GPU kernels: standard)");
+    require(c->update == EVB_UPD_STANDARD || c->update == EVB_UPD_SPHERICAL,
+            "pso builder: unknown update strategy (GPU kernels: standard, spherical)");
+    if (c->update == EVB_UPD_SPHERICAL)
+      require(size_t(dim) * (2 * 8 + 2 * (dtype == EVB_F64 ? 8 : 4)) <= 200 * 1024,
+              "pso: spherical update keeps 4 rows per particle in shared memory (dim <= 6400)");
     require(pop_size >= 1 && dim >= 1, "pso: pop_size and dim must be positive");
     auto* s = new evb_pso_s();
     try {
@@ -296,6 +404,7 @@ int evb_pso_create(int dtype, const evb_pso_config* c, int pop_size, int dim, ev
       s->c1 = c->cognitive;
       s->c2 = c->social;
       s->vmax = c->vmax;
+      s->attraction = c->attraction;
       const size_t es = dtype == EVB_F64 ? 8 : 4;
       s->ldb = round_up(dim, 16 / int64_t(es));
       EVB_CUDA(cudaMalloc(&s->pbest, es * s->ldb * pop_size));

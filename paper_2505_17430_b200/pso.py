@@ -17,12 +17,13 @@ from .de import Rng, _sigs as _de_sigs
 from .problems import EvalScratch, ProblemInstance, _stream_ptr, dtype_of
 
 TOPOLOGIES = {"gbest": 0, "lbest_ring": 1}
-UPDATES = {"standard": 0}
+UPDATES = {"standard": 0, "spherical": 1}
 
 
 class _Cfg(ctypes.Structure):
     _fields_ = [("topology", ctypes.c_int), ("update", ctypes.c_int), ("inertia", ctypes.c_double),
-                ("cognitive", ctypes.c_double), ("social", ctypes.c_double), ("vmax", ctypes.c_double)]
+                ("cognitive", ctypes.c_double), ("social", ctypes.c_double), ("vmax", ctypes.c_double),
+                ("attraction", ctypes.c_double)]
 
 
 @dataclass
@@ -35,6 +36,7 @@ class PSOConfig:
     cognitive: float = 0.5 + math.log(2.0)
     social: float = 0.5 + math.log(2.0)
     vmax: float = 0.0  # > 0: clamp |v| (BASELINE config 3: 0.2 * range = 40)
+    attraction: float = 0.5 + math.log(2.0)  # spherical rule's c
 
     def to_c(self) -> _Cfg:
         if self.topology not in TOPOLOGIES:
@@ -42,7 +44,12 @@ class PSOConfig:
         if self.update not in UPDATES:
             raise ConfigError(f"pso builder: unknown update strategy '{self.update}' (no GPU kernel)")
         return _Cfg(TOPOLOGIES[self.topology], UPDATES[self.update], self.inertia, self.cognitive, self.social,
-                    self.vmax)
+                    self.vmax, self.attraction)
+
+
+def preset_spso2011() -> PSOConfig:
+    """presets.hpp build_pso(spherical_ring = true): lbest ring + spherical update, SPSO2011 constants."""
+    return PSOConfig("lbest_ring", "spherical")
 
 
 def config3(topology: str) -> PSOConfig:
@@ -134,10 +141,13 @@ class PSOEngine:
             pass
 
 
-def scripted_words_for_generation(key: int, generation: int, pop_size: int, dim: int, philox=None):
+def scripted_words_for_generation(key: int, generation: int, pop_size: int, dim: int, philox=None,
+                                  update: str = "standard"):
     """The sequential words the reference driver consumes for one Philox-mode PSO generation:
-    particle i's sub-stream (g << 32) | i, 2*dim words (r1, r2 per gene), in particle order."""
+    particle i's sub-stream (g << 32) | i in particle order — 2*dim words (r1, r2 per gene) for the
+    standard rule, 2*dim + 1 (dim normal pairs, then the radius uniform) for the spherical rule."""
     from .de import philox_words
 
     gen = philox or philox_words
-    return np.concatenate([gen(key, (generation << 32) | i, 0, 2 * dim) for i in range(pop_size)])
+    n = 2 * dim + (1 if update == "spherical" else 0)
+    return np.concatenate([gen(key, (generation << 32) | i, 0, n) for i in range(pop_size)])

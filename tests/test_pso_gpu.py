@@ -68,3 +68,50 @@ def test_config3_small(dev, topology, nd):
 def test_config3_full_size_fp64(dev, topology):
     # D=1000, pop 1024 (the config's full size) for two generations
     run(dev, topology, np.float64, 1024, 1000, 2)
+
+
+@pytest.mark.parametrize("topology", ["lbest_ring", "gbest"])
+@pytest.mark.parametrize("nd,P,D", [(np.float64, 64, 30), (np.float32, 64, 30), (np.float64, 256, 1000)])
+def test_spso2011_spherical_lockstep(dev, topology, nd, P, D):
+    # SPSO2011 rule (pso/update.hpp:81-114 spherical_update + sample_in_ball :24-43) in the
+    # synchronous generation: the reference driver applies the UNMODIFIED spherical_update with the
+    # exported words (2D + 1 per particle) and must consume exactly that many.  log/cos/pow come
+    # from CUDA vs glibc, so positions agree to ulps (tolerance), and the GPU is re-synced each
+    # generation; the neighbour-is-self case (G from x and p* only) is exercised by gbest's best
+    from paper_2505_17430_b200.pso import PSOConfig
+    dtype = evb.EVB_F64 if nd == np.float64 else evb.EVB_F32
+    tdt = torch.float64 if nd == np.float64 else torch.float32
+    key, G = 0x5B0 + D, 6
+    cfg = PSOConfig(topology, "spherical")
+    o, m = O.shift_rotation(31, D)
+    o, m = o.astype(nd), m.astype(nd)
+    prob = evb.ProblemInstance.base(evb.BaseKind.sphere, o, m, 0.0, dtype=dtype)
+    eng = PSOEngine(cfg, P, D, dtype)
+    rng = Rng.philox(key)
+    X = torch.empty((P, D), dtype=tdt, device=dev)
+    V = torch.empty((P, D), dtype=tdt, device=dev)
+    eng.init_uniform(X, -100.0, 100.0, rng)
+    eng.init_uniform(V, -20.0, 20.0, rng)
+    fit = torch.empty(P, dtype=tdt, device=dev)
+    evb.evaluate_batch(prob, X, evb.EvalScratch(), fit)
+    eng.prepare(X, fit)
+    ref = O.RefPSO(nd, 0 if topology == "gbest" else 1, cfg.inertia, cfg.cognitive, cfg.social, 0.0, P, D, 0, o, m,
+                   update=1, attraction=cfg.attraction)
+    ref.set(X.cpu().numpy(), V.cpu().numpy(), fit.cpu().numpy())
+    tol = 1e-9 if nd == np.float64 else 2e-4
+    for g in range(G):
+        eng.generation(prob, X, V, fit, -100.0, 100.0, rng)
+        st_gpu = eng.personal_bests()
+        words = scripted_words_for_generation(key, st_gpu["generation"], P, D, philox=O.philox_words,
+                                              update="spherical")
+        assert ref.step(words, -100.0, 100.0), g
+        st = ref.get()
+        for name, got in (("x", X), ("v", V)):
+            a = got.cpu().numpy().astype(np.float64)
+            b = st[name].astype(np.float64)
+            scale = np.maximum(1.0, np.abs(b))
+            assert np.max(np.abs(a - b) / scale) <= tol, (g, name)
+        X.copy_(torch.from_numpy(st["x"]))
+        V.copy_(torch.from_numpy(st["v"]))
+        fit.copy_(torch.from_numpy(st["fit"]))
+        eng.set_personal_bests(st["pbest"], st["pbest_fit"])
