@@ -78,17 +78,24 @@ struct fused_params {
                      // corrections in separate TMEM accumulators (summed in the epilogue)
 };
 
+// cosine of the fused epilogue: library cos for fp64, the reference's batched fast_cos for fp32
+template <typename T>
+__device__ __forceinline__ T epi_cos(T x) { return trig<T, true>::cos_(x); }
+
 template <typename T>
 __device__ __forceinline__ T term_value(int term, T v, int col, const T* ell_w) {
   using F = fop<T>;
   switch (term) {
     case TERM_SQ: return F::mul(v, v);
     case TERM_WSQ: return elliptic_term<T>(ell_w[col], v);
-    case TERM_RAST: return rastrigin_term<T, true>(v);
-    case TERM_COS: return trig<T, true>::cos_(F::mul(two_pi_v<T>(), v));
+    case TERM_RAST: {  // v*v - T(10) * cos(two_pi * v) + T(10)  (problems/batch.hpp:161)
+      const T c = epi_cos<T>(F::mul(two_pi_v<T>(), v));
+      return F::add(F::sub(F::mul(v, v), F::mul(T(10), c)), T(10));
+    }
+    case TERM_COS: return epi_cos<T>(F::mul(two_pi_v<T>(), v));
     case TERM_TAIL: return col >= 1 ? F::mul(v, v) : T(0);
     case TERM_HEAD: return col == 0 ? v : T(0);
-    case TERM_GCOS: return trig<T, true>::cos_(F::div(v, F::sqrt_(T(col + 1))));
+    case TERM_GCOS: return epi_cos<T>(F::div(v, F::sqrt_(T(col + 1))));
   }
   return T(0);
 }
@@ -347,19 +354,25 @@ __global__ void __launch_bounds__(f64_cfg<BM, BN, WM, WN, STAGES>::THREADS, MINB
     const uint32_t sA = smem_base + s * C::STAGE_BYTES;
     const uint32_t sB = sA + C::A_BYTES;
     const uint32_t sO = sB + C::B_BYTES;
-#pragma unroll
-    for (int ks = 0; ks < C::KB / 4; ++ks) {
+    // fragments double-buffered across the stage's k4 steps: step ks+1's loads and its shift
+    // subtraction are issued before step ks's DMMAs, so their latency hides behind the MMAs
+    double a[2][C::TM], b[2][C::TN];
+    auto load = [&](int ks, int buf) {
       const int kk = ks * 4 + t;
       const double o = ptx::lds_f64(sO + kk * 8);
-      double a[C::TM], b[C::TN];
 #pragma unroll
-      for (int i = 0; i < C::TM; ++i) a[i] = __dsub_rn(ptx::lds_f64(sA + swz<8>(rA + i * 8 + g, kk)), o);
+      for (int i = 0; i < C::TM; ++i) a[buf][i] = __dsub_rn(ptx::lds_f64(sA + swz<8>(rA + i * 8 + g, kk)), o);
 #pragma unroll
-      for (int j = 0; j < C::TN; ++j) b[j] = ptx::lds_f64(sB + swz<8>(rB + j * 8 + g, kk));
+      for (int j = 0; j < C::TN; ++j) b[buf][j] = ptx::lds_f64(sB + swz<8>(rB + j * 8 + g, kk));
+    };
+    load(0, 0);
+#pragma unroll
+    for (int ks = 0; ks < C::KB / 4; ++ks) {
+      if (ks + 1 < C::KB / 4) load(ks + 1, (ks + 1) & 1);
 #pragma unroll
       for (int i = 0; i < C::TM; ++i)
 #pragma unroll
-        for (int j = 0; j < C::TN; ++j) ptx::dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        for (int j = 0; j < C::TN; ++j) ptx::dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[ks & 1][i], b[ks & 1][j]);
     }
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(&empty[s]);
@@ -993,7 +1006,8 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
       }
     }
     if (force && std::string(force) == "classic" && best == 0) best = 1;
-    if (force && std::string(force) == "pair") best = 0;
+    if (force && (std::string(force) == "pair" || std::string(force) == "pair2")) best = 0;
+    if (force && std::string(force) == "wide2") best = 1;
     BM = cands[best][0];
     BN = cands[best][1];
     if (use_persistent) {
@@ -1112,7 +1126,11 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
       launch_f64_persistent<64, 56>(tmX, tmM, fp, rq.stream);
       return;
     }
-    if (BM == 64 && BN == 56) launch_f64<64, 56, 4, 1, 6, 2>(tmX, tmM, fp, rq.stream);
+    static const bool pair2 = force && std::string(force) == "pair2";
+    static const bool wide2 = force && std::string(force) == "wide2";
+    if (pair2) launch_f64<64, 56, 2, 1, 6, 2>(tmX, tmM, fp, rq.stream);  // 32 x 56 warp tiles (A/B)
+    else if (wide2) launch_f64<64, 112, 2, 2, 6, 1>(tmX, tmM, fp, rq.stream);
+    else if (BM == 64 && BN == 56) launch_f64<64, 56, 4, 1, 6, 2>(tmX, tmM, fp, rq.stream);
     else if (BM == 64 && BN == 112) launch_f64<64, 112, 4, 2>(tmX, tmM, fp, rq.stream);
     else if (BM == 64 && BN == 128) launch_f64<64, 128, 4, 2>(tmX, tmM, fp, rq.stream);
     else launch_f64<32, 128, 2, 4>(tmX, tmM, fp, rq.stream);

@@ -14,9 +14,11 @@
 //   select    trial replaces parent when f_trial <= f_parent (de/engine.hpp:36)
 // Supported here: rand/1 or best/1 with a fixed adapter and no archive (the `de` preset,
 // presets.hpp:59-69) on base or composition problems whose data fit in shared memory.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -53,6 +55,7 @@ struct runs_args {
   int init;
   int rec_on;
   rec_view<double> rec;  // best-so-far recorder, run r -> recorder run r
+  int split;             // CTAs per run (1, or a 2-CTA cluster that splits every evaluation)
 };
 
 __device__ __forceinline__ double clip_or_mid(double v, double target, double lb, double ub, int repair) {
@@ -181,10 +184,20 @@ __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int
   __syncthreads();
 }
 
+// With a.split == 2 the run is owned by a 2-CTA cluster: both CTAs hold the full run state and
+// make the same draws, trials and selections (bit-identical, deterministic), and each evaluates
+// half of the individuals; the halves of the fitness vector are exchanged through distributed
+// shared memory.  The trial fitness is double-buffered by generation parity, so one cluster
+// barrier per generation suffices (a CTA can only write the buffer its peer reads next).
 __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
+  namespace cg = cooperative_groups;
   extern __shared__ __align__(16) double sm[];
   const int P = a.P, D = a.D, S = (D % 2 == 1) ? D : D + 1;
-  const int run = blockIdx.x;
+  const int run = blockIdx.x / a.split;
+  const int rank = a.split == 2 ? int(cg::this_cluster().block_rank()) : 0;
+  const int half = (P + 1) / 2;
+  const int p0 = a.split == 2 ? rank * half : 0;
+  const int p1 = a.split == 2 ? min(P, p0 + half) : P;
   double* sPop = sm;                           // P x D
   double* sTrial = sPop + P * D;               // P x D
   double* sM = sTrial + P * D;                 // D x S
@@ -192,8 +205,8 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
   double* sS = sZ + P * D;                     // P x D  (x - o of the current component)
   double* sO = sS + P * D;                     // D
   double* sFit = sO + D;                       // P
-  double* sTfit = sFit + P;                    // P
-  double* sFk = sTfit + P;                     // P x 4
+  double* sTfit2 = sFit + P;                   // 2 x P (generation parity)
+  double* sFk = sTfit2 + 2 * P;                // P x 4
   double* sDist = sFk + P * kRunsMaxComp;      // P x 4
   int* sIdx = reinterpret_cast<int*>(sDist + P * kRunsMaxComp);  // P x 4 (a, b, c, word offset)
   const run_problem pr = a.probs[run];
@@ -201,14 +214,25 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
   double* gpop = a.pop + size_t(run) * P * D;
   double* gfit = a.fit + size_t(run) * P;
   word_source src{RNG_PHILOX, key, nullptr, 0};
+  // evaluate rows [p0, p1) of X into f, then (split) publish them into the peer's f
+  auto evaluate = [&](const double* X, double* f) {
+    runs_evaluate(pr, X + size_t(p0) * D, p1 - p0, D, S, sM, sZ, sS, sO, sFk, sDist, f + p0);
+    if (a.split == 2) {
+      cg::cluster_group cl = cg::this_cluster();
+      double* peer = cl.map_shared_rank(f, rank ^ 1);
+      for (int i = p0 + int(threadIdx.x); i < p1; i += blockDim.x) peer[i] = f[i];
+      cl.sync();
+    }
+  };
+  if (a.split == 2) cg::this_cluster().sync();  // the peer's shared memory exists from here on
 
   if (a.init) {  // init_population (core/population.hpp:88-98), sub-stream kSubInit of gen0
     const uint64_t ctr = (uint64_t(a.gen0) << 32) | kSubInit;
     for (int e = threadIdx.x; e < P * D; e += blockDim.x)
       sPop[e] = __dadd_rn(a.lb, __dmul_rn(__dsub_rn(a.ub, a.lb), u01_of(philox_word(key, ctr, uint64_t(e)))));  // once
     __syncthreads();
-    runs_evaluate(pr, sPop, P, D, S, sM, sZ, sS, sO, sFk, sDist, sFit);
-    if (a.rec_on && threadIdx.x == 0) rec_observe_seq<double>(a.rec, run, sFit, P);
+    evaluate(sPop, sFit);
+    if (a.rec_on && rank == 0 && threadIdx.x == 0) rec_observe_seq<double>(a.rec, run, sFit, P);
   } else {
     for (int e = threadIdx.x; e < P * D; e += blockDim.x) sPop[e] = gpop[e];
     for (int i = threadIdx.x; i < P; i += blockDim.x) sFit[i] = gfit[i];
@@ -217,6 +241,7 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
   const uint32_t g_first = a.gen0 + (a.init ? 1u : 0u);
   for (int g = 0; g < a.G; ++g) {
     const uint32_t gen = g_first + uint32_t(g);
+    double* sTfit = sTfit2 + (g & 1) * P;
     // draws (thread per individual)
     for (int i = threadIdx.x; i < P; i += blockDim.x) {
       word_reader r{&src, (uint64_t(gen) << 32) | uint32_t(i), 0, 0, nullptr};
@@ -260,8 +285,8 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
       }
     }
     __syncthreads();
-    runs_evaluate(pr, sTrial, P, D, S, sM, sZ, sS, sO, sFk, sDist, sTfit);
-    if (a.rec_on && threadIdx.x == 0) rec_observe_seq<double>(a.rec, run, sTfit, P);  // trials, i order
+    evaluate(sTrial, sTfit);
+    if (a.rec_on && rank == 0 && threadIdx.x == 0) rec_observe_seq<double>(a.rec, run, sTfit, P);  // trials, i order
     // selection
     {
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
@@ -274,13 +299,16 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
       if (sTfit[i] <= sFit[i]) sFit[i] = sTfit[i];
     __syncthreads();
   }
-  for (int e = threadIdx.x; e < P * D; e += blockDim.x) gpop[e] = sPop[e];
-  for (int i = threadIdx.x; i < P; i += blockDim.x) gfit[i] = sFit[i];
+  if (rank == 0) {
+    for (int e = threadIdx.x; e < P * D; e += blockDim.x) gpop[e] = sPop[e];
+    for (int i = threadIdx.x; i < P; i += blockDim.x) gfit[i] = sFit[i];
+  }
+  if (a.split == 2) cg::this_cluster().sync();  // no CTA leaves while its peer may still write into it
 }
 
 size_t runs_smem(int P, int D) {
   const int S = (D % 2 == 1) ? D : D + 1;
-  return sizeof(double) * (size_t(4) * P * D + size_t(D) * S + D + 2 * P + 2 * P * kRunsMaxComp) +
+  return sizeof(double) * (size_t(4) * P * D + size_t(D) * S + D + 3 * P + 2 * P * kRunsMaxComp) +
          sizeof(int) * 4 * P + 64;
 }
 
@@ -391,9 +419,33 @@ extern "C" int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int 
       a.rec = rec_view<double>{static_cast<double*>(grid), static_cast<double*>(running), next, fes, nck, itv};
     }
     EVB_CUDA(cudaFuncSetAttribute(de_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    de_runs_kernel<<<n_runs, 512, smem, st>>>(a);
+    // one run per SM leaves SMs idle when there are fewer runs than SMs: then a 2-CTA cluster
+    // shares each run's evaluations (EVB_RUNS_SPLIT=1|2 overrides)
+    int sms = 0;
+    EVB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    static const char* split_env = std::getenv("EVB_RUNS_SPLIT");
+    a.split = split_env ? (std::atoi(split_env) == 2 ? 2 : 1) : (2 * n_runs <= sms ? 2 : 1);
+    cudaError_t err;
+    if (a.split == 2) {
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(2 * n_runs);
+      lc.blockDim = dim3(512);
+      lc.dynamicSmemBytes = smem;
+      lc.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      lc.attrs = attr;
+      lc.numAttrs = 1;
+      err = cudaLaunchKernelEx(&lc, de_runs_kernel, a);
+    } else {
+      de_runs_kernel<<<n_runs, 512, smem, st>>>(a);
+      err = cudaGetLastError();
+    }
     count_launch();
-    const cudaError_t err = cudaGetLastError();
+    if (err == cudaSuccess) err = cudaGetLastError();
     EVB_CUDA(cudaStreamSynchronize(st));
     cudaFree(dprobs);
     cudaFree(dkeys);
