@@ -56,6 +56,8 @@ struct runs_args {
   int rec_on;
   rec_view<double> rec;  // best-so-far recorder, run r -> recorder run r
   int split;             // CTAs per run (1, or a 2-CTA cluster that splits every evaluation)
+  int resident;          // all rotations / shifts of a run staged in shared memory once
+  int n_mat;             // max components over the runs (resident slots)
 };
 
 __device__ __forceinline__ double clip_or_mid(double v, double target, double lb, double ub, int repair) {
@@ -75,17 +77,23 @@ __device__ __forceinline__ double clip_or_mid(double v, double target, double lb
 // lane r owns one row of M (conflict-free, odd stride) and up to 8 individuals of its group, whose
 // s[i][k] are warp-broadcast loads — ~8x fewer shared-memory wavefronts per MAC than one dot per
 // thread.  Base values and composition weights are sequential per individual (exact order).
-__device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int D, int S, double* sM, double* sZ,
-                              double* sS, double* sO, double* sFk, double* sDist, double* f) {
+__device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int D, int S, double* sMbase,
+                              double* sZ, double* sS, double* sObase, double* sFk, double* sDist, double* f,
+                              bool resident) {
   const int ncomp = pr.n_comp > 0 ? pr.n_comp : 1;
   const int RP = (D + 31) / 32 * 32;           // threads per row group
   const int NG = max(1, int(blockDim.x) / RP);  // individual groups
   for (int c = 0; c < ncomp; ++c) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-    for (int r = warp; r < D; r += nwarps)
-      for (int k = lane; k < D; k += 32) sM[r * S + k] = pr.rot[c][r * pr.ld + k];
-    for (int e = threadIdx.x; e < D; e += blockDim.x) sO[e] = pr.shift[c][e];
-    __syncthreads();
+    // resident: every component's M and o were staged once at kernel start
+    double* sM = resident ? sMbase + size_t(c) * D * S : sMbase;
+    double* sO = resident ? sObase + size_t(c) * D : sObase;
+    if (!resident) {
+      for (int r = warp; r < D; r += nwarps)
+        for (int k = lane; k < D; k += 32) sM[r * S + k] = pr.rot[c][r * pr.ld + k];
+      for (int e = threadIdx.x; e < D; e += blockDim.x) sO[e] = pr.shift[c][e];
+      __syncthreads();
+    }
     for (int i = warp; i < P; i += nwarps)
       for (int k = lane; k < D; k += 32) sS[i * D + k] = __dsub_rn(X[i * D + k], sO[k]);
     __syncthreads();
@@ -198,25 +206,37 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
   const int half = (P + 1) / 2;
   const int p0 = a.split == 2 ? rank * half : 0;
   const int p1 = a.split == 2 ? min(P, p0 + half) : P;
+  const int R = p1 - p0 > 0 ? (a.split == 2 ? half : P) : 1;  // rows this CTA evaluates
+  const int NM = a.resident ? a.n_mat : 1;     // rotation / shift slots
   double* sPop = sm;                           // P x D
   double* sTrial = sPop + P * D;               // P x D
-  double* sM = sTrial + P * D;                 // D x S
-  double* sZ = sM + D * S;                     // P x D
-  double* sS = sZ + P * D;                     // P x D  (x - o of the current component)
-  double* sO = sS + P * D;                     // D
-  double* sFit = sO + D;                       // P
+  double* sM = sTrial + P * D;                 // NM x D x S
+  double* sZ = sM + size_t(NM) * D * S;        // R x D
+  double* sS = sZ + R * D;                     // R x D  (x - o of the current component)
+  double* sO = sS + R * D;                     // NM x D
+  double* sFit = sO + NM * D;                  // P
   double* sTfit2 = sFit + P;                   // 2 x P (generation parity)
-  double* sFk = sTfit2 + 2 * P;                // P x 4
-  double* sDist = sFk + P * kRunsMaxComp;      // P x 4
-  int* sIdx = reinterpret_cast<int*>(sDist + P * kRunsMaxComp);  // P x 4 (a, b, c, word offset)
+  double* sFk = sTfit2 + 2 * P;                // R x 4
+  double* sDist = sFk + R * kRunsMaxComp;      // R x 4
+  int* sIdx = reinterpret_cast<int*>(sDist + R * kRunsMaxComp);  // P x 4 (a, b, c, word offset)
   const run_problem pr = a.probs[run];
+  if (a.resident) {  // stage every component's rotation and shift once for all generations
+    const int nc = pr.n_comp > 0 ? pr.n_comp : 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    for (int c = 0; c < nc; ++c) {
+      for (int r = warp; r < D; r += nwarps)
+        for (int k = lane; k < D; k += 32) sM[(size_t(c) * D + r) * S + k] = pr.rot[c][r * pr.ld + k];
+      for (int e = threadIdx.x; e < D; e += blockDim.x) sO[c * D + e] = pr.shift[c][e];
+    }
+    __syncthreads();
+  }
   const uint64_t key = a.keys[run];
   double* gpop = a.pop + size_t(run) * P * D;
   double* gfit = a.fit + size_t(run) * P;
   word_source src{RNG_PHILOX, key, nullptr, 0};
   // evaluate rows [p0, p1) of X into f, then (split) publish them into the peer's f
   auto evaluate = [&](const double* X, double* f) {
-    runs_evaluate(pr, X + size_t(p0) * D, p1 - p0, D, S, sM, sZ, sS, sO, sFk, sDist, f + p0);
+    runs_evaluate(pr, X + size_t(p0) * D, p1 - p0, D, S, sM, sZ, sS, sO, sFk, sDist, f + p0, a.resident != 0);
     if (a.split == 2) {
       cg::cluster_group cl = cg::this_cluster();
       double* peer = cl.map_shared_rank(f, rank ^ 1);
@@ -306,9 +326,11 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
   if (a.split == 2) cg::this_cluster().sync();  // no CTA leaves while its peer may still write into it
 }
 
-size_t runs_smem(int P, int D) {
+size_t runs_smem(int P, int D, int split = 1, int n_mat = 1) {
   const int S = (D % 2 == 1) ? D : D + 1;
-  return sizeof(double) * (size_t(4) * P * D + size_t(D) * S + D + 3 * P + 2 * P * kRunsMaxComp) +
+  const size_t R = split == 2 ? size_t((P + 1) / 2) : size_t(P);
+  return sizeof(double) * (size_t(2) * P * D + size_t(n_mat) * D * S + 2 * R * D + size_t(n_mat) * D + 3 * P +
+                           2 * R * kRunsMaxComp) +
          sizeof(int) * 4 * P + 64;
 }
 
@@ -353,7 +375,6 @@ extern "C" int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int 
     require(n_runs >= 1 && dim >= 1 && dim < 65536 && generations >= 0, "de_runs: bad sizes");
     const std::string why = runs_kernel_unsupported(dtype, cfg, pop_size, dim, problems, n_runs);
     if (!why.empty()) throw config_error(why);
-    const size_t smem = runs_smem(pop_size, dim);
     std::vector<run_problem> rp(n_runs);
     for (int r = 0; r < n_runs; ++r) {
       const device_problem& p = problems[r]->p;
@@ -418,13 +439,21 @@ extern "C" int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int 
       a.rec_on = 1;
       a.rec = rec_view<double>{static_cast<double*>(grid), static_cast<double*>(running), next, fes, nck, itv};
     }
-    EVB_CUDA(cudaFuncSetAttribute(de_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     // one run per SM leaves SMs idle when there are fewer runs than SMs: then a 2-CTA cluster
     // shares each run's evaluations (EVB_RUNS_SPLIT=1|2 overrides)
     int sms = 0;
     EVB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     static const char* split_env = std::getenv("EVB_RUNS_SPLIT");
     a.split = split_env ? (std::atoi(split_env) == 2 ? 2 : 1) : (2 * n_runs <= sms ? 2 : 1);
+    // keep every component's rotation resident when it fits (no per-generation reload);
+    // EVB_RUNS_RESIDENT=0 forces the reload path
+    a.n_mat = 1;
+    for (const run_problem& q : rp) a.n_mat = std::max(a.n_mat, std::max(1, q.n_comp));
+    static const char* res_env = std::getenv("EVB_RUNS_RESIDENT");
+    a.resident = (!res_env || std::atoi(res_env) != 0) && runs_smem(pop_size, dim, a.split, a.n_mat) <= 227 * 1024;
+    const size_t smem = runs_smem(pop_size, dim, a.split, a.resident ? a.n_mat : 1);
+    require(smem <= 227 * 1024, "de_runs: run state does not fit in shared memory");
+    EVB_CUDA(cudaFuncSetAttribute(de_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     cudaError_t err;
     if (a.split == 2) {
       cudaLaunchConfig_t lc{};
