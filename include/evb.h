@@ -337,6 +337,27 @@ EVB_API int evb_pso_init_uniform(evb_pso s, void* A, int64_t lda, double lo, dou
                                  void* stream);
 EVB_API int evb_pso_get(evb_pso s, void* pbest_host, void* pbest_fit_host, int* nb_host, uint32_t* generation);
 EVB_API int evb_pso_set_pbest(evb_pso s, const void* pbest_host, const void* pbest_fit_host);
+/* pso_engine::optimize (pso/engine.hpp:84-105) with the synchronous generation: init_population,
+ * evaluate, zero velocities, prepare, generations while fes < max_fes; the best personal best. */
+EVB_API int evb_pso_optimize(evb_pso s, evb_problem objective, evb_scratch sc, void* X, int64_t ldx, void* V,
+                             int64_t ldv, void* fitness, double lb, double ub, int64_t max_fes, evb_rng rng,
+                             int* best_index, double* best_fitness, int* generations, void* stream);
+/* Report every evaluation (init inside optimize, each generation's particles in i order) to
+ * recorder run `run`; r = NULL detaches. */
+EVB_API int evb_pso_attach_recorder(evb_pso s, evb_recorder r, int run);
+
+/* evo_bench for the swarm presets (presets.hpp make_algorithm "pso" / "spso2011" / "cso"), same
+ * task layout, Philox keys, recorder slots and best_host as evb_evo_bench_de; each task runs
+ * evb_pso_optimize (synchronous generation) or evb_cso_optimize (the reference's
+ * generation exactly, pop_size even). */
+EVB_API int evb_evo_bench_pso(int dtype, const evb_pso_config* cfg, int pop_size, int dim,
+                              const evb_problem* problems, int problem_count, int instance_count, int runs,
+                              int64_t max_fes, uint64_t master_seed, double lb, double ub, evb_recorder rec,
+                              double* best_host, void* stream);
+EVB_API int evb_evo_bench_cso(int dtype, double phi, int pop_size, int dim, const evb_problem* problems,
+                              int problem_count, int instance_count, int runs, int64_t max_fes,
+                              uint64_t master_seed, double lb, double ub, evb_recorder rec, double* best_host,
+                              void* stream);
 
 /* Kernel launches this library has issued on the calling thread (monotonic counter; used by
  * bench.py to report gpu_launches inside its timed region). */

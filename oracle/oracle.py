@@ -636,3 +636,28 @@ class RefCSO:
             REF().ref_cso_destroy(self.dt, self.h)
         except Exception:
             pass
+
+
+register_ref({"ref_evo_bench_cso": (i64, [c_double, c_int, c_int, c_int, vp, c_int, c_int, ctypes.c_longlong,
+                                          ctypes.c_longlong, vp, vp, vp, c_double, vp, vp, c_double, c_double, c_int,
+                                          vp, i64, vp])})
+
+
+def ref_evo_bench_cso(phi, P, D, problem_ids, instances, runs, max_fes, interval, kinds, shifts, rots, bias,
+                      task_words, lb=-100.0, ub=100.0, threads=0):
+    """experiment::evo_bench with the `cso` preset, the reference recorder attached; task t replays
+    task_words[t].  Returns (csv, best per task)."""
+    ids = np.ascontiguousarray(problem_ids, np.int32)
+    k = np.ascontiguousarray(kinds, np.int32)
+    sh = np.ascontiguousarray(shifts, np.float64)
+    ro = np.ascontiguousarray(rots, np.float64)
+    words = np.ascontiguousarray(np.concatenate(task_words), np.uint64)
+    off = np.zeros(len(task_words) + 1, np.int64)
+    off[1:] = np.cumsum([len(w) for w in task_words])
+    best = np.zeros(len(task_words))
+    args = (phi, P, D, len(ids), ptr(ids), instances, runs, max_fes, interval, ptr(k), ptr(sh), ptr(ro), bias,
+            ptr(words), ptr(off), lb, ub, threads)
+    n = REF().ref_evo_bench_cso(*args, None, 0, ptr(best))
+    buf = ctypes.create_string_buffer(int(n) + 1)
+    REF().ref_evo_bench_cso(*args, buf, int(n), ptr(best))
+    return buf.raw[:n].decode(), best

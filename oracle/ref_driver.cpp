@@ -772,3 +772,35 @@ REF_API void ref_cso_destroy(int dtype, void* h) {
   if (dtype == 1) delete static_cast<ref_cso_run<double>*>(h);
   else delete static_cast<ref_cso_run<float>*>(h);
 }
+
+// evo_bench with the `cso` preset (presets.hpp: cso_optimizer{phi}.optimize(h, ...)), words
+// substituted per task exactly like ref_evo_bench_de
+REF_API int64_t ref_evo_bench_cso(double phi, int P, int D, int n_problems, const int* problem_ids, int instances,
+                                  int runs, long long max_fes, long long interval, const int* kinds,
+                                  const double* shifts, const double* rots, double bias, const uint64_t* words,
+                                  const int64_t* off, double lb, double ub, int threads, char* csv, int64_t cap,
+                                  double* best) {
+  std::vector<problem_instance<double>> inst;
+  for (int q = 0; q < n_problems * instances; ++q)
+    inst.push_back(make_base<double>(kinds[q], D, shifts + size_t(q) * D, rots + size_t(q) * D * D, bias));
+  problems::suite<double> su("gpu", D, std::vector<int>(problem_ids, problem_ids + n_problems), instances, 0,
+                             std::move(inst));
+  experiment::best_so_far_record<double> rec(su, runs, max_fes, interval);
+  experiment::bench_options opt;
+  opt.independent_runs = runs;
+  opt.max_fes = max_fes;
+  opt.threads = threads;
+  opt.parallel = threads != 1;
+  auto alg = [&](experiment::run_handle<double>& h) {
+    const auto& k = h.key();
+    const int64_t t = (int64_t(k.problem_ordinal) * instances + k.instance_ordinal) * runs + k.run_index;
+    rng_stream rng = rng_stream::scripted(std::vector<uint64_t>(words + off[t], words + off[t + 1]));
+    pso::cso_optimizer<double> engine{phi};
+    const auto b = engine.optimize(h, lb, ub, P, D, max_fes, rng);
+    best[t] = b.fitness;
+  };
+  experiment::evo_bench<double>(alg, su, rec, opt);
+  const std::string s = rec.to_csv();
+  if (csv) std::memcpy(csv, s.data(), std::min<size_t>(size_t(cap), s.size()));
+  return int64_t(s.size());
+}

@@ -334,12 +334,18 @@ __device__ __forceinline__ T repair_gene(int repair, T v, T xij, T lb, T ub) {
 }
 
 template <typename T>
-__global__ void de_trial_kernel(const de_dev<T> d) {
+__device__ __forceinline__ T donor_gene(int mutation, T xij, T xaj, T xbj, T xcj, T Fi) {
   using F_ = fop<T>;
+  if (mutation == EVB_MUT_TTPB1)  // x_i + F(x_pb - x_i) + F(x_r1 - x~_r2), de/strategy.hpp:159
+    return F_::add(F_::add(xij, F_::mul(Fi, F_::sub(xaj, xij))), F_::mul(Fi, F_::sub(xbj, xcj)));
+  return F_::add(xaj, F_::mul(Fi, F_::sub(xbj, xcj)));  // x_a + F(x_b - x_c), de/strategy.hpp:93 / :117
+}
+
+template <typename T, int CX>
+__global__ void de_trial_kernel(const de_dev<T> d) {
   const int i = blockIdx.x;
   const int D = d.D;
   const T Fi = d.F[i];
-  const double cr = double(d.CR[i]);
   const int jr = d.jrand[i];
   const int a = d.idx[4 * i + 0], b = d.idx[4 * i + 1], c = d.idx[4 * i + 2];
   const T* xi = d.pop + size_t(i) * d.ldp;
@@ -350,50 +356,67 @@ __global__ void de_trial_kernel(const de_dev<T> d) {
   T* out = d.trial + size_t(i) * d.ldt;
   const uint64_t ctr_hi = (uint64_t(*d.gen_ptr) << 32) | uint32_t(i);
   const T lb = d.lb, ub = d.ub;
-  const int repair = d.cfg.repair;
-  auto gene = [&](int j, bool take) {
-    T v;
-    if (take) {
-      if (d.cfg.mutation == EVB_MUT_TTPB1)  // x_i + F(x_pb - x_i) + F(x_r1 - x~_r2), de/strategy.hpp:159
-        v = F_::add(F_::add(xi[j], F_::mul(Fi, F_::sub(xa[j], xi[j]))), F_::mul(Fi, F_::sub(xb[j], xc[j])));
-      else  // x_a + F(x_b - x_c), de/strategy.hpp:93 / :117
-        v = F_::add(xa[j], F_::mul(Fi, F_::sub(xb[j], xc[j])));
-    } else {
-      v = xi[j];
-    }
-    out[j] = repair_gene<T>(repair, v, xi[j], lb, ub);
-  };
-  if (d.cfg.crossover == EVB_CX_BINOMIAL) {
+  const int repair = d.cfg.repair, mutation = d.cfg.mutation;
+  if (CX == EVB_CX_BINOMIAL) {
+    const double cr = double(d.CR[i]);
     const int64_t s0 = d.woff[i];  // stream index of gene 0's uniform
     // Philox blocks covering stream words [s0, s0 + D)
     const int64_t blk0 = s0 >> 1;
     const int64_t nblk = ((s0 + D + 1) >> 1) - blk0;
     for (int64_t q = threadIdx.x; q < nblk; q += blockDim.x) {
-      uint64_t w[2];
+      uint64_t w0, w1;
       const int64_t n0 = (blk0 + q) * 2;
       if (d.src.mode == RNG_PHILOX) {
-        philox_pair(d.src.key, ctr_hi, uint64_t(blk0 + q), w[0], w[1]);
+        philox_pair(d.src.key, ctr_hi, uint64_t(blk0 + q), w0, w1);
       } else {
         // WORDS: s0 is the absolute list position of gene 0
-        w[0] = (n0 >= s0 && n0 < s0 + D && n0 < d.src.n_words) ? d.src.words[n0] : 0;
-        w[1] = (n0 + 1 >= s0 && n0 + 1 < s0 + D && n0 + 1 < d.src.n_words) ? d.src.words[n0 + 1] : 0;
+        w0 = (n0 >= s0 && n0 < s0 + D && n0 < d.src.n_words) ? d.src.words[n0] : 0;
+        w1 = (n0 + 1 >= s0 && n0 + 1 < s0 + D && n0 + 1 < d.src.n_words) ? d.src.words[n0 + 1] : 0;
       }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int64_t j64 = n0 + h - s0;
         if (j64 < 0 || j64 >= D) continue;
         const int j = int(j64);
-        gene(j, u01_of(w[h]) < cr || j == jr);
+        // the target row is read only where it is used (non-donor genes, ttpb/1, midpoint repair)
+        T v;
+        if (u01_of(h ? w1 : w0) < cr || j == jr) {
+          if (mutation == EVB_MUT_TTPB1) v = donor_gene<T>(mutation, xi[j], xa[j], xb[j], xc[j], Fi);
+          else v = donor_gene<T>(mutation, T(0), xa[j], xb[j], xc[j], Fi);
+        } else {
+          v = xi[j];
+        }
+        if (repair == EVB_REP_CLIP) {
+          if (v < lb) v = lb;
+          if (v > ub) v = ub;
+        } else if (repair != EVB_REP_REINITIALIZE) {
+          if (v < lb || v > ub) v = repair_gene<T>(repair, v, xi[j], lb, ub);
+        }
+        out[j] = v;
       }
     }
-  } else {  // exponential, de/strategy.hpp:203-214
+  } else {  // exponential, de/strategy.hpp:203-214: donor genes [start, start + L) mod D
     const int L = d.xlen[i];
-    for (int j = threadIdx.x; j < D; j += blockDim.x) gene(j, ((j - jr + D) % D) < L);
+    for (int j = threadIdx.x; j < D; j += blockDim.x) {
+      const T xij = xi[j];
+      const bool take = ((j - jr + D) % D) < L;
+      const T v = take ? donor_gene<T>(mutation, xij, xa[j], xb[j], xc[j], Fi) : xij;
+      out[j] = repair_gene<T>(repair, v, xij, lb, ub);
+    }
   }
-  if (repair != EVB_REP_REINITIALIZE) return;
-  // reinitialize repair (de/strategy.hpp:285-289): g = T(uniform(lb, ub)) per violating gene, in j order
+}
+
+// reinitialize repair (de/strategy.hpp:285-289), a second pass over the trial rows: every gene
+// still outside [lb, ub] takes T(uniform(lb, ub)); the words follow the crossover words in j
+// order, so each violating gene's word is its rank among the violations (block prefix count).
+template <typename T>
+__global__ void de_reinit_kernel(const de_dev<T> d) {
+  const int i = blockIdx.x;
+  const int D = d.D;
+  T* out = d.trial + size_t(i) * d.ldt;
+  const uint64_t ctr_hi = (uint64_t(*d.gen_ptr) << 32) | uint32_t(i);
+  const T lb = d.lb, ub = d.ub;
   __shared__ int warp_tot[32];
-  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
   const int64_t r0 = d.rword[i];
   int running = 0;
@@ -412,9 +435,9 @@ __global__ void de_trial_kernel(const de_dev<T> d) {
       const int64_t s = r0 + running + before + __popc(m & ((1u << lane) - 1u));
       uint64_t word;
       if (d.src.mode == RNG_PHILOX) {
-        uint64_t w2[2];
-        philox_pair(d.src.key, ctr_hi, uint64_t(s >> 1), w2[0], w2[1]);
-        word = w2[s & 1];
+        uint64_t wa, wb;
+        philox_pair(d.src.key, ctr_hi, uint64_t(s >> 1), wa, wb);
+        word = (s & 1) ? wb : wa;
       } else {
         word = s < d.src.n_words ? d.src.words[s] : 0;
         if (s >= d.src.n_words) *d.overflow = 1;
@@ -667,8 +690,13 @@ void generation_t(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, vo
   count_launch();
   {
     const int th = std::min(256, int(round_up((e->D + 2) / 2 + 1, 32)));
-    de_trial_kernel<T><<<e->P, th, 0, st>>>(d);
+    if (e->cfg.crossover == EVB_CX_EXPONENTIAL) de_trial_kernel<T, EVB_CX_EXPONENTIAL><<<e->P, th, 0, st>>>(d);
+    else de_trial_kernel<T, EVB_CX_BINOMIAL><<<e->P, th, 0, st>>>(d);
     count_launch();
+    if (e->cfg.repair == EVB_REP_REINITIALIZE) {
+      de_reinit_kernel<T><<<e->P, std::max(32, std::min(256, int(round_up(e->D, 32)))), 0, st>>>(d);
+      count_launch();
+    }
   }
   EVB_CUDA(cudaGetLastError());
   // evaluate the trials with the scalar path's semantics (problem.evaluate via individual::evaluate)

@@ -53,6 +53,69 @@ void best_of(const std::vector<uint8_t>& fit, int P, int tasks, double* best) {
   }
 }
 
+// validation shared by the suite entry points (runner.hpp:106-108, presets.hpp:133)
+int suite_tasks(int dtype, int pop_size, int dim, const evb_problem* problems, int problem_count, int instance_count,
+                int runs, int64_t max_fes, evb_recorder rec) {
+  require(problems != nullptr, "evo_bench: null argument");
+  require(runs >= 1, "evo_bench: independent_runs must be at least 1");
+  require(max_fes >= 1, "evo_bench: max_fes must be positive");
+  require(pop_size >= 4, "algorithm: pop size must be at least 4");
+  require(problem_count >= 1 && instance_count >= 1, "evo_bench: empty suite");
+  require(dtype == EVB_F32 || dtype == EVB_F64, "evo_bench: dtype must be EVB_F32 or EVB_F64");
+  const int64_t total64 = int64_t(problem_count) * instance_count * runs;
+  require(total64 <= (int64_t(1) << 24), "evo_bench: too many tasks");
+  const int tasks = int(total64);
+  if (rec)
+    require(recorder_runs(rec) >= tasks && recorder_dtype(rec) == dtype, "evo_bench: recorder runs / dtype mismatch");
+  for (int q = 0; q < problem_count * instance_count; ++q) {
+    require(problems[q] != nullptr, "evo_bench: null problem");
+    if (problems[q]->p.dim != dim) throw invalid_argument("evo_bench: problem dimension mismatch");
+    require(problems[q]->p.dtype == dtype, "evo_bench: problem dtype mismatch");
+  }
+  return tasks;
+}
+
+// Task loop for the swarm optimizers: per task a fresh Philox stream, X / V / fitness buffers
+// reused, run_task(t, problem, rng, X, V, fit, &best) runs one optimize().
+template <typename Run>
+void swarm_tasks(int dtype, int pop_size, int dim, const evb_problem* problems, int runs, int tasks,
+                 uint64_t master_seed, evb_recorder rec, double* best_host, cudaStream_t st, Run&& run_task) {
+  const size_t es = dtype == EVB_F64 ? 8 : 4;
+  void* X = nullptr;
+  void* V = nullptr;
+  void* fit = nullptr;
+  try {
+    EVB_CUDA(cudaMalloc(&X, es * size_t(pop_size) * dim));
+    EVB_CUDA(cudaMalloc(&V, es * size_t(pop_size) * dim));
+    EVB_CUDA(cudaMalloc(&fit, es * size_t(pop_size)));
+    for (int t = 0; t < tasks; ++t) {
+      evb_rng r = nullptr;
+      check_status(evb_rng_create_philox(task_key(master_seed, uint64_t(t)), &r));
+      double best = 0.0;
+      int rc = EVB_OK;
+      try {
+        rc = run_task(t, problems[t / runs], r, X, V, fit, &best);
+      } catch (...) {
+        evb_rng_destroy(r);
+        throw;
+      }
+      evb_rng_destroy(r);
+      check_status(rc);
+      if (best_host) best_host[t] = best;
+    }
+    if (rec) check_status(evb_recorder_finish(rec, 0, tasks, st));
+    EVB_CUDA(cudaStreamSynchronize(st));
+  } catch (...) {
+    cudaFree(X);
+    cudaFree(V);
+    cudaFree(fit);
+    throw;
+  }
+  cudaFree(X);
+  cudaFree(V);
+  cudaFree(fit);
+}
+
 }  // namespace
 }  // namespace evb
 
@@ -67,21 +130,8 @@ int evb_evo_bench_de(int dtype, const evb_de_config* cfg, int pop_size, int dim,
                      double lb, double ub, evb_recorder rec, double* best_host, int flags, int* path_used,
                      void* stream) {
   return guarded([&] {
-    require(cfg && problems, "evo_bench: null argument");
-    require(runs >= 1, "evo_bench: independent_runs must be at least 1");     // runner.hpp:106-107
-    require(max_fes >= 1, "evo_bench: max_fes must be positive");             // runner.hpp:108
-    require(pop_size >= 4, "algorithm: pop size must be at least 4");         // presets.hpp:133
-    require(problem_count >= 1 && instance_count >= 1, "evo_bench: empty suite");
-    require(dtype == EVB_F32 || dtype == EVB_F64, "evo_bench: dtype must be EVB_F32 or EVB_F64");
-    const int64_t total64 = int64_t(problem_count) * instance_count * runs;
-    require(total64 <= (int64_t(1) << 24), "evo_bench: too many tasks");
-    const int tasks = int(total64);
-    if (rec) require(recorder_runs(rec) >= tasks && recorder_dtype(rec) == dtype, "evo_bench: recorder runs / dtype mismatch");
-    for (int q = 0; q < problem_count * instance_count; ++q) {
-      require(problems[q] != nullptr, "evo_bench: null problem");
-      if (problems[q]->p.dim != dim) throw invalid_argument("evo_bench: problem dimension mismatch");
-      require(problems[q]->p.dtype == dtype, "evo_bench: problem dtype mismatch");
-    }
+    require(cfg != nullptr, "evo_bench: null argument");
+    const int tasks = suite_tasks(dtype, pop_size, dim, problems, problem_count, instance_count, runs, max_fes, rec);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int P = pop_size, D = dim;
     // optimize(): P initial evaluations, then one generation (P trials) while fes < max_fes
@@ -156,6 +206,60 @@ int evb_evo_bench_de(int dtype, const evb_de_config* cfg, int pop_size, int dim,
       else best_of<float>(fit_host, P, tasks, best_host);
     }
     if (path_used) *path_used = k8 ? 1 : 2;
+  });
+}
+
+int evb_evo_bench_pso(int dtype, const evb_pso_config* cfg, int pop_size, int dim, const evb_problem* problems,
+                      int problem_count, int instance_count, int runs, int64_t max_fes, uint64_t master_seed,
+                      double lb, double ub, evb_recorder rec, double* best_host, void* stream) {
+  return guarded([&] {
+    require(cfg != nullptr, "evo_bench: null argument");
+    const int tasks = suite_tasks(dtype, pop_size, dim, problems, problem_count, instance_count, runs, max_fes, rec);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    evb_pso eng = nullptr;
+    check_status(evb_pso_create(dtype, cfg, pop_size, dim, &eng));
+    try {
+      swarm_tasks(dtype, pop_size, dim, problems, runs, tasks, master_seed, rec, best_host, st,
+                  [&](int t, evb_problem p, evb_rng r, void* X, void* V, void* fit, double* best) {
+                    int rc = rec ? evb_pso_attach_recorder(eng, rec, t) : EVB_OK;
+                    int bi = 0, g = 0;
+                    if (rc == EVB_OK)
+                      rc = evb_pso_optimize(eng, p, nullptr, X, dim, V, dim, fit, lb, ub, max_fes, r, &bi, best, &g,
+                                            stream);
+                    return rc;
+                  });
+    } catch (...) {
+      evb_pso_destroy(eng);
+      throw;
+    }
+    evb_pso_destroy(eng);
+  });
+}
+
+int evb_evo_bench_cso(int dtype, double phi, int pop_size, int dim, const evb_problem* problems, int problem_count,
+                      int instance_count, int runs, int64_t max_fes, uint64_t master_seed, double lb, double ub,
+                      evb_recorder rec, double* best_host, void* stream) {
+  return guarded([&] {
+    const int tasks = suite_tasks(dtype, pop_size, dim, problems, problem_count, instance_count, runs, max_fes, rec);
+    require(pop_size % 2 == 0, "algorithm cso: pop size must be even");  // presets.hpp:181
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    evb_cso eng = nullptr;
+    check_status(evb_cso_create(dtype, phi, pop_size, dim, &eng));
+    try {
+      swarm_tasks(dtype, pop_size, dim, problems, runs, tasks, master_seed, rec, best_host, st,
+                  [&](int t, evb_problem p, evb_rng r, void* X, void* V, void* fit, double* best) {
+                    int rc = rec ? evb_cso_attach_recorder(eng, rec, t) : EVB_OK;
+                    int bi = 0, g = 0;
+                    if (rc == EVB_OK)
+                      rc = evb_cso_optimize(eng, p, nullptr, X, dim, V, dim, fit, lb, ub, max_fes, r, &bi, best, &g,
+                                            stream);
+                    return rc;
+                  });
+    } catch (...) {
+      evb_cso_destroy(eng);
+      throw;
+    }
+    evb_cso_destroy(eng);
   });
 }
 

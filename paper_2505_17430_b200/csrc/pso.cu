@@ -38,6 +38,8 @@ struct evb_pso_s {
   int prepared = 0;
   uint32_t last_gen = 0;
   evb_scratch_s* eval_scratch = nullptr;
+  evb_recorder_s* rec = nullptr;  // attached best-so-far recorder (may be null)
+  int rec_run = 0;
 };
 
 namespace evb {
@@ -349,6 +351,7 @@ void generation_t(evb_pso_s* s, const device_problem* prob, evb_scratch_s* sc, v
   rq.stream = st;
   rq.scalar_trig = true;
   eval_dispatch(rq);
+  if (s->rec) recorder_observe(s->rec, s->rec_run, s->fit_new, s->P, st);  // particles in i (FE) order
   pso_pbest_kernel<T><<<s->P, std::min(256, int(round_up(s->D, 32))), 0, st>>>(
       static_cast<const T*>(X), ldx, static_cast<const T*>(s->fit_new), static_cast<T*>(fit),
       static_cast<T*>(s->pbest), s->ldb, static_cast<T*>(s->pbest_fit), s->D, r->d_gen);
@@ -465,6 +468,82 @@ int evb_pso_generation(evb_pso s, evb_problem objective, evb_scratch sc, void* X
     evb_scratch_s* scr = sc ? sc : s->eval_scratch;
     if (s->dtype == EVB_F64) generation_t<double>(s, &objective->p, scr, X, ldx, V, ldv, fitness, lb, ub, rng, st);
     else generation_t<float>(s, &objective->p, scr, X, ldx, V, ldv, fitness, lb, ub, rng, st);
+  });
+}
+
+int evb_pso_attach_recorder(evb_pso s, evb_recorder rec, int run) {
+  return guarded([&] {
+    require(s != nullptr, "pso: null handle");
+    if (rec) {
+      require(recorder_dtype(rec) == s->dtype, "pso_attach_recorder: dtype mismatch");
+      require(run >= 0 && run < recorder_runs(rec), "pso_attach_recorder: run out of range");
+    }
+    s->rec = rec;
+    s->rec_run = run;
+  });
+}
+
+// pso_engine::optimize (pso/engine.hpp:84-105) with the synchronous generation: init_population,
+// evaluate, zero velocities, prepare, generations while fes < max_fes; best personal best
+// (lowest fitness, ties to the lowest index).
+int evb_pso_optimize(evb_pso s, evb_problem objective, evb_scratch sc, void* X, int64_t ldx, void* V, int64_t ldv,
+                     void* fitness, double lb, double ub, int64_t max_fes, evb_rng rng, int* best_index,
+                     double* best_fitness, int* generations, void* stream) {
+  return guarded([&] {
+    require(s && objective && X && V && fitness && rng, "pso_optimize: null argument");
+    require(max_fes > 0, "evolution_state: max_fes must be positive");
+    if (objective->p.dim != s->D) throw invalid_argument("pso_optimize: problem dimension mismatch");
+    if (objective->p.dtype != s->dtype) throw config_error("pso_optimize: problem dtype differs from engine");
+    if (ldx < s->D || ldv < s->D) throw invalid_argument("pso_optimize: leading dimension < dim");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    evb_scratch_s* scr = sc ? sc : s->eval_scratch;
+    const size_t es = s->dtype == EVB_F64 ? 8 : 4;
+    population_init(s->dtype, s->P, s->D, X, ldx, lb, ub, rng, st);
+    eval_request rq{};
+    rq.prob = &objective->p;
+    rq.scratch = scr;
+    rq.X = X;
+    rq.n = s->P;
+    rq.ldx = ldx;
+    rq.out = fitness;
+    rq.ldo = s->P;
+    rq.n_out = 1;
+    rq.kinds[0] = objective->p.kind;
+    rq.biases[0] = objective->p.bias;
+    rq.stream = st;
+    rq.scalar_trig = true;
+    eval_dispatch(rq);
+    if (s->rec) recorder_observe(s->rec, s->rec_run, fitness, s->P, st);
+    EVB_CUDA(cudaMemset2DAsync(V, ldv * es, 0, s->D * es, s->P, st));
+    if (s->dtype == EVB_F64)
+      copy_rows_kernel<double><<<s->P, 128, 0, st>>>(static_cast<const double*>(X), ldx,
+                                                     static_cast<double*>(s->pbest), s->ldb, s->D);
+    else
+      copy_rows_kernel<float><<<s->P, 128, 0, st>>>(static_cast<const float*>(X), ldx, static_cast<float*>(s->pbest),
+                                                    s->ldb, s->D);
+    count_launch();
+    EVB_CUDA(cudaMemcpyAsync(s->pbest_fit, fitness, es * s->P, cudaMemcpyDeviceToDevice, st));
+    s->prepared = 1;
+    int64_t fes = s->P;
+    int gens = 0;
+    while (fes < max_fes) {
+      if (s->dtype == EVB_F64) generation_t<double>(s, &objective->p, scr, X, ldx, V, ldv, fitness, lb, ub, rng, st);
+      else generation_t<float>(s, &objective->p, scr, X, ldx, V, ldv, fitness, lb, ub, rng, st);
+      fes += s->P;
+      ++gens;
+    }
+    std::vector<uint8_t> f(es * s->P);
+    EVB_CUDA(cudaMemcpyAsync(f.data(), s->pbest_fit, es * s->P, cudaMemcpyDeviceToHost, st));
+    EVB_CUDA(cudaStreamSynchronize(st));
+    auto val = [&](int i) {
+      return s->dtype == EVB_F64 ? reinterpret_cast<double*>(f.data())[i] : double(reinterpret_cast<float*>(f.data())[i]);
+    };
+    int best = 0;
+    for (int i = 1; i < s->P; ++i)
+      if (val(i) < val(best)) best = i;
+    if (best_index) *best_index = best;
+    if (best_fitness) *best_fitness = val(best);
+    if (generations) *generations = gens;
   });
 }
 

@@ -75,6 +75,9 @@ def _sigs():
         "evb_pso_init_uniform": (c_int, [vp, vp, i64, c_double, c_double, vp, vp]),
         "evb_pso_get": (c_int, [vp, vp, vp, vp, P(u32)]),
         "evb_pso_set_pbest": (c_int, [vp, vp, vp]),
+        "evb_pso_optimize": (c_int, [vp, vp, vp, vp, i64, vp, i64, vp, c_double, c_double, i64, vp, P(c_int),
+                                     P(c_double), P(c_int), vp]),
+        "evb_pso_attach_recorder": (c_int, [vp, vp, c_int]),
     })
     _REG = True
 
@@ -113,6 +116,25 @@ class PSOEngine:
                                             ctypes.c_void_p(X.data_ptr()), X.stride(0), ctypes.c_void_p(V.data_ptr()),
                                             V.stride(0), ctypes.c_void_p(fitness.data_ptr()), lb, ub, rng.handle,
                                             _stream_ptr(stream)), "pso_generation")
+
+    def optimize(self, problem: ProblemInstance, X, V, fitness, lb: float, ub: float, max_fes: int, rng: Rng,
+                 scratch: EvalScratch | None = None, stream=None):
+        """pso_engine::optimize (pso/engine.hpp:84-105) with the synchronous generation."""
+        self._chk(X, V, fitness)
+        bi, bf, g = ctypes.c_int(), ctypes.c_double(), ctypes.c_int()
+        check(_lib.lib().evb_pso_optimize(self._h, problem.handle, scratch.handle if scratch else None,
+                                          ctypes.c_void_p(X.data_ptr()), X.stride(0), ctypes.c_void_p(V.data_ptr()),
+                                          V.stride(0), ctypes.c_void_p(fitness.data_ptr()), lb, ub, max_fes,
+                                          rng.handle, ctypes.byref(bi), ctypes.byref(bf), ctypes.byref(g),
+                                          _stream_ptr(stream)), "pso_optimize")
+        return {"best_index": bi.value, "best_fitness": bf.value, "generations": g.value}
+
+    def attach_recorder(self, recorder, run: int = 0) -> None:
+        from .recorder import _sigs as _rec_sigs
+        _rec_sigs()
+        check(_lib.lib().evb_pso_attach_recorder(self._h, recorder.handle if recorder is not None else None, run),
+              "pso_attach_recorder")
+        self._recorder = recorder
 
     def personal_bests(self):
         pb = np.zeros((self.pop_size, self.dim), self._np())

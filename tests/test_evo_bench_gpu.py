@@ -121,3 +121,46 @@ def test_engine_path_lshade(dev):
     assert np.all(fes >= max_fes) and np.all(fes < max_fes + P)
     assert np.all(fes != P * (max_fes // P))  # sizes shrank, so the count is not a multiple of P
     assert np.all(np.diff(grid, axis=1) <= 0)
+
+
+def test_evo_bench_cso_matches_reference(dev):
+    # the `cso` preset over a suite: GPU generations are the reference's generations, so with a
+    # transcendental-free objective the CSV must equal the reference harness's byte for byte
+    from paper_2505_17430_b200.cso import scripted_words_for_generation as cso_words
+    from paper_2505_17430_b200.experiment import evo_bench_cso
+    D, P, runs, seed, interval = 12, 20, 2, 5, 30
+    max_fes = P + 15 * (P // 2) + 3
+    kinds, ids, instances = [K.sphere, K.elliptic], [1, 2], 2
+    suite, flat = make_suite(D, kinds, instances)
+    tasks = len(kinds) * instances * runs
+    rec = BestSoFarRecorder(tasks, max_fes, interval)
+    res = evo_bench_cso(0.1, P, suite, runs, max_fes, master_seed=seed, recorder=rec)
+    gens = -(-(max_fes - P) // (P // 2))
+    words = []
+    for t in range(tasks):
+        key = task_key(seed, t)
+        words.append(np.concatenate([O.philox_words(key, 0xFFFFFFF0, 0, P * D)] +
+                                    [cso_words(key, g, P, D, philox=O.philox_words) for g in range(1, gens + 1)]))
+    ref_csv, ref_best = O.ref_evo_bench_cso(0.1, P, D, ids, instances, runs, max_fes, interval,
+                                            [k for k, _, _ in flat], np.stack([o for _, o, _ in flat]),
+                                            np.stack([m for _, _, m in flat]), 0.0, words)
+    assert rec.to_csv("gpu", D, ids, instances, runs) == ref_csv
+    assert np.array_equal(res["best"], ref_best)
+
+
+def test_evo_bench_pso_presets(dev):
+    # "pso" (gbest + standard) and "spso2011" (ring + spherical) over a suite: synchronous
+    # generations; the harness contract — FE counts, monotone checkpoints, best ==
+    # the final checkpoint when max_fes is a generation boundary — holds
+    from paper_2505_17430_b200.experiment import evo_bench_pso
+    from paper_2505_17430_b200.pso import PSOConfig, preset_spso2011
+    D, P, runs = 10, 20, 2
+    max_fes = P * 12
+    suite, _ = make_suite(D, [K.rastrigin, K.sphere], 2)
+    for cfg in (PSOConfig("gbest", "standard"), preset_spso2011()):
+        rec = BestSoFarRecorder(8, max_fes, P)
+        res = evo_bench_pso(cfg, P, suite, runs, max_fes, master_seed=9, recorder=rec)
+        grid, fes = rec.grid()
+        assert np.all(fes == max_fes)
+        assert np.all(np.diff(grid, axis=1) <= 0)
+        assert np.array_equal(grid[:, -1], res["best"])

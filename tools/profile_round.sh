@@ -13,8 +13,10 @@ python tools/prof_eval.py f32 5 4 > $OUT/eval32_plain.log 2>&1 &&
 ncu --set full --clock-control none --import-source on -k regex:eval_f32 -s 2 -c 1 -o $OUT/eval_f32 \
     python tools/prof_eval.py f32 5 4 > $OUT/eval32_ncu.log 2>&1
 python bench_configs.py --only hbm > $OUT/hbm_plain.json 2>&1 &&
-ncu --set full --clock-control none -k regex:"de_trial|pso_update|de_select" -c 6 -o $OUT/updates \
+ncu --set full --clock-control none -k regex:"de_trial|de_select" -s 3 -c 3 -o $OUT/updates \
     python bench_configs.py --only hbm > $OUT/updates_ncu.log 2>&1
+ncu --set full --clock-control none -k regex:pso_update -s 1 -c 1 -o $OUT/pso_update \
+    python bench_configs.py --only hbm > $OUT/pso_ncu.log 2>&1
 python tools/prof_runs.py 50 > $OUT/runs_plain.log 2>&1 &&
 ncu --set full --clock-control none --import-source on -k regex:de_runs -s 1 -c 1 -o $OUT/runs \
     python tools/prof_runs.py 50 > $OUT/runs_ncu.log 2>&1

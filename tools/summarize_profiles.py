@@ -64,7 +64,8 @@ def main():
                "kernels": {}}
     traffic = {}
     for name, rep in (("eval_f64_dmma", "eval_f64.ncu-rep"), ("eval_f32_ffma", "eval_f32.ncu-rep"),
-                      ("de_runs", "runs.ncu-rep"), ("updates", "updates.ncu-rep")):
+                      ("de_runs", "runs.ncu-rep"), ("updates", "updates.ncu-rep"),
+                      ("updates", "pso_update.ncu-rep")):
         p = SRC / rep
         if not p.exists():
             continue
