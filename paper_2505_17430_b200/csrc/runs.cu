@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <vector>
@@ -31,6 +32,23 @@ namespace evb {
 namespace {
 
 constexpr int kRunsMaxComp = 4;
+
+// EVB_RUNS_PROFILE=1: CTA 0's thread 0 accumulates clock64() per phase (the phases end at block
+// barriers, so its clock marks the phase boundary) — a tuning aid, off by default.
+struct phase_clock {
+  unsigned long long* acc;  // null: off
+  long long last;
+  __device__ __forceinline__ void start() {
+    if (acc && threadIdx.x == 0) last = clock64();
+  }
+  __device__ __forceinline__ void mark(int k) {
+    if (acc && threadIdx.x == 0) {
+      const long long t = clock64();
+      acc[k] += (unsigned long long)(t - last);
+      last = t;
+    }
+  }
+};
 
 struct run_problem {
   const double* shift[kRunsMaxComp];  // per component (base problem: component 0)
@@ -55,6 +73,7 @@ struct runs_args {
   int init;
   int rec_on;
   rec_view<double> rec;  // best-so-far recorder, run r -> recorder run r
+  unsigned long long* prof;  // EVB_RUNS_PROFILE: per-phase clocks of CTA 0 (else null)
   int split;             // CTAs per run (1, or a 2-CTA cluster that splits every evaluation)
   int resident;          // all rotations / shifts of a run staged in shared memory once
   int n_mat;             // max components over the runs (resident slots)
@@ -77,12 +96,12 @@ __device__ __forceinline__ double clip_or_mid(double v, double target, double lb
 // lane r owns one row of M (conflict-free, odd stride) and up to 8 individuals of its group, whose
 // s[i][k] are warp-broadcast loads — ~8x fewer shared-memory wavefronts per MAC than one dot per
 // thread.  Base values and composition weights are sequential per individual (exact order).
+// Q dot products z[i][r] = sum_k M[r][k] s[i][k] of one row r (individuals i0, i0 + G, ...),
+// accumulated in the reference's order (separate mul and add, increasing k).
 __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int D, int S, double* sMbase,
                               double* sZ, double* sS, double* sObase, double* sFk, double* sDist, double* f,
-                              bool resident) {
+                              bool resident, phase_clock& pc) {
   const int ncomp = pr.n_comp > 0 ? pr.n_comp : 1;
-  const int RP = (D + 31) / 32 * 32;           // threads per row group
-  const int NG = max(1, int(blockDim.x) / RP);  // individual groups
   for (int c = 0; c < ncomp; ++c) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
     // resident: every component's M and o were staged once at kernel start
@@ -97,15 +116,29 @@ __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int
     for (int i = warp; i < P; i += nwarps)
       for (int k = lane; k < D; k += 32) sS[i * D + k] = __dsub_rn(X[i * D + k], sO[k]);
     __syncthreads();
-    if (pr.n_comp > 0)
-      for (int i = threadIdx.x; i < P; i += blockDim.x) {  // dist^2 in double (problems/instance.hpp:127-134)
-        double d2 = 0.0;
-        const double* si = sS + i * D;
-        for (int j = 0; j < D; ++j) d2 = __dadd_rn(d2, __dmul_rn(si[j], si[j]));
-        sDist[i * kRunsMaxComp + c] = d2;
-      }
+    pc.mark(2);
     {
+      // register blocking: thread (g, r) owns row r of M (lanes over rows: conflict-free, odd
+      // stride) and individuals g, g + NG, ... 8 at a time, whose s[i][k] are warp-broadcast loads
+      const int RP = (D + 31) / 32 * 32;           // threads per row group
+      const int NG = max(1, int(blockDim.x) / RP);  // individual groups
       const int r = int(threadIdx.x) % RP, g = int(threadIdx.x) / RP;
+      // dist^2 in double (problems/instance.hpp:127-134), a sequential chain per individual, runs
+      // on the lanes the row mapping leaves idle (r >= D) so it overlaps the dot products
+      const int n_idle = NG * (RP - D) + max(0, int(blockDim.x) - NG * RP);
+      const int idle_id = g < NG ? (r >= D ? g * (RP - D) + (r - D) : -1) : NG * (RP - D) + int(threadIdx.x) - NG * RP;
+      if (pr.n_comp > 0) {
+        const bool idle_path = n_idle * 4 >= P;
+        const int id = idle_path ? idle_id : int(threadIdx.x);
+        const int stride = idle_path ? n_idle : int(blockDim.x);
+        if (id >= 0)
+          for (int i = id; i < P; i += stride) {
+            double d2 = 0.0;
+            const double* si = sS + i * D;
+            for (int j = 0; j < D; ++j) d2 = __dadd_rn(d2, __dmul_rn(si[j], si[j]));
+            sDist[i * kRunsMaxComp + c] = d2;
+          }
+      }
       if (r < D && g < NG) {
         const double* m = sM + r * S;
         for (int i0 = g; i0 < P; i0 += 8 * NG) {
@@ -131,15 +164,18 @@ __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int
       }
     }
     __syncthreads();
+    pc.mark(3);
     const int kind = pr.kind[c];
     if (kind_has_pre(kind)) {  // transcendental terms in parallel over all P*D elements (into sS)
-      for (int i = warp; i < P; i += nwarps) {
+      for (int e = threadIdx.x; e < P * D; e += blockDim.x) {
+        const int i = e / D, k = e - i * D;
         const double* zr = sZ + i * D;
         auto z = [&](int q) { return zr[q]; };
-        for (int k = lane; k < D; k += 32) sS[i * D + k] = base_pre_term<double, false>(kind, D, z, k);
+        sS[e] = base_pre_term<double, false>(kind, D, z, k);
       }
       __syncthreads();
     }
+    pc.mark(4);
     for (int i = threadIdx.x; i < P; i += blockDim.x) {
       const double* zr = sZ + i * D;
       const double* pe = sS + i * D;
@@ -148,6 +184,7 @@ __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int
       sFk[i * kRunsMaxComp + c] = base_value_pre<double, false>(kind, D, z, pre, pr.ell_w);
     }
     __syncthreads();
+    pc.mark(5);
   }
   for (int i = threadIdx.x; i < P; i += blockDim.x) {
     if (pr.n_comp == 0) {
@@ -190,6 +227,7 @@ __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int
     f[i] = __dadd_rn(value, pr.bias);
   }
   __syncthreads();
+  pc.mark(6);
 }
 
 // With a.split == 2 the run is owned by a 2-CTA cluster: both CTAs hold the full run state and
@@ -234,15 +272,17 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
   double* gpop = a.pop + size_t(run) * P * D;
   double* gfit = a.fit + size_t(run) * P;
   word_source src{RNG_PHILOX, key, nullptr, 0};
-  // evaluate rows [p0, p1) of X into f, then (split) publish them into the peer's f
+  phase_clock pc{blockIdx.x == 0 ? a.prof : nullptr, 0};
+  // evaluate rows [p0, p1) of X into f
   auto evaluate = [&](const double* X, double* f) {
-    runs_evaluate(pr, X + size_t(p0) * D, p1 - p0, D, S, sM, sZ, sS, sO, sFk, sDist, f + p0, a.resident != 0);
-    if (a.split == 2) {
-      cg::cluster_group cl = cg::this_cluster();
-      double* peer = cl.map_shared_rank(f, rank ^ 1);
-      for (int i = p0 + int(threadIdx.x); i < p1; i += blockDim.x) peer[i] = f[i];
-      cl.sync();
-    }
+    runs_evaluate(pr, X + size_t(p0) * D, p1 - p0, D, S, sM, sZ, sS, sO, sFk, sDist, f + p0, a.resident != 0, pc);
+  };
+  // (split) publish this CTA's rows [p0, p1) of the given arrays into the peer's copies
+  auto publish = [&](double* rows, int row_len) {
+    cg::cluster_group cl = cg::this_cluster();
+    double* peer = cl.map_shared_rank(rows, rank ^ 1);
+    for (int e = int(threadIdx.x); e < (p1 - p0) * row_len; e += blockDim.x)
+      peer[size_t(p0) * row_len + e] = rows[size_t(p0) * row_len + e];
   };
   if (a.split == 2) cg::this_cluster().sync();  // the peer's shared memory exists from here on
 
@@ -252,6 +292,10 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
       sPop[e] = __dadd_rn(a.lb, __dmul_rn(__dsub_rn(a.ub, a.lb), u01_of(philox_word(key, ctr, uint64_t(e)))));  // once
     __syncthreads();
     evaluate(sPop, sFit);
+    if (a.split == 2) {
+      publish(sFit, 1);
+      cg::this_cluster().sync();
+    }
     if (a.rec_on && rank == 0 && threadIdx.x == 0) rec_observe_seq<double>(a.rec, run, sFit, P);
   } else {
     for (int e = threadIdx.x; e < P * D; e += blockDim.x) sPop[e] = gpop[e];
@@ -259,11 +303,12 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
     __syncthreads();
   }
   const uint32_t g_first = a.gen0 + (a.init ? 1u : 0u);
+  pc.start();
   for (int g = 0; g < a.G; ++g) {
     const uint32_t gen = g_first + uint32_t(g);
     double* sTfit = sTfit2 + (g & 1) * P;
-    // draws (thread per individual)
-    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    // draws (thread per individual of this CTA's half)
+    for (int i = p0 + int(threadIdx.x); i < p1; i += blockDim.x) {
       word_reader r{&src, (uint64_t(gen) << 32) | uint32_t(i), 0, 0, nullptr};
       int x1, x2, x3;
       if (a.mutation == EVB_MUT_RAND1) {
@@ -285,39 +330,60 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
       sIdx[4 * i + 3] = (int(r.count) << 16) | jr;  // gene words start after the scalar words
     }
     __syncthreads();
-    // trial (warp per individual, lanes over genes)
+    pc.mark(0);
+    // trial (warp per individual of this half; each lane owns one Philox block = two gene words)
     {
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-      for (int i = warp; i < P; i += nwarps) {
+      for (int i = p0 + warp; i < p1; i += nwarps) {
         const int packed = sIdx[4 * i + 3];
         const int s0 = packed >> 16, jr = packed & 0xFFFF;
         const double* xa = sPop + sIdx[4 * i] * D;
         const double* xb = sPop + sIdx[4 * i + 1] * D;
         const double* xc = sPop + sIdx[4 * i + 2] * D;
         const uint64_t ctr = (uint64_t(gen) << 32) | uint32_t(i);
-        for (int j = lane; j < D; j += 32) {
-          const double u = u01_of(philox_word(key, ctr, uint64_t(s0 + j)));
-          const double xi = sPop[i * D + j];
-          double v = xi;
-          if (u < a.CR || j == jr) v = __dadd_rn(xa[j], __dmul_rn(a.F, __dsub_rn(xb[j], xc[j])));
-          sTrial[i * D + j] = clip_or_mid(v, xi, a.lb, a.ub, a.repair);
+        const int blk0 = s0 >> 1, nblk = ((s0 + D + 1) >> 1) - blk0;
+        for (int q = lane; q < nblk; q += 32) {
+          uint64_t w0, w1;
+          philox_pair(key, ctr, uint64_t(blk0 + q), w0, w1);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int j = 2 * (blk0 + q) + h - s0;
+            if (j < 0 || j >= D) continue;
+            const double u = u01_of(h ? w1 : w0);
+            const double xi = sPop[i * D + j];
+            double v = xi;
+            if (u < a.CR || j == jr) v = __dadd_rn(xa[j], __dmul_rn(a.F, __dsub_rn(xb[j], xc[j])));
+            sTrial[i * D + j] = clip_or_mid(v, xi, a.lb, a.ub, a.repair);
+          }
         }
       }
     }
     __syncthreads();
+    pc.mark(1);
     evaluate(sTrial, sTfit);
-    if (a.rec_on && rank == 0 && threadIdx.x == 0) rec_observe_seq<double>(a.rec, run, sTfit, P);  // trials, i order
-    // selection
+    // selection on this half (de/engine.hpp:36: replace when f_trial <= f_parent)
     {
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-      for (int i = warp; i < P; i += nwarps)
+      for (int i = p0 + warp; i < p1; i += nwarps)
         if (sTfit[i] <= sFit[i])
           for (int j = lane; j < D; j += 32) sPop[i * D + j] = sTrial[i * D + j];
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < P; i += blockDim.x)
+    for (int i = p0 + int(threadIdx.x); i < p1; i += blockDim.x)
       if (sTfit[i] <= sFit[i]) sFit[i] = sTfit[i];
     __syncthreads();
+    pc.mark(8);
+    if (a.split == 2) {
+      // the peer has finished reading this half's rows (its trials) once it reaches the barrier;
+      // then both halves cross over and the second barrier publishes them
+      cg::this_cluster().sync();
+      publish(sPop, D);
+      publish(sFit, 1);
+      publish(sTfit, 1);
+      cg::this_cluster().sync();
+      pc.mark(7);
+    }
+    if (a.rec_on && rank == 0 && threadIdx.x == 0) rec_observe_seq<double>(a.rec, run, sTfit, P);  // trials, i order
   }
   if (rank == 0) {
     for (int e = threadIdx.x; e < P * D; e += blockDim.x) gpop[e] = sPop[e];
@@ -454,6 +520,13 @@ extern "C" int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int 
     const size_t smem = runs_smem(pop_size, dim, a.split, a.resident ? a.n_mat : 1);
     require(smem <= 227 * 1024, "de_runs: run state does not fit in shared memory");
     EVB_CUDA(cudaFuncSetAttribute(de_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    static const bool prof = std::getenv("EVB_RUNS_PROFILE") != nullptr;
+    unsigned long long* dprof = nullptr;
+    if (prof) {
+      EVB_CUDA(cudaMalloc(&dprof, 16 * sizeof(unsigned long long)));
+      EVB_CUDA(cudaMemset(dprof, 0, 16 * sizeof(unsigned long long)));
+    }
+    a.prof = dprof;
     cudaError_t err;
     if (a.split == 2) {
       cudaLaunchConfig_t lc{};
@@ -476,6 +549,15 @@ extern "C" int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int 
     count_launch();
     if (err == cudaSuccess) err = cudaGetLastError();
     EVB_CUDA(cudaStreamSynchronize(st));
+    if (dprof) {
+      unsigned long long h[16];
+      EVB_CUDA(cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost));
+      cudaFree(dprof);
+      const char* names[] = {"draws", "trial", "x-o", "dist+dot", "pre", "base", "weights", "exchange", "select"};
+      std::string line = "[evb runs] cycles/generation:";
+      for (int k = 0; k < 9; ++k) line += std::string(" ") + names[k] + "=" + std::to_string(h[k] / std::max(1, generations));
+      std::fprintf(stderr, "%s\n", line.c_str());
+    }
     cudaFree(dprobs);
     cudaFree(dkeys);
     EVB_CUDA(err);
