@@ -1006,10 +1006,10 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
       }
     }
     if (force && std::string(force) == "classic" && best == 0) best = 1;
-    if (force && (std::string(force) == "pair" || std::string(force) == "pair2")) best = 0;
-    if (force && std::string(force) == "wide2") best = 1;
+    if (force && std::string(force) == "pair") best = 0;
     BM = cands[best][0];
     BN = cands[best][1];
+
     if (use_persistent) {
       BM = 64;
       BN = 56;
@@ -1126,11 +1126,9 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
       launch_f64_persistent<64, 56>(tmX, tmM, fp, rq.stream);
       return;
     }
-    static const bool pair2 = force && std::string(force) == "pair2";
-    static const bool wide2 = force && std::string(force) == "wide2";
-    if (pair2) launch_f64<64, 56, 2, 1, 6, 2>(tmX, tmM, fp, rq.stream);  // 32 x 56 warp tiles (A/B)
-    else if (wide2) launch_f64<64, 112, 2, 2, 6, 1>(tmX, tmM, fp, rq.stream);
-    else if (BM == 64 && BN == 56) launch_f64<64, 56, 4, 1, 6, 2>(tmX, tmM, fp, rq.stream);
+    // (measured alternatives: 64 x 40 and 48 x 56 tiles at 3 CTAs / SM, 32 x 56 warp tiles —
+    // all slower: 91, 115 and 146 us against 81.5 us per config-1 batch)
+    if (BM == 64 && BN == 56) launch_f64<64, 56, 4, 1, 6, 2>(tmX, tmM, fp, rq.stream);
     else if (BM == 64 && BN == 112) launch_f64<64, 112, 4, 2>(tmX, tmM, fp, rq.stream);
     else if (BM == 64 && BN == 128) launch_f64<64, 128, 4, 2>(tmX, tmM, fp, rq.stream);
     else launch_f64<32, 128, 2, 4>(tmX, tmM, fp, rq.stream);
