@@ -555,40 +555,74 @@ __global__ void __launch_bounds__(kSelThreads) de_select_scan_kernel(const de_de
     *d.arch_words = nv;
     if (d.src.mode == RNG_WORDS) *d.cursor = wpos + nv;
   }
-  // adapter update
-  if (tid != 0 || n_succ == 0) return;
-  if (d.cfg.parameter == EVB_PAR_SHADE) {
-    double gain_sum = 0.0;
-    for (int s = 0; s < n_succ; ++s) {
+  // adapter update: the sums stay sequential in success order (the reference's loops), but the
+  // successes' (gain, F, CR) are first staged into shared memory by the whole block — one thread
+  // chasing succ[s] -> fit[i] through global memory paid the L2 latency per success
+  if (n_succ == 0 || (d.cfg.parameter != EVB_PAR_SHADE && d.cfg.parameter != EVB_PAR_JADE)) return;
+  __shared__ double st_g[kSelThreads], st_f[kSelThreads], st_c[kSelThreads];
+  __shared__ double acc_s[4];
+  auto stage = [&](int base) {
+    const int s = base + tid;
+    if (s < n_succ) {
       const int i = d.succ[s];
-      gain_sum = __dadd_rn(gain_sum, double(fop<T>::sub(d.fit[i], d.trial_fit[i])));
+      st_g[tid] = double(fop<T>::sub(d.fit[i], d.trial_fit[i]));
+      st_f[tid] = double(d.F[i]);
+      st_c[tid] = double(d.CR[i]);
+    }
+  };
+  const bool one_chunk = n_succ <= int(blockDim.x);
+  if (d.cfg.parameter == EVB_PAR_SHADE) {  // de/parameter.hpp:166-184
+    double gain_sum = 0.0;
+    for (int base = 0; base < n_succ; base += blockDim.x) {
+      stage(base);
+      __syncthreads();
+      if (tid == 0)
+        for (int t = 0; t < min(int(blockDim.x), n_succ - base); ++t) gain_sum = __dadd_rn(gain_sum, st_g[t]);
+      __syncthreads();
     }
     double f_num = 0.0, f_den = 0.0, cr_acc = 0.0;
-    for (int s = 0; s < n_succ; ++s) {
-      const int i = d.succ[s];
-      const double w = __ddiv_rn(double(fop<T>::sub(d.fit[i], d.trial_fit[i])), gain_sum);
-      const double f = double(d.F[i]);
-      f_num = __dadd_rn(f_num, __dmul_rn(__dmul_rn(w, f), f));
-      f_den = __dadd_rn(f_den, __dmul_rn(w, f));
-      cr_acc = __dadd_rn(cr_acc, __dmul_rn(w, double(d.CR[i])));
+    if (tid == 0) acc_s[0] = gain_sum;
+    for (int base = 0; base < n_succ; base += blockDim.x) {
+      if (!one_chunk) stage(base);
+      __syncthreads();
+      if (tid == 0)
+        for (int t = 0; t < min(int(blockDim.x), n_succ - base); ++t) {
+          const double w = __ddiv_rn(st_g[t], gain_sum);
+          const double f = st_f[t];
+          f_num = __dadd_rn(f_num, __dmul_rn(__dmul_rn(w, f), f));
+          f_den = __dadd_rn(f_den, __dmul_rn(w, f));
+          cr_acc = __dadd_rn(cr_acc, __dmul_rn(w, st_c[t]));
+        }
+      __syncthreads();
     }
-    const int k = *d.write_index;
-    d.mem_f[k] = T(__ddiv_rn(f_num, f_den));
-    d.mem_cr[k] = T(cr_acc);
-    *d.write_index = (k + 1) % d.cfg.memory_size;
-  } else if (d.cfg.parameter == EVB_PAR_JADE) {  // de/parameter.hpp:107-120
+    if (tid == 0) {
+      const int k = *d.write_index;
+      d.mem_f[k] = T(__ddiv_rn(f_num, f_den));
+      d.mem_cr[k] = T(cr_acc);
+      *d.write_index = (k + 1) % d.cfg.memory_size;
+    }
+  } else {  // JADE, de/parameter.hpp:107-120 (lehmer_mean :45-52)
     double num = 0.0, den = 0.0, crm = 0.0;
-    for (int s = 0; s < n_succ; ++s) {  // lehmer_mean, de/parameter.hpp:45-52
-      const double v = double(d.F[d.succ[s]]);
-      num = __dadd_rn(num, __dmul_rn(v, v));
-      den = __dadd_rn(den, v);
+    for (int base = 0; base < n_succ; base += blockDim.x) {
+      stage(base);
+      __syncthreads();
+      if (tid == 0) {
+        const int n = min(int(blockDim.x), n_succ - base);
+        for (int t = 0; t < n; ++t) {
+          num = __dadd_rn(num, __dmul_rn(st_f[t], st_f[t]));
+          den = __dadd_rn(den, st_f[t]);
+        }
+        for (int t = 0; t < n; ++t) crm = __dadd_rn(crm, st_c[t]);
+      }
+      __syncthreads();
     }
-    const double lehmer = __ddiv_rn(num, den);
-    for (int s = 0; s < n_succ; ++s) crm = __dadd_rn(crm, double(d.CR[d.succ[s]]));
-    crm = __ddiv_rn(crm, double(n_succ));
-    const double c = double(T(d.cfg.jade_c));
-    d.mem_f[0] = T(__dadd_rn(__dmul_rn(__dsub_rn(1.0, c), double(d.mem_f[0])), __dmul_rn(c, lehmer)));
-    d.mem_cr[0] = T(__dadd_rn(__dmul_rn(__dsub_rn(1.0, c), double(d.mem_cr[0])), __dmul_rn(c, crm)));
+    if (tid == 0) {
+      const double lehmer = __ddiv_rn(num, den);
+      crm = __ddiv_rn(crm, double(n_succ));
+      const double c = double(T(d.cfg.jade_c));
+      d.mem_f[0] = T(__dadd_rn(__dmul_rn(__dsub_rn(1.0, c), double(d.mem_f[0])), __dmul_rn(c, lehmer)));
+      d.mem_cr[0] = T(__dadd_rn(__dmul_rn(__dsub_rn(1.0, c), double(d.mem_cr[0])), __dmul_rn(c, crm)));
+    }
   }
 }
 

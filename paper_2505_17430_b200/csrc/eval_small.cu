@@ -71,6 +71,28 @@ __device__ T hybrid_value(const int* perm, const int* sub_kinds, const int* chun
   return total;
 }
 
+// Stage a rows x cols block (global row stride ld) into shared memory (row stride S): eight
+// independent loads in flight per thread — a plain one-load-per-iteration loop waited out the L2
+// latency 40 times per thread at D = 100 (12 us of a 24 us evaluation).
+template <typename T>
+__device__ __forceinline__ void stage_rows(T* __restrict__ dst, int S, const T* __restrict__ src, int64_t ld, int rows,
+                                           int cols) {
+  const int n = rows * cols;
+  for (int base = threadIdx.x; base < n; base += 8 * blockDim.x) {
+    T v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = base + u * blockDim.x;
+      v[u] = idx < n ? __ldg(src + size_t(idx / cols) * ld + idx % cols) : T(0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = base + u * blockDim.x;
+      if (idx < n) dst[(idx / cols) * S + idx % cols] = v[u];
+    }
+  }
+}
+
 template <typename T>
 __global__ void eval_small_kernel(const small_args<T> a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -79,10 +101,7 @@ __global__ void eval_small_kernel(const small_args<T> a) {
   T* sZ = sS + size_t(a.PB) * a.D;
   const int b0 = blockIdx.x * a.PB;
   const int D = a.D;
-  for (int idx = threadIdx.x; idx < D * D; idx += blockDim.x) {
-    const int i = idx / D, k = idx % D;
-    sM[i * a.S + k] = a.rot[size_t(i) * a.ld + k];
-  }
+  stage_rows<T>(sM, a.S, a.rot, a.ld, D, D);
   for (int idx = threadIdx.x; idx < a.PB * D; idx += blockDim.x) {
     const int pb = idx / D, k = idx % D;
     const int b = b0 + pb;
@@ -203,10 +222,7 @@ __global__ void eval_comp_small_kernel(const comp_args<T> a) {
   for (int c = 0; c < a.n_comp; ++c) {
     const T* rot = a.rots + size_t(c) * D * a.ld;
     const T* o = a.shifts + size_t(c) * a.ld;
-    for (int idx = threadIdx.x; idx < D * D; idx += blockDim.x) {
-      const int i = idx / D, k = idx % D;
-      sM[i * a.S + k] = rot[size_t(i) * a.ld + k];
-    }
+    stage_rows<T>(sM, a.S, rot, a.ld, D, D);
     for (int idx = threadIdx.x; idx < a.PB * D; idx += blockDim.x) {
       const int pb = idx / D, k = idx % D;
       const int b = b0 + pb;
@@ -335,11 +351,19 @@ size_t small_smem(int D, int PB, bool comp) {
 
 constexpr size_t kSmallSmemMax = 200 * 1024;
 
+// Individuals per block: as many as amortise staging M (up to 2048 / D), but never so many that
+// fewer than two blocks per SM remain — a 180 x 100 batch in 9 blocks of 20 took 40 us, in 90
+// blocks of 2 a few us (M is re-read from L2 per block, 80 KB at D = 100).
 template <typename T>
 int pick_pb(int D, int P, bool comp) {
+  static int sms = [] {
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, 0);
+    return n;
+  }();
   int pb = std::max(1, std::min(32, 2048 / std::max(D, 1)));
+  pb = std::min(pb, std::max(1, (P + 2 * sms - 1) / (2 * sms)));
   while (pb > 1 && small_smem<T>(D, pb, comp) > kSmallSmemMax) --pb;
-  (void)P;
   return pb;
 }
 
