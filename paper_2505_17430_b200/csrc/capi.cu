@@ -459,19 +459,22 @@ int evb_evaluate_batch_host(evb_problem p, evb_scratch s, const void* X_host, in
         for (auto& e : tev) EVB_CUDA(cudaEventCreate(&e));
       if (trace) EVB_CUDA(cudaEventRecord(tev[0], s->copy_stream));
       // the previous call on this scratch synchronised st, so dx is free to overwrite
+      bool gates_ok = true;
       for (int c = 0; c < n_chunks; ++c) {
         const int64_t b = c ? rq.kgate_end[c - 1] : 0, w = rq.kgate_end[c] - b;
         EVB_CUDA(cudaMemcpy2DAsync(static_cast<uint8_t*>(s->dx) + b * es, ldd * es,
                                    static_cast<const uint8_t*>(X_host) + b * es, ldx * es, w * es, n_points,
                                    cudaMemcpyHostToDevice, s->copy_stream));
-        EVB_CUDA(cudaEventRecord(s->ev_chunk[c], s->copy_stream));
-        EVB_CUDA(cudaStreamWaitEvent(s->gate_stream, s->ev_chunk[c], 0));
-        if (wv(s->gate_stream, CUdeviceptr(s->gate + c), epoch, 0) != CUDA_SUCCESS)
-          throw runtime_error("evaluate_batch_host: cuStreamWriteValue32 failed");
+        if (gates_ok) {
+          EVB_CUDA(cudaEventRecord(s->ev_chunk[c], s->copy_stream));
+          EVB_CUDA(cudaStreamWaitEvent(s->gate_stream, s->ev_chunk[c], 0));
+          // a driver that refuses stream memory operations: fall back to waiting for all of X
+          gates_ok = wv(s->gate_stream, CUdeviceptr(s->gate + c), epoch, 0) == CUDA_SUCCESS;
+        }
         if (trace) EVB_CUDA(cudaEventRecord(tev[1 + c], s->copy_stream));
       }
       EVB_CUDA(cudaEventRecord(s->ev_x_ready, s->copy_stream));
-      rq.kgate = s->gate;
+      rq.kgate = gates_ok ? s->gate : nullptr;
       rq.kgate_epoch = epoch;
       rq.x_ready = s->ev_x_ready;
       if (trace) EVB_CUDA(cudaStreamWaitEvent(st, tev[0], 0));
