@@ -175,6 +175,22 @@ EVB_API int evb_recorder_csv(evb_recorder r, const char* suite_name, int dim, in
                              const int* problem_ids, int instances, int runs, char* buf, int64_t cap,
                              int64_t* len);
 
+/* ---- parameter_record (experiment/parameter_record.hpp:15-95) ------------------------------- */
+
+/* Per run, the (generation, mu_F, mu_CR) series an adaptive DE engine reports after each
+ * generation (de/engine.hpp:126-129 on_generation; JADE: mu, SHADE: memory means). */
+typedef struct evb_param_trace_s* evb_param_trace;
+
+EVB_API int evb_param_trace_create(int dtype, int n_runs, int capacity, evb_param_trace* out);
+EVB_API int evb_param_trace_destroy(evb_param_trace t);
+/* run `run`'s series (up to cap entries; *count = entries recorded; mu arrays in the dtype) */
+EVB_API int evb_param_trace_get(evb_param_trace t, int run, int* generations, void* mu_f, void* mu_cr, int cap,
+                                int* count);
+/* parameter_record::to_csv (problem,instance,run,generation,mu_f,mu_cr), runs laid out
+ * problem-major, run index fastest; *len = full length (buf may be NULL). */
+EVB_API int evb_param_trace_csv(evb_param_trace t, int n_problems, const int* problem_ids, int instances, int runs,
+                                char* buf, int64_t cap, int64_t* len);
+
 /* ---- DE engine (de/engine.hpp:51-173, de/builder.hpp:16-78) --------------------------- */
 
 /* strategy slots, by the reference's names (de/strategy.hpp, de/parameter.hpp) */
@@ -251,6 +267,10 @@ EVB_API int evb_de_last_reduction(evb_de e, int* pop_before, int* pop_after, int
  * reported, in FE order, to recorder run `run` (run_handle::evaluate -> on_evaluate,
  * experiment/runner.hpp:38-45); r = NULL detaches. */
 EVB_API int evb_de_attach_recorder(evb_de e, evb_recorder r, int run);
+/* Append (generation, mu_F, mu_CR) to trace run `run` after every generation of a JADE / SHADE
+ * engine (fixed adapters report nothing, as in the reference); t = NULL detaches.  The
+ * generation number counts from 1 after each evb_de_optimize start (evolution_state). */
+EVB_API int evb_de_attach_param_trace(evb_de e, evb_param_trace t, int run);
 EVB_API int evb_de_last_draws(evb_de e, int64_t* word_counts, int64_t* archive_words, uint32_t* generation,
                               void* F_host, void* CR_host, int* idx_host, int* jrand_host);
 
@@ -301,12 +321,14 @@ enum { EVB_BENCH_FORCE_ENGINE = 1 /* run every task through the per-generation e
  * problems[(p * instance_count) + i] is instance i of problem p (suite::at(p, i)); task
  * t = ((p * instance_count) + i) * runs + r runs de_engine::optimize(max_fes) from Philox key
  * evb_task_key(master_seed, t) and reports its evaluations, in FE order, to recorder run t (may
- * be NULL), then on_run_end.  best_host (may be NULL): each task's best fitness.  *path_used:
+ * be NULL), then on_run_end; adaptive configurations report (generation, mu_F, mu_CR) to
+ * ptrace run t (may be NULL; parameter_record).  best_host (may be NULL): each task's best.  *path_used:
  * 1 = all tasks in one persistent launch (evb_de_runs), 2 = per-task engines. */
 EVB_API int evb_evo_bench_de(int dtype, const evb_de_config* cfg, int pop_size, int dim,
                              const evb_problem* problems, int problem_count, int instance_count, int runs,
                              int64_t max_fes, uint64_t master_seed, double lb, double ub, evb_recorder rec,
-                             double* best_host, int flags, int* path_used, void* stream);
+                             evb_param_trace ptrace, double* best_host, int flags, int* path_used,
+                             void* stream);
 
 /* ---- PSO engine (pso/engine.hpp:33-153, pso/topology.hpp, pso/update.hpp) ------------------ */
 

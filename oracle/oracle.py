@@ -661,3 +661,36 @@ def ref_evo_bench_cso(phi, P, D, problem_ids, instances, runs, max_fes, interval
     buf = ctypes.create_string_buffer(int(n) + 1)
     REF().ref_evo_bench_cso(*args, buf, int(n), ptr(best))
     return buf.raw[:n].decode(), best
+
+
+register_ref({
+    "ref_de_params": (c_int, [vp, vp, vp]),
+    "ref_param_record": (i64, [vp, vp, vp, c_int, vp, c_int, vp, c_int, c_int, c_int, vp, i64]),
+})
+
+
+def _refde_params(self):
+    f, c = ctypes.c_double(), ctypes.c_double()
+    n = REF().ref_de_params(self.h, ctypes.byref(f), ctypes.byref(c))
+    return (f.value, c.value) if n else None
+
+
+RefDE.params = _refde_params
+
+
+def ref_param_record(series, problem_ids, instances, runs, dim=10):
+    """The reference parameter_record fed with per-run [(generation, mu_f, mu_cr), ...] series."""
+    n = max(1, max(len(s) for s in series))
+    gens = np.zeros((len(series), n), np.int32)
+    mf = np.zeros((len(series), n))
+    mc = np.zeros((len(series), n))
+    counts = np.array([len(s) for s in series], np.int32)
+    for r, s in enumerate(series):
+        for e, (g, a, b) in enumerate(s):
+            gens[r, e], mf[r, e], mc[r, e] = g, a, b
+    ids = np.ascontiguousarray(problem_ids, np.int32)
+    args = (ptr(gens), ptr(mf), ptr(mc), n, ptr(counts), len(ids), ptr(ids), instances, runs, dim)
+    ln = REF().ref_param_record(*args, None, 0)
+    buf = ctypes.create_string_buffer(int(ln) + 1)
+    REF().ref_param_record(*args, buf, int(ln))
+    return buf.raw[:ln].decode()

@@ -804,3 +804,43 @@ REF_API int64_t ref_evo_bench_cso(double phi, int P, int D, int n_problems, cons
   if (csv) std::memcpy(csv, s.data(), std::min<size_t>(size_t(cap), s.size()));
   return int64_t(s.size());
 }
+
+// ---- parameter_record (experiment/parameter_record.hpp) fed with given series ------------------
+#include "evobench/experiment/parameter_record.hpp"
+
+// mu_F / mu_CR the engine's adapter reports now (parameter_adapter::append_parameters)
+REF_API int ref_de_params(void* h, double* mu_f, double* mu_cr) {
+  auto* r = static_cast<ref_de_run*>(h);
+  std::vector<named_value<double>> v;
+  r->engine->parameter().append_parameters(v);
+  for (const auto& nv : v) {
+    if (nv.name == "mu_f") *mu_f = nv.value;
+    if (nv.name == "mu_cr") *mu_cr = nv.value;
+  }
+  return int(v.size());
+}
+
+// runs x n entries (counts[r] used), on_generation per entry, returns to_csv's length
+REF_API int64_t ref_param_record(const int* gens, const double* mu_f, const double* mu_cr, int n, const int* counts,
+                                 int n_problems, const int* problem_ids, int instances, int runs, int dim, char* csv,
+                                 int64_t cap) {
+  std::vector<problem_instance<double>> inst;
+  for (int q = 0; q < n_problems * instances; ++q) inst.push_back(make_instance<double>(1, dim, 1, 0));
+  problems::suite<double> su("gpu", dim, std::vector<int>(problem_ids, problem_ids + n_problems), instances, 0,
+                             std::move(inst));
+  experiment::parameter_record<double> rec(su, runs);
+  for (int p = 0; p < n_problems; ++p)
+    for (int i = 0; i < instances; ++i)
+      for (int k = 0; k < runs; ++k) {
+        const int run = (p * instances + i) * runs + k;
+        experiment::run_key key{problem_ids[p], i + 1, p, i, k};
+        for (int e = 0; e < counts[run]; ++e) {
+          const size_t q = size_t(run) * n + e;
+          const named_value<double> params[2] = {{"mu_f", mu_f[q]}, {"mu_cr", mu_cr[q]}};
+          rec.on_generation(key, gens[q], std::span<const named_value<double>>(params, 2));
+        }
+      }
+  const std::string s = rec.to_csv();
+  if (csv) std::memcpy(csv, s.data(), std::min<size_t>(size_t(cap), s.size()));
+  return int64_t(s.size());
+}

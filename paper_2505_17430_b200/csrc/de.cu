@@ -96,6 +96,9 @@ struct evb_de_s {
   int64_t* d_shrink_words = nullptr;
   int last_shrink_valid = 0;
   int gen_P = 0;  // population size at the start of the last generation (its trial count)
+  evb_param_trace_s* ptrace = nullptr;  // attached parameter_record trace (may be null)
+  int ptrace_run = 0;
+  int gen_count = 0;  // evolution_state::generation() (reset by evb_de_optimize)
 };
 
 namespace evb {
@@ -703,6 +706,32 @@ de_dev<T> make_dev(evb_de_s* e, void* pop, int64_t ldp, void* fit, double lb, do
   return d;
 }
 
+// adapter means after a generation -> parameter_record (de/parameter.hpp:130-133 JADE mu,
+// :186-195 SHADE mean of the memories: sequential double sum / H, cast to T)
+template <typename T>
+__global__ void param_trace_kernel(const T* mem_f, const T* mem_cr, int H, int shade, int* gen_out, T* mf_out,
+                                   T* mc_out, int* count, int cap, int generation) {
+  if (threadIdx.x != 0) return;
+  T mf, mc;
+  if (shade) {
+    double sf = 0.0, sc = 0.0;
+    for (int k = 0; k < H; ++k) sf = __dadd_rn(sf, double(mem_f[k]));
+    for (int k = 0; k < H; ++k) sc = __dadd_rn(sc, double(mem_cr[k]));
+    mf = T(__ddiv_rn(sf, double(H)));
+    mc = T(__ddiv_rn(sc, double(H)));
+  } else {
+    mf = mem_f[0];
+    mc = mem_cr[0];
+  }
+  const int n = *count;
+  if (n < cap) {
+    gen_out[n] = generation;
+    mf_out[n] = mf;
+    mc_out[n] = mc;
+  }
+  *count = n + 1;
+}
+
 template <typename T>
 void reduce_t(evb_de_s* e, void* pop, int64_t ldp, void* fit, evb_rng_s* r, cudaStream_t st);
 
@@ -758,6 +787,17 @@ void generation_t(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, vo
   }
   EVB_CUDA(cudaGetLastError());
   e->fes += e->P;  // st.add_fes(1) per trial (de/engine.hpp:88)
+  ++e->gen_count;
+  if (e->ptrace && (e->cfg.parameter == EVB_PAR_SHADE || e->cfg.parameter == EVB_PAR_JADE)) {
+    evb_param_trace_s* t = e->ptrace;
+    const size_t off = size_t(e->ptrace_run) * t->cap;
+    param_trace_kernel<T><<<1, 32, 0, st>>>(static_cast<const T*>(e->mem_f), static_cast<const T*>(e->mem_cr),
+                                            e->cfg.memory_size, e->cfg.parameter == EVB_PAR_SHADE ? 1 : 0,
+                                            t->gen + off, static_cast<T*>(t->mu_f) + off,
+                                            static_cast<T*>(t->mu_cr) + off, t->count + e->ptrace_run, t->cap,
+                                            e->gen_count);
+    count_launch();
+  }
   reduce_t<T>(e, pop, ldp, fit, r, st);
   e->last_gen = r->gen;
   r->gen++;
@@ -1233,7 +1273,7 @@ int evb_de_generations(evb_de e, evb_problem objective, evb_scratch s, void* pop
       throw config_error("de_generations: linear population reduction needs a budget (evb_de_set_budget)");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     evb_scratch_s* sc = s ? s : e->eval_scratch;
-    if (e->reduction) {  // the population size changes between generations: no graph replay
+    if (e->reduction || e->ptrace) {  // size changes / per-generation trace arguments: no graph replay
       for (int g = 0; g < n; ++g) de_generation(e, &objective->p, sc, pop, ldp, fitness, lb, ub, rng, st);
       return;
     }
@@ -1250,6 +1290,8 @@ int evb_de_generations(evb_de e, evb_problem objective, evb_scratch s, void* pop
       if (!e->cap_stream) EVB_CUDA(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
       EVB_CUDA(cudaStreamSynchronize(st));
       const uint32_t host_gen = rng->gen, host_last = e->last_gen;
+      const int64_t host_fes = e->fes;
+      const int host_count = e->gen_count;
       const int k0 = last_launch_count();
       cudaGraph_t g = nullptr;
       EVB_CUDA(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
@@ -1265,6 +1307,8 @@ int evb_de_generations(evb_de e, evb_problem objective, evb_scratch s, void* pop
       count_launch(-e->g_kernels);  // captured, not launched
       rng->gen = host_gen;
       e->last_gen = host_last;
+      e->fes = host_fes;
+      e->gen_count = host_count;
       const cudaError_t ie = cudaGraphInstantiate(&e->graph, g, 0);
       cudaGraphDestroy(g);
       EVB_CUDA(ie);
@@ -1276,6 +1320,8 @@ int evb_de_generations(evb_de e, evb_problem objective, evb_scratch s, void* pop
       EVB_CUDA(cudaGraphLaunch(e->graph, st));
       e->last_gen = rng->gen;
       rng->gen++;
+      e->fes += e->P;
+      ++e->gen_count;
       count_launch(e->g_kernels);
     }
   });
@@ -1342,6 +1388,22 @@ int evb_de_attach_recorder(evb_de e, evb_recorder r, int run) {
   });
 }
 
+int evb_de_attach_param_trace(evb_de e, evb_param_trace t, int run) {
+  return guarded([&] {
+    require(e != nullptr, "de: null handle");
+    if (t) {
+      require(t->dtype == e->dtype, "de_attach_param_trace: dtype mismatch");
+      require(run >= 0 && run < t->n_runs, "de_attach_param_trace: run out of range");
+    }
+    e->ptrace = t;
+    e->ptrace_run = run;
+    if (e->graph) {  // the captured generation does not contain the trace call
+      EVB_CUDA(cudaGraphExecDestroy(e->graph));
+      e->graph = nullptr;
+    }
+  });
+}
+
 int evb_de_last_draws(evb_de e, int64_t* word_counts, int64_t* archive_words, uint32_t* generation, void* F_host,
                       void* CR_host, int* idx_host, int* jrand_host) {
   return guarded([&] {
@@ -1388,6 +1450,7 @@ int evb_de_optimize(evb_de e, evb_problem objective, evb_scratch s, void* pop, i
     if (e->rec) recorder_observe(e->rec, e->rec_run, fitness, e->P, st);  // initial evaluations
     e->max_fes = max_fes;  // evolution_state st(max_fes, ...); st.add_fes(P) for the initial members
     e->fes = e->P;
+    e->gen_count = 0;
     int gens = 0;
     while (e->fes < max_fes) {
       de_generation(e, &objective->p, sc, pop, ldp, fitness, lb, ub, rng, st);

@@ -217,6 +217,20 @@ void eval_dispatch(const eval_request& rq);
 // true when eval_dispatch runs the request on the fused fp64 GEMM, whose producer honours kgate
 bool gate_eligible(const eval_request& rq);
 
+}  // namespace evb
+
+// parameter_record trace (recorder.cu): per run (generation, mu_F, mu_CR) series on the device
+struct evb_param_trace_s {
+  int dtype = EVB_F64;
+  int n_runs = 0, cap = 0;
+  int* gen = nullptr;      // n_runs x cap
+  void* mu_f = nullptr;    // n_runs x cap (T)
+  void* mu_cr = nullptr;   // n_runs x cap (T)
+  int* count = nullptr;    // n_runs
+};
+
+namespace evb {
+
 // best-so-far recorder (recorder.cu)
 void recorder_observe(evb_recorder_s* rec, int run, const void* values, int64_t n, cudaStream_t st);
 void* recorder_view(evb_recorder_s* rec, int* n_ckpt, int64_t* interval, void** running, int** next, int64_t** fes);

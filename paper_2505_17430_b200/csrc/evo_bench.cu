@@ -127,8 +127,8 @@ uint64_t evb_task_key(uint64_t master_seed, uint64_t task_index) { return task_k
 
 int evb_evo_bench_de(int dtype, const evb_de_config* cfg, int pop_size, int dim, const evb_problem* problems,
                      int problem_count, int instance_count, int runs, int64_t max_fes, uint64_t master_seed,
-                     double lb, double ub, evb_recorder rec, double* best_host, int flags, int* path_used,
-                     void* stream) {
+                     double lb, double ub, evb_recorder rec, evb_param_trace ptrace, double* best_host, int flags,
+                     int* path_used, void* stream) {
   return guarded([&] {
     require(cfg != nullptr, "evo_bench: null argument");
     const int tasks = suite_tasks(dtype, pop_size, dim, problems, problem_count, instance_count, runs, max_fes, rec);
@@ -175,6 +175,7 @@ int evb_evo_bench_de(int dtype, const evb_de_config* cfg, int pop_size, int dim,
           check_status(evb_de_create(dtype, cfg, P, D, &e));
           int rc = evb_rng_create_philox(keys[t], &r);
           if (rc == EVB_OK && rec) rc = evb_de_attach_recorder(e, rec, t);
+          if (rc == EVB_OK && ptrace) rc = evb_de_attach_param_trace(e, ptrace, t);
           int bi = 0, g = 0;
           double bf = 0.0;
           if (rc == EVB_OK)

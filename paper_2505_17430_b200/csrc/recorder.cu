@@ -232,4 +232,109 @@ int evb_recorder_csv(evb_recorder r, const char* suite_name, int dim, int n_prob
   });
 }
 
+// ---- parameter_record (experiment/parameter_record.hpp:15-95) ---------------------------------
+// Per run a series of (generation, mu_F, mu_CR) appended on the device after each generation of
+// an adaptive DE engine (de/engine.hpp:126-129 -> on_generation), exported as the reference CSV.
+
+int evb_param_trace_create(int dtype, int n_runs, int capacity, evb_param_trace* out) {
+  return guarded([&] {
+    require(dtype == EVB_F32 || dtype == EVB_F64, "parameter_record: dtype must be EVB_F32 or EVB_F64");
+    require(out != nullptr && n_runs > 0 && capacity > 0, "parameter_record: bad arguments");
+    auto* t = new evb_param_trace_s();
+    t->dtype = dtype;
+    t->n_runs = n_runs;
+    t->cap = capacity;
+    const size_t es = dtype == EVB_F64 ? 8 : 4;
+    try {
+      EVB_CUDA(cudaMalloc(&t->gen, sizeof(int) * size_t(n_runs) * capacity));
+      EVB_CUDA(cudaMalloc(&t->mu_f, es * size_t(n_runs) * capacity));
+      EVB_CUDA(cudaMalloc(&t->mu_cr, es * size_t(n_runs) * capacity));
+      EVB_CUDA(cudaMalloc(&t->count, sizeof(int) * n_runs));
+      EVB_CUDA(cudaMemset(t->count, 0, sizeof(int) * n_runs));
+    } catch (...) {
+      cudaFree(t->gen);
+      cudaFree(t->mu_f);
+      cudaFree(t->mu_cr);
+      cudaFree(t->count);
+      delete t;
+      throw;
+    }
+    *out = t;
+  });
+}
+
+int evb_param_trace_destroy(evb_param_trace t) {
+  return guarded([&] {
+    if (!t) return;
+    cudaFree(t->gen);
+    cudaFree(t->mu_f);
+    cudaFree(t->mu_cr);
+    cudaFree(t->count);
+    delete t;
+  });
+}
+
+// series of run `run`: up to `cap` entries; *count receives the number recorded
+int evb_param_trace_get(evb_param_trace t, int run, int* gens, void* mu_f, void* mu_cr, int cap, int* count) {
+  return guarded([&] {
+    require(t != nullptr && run >= 0 && run < t->n_runs && count, "parameter_record: bad arguments");
+    EVB_CUDA(cudaDeviceSynchronize());
+    int n = 0;
+    EVB_CUDA(cudaMemcpy(&n, t->count + run, sizeof(int), cudaMemcpyDeviceToHost));
+    n = std::min(n, t->cap);
+    *count = n;
+    const int m = std::min(n, cap);
+    const size_t es = t->dtype == EVB_F64 ? 8 : 4;
+    const size_t off = size_t(run) * t->cap;
+    if (m > 0 && gens) EVB_CUDA(cudaMemcpy(gens, t->gen + off, sizeof(int) * m, cudaMemcpyDeviceToHost));
+    if (m > 0 && mu_f)
+      EVB_CUDA(cudaMemcpy(mu_f, static_cast<uint8_t*>(t->mu_f) + off * es, es * m, cudaMemcpyDeviceToHost));
+    if (m > 0 && mu_cr)
+      EVB_CUDA(cudaMemcpy(mu_cr, static_cast<uint8_t*>(t->mu_cr) + off * es, es * m, cudaMemcpyDeviceToHost));
+  });
+}
+
+// parameter_record::to_csv (parameter_record.hpp:58-78): problem,instance,run,generation,mu_f,mu_cr
+int evb_param_trace_csv(evb_param_trace t, int n_problems, const int* problem_ids, int instances, int runs, char* buf,
+                        int64_t cap, int64_t* len) {
+  return guarded([&] {
+    require(t != nullptr && problem_ids && len, "parameter_record_csv: null argument");
+    require(int64_t(n_problems) * instances * runs == t->n_runs, "parameter_record_csv: layout does not match the runs");
+    EVB_CUDA(cudaDeviceSynchronize());
+    const size_t es = t->dtype == EVB_F64 ? 8 : 4;
+    const size_t cells = size_t(t->n_runs) * t->cap;
+    std::vector<int> cnt(t->n_runs), gen(cells);
+    std::vector<uint8_t> mf(es * cells), mc(es * cells);
+    EVB_CUDA(cudaMemcpy(cnt.data(), t->count, sizeof(int) * t->n_runs, cudaMemcpyDeviceToHost));
+    EVB_CUDA(cudaMemcpy(gen.data(), t->gen, sizeof(int) * cells, cudaMemcpyDeviceToHost));
+    EVB_CUDA(cudaMemcpy(mf.data(), t->mu_f, es * cells, cudaMemcpyDeviceToHost));
+    EVB_CUDA(cudaMemcpy(mc.data(), t->mu_cr, es * cells, cudaMemcpyDeviceToHost));
+    std::string out = "problem,instance,run,generation,mu_f,mu_cr\n";
+    auto val = [&](const std::vector<uint8_t>& v, size_t k) {
+      return t->dtype == EVB_F64 ? fmt(reinterpret_cast<const double*>(v.data())[k])
+                                 : fmt(reinterpret_cast<const float*>(v.data())[k]);
+    };
+    for (int p = 0; p < n_problems; ++p)
+      for (int i = 0; i < instances; ++i)
+        for (int r = 0; r < runs; ++r) {
+          const size_t run = (size_t(p) * instances + i) * runs + r;
+          const std::string prefix =
+              std::to_string(problem_ids[p]) + "," + std::to_string(i + 1) + "," + std::to_string(r + 1) + ",";
+          const int n = std::min(cnt[run], t->cap);
+          for (int e = 0; e < n; ++e) {
+            const size_t k = run * t->cap + e;
+            out += prefix;
+            out += std::to_string(gen[k]);
+            out += ',';
+            out += val(mf, k);
+            out += ',';
+            out += val(mc, k);
+            out += '\n';
+          }
+        }
+    *len = int64_t(out.size());
+    if (buf && cap > 0) std::memcpy(buf, out.data(), std::min<size_t>(size_t(cap), out.size()));
+  });
+}
+
 }  // extern "C"

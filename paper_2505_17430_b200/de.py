@@ -239,6 +239,14 @@ class DEEngine:
               "de_last_reduction")
         return {"pop_before": b.value, "pop_after": a.value, "shrink_words": w.value}
 
+    def attach_param_trace(self, trace, run: int = 0) -> None:
+        """Report (generation, mu_F, mu_CR) after every generation (parameter_record)."""
+        from .recorder import _sigs as _rec_sigs
+        _rec_sigs()
+        check(_lib.lib().evb_de_attach_param_trace(self._h, trace.handle if trace is not None else None, run),
+              "de_attach_param_trace")
+        self._ptrace = trace
+
     def attach_recorder(self, recorder, run: int = 0) -> None:
         """Report every later evaluation (init inside optimize, each generation's trials, FE order)
         to `recorder` as run `run` (experiment/runner.hpp:38-52 run_handle). None detaches."""

@@ -29,7 +29,7 @@ def _sigs():
     _lib.register_signatures({
         "evb_task_key": (u64, [u64, u64]),
         "evb_evo_bench_de": (c_int, [c_int, ctypes.POINTER(_Cfg), c_int, c_int, vp, c_int, c_int, c_int, i64, u64,
-                                     c_double, c_double, vp, vp, c_int, ctypes.POINTER(c_int), vp]),
+                                     c_double, c_double, vp, vp, vp, c_int, ctypes.POINTER(c_int), vp]),
         "evb_evo_bench_pso": (c_int, [c_int, ctypes.POINTER(_PsoCfg), c_int, c_int, vp, c_int, c_int, c_int, i64, u64,
                                       c_double, c_double, vp, vp, vp]),
         "evb_evo_bench_cso": (c_int, [c_int, c_double, c_int, c_int, vp, c_int, c_int, c_int, i64, u64, c_double,
@@ -44,7 +44,7 @@ def task_key(master_seed: int, task_index: int) -> int:
 
 
 def evo_bench_de(cfg: DEConfig, pop_size: int, suite: Sequence[Sequence[ProblemInstance]], runs: int, max_fes: int,
-                 master_seed: int = 0, lb: float = -100.0, ub: float = 100.0, recorder=None,
+                 master_seed: int = 0, lb: float = -100.0, ub: float = 100.0, recorder=None, param_trace=None,
                  force_engine: bool = False, dtype: int = EVB_F64, stream=None):
     """evo_bench(make_algorithm(cfg, pop_size), suite, recorder, {runs, max_fes, master_seed}).
     suite[p][i] is instance i of problem p.  Returns {"best": per-task best fitness (task index
@@ -61,6 +61,7 @@ def evo_bench_de(cfg: DEConfig, pop_size: int, suite: Sequence[Sequence[ProblemI
     path = ctypes.c_int()
     check(_lib.lib().evb_evo_bench_de(dtype, ctypes.byref(c), pop_size, dim, handles, n_problems, instances, runs,
                                       max_fes, master_seed, lb, ub, recorder.handle if recorder is not None else None,
+                                      param_trace.handle if param_trace is not None else None,
                                       ctypes.c_void_p(best.ctypes.data), 1 if force_engine else 0, ctypes.byref(path),
                                       _stream_ptr(stream)), "evo_bench_de")
     return {"best": best, "path": "batched" if path.value == 1 else "engine"}

@@ -166,3 +166,58 @@ def test_batched_runs_recording(dev):
     # exact-order arithmetic: identical unless a libm-vs-CUDA ulp flipped a near-tie selection
     rel = np.abs(grid[0] - ref_grid[0]) / np.maximum(1.0, np.abs(ref_grid[0]))
     assert rel.max() <= 1e-10
+
+
+def test_param_trace_shade_matches_reference(dev):
+    # parameter_record (experiment/parameter_record.hpp): after every SHADE generation the engine
+    # appends (generation, mean M_F, mean M_CR); compared with the reference adapter's own
+    # append_parameters in lockstep, and the CSV with the reference parameter_record's
+    from paper_2505_17430_b200.de import preset_shade, scripted_words_for_generation
+    from paper_2505_17430_b200.recorder import ParamTrace
+    P, D, G, key = 40, 12, 8, 0xAB
+    o, m = O.shift_rotation(19, D)
+    cfg = preset_shade(0.11, 10, 1.0)
+    prob = evb.ProblemInstance.base(evb.BaseKind.sphere, o, m, 0.0)
+    eng = DEEngine(cfg, P, D)
+    trace = ParamTrace(1, 64)
+    eng.attach_param_trace(trace, 0)
+    rng = Rng.philox(key)
+    pop = torch.empty((P, D), dtype=torch.float64, device=dev)
+    eng.init_population(pop, -100.0, 100.0, rng)
+    fit = torch.empty(P, dtype=torch.float64, device=dev)
+    evb.evaluate_batch(prob, pop, evb.EvalScratch(), fit)
+    ref = O.RefDE(cfg, P, D)
+    ref.set_problem_base(0, o, m, 0.0)
+    ref.set_pop(pop.cpu().numpy(), fit.cpu().numpy())
+    for g in range(G):
+        eng.generation(prob, pop, fit, -100.0, 100.0, rng)
+        dr = eng.last_draws()
+        assert ref.generation(scripted_words_for_generation(key, dr["generation"], dr["word_counts"],
+                                                            dr["archive_words"], philox=O.philox_words),
+                              -100.0, 100.0)
+        gens, mf, mc = trace.series(0)
+        assert list(gens) == list(range(1, g + 2))
+        want = ref.params()
+        assert abs(mf[-1] - want[0]) <= 1e-12 and abs(mc[-1] - want[1]) <= 1e-12, g
+        st = ref.get()  # re-sync (F/CR ulps, as in the config-2 lockstep)
+        pop.copy_(torch.from_numpy(st["pop"]))
+        fit.copy_(torch.from_numpy(st["fit"]))
+        eng.set_state(st["archive"], st["memory_f"], st["memory_cr"], st["write_index"])
+    gens, mf, mc = trace.series(0)
+    ref_csv = O.ref_param_record([list(zip(gens, mf, mc))], [3], 1, 1)
+    assert trace.to_csv([3], 1, 1) == ref_csv
+
+
+def test_param_trace_fixed_adapter_reports_nothing(dev):
+    from paper_2505_17430_b200.recorder import ParamTrace
+    P, D = 20, 5
+    o, m = O.shift_rotation(3, D)
+    prob = evb.ProblemInstance.base(evb.BaseKind.sphere, o, m, 0.0)
+    eng = DEEngine(preset_de(), P, D)
+    trace = ParamTrace(1, 8)
+    eng.attach_param_trace(trace, 0)
+    pop = torch.empty((P, D), dtype=torch.float64, device=dev)
+    fit = torch.empty(P, dtype=torch.float64, device=dev)
+    eng.optimize(prob, pop, fit, -100.0, 100.0, P * 5, Rng.philox(1))
+    assert len(trace.series(0)[0]) == 0
+    assert trace.to_csv([1], 1, 1) == "problem,instance,run,generation,mu_f,mu_cr\n"
