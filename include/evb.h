@@ -276,7 +276,7 @@ EVB_API int evb_de_last_draws(evb_de e, int64_t* word_counts, int64_t* archive_w
 
 /* K8: n_runs independent DE runs in ONE persistent launch (one CTA per run, every generation
  * inside the kernel; experiment/runner.hpp:101-160 evo_bench over a suite).  Run r evaluates
- * problems[r] (base or composition, fp64) and draws from Philox key keys[r]; pops / fits are
+ * problems[r] (base, hybrid or composition, fp64) and draws from Philox key keys[r]; pops / fits are
  * device arrays (n_runs x pop_size x dim, n_runs x pop_size).  init != 0: draw and evaluate the
  * initial populations first (generation id gen0), then run `generations` generations (ids
  * gen0+1 ...); otherwise continue from the given populations (ids gen0 ...).  Supports the `de`

@@ -54,22 +54,6 @@ struct small_args {
   int scalar_trig;
 };
 
-template <typename T>
-__device__ T hybrid_value(const int* perm, const int* sub_kinds, const int* chunk_sizes, int n_chunks,
-                          const T* hyb_w, const T* zrow, int64_t zstride) {
-  // problems/instance.hpp:97-112: permute, split into chunks, sum chunk base values (libm trig)
-  using F = fop<T>;
-  T total = T(0);
-  int offset = 0;
-  for (int c = 0; c < n_chunks; ++c) {
-    const int len = chunk_sizes[c];
-    const int off = offset;
-    auto z = [&](int i) { return zrow[int64_t(perm[off + i]) * zstride]; };
-    total = F::add(total, base_value_seq<T, false>(sub_kinds[c], len, z, hyb_w + off));
-    offset += len;
-  }
-  return total;
-}
 
 // Stage a rows x cols block (global row stride ld) into shared memory (row stride S): eight
 // independent loads in flight per thread — a plain one-load-per-iteration loop waited out the L2

@@ -279,4 +279,23 @@ __device__ T base_value_pre(int kind, int n, const Z& z, const PRE& pre, const T
   }
 }
 
+// hybrid problems (problems/instance.hpp:97-112): z permuted, split into chunks, the chunks'
+// base values (libm trig) summed in order; hyb_w holds each chunk's elliptic weights at its offset
+template <typename T>
+__device__ __forceinline__ T hybrid_value(const int* perm, const int* sub_kinds, const int* chunk_sizes, int n_chunks,
+                          const T* hyb_w, const T* zrow, int64_t zstride) {
+  // problems/instance.hpp:97-112: permute, split into chunks, sum chunk base values (libm trig)
+  using F = fop<T>;
+  T total = T(0);
+  int offset = 0;
+  for (int c = 0; c < n_chunks; ++c) {
+    const int len = chunk_sizes[c];
+    const int off = offset;
+    auto z = [&](int i) { return zrow[int64_t(perm[off + i]) * zstride]; };
+    total = F::add(total, base_value_seq<T, false>(sub_kinds[c], len, z, hyb_w + off));
+    offset += len;
+  }
+  return total;
+}
+
 }  // namespace evb

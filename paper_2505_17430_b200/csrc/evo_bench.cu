@@ -11,8 +11,9 @@
 //   recorder     run slot t; on_run_end for every task after its run (runner.hpp:121-122)
 //
 // Configurations the persistent batched-runs kernel supports (the `de` preset family) run as
-// ONE launch over all tasks; any other DE configuration (JADE, SHADE, archive, reflect repair,
-// fp32, hybrids) runs each task through the per-generation engine, tasks in order.
+// ONE launch over all tasks (base, hybrid and composition problems mixed); any other DE
+// configuration (JADE, SHADE, archive, other strategies, fp32) runs each task through the
+// per-generation engine, tasks in order.
 #include <cuda_runtime.h>
 
 #include <algorithm>

@@ -55,10 +55,16 @@ struct run_problem {
   const double* rot[kRunsMaxComp];
   int kind[kRunsMaxComp];
   double sigma[kRunsMaxComp], lambda[kRunsMaxComp], cbias[kRunsMaxComp];
-  int n_comp;  // 0: base problem (shift[0], rot[0], kind[0])
+  int n_comp;  // 0: base or hybrid problem (shift[0], rot[0], kind[0])
   int ld;      // row stride of the rotations
   double bias;
   const double* ell_w;
+  // hybrid (problems/instance.hpp:97-112): permutation, chunk kinds / sizes, per-chunk weights
+  int hybrid, n_chunks;
+  const int* perm;
+  const int* sub_kinds;
+  const int* chunk_sizes;
+  const double* hyb_w;
 };
 
 struct runs_args {
@@ -165,6 +171,13 @@ __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int
     }
     __syncthreads();
     pc.mark(3);
+    if (pr.hybrid) {  // permuted chunks, sequential per individual
+      for (int i = threadIdx.x; i < P; i += blockDim.x)
+        sFk[i * kRunsMaxComp] =
+            hybrid_value<double>(pr.perm, pr.sub_kinds, pr.chunk_sizes, pr.n_chunks, pr.hyb_w, sZ + i * D, 1);
+      __syncthreads();
+      continue;
+    }
     const int kind = pr.kind[c];
     if (kind_has_pre(kind)) {  // transcendental terms in parallel over all P*D elements (into sS)
       for (int e = threadIdx.x; e < P * D; e += blockDim.x) {
@@ -424,7 +437,6 @@ std::string runs_kernel_unsupported(int dtype, const evb_de_config* cfg, int pop
   for (int r = 0; r < n_runs; ++r) {
     const device_problem& p = problems[r]->p;
     if (p.dtype != EVB_F64 || p.dim != dim) return "de_runs: problem dtype / dim mismatch";
-    if (p.spec == SPEC_HYBRID) return "de_runs: hybrid problems are not supported by the persistent kernel";
     if (p.spec == SPEC_COMPOSITION && p.n_comp > kRunsMaxComp) return "de_runs: at most 4 composition components";
   }
   return {};
@@ -448,7 +460,15 @@ extern "C" int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int 
       q.bias = p.bias;
       q.ld = p.ld;
       q.ell_w = static_cast<const double*>(p.ell_w);
-      if (p.spec == SPEC_BASE) {
+      q.hybrid = p.spec == SPEC_HYBRID ? 1 : 0;
+      if (q.hybrid) {
+        q.n_chunks = p.n_chunks;
+        q.perm = p.perm;
+        q.sub_kinds = p.sub_kinds;
+        q.chunk_sizes = p.chunk_sizes;
+        q.hyb_w = static_cast<const double*>(p.hyb_w);
+      }
+      if (p.spec != SPEC_COMPOSITION) {
         q.n_comp = 0;
         q.shift[0] = static_cast<const double*>(p.shift);
         q.rot[0] = static_cast<const double*>(p.rotation);

@@ -164,3 +164,28 @@ def test_evo_bench_pso_presets(dev):
         assert np.all(fes == max_fes)
         assert np.all(np.diff(grid, axis=1) <= 0)
         assert np.array_equal(grid[:, -1], res["best"])
+
+
+def test_batched_runs_hybrid_and_mixed_suite(dev):
+    # the persistent kernel runs hybrid problems too (permuted chunks, problems/instance.hpp:97-112):
+    # a suite mixing base, hybrid and composition problems in ONE launch agrees with the
+    # per-task engine path (same positional streams, both exact-order evaluation)
+    D, P, max_fes, runs = 20, 24, 24 * 15, 2
+    rs = np.random.default_rng(4)
+    o, m = O.shift_rotation(61, D)
+    perm = rs.permutation(D)
+    hyb = evb.ProblemInstance.hybrid(o, m, [int(K.elliptic), int(K.rastrigin), int(K.ackley)], [6, 8, 6], perm, 100.0)
+    base = evb.ProblemInstance.base(K.griewank, *O.shift_rotation(62, D), 0.0)
+    s3, m3 = O.composition_components(77, D)
+    comp = evb.ProblemInstance.composition(O.CONFIG4_KINDS, s3, m3, O.CONFIG4_SIGMA, O.CONFIG4_LAMBDA, O.CONFIG4_BIAS,
+                                           0.0)
+    suite = [[hyb], [base], [comp]]
+    out = []
+    for force in (False, True):
+        rec = BestSoFarRecorder(3 * runs, max_fes, P)
+        res = evo_bench_de(preset_de(0.5, 0.9), P, suite, runs, max_fes, master_seed=21, recorder=rec,
+                           force_engine=force)
+        assert res["path"] == ("engine" if force else "batched")
+        out.append((rec.grid()[0], res["best"]))
+    (g0, b0), (g1, b1) = out
+    assert np.allclose(g0, g1, rtol=1e-12, atol=0) and np.allclose(b0, b1, rtol=1e-12, atol=0)
