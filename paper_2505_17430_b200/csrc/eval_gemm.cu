@@ -379,6 +379,8 @@ __global__ void __launch_bounds__(f64_cfg<BM, BN, WM, WN, STAGES>::THREADS, MINB
   }
 
   // park the accumulator tile in the (drained) stage ring, then run the epilogue from smem
+  // (measured: a register-direct epilogue — quad shuffles on the DMMA fragments, no parking —
+  // was slower, 89 vs 81.6 us per batch: the inlined transcendental code bloats the kernel)
   ptx::named_bar_sync(1, C::NCW * 32);
   double* zt = reinterpret_cast<double*>(smem);
   constexpr int LDT = BN + 1;
