@@ -104,6 +104,28 @@ __device__ __forceinline__ double clip_or_mid(double v, double target, double lb
 // thread.  Base values and composition weights are sequential per individual (exact order).
 // Q dot products z[i][r] = sum_k M[r][k] s[i][k] of one row r (individuals i0, i0 + G, ...),
 // accumulated in the reference's order (separate mul and add, increasing k).
+// Q dot products z[i][r] = sum_k M[r][k] s[i][k] of row r, individuals i0, i0 + G, ... (the first
+// n <= Q are real), accumulated in the reference's order (separate mul and add, increasing k).
+template <int Q, bool EXACT>
+__device__ __forceinline__ void dot_rows(const double* __restrict__ m, const double* __restrict__ sS, int D, int i0,
+                                         int G, int n, double* __restrict__ sZ, int r) {
+  double acc[Q];
+  const double* sp[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    acc[q] = 0.0;
+    sp[q] = sS + (i0 + (EXACT ? q : min(q, n - 1)) * G) * D;
+  }
+  for (int k = 0; k < D; ++k) {
+    const double mk = m[k];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(mk, sp[q][k]));
+  }
+#pragma unroll
+  for (int q = 0; q < Q; ++q)
+    if (EXACT || q < n) sZ[(i0 + q * G) * D + r] = acc[q];
+}
+
 __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int D, int S, double* sMbase,
                               double* sZ, double* sS, double* sObase, double* sFk, double* sDist, double* f,
                               bool resident, phase_clock& pc) {
@@ -124,48 +146,26 @@ __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int
     __syncthreads();
     pc.mark(2);
     {
-      // register blocking: thread (g, r) owns row r of M (lanes over rows: conflict-free, odd
-      // stride) and individuals g, g + NG, ... 8 at a time, whose s[i][k] are warp-broadcast loads
-      const int RP = (D + 31) / 32 * 32;           // threads per row group
-      const int NG = max(1, int(blockDim.x) / RP);  // individual groups
-      const int r = int(threadIdx.x) % RP, g = int(threadIdx.x) / RP;
-      // dist^2 in double (problems/instance.hpp:127-134), a sequential chain per individual, runs
-      // on the lanes the row mapping leaves idle (r >= D) so it overlaps the dot products
-      const int n_idle = NG * (RP - D) + max(0, int(blockDim.x) - NG * RP);
-      const int idle_id = g < NG ? (r >= D ? g * (RP - D) + (r - D) : -1) : NG * (RP - D) + int(threadIdx.x) - NG * RP;
-      if (pr.n_comp > 0) {
-        const bool idle_path = n_idle * 4 >= P;
-        const int id = idle_path ? idle_id : int(threadIdx.x);
-        const int stride = idle_path ? n_idle : int(blockDim.x);
-        if (id >= 0)
-          for (int i = id; i < P; i += stride) {
-            double d2 = 0.0;
-            const double* si = sS + i * D;
-            for (int j = 0; j < D; ++j) d2 = __dadd_rn(d2, __dmul_rn(si[j], si[j]));
-            sDist[i * kRunsMaxComp + c] = d2;
-          }
-      }
-      if (r < D && g < NG) {
+      // dist^2 in double (problems/instance.hpp:127-134): one sequential chain per individual
+      if (pr.n_comp > 0)
+        for (int i = threadIdx.x; i < P; i += blockDim.x) {
+          double d2 = 0.0;
+          const double* si = sS + i * D;
+          for (int j = 0; j < D; ++j) d2 = __dadd_rn(d2, __dmul_rn(si[j], si[j]));
+          sDist[i * kRunsMaxComp + c] = d2;
+        }
+      // thread t owns row r = t % D for individual group g = t / D (G groups): individuals g,
+      // g + G, ... — rows over consecutive lanes (odd stride: conflict-free), every chain real
+      const int G = max(1, int(blockDim.x) / D);
+      const int t = int(threadIdx.x);
+      if (t < G * D) {
+        const int r = t % D, g = t / D;
         const double* m = sM + r * S;
-        for (int i0 = g; i0 < P; i0 += 8 * NG) {
-          double acc[8];
-          const double* sp[8];
-          int n = 0;
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int i = i0 + q * NG;
-            acc[q] = 0.0;
-            sp[q] = sS + min(i, P - 1) * D;
-            n += i < P ? 1 : 0;
-          }
-          for (int k = 0; k < D; ++k) {
-            const double mk = m[k];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(mk, sp[q][k]));
-          }
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (q < n) sZ[(i0 + q * NG) * D + r] = acc[q];
+        for (int i0 = g; i0 < P; i0 += 8 * G) {
+          const int n = min(8, (P - i0 + G - 1) / G);
+          if (n == 8) dot_rows<8, true>(m, sS, D, i0, G, n, sZ, r);
+          else if (n == 5) dot_rows<5, true>(m, sS, D, i0, G, n, sZ, r);
+          else dot_rows<8, false>(m, sS, D, i0, G, n, sZ, r);
         }
       }
     }
