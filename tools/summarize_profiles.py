@@ -100,9 +100,10 @@ def main():
     lc = SRC / "bench_launches.csv"
     if lc.exists():
         shutil.copy(lc, DST / f"bench_launches_{tag}.csv")
-    rep = SRC / "eval_f64.ncu-rep"
-    if rep.exists():
-        shutil.copy(rep, DST / f"eval_f64_{tag}.ncu-rep")
+    for name in ("eval_f64", "eval_f32", "runs", "updates", "pso_update"):
+        rep = SRC / f"{name}.ncu-rep"
+        if rep.exists():
+            shutil.copy(rep, DST / f"{name}_{tag}.ncu-rep")
     for f in ("hbm_plain.json", "bench_plain.log"):
         if (SRC / f).exists():
             shutil.copy(SRC / f, DST / f"{Path(f).stem}_{tag}{Path(f).suffix}")
