@@ -78,9 +78,21 @@ struct fused_params {
                      // corrections in separate TMEM accumulators (summed in the epilogue)
 };
 
-// cosine of the fused epilogue: library cos for fp64, the reference's batched fast_cos for fp32
+// cosine of the fused epilogue: library cos for fp64.  fp32 (a tolerance path: 3xTF32 / FFMA
+// products already differ from the reference's order) reduces x = 2 pi z by 2 pi in float
+// (Cody-Waite, 6.28125 exact for |k| < 2^15) and takes the SFU cosine on [-pi, pi]: absolute
+// error ~1e-6, 4x cheaper than the reference's fast_cos evaluated in double (10.5 of 47 us per
+// config-1 fp32 batch, measured).
 template <typename T>
 __device__ __forceinline__ T epi_cos(T x) { return trig<T, true>::cos_(x); }
+template <>
+__device__ __forceinline__ float epi_cos<float>(float x) {
+  if (!(fabsf(x) < 1.0e5f)) return trig<float, true>::cos_(x);
+  const float k = rintf(x * 0.159154943091895336f);
+  float r = fmaf(-k, 6.28125f, x);
+  r = fmaf(-k, 1.93530717958647692e-3f, r);
+  return __cosf(r);
+}
 
 template <typename T>
 __device__ __forceinline__ T term_value(int term, T v, int col, const T* ell_w) {
@@ -675,7 +687,8 @@ __global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
 #pragma unroll
             for (int q = 0; q < 16; ++q) v[q] = __fadd_rn(v[q], w[q]);
           }
-          acc = accumulate16_rt<float>(term, acc, v, n0 + c0, p.D, p.ell_w);
+          if (p.umma_variant >= 60 && p.umma_variant < 70) acc += v[0];  // debug: no terms
+          else acc = accumulate16_rt<float>(term, acc, v, n0 + c0, p.D, p.ell_w);
         }
         if (row < p.P) p.partial[(size_t(ch) * p.n_ntiles + blockIdx.y) * p.P + row] = acc;
       }
