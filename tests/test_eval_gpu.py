@@ -233,3 +233,30 @@ def test_host_path_overlapped_copy_bit_identical(config1, dev, kind):
     wide[:, :1000] = X[:64]
     got = evb.batched_evaluate(p, wide[:, :1000], sc)
     assert np.array_equal(got, want[64])
+
+
+SWEEP = [(159, 63), (160, 65), (161, 1), (161, 300), (255, 129), (256, 64), (257, 65), (1003, 7), (2049, 65)]
+
+
+@pytest.mark.parametrize("dim,n", SWEEP)
+@pytest.mark.parametrize("dtype", [evb.EVB_F64, evb.EVB_F32])
+def test_shape_sweep_path_boundaries(dev, dim, n, dtype):
+    # around the small-D / GEMM switch (D = 160), the tile edges (56 / 64 / 128 / 32-float K-slices)
+    # and ragged batches: every path against the C restatement; multi-output fused epilogue too
+    o, m = O.shift_rotation(900 + dim, dim)
+    X = O.population(901 + dim, n, dim)
+    nd = np.float64 if dtype == evb.EVB_F64 else np.float32
+    o, m, X = o.astype(nd), m.astype(nd), X.astype(nd)
+    tol = 1e-10 if dtype == evb.EVB_F64 else 1e-4
+    kinds = [K.elliptic, K.rastrigin, K.ackley, K.griewank]
+    for kind in kinds:
+        p = evb.ProblemInstance.base(kind, o, m, 7.0, dtype=dtype)
+        assert rel_err(gpu_eval(p, X, dev), O.eval_batch(int(kind), o, m, 7.0, X)) <= tol, (kind, dim, n)
+    p = evb.ProblemInstance.base(K.sphere, o, m, 0.0, dtype=dtype)
+    Xd = torch.from_numpy(np.ascontiguousarray(X)).to(dev)
+    out = torch.empty((3, n), dtype=Xd.dtype, device=dev)
+    evb.evaluate_batch_multi(p, [int(K.elliptic), int(K.rastrigin), int(K.ackley)], [1.0, 2.0, 3.0], Xd,
+                             evb.EvalScratch(), out)
+    got = out.cpu().numpy()
+    for r, (kind, b) in enumerate(((K.elliptic, 1.0), (K.rastrigin, 2.0), (K.ackley, 3.0))):
+        assert rel_err(got[r], O.eval_batch(int(kind), o, m, b, X)) <= tol, ("multi", kind, dim, n)
