@@ -382,132 +382,172 @@ int evb_evaluate_batch_multi(evb_problem p, evb_scratch s, int n_kinds, const in
   });
 }
 
-int evb_evaluate_batch_host(evb_problem p, evb_scratch s, const void* X_host, int64_t n_points, int64_t ldx,
-                            void* out_host) {
-  return guarded([&] {
-    validate_eval(p, s, n_points, ldx);
-    if (n_points == 0) return;
-    if (!X_host || !out_host) throw config_error("evaluate_batch_host: null X or out");
-    if (!s->own_stream) EVB_CUDA(cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking));
-    cudaStream_t st = s->own_stream;
-    const size_t es = elem_size(p->p.dtype);
-    const int64_t D = p->p.dim;
-    const int64_t ldd = round_up(D, 16 / int64_t(es));
-    ensure_buffer(&s->dx, &s->dx_bytes, size_t(ldd) * n_points * es, st);
-    ensure_buffer(&s->dout, &s->dout_bytes, size_t(n_points) * es, st);
+}  // extern "C"
+
+namespace {
+
+// Host-buffer evaluation of one population on n_prob problems (same dim / dtype): X crosses the
+// host link once; the first problem's fused GEMM consumes it chunk by chunk as it lands, the
+// others run on the resident copy; each out_host[k] gets problem k's fitness.
+void host_eval(const evb_problem* probs, int n_prob, evb_scratch s, const void* X_host, int64_t n_points, int64_t ldx,
+               void* const* outs_host) {
+  require(probs != nullptr && n_prob >= 1 && outs_host != nullptr, "evaluate_batch_host: null problems or outputs");
+  evb_problem p = probs[0];
+  validate_eval(p, s, n_points, ldx);
+  for (int k = 1; k < n_prob; ++k) {
+    validate_eval(probs[k], s, n_points, ldx);
+    if (probs[k]->p.dim != p->p.dim || probs[k]->p.dtype != p->p.dtype)
+      throw invalid_argument("evaluate_batch_host: problems differ in dimension or dtype");
+  }
+  if (n_points == 0) return;
+  if (!X_host) throw config_error("evaluate_batch_host: null X or out");
+  for (int k = 0; k < n_prob; ++k)
+    if (!outs_host[k]) throw config_error("evaluate_batch_host: null X or out");
+  if (!s->own_stream) EVB_CUDA(cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking));
+  cudaStream_t st = s->own_stream;
+  const size_t es = elem_size(p->p.dtype);
+  const int64_t D = p->p.dim;
+  const int64_t ldd = round_up(D, 16 / int64_t(es));
+  ensure_buffer(&s->dx, &s->dx_bytes, size_t(ldd) * n_points * es, st);
+  ensure_buffer(&s->dout, &s->dout_bytes, size_t(n_points) * es * n_prob, st);
+  // Page-locked outputs (cudaHostAlloc / cudaHostRegister) are written by the kernels directly
+  // (mapped, same address under UVA): no device staging and no D2H copy at the end.
+  std::vector<void*> dst(n_prob);
+  for (int k = 0; k < n_prob; ++k) {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, outs_host[k]) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+        pa.devicePointer == outs_host[k])
+      dst[k] = outs_host[k];
+    else {
+      cudaGetLastError();
+      dst[k] = static_cast<uint8_t*>(s->dout) + size_t(k) * n_points * es;
+    }
+  }
+  auto request = [&](int k) {
     eval_request rq{};
-    rq.prob = &p->p;
+    rq.prob = &probs[k]->p;
     rq.scratch = s;
     rq.X = s->dx;
     rq.n = n_points;
     rq.ldx = ldd;
-    rq.out = s->dout;
+    rq.out = dst[k];
     rq.ldo = n_points;
     rq.n_out = 1;
-    rq.kinds[0] = p->p.kind;
-    rq.biases[0] = p->p.bias;
+    rq.kinds[0] = probs[k]->p.kind;
+    rq.biases[0] = probs[k]->p.bias;
     rq.stream = st;
-    // Page-locked `out` (cudaHostAlloc / cudaHostRegister) is written by the kernel directly
-    // (mapped, same address under UVA): no device staging and no D2H copy at the end.
-    cudaPointerAttributes pa{};
-    if (cudaPointerGetAttributes(&pa, out_host) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
-        pa.devicePointer == out_host)
-      rq.out = out_host;
-    else
-      cudaGetLastError();
-    // The fused fp64 GEMM starts while X is still crossing the host link: X goes over in column
-    // chunks on a second stream, each chunk followed by a stream write of its gate word, and the
-    // GEMM producer waits per chunk before its TMA loads (the copy is the e2e bound: ~8 MB per
-    // batch at D=1000, P=1024).  All copies are enqueued before the kernel, so the kernel only
-    // ever waits on work queued ahead of it.  Other paths copy X whole, then launch.
-    rq.X = s->dx;
-    rq.ldx = ldd;
-    static const char* chunks_env = std::getenv("EVB_H2D_CHUNKS");
-    static const char* split_env = std::getenv("EVB_H2D_SPLIT");
-    const int want = std::min(kMaxGates, chunks_env ? std::max(1, std::atoi(chunks_env)) : 4);
-    const bool geometric = !(split_env && std::string(split_env) == "uniform");
-    write_value32_fn wv = stream_write_value32();
-    if (want > 1 && wv && gate_eligible(rq)) {
-      if (!s->copy_stream) EVB_CUDA(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
-      if (!s->gate_stream) EVB_CUDA(cudaStreamCreateWithFlags(&s->gate_stream, cudaStreamNonBlocking));
-      if (!s->ev_x_ready) EVB_CUDA(cudaEventCreateWithFlags(&s->ev_x_ready, cudaEventDisableTiming));
-      for (auto& e : s->ev_chunk)
-        if (!e) EVB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      if (!s->gate) {
-        EVB_CUDA(cudaMalloc(&s->gate, kMaxGates * sizeof(unsigned)));
-        EVB_CUDA(cudaMemset(s->gate, 0, kMaxGates * sizeof(unsigned)));
-      }
-      // chunk boundaries (multiples of 16 columns = the GEMM's K-slice): uniform, or halving
-      // so the compute left after the last chunk lands is small
-      int n_chunks = 0;
-      int64_t c0 = 0;
-      while (c0 < D) {
-        int64_t w;
-        if (n_chunks == want - 1) w = D - c0;
-        else if (geometric) w = round_up((D - c0 + 1) / 2, 16);
-        else w = round_up((D + want - 1) / want, 16);
-        w = std::min<int64_t>(std::max<int64_t>(w, 16), D - c0);
-        rq.kgate_end[n_chunks++] = int(c0 + w);
-        c0 += w;
-      }
-      rq.kgate_n = n_chunks;
-      const unsigned epoch = ++s->gate_epoch == 0 ? ++s->gate_epoch : s->gate_epoch;
-      // EVB_H2D_TRACE=1: print the copy / kernel timeline of each call (tuning aid)
-      static const bool trace = std::getenv("EVB_H2D_TRACE") != nullptr;
-      static cudaEvent_t tev[kMaxGates + 3];
-      if (trace && !tev[0])
-        for (auto& e : tev) EVB_CUDA(cudaEventCreate(&e));
-      if (trace) EVB_CUDA(cudaEventRecord(tev[0], s->copy_stream));
-      // the previous call on this scratch synchronised st, so dx is free to overwrite
-      bool gates_ok = true;
-      for (int c = 0; c < n_chunks; ++c) {
-        const int64_t b = c ? rq.kgate_end[c - 1] : 0, w = rq.kgate_end[c] - b;
-        EVB_CUDA(cudaMemcpy2DAsync(static_cast<uint8_t*>(s->dx) + b * es, ldd * es,
-                                   static_cast<const uint8_t*>(X_host) + b * es, ldx * es, w * es, n_points,
-                                   cudaMemcpyHostToDevice, s->copy_stream));
-        if (gates_ok) {
-          EVB_CUDA(cudaEventRecord(s->ev_chunk[c], s->copy_stream));
-          EVB_CUDA(cudaStreamWaitEvent(s->gate_stream, s->ev_chunk[c], 0));
-          // a driver that refuses stream memory operations: fall back to waiting for all of X
-          gates_ok = wv(s->gate_stream, CUdeviceptr(s->gate + c), epoch, 0) == CUDA_SUCCESS;
-        }
-        if (trace) EVB_CUDA(cudaEventRecord(tev[1 + c], s->copy_stream));
-      }
-      EVB_CUDA(cudaEventRecord(s->ev_x_ready, s->copy_stream));
-      rq.kgate = gates_ok ? s->gate : nullptr;
-      rq.kgate_epoch = epoch;
-      rq.x_ready = s->ev_x_ready;
-      if (trace) EVB_CUDA(cudaStreamWaitEvent(st, tev[0], 0));
-      eval_dispatch(rq);
-      if (trace) EVB_CUDA(cudaEventRecord(tev[n_chunks + 1], st));
-      EVB_CUDA(cudaStreamWaitEvent(st, s->ev_x_ready, 0));
-      if (trace) {
-        if (rq.out != out_host)
-          EVB_CUDA(cudaMemcpyAsync(out_host, s->dout, size_t(n_points) * es, cudaMemcpyDeviceToHost, st));
-        EVB_CUDA(cudaEventRecord(tev[n_chunks + 2], st));
-        EVB_CUDA(cudaStreamSynchronize(st));
-        std::string line = "[evb h2d]";
-        for (int c = 1; c <= n_chunks + 2; ++c) {
-          float ms = 0.f;
-          cudaEventElapsedTime(&ms, tev[0], tev[c]);
-          line += (c == n_chunks + 1 ? " kernel_end " : c == n_chunks + 2 ? " d2h_end " : " ") +
-                  std::to_string(int(ms * 1000.f));
-        }
-        std::fprintf(stderr, "%s us\n", line.c_str());
-      }
-    } else {
-      // one linear copy when the rows are packed (the DMA engines run 2D copies of wide rows at
-      // about half the rate of a linear copy of the same bytes: 300 vs 160 us for 8 MB)
-      if (ldx == ldd)
-        EVB_CUDA(cudaMemcpyAsync(s->dx, X_host, size_t(ldd) * n_points * es, cudaMemcpyHostToDevice, st));
-      else
-        EVB_CUDA(cudaMemcpy2DAsync(s->dx, ldd * es, X_host, ldx * es, D * es, n_points, cudaMemcpyHostToDevice, st));
-      eval_dispatch(rq);
+    return rq;
+  };
+  eval_request rq = request(0);
+  // The fused fp64 GEMM starts while X is still crossing the host link: X goes over in column
+  // chunks on a second stream, each chunk followed by a stream write of its gate word, and the
+  // GEMM producer waits per chunk before its TMA loads (the copy is the e2e bound: ~8 MB per
+  // batch at D=1000, P=1024).  All copies are enqueued before the kernel, so the kernel only
+  // ever waits on work queued ahead of it.  Other paths copy X whole, then launch.
+  rq.X = s->dx;
+  rq.ldx = ldd;
+  static const char* chunks_env = std::getenv("EVB_H2D_CHUNKS");
+  static const char* split_env = std::getenv("EVB_H2D_SPLIT");
+  const int want = std::min(kMaxGates, chunks_env ? std::max(1, std::atoi(chunks_env)) : 4);
+  const bool geometric = !(split_env && std::string(split_env) == "uniform");
+  write_value32_fn wv = stream_write_value32();
+  if (want > 1 && wv && gate_eligible(rq)) {
+    if (!s->copy_stream) EVB_CUDA(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
+    if (!s->gate_stream) EVB_CUDA(cudaStreamCreateWithFlags(&s->gate_stream, cudaStreamNonBlocking));
+    if (!s->ev_x_ready) EVB_CUDA(cudaEventCreateWithFlags(&s->ev_x_ready, cudaEventDisableTiming));
+    for (auto& e : s->ev_chunk)
+      if (!e) EVB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    if (!s->gate) {
+      EVB_CUDA(cudaMalloc(&s->gate, kMaxGates * sizeof(unsigned)));
+      EVB_CUDA(cudaMemset(s->gate, 0, kMaxGates * sizeof(unsigned)));
     }
-    if (rq.out != out_host)
-      EVB_CUDA(cudaMemcpyAsync(out_host, s->dout, size_t(n_points) * es, cudaMemcpyDeviceToHost, st));
-    EVB_CUDA(cudaStreamSynchronize(st));
-  });
+    // chunk boundaries (multiples of 16 columns = the GEMM's K-slice): uniform, or halving
+    // so the compute left after the last chunk lands is small
+    int n_chunks = 0;
+    int64_t c0 = 0;
+    while (c0 < D) {
+      int64_t w;
+      if (n_chunks == want - 1) w = D - c0;
+      else if (geometric) w = round_up((D - c0 + 1) / 2, 16);
+      else w = round_up((D + want - 1) / want, 16);
+      w = std::min<int64_t>(std::max<int64_t>(w, 16), D - c0);
+      rq.kgate_end[n_chunks++] = int(c0 + w);
+      c0 += w;
+    }
+    rq.kgate_n = n_chunks;
+    const unsigned epoch = ++s->gate_epoch == 0 ? ++s->gate_epoch : s->gate_epoch;
+    // EVB_H2D_TRACE=1: print the copy / kernel timeline of each call (tuning aid)
+    static const bool trace = std::getenv("EVB_H2D_TRACE") != nullptr;
+    static cudaEvent_t tev[kMaxGates + 3];
+    if (trace && !tev[0])
+      for (auto& e : tev) EVB_CUDA(cudaEventCreate(&e));
+    if (trace) EVB_CUDA(cudaEventRecord(tev[0], s->copy_stream));
+    // the previous call on this scratch synchronised st, so dx is free to overwrite
+    bool gates_ok = true;
+    for (int c = 0; c < n_chunks; ++c) {
+      const int64_t b = c ? rq.kgate_end[c - 1] : 0, w = rq.kgate_end[c] - b;
+      EVB_CUDA(cudaMemcpy2DAsync(static_cast<uint8_t*>(s->dx) + b * es, ldd * es,
+                                 static_cast<const uint8_t*>(X_host) + b * es, ldx * es, w * es, n_points,
+                                 cudaMemcpyHostToDevice, s->copy_stream));
+      if (gates_ok) {
+        EVB_CUDA(cudaEventRecord(s->ev_chunk[c], s->copy_stream));
+        EVB_CUDA(cudaStreamWaitEvent(s->gate_stream, s->ev_chunk[c], 0));
+        // a driver that refuses stream memory operations: fall back to waiting for all of X
+        gates_ok = wv(s->gate_stream, CUdeviceptr(s->gate + c), epoch, 0) == CUDA_SUCCESS;
+      }
+      if (trace) EVB_CUDA(cudaEventRecord(tev[1 + c], s->copy_stream));
+    }
+    EVB_CUDA(cudaEventRecord(s->ev_x_ready, s->copy_stream));
+    rq.kgate = gates_ok ? s->gate : nullptr;
+    rq.kgate_epoch = epoch;
+    rq.x_ready = s->ev_x_ready;
+    if (trace) EVB_CUDA(cudaStreamWaitEvent(st, tev[0], 0));
+    eval_dispatch(rq);
+    if (trace) EVB_CUDA(cudaEventRecord(tev[n_chunks + 1], st));
+    EVB_CUDA(cudaStreamWaitEvent(st, s->ev_x_ready, 0));
+    if (trace) {
+      if (dst[0] != outs_host[0])
+        EVB_CUDA(cudaMemcpyAsync(outs_host[0], dst[0], size_t(n_points) * es, cudaMemcpyDeviceToHost, st));
+      EVB_CUDA(cudaEventRecord(tev[n_chunks + 2], st));
+      EVB_CUDA(cudaStreamSynchronize(st));
+      std::string line = "[evb h2d]";
+      for (int c = 1; c <= n_chunks + 2; ++c) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, tev[0], tev[c]);
+        line += (c == n_chunks + 1 ? " kernel_end " : c == n_chunks + 2 ? " d2h_end " : " ") +
+                std::to_string(int(ms * 1000.f));
+      }
+      std::fprintf(stderr, "%s us\n", line.c_str());
+    }
+  } else {
+    // one linear copy when the rows are packed (the DMA engines run 2D copies of wide rows at
+    // about half the rate of a linear copy of the same bytes: 300 vs 160 us for 8 MB)
+    if (ldx == ldd)
+      EVB_CUDA(cudaMemcpyAsync(s->dx, X_host, size_t(ldd) * n_points * es, cudaMemcpyHostToDevice, st));
+    else
+      EVB_CUDA(cudaMemcpy2DAsync(s->dx, ldd * es, X_host, ldx * es, D * es, n_points, cudaMemcpyHostToDevice, st));
+    eval_dispatch(rq);
+  }
+  // the remaining problems evaluate the resident copy (the stream already waits for all of X)
+  for (int k = 1; k < n_prob; ++k) eval_dispatch(request(k));
+  for (int k = 0; k < n_prob; ++k)
+    if (dst[k] != outs_host[k])
+      EVB_CUDA(cudaMemcpyAsync(outs_host[k], dst[k], size_t(n_points) * es, cudaMemcpyDeviceToHost, st));
+  EVB_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace
+
+extern "C" {
+
+int evb_evaluate_batch_host(evb_problem p, evb_scratch s, const void* X_host, int64_t n_points, int64_t ldx,
+                            void* out_host) {
+  return guarded([&] { host_eval(&p, 1, s, X_host, n_points, ldx, &out_host); });
+}
+
+int evb_evaluate_batch_host_many(const evb_problem* problems, int n_problems, evb_scratch s, const void* X_host,
+                                 int64_t n_points, int64_t ldx, void* const* out_host) {
+  return guarded([&] { host_eval(problems, n_problems, s, X_host, n_points, ldx, out_host); });
 }
 
 int evb_launch_count(void) { return last_launch_count(); }

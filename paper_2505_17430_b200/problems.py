@@ -219,3 +219,23 @@ def batched_evaluate(problem: ProblemInstance, xs, scratch: EvalScratch | None =
     check(_lib.lib().evb_evaluate_batch_host(problem.handle, sc.handle, _ptr(x), x.shape[0], x.shape[1], _ptr(out)),
           "batched_evaluate")
     return out
+
+
+def batched_evaluate_many(problems: Sequence[ProblemInstance], xs, scratch: EvalScratch | None = None):
+    """One host population on several problems (evb_evaluate_batch_host_many): X is copied to the
+    device once; returns one fitness array per problem."""
+    if not problems:
+        return []
+    nd = _np_dtype(problems[0].dtype)
+    x = np.ascontiguousarray(xs, dtype=nd)
+    if x.size == 0:
+        return [np.zeros(0, dtype=nd) for _ in problems]
+    if x.ndim != 2 or x.shape[1] != problems[0].dim:
+        raise InvalidArgument("evaluate_batch: point dimension mismatch")
+    outs = [np.empty(x.shape[0], dtype=nd) for _ in problems]
+    handles = (ctypes.c_void_p * len(problems))(*[p.handle.value for p in problems])
+    optrs = (ctypes.c_void_p * len(problems))(*[o.ctypes.data for o in outs])
+    sc = scratch or EvalScratch()
+    check(_lib.lib().evb_evaluate_batch_host_many(handles, len(problems), sc.handle, _ptr(x), x.shape[0], x.shape[1],
+                                                  optrs), "batched_evaluate_many")
+    return outs

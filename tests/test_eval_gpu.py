@@ -260,3 +260,22 @@ def test_shape_sweep_path_boundaries(dev, dim, n, dtype):
     got = out.cpu().numpy()
     for r, (kind, b) in enumerate(((K.elliptic, 1.0), (K.rastrigin, 2.0), (K.ackley, 3.0))):
         assert rel_err(got[r], O.eval_batch(int(kind), o, m, b, X)) <= tol, ("multi", kind, dim, n)
+
+
+def test_host_many_one_copy_equals_device(config1, dev):
+    # several problems on one host population: one H2D copy, results identical to the device path
+    o, m, X = config1
+    kinds = [K.elliptic, K.rastrigin, K.ackley, K.griewank]
+    probs = [evb.ProblemInstance.base(k, o, m, float(i)) for i, k in enumerate(kinds)]
+    want = [gpu_eval(p, X, dev) for p in probs]
+    sc = evb.EvalScratch()
+    for _ in range(2):
+        got = evb.batched_evaluate_many(probs, X, sc)
+        for g, w in zip(got, want):
+            assert np.array_equal(g, w)
+    small = [evb.ProblemInstance.base(k, *O.shift_rotation(5, 30), 0.0) for k in kinds]
+    Xs = O.population(6, 17, 30)
+    for p, g in zip(small, evb.batched_evaluate_many(small, Xs, sc)):
+        assert np.array_equal(g, gpu_eval(p, Xs, dev))
+    with pytest.raises(evb.InvalidArgument):
+        evb.batched_evaluate_many([probs[0], small[0]], X, sc)
