@@ -10,7 +10,10 @@
 //   rng_stream                     core/rng.hpp:37     evb::gpu_rng (Philox / oracle word list)
 //   de::de_engine<T>               de/engine.hpp:68    evb::gpu_de_engine<T>
 //   pso::pso_engine<T>             pso/engine.hpp:33   evb::gpu_pso_engine<T>  (synchronous)
-//   evo_bench over DE runs         runner.hpp:101      evb::de_runs(...)       (one launch)
+//   pso::cso_optimizer<T>          pso/cso.hpp:19      evb::gpu_cso<T>         (exact generation)
+//   experiment::best_so_far_record recorder.hpp:35     evb::gpu_recorder<T>    (device, same CSV)
+//   experiment::evo_bench(alg, su, obs, opt)           evb::evo_bench_de / _pso / _cso
+//                                  runner.hpp:101      (all tasks of a suite; DE presets in one launch)
 //
 // Errors are rethrown as the reference's types: std::invalid_argument (dimension mismatch),
 // evb::config_error (a std::runtime_error, like evobench::config_error, common.hpp:12-15),
@@ -317,5 +320,109 @@ class gpu_pso_engine {
  private:
   evb_pso h_ = nullptr;
 };
+
+// experiment::best_so_far_record<T> on the device: engines report their evaluations in FE order;
+// grid() / to_csv() give the reference's checkpoint grid and CSV (recorder.hpp:35-155).
+template <typename T>
+class gpu_recorder {
+ public:
+  gpu_recorder(int n_runs, long long max_fes, long long interval) : runs_(n_runs) {
+    check(evb_recorder_create(dtype_of<T>(), n_runs, max_fes, interval, &h_), "recorder_create");
+  }
+  gpu_recorder(const gpu_recorder&) = delete;
+  ~gpu_recorder() {
+    if (h_) evb_recorder_destroy(h_);
+  }
+  evb_recorder handle() const { return h_; }
+  int checkpoint_count() const { return evb_recorder_checkpoints(h_); }
+  // on_evaluate for n device values of run `run`, in order
+  void observe(int run, const T* values, int64_t n, void* stream = nullptr) {
+    check(evb_recorder_observe(h_, run, values, n, stream), "recorder_observe");
+  }
+  void finish(void* stream = nullptr) { check(evb_recorder_finish(h_, 0, runs_, stream), "recorder_finish"); }
+  std::vector<T> grid() const {  // runs x checkpoints
+    std::vector<T> g(size_t(runs_) * checkpoint_count());
+    check(evb_recorder_grid(h_, g.data(), nullptr), "recorder_grid");
+    return g;
+  }
+  std::string to_csv(const std::string& suite_name, int dim, const std::vector<int>& problem_ids, int instances,
+                     int runs) const {
+    int64_t n = 0;
+    check(evb_recorder_csv(h_, suite_name.c_str(), dim, int(problem_ids.size()), problem_ids.data(), instances, runs,
+                           nullptr, 0, &n),
+          "recorder_csv");
+    std::string out(size_t(n), '\0');
+    check(evb_recorder_csv(h_, suite_name.c_str(), dim, int(problem_ids.size()), problem_ids.data(), instances, runs,
+                           out.data(), n, &n),
+          "recorder_csv");
+    return out;
+  }
+
+ private:
+  evb_recorder h_ = nullptr;
+  int runs_;
+};
+
+// pso::cso_optimizer<T>(phi): the device generation is the reference's generation
+template <typename T>
+class gpu_cso {
+ public:
+  gpu_cso(double phi, int pop_size, int dim) { check(evb_cso_create(dtype_of<T>(), phi, pop_size, dim, &h_), "cso_create"); }
+  gpu_cso(const gpu_cso&) = delete;
+  ~gpu_cso() {
+    if (h_) evb_cso_destroy(h_);
+  }
+  void generation(const gpu_problem<T>& objective, T* X, int64_t ldx, T* V, int64_t ldv, T* fitness, T lb, T ub,
+                  gpu_rng& rng, void* stream = nullptr) {
+    check(evb_cso_generation(h_, objective.handle(), nullptr, X, ldx, V, ldv, fitness, double(lb), double(ub),
+                             rng.handle(), stream),
+          "cso_generation");
+  }
+  double optimize(const gpu_problem<T>& objective, T* X, int64_t ldx, T* V, int64_t ldv, T* fitness, T lb, T ub,
+                  long long max_fes, gpu_rng& rng, void* stream = nullptr) {
+    int bi = 0, g = 0;
+    double bf = 0;
+    check(evb_cso_optimize(h_, objective.handle(), nullptr, X, ldx, V, ldv, fitness, double(lb), double(ub), max_fes,
+                           rng.handle(), &bi, &bf, &g, stream),
+          "cso_optimize");
+    return bf;
+  }
+
+ private:
+  evb_cso h_ = nullptr;
+};
+
+// experiment::evo_bench over a suite (instances[p * instance_count + i] = suite.at(p, i)) with a
+// recorder (may be null); returns each task's best fitness (task ((p * I) + i) * runs + r)
+template <typename T>
+std::vector<double> evo_bench_de(const evb_de_config& cfg, int pop_size, const std::vector<const gpu_problem<T>*>& instances,
+                                 int problem_count, int runs, long long max_fes, uint64_t seed, T lb, T ub,
+                                 gpu_recorder<T>* rec = nullptr) {
+  std::vector<evb_problem> h;
+  for (const auto* p : instances) h.push_back(p->handle());
+  const int instance_count = int(h.size()) / problem_count;
+  std::vector<double> best(h.size() * size_t(runs));
+  int path = 0;
+  check(evb_evo_bench_de(dtype_of<T>(), &cfg, pop_size, instances.front()->dim(), h.data(), problem_count,
+                         instance_count, runs, max_fes, seed, double(lb), double(ub), rec ? rec->handle() : nullptr,
+                         nullptr, best.data(), 0, &path, nullptr),
+        "evo_bench_de");
+  return best;
+}
+
+template <typename T>
+std::vector<double> evo_bench_cso(double phi, int pop_size, const std::vector<const gpu_problem<T>*>& instances,
+                                  int problem_count, int runs, long long max_fes, uint64_t seed, T lb, T ub,
+                                  gpu_recorder<T>* rec = nullptr) {
+  std::vector<evb_problem> h;
+  for (const auto* p : instances) h.push_back(p->handle());
+  const int instance_count = int(h.size()) / problem_count;
+  std::vector<double> best(h.size() * size_t(runs));
+  check(evb_evo_bench_cso(dtype_of<T>(), phi, pop_size, instances.front()->dim(), h.data(), problem_count,
+                          instance_count, runs, max_fes, seed, double(lb), double(ub), rec ? rec->handle() : nullptr,
+                          best.data(), nullptr),
+        "evo_bench_cso");
+  return best;
+}
 
 }  // namespace evb

@@ -9,6 +9,10 @@
 
 #include "evb/evb.hpp"
 #include "evb/evobench_adapter.hpp"
+#include "evobench/experiment/recorder.hpp"
+#include "evobench/experiment/runner.hpp"
+#include "evobench/pso/cso.hpp"
+#include "evobench/presets.hpp"
 #include "evobench/core/rng.hpp"
 #include "evobench/de/engine.hpp"
 #include "evobench/presets.hpp"
@@ -114,6 +118,62 @@ int main() {
     for (int i = 0; i < P; ++i)
       for (int j = 0; j < D; ++j) same = same && hp[size_t(i) * D + j] == pop[i].genome[size_t(j)];
     report("DE rand/1/bin 20 generations on rng_stream(42, 0): bit-exact population", same);
+  }
+  // A whole experiment on the device: experiment::evo_bench with the `cso` preset over a registry
+  // suite (transcendental-free problems, so every evaluation is bit-exact), recorded by the device
+  // best_so_far_record, against the reference's own evo_bench + best_so_far_record where each task
+  // replays the words of the GPU task's positional Philox stream.
+  {
+    const int D = 10, P = 20, runs = 2;
+    const long long max_fes = P + 12 * (P / 2) + 5, interval = 25;
+    const uint64_t seed = 77;
+    const double phi = 0.1;
+    auto su = problems::suite_builder<double>().name("cec").dim(D).problem_ids({1, 2, 3, 7}).instance_count(2).seed(9).build();
+    std::vector<evb::gpu_problem<double>> gpu;
+    for (int p = 0; p < su.problem_count(); ++p)
+      for (int i = 0; i < su.instance_count(); ++i) gpu.push_back(evb::adapt::to_gpu(su.at(p, i)));
+    std::vector<const evb::gpu_problem<double>*> inst;
+    for (const auto& g : gpu) inst.push_back(&g);
+    const int tasks = su.problem_count() * su.instance_count() * runs;
+    evb::gpu_recorder<double> grec(tasks, max_fes, interval);
+    auto gbest = evb::evo_bench_cso<double>(phi, P, inst, su.problem_count(), runs, max_fes, seed, -100.0, 100.0, &grec);
+    const std::string gcsv = grec.to_csv(su.name(), D, su.problem_ids(), su.instance_count(), runs);
+
+    // words each task consumes: init_population, then per generation the P-1 Fisher-Yates draws
+    // (sub-stream 0xFFFFFFFD) and pair t's 3*D gene draws (sub-stream t)
+    const int gens = int((max_fes - P + P / 2 - 1) / (P / 2));
+    auto words_of = [&](int64_t t) {
+      const uint64_t key = evb_task_key(seed, uint64_t(t));
+      std::vector<uint64_t> w(size_t(P) * D);
+      evb::check(evb_philox_words(key, 0xFFFFFFF0ull, 0, int64_t(P) * D, w.data()), "philox_words");
+      for (uint64_t g = 1; g <= uint64_t(gens); ++g) {
+        std::vector<uint64_t> part(size_t(P - 1));
+        evb::check(evb_philox_words(key, (g << 32) | 0xFFFFFFFDull, 0, P - 1, part.data()), "philox_words");
+        w.insert(w.end(), part.begin(), part.end());
+        for (uint64_t pr = 0; pr < uint64_t(P / 2); ++pr) {
+          std::vector<uint64_t> q(size_t(3) * D);
+          evb::check(evb_philox_words(key, (g << 32) | pr, 0, 3 * D, q.data()), "philox_words");
+          w.insert(w.end(), q.begin(), q.end());
+        }
+      }
+      return w;
+    };
+    experiment::best_so_far_record<double> rrec(su, runs, max_fes, interval);
+    experiment::bench_options opt;
+    opt.independent_runs = runs;
+    opt.max_fes = max_fes;
+    opt.master_seed = seed;
+    std::vector<double> rbest(static_cast<size_t>(tasks));
+    auto alg = [&](experiment::run_handle<double>& h) {
+      const auto& k = h.key();
+      const int64_t t = (int64_t(k.problem_ordinal) * su.instance_count() + k.instance_ordinal) * runs + k.run_index;
+      rng_stream rng = rng_stream::scripted(words_of(t));
+      pso::cso_optimizer<double> engine{phi};
+      rbest[size_t(t)] = engine.optimize(h, h.lb(), h.ub(), P, D, max_fes, rng).fitness;
+    };
+    experiment::evo_bench<double>(alg, su, rrec, opt);
+    report("evo_bench cso over a registry suite: device recorder CSV == reference CSV", gcsv == rrec.to_csv());
+    report("evo_bench cso: best per task equal", gbest == rbest);
   }
   std::printf("%d failure(s)\n", failures);
   return failures;
