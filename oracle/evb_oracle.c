@@ -843,3 +843,43 @@ ORC_API void orc_make_composition(uint64_t seed, uint64_t stream_id, int dim, in
     orc_random_rotation(&r, dim, rots + (size_t)c * dim * dim);
   }
 }
+
+/* ---- cso_optimizer::generation (pso/cso.hpp:31-72), fp64, base objective ------------------------ */
+/* x, v: P x D (row-major), fit: P; words consumed in the reference's order (scripted rng).  The
+ * losers' new fitness uses the scalar path (problems/instance.hpp:221-233).  Returns words used. */
+ORC_API int64_t orc_cso_generation_f64(int P, int D, double phi, int kind, const double* shift, const double* rot,
+                                       double bias, double* x, double* v, double* fit, double lb, double ub,
+                                       const uint64_t* words, int64_t n_words) {
+  orc_rng r;
+  orc_rng_scripted(&r, words, n_words);
+  double* mean = (double*)calloc((size_t)D, sizeof(double));
+  int* perm = (int*)malloc(sizeof(int) * (size_t)P);
+  for (int i = 0; i < P; ++i)
+    for (int j = 0; j < D; ++j) mean[j] += x[(size_t)i * D + j]; /* cso.hpp:37-40, i ascending */
+  for (int j = 0; j < D; ++j) mean[j] /= (double)P;              /* :41-42 */
+  for (int i = 0; i < P; ++i) perm[i] = i;                        /* iota, :44 */
+  for (int k = P - 1; k >= 1; --k) {                              /* Fisher-Yates, :45-47 */
+    const int q = uniform_int(&r, k + 1);
+    const int t = perm[k];
+    perm[k] = perm[q];
+    perm[q] = t;
+  }
+  for (int t = 0; t < P / 2; ++t) { /* :49-69 */
+    const int a = perm[2 * t], b = perm[2 * t + 1];
+    const int w = fit[a] <= fit[b] ? a : b;
+    const int l = w == a ? b : a;
+    double* xl = x + (size_t)l * D;
+    double* vl = v + (size_t)l * D;
+    const double* xw = x + (size_t)w * D;
+    for (int j = 0; j < D; ++j) {
+      const double r1 = uniform01(&r), r2 = uniform01(&r), r3 = uniform01(&r);
+      vl[j] = r1 * vl[j] + r2 * (xw[j] - xl[j]) + phi * r3 * (mean[j] - xl[j]);
+      xl[j] += vl[j];
+      xl[j] = xl[j] < lb ? lb : (ub < xl[j] ? ub : xl[j]); /* std::clamp */
+    }
+    fit[l] = orc_eval_scalar_f64(kind, D, shift, rot, bias, xl);
+  }
+  free(mean);
+  free(perm);
+  return r.consumed;
+}

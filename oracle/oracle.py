@@ -694,3 +694,16 @@ def ref_param_record(series, problem_ids, instances, runs, dim=10):
     buf = ctypes.create_string_buffer(int(ln) + 1)
     REF().ref_param_record(*args, buf, int(ln))
     return buf.raw[:ln].decode()
+
+
+register_c({"orc_cso_generation_f64": (i64, [c_int, c_int, c_double, c_int, vp, vp, c_double, vp, vp, vp, c_double,
+                                             c_double, vp, i64])})
+
+
+def cso_generation_c(P, D, phi, kind, shift, rot, bias, x, v, fit, lb, ub, words):
+    """The C restatement of cso_optimizer::generation (in place on x, v, fit); returns words used."""
+    o = np.ascontiguousarray(shift, np.float64)
+    m = np.ascontiguousarray(rot, np.float64).ravel()
+    w = np.ascontiguousarray(words, np.uint64)
+    return int(C().orc_cso_generation_f64(P, D, phi, kind, ptr(o), ptr(m), bias, ptr(x), ptr(v), ptr(fit), lb, ub,
+                                          ptr(w), len(w)))
