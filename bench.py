@@ -337,9 +337,9 @@ def run_evb(args, rank, world, local):
     e2e = {"value": world * e2e_steps * 3 * P / e2e_s, "unit": UNIT, "h2d_bytes_per_step": P * D * 8,
            "d2h_bytes_per_step": 3 * P * 8,
            "how": "evb_evaluate_batch_host_many per step (C ABI): the step's population, pinned host memory, "
-                  "crosses the host link once in column chunks that the first objective's fused GEMM consumes "
-                  "as they land; the other two objectives run on the resident copy; fitness written to pinned "
-                  "host memory; wall clock with device sync, max over ranks",
+                  "crosses the host link once in column chunks that one multi-problem fused GEMM (all three "
+                  "objectives, X read once per stage) consumes as they land; fitness written to pinned host "
+                  "memory; wall clock with device sync, max over ranks",
            "per_call": {"value": world * e2e_steps * 3 * P / per_call_s, "unit": UNIT,
                         "h2d_bytes_per_step": 3 * P * D * 8,
                         "how": "3 x evb_evaluate_batch_host (the population copied in once per objective)"}}

@@ -133,6 +133,12 @@ EVB_API int evb_evaluate_batch_multi(evb_problem p, evb_scratch s, int n_kinds, 
  * kernel directly.  Pinned X_host gives full host-link bandwidth. */
 EVB_API int evb_evaluate_batch_host(evb_problem p, evb_scratch s, const void* X_host, int64_t n_points,
                             int64_t ldx, void* out_host);
+/* One device population on several problems (same dimension and dtype): outs[k] (device,
+ * n_points) receives problem k's fitness.  Two or three fp64 base problems with fused kinds run
+ * as ONE launch whose stages carry X once for all problems; otherwise one launch per problem. */
+EVB_API int evb_evaluate_batch_problems(const evb_problem* problems, int n_problems, evb_scratch s, const void* X,
+                                        int64_t n_points, int64_t ldx, void* const* outs, void* stream);
+
 /* One host population on several problems (same dimension and dtype): X crosses the host link
  * once — overlapped with the first problem's fused GEMM — and every problem is evaluated on the
  * resident copy; out_host[k] (n_points values) receives problem k's fitness.  Equivalent to

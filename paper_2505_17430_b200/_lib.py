@@ -99,6 +99,8 @@ def lib() -> ctypes.CDLL:
         ),
         "evb_evaluate_batch_host": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p]),
         "evb_evaluate_batch_host_many": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_int64, c_int64, c_void_p]),
+        "evb_evaluate_batch_problems": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_int64, c_int64, c_void_p,
+                                                c_void_p]),
         "evb_launch_count": (c_int, []),
         "evb_probe_peak_tflops": (c_int, [c_int, c_int, P(c_double)]),
     }

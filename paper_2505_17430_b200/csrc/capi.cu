@@ -439,6 +439,9 @@ void host_eval(const evb_problem* probs, int n_prob, evb_scratch s, const void* 
     return rq;
   };
   eval_request rq = request(0);
+  std::vector<eval_request> all(static_cast<size_t>(n_prob));
+  for (int k = 0; k < n_prob; ++k) all[size_t(k)] = request(k);
+  bool multi = multi_eligible(all.data(), n_prob);
   // The fused fp64 GEMM starts while X is still crossing the host link: X goes over in column
   // chunks on a second stream, each chunk followed by a stream write of its gate word, and the
   // GEMM producer waits per chunk before its TMA loads (the copy is the e2e bound: ~8 MB per
@@ -502,7 +505,13 @@ void host_eval(const evb_problem* probs, int n_prob, evb_scratch s, const void* 
     rq.kgate_epoch = epoch;
     rq.x_ready = s->ev_x_ready;
     if (trace) EVB_CUDA(cudaStreamWaitEvent(st, tev[0], 0));
-    eval_dispatch(rq);
+    if (multi) {  // every problem in one launch, all consuming the chunks as they land
+      std::vector<eval_request> rqs(static_cast<size_t>(n_prob));
+      for (int k = 0; k < n_prob; ++k) rqs[size_t(k)] = request(k);
+      rqs[0] = rq;
+      if (!gemm_eval_multi(rqs.data(), n_prob, s->dx, ldd)) multi = false;
+    }
+    if (!multi) eval_dispatch(rq);
     if (trace) EVB_CUDA(cudaEventRecord(tev[n_chunks + 1], st));
     EVB_CUDA(cudaStreamWaitEvent(st, s->ev_x_ready, 0));
     if (trace) {
@@ -526,10 +535,12 @@ void host_eval(const evb_problem* probs, int n_prob, evb_scratch s, const void* 
       EVB_CUDA(cudaMemcpyAsync(s->dx, X_host, size_t(ldd) * n_points * es, cudaMemcpyHostToDevice, st));
     else
       EVB_CUDA(cudaMemcpy2DAsync(s->dx, ldd * es, X_host, ldx * es, D * es, n_points, cudaMemcpyHostToDevice, st));
-    eval_dispatch(rq);
+    if (multi && !gemm_eval_multi(all.data(), n_prob, s->dx, ldd)) multi = false;
+    if (!multi) eval_dispatch(rq);
   }
   // the remaining problems evaluate the resident copy (the stream already waits for all of X)
-  for (int k = 1; k < n_prob; ++k) eval_dispatch(request(k));
+  if (!multi)
+    for (int k = 1; k < n_prob; ++k) eval_dispatch(request(k));
   for (int k = 0; k < n_prob; ++k)
     if (dst[k] != outs_host[k])
       EVB_CUDA(cudaMemcpyAsync(outs_host[k], dst[k], size_t(n_points) * es, cudaMemcpyDeviceToHost, st));
@@ -543,6 +554,34 @@ extern "C" {
 int evb_evaluate_batch_host(evb_problem p, evb_scratch s, const void* X_host, int64_t n_points, int64_t ldx,
                             void* out_host) {
   return guarded([&] { host_eval(&p, 1, s, X_host, n_points, ldx, &out_host); });
+}
+
+int evb_evaluate_batch_problems(const evb_problem* problems, int n_problems, evb_scratch s, const void* X,
+                                int64_t n_points, int64_t ldx, void* const* outs, void* stream) {
+  return guarded([&] {
+    require(problems != nullptr && n_problems >= 1 && outs != nullptr, "evaluate_batch_problems: null argument");
+    std::vector<eval_request> rqs(static_cast<size_t>(n_problems));
+    for (int k = 0; k < n_problems; ++k) {
+      validate_eval(problems[k], s, n_points, ldx);
+      if (problems[k]->p.dim != problems[0]->p.dim || problems[k]->p.dtype != problems[0]->p.dtype)
+        throw invalid_argument("evaluate_batch_problems: problems differ in dimension or dtype");
+      eval_request& rq = rqs[size_t(k)];
+      rq.prob = &problems[k]->p;
+      rq.scratch = s;
+      rq.X = X;
+      rq.n = n_points;
+      rq.ldx = ldx;
+      rq.out = outs[k];
+      rq.ldo = n_points;
+      rq.n_out = 1;
+      rq.kinds[0] = problems[k]->p.kind;
+      rq.biases[0] = problems[k]->p.bias;
+      rq.stream = static_cast<cudaStream_t>(stream);
+    }
+    if (n_points == 0) return;
+    if (multi_eligible(rqs.data(), n_problems) && gemm_eval_multi(rqs.data(), n_problems, X, ldx)) return;
+    for (auto& rq : rqs) eval_dispatch(rq);
+  });
 }
 
 int evb_evaluate_batch_host_many(const evb_problem* problems, int n_problems, evb_scratch s, const void* X_host,

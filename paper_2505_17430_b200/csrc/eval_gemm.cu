@@ -407,6 +407,149 @@ __global__ void __launch_bounds__(f64_cfg<BM, BN, WM, WN, STAGES>::THREADS, MINB
 }
 
 // ---------------------------------------------------------------------------------------
+// K1 (several problems, one population): NP problems sharing X (e.g. a suite's objectives at
+// the same population, or config 1's three objectives).  One CTA per (row block, column block)
+// holds NP warp groups — group g computes problem g's 64 x 56 tile with the pair kernel's 16 x 56
+// warp tiles — and one producer whose stage carries ONE X tile plus the NP rotation tiles and
+// shift slices, so X is read once for all problems.  12 MMA warps per SM at NP = 3 (3 per
+// SMSP) hide more DMMA latency than two 4-warp CTAs; each group then runs the usual epilogue on
+// its own parked tile, with its own partials / tickets.
+constexpr int kMultiBM = 64, kMultiBN = 56, kMultiStages = 6;
+
+template <int NP>
+struct f64m_cfg {
+  static constexpr int BM = kMultiBM, BN = kMultiBN, KB = 16, STAGES = kMultiStages;
+  static constexpr int WM = 4;  // MMA warps per group (16 x 56 warp tiles)
+  static constexpr int NCW = NP * WM;
+  static constexpr int THREADS = (NCW + 1) * 32;
+  static constexpr int TM = 2, TN = 7;
+  static constexpr int A_BYTES = BM * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int O_BYTES = 128;
+  static constexpr int STAGE_BYTES = ((A_BYTES + NP * (B_BYTES + O_BYTES) + 1023) / 1024) * 1024;
+  static constexpr int LDT = BN + 1;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 2 * STAGES * 8 + 64;
+  static_assert(NP * BM * LDT * 8 <= STAGES * STAGE_BYTES, "parked tiles must fit the stage ring");
+};
+
+template <int NP>
+struct multi_maps {
+  CUtensorMap m[NP];
+};
+
+template <int NP>
+__global__ void __launch_bounds__(f64m_cfg<NP>::THREADS, 1)
+    eval_f64_dmma_multi_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ multi_maps<NP> tmM,
+                               const __grid_constant__ fused_params<double> p0,
+                               const __grid_constant__ fused_params<double> p1,
+                               const __grid_constant__ fused_params<double> p2) {
+  using C = f64m_cfg<NP>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  int* last_flag = reinterpret_cast<int*>(empty + C::STAGES);  // NP flags
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * C::BM, n0 = blockIdx.y * C::BN;
+  const int KT = (p0.D + C::KB - 1) / C::KB;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], C::NCW);
+    }
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == C::NCW) {
+    // ---------------- producer: X once, then each problem's rotation tile and shift slice ----
+    if (lane == 0) {
+      ptx::prefetch_tma(&tmX);
+      for (int g = 0; g < NP; ++g) ptx::prefetch_tma(&tmM.m[g]);
+      int chunk = 0, chunk_end = 0;
+      for (int kb = 0; kb < KT; ++kb) {
+        const int s = kb % C::STAGES;
+        if (kb >= C::STAGES) ptx::mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
+        if (p0.kgate) {
+          while (kb * C::KB >= chunk_end) {
+            ptx::wait_gate(p0.kgate + chunk, p0.kgate_epoch);
+            chunk_end = chunk + 1 < p0.kgate_n ? p0.kgate_end[chunk] : 1 << 30;
+            ++chunk;
+          }
+        }
+        uint8_t* st = smem + s * C::STAGE_BYTES;
+        ptx::mbar_arrive_expect_tx(&full[s], C::A_BYTES + NP * (C::B_BYTES + C::O_BYTES));
+        ptx::tma_load_2d(st, &tmX, &full[s], kb * C::KB, m0);
+#pragma unroll
+        for (int g = 0; g < NP; ++g) {
+          const fused_params<double>& pg = g == 0 ? p0 : (g == 1 ? p1 : p2);
+          ptx::tma_load_2d(st + C::A_BYTES + g * C::B_BYTES, &tmM.m[g], &full[s], kb * C::KB, n0);
+          ptx::bulk_load(st + C::A_BYTES + NP * C::B_BYTES + g * C::O_BYTES, pg.shift + size_t(kb) * C::KB, C::O_BYTES,
+                         &full[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers: group g = warp / 4 computes problem g ----------------
+  const int grp = warp / C::WM, wg = warp % C::WM;
+  const int g8 = lane >> 2, t = lane & 3;
+  const int rA = wg * 16;
+  double acc[C::TM][C::TN][2];
+#pragma unroll
+  for (int i = 0; i < C::TM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const uint32_t smem_base = ptx::smem_u32(smem);
+  for (int kb = 0; kb < KT; ++kb) {
+    const int s = kb % C::STAGES;
+    ptx::mbar_wait(&full[s], (kb / C::STAGES) & 1);
+    const uint32_t sA = smem_base + s * C::STAGE_BYTES;
+    const uint32_t sB = sA + C::A_BYTES + grp * C::B_BYTES;
+    const uint32_t sO = sA + C::A_BYTES + NP * C::B_BYTES + grp * C::O_BYTES;
+    double a[2][C::TM], b[2][C::TN];
+    auto load = [&](int ks, int buf) {
+      const int kk = ks * 4 + t;
+      const double o = ptx::lds_f64(sO + kk * 8);
+#pragma unroll
+      for (int i = 0; i < C::TM; ++i) a[buf][i] = __dsub_rn(ptx::lds_f64(sA + swz<8>(rA + i * 8 + g8, kk)), o);
+#pragma unroll
+      for (int j = 0; j < C::TN; ++j) b[buf][j] = ptx::lds_f64(sB + swz<8>(j * 8 + g8, kk));
+    };
+    load(0, 0);
+#pragma unroll
+    for (int ks = 0; ks < C::KB / 4; ++ks) {
+      if (ks + 1 < C::KB / 4) load(ks + 1, (ks + 1) & 1);
+#pragma unroll
+      for (int i = 0; i < C::TM; ++i)
+#pragma unroll
+        for (int j = 0; j < C::TN; ++j) ptx::dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[ks & 1][i], b[ks & 1][j]);
+    }
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&empty[s]);
+  }
+
+  // every group has drained the ring: park each group's tile in its own region, then per group
+  // the fused epilogue (named barrier 2 + g over the group's 128 threads)
+  ptx::named_bar_sync(1, C::NCW * 32);
+  double* zt = reinterpret_cast<double*>(smem) + size_t(grp) * C::BM * C::LDT;
+#pragma unroll
+  for (int i = 0; i < C::TM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::TN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) zt[(rA + i * 8 + g8) * C::LDT + j * 8 + 2 * t + h] = acc[i][j][h];
+  ptx::named_bar_sync(2 + grp, C::WM * 32);
+  const fused_params<double>& pg = grp == 0 ? p0 : (grp == 1 ? p1 : p2);
+  tile_epilogue<double, C::BM, C::BN>(pg, zt, C::LDT, m0, n0, threadIdx.x - grp * C::WM * 32, C::WM * 32,
+                                      last_flag + grp, blockIdx.x, blockIdx.y, 2 + grp);
+}
+
+// ---------------------------------------------------------------------------------------
 // K1 (persistent): one CTA per SM walks a static list of BM x BN tiles.  Warp roles:
 //   warps 0-7   MMA      (warp tile 8 x 56: 7 DMMA m8n8k4 per k4 step, 2 warps per SMSP)
 //   warps 8-11  epilogue (transform terms + row sums of the previous tile, from smem)
@@ -1150,6 +1293,85 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
   } else {
     launch_f32<64, 128>(tmX, tmM, fp, rq.stream);
   }
+}
+
+// NP base problems (same D) on one device X: one multi-problem K1 launch; rqs[g] carries problem
+// g's kinds / biases / output, rqs[0] the gates.  Returns false when the shapes do not fit.
+bool gemm_eval_multi(const eval_request* rqs, int np, const void* X, int64_t ldx) {
+  if (np < 2 || np > 3) return false;
+  const int P = int(rqs[0].n), D = rqs[0].prob->dim;
+  evb_scratch_s* sc = rqs[0].scratch;
+  fused_params<double> fp[3]{};
+  multi_maps<3> maps3{};
+  multi_maps<2> maps2{};
+  constexpr int BM = kMultiBM, BN = kMultiBN;
+  const int n_ntiles = (D + BN - 1) / BN, n_mtiles = (P + BM - 1) / BM;
+  CUtensorMap tmX;
+  if (!make_tma_2d(&tmX, X, EVB_F64, uint64_t(D), uint64_t(P), uint64_t(ldx) * 8, 16, BM)) return false;
+  size_t part_total = 0;
+  for (int g = 0; g < np; ++g) {
+    const eval_request& rq = rqs[g];
+    fused_params<double>& f = fp[g];
+    f.P = P;
+    f.D = D;
+    f.ell_w = static_cast<const double*>(rq.prob->ell_w);
+    f.shift = static_cast<const double*>(rq.prob->shift);
+    f.out = static_cast<double*>(rq.out);
+    f.ldo = rq.ldo;
+    if (!build_plan<double>(f, rq.n_out, rq.kinds, rq.biases)) return false;
+    f.n_ntiles = n_ntiles;
+    part_total += size_t(f.n_ch) * n_ntiles * P;
+    CUtensorMap& m = np == 3 ? maps3.m[g] : maps2.m[g];
+    if (!make_tma_2d(&m, rq.prob->rotation, EVB_F64, uint64_t(rq.prob->ld), uint64_t(D), uint64_t(rq.prob->ld) * 8, 16,
+                     BN))
+      return false;
+  }
+  cudaStream_t st = rqs[0].stream;
+  ensure_buffer(&sc->partial, &sc->partial_bytes, part_total * sizeof(double), st);
+  const size_t need_counters = size_t(np) * n_mtiles;
+  if (sc->counters_n < need_counters) {
+    size_t cap = sc->counters_n * sizeof(unsigned);
+    void* ptr = sc->counters;
+    ensure_buffer(&ptr, &cap, need_counters * sizeof(unsigned), st);
+    sc->counters = static_cast<unsigned*>(ptr);
+    sc->counters_n = cap / sizeof(unsigned);
+    EVB_CUDA(cudaMemsetAsync(sc->counters, 0, cap, st));
+  }
+  size_t off = 0;
+  for (int g = 0; g < np; ++g) {
+    fp[g].partial = static_cast<double*>(sc->partial) + off;
+    off += size_t(fp[g].n_ch) * n_ntiles * P;
+    fp[g].counters = sc->counters + size_t(g) * n_mtiles;
+  }
+  if (rqs[0].kgate) {
+    fp[0].kgate = rqs[0].kgate;
+    fp[0].kgate_n = rqs[0].kgate_n;
+    for (int c = 0; c < rqs[0].kgate_n; ++c) fp[0].kgate_end[c] = rqs[0].kgate_end[c];
+    fp[0].kgate_epoch = rqs[0].kgate_epoch;
+  } else if (rqs[0].x_ready) {
+    EVB_CUDA(cudaStreamWaitEvent(st, rqs[0].x_ready, 0));
+  }
+  dim3 grid(n_mtiles, n_ntiles);
+  if (np == 3) {
+    using C = f64m_cfg<3>;
+    static bool attr = false;
+    if (!attr) {
+      EVB_CUDA(cudaFuncSetAttribute(eval_f64_dmma_multi_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+      attr = true;
+    }
+    eval_f64_dmma_multi_kernel<3><<<grid, C::THREADS, C::SMEM, st>>>(tmX, maps3, fp[0], fp[1], fp[2]);
+  } else {
+    using C = f64m_cfg<2>;
+    static bool attr = false;
+    if (!attr) {
+      EVB_CUDA(cudaFuncSetAttribute(eval_f64_dmma_multi_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+      attr = true;
+    }
+    eval_f64_dmma_multi_kernel<2><<<grid, C::THREADS, C::SMEM, st>>>(tmX, maps2, fp[0], fp[1], fp[1]);
+  }
+  EVB_CUDA(cudaGetLastError());
+  count_launch();
+  return true;
 }
 
 template void gemm_eval<double>(const eval_request&, const void*, int64_t, bool, double*, int64_t, const double*,

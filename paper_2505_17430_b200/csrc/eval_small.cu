@@ -486,6 +486,17 @@ bool gate_eligible(const eval_request& rq) {
          (rq.ldx * 8) % 16 == 0 && !(std::getenv("EVB_F64_KERNEL") && std::string(std::getenv("EVB_F64_KERNEL")) == "persistent");
 }
 
+bool multi_eligible(const eval_request* rqs, int np) {
+  if (np < 2 || np > 3 || (std::getenv("EVB_MULTI") && std::string(std::getenv("EVB_MULTI")) == "0")) return false;
+  for (int g = 0; g < np; ++g) {
+    eval_request r = rqs[g];
+    r.X = rqs[0].X;
+    r.ldx = rqs[0].ldx;
+    if (!gate_eligible(r) || r.n_out != 1 || rqs[g].prob->dim != rqs[0].prob->dim) return false;
+  }
+  return true;
+}
+
 void eval_dispatch(const eval_request& rq) {
   if (rq.n == 0) return;
   if (rq.prob->dtype == EVB_F64) dispatch_t<double>(rq);

@@ -216,6 +216,10 @@ constexpr int kMaxGates = 8;
 void eval_dispatch(const eval_request& rq);
 // true when eval_dispatch runs the request on the fused fp64 GEMM, whose producer honours kgate
 bool gate_eligible(const eval_request& rq);
+// several base problems (same D, fp64, fused kinds) on one device X in one multi-problem K1
+// launch (eval_gemm.cu); false when the requests do not qualify (caller falls back)
+bool multi_eligible(const eval_request* rqs, int np);
+bool gemm_eval_multi(const eval_request* rqs, int np, const void* X, int64_t ldx);
 
 }  // namespace evb
 

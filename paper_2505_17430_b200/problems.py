@@ -239,3 +239,13 @@ def batched_evaluate_many(problems: Sequence[ProblemInstance], xs, scratch: Eval
     check(_lib.lib().evb_evaluate_batch_host_many(handles, len(problems), sc.handle, _ptr(x), x.shape[0], x.shape[1],
                                                   optrs), "batched_evaluate_many")
     return outs
+
+
+def evaluate_batch_problems(problems: Sequence[ProblemInstance], X, scratch: EvalScratch, outs, stream=None) -> None:
+    """One device population on several problems (evb_evaluate_batch_problems); outs[k] is a
+    device vector for problem k.  Two or three fp64 base problems run as one launch."""
+    xp, n, ld = _dev_ptr_and_ld(X, problems[0].dim)
+    handles = (ctypes.c_void_p * len(problems))(*[p.handle.value for p in problems])
+    optrs = (ctypes.c_void_p * len(problems))(*[o.data_ptr() for o in outs])
+    check(_lib.lib().evb_evaluate_batch_problems(handles, len(problems), scratch.handle, xp, n, ld, optrs,
+                                                 _stream_ptr(stream)), "evaluate_batch_problems")

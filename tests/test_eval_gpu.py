@@ -279,3 +279,25 @@ def test_host_many_one_copy_equals_device(config1, dev):
         assert np.array_equal(g, gpu_eval(p, Xs, dev))
     with pytest.raises(evb.InvalidArgument):
         evb.batched_evaluate_many([probs[0], small[0]], X, sc)
+
+
+@pytest.mark.parametrize("n_prob", [2, 3])
+def test_problems_one_launch_bit_identical(config1, dev, n_prob):
+    # several fp64 problems on one X in ONE launch (stages carry X once) == one launch per problem,
+    # bit for bit (same tiles, K order, epilogue); with different shifts / rotations per problem
+    o, m, X = config1
+    o2, m2 = O.shift_rotation(8, 1000)
+    specs = [(K.elliptic, o, m, 1.0), (K.rastrigin, o2, m2, 2.0), (K.ackley, o, m2, 3.0)][:n_prob]
+    probs = [evb.ProblemInstance.base(k, oo, mm, b) for k, oo, mm, b in specs]
+    want = [gpu_eval(p, X, dev) for p in probs]
+    Xd = torch.from_numpy(X).to(dev)
+    outs = [torch.empty(1024, dtype=torch.float64, device=dev) for _ in probs]
+    n0 = evb.launch_count()
+    evb.evaluate_batch_problems(probs, Xd, evb.EvalScratch(), outs)
+    torch.cuda.synchronize()
+    assert evb.launch_count() - n0 == 1
+    for o_, w in zip(outs, want):
+        assert np.array_equal(o_.cpu().numpy(), w)
+    got = evb.batched_evaluate_many(probs, X)
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)

@@ -50,3 +50,17 @@ for concurrent in (False, True):
         ts.append(a.elapsed_time(b) * 1e3)
     t = np.median(ts[10:])
     print(f"concurrent={concurrent}: step {t:.1f} us -> {3 * 1024 / (t * 1e-6) / 1e6:.2f} M evals/s")
+
+outs3 = [torch.empty(1024, dtype=torch.float64, device="cuda") for _ in probs]
+sc3 = evb.EvalScratch()
+ts = []
+for it in range(60):
+    flush.zero_()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(main)
+    evb.evaluate_batch_problems(probs, X, sc3, outs3, main)
+    b.record(main)
+    b.synchronize()
+    ts.append(a.elapsed_time(b) * 1e3)
+t = np.median(ts[10:])
+print(f"one launch (evaluate_batch_problems): step {t:.1f} us -> {3 * 1024 / (t * 1e-6) / 1e6:.2f} M evals/s")
