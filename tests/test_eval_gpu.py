@@ -301,3 +301,28 @@ def test_problems_one_launch_bit_identical(config1, dev, n_prob):
     got = evb.batched_evaluate_many(probs, X)
     for g, w in zip(got, want):
         assert np.array_equal(g, w)
+
+
+@pytest.mark.parametrize("n,dim", [(262144, 1000), (1024, 8192)])
+def test_large_sizes_sampled(dev, n, dim):
+    # maximum-size style batches (2.1 GB of X; a 537 MB rotation): checked on sampled rows against
+    # the C restatement, and the fp64 result is deterministic across two launches
+    rs = np.random.default_rng(dim)
+    o = rs.uniform(-80, 80, dim)
+    q, _ = np.linalg.qr(rs.standard_normal((dim, dim)))
+    p = evb.ProblemInstance.base(K.rastrigin, o, q, 5.0)
+    gen = torch.Generator(device=dev).manual_seed(dim)
+    Xd = torch.rand((n, dim), dtype=torch.float64, device=dev, generator=gen) * 200.0 - 100.0
+    out = torch.empty(n, dtype=torch.float64, device=dev)
+    sc = evb.EvalScratch()
+    evb.evaluate_batch(p, Xd, sc, out)
+    out2 = torch.empty_like(out)
+    evb.evaluate_batch(p, Xd, sc, out2)
+    torch.cuda.synchronize()
+    assert torch.equal(out, out2)
+    rows = np.unique(np.concatenate([[0, n - 1], rs.integers(0, n, 14)]))
+    Xs = Xd[torch.from_numpy(rows).to(dev)].cpu().numpy()
+    ref = O.eval_batch(int(K.rastrigin), o, q, 5.0, Xs)
+    assert rel_err(out.cpu().numpy()[rows], ref) <= 1e-10
+    del Xd
+    torch.cuda.empty_cache()
