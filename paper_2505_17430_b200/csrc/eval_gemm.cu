@@ -74,8 +74,6 @@ struct fused_params {
   int kgate_n;
   int kgate_end[8];
   unsigned kgate_epoch;
-  int umma_variant;  // tf32 path: 0 = 3 products in one accumulator, 1 = + lo*lo, 2 = hi*hi and
-                     // corrections in separate TMEM accumulators (summed in the epilogue)
 };
 
 // cosine of the fused epilogue: library cos for fp64.  fp32 (a tolerance path: 3xTF32 / FFMA
@@ -749,10 +747,6 @@ __global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
         const int s = kb % C::STAGES;
         if (kb >= C::STAGES) ptx::mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
         uint8_t* st = smem + s * C::STAGE_BYTES;
-        if (p.umma_variant >= 20) {  // debug: no loads
-          ptx::mbar_arrive(&full[s]);
-          continue;
-        }
         ptx::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
         ptx::tma_load_2d(st, &tmShi, &full[s], kb * C::KB, m0);
         ptx::tma_load_2d(st + C::A_BYTES, &tmSlo, &full[s], kb * C::KB, m0);
@@ -767,30 +761,22 @@ __global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
       for (int kb = 0; kb < KT; ++kb) {
         const int s = kb % C::STAGES;
         ptx::mbar_wait(&full[s], (kb / C::STAGES) & 1);
-        if (p.umma_variant < 40) umma::fence_after();
-        if (p.umma_variant >= 10 && p.umma_variant < 20) {  // debug: no MMA
-          ptx::mbar_arrive(&empty[s]);
-          continue;
-        }
+        umma::fence_after();
         const uint32_t sa_hi = base + s * C::STAGE_BYTES, sa_lo = sa_hi + C::A_BYTES;
         const uint32_t sb_hi = sa_hi + 2 * C::A_BYTES, sb_lo = sb_hi + C::B_BYTES;
-        const uint32_t tcorr = (p.umma_variant % 10) == 2 ? tmem + BN : tmem;
+        const uint32_t tcorr = tmem + BN;  // corrections accumulate apart from the main product
 #pragma unroll
         for (int k = 0; k < C::KB / 8; ++k) {  // K = 8 tf32 = 32 bytes per instruction
           const uint32_t off = k * 32;
           const uint32_t acc0 = (kb | k) ? 1u : 0u;
           umma::mma_tf32(tcorr, umma::smem_desc(sa_lo + off), umma::smem_desc(sb_hi + off), idesc, acc0);
           umma::mma_tf32(tcorr, umma::smem_desc(sa_hi + off), umma::smem_desc(sb_lo + off), idesc, 1u);
-          if ((p.umma_variant % 10) == 1)
-            umma::mma_tf32(tcorr, umma::smem_desc(sa_lo + off), umma::smem_desc(sb_lo + off), idesc, 1u);
           umma::mma_tf32(tmem, umma::smem_desc(sa_hi + off), umma::smem_desc(sb_hi + off), idesc,
-                         (p.umma_variant % 10) == 2 ? acc0 : 1u);
+                         acc0);
         }
-        if (p.umma_variant >= 50 && p.umma_variant < 60 && kb + C::STAGES < KT) ptx::mbar_arrive(&empty[s]);  // debug
-        else umma::commit(&empty[s]);  // frees the stage when these MMAs have read it
+        umma::commit(&empty[s]);  // frees the stage when these MMAs have read it
       }
-      if (p.umma_variant >= 10 && p.umma_variant < 20) ptx::mbar_arrive(accfull);
-      else umma::commit(accfull);  // accumulator complete
+      umma::commit(accfull);  // accumulator complete
     }
   } else {
     // ---------------- epilogue warps 2..5: one output row per thread ----------------
@@ -805,7 +791,7 @@ __global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
       for (int c0 = 0; c0 < BN; c0 += 16) {
         float v[16];
         umma::tmem_ld16(taddr + c0, v);
-        if ((p.umma_variant % 10) == 2) {
+        {
           float w[16];
           umma::tmem_ld16(taddr + BN + c0, w);
 #pragma unroll
@@ -824,14 +810,13 @@ __global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
         for (int c0 = 0; c0 < BN; c0 += 16) {
           float v[16];
           umma::tmem_ld16(taddr + c0, v);
-          if ((p.umma_variant % 10) == 2) {
+          {
             float w[16];
             umma::tmem_ld16(taddr + BN + c0, w);
 #pragma unroll
             for (int q = 0; q < 16; ++q) v[q] = __fadd_rn(v[q], w[q]);
           }
-          if (p.umma_variant >= 60 && p.umma_variant < 70) acc += v[0];  // debug: no terms
-          else acc = accumulate16_rt<float>(term, acc, v, n0 + c0, p.D, p.ell_w);
+          acc = accumulate16_rt<float>(term, acc, v, n0 + c0, p.D, p.ell_w);
         }
         if (row < p.P) p.partial[(size_t(ch) * p.n_ntiles + blockIdx.y) * p.P + row] = acc;
       }
@@ -1236,8 +1221,6 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
         fp.partial = static_cast<T*>(sc->partial);
         fp.counters = sc->counters;
       }
-      static const char* var = std::getenv("EVB_UMMA_VARIANT");
-      fp.umma_variant = var ? std::atoi(var) : 2;
       if (UBN == 256) launch_f32_umma<256>(ta_hi, ta_lo, tb_hi, tb_lo, fp, rq.stream);
       else if (UBN == 128) launch_f32_umma<128>(ta_hi, ta_lo, tb_hi, tb_lo, fp, rq.stream);
       else launch_f32_umma<64>(ta_hi, ta_lo, tb_hi, tb_lo, fp, rq.stream);

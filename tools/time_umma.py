@@ -1,4 +1,4 @@
-"""Time the fp32 evaluation (config-1 shape) under EVB_UMMA_VARIANT debug variants."""
+"""Time the fp32 evaluation (config-1 shape, Rastrigin)."""
 import sys
 from pathlib import Path
 
