@@ -258,6 +258,15 @@ EVB_API int evb_de_init_population(evb_de e, void* pop, int64_t ldp, double lb, 
 EVB_API int evb_de_optimize(evb_de e, evb_problem objective, evb_scratch s, void* pop, int64_t ldp,
                             void* fitness, double lb, double ub, int64_t max_fes, evb_rng rng,
                             int* best_index, double* best_fitness, int* generations, void* stream);
+/* hybrid::restart_run (hybrid/restart.hpp:37-88, the "restart-lshade" preset) around this engine:
+ * runs fresh engine states (adapter, archive, population size reset; the population re-drawn
+ * from the continuing rng) until total_budget evaluations are spent, stopping a run once
+ * stagnation_evals evaluations passed without improving the best seen by more than epsilon.
+ * Recorder / parameter trace see one continuous run (generation numbers continue). */
+EVB_API int evb_de_optimize_restart(evb_de e, evb_problem objective, evb_scratch s, void* pop, int64_t ldp,
+                                    void* fitness, double lb, double ub, int64_t total_budget,
+                                    int64_t stagnation_evals, double epsilon, evb_rng rng, double* best_fitness,
+                                    int* engine_runs, int64_t* evaluations, void* stream);
 /* Engine state (archive members row-major cap x dim, size; SHADE/JADE memories; write index). */
 EVB_API int evb_de_get_state(evb_de e, void* archive_host, int* archive_size, void* mem_f_host,
                              void* mem_cr_host, int* write_index);

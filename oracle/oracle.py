@@ -707,3 +707,18 @@ def cso_generation_c(P, D, phi, kind, shift, rot, bias, x, v, fit, lb, ub, words
     w = np.ascontiguousarray(words, np.uint64)
     return int(C().orc_cso_generation_f64(P, D, phi, kind, ptr(o), ptr(m), bias, ptr(x), ptr(v), ptr(fit), lb, ub,
                                           ptr(w), len(w)))
+
+
+register_ref({"ref_restart_lshade": (c_double, [ctypes.c_uint64, ctypes.c_uint64, c_int, c_int, c_int, c_double,
+                                                 c_double, c_int, ctypes.c_longlong, ctypes.c_longlong, c_double,
+                                                 c_int, vp, vp, c_double, vp, vp, c_double, c_double])})
+
+
+def ref_restart_lshade(seed, stream, P, D, H, p_best, archive_rate, n_min, budget, stagnation, eps, kind, shift, rot,
+                       bias=0.0, lb=-100.0, ub=100.0):
+    o = np.ascontiguousarray(shift, np.float64)
+    m = np.ascontiguousarray(rot, np.float64).ravel()
+    runs, ev = ctypes.c_int(), ctypes.c_longlong()
+    best = REF().ref_restart_lshade(seed, stream, P, D, H, p_best, archive_rate, n_min, budget, stagnation, eps, kind,
+                                    ptr(o), ptr(m), bias, ctypes.byref(runs), ctypes.byref(ev), lb, ub)
+    return {"best_fitness": best, "engine_runs": runs.value, "evaluations": ev.value}

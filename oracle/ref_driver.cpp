@@ -844,3 +844,26 @@ REF_API int64_t ref_param_record(const int* gens, const double* mu_f, const doub
   if (csv) std::memcpy(csv, s.data(), std::min<size_t>(size_t(cap), s.size()));
   return int64_t(s.size());
 }
+
+// ---- hybrid::restart_run with the restart-lshade factory (presets.hpp), native stream ----------
+#include "evobench/hybrid/restart.hpp"
+
+REF_API double ref_restart_lshade(uint64_t seed, uint64_t stream, int P, int D, int H, double p_best,
+                                  double archive_rate, int n_min, long long budget, long long stagnation, double eps,
+                                  int kind, const double* shift, const double* rot, double bias, int* runs,
+                                  long long* evals, double lb, double ub) {
+  auto problem = make_base<double>(kind, D, shift, rot, bias);
+  eval_scratch<double> scratch;
+  auto objective = [&](std::span<const double> x) { return problem.evaluate(x, scratch); };
+  hybrid::restart_criterion crit;
+  crit.stagnation_evals = stagnation;
+  crit.epsilon = eps;
+  const auto factory = [&] {
+    return presets::detail::build_shade<double>(p_best, H, archive_rate, de::population_policy::linear_reduction(P, n_min));
+  };
+  rng_stream rng(seed, stream);
+  auto res = hybrid::restart_run<double>(factory, crit, objective, lb, ub, P, D, budget, rng, [](int, auto) {});
+  *runs = res.engine_runs;
+  *evals = res.evaluations;
+  return res.best.fitness;
+}

@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <limits>
 #include <cmath>
 #include <vector>
 
@@ -98,7 +99,12 @@ struct evb_de_s {
   int gen_P = 0;  // population size at the start of the last generation (its trial count)
   evb_param_trace_s* ptrace = nullptr;  // attached parameter_record trace (may be null)
   int ptrace_run = 0;
-  int gen_count = 0;  // evolution_state::generation() (reset by evb_de_optimize)
+  int gen_count = 0;   // evolution_state::generation() (reset by evb_de_optimize)
+  int gen_offset = 0;  // restart_run: generations reported by earlier engine runs
+  // restart_run's stagnation monitor (hybrid/restart.hpp:55-65), device-resident
+  double* d_mon = nullptr;  // [best_seen, since_improvement, evaluations] (doubles)
+  int mon_on = 0;
+  double mon_eps = 0.0;
 };
 
 namespace evb {
@@ -706,6 +712,27 @@ de_dev<T> make_dev(evb_de_s* e, void* pop, int64_t ldp, void* fit, double lb, do
   return d;
 }
 
+// restart_run's monitored objective (hybrid/restart.hpp:55-65): per evaluation in FE order,
+// best_seen improves only by more than epsilon, else since_improvement counts up
+template <typename T>
+__global__ void restart_monitor_kernel(const T* v, int n, double* mon, double eps) {
+  if (threadIdx.x != 0) return;
+  double best = mon[0], since = mon[1], evals = mon[2];
+  for (int i = 0; i < n; ++i) {
+    const double x = double(v[i]);
+    evals += 1.0;
+    if (x < __dsub_rn(best, eps)) {
+      best = x;
+      since = 0.0;
+    } else {
+      since += 1.0;
+    }
+  }
+  mon[0] = best;
+  mon[1] = since;
+  mon[2] = evals;
+}
+
 // adapter means after a generation -> parameter_record (de/parameter.hpp:130-133 JADE mu,
 // :186-195 SHADE mean of the memories: sequential double sum / H, cast to T)
 template <typename T>
@@ -778,6 +805,10 @@ void generation_t(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, vo
   rq.scalar_trig = true;
   eval_dispatch(rq);
   if (e->rec) recorder_observe(e->rec, e->rec_run, e->trial_fit, e->P, st);  // trials in FE (i) order
+  if (e->mon_on) {
+    restart_monitor_kernel<T><<<1, 32, 0, st>>>(static_cast<const T*>(e->trial_fit), e->P, e->d_mon, e->mon_eps);
+    count_launch();
+  }
   de_select_scan_kernel<T><<<1, kSelThreads, 0, st>>>(d);
   count_launch();
   {
@@ -795,7 +826,7 @@ void generation_t(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, vo
                                             e->cfg.memory_size, e->cfg.parameter == EVB_PAR_SHADE ? 1 : 0,
                                             t->gen + off, static_cast<T*>(t->mu_f) + off,
                                             static_cast<T*>(t->mu_cr) + off, t->count + e->ptrace_run, t->cap,
-                                            e->gen_count);
+                                            e->gen_offset + e->gen_count);
     count_launch();
   }
   reduce_t<T>(e, pop, ldp, fit, r, st);
@@ -991,7 +1022,7 @@ void free_de(evb_de_s* e) {
   if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
   void* ptrs[] = {e->trial, e->trial_fit, e->F, e->CR, e->slot, e->idx, e->jrand, e->xlen, e->rword, e->woff, e->wcount, e->order,
                   e->win, e->arch_slot, e->owner, e->succ, e->archive, e->d_arch_size, e->d_write_index,
-                  e->d_arch_words, e->mem_f, e->mem_cr, e->rank, e->d_shrink_words};
+                  e->d_arch_words, e->mem_f, e->mem_cr, e->rank, e->d_shrink_words, e->d_mon};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (e->eval_scratch) evb_scratch_destroy(e->eval_scratch);
@@ -1420,56 +1451,143 @@ int evb_de_last_draws(evb_de e, int64_t* word_counts, int64_t* archive_words, ui
   });
 }
 
+}  // extern "C"
+
+namespace evb {
+namespace {
+
+// de_engine::optimize (de/engine.hpp:107-133): init, evaluate, generations while the budget is
+// left and stop() is false (checked before every generation); returns the generations run and
+// the population's best (lowest fitness, ties to the lowest index).
+template <typename Stop>
+int optimize_impl(evb_de_s* e, evb_problem objective, evb_scratch_s* sc, void* pop, int64_t ldp, void* fitness,
+                  double lb, double ub, int64_t max_fes, evb_rng_s* rng, cudaStream_t st, Stop&& stop, int* best_index,
+                  double* best_fitness) {
+  restore_size(e);
+  de_init_population(e, pop, ldp, lb, ub, rng, st);
+  eval_request rq{};
+  rq.prob = &objective->p;
+  rq.scratch = sc;
+  rq.X = pop;
+  rq.n = e->P;
+  rq.ldx = ldp;
+  rq.out = fitness;
+  rq.ldo = e->P;
+  rq.n_out = 1;
+  rq.kinds[0] = objective->p.kind;
+  rq.biases[0] = objective->p.bias;
+  rq.stream = st;
+  rq.scalar_trig = true;
+  eval_dispatch(rq);
+  if (e->rec) recorder_observe(e->rec, e->rec_run, fitness, e->P, st);  // initial evaluations
+  if (e->mon_on) {
+    if (e->dtype == EVB_F64)
+      restart_monitor_kernel<double><<<1, 32, 0, st>>>(static_cast<const double*>(fitness), e->P, e->d_mon, e->mon_eps);
+    else
+      restart_monitor_kernel<float><<<1, 32, 0, st>>>(static_cast<const float*>(fitness), e->P, e->d_mon, e->mon_eps);
+    count_launch();
+  }
+  e->max_fes = max_fes;  // evolution_state st(max_fes, ...); st.add_fes(P) for the initial members
+  e->fes = e->P;
+  e->gen_count = 0;
+  int gens = 0;
+  while (e->fes < max_fes && !stop()) {
+    de_generation(e, &objective->p, sc, pop, ldp, fitness, lb, ub, rng, st);
+    ++gens;
+  }
+  const size_t es = e->dtype == EVB_F64 ? 8 : 4;
+  std::vector<uint8_t> f(es * e->P);
+  EVB_CUDA(cudaMemcpyAsync(f.data(), fitness, es * e->P, cudaMemcpyDeviceToHost, st));
+  EVB_CUDA(cudaStreamSynchronize(st));
+  int best = 0;
+  auto val = [&](int i) {
+    return e->dtype == EVB_F64 ? reinterpret_cast<double*>(f.data())[i] : double(reinterpret_cast<float*>(f.data())[i]);
+  };
+  for (int i = 1; i < e->P; ++i)
+    if (val(i) < val(best)) best = i;
+  if (best_index) *best_index = best;
+  if (best_fitness) *best_fitness = val(best);
+  return gens;
+}
+
+}  // namespace
+}  // namespace evb
+
+extern "C" {
+
 int evb_de_optimize(evb_de e, evb_problem objective, evb_scratch s, void* pop, int64_t ldp, void* fitness, double lb,
                     double ub, int64_t max_fes, evb_rng rng, int* best_index, double* best_fitness, int* generations,
                     void* stream) {
   return guarded([&] {
-    // de/engine.hpp:107-133
     require(e && objective && rng && pop && fitness, "de_optimize: null argument");
     require(max_fes > 0, "evolution_state: max_fes must be positive");
     require(e->P >= 4, "init_population: pop_size must be at least 4");
     if (objective->p.dim != e->D) throw invalid_argument("de_optimize: problem dimension mismatch");
+    e->gen_offset = 0;
+    const int g = optimize_impl(e, objective, s ? s : e->eval_scratch, pop, ldp, fitness, lb, ub, max_fes, rng,
+                                static_cast<cudaStream_t>(stream), [] { return false; }, best_index, best_fitness);
+    if (generations) *generations = g;
+  });
+}
+
+// hybrid::restart_run (hybrid/restart.hpp:37-88) around this engine's optimize: fresh engine state
+// (adapter, archive, population size) per run, stop once since_improvement >= stagnation_evals,
+// until the total budget is spent; the best over all runs.
+int evb_de_optimize_restart(evb_de e, evb_problem objective, evb_scratch s, void* pop, int64_t ldp, void* fitness,
+                            double lb, double ub, int64_t total_budget, int64_t stagnation_evals, double epsilon,
+                            evb_rng rng, double* best_fitness, int* engine_runs, int64_t* evaluations, void* stream) {
+  return guarded([&] {
+    require(e && objective && rng && pop && fitness, "de_optimize_restart: null argument");
+    require(stagnation_evals >= 1, "restart: stagnation_evals must be at least 1");
+    require(epsilon >= 0.0, "restart: epsilon must be non-negative");
+    require(total_budget >= e->P_alloc, "restart: budget below one initialization");
+    if (objective->p.dim != e->D) throw invalid_argument("de_optimize_restart: problem dimension mismatch");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     evb_scratch_s* sc = s ? s : e->eval_scratch;
-    restore_size(e);
-    de_init_population(e, pop, ldp, lb, ub, rng, st);
-    eval_request rq{};
-    rq.prob = &objective->p;
-    rq.scratch = sc;
-    rq.X = pop;
-    rq.n = e->P;
-    rq.ldx = ldp;
-    rq.out = fitness;
-    rq.ldo = e->P;
-    rq.n_out = 1;
-    rq.kinds[0] = objective->p.kind;
-    rq.biases[0] = objective->p.bias;
-    rq.stream = st;
-    rq.scalar_trig = true;
-    eval_dispatch(rq);
-    if (e->rec) recorder_observe(e->rec, e->rec_run, fitness, e->P, st);  // initial evaluations
-    e->max_fes = max_fes;  // evolution_state st(max_fes, ...); st.add_fes(P) for the initial members
-    e->fes = e->P;
-    e->gen_count = 0;
-    int gens = 0;
-    while (e->fes < max_fes) {
-      de_generation(e, &objective->p, sc, pop, ldp, fitness, lb, ub, rng, st);
-      ++gens;
-    }
-    // best (core/population.hpp:59-65): lowest fitness, ties to the lowest index
-    const size_t es = e->dtype == EVB_F64 ? 8 : 4;
-    std::vector<uint8_t> f(es * e->P);
-    EVB_CUDA(cudaMemcpyAsync(f.data(), fitness, es * e->P, cudaMemcpyDeviceToHost, st));
-    EVB_CUDA(cudaStreamSynchronize(st));
-    int best = 0;
-    auto val = [&](int i) {
-      return e->dtype == EVB_F64 ? reinterpret_cast<double*>(f.data())[i] : double(reinterpret_cast<float*>(f.data())[i]);
+    if (!e->d_mon) EVB_CUDA(cudaMalloc(&e->d_mon, 3 * sizeof(double)));
+    const double init[3] = {std::numeric_limits<double>::infinity(), 0.0, 0.0};
+    EVB_CUDA(cudaMemcpyAsync(e->d_mon, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    e->mon_on = 1;
+    e->mon_eps = epsilon;
+    e->gen_offset = 0;
+    double best = std::numeric_limits<double>::infinity();
+    int runs = 0;
+    double h[3] = {0, 0, 0};
+    auto read_mon = [&] {
+      EVB_CUDA(cudaMemcpyAsync(h, e->d_mon, sizeof(h), cudaMemcpyDeviceToHost, st));
+      EVB_CUDA(cudaStreamSynchronize(st));
     };
-    for (int i = 1; i < e->P; ++i)
-      if (val(i) < val(best)) best = i;
-    if (best_index) *best_index = best;
-    if (best_fitness) *best_fitness = val(best);
-    if (generations) *generations = gens;
+    try {
+      for (;;) {
+        read_mon();
+        if (int64_t(h[2]) >= total_budget) break;
+        const double zero = 0.0;  // since_improvement = 0 for the new engine
+        EVB_CUDA(cudaMemcpyAsync(e->d_mon + 1, &zero, sizeof(double), cudaMemcpyHostToDevice, st));
+        if (e->dtype == EVB_F64) reset_adapter<double>(e);  // make_engine(): a fresh engine
+        else reset_adapter<float>(e);
+        EVB_CUDA(cudaMemsetAsync(e->d_arch_size, 0, sizeof(int), st));
+        const int64_t remaining = total_budget - int64_t(h[2]);
+        double cand = 0.0;
+        optimize_impl(e, objective, sc, pop, ldp, fitness, lb, ub, remaining, rng, st,
+                      [&] {
+                        read_mon();
+                        return int64_t(h[1]) >= stagnation_evals;
+                      },
+                      nullptr, &cand);
+        e->gen_offset += e->gen_count;  // generation_offset = last reported generation
+        ++runs;
+        if (cand < best) best = cand;
+        read_mon();
+        if (int64_t(h[1]) < stagnation_evals) break;  // the budget ran out rather than stagnation
+      }
+    } catch (...) {
+      e->mon_on = 0;
+      throw;
+    }
+    e->mon_on = 0;
+    if (best_fitness) *best_fitness = best;
+    if (engine_runs) *engine_runs = runs;
+    if (evaluations) *evaluations = int64_t(h[2]);
   });
 }
 

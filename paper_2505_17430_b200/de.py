@@ -107,6 +107,8 @@ def _sigs():
         "evb_de_archive_capacity": (c_int, [vp]),
         "evb_de_p_count": (c_int, [vp]),
         "evb_de_pop_size": (c_int, [vp]),
+        "evb_de_optimize_restart": (c_int, [vp, vp, vp, vp, i64, vp, c_double, c_double, i64, i64, c_double, vp,
+                                            P(c_double), P(c_int), P(i64), vp]),
         "evb_de_set_budget": (c_int, [vp, i64, i64]),
         "evb_de_last_reduction": (c_int, [vp, P(c_int), P(c_int), P(i64)]),
         "evb_de_generation": (c_int, [vp, vp, vp, vp, i64, vp, c_double, c_double, vp, vp]),
@@ -268,6 +270,19 @@ class DEEngine:
                                          ub, max_fes, rng.handle, ctypes.byref(bi), ctypes.byref(bf),
                                          ctypes.byref(g), _stream_ptr(stream)), "de_optimize")
         return {"best_index": bi.value, "best_fitness": bf.value, "generations": g.value}
+
+    def optimize_restart(self, problem: ProblemInstance, pop, fitness, lb: float, ub: float, total_budget: int,
+                         stagnation_evals: int, epsilon: float, rng: Rng, scratch: EvalScratch | None = None,
+                         stream=None):
+        """hybrid::restart_run around this engine (the "restart-lshade" preset with an L-SHADE
+        configuration): fresh engine states until the budget is spent."""
+        p, ld, f = self._pop(pop, fitness)
+        bf, runs, ev = ctypes.c_double(), ctypes.c_int(), ctypes.c_int64()
+        check(_lib.lib().evb_de_optimize_restart(self._h, problem.handle, scratch.handle if scratch else None, p, ld, f,
+                                                 lb, ub, total_budget, stagnation_evals, epsilon, rng.handle,
+                                                 ctypes.byref(bf), ctypes.byref(runs), ctypes.byref(ev),
+                                                 _stream_ptr(stream)), "de_optimize_restart")
+        return {"best_fitness": bf.value, "engine_runs": runs.value, "evaluations": ev.value}
 
     def _np(self):
         return np.float64 if self.dtype == EVB_F64 else np.float32

@@ -362,3 +362,25 @@ def test_lshade_reduction_lockstep(dev, rate):
     assert flips <= 3
     if rate < 1.0:
         assert shrunk > 0
+
+
+@pytest.mark.parametrize("stagnation,budget", [(150, 3000), (400, 2500)])
+def test_restart_lshade_matches_reference(dev, stagnation, budget):
+    # the "restart-lshade" preset: hybrid::restart_run (hybrid/restart.hpp) around L-SHADE, on the
+    # reference's native stream (WORDS mode) — the GPU restarts at the same evaluations and spends
+    # the same budget; the best matches the reference's (sphere: transcendental-free evaluation)
+    from paper_2505_17430_b200.de import preset_lshade
+    P, D, seed = 20, 5, 99
+    o, m = O.shift_rotation(seed, D)
+    cfg = preset_lshade(0.11, P, 1.0, n_min=4)
+    prob = evb.ProblemInstance.base(evb.BaseKind.sphere, o, m, 0.0)
+    eng = DEEngine(cfg, P, D)
+    rng = Rng.words(O.rng_words(seed, 0, 400000))
+    pop = torch.empty((P, D), dtype=torch.float64, device=dev)
+    fit = torch.empty(P, dtype=torch.float64, device=dev)
+    got = eng.optimize_restart(prob, pop, fit, -100.0, 100.0, budget, stagnation, 1e-8, rng)
+    ref = O.ref_restart_lshade(seed, 0, P, D, P, 0.11, 1.0, 4, budget, stagnation, 1e-8, 0, o, m)
+    assert got["engine_runs"] == ref["engine_runs"] and got["engine_runs"] >= 2
+    assert got["evaluations"] == ref["evaluations"]
+    assert abs(got["best_fitness"] - ref["best_fitness"]) <= 1e-10 * max(1.0, abs(ref["best_fitness"]))
+    assert not rng.state()["overflow"]
