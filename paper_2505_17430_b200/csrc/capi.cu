@@ -464,20 +464,42 @@ void host_eval(const evb_problem* probs, int n_prob, evb_scratch s, const void* 
       EVB_CUDA(cudaMalloc(&s->gate, kMaxGates * sizeof(unsigned)));
       EVB_CUDA(cudaMemset(s->gate, 0, kMaxGates * sizeof(unsigned)));
     }
-    // chunk boundaries (multiples of 16 columns = the GEMM's K-slice): uniform, or halving
-    // so the compute left after the last chunk lands is small
+    // Rows: when the multi-problem kernel needs two waves, the first wave's rows (all their
+    // column chunks) cross first and the rest follow, so the second wave's data lands while the
+    // first computes (kgate_rows).  Columns: chunk boundaries are multiples of 16 (the GEMM's
+    // K-slice): uniform, halving (single wave: the compute left after the last chunk lands is
+    // small), or EVB_H2D_WIDTHS="w0,w1,..." (tuning aid).
+    static const char* rows_env = std::getenv("EVB_H2D_ROWSPLIT");
+    static const char* widths_env = std::getenv("EVB_H2D_WIDTHS");
+    const int64_t rows_a =
+        multi && !(rows_env && std::string(rows_env) == "0") ? multi_first_wave_rows(n_prob, n_points, D) : 0;
+    const bool uniform = rows_a > 0 ? !(split_env && std::string(split_env) == "geo") : !geometric;
+    std::vector<int64_t> widths;
+    if (widths_env) {
+      std::string w = widths_env;
+      for (size_t pos = 0; pos < w.size();) {
+        size_t nx = w.find(',', pos);
+        if (nx == std::string::npos) nx = w.size();
+        widths.push_back(std::max<int64_t>(16, round_up(std::atoll(w.substr(pos, nx - pos).c_str()), 16)));
+        pos = nx + 1;
+      }
+    }
     int n_chunks = 0;
     int64_t c0 = 0;
+    const int max_chunks = rows_a > 0 ? std::min(want, kMaxGates / 2) : want;
     while (c0 < D) {
       int64_t w;
-      if (n_chunks == want - 1) w = D - c0;
-      else if (geometric) w = round_up((D - c0 + 1) / 2, 16);
-      else w = round_up((D + want - 1) / want, 16);
+      if (n_chunks == max_chunks - 1) w = D - c0;
+      else if (!widths.empty()) w = n_chunks < int(widths.size()) ? widths[size_t(n_chunks)] : D - c0;
+      else if (!uniform) w = round_up((D - c0 + 1) / 2, 16);
+      else w = round_up((D + max_chunks - 1) / max_chunks, 16);
       w = std::min<int64_t>(std::max<int64_t>(w, 16), D - c0);
       rq.kgate_end[n_chunks++] = int(c0 + w);
       c0 += w;
     }
     rq.kgate_n = n_chunks;
+    rq.kgate_rows = int(rows_a);
+    const int n_groups = rows_a > 0 ? 2 : 1;
     const unsigned epoch = ++s->gate_epoch == 0 ? ++s->gate_epoch : s->gate_epoch;
     // EVB_H2D_TRACE=1: print the copy / kernel timeline of each call (tuning aid)
     static const bool trace = std::getenv("EVB_H2D_TRACE") != nullptr;
@@ -487,18 +509,22 @@ void host_eval(const evb_problem* probs, int n_prob, evb_scratch s, const void* 
     if (trace) EVB_CUDA(cudaEventRecord(tev[0], s->copy_stream));
     // the previous call on this scratch synchronised st, so dx is free to overwrite
     bool gates_ok = true;
-    for (int c = 0; c < n_chunks; ++c) {
-      const int64_t b = c ? rq.kgate_end[c - 1] : 0, w = rq.kgate_end[c] - b;
-      EVB_CUDA(cudaMemcpy2DAsync(static_cast<uint8_t*>(s->dx) + b * es, ldd * es,
-                                 static_cast<const uint8_t*>(X_host) + b * es, ldx * es, w * es, n_points,
-                                 cudaMemcpyHostToDevice, s->copy_stream));
-      if (gates_ok) {
-        EVB_CUDA(cudaEventRecord(s->ev_chunk[c], s->copy_stream));
-        EVB_CUDA(cudaStreamWaitEvent(s->gate_stream, s->ev_chunk[c], 0));
-        // a driver that refuses stream memory operations: fall back to waiting for all of X
-        gates_ok = wv(s->gate_stream, CUdeviceptr(s->gate + c), epoch, 0) == CUDA_SUCCESS;
+    for (int g = 0; g < n_groups; ++g) {
+      const int64_t r0 = g ? rows_a : 0, nr = n_groups == 1 ? n_points : (g ? n_points - rows_a : rows_a);
+      for (int c = 0; c < n_chunks; ++c) {
+        const int gi = g * n_chunks + c;
+        const int64_t b = c ? rq.kgate_end[c - 1] : 0, w = rq.kgate_end[c] - b;
+        EVB_CUDA(cudaMemcpy2DAsync(static_cast<uint8_t*>(s->dx) + (r0 * ldd + b) * es, ldd * es,
+                                   static_cast<const uint8_t*>(X_host) + (r0 * ldx + b) * es, ldx * es, w * es, nr,
+                                   cudaMemcpyHostToDevice, s->copy_stream));
+        if (gates_ok) {
+          EVB_CUDA(cudaEventRecord(s->ev_chunk[gi], s->copy_stream));
+          EVB_CUDA(cudaStreamWaitEvent(s->gate_stream, s->ev_chunk[gi], 0));
+          // a driver that refuses stream memory operations: fall back to waiting for all of X
+          gates_ok = wv(s->gate_stream, CUdeviceptr(s->gate + gi), epoch, 0) == CUDA_SUCCESS;
+        }
+        if (trace) EVB_CUDA(cudaEventRecord(tev[1 + gi], s->copy_stream));
       }
-      if (trace) EVB_CUDA(cudaEventRecord(tev[1 + c], s->copy_stream));
     }
     EVB_CUDA(cudaEventRecord(s->ev_x_ready, s->copy_stream));
     rq.kgate = gates_ok ? s->gate : nullptr;
@@ -511,19 +537,21 @@ void host_eval(const evb_problem* probs, int n_prob, evb_scratch s, const void* 
       rqs[0] = rq;
       if (!gemm_eval_multi(rqs.data(), n_prob, s->dx, ldd)) multi = false;
     }
+    if (!multi && rows_a > 0) rq.kgate = nullptr;  // single-problem kernels know one gate group only
     if (!multi) eval_dispatch(rq);
-    if (trace) EVB_CUDA(cudaEventRecord(tev[n_chunks + 1], st));
+    const int n_ev = n_chunks * n_groups;
+    if (trace) EVB_CUDA(cudaEventRecord(tev[n_ev + 1], st));
     EVB_CUDA(cudaStreamWaitEvent(st, s->ev_x_ready, 0));
     if (trace) {
       if (dst[0] != outs_host[0])
         EVB_CUDA(cudaMemcpyAsync(outs_host[0], dst[0], size_t(n_points) * es, cudaMemcpyDeviceToHost, st));
-      EVB_CUDA(cudaEventRecord(tev[n_chunks + 2], st));
+      EVB_CUDA(cudaEventRecord(tev[n_ev + 2], st));
       EVB_CUDA(cudaStreamSynchronize(st));
-      std::string line = "[evb h2d]";
-      for (int c = 1; c <= n_chunks + 2; ++c) {
+      std::string line = "[evb h2d] rows_a " + std::to_string(rows_a) + " |";
+      for (int c = 1; c <= n_ev + 2; ++c) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, tev[0], tev[c]);
-        line += (c == n_chunks + 1 ? " kernel_end " : c == n_chunks + 2 ? " d2h_end " : " ") +
+        line += (c == n_ev + 1 ? " kernel_end " : c == n_ev + 2 ? " d2h_end " : " ") +
                 std::to_string(int(ms * 1000.f));
       }
       std::fprintf(stderr, "%s us\n", line.c_str());

@@ -74,6 +74,8 @@ struct fused_params {
   int kgate_n;
   int kgate_end[8];
   unsigned kgate_epoch;
+  int kgate_rows;   // > 0: rows >= kgate_rows wait on the second gate group kgate[kgate_n + c]
+  int tiles_nfast;  // multi kernel: blockIdx.x walks column tiles (row blocks form the waves)
 };
 
 // cosine of the fused epilogue: library cos for fp64.  fp32 (a tolerance path: 3xTF32 / FFMA
@@ -449,7 +451,8 @@ __global__ void __launch_bounds__(f64m_cfg<NP>::THREADS, 1)
   int* last_flag = reinterpret_cast<int*>(empty + C::STAGES);  // NP flags
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * C::BM, n0 = blockIdx.y * C::BN;
+  const int mtile = p0.tiles_nfast ? blockIdx.y : blockIdx.x, ntile = p0.tiles_nfast ? blockIdx.x : blockIdx.y;
+  const int m0 = mtile * C::BM, n0 = ntile * C::BN;
   const int KT = (p0.D + C::KB - 1) / C::KB;
 
   if (threadIdx.x == 0) {
@@ -471,8 +474,9 @@ __global__ void __launch_bounds__(f64m_cfg<NP>::THREADS, 1)
         const int s = kb % C::STAGES;
         if (kb >= C::STAGES) ptx::mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
         if (p0.kgate) {
+          const int gbase = (p0.kgate_rows > 0 && m0 >= p0.kgate_rows) ? p0.kgate_n : 0;
           while (kb * C::KB >= chunk_end) {
-            ptx::wait_gate(p0.kgate + chunk, p0.kgate_epoch);
+            ptx::wait_gate(p0.kgate + gbase + chunk, p0.kgate_epoch);
             chunk_end = chunk + 1 < p0.kgate_n ? p0.kgate_end[chunk] : 1 << 30;
             ++chunk;
           }
@@ -544,7 +548,7 @@ __global__ void __launch_bounds__(f64m_cfg<NP>::THREADS, 1)
   ptx::named_bar_sync(2 + grp, C::WM * 32);
   const fused_params<double>& pg = grp == 0 ? p0 : (grp == 1 ? p1 : p2);
   tile_epilogue<double, C::BM, C::BN>(pg, zt, C::LDT, m0, n0, threadIdx.x - grp * C::WM * 32, C::WM * 32,
-                                      last_flag + grp, blockIdx.x, blockIdx.y, 2 + grp);
+                                      last_flag + grp, mtile, ntile, 2 + grp);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1278,6 +1282,34 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
   }
 }
 
+int multi_first_wave_rows(int np, int64_t n_points, int64_t dim) {
+  if (np < 2 || np > 3) return 0;
+  constexpr int BM = kMultiBM, BN = kMultiBN;
+  const int64_t n_ntiles = (dim + BN - 1) / BN, n_mtiles = (n_points + BM - 1) / BM;
+  int dev = 0, sms = 0, per_sm = 0;
+  EVB_CUDA(cudaGetDevice(&dev));
+  EVB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (np == 3) {
+    EVB_CUDA(cudaFuncSetAttribute(eval_f64_dmma_multi_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  f64m_cfg<3>::SMEM));
+    EVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eval_f64_dmma_multi_kernel<3>,
+                                                           f64m_cfg<3>::THREADS, f64m_cfg<3>::SMEM));
+  } else {
+    EVB_CUDA(cudaFuncSetAttribute(eval_f64_dmma_multi_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  f64m_cfg<2>::SMEM));
+    EVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eval_f64_dmma_multi_kernel<2>,
+                                                           f64m_cfg<2>::THREADS, f64m_cfg<2>::SMEM));
+  }
+  const int64_t wave = int64_t(sms) * std::max(per_sm, 1);
+  if (n_ntiles * n_mtiles <= wave) return 0;
+  // row blocks the first wave covers completely (EVB_H2D_ROWS=ceil: also the partly covered one,
+  // tuning aid); the first wave's few tiles of the next row block wait for the second group
+  static const char* env = std::getenv("EVB_H2D_ROWS");
+  const bool ceil_rows = env && std::string(env) == "ceil";
+  const int64_t rb = ceil_rows ? (wave + n_ntiles - 1) / n_ntiles : wave / n_ntiles;
+  return rb >= n_mtiles || rb == 0 ? 0 : int(rb * BM);
+}
+
 // NP base problems (same D) on one device X: one multi-problem K1 launch; rqs[g] carries problem
 // g's kinds / biases / output, rqs[0] the gates.  Returns false when the shapes do not fit.
 bool gemm_eval_multi(const eval_request* rqs, int np, const void* X, int64_t ldx) {
@@ -1331,10 +1363,14 @@ bool gemm_eval_multi(const eval_request* rqs, int np, const void* X, int64_t ldx
     fp[0].kgate_n = rqs[0].kgate_n;
     for (int c = 0; c < rqs[0].kgate_n; ++c) fp[0].kgate_end[c] = rqs[0].kgate_end[c];
     fp[0].kgate_epoch = rqs[0].kgate_epoch;
+    fp[0].kgate_rows = rqs[0].kgate_rows;
   } else if (rqs[0].x_ready) {
     EVB_CUDA(cudaStreamWaitEvent(st, rqs[0].x_ready, 0));
   }
-  dim3 grid(n_mtiles, n_ntiles);
+  // with the rows split into two gate groups the first wave must be the first rows' tiles
+  const bool nfast = rqs[0].kgate && rqs[0].kgate_rows > 0;
+  fp[0].tiles_nfast = nfast ? 1 : 0;
+  dim3 grid(nfast ? n_ntiles : n_mtiles, nfast ? n_mtiles : n_ntiles);
   if (np == 3) {
     using C = f64m_cfg<3>;
     static bool attr = false;

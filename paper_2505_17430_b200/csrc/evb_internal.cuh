@@ -161,7 +161,7 @@ struct evb_scratch_s {
   unsigned* gate = nullptr;  // kMaxGates words
   unsigned gate_epoch = 0;
   cudaEvent_t ev_x_ready = nullptr;
-  cudaEvent_t ev_chunk[8] = {};
+  cudaEvent_t ev_chunk[16] = {};
 };
 
 namespace evb {
@@ -208,10 +208,18 @@ struct eval_request {
   int kgate_n = 0;
   int kgate_end[8] = {};  // exclusive end column of chunk c (multiples of 16 but the last)
   unsigned kgate_epoch = 0;
+  // > 0 (multi-problem K1 only): rows [kgate_rows, n) arrive after rows [0, kgate_rows), in the
+  // same column chunks, gated by kgate[kgate_n + c]; the kernel then runs the first rows' tiles
+  // as its first wave
+  int kgate_rows = 0;
   cudaEvent_t x_ready = nullptr;
 };
 
-constexpr int kMaxGates = 8;
+constexpr int kMaxGates = 16;
+
+// rows whose tiles make up the first wave of the multi-problem K1 at this size (a multiple of
+// its row tile), or 0 when every tile is resident at once (eval_gemm.cu)
+int multi_first_wave_rows(int np, int64_t n_points, int64_t dim);
 
 void eval_dispatch(const eval_request& rq);
 // true when eval_dispatch runs the request on the fused fp64 GEMM, whose producer honours kgate

@@ -282,6 +282,34 @@ def test_host_many_one_copy_equals_device(config1, dev):
 
 
 @pytest.mark.parametrize("n_prob", [2, 3])
+def test_host_many_row_split_gates(config1, dev, n_prob):
+    # two or three problems on one host population: one multi-problem launch whose first wave is
+    # the first rows' tiles, fed by two gate groups (first-wave rows, then the rest) of column
+    # chunks; bit-identical to the device path, call after call, at one- and two-wave sizes
+    o, m, X = config1
+    o2, m2 = O.shift_rotation(8, 1000)
+    specs = [(K.elliptic, o, m, 1.0), (K.rastrigin, o2, m2, 2.0), (K.ackley, o, m2, 3.0)][:n_prob]
+    probs = [evb.ProblemInstance.base(k, oo, mm, b) for k, oo, mm, b in specs]
+    big = np.concatenate([X, O.population(77, 1000, 1000)])  # 2024 rows: 32 row tiles
+    sc = evb.EvalScratch()
+    for rows in (1024, 2024, 600, 1024, 37, 2024):
+        Xr = np.ascontiguousarray(big[:rows])
+        Xd = torch.from_numpy(Xr).to(dev)
+        outs = [torch.empty(rows, dtype=torch.float64, device=dev) for _ in probs]
+        evb.evaluate_batch_problems(probs, Xd, evb.EvalScratch(), outs)
+        torch.cuda.synchronize()
+        got = evb.batched_evaluate_many(probs, Xr, sc)
+        for g, w in zip(got, outs):
+            assert np.array_equal(g, w.cpu().numpy()), rows
+    # a non-contiguous view of a wider array
+    wide = np.zeros((1024, 1003))
+    wide[:, :1000] = X
+    want = evb.batched_evaluate_many(probs, X, sc)
+    for g, w in zip(evb.batched_evaluate_many(probs, wide[:, :1000], sc), want):
+        assert np.array_equal(g, w)
+
+
+@pytest.mark.parametrize("n_prob", [2, 3])
 def test_problems_one_launch_bit_identical(config1, dev, n_prob):
     # several fp64 problems on one X in ONE launch (stages carry X once) == one launch per problem,
     # bit for bit (same tiles, K order, epilogue); with different shifts / rotations per problem
