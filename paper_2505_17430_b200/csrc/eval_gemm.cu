@@ -29,6 +29,8 @@
 #include <cstdlib>
 #include <string>
 #include <type_traits>
+#include <vector>
+#include <cstdio>
 
 #include "evb_internal.cuh"
 #include "evb_math.cuh"
@@ -76,6 +78,7 @@ struct fused_params {
   unsigned kgate_epoch;
   int kgate_rows;   // > 0: rows >= kgate_rows wait on the second gate group kgate[kgate_n + c]
   int tiles_nfast;  // multi kernel: blockIdx.x walks column tiles (row blocks form the waves)
+  unsigned long long* dbg_ts;  // EVB_K1_TIMELINE=1 (tuning aid): per-CTA globaltimer phase stamps
 };
 
 // cosine of the fused epilogue: library cos for fp64.  fp32 (a tolerance path: 3xTF32 / FFMA
@@ -94,6 +97,35 @@ __device__ __forceinline__ float epi_cos<float>(float x) {
   return __cosf(r);
 }
 
+// cos(2 pi v) of the Rastrigin / Ackley terms.  fp64: the period is taken out exactly
+// (r = v - rint(v), rint by the 1.5 * 2^52 round-to-nearest trick: two adds, |r| <= 1/2) and
+// cos(2 pi r) is a degree-11 polynomial in r^2 (Chebyshev interpolation on [0, 1/4], fitted in
+// 50-digit arithmetic; max error 8e-16 over [-1/2, 1/2] evaluated in double) — 14 FP64 ops on
+// the DFMA pipe instead of the library cos's reduction.  It differs from the reference's
+// cos(fl(2 pi * v)) by the rounding of that product (|2 pi v| * 2^-53, ~1e-13 at |v| ~ 100)
+// plus ~1e-15: far inside the 1e-10 relative fitness tolerance of this tensor-core-order path.
+template <typename T>
+__device__ __forceinline__ T epi_cos2pi(T v) { return epi_cos<T>(fop<T>::mul(two_pi_v<T>(), v)); }
+template <>
+__device__ __forceinline__ double epi_cos2pi<double>(double v) {
+  // |v| >= 2^51 (v a multiple of 1/2) takes rint; inf / NaN give NaN like cos
+  const double t = fabs(v) < 0x1p51 ? __dsub_rn(__dadd_rn(v, 0x1.8p52), 0x1.8p52) : rint(v);
+  const double r = __dsub_rn(v, t);
+  const double u = __dmul_rn(r, r);
+  double c = -0.0002900600501912893;
+  c = fma(c, u, 0.003758590561310354);
+  c = fma(c, u, -0.03637490036340231);
+  c = fma(c, u, 0.28200407958316315);
+  c = fma(c, u, -1.7143904138098518);
+  c = fma(c, u, 7.903536340077173);
+  c = fma(c, u, -26.42625678121189);
+  c = fma(c, u, 60.24464137178173);
+  c = fma(c, u, -85.45681720669127);
+  c = fma(c, u, 64.93939402266825);
+  c = fma(c, u, -19.739208802178716);
+  return fma(c, u, 1.0);
+}
+
 template <typename T>
 __device__ __forceinline__ T term_value(int term, T v, int col, const T* ell_w) {
   using F = fop<T>;
@@ -101,10 +133,10 @@ __device__ __forceinline__ T term_value(int term, T v, int col, const T* ell_w) 
     case TERM_SQ: return F::mul(v, v);
     case TERM_WSQ: return elliptic_term<T>(ell_w[col], v);
     case TERM_RAST: {  // v*v - T(10) * cos(two_pi * v) + T(10)  (problems/batch.hpp:161)
-      const T c = epi_cos<T>(F::mul(two_pi_v<T>(), v));
+      const T c = epi_cos2pi<T>(v);
       return F::add(F::sub(F::mul(v, v), F::mul(T(10), c)), T(10));
     }
-    case TERM_COS: return epi_cos<T>(F::mul(two_pi_v<T>(), v));
+    case TERM_COS: return epi_cos2pi<T>(v);
     case TERM_TAIL: return col >= 1 ? F::mul(v, v) : T(0);
     case TERM_HEAD: return col == 0 ? v : T(0);
     case TERM_GCOS: return epi_cos<T>(F::div(v, F::sqrt_(T(col + 1))));
@@ -179,22 +211,41 @@ __device__ __forceinline__ void epilogue_rows(const fused_params<T>& p, const T*
   constexpr int CPL = (BN + 31) / 32;  // columns per lane
   constexpr bool prod = TERM == TERM_GCOS;
   const T ident = prod ? T(1) : T(0);
+  // per-lane column data once per tile (elliptic weight, Griewank sqrt(i+1)); tile edges are
+  // predicated (a select keeps the running value), so every element of the unrolled 8-row x
+  // CPL-column block is an independent straight-line chain (no per-element branches: ILP)
+  int cl[CPL];
+  bool cv[CPL];
+  T cw[CPL];
+#pragma unroll
+  for (int cc = 0; cc < CPL; ++cc) {
+    const int c = lane + 32 * cc;
+    cv[cc] = c < BN && n0 + c < p.D;
+    cl[cc] = cv[cc] ? c : 0;
+    const int col = n0 + cl[cc];
+    if (TERM == TERM_WSQ) cw[cc] = p.ell_w[col];
+    else if (TERM == TERM_GCOS) cw[cc] = F::sqrt_(T(col + 1));
+    else cw[cc] = T(0);
+  }
+  const uint32_t zs = static_cast<uint32_t>(__cvta_generic_to_shared(zt));
   for (int r0 = 0; r0 < rpw; r0 += 8) {
     T s[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int r = warp + (r0 + q) * nwarps;
-      s[q] = ident;
-      if (r0 + q < rpw && r < BM) {
+    for (int q = 0; q < 8; ++q) s[q] = ident;
 #pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) {
-          const int c = lane + 32 * cc;
-          const int col = n0 + c;
-          if (c < BN && col < p.D) {
-            const T v = term_value<T>(TERM, zt[r * ldt + c], col, p.ell_w);
-            s[q] = prod ? F::mul(s[q], v) : F::add(s[q], v);
-          }
-        }
+    for (int cc = 0; cc < CPL; ++cc) {
+      const int col = n0 + cl[cc];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int r = warp + (r0 + q) * nwarps;
+        const bool ok = cv[cc] && r0 + q < rpw && r < BM;
+        const T z = ptx::lds<T>(zs + uint32_t(((ok ? r : 0) * ldt + cl[cc]) * int(sizeof(T))));
+        T v;
+        if (TERM == TERM_WSQ) v = elliptic_term<T>(cw[cc], z);
+        else if (TERM == TERM_GCOS) v = epi_cos<T>(F::div(z, cw[cc]));
+        else v = term_value<T>(TERM, z, col, p.ell_w);
+        const T acc = prod ? F::mul(s[q], v) : F::add(s[q], v);
+        s[q] = ok ? acc : s[q];
       }
     }
 #pragma unroll
@@ -242,33 +293,67 @@ __device__ void tile_epilogue(const fused_params<T>& p, const T* zt, int ldt, in
       default: epilogue_rows<TERM_GCOS, T, BM, BN>(p, zt, ldt, m0, n0, warp, lane, nwarps, rpw, ch, ntile); break;
     }
   }
-  __threadfence();
+  // ticket: the barrier orders every thread's partial stores before thread 0's gpu-scope fence
+  // (cumulative release), and the last CTA's fence after the atomic is the acquire side
   ptx::named_bar_sync(bar_id, nthreads);
   if (tid == 0) {
+    __threadfence();
     const unsigned ticket = atomicAdd(&p.counters[mtile], 1u);
-    *last_flag = (ticket == unsigned(p.n_ntiles - 1)) ? 1 : 0;
+    const int last = (ticket == unsigned(p.n_ntiles - 1)) ? 1 : 0;
+    if (last) __threadfence();
+    *last_flag = last;
   }
   ptx::named_bar_sync(bar_id, nthreads);
+  if (p.dbg_ts && tid == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.dbg_ts[8 * (ntile * gridDim.x + mtile) + 3] = t;
+  }
   if (!*last_flag) return;
-  __threadfence();
-  for (int r = tid; r < BM; r += nthreads) {
-    const int row = m0 + r;
-    if (row >= p.P) continue;
-    T chv[kMaxCh];
-    for (int ch = 0; ch < p.n_ch; ++ch) {
-      const bool prod = term_is_product(p.ch_term[ch]);
-      const T* src = p.partial + size_t(ch) * p.n_ntiles * p.P + row;
-      T v = __ldcg(src);
-      for (int t = 1; t < p.n_ntiles; ++t) {
-        const T x = __ldcg(src + size_t(t) * p.P);
-        v = prod ? F::mul(v, x) : F::add(v, x);
-      }
-      chv[ch] = v;
+  // N-tile partials combined in tile order per channel, eight L2 loads in flight per round (a
+  // dependent load-add chain of n_ntiles L2 round trips sat on the kernel's critical path).
+  // When the CTA has a thread per (row, channel), the channels' chains run in parallel and meet
+  // in shared memory (the parked tile is dead by now) before the final formula.
+  auto chain = [&](int ch, int row) {
+    const bool prod = term_is_product(p.ch_term[ch]);
+    const T* src = p.partial + size_t(ch) * p.n_ntiles * p.P + row;
+    T v = __ldcg(src);
+    for (int t0 = 1; t0 < p.n_ntiles; t0 += 8) {
+      T x[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (t0 + q < p.n_ntiles) x[q] = __ldcg(src + size_t(t0 + q) * p.P);
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (t0 + q < p.n_ntiles) v = prod ? F::mul(v, x[q]) : F::add(v, x[q]);
     }
+    return v;
+  };
+  auto final_row = [&](int row, const T* chv) {
     for (int o = 0; o < p.n_out; ++o) {
       const T s0 = chv[p.out_ch0[o]];
       const T s1 = p.out_ch1[o] >= 0 ? chv[p.out_ch1[o]] : T(0);
       p.out[o * p.ldo + row] = finalize<T>(p.out_kind[o], s0, s1, p.D, T(p.out_bias[o]));
+    }
+  };
+  if (p.n_ch > 1 && p.n_ch * BM <= nthreads) {
+    T* xs = const_cast<T*>(zt);  // [n_ch][BM]
+    const int ch = tid / BM, r = tid % BM;
+    if (ch < p.n_ch && m0 + r < p.P) xs[ch * BM + r] = chain(ch, m0 + r);
+    ptx::named_bar_sync(bar_id, nthreads);
+    for (int r2 = tid; r2 < BM; r2 += nthreads) {
+      if (m0 + r2 >= p.P) continue;
+      T chv[kMaxCh];
+      for (int c = 0; c < p.n_ch; ++c) chv[c] = xs[c * BM + r2];
+      final_row(m0 + r2, chv);
+    }
+  } else {
+    for (int r = tid; r < BM; r += nthreads) {
+      const int row = m0 + r;
+      if (row >= p.P) continue;
+      T chv[kMaxCh];
+      for (int c = 0; c < p.n_ch; ++c) chv[c] = chain(c, row);
+      final_row(row, chv);
     }
   }
   if (tid == 0) p.counters[mtile] = 0u;  // re-arm for the next launch
@@ -305,7 +390,7 @@ __global__ void __launch_bounds__(f64_cfg<BM, BN, WM, WN, STAGES>::THREADS, MINB
                          const fused_params<double> p) {
   using C = f64_cfg<BM, BN, WM, WN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   int* last_flag = reinterpret_cast<int*>(empty + STAGES);
@@ -313,6 +398,20 @@ __global__ void __launch_bounds__(f64_cfg<BM, BN, WM, WN, STAGES>::THREADS, MINB
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   const int KT = (p.D + C::KB - 1) / C::KB;
+  unsigned long long* ts = p.dbg_ts ? p.dbg_ts + 8 * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
+  auto stamp = [&](int i) {
+    if (ts && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      ts[i] = t;
+    }
+  };
+  stamp(0);
+  if (ts && threadIdx.x == 0) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    ts[7] = sm;
+  }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -363,6 +462,7 @@ __global__ void __launch_bounds__(f64_cfg<BM, BN, WM, WN, STAGES>::THREADS, MINB
   for (int kb = 0; kb < KT; ++kb) {
     const int s = kb % STAGES;
     ptx::mbar_wait(&full[s], (kb / STAGES) & 1);
+    if (kb == 0) stamp(1);
     const uint32_t sA = smem_base + s * C::STAGE_BYTES;
     const uint32_t sB = sA + C::A_BYTES;
     const uint32_t sO = sB + C::B_BYTES;
@@ -393,6 +493,7 @@ __global__ void __launch_bounds__(f64_cfg<BM, BN, WM, WN, STAGES>::THREADS, MINB
   // park the accumulator tile in the (drained) stage ring, then run the epilogue from smem
   // (measured: a register-direct epilogue — quad shuffles on the DMMA fragments, no parking —
   // was slower, 89 vs 81.6 us per batch: the inlined transcendental code bloats the kernel)
+  stamp(2);
   ptx::named_bar_sync(1, C::NCW * 32);
   double* zt = reinterpret_cast<double*>(smem);
   constexpr int LDT = BN + 1;
@@ -404,6 +505,8 @@ __global__ void __launch_bounds__(f64_cfg<BM, BN, WM, WN, STAGES>::THREADS, MINB
       for (int h = 0; h < 2; ++h) zt[(rA + i * 8 + g) * LDT + rB + j * 8 + 2 * t + h] = acc[i][j][h];
   ptx::named_bar_sync(1, C::NCW * 32);
   tile_epilogue<double, BM, BN>(p, zt, LDT, m0, n0, threadIdx.x, C::NCW * 32, last_flag, blockIdx.x, blockIdx.y, 1);
+  stamp(4);
+  if (ts && threadIdx.x == 0) ts[5] = *last_flag;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -445,7 +548,7 @@ __global__ void __launch_bounds__(f64m_cfg<NP>::THREADS, 1)
                                const __grid_constant__ fused_params<double> p2) {
   using C = f64m_cfg<NP>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + C::STAGES;
   int* last_flag = reinterpret_cast<int*>(empty + C::STAGES);  // NP flags
@@ -584,7 +687,7 @@ __global__ void __launch_bounds__(f64p_cfg<BM, BN, STAGES>::THREADS, 1)
                              const fused_params<double> p, int n_mtiles, int n_tiles) {
   using C = f64p_cfg<BM, BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   double* ebuf = reinterpret_cast<double*>(smem + STAGES * C::STAGE_BYTES);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES + 2 * C::EBUF_BYTES);
   uint64_t* empty = full + STAGES;
@@ -716,7 +819,7 @@ __global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
                          const fused_params<float> p) {
   using C = umma_cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* accfull = empty + C::STAGES;
@@ -888,7 +991,7 @@ __global__ void __launch_bounds__(f32_cfg<BM, BN, STAGES>::THREADS, 1)
                          const fused_params<float> p) {
   using C = f32_cfg<BM, BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   int* last_flag = reinterpret_cast<int*>(empty + STAGES);
@@ -1242,6 +1345,7 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
   if (!make_tma_2d(&tmM, rotation, dtype, uint64_t(ldm), uint64_t(D), uint64_t(ldm) * sizeof(T), KB, BN))
     throw runtime_error("gemm_eval: cannot encode the TMA descriptor of M");
   fp.n_ntiles = (D + BN - 1) / BN;
+  static const bool timeline = std::getenv("EVB_K1_TIMELINE") != nullptr;
   const int n_mtiles = (P + BM - 1) / BM;
   if (!zstore) {
     ensure_buffer(&sc->partial, &sc->partial_bytes, size_t(fp.n_ch) * fp.n_ntiles * P * sizeof(T), rq.stream);
@@ -1273,7 +1377,26 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
     }
     // (measured alternatives: 64 x 40 and 48 x 56 tiles at 3 CTAs / SM, 32 x 56 warp tiles —
     // all slower: 91, 115 and 146 us against 81.5 us per config-1 batch)
-    if (BM == 64 && BN == 56) launch_f64<64, 56, 4, 1, 6, 2>(tmX, tmM, fp, rq.stream);
+    if (BM == 64 && BN == 56 && timeline) {  // one synchronous launch, phase stamps appended to a CSV
+      const int nct = int(((P + BM - 1) / BM) * fp.n_ntiles);
+      unsigned long long* d = nullptr;
+      EVB_CUDA(cudaMalloc(&d, size_t(nct) * 8 * 8));
+      EVB_CUDA(cudaMemset(d, 0, size_t(nct) * 8 * 8));
+      fused_params<double> f2 = fp;
+      f2.dbg_ts = d;
+      launch_f64<64, 56, 4, 1, 6, 2>(tmX, tmM, f2, rq.stream);
+      EVB_CUDA(cudaStreamSynchronize(rq.stream));
+      std::vector<unsigned long long> h(size_t(nct) * 8);
+      EVB_CUDA(cudaMemcpy(h.data(), d, h.size() * 8, cudaMemcpyDeviceToHost));
+      cudaFree(d);
+      if (FILE* f = std::fopen("gpurun_out/k1_ts.csv", "a")) {
+        for (int c = 0; c < nct; ++c)
+          std::fprintf(f, "%d,%llu,%llu,%llu,%llu,%llu,%llu,%llu\n", c, h[c * 8 + 0], h[c * 8 + 1], h[c * 8 + 2],
+                       h[c * 8 + 3], h[c * 8 + 4], h[c * 8 + 5], h[c * 8 + 7]);
+        std::fprintf(f, "end\n");
+        std::fclose(f);
+      }
+    } else if (BM == 64 && BN == 56) launch_f64<64, 56, 4, 1, 6, 2>(tmX, tmM, fp, rq.stream);
     else if (BM == 64 && BN == 112) launch_f64<64, 112, 4, 2>(tmX, tmM, fp, rq.stream);
     else if (BM == 64 && BN == 128) launch_f64<64, 128, 4, 2>(tmX, tmM, fp, rq.stream);
     else launch_f64<32, 128, 2, 4>(tmX, tmM, fp, rq.stream);
