@@ -367,6 +367,46 @@ __device__ __forceinline__ uint32_t swz(int r, int kk) {
 }
 
 // ---------------------------------------------------------------------------------------
+// One 16-deep K-slice (one SWIZZLE_128B stage row) of a warp's (TM*8) x (TN*8) tile of
+// z += (X - o) M^T: four m8n8k4 DMMA steps.  The k order inside the slice is permuted so that
+// lane t's operands for steps 2p and 2p+1 sit in one 16-byte chunk (physical k = 4t + 2p + h,
+// chunk 2t + p): each fragment is one LDS.128 instead of two LDS.64, and the 8 lanes of a
+// quarter-warp phase (rows g, g+1; t = 0..3) hit 8 distinct chunks under the row XOR
+// swizzle (conflict-free).  The shift is subtracted in fp64 as the fragment is formed
+// (problems/batch.hpp:50).  Pair p+1's loads are issued before pair p's DMMAs.
+template <int TM, int TN>
+__device__ __forceinline__ void dmma_kslice(double (&acc)[TM][TN][2], uint32_t sA, uint32_t sB, uint32_t sO, int rA,
+                                            int rB, int g, int t) {
+  double2 a[2][TM], b[2][TN];
+  auto load = [&](int pp, int buf) {
+    const int ch = 2 * t + pp;
+    const double2 o = ptx::lds_f64x2(sO + (4 * t + 2 * pp) * 8);
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const int r = rA + i * 8 + g;
+      const double2 x = ptx::lds_f64x2(sA + r * 128 + ((ch ^ (r & 7)) << 4));
+      a[buf][i] = make_double2(__dsub_rn(x.x, o.x), __dsub_rn(x.y, o.y));
+    }
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int n = rB + j * 8 + g;
+      b[buf][j] = ptx::lds_f64x2(sB + n * 128 + ((ch ^ (n & 7)) << 4));
+    }
+  };
+  load(0, 0);
+  load(1, 1);
+#pragma unroll
+  for (int pp = 0; pp < 2; ++pp)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+          ptx::dmma_8x8x4(acc[i][j][0], acc[i][j][1], h ? a[pp][i].y : a[pp][i].x, h ? b[pp][j].y : b[pp][j].x);
+}
+
+// ---------------------------------------------------------------------------------------
 // K1: FP64 DMMA kernel
 template <int BM, int BN, int WM, int WN, int STAGES>
 struct f64_cfg {
@@ -466,26 +506,7 @@ __global__ void __launch_bounds__(f64_cfg<BM, BN, WM, WN, STAGES>::THREADS, MINB
     const uint32_t sA = smem_base + s * C::STAGE_BYTES;
     const uint32_t sB = sA + C::A_BYTES;
     const uint32_t sO = sB + C::B_BYTES;
-    // fragments double-buffered across the stage's k4 steps: step ks+1's loads and its shift
-    // subtraction are issued before step ks's DMMAs, so their latency hides behind the MMAs
-    double a[2][C::TM], b[2][C::TN];
-    auto load = [&](int ks, int buf) {
-      const int kk = ks * 4 + t;
-      const double o = ptx::lds_f64(sO + kk * 8);
-#pragma unroll
-      for (int i = 0; i < C::TM; ++i) a[buf][i] = __dsub_rn(ptx::lds_f64(sA + swz<8>(rA + i * 8 + g, kk)), o);
-#pragma unroll
-      for (int j = 0; j < C::TN; ++j) b[buf][j] = ptx::lds_f64(sB + swz<8>(rB + j * 8 + g, kk));
-    };
-    load(0, 0);
-#pragma unroll
-    for (int ks = 0; ks < C::KB / 4; ++ks) {
-      if (ks + 1 < C::KB / 4) load(ks + 1, (ks + 1) & 1);
-#pragma unroll
-      for (int i = 0; i < C::TM; ++i)
-#pragma unroll
-        for (int j = 0; j < C::TN; ++j) ptx::dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[ks & 1][i], b[ks & 1][j]);
-    }
+    dmma_kslice<C::TM, C::TN>(acc, sA, sB, sO, rA, rB, g, t);
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(&empty[s]);
   }
@@ -616,24 +637,7 @@ __global__ void __launch_bounds__(f64m_cfg<NP>::THREADS, 1)
     const uint32_t sA = smem_base + s * C::STAGE_BYTES;
     const uint32_t sB = sA + C::A_BYTES + grp * C::B_BYTES;
     const uint32_t sO = sA + C::A_BYTES + NP * C::B_BYTES + grp * C::O_BYTES;
-    double a[2][C::TM], b[2][C::TN];
-    auto load = [&](int ks, int buf) {
-      const int kk = ks * 4 + t;
-      const double o = ptx::lds_f64(sO + kk * 8);
-#pragma unroll
-      for (int i = 0; i < C::TM; ++i) a[buf][i] = __dsub_rn(ptx::lds_f64(sA + swz<8>(rA + i * 8 + g8, kk)), o);
-#pragma unroll
-      for (int j = 0; j < C::TN; ++j) b[buf][j] = ptx::lds_f64(sB + swz<8>(j * 8 + g8, kk));
-    };
-    load(0, 0);
-#pragma unroll
-    for (int ks = 0; ks < C::KB / 4; ++ks) {
-      if (ks + 1 < C::KB / 4) load(ks + 1, (ks + 1) & 1);
-#pragma unroll
-      for (int i = 0; i < C::TM; ++i)
-#pragma unroll
-        for (int j = 0; j < C::TN; ++j) ptx::dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[ks & 1][i], b[ks & 1][j]);
-    }
+    dmma_kslice<C::TM, C::TN>(acc, sA, sB, sO, rA, 0, g8, t);
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(&empty[s]);
   }
@@ -765,20 +769,7 @@ __global__ void __launch_bounds__(f64p_cfg<BM, BN, STAGES>::THREADS, 1)
       const uint32_t sA = smem_base + s * C::STAGE_BYTES;
       const uint32_t sB = sA + C::A_BYTES;
       const uint32_t sO = sB + C::B_BYTES;
-#pragma unroll
-      for (int ks = 0; ks < C::KB / 4; ++ks) {
-        const int kk = ks * 4 + t;
-        const double o = ptx::lds_f64(sO + kk * 8);
-        double a[C::TM], bf[C::TN];
-#pragma unroll
-        for (int i = 0; i < C::TM; ++i) a[i] = __dsub_rn(ptx::lds_f64(sA + swz<8>(rA + i * 8 + g, kk)), o);
-#pragma unroll
-        for (int j = 0; j < C::TN; ++j) bf[j] = ptx::lds_f64(sB + swz<8>(j * 8 + g, kk));
-#pragma unroll
-        for (int i = 0; i < C::TM; ++i)
-#pragma unroll
-          for (int j = 0; j < C::TN; ++j) ptx::dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], bf[j]);
-      }
+      dmma_kslice<C::TM, C::TN>(acc, sA, sB, sO, rA, 0, g, t);
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&empty[s]);
     }
