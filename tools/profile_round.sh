@@ -9,6 +9,9 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 python tools/prof_eval.py f64 5 4 > $OUT/eval_plain.log 2>&1 &&
 ncu --set full --clock-control none --import-source on -k regex:eval_f64 -s 2 -c 1 -o $OUT/eval_f64 \
     python tools/prof_eval.py f64 5 4 > $OUT/eval_ncu.log 2>&1
+python tools/time_multi.py > $OUT/multi_plain.log 2>&1 &&
+ncu --set full --clock-control none --import-source on -k regex:eval_f64_dmma_multi -s 2 -c 1 -o $OUT/eval_multi \
+    python tools/time_multi.py > $OUT/multi_ncu.log 2>&1
 python tools/prof_eval.py f32 5 4 > $OUT/eval32_plain.log 2>&1 &&
 ncu --set full --clock-control none --import-source on -k regex:eval_f32 -s 2 -c 1 -o $OUT/eval_f32 \
     python tools/prof_eval.py f32 5 4 > $OUT/eval32_ncu.log 2>&1

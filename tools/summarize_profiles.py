@@ -63,7 +63,8 @@ def main():
     summary = {"round": tag, "source": "tools/profile_round.sh on 1 B200 (gpurun), ncu --set full --clock-control none",
                "kernels": {}}
     traffic = {}
-    for name, rep in (("eval_f64_dmma", "eval_f64.ncu-rep"), ("eval_f32_ffma", "eval_f32.ncu-rep"),
+    for name, rep in (("eval_f64_multi", "eval_multi.ncu-rep"), ("eval_f64_dmma", "eval_f64.ncu-rep"),
+                      ("eval_f32_ffma", "eval_f32.ncu-rep"),
                       ("de_runs", "runs.ncu-rep"), ("updates", "updates.ncu-rep"),
                       ("updates", "pso_update.ncu-rep")):
         p = SRC / rep
@@ -83,6 +84,10 @@ def main():
                 e["algorithmic_flop"] = 2.0 * 1000 * 1000 * 1024
                 e["achieved_TFLOPs_under_ncu"] = e["algorithmic_flop"] / (dur * 1e-6) / 1e12
                 traffic["eval_f64_dmma_kernel"] = rd + wr
+            if name == "eval_f64_multi":
+                e["algorithmic_flop"] = 3 * 2.0 * 1000 * 1000 * 1024
+                e["achieved_TFLOPs_under_ncu"] = e["algorithmic_flop"] / (dur * 1e-6) / 1e12
+                traffic["eval_f64_dmma_multi_kernel"] = rd + wr
             if "pso_update" in kn:
                 e["algorithmic_bytes"] = 5 * 8 * 16384 * 1000
                 e["algorithmic_GBps"] = e["algorithmic_bytes"] / (dur * 1e-6) / 1e9
@@ -100,7 +105,7 @@ def main():
     lc = SRC / "bench_launches.csv"
     if lc.exists():
         shutil.copy(lc, DST / f"bench_launches_{tag}.csv")
-    for name in ("eval_f64", "eval_f32", "runs", "updates", "pso_update"):
+    for name in ("eval_multi", "eval_f64", "eval_f32", "runs", "updates", "pso_update"):
         rep = SRC / f"{name}.ncu-rep"
         if rep.exists():
             shutil.copy(rep, DST / f"{name}_{tag}.ncu-rep")

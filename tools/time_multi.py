@@ -1,3 +1,4 @@
+"""Device time of the multi-problem K1 launch (config 1: three problems on one population), L2 flushed."""
 import sys; sys.path.insert(0,'.'); sys.path.insert(0,'oracle')
 import numpy as np, torch, oracle as O, paper_2505_17430_b200 as evb
 o, m = O.shift_rotation(7, 1000); X = torch.from_numpy(O.population(7, 1024, 1000)).cuda()
