@@ -83,6 +83,17 @@ void* upload_padded(const void* host, int rows, int dim, int ld, int extra, size
   return upload(buf.data(), buf.size());
 }
 
+// M^T, dense (dim x dim), padded to a 16-byte multiple: the small-D kernel's bulk-copy source
+void* upload_transposed(const void* host, int dim, size_t es) {
+  std::vector<uint8_t> buf((size_t(dim) * dim * es + 15) / 16 * 16, 0);
+  for (int i = 0; i < dim; ++i)
+    for (int k = 0; k < dim; ++k)
+      std::memcpy(buf.data() + (size_t(k) * dim + i) * es, static_cast<const uint8_t*>(host) + (size_t(i) * dim + k) * es,
+                  es);
+  return upload(buf.data(), buf.size());
+}
+constexpr int kSmallTransposeMaxDim = 160;
+
 template <typename T>
 void* upload_weights(const std::vector<T>& w) {
   return upload(w.data(), w.size() * sizeof(T));
@@ -95,7 +106,7 @@ void fill_weights(device_problem& p) {
 
 void free_problem(device_problem& p) {
   void* ptrs[] = {p.shift, p.rotation, p.ell_w, p.hyb_w, p.perm, p.sub_kinds, p.chunk_sizes, p.comp_kinds,
-                  p.comp_shift, p.comp_rot, p.comp_sigma, p.comp_lambda, p.comp_bias, p.rot_hi, p.rot_lo};
+                  p.comp_shift, p.comp_rot, p.comp_sigma, p.comp_lambda, p.comp_bias, p.rot_hi, p.rot_lo, p.rot_t};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -181,6 +192,7 @@ int evb_problem_create_base(int dtype, int dim, int kind, const void* shift, con
       const size_t es = elem_size(dtype);
       p.shift = upload_padded(shift, 1, dim, p.ld, 64, es);
       p.rotation = upload_padded(rotation, dim, dim, p.ld, 0, es);
+      if (dim <= kSmallTransposeMaxDim) p.rot_t = upload_transposed(rotation, dim, es);
       fill_weights(p);
     } catch (...) {
       free_problem(p);
@@ -223,6 +235,7 @@ int evb_problem_create_hybrid(int dtype, int dim, const void* shift, const void*
       const size_t es = elem_size(dtype);
       p.shift = upload_padded(shift, 1, dim, p.ld, 64, es);
       p.rotation = upload_padded(rotation, dim, dim, p.ld, 0, es);
+      if (dim <= kSmallTransposeMaxDim) p.rot_t = upload_transposed(rotation, dim, es);
       fill_weights(p);
       p.n_chunks = n_chunks;
       p.perm = static_cast<int*>(upload(permutation, sizeof(int) * dim));

@@ -18,6 +18,7 @@
 
 #include "evb_internal.cuh"
 #include "evb_math.cuh"
+#include "ptx.cuh"
 
 namespace evb {
 
@@ -37,6 +38,7 @@ struct small_args {
   int64_t ldx;
   const T* shift;
   const T* rot;
+  const T* rot_t;  // M^T dense (device_problem::rot_t)
   int ld;
   int spec;
   const T* ell_w;
@@ -79,25 +81,51 @@ __device__ __forceinline__ void stage_rows(T* __restrict__ dst, int S, const T* 
 
 template <typename T>
 __global__ void eval_small_kernel(const small_args<T> a) {
+  // layout: M^T (bulk copy, 16-byte padded) | s = x - o (PB x D) | z (PB x D) | mbarrier
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  T* sM = reinterpret_cast<T*>(smem_raw);
-  T* sS = sM + size_t(a.D) * a.S;
-  T* sZ = sS + size_t(a.PB) * a.D;
-  const int b0 = blockIdx.x * a.PB;
   const int D = a.D;
-  stage_rows<T>(sM, a.S, a.rot, a.ld, D, D);
+  const uint32_t mt_bytes = uint32_t((size_t(D) * D * sizeof(T) + 15) / 16 * 16);
+  T* sMT = reinterpret_cast<T*>(smem_raw);
+  T* sS = reinterpret_cast<T*>(smem_raw + mt_bytes);
+  T* sZ = sS + size_t(a.PB) * D;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + ((mt_bytes + 2 * size_t(a.PB) * D * sizeof(T) + 7) / 8) * 8);
+  const int b0 = blockIdx.x * a.PB;
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(bar, 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // one bulk copy of M^T, overlapped with forming x - o below
+    ptx::mbar_arrive_expect_tx(bar, mt_bytes);
+    ptx::bulk_load(sMT, a.rot_t, mt_bytes, bar);
+  }
   for (int idx = threadIdx.x; idx < a.PB * D; idx += blockDim.x) {
     const int pb = idx / D, k = idx % D;
     const int b = b0 + pb;
     sS[idx] = b < a.P ? fop<T>::sub(a.X[size_t(b) * a.ldx + k], a.shift[k]) : T(0);
   }
   __syncthreads();
+  ptx::mbar_wait(bar, 0);
+  // z_i = sum_k M[i][k] * s_k in increasing k, product and sum rounded separately (the reference
+  // order, problems/batch.hpp:62-67); thread per (individual, row i): lanes read consecutive
+  // words of M^T, s_k is a broadcast; eight k per round with the loads ahead of the chain
   for (int idx = threadIdx.x; idx < a.PB * D; idx += blockDim.x) {
     const int pb = idx / D, i = idx % D;
-    const T* mrow = sM + i * a.S;
+    const T* mcol = sMT + i;
     const T* s = sS + pb * D;
     T acc = T(0);
-    for (int k = 0; k < D; ++k) acc = fop<T>::add(acc, fop<T>::mul(mrow[k], s[k]));
+    int k = 0;
+    for (; k + 8 <= D; k += 8) {
+      T mv[8], sv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        mv[u] = mcol[(k + u) * D];
+        sv[u] = s[k + u];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = fop<T>::add(acc, fop<T>::mul(mv[u], sv[u]));
+    }
+    for (; k < D; ++k) acc = fop<T>::add(acc, fop<T>::mul(mcol[k * D], s[k]));
     sZ[idx] = acc;
   }
   __syncthreads();
@@ -330,6 +358,7 @@ size_t small_smem(int D, int PB, bool comp) {
   const int S = (D % 2 == 1) ? D : D + 1;
   size_t bytes = (size_t(D) * S + 2 * size_t(PB) * D) * sizeof(T);
   if (comp) bytes += PB * kMaxComp * (sizeof(double) + sizeof(T)) + 16;
+  else bytes += 32;  // base / hybrid: M^T padded to 16 bytes + the bulk-copy mbarrier
   return bytes;
 }
 
@@ -353,7 +382,11 @@ int pick_pb(int D, int P, bool comp) {
 
 template <typename T>
 bool small_fits(int D, bool comp) {
-  return small_smem<T>(D, 1, comp) <= kSmallSmemMax && D <= 160;
+  // (the switch point predates the bulk-copy staging: measured against the M + x - o + z layout)
+  const int S = (D % 2 == 1) ? D : D + 1;
+  size_t legacy = (size_t(D) * S + 2 * size_t(D)) * sizeof(T);
+  if (comp) legacy += kMaxComp * (sizeof(double) + sizeof(T)) + 16;
+  return legacy <= kSmallSmemMax && D <= 160;
 }
 
 template <typename T>
@@ -414,6 +447,8 @@ void dispatch_t(const eval_request& rq_in) {
       a.P = P; a.D = D; a.S = (D % 2 == 1) ? D : D + 1; a.PB = PB;
       a.X = static_cast<const T*>(rq.X); a.ldx = rq.ldx;
       a.shift = static_cast<const T*>(pr.shift); a.rot = static_cast<const T*>(pr.rotation); a.ld = pr.ld;
+      a.rot_t = static_cast<const T*>(pr.rot_t);
+      if (!a.rot_t) throw runtime_error("evaluate_batch: small-D problem without its transposed rotation");
       a.spec = pr.spec; a.ell_w = static_cast<const T*>(pr.ell_w); a.hyb_w = static_cast<const T*>(pr.hyb_w);
       a.perm = pr.perm; a.sub_kinds = pr.sub_kinds; a.chunk_sizes = pr.chunk_sizes; a.n_chunks = pr.n_chunks;
       a.bias = T(pr.bias); a.n_out = rq.n_out;

@@ -103,6 +103,10 @@ struct device_problem {
   double* comp_lambda = nullptr;
   double* comp_bias = nullptr;
   void* hyb_w = nullptr;      // hybrid: per-chunk elliptic weights, chunk c at its offset
+  // small D (eval_small_kernel): M transposed and dense, rot_t[k * dim + i] = M[i][k], padded to
+  // a 16-byte multiple — one bulk copy stages it, and the row-per-thread dot products then read
+  // consecutive shared-memory words (conflict-free)
+  void* rot_t = nullptr;
   // fp32 tensor-core path: TF32 head / remainder split of the rotation (made on first use)
   void* rot_hi = nullptr;
   void* rot_lo = nullptr;
