@@ -580,28 +580,53 @@ __global__ void __launch_bounds__(kSelThreads) de_select_scan_kernel(const de_de
     }
   };
   const bool one_chunk = n_succ <= int(blockDim.x);
+  // thread 0's sequential sums read eight staged values per round with the loads ahead of the
+  // dependent add chain; every per-success product is formed by its own thread first (the same
+  // roundings as the reference's loop body, so the sums are bit-identical)
+  auto seq_sum = [&](double acc, const double* v, int n) {
+    int t = 0;
+    for (; t + 8 <= n; t += 8) {
+      double x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = v[t + u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, x[u]);
+    }
+    for (; t < n; ++t) acc = __dadd_rn(acc, v[t]);
+    return acc;
+  };
   if (d.cfg.parameter == EVB_PAR_SHADE) {  // de/parameter.hpp:166-184
     double gain_sum = 0.0;
     for (int base = 0; base < n_succ; base += blockDim.x) {
       stage(base);
       __syncthreads();
-      if (tid == 0)
-        for (int t = 0; t < min(int(blockDim.x), n_succ - base); ++t) gain_sum = __dadd_rn(gain_sum, st_g[t]);
+      if (tid == 0) gain_sum = seq_sum(gain_sum, st_g, min(int(blockDim.x), n_succ - base));
       __syncthreads();
     }
-    double f_num = 0.0, f_den = 0.0, cr_acc = 0.0;
     if (tid == 0) acc_s[0] = gain_sum;
+    __syncthreads();
+    gain_sum = acc_s[0];
+    double f_num = 0.0, f_den = 0.0, cr_acc = 0.0;
     for (int base = 0; base < n_succ; base += blockDim.x) {
-      if (!one_chunk) stage(base);
+      if (!one_chunk) {
+        stage(base);
+        __syncthreads();
+      }
+      if (base + tid < n_succ) {  // w = gain / sum; (w f) f, w f, w cr
+        const double w = __ddiv_rn(st_g[tid], gain_sum);
+        const double f = st_f[tid];
+        const double wf = __dmul_rn(w, f);
+        st_g[tid] = __dmul_rn(wf, f);
+        st_f[tid] = wf;
+        st_c[tid] = __dmul_rn(w, st_c[tid]);
+      }
       __syncthreads();
-      if (tid == 0)
-        for (int t = 0; t < min(int(blockDim.x), n_succ - base); ++t) {
-          const double w = __ddiv_rn(st_g[t], gain_sum);
-          const double f = st_f[t];
-          f_num = __dadd_rn(f_num, __dmul_rn(__dmul_rn(w, f), f));
-          f_den = __dadd_rn(f_den, __dmul_rn(w, f));
-          cr_acc = __dadd_rn(cr_acc, __dmul_rn(w, st_c[t]));
-        }
+      if (tid == 0) {
+        const int n = min(int(blockDim.x), n_succ - base);
+        f_num = seq_sum(f_num, st_g, n);
+        f_den = seq_sum(f_den, st_f, n);
+        cr_acc = seq_sum(cr_acc, st_c, n);
+      }
       __syncthreads();
     }
     if (tid == 0) {
@@ -615,13 +640,13 @@ __global__ void __launch_bounds__(kSelThreads) de_select_scan_kernel(const de_de
     for (int base = 0; base < n_succ; base += blockDim.x) {
       stage(base);
       __syncthreads();
+      if (base + tid < n_succ) st_g[tid] = __dmul_rn(st_f[tid], st_f[tid]);  // f * f
+      __syncthreads();
       if (tid == 0) {
         const int n = min(int(blockDim.x), n_succ - base);
-        for (int t = 0; t < n; ++t) {
-          num = __dadd_rn(num, __dmul_rn(st_f[t], st_f[t]));
-          den = __dadd_rn(den, st_f[t]);
-        }
-        for (int t = 0; t < n; ++t) crm = __dadd_rn(crm, st_c[t]);
+        num = seq_sum(num, st_g, n);
+        den = seq_sum(den, st_f, n);
+        crm = seq_sum(crm, st_c, n);
       }
       __syncthreads();
     }
