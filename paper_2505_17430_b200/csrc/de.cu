@@ -475,7 +475,12 @@ template <typename T>
 __global__ void __launch_bounds__(kSelThreads) de_select_scan_kernel(const de_dev<T> d) {
   __shared__ int warp_sum[2][kSelThreads / 32];
   __shared__ int carry[2];
+  // successes' (gain, F, CR) in success order, for the adapter update below
+  __shared__ double st_g[kSelThreads], st_f[kSelThreads], st_c[kSelThreads];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const bool adapt = d.cfg.parameter == EVB_PAR_SHADE || d.cfg.parameter == EVB_PAR_JADE;
+  // one pass-1 chunk: pass 1 stages the successes itself (no second trip through global memory)
+  const bool staged_in_pass1 = adapt && d.P <= int(blockDim.x);
   for (int s = tid; s < d.archive_cap; s += blockDim.x) d.owner[s] = -1;
   const int size0 = *d.arch_size;
   const int room = d.archive_cap - size0;
@@ -487,9 +492,15 @@ __global__ void __launch_bounds__(kSelThreads) de_select_scan_kernel(const de_de
   for (int base = 0; base < d.P; base += blockDim.x) {
     const int i = base + tid;
     int w = 0, s = 0;
+    double gain = 0.0, fi = 0.0, ci = 0.0;
     if (i < d.P) {
       const T ft = d.trial_fit[i], fp = d.fit[i];
+      if (staged_in_pass1) {  // loads issued with the fitness loads, ahead of the scans
+        fi = double(d.F[i]);
+        ci = double(d.CR[i]);
+      }
       w = (ft <= fp) ? 1 : 0;
+      gain = double(fop<T>::sub(fp, ft));
       s = (w && fop<T>::sub(fp, ft) > T(0)) ? 1 : 0;
       d.arch_slot[i] = -1;
     }
@@ -528,6 +539,11 @@ __global__ void __launch_bounds__(kSelThreads) de_select_scan_kernel(const de_de
     if (i < d.P) {
       d.win[i] = w ? q + 1 : 0;  // winner flag carrying its push index
       if (s) d.succ[k] = i;
+      if (s && staged_in_pass1) {
+        st_g[k] = gain;
+        st_f[k] = fi;
+        st_c[k] = ci;
+      }
       if (w && d.archive_cap > 0) {
         int sl;
         if (q < room) {
@@ -567,12 +583,11 @@ __global__ void __launch_bounds__(kSelThreads) de_select_scan_kernel(const de_de
   // adapter update: the sums stay sequential in success order (the reference's loops), but the
   // successes' (gain, F, CR) are first staged into shared memory by the whole block — one thread
   // chasing succ[s] -> fit[i] through global memory paid the L2 latency per success
-  if (n_succ == 0 || (d.cfg.parameter != EVB_PAR_SHADE && d.cfg.parameter != EVB_PAR_JADE)) return;
-  __shared__ double st_g[kSelThreads], st_f[kSelThreads], st_c[kSelThreads];
+  if (n_succ == 0 || !adapt) return;
   __shared__ double acc_s[4];
   auto stage = [&](int base) {
     const int s = base + tid;
-    if (s < n_succ) {
+    if (s < n_succ && !staged_in_pass1) {
       const int i = d.succ[s];
       st_g[tid] = double(fop<T>::sub(d.fit[i], d.trial_fit[i]));
       st_f[tid] = double(d.F[i]);
