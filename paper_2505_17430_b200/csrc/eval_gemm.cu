@@ -797,7 +797,7 @@ struct umma_cfg {
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // hi + lo of both operands
   static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) < 4 ? (200 * 1024 / STAGE_BYTES) : 4;
-  static constexpr int THREADS = 6 * 32;
+  static constexpr int THREADS = 10 * 32;  // producer, MMA issuer, 8 epilogue warps
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // [0,BN): main, [BN,2BN): corrections
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + (2 * STAGES + 1) * 8 + 64;
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
@@ -820,6 +820,15 @@ __global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * C::BM, n0 = blockIdx.y * BN;
   const int KT = (p.D + C::KB - 1) / C::KB;
+  unsigned long long* ts = p.dbg_ts ? p.dbg_ts + 8 * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
+  auto stamp = [&](int i) {  // EVB_K1_TIMELINE=1 (tuning aid): phase stamps, one thread per phase
+    if (ts) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      ts[i] = t;
+    }
+  };
+  if (threadIdx.x == 0) stamp(0);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -859,6 +868,7 @@ __global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
       for (int kb = 0; kb < KT; ++kb) {
         const int s = kb % C::STAGES;
         ptx::mbar_wait(&full[s], (kb / C::STAGES) & 1);
+        if (kb == 0) stamp(1);
         umma::fence_after();
         const uint32_t sa_hi = base + s * C::STAGE_BYTES, sa_lo = sa_hi + C::A_BYTES;
         const uint32_t sb_hi = sa_hi + 2 * C::A_BYTES, sb_lo = sb_hi + C::B_BYTES;
@@ -877,73 +887,100 @@ __global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
       umma::commit(accfull);  // accumulator complete
     }
   } else {
-    // ---------------- epilogue warps 2..5: one output row per thread ----------------
-    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    // ---------------- epilogue warps 2..9: (row, column half) per thread ----------------
+    // warp w reads TMEM lane quarter w % 4; warps 2-5 take the tile's first BN/2 columns, 6-9 the
+    // rest; main and correction accumulators are loaded together (one wait per 16 columns)
+    constexpr int HC = BN / 2;
+    const int ew = warp - 2, half = ew >> 2;
+    const int quarter = warp & 3;
     const int r = quarter * 32 + lane;
     const int row = m0 + r;
+    const int etid = threadIdx.x - 64;  // 0..255
     ptx::mbar_wait_sleep(accfull, 0);
+    if (threadIdx.x == 64) stamp(3);
     umma::fence_after();
-    const uint32_t taddr = tmem + (uint32_t(quarter * 32) << 16);
+    const uint32_t taddr = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(half * HC);
+    auto load16 = [&](int c0, float (&v)[16]) {
+      uint32_t a[16], b[16];
+      umma::tmem_ld16_raw(taddr + c0, a);
+      umma::tmem_ld16_raw(taddr + BN + c0, b);
+      umma::tmem_wait_ld();
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = __fadd_rn(__uint_as_float(a[q]), __uint_as_float(b[q]));
+    };
     if (p.zbuf) {
-#pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 16) {
+#pragma unroll 1
+      for (int c0 = 0; c0 < HC; c0 += 16) {
         float v[16];
-        umma::tmem_ld16(taddr + c0, v);
-        {
-          float w[16];
-          umma::tmem_ld16(taddr + BN + c0, w);
-#pragma unroll
-          for (int q = 0; q < 16; ++q) v[q] = __fadd_rn(v[q], w[q]);
-        }
+        load16(c0, v);
+        const int cb = n0 + half * HC + c0;
 #pragma unroll
         for (int q = 0; q < 16; ++q)
-          if (row < p.P && n0 + c0 + q < p.D) p.zbuf[size_t(n0 + c0 + q) * p.ldz + row] = v[q];
+          if (row < p.P && cb + q < p.D) p.zbuf[size_t(cb + q) * p.ldz + row] = v[q];
       }
     } else {
+      // per channel: the thread's half-row sum, then the halves meet in shared memory (the stage
+      // ring is drained once accfull fired): xs[half][ch][row]
+      float* xs = reinterpret_cast<float*>(smem);
       for (int ch = 0; ch < p.n_ch; ++ch) {
         const int term = p.ch_term[ch];
-        const bool prod = term_is_product(term);
-        float acc = prod ? 1.f : 0.f;
+        float a = term_is_product(term) ? 1.f : 0.f;
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 16) {
+        for (int c0 = 0; c0 < HC; c0 += 16) {
           float v[16];
-          umma::tmem_ld16(taddr + c0, v);
-          {
-            float w[16];
-            umma::tmem_ld16(taddr + BN + c0, w);
-#pragma unroll
-            for (int q = 0; q < 16; ++q) v[q] = __fadd_rn(v[q], w[q]);
-          }
-          acc = accumulate16_rt<float>(term, acc, v, n0 + c0, p.D, p.ell_w);
+          load16(c0, v);
+          a = accumulate16_rt<float>(term, a, v, n0 + half * HC + c0, p.D, p.ell_w);
         }
-        if (row < p.P) p.partial[(size_t(ch) * p.n_ntiles + blockIdx.y) * p.P + row] = acc;
+        xs[(half * kMaxCh + ch) * C::BM + r] = a;
       }
-      __threadfence();
-      ptx::named_bar_sync(1, 128);
-      const int etid = threadIdx.x - 64;
+      ptx::named_bar_sync(1, 256);
+      if (half == 0 && row < p.P)
+        for (int ch = 0; ch < p.n_ch; ++ch) {
+          const float a0 = xs[ch * C::BM + r], a1 = xs[(kMaxCh + ch) * C::BM + r];
+          const float v = term_is_product(p.ch_term[ch]) ? __fmul_rn(a0, a1) : __fadd_rn(a0, a1);
+          p.partial[(size_t(ch) * p.n_ntiles + blockIdx.y) * p.P + row] = v;
+        }
+      if (threadIdx.x == 64) stamp(4);
+      // ticket and combine as in tile_epilogue: one thread's fences around the atomic; N-tile
+      // partials summed in tile order, eight L2 loads in flight per round, channels in parallel
+      ptx::named_bar_sync(1, 256);
       if (etid == 0) {
-        const unsigned ticket = atomicAdd(&p.counters[blockIdx.x], 1u);
-        *last_flag = (ticket == unsigned(p.n_ntiles - 1)) ? 1 : 0;
-      }
-      ptx::named_bar_sync(1, 128);
-      if (*last_flag) {
         __threadfence();
-        if (row < p.P) {
-          float chv[kMaxCh];
-          for (int ch = 0; ch < p.n_ch; ++ch) {
-            const bool prod = term_is_product(p.ch_term[ch]);
-            const float* src = p.partial + size_t(ch) * p.n_ntiles * p.P + row;
-            float v = __ldcg(src);
-            for (int t = 1; t < p.n_ntiles; ++t) {
-              const float x = __ldcg(src + size_t(t) * p.P);
-              v = prod ? __fmul_rn(v, x) : __fadd_rn(v, x);
-            }
-            chv[ch] = v;
+        const unsigned ticket = atomicAdd(&p.counters[blockIdx.x], 1u);
+        const int last = (ticket == unsigned(p.n_ntiles - 1)) ? 1 : 0;
+        if (last) __threadfence();
+        *last_flag = last;
+      }
+      ptx::named_bar_sync(1, 256);
+      if (*last_flag) {
+        auto chain = [&](int ch, int rw) {
+          const bool prod = term_is_product(p.ch_term[ch]);
+          const float* src = p.partial + size_t(ch) * p.n_ntiles * p.P + rw;
+          float v = __ldcg(src);
+          for (int t0 = 1; t0 < p.n_ntiles; t0 += 8) {
+            float x[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (t0 + q < p.n_ntiles) x[q] = __ldcg(src + size_t(t0 + q) * p.P);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (t0 + q < p.n_ntiles) v = prod ? __fmul_rn(v, x[q]) : __fadd_rn(v, x[q]);
           }
+          return v;
+        };
+        const bool par = p.n_ch > 1 && p.n_ch * C::BM <= 256;
+        if (par) {
+          const int ch = etid / C::BM, rr = etid % C::BM;
+          if (ch < p.n_ch && m0 + rr < p.P) xs[ch * C::BM + rr] = chain(ch, m0 + rr);
+          ptx::named_bar_sync(1, 256);
+        }
+        if (etid < C::BM && m0 + etid < p.P) {
+          float chv[kMaxCh];
+          for (int ch = 0; ch < p.n_ch; ++ch) chv[ch] = par ? xs[ch * C::BM + etid] : chain(ch, m0 + etid);
           for (int o = 0; o < p.n_out; ++o) {
             const float s0 = chv[p.out_ch0[o]];
             const float s1 = p.out_ch1[o] >= 0 ? chv[p.out_ch1[o]] : 0.f;
-            p.out[o * p.ldo + row] = finalize<float>(p.out_kind[o], s0, s1, p.D, float(p.out_bias[o]));
+            p.out[o * p.ldo + m0 + etid] = finalize<float>(p.out_kind[o], s0, s1, p.D, float(p.out_bias[o]));
           }
         }
         if (etid == 0) p.counters[blockIdx.x] = 0u;
@@ -952,6 +989,10 @@ __global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
   }
   umma::fence_before();
   __syncthreads();
+  if (threadIdx.x == 64) {
+    stamp(5);
+    if (ts) ts[6] = *last_flag;
+  }
   if (warp == 1) umma::tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
@@ -1319,7 +1360,27 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
         fp.partial = static_cast<T*>(sc->partial);
         fp.counters = sc->counters;
       }
-      if (UBN == 256) launch_f32_umma<256>(ta_hi, ta_lo, tb_hi, tb_lo, fp, rq.stream);
+      static const bool timeline = std::getenv("EVB_K1_TIMELINE") != nullptr;
+      if (timeline && UBN == 64) {  // one synchronous launch, phase stamps appended to a CSV
+        const int nct = int(((P + 127) / 128) * ((D + 63) / 64));
+        unsigned long long* d = nullptr;
+        EVB_CUDA(cudaMalloc(&d, size_t(nct) * 8 * 8));
+        EVB_CUDA(cudaMemset(d, 0, size_t(nct) * 8 * 8));
+        fused_params<float> f2 = fp;
+        f2.dbg_ts = d;
+        launch_f32_umma<64>(ta_hi, ta_lo, tb_hi, tb_lo, f2, rq.stream);
+        EVB_CUDA(cudaStreamSynchronize(rq.stream));
+        std::vector<unsigned long long> h(size_t(nct) * 8);
+        EVB_CUDA(cudaMemcpy(h.data(), d, h.size() * 8, cudaMemcpyDeviceToHost));
+        cudaFree(d);
+        if (FILE* f = std::fopen("gpurun_out/k2_ts.csv", "a")) {
+          for (int c = 0; c < nct; ++c)
+            std::fprintf(f, "%d,%llu,%llu,%llu,%llu,%llu,%llu\n", c, h[c * 8 + 0], h[c * 8 + 1], h[c * 8 + 3],
+                         h[c * 8 + 4], h[c * 8 + 5], h[c * 8 + 6]);
+          std::fprintf(f, "end\n");
+          std::fclose(f);
+        }
+      } else if (UBN == 256) launch_f32_umma<256>(ta_hi, ta_lo, tb_hi, tb_lo, fp, rq.stream);
       else if (UBN == 128) launch_f32_umma<128>(ta_hi, ta_lo, tb_hi, tb_lo, fp, rq.stream);
       else launch_f32_umma<64>(ta_hi, ta_lo, tb_hi, tb_lo, fp, rq.stream);
       if (!own_rot) {
