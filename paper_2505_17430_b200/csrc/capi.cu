@@ -70,7 +70,7 @@ std::vector<T> elliptic_weights(int len) {
 void* upload(const void* host, size_t bytes) {
   void* d = nullptr;
   EVB_CUDA(cudaMalloc(&d, std::max<size_t>(bytes, 16)));
-  if (bytes) EVB_CUDA(cudaMemcpy(d, host, bytes, cudaMemcpyHostToDevice));
+  if (bytes) EVB_CUDA(copy_h2d_now(d, host, bytes));
   return d;
 }
 
@@ -164,7 +164,7 @@ int evb_device_free(void* ptr) {
   });
 }
 int evb_copy_to_device(void* dst, const void* src, size_t bytes) {
-  return guarded([&] { EVB_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice)); });
+  return guarded([&] { EVB_CUDA(copy_h2d_now(dst, src, bytes)); });
 }
 int evb_copy_to_host(void* dst, const void* src, size_t bytes) {
   return guarded([&] { EVB_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost)); });
@@ -475,7 +475,7 @@ void host_eval(const evb_problem* probs, int n_prob, evb_scratch s, const void* 
       if (!e) EVB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     if (!s->gate) {
       EVB_CUDA(cudaMalloc(&s->gate, kMaxGates * sizeof(unsigned)));
-      EVB_CUDA(cudaMemset(s->gate, 0, kMaxGates * sizeof(unsigned)));
+      EVB_CUDA(memset_now(s->gate, 0, kMaxGates * sizeof(unsigned)));
     }
     // Rows: when the multi-problem kernel needs two waves, the first wave's rows (all their
     // column chunks) cross first and the rest follow, so the second wave's data lands while the

@@ -240,7 +240,7 @@ int evb_cso_create(int dtype, double phi, int pop_size, int dim, evb_cso* out) {
       EVB_CUDA(cudaMalloc(&c->perm, sizeof(int) * pop_size));
       EVB_CUDA(cudaMalloc(&c->loser, sizeof(int) * (pop_size / 2)));
       EVB_CUDA(cudaMalloc(&c->stage, es * c->lds * (pop_size / 2)));
-      EVB_CUDA(cudaMemset(c->stage, 0, es * c->lds * (pop_size / 2)));
+      EVB_CUDA(memset_now(c->stage, 0, es * c->lds * (pop_size / 2)));
       EVB_CUDA(cudaMalloc(&c->stage_fit, es * (pop_size / 2)));
       require(evb_scratch_create(&c->eval_scratch) == EVB_OK, "cso: scratch allocation failed");
     } catch (...) {

@@ -1053,7 +1053,7 @@ template <typename T>
 void* dalloc(size_t n) {
   void* p = nullptr;
   EVB_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
-  EVB_CUDA(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(T)));
+  EVB_CUDA(memset_now(p, 0, std::max<size_t>(n, 1) * sizeof(T)));
   return p;
 }
 
@@ -1083,9 +1083,9 @@ template <typename T>
 void reset_adapter(evb_de_s* e) {
   const int H = std::max(1, e->cfg.memory_size);
   std::vector<T> half(H, T(0.5));
-  EVB_CUDA(cudaMemcpy(e->mem_f, half.data(), sizeof(T) * H, cudaMemcpyHostToDevice));
-  EVB_CUDA(cudaMemcpy(e->mem_cr, half.data(), sizeof(T) * H, cudaMemcpyHostToDevice));
-  EVB_CUDA(cudaMemset(e->d_write_index, 0, sizeof(int)));
+  EVB_CUDA(copy_h2d_now(e->mem_f, half.data(), sizeof(T) * H));
+  EVB_CUDA(copy_h2d_now(e->mem_cr, half.data(), sizeof(T) * H));
+  EVB_CUDA(memset_now(e->d_write_index, 0, sizeof(int)));
 }
 
 }  // namespace
@@ -1102,11 +1102,11 @@ int evb_rng_create_philox(uint64_t key, evb_rng* out) {
     r->mode = RNG_PHILOX;
     r->key = key;
     EVB_CUDA(cudaMalloc(&r->d_gen, sizeof(uint32_t)));
-    EVB_CUDA(cudaMemset(r->d_gen, 0, sizeof(uint32_t)));
+    EVB_CUDA(memset_now(r->d_gen, 0, sizeof(uint32_t)));
     EVB_CUDA(cudaMalloc(&r->d_overflow, sizeof(int)));
-    EVB_CUDA(cudaMemset(r->d_overflow, 0, sizeof(int)));
+    EVB_CUDA(memset_now(r->d_overflow, 0, sizeof(int)));
     EVB_CUDA(cudaMalloc(&r->d_cursor, sizeof(int64_t)));
-    EVB_CUDA(cudaMemset(r->d_cursor, 0, sizeof(int64_t)));
+    EVB_CUDA(memset_now(r->d_cursor, 0, sizeof(int64_t)));
     *out = r;
   });
 }
@@ -1119,13 +1119,13 @@ int evb_rng_create_words(const uint64_t* words, int64_t n_words, evb_rng* out) {
     r->mode = RNG_WORDS;
     r->n_words = n_words;
     EVB_CUDA(cudaMalloc(&r->d_gen, sizeof(uint32_t)));
-    EVB_CUDA(cudaMemset(r->d_gen, 0, sizeof(uint32_t)));
+    EVB_CUDA(memset_now(r->d_gen, 0, sizeof(uint32_t)));
     EVB_CUDA(cudaMalloc(&r->d_words, std::max<int64_t>(n_words, 1) * sizeof(uint64_t)));
-    if (n_words) EVB_CUDA(cudaMemcpy(r->d_words, words, n_words * sizeof(uint64_t), cudaMemcpyHostToDevice));
+    if (n_words) EVB_CUDA(copy_h2d_now(r->d_words, words, n_words * sizeof(uint64_t)));
     EVB_CUDA(cudaMalloc(&r->d_overflow, sizeof(int)));
-    EVB_CUDA(cudaMemset(r->d_overflow, 0, sizeof(int)));
+    EVB_CUDA(memset_now(r->d_overflow, 0, sizeof(int)));
     EVB_CUDA(cudaMalloc(&r->d_cursor, sizeof(int64_t)));
-    EVB_CUDA(cudaMemset(r->d_cursor, 0, sizeof(int64_t)));
+    EVB_CUDA(memset_now(r->d_cursor, 0, sizeof(int64_t)));
     *out = r;
   });
 }
@@ -1160,7 +1160,7 @@ int evb_rng_set_generation(evb_rng r, uint32_t generation) {
     require(r != nullptr, "rng: null handle");
     r->gen = generation;
     EVB_CUDA(cudaDeviceSynchronize());
-    EVB_CUDA(cudaMemcpy(r->d_gen, &generation, sizeof(uint32_t), cudaMemcpyHostToDevice));
+    EVB_CUDA(copy_h2d_now(r->d_gen, &generation, sizeof(uint32_t)));
   });
 }
 
@@ -1230,7 +1230,7 @@ int evb_de_create(int dtype, const evb_de_config* c, int pop_size, int dim, evb_
       e->ldt = round_up(dim, 16 / int64_t(es));
       auto bytes = [&](size_t n) { return n * es; };
       EVB_CUDA(cudaMalloc(&e->trial, bytes(size_t(pop_size) * e->ldt)));
-      EVB_CUDA(cudaMemset(e->trial, 0, bytes(size_t(pop_size) * e->ldt)));
+      EVB_CUDA(memset_now(e->trial, 0, bytes(size_t(pop_size) * e->ldt)));
       EVB_CUDA(cudaMalloc(&e->trial_fit, bytes(pop_size)));
       EVB_CUDA(cudaMalloc(&e->F, bytes(pop_size)));
       EVB_CUDA(cudaMalloc(&e->CR, bytes(pop_size)));
@@ -1247,7 +1247,7 @@ int evb_de_create(int dtype, const evb_de_config* c, int pop_size, int dim, evb_
       e->owner = static_cast<int*>(dalloc<int>(std::max(1, e->archive_cap)));
       e->succ = static_cast<int*>(dalloc<int>(pop_size));
       EVB_CUDA(cudaMalloc(&e->archive, bytes(size_t(std::max(1, e->archive_cap)) * e->ldt)));
-      EVB_CUDA(cudaMemset(e->archive, 0, bytes(size_t(std::max(1, e->archive_cap)) * e->ldt)));
+      EVB_CUDA(memset_now(e->archive, 0, bytes(size_t(std::max(1, e->archive_cap)) * e->ldt)));
       e->d_arch_size = static_cast<int*>(dalloc<int>(1));
       e->d_write_index = static_cast<int*>(dalloc<int>(1));
       e->d_arch_words = static_cast<int64_t*>(dalloc<int64_t>(1));
@@ -1280,7 +1280,7 @@ int evb_de_reset(evb_de e) {
     require(e != nullptr, "de: null handle");
     if (e->dtype == EVB_F64) reset_adapter<double>(e);
     else reset_adapter<float>(e);
-    EVB_CUDA(cudaMemset(e->d_arch_size, 0, sizeof(int)));
+    EVB_CUDA(memset_now(e->d_arch_size, 0, sizeof(int)));
     restore_size(e);
   });
 }
@@ -1435,11 +1435,11 @@ int evb_de_set_state(evb_de e, const void* archive_host, int archive_size, const
     if (archive_host && archive_size > 0)
       EVB_CUDA(cudaMemcpy2D(e->archive, e->ldt * es, archive_host, e->D * es, e->D * es, archive_size,
                             cudaMemcpyHostToDevice));
-    EVB_CUDA(cudaMemcpy(e->d_arch_size, &archive_size, sizeof(int), cudaMemcpyHostToDevice));
-    if (mem_f_host) EVB_CUDA(cudaMemcpy(e->mem_f, mem_f_host, es * e->cfg.memory_size, cudaMemcpyHostToDevice));
-    if (mem_cr_host) EVB_CUDA(cudaMemcpy(e->mem_cr, mem_cr_host, es * e->cfg.memory_size, cudaMemcpyHostToDevice));
+    EVB_CUDA(copy_h2d_now(e->d_arch_size, &archive_size, sizeof(int)));
+    if (mem_f_host) EVB_CUDA(copy_h2d_now(e->mem_f, mem_f_host, es * e->cfg.memory_size));
+    if (mem_cr_host) EVB_CUDA(copy_h2d_now(e->mem_cr, mem_cr_host, es * e->cfg.memory_size));
     require(write_index >= 0 && write_index < e->cfg.memory_size, "de_set_state: write index out of range");
-    EVB_CUDA(cudaMemcpy(e->d_write_index, &write_index, sizeof(int), cudaMemcpyHostToDevice));
+    EVB_CUDA(copy_h2d_now(e->d_write_index, &write_index, sizeof(int)));
   });
 }
 

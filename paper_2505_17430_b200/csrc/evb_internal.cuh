@@ -170,6 +170,22 @@ struct evb_scratch_s {
 
 namespace evb {
 
+// Zero-fill at object creation, complete before returning.  cudaMemset on device memory returns
+// before the fill lands and runs on the legacy stream, which the library's non-blocking streams do
+// not wait for: a gate word cleared that way could overwrite the first epoch written on the gate
+// stream (the kernel then waits until its 10-s trap).
+inline cudaError_t memset_now(void* p, int v, size_t n) {
+  const cudaError_t e = cudaMemset(p, v, n);
+  return e != cudaSuccess ? e : cudaStreamSynchronize(nullptr);
+}
+
+// Host -> device copy complete before returning.  A cudaMemcpy from pageable memory returns once
+// the data is staged, not when the DMA has landed, and it is ordered only on the legacy stream.
+inline cudaError_t copy_h2d_now(void* dst, const void* src, size_t n) {
+  const cudaError_t e = cudaMemcpy(dst, src, n, cudaMemcpyHostToDevice);
+  return e != cudaSuccess ? e : cudaStreamSynchronize(nullptr);
+}
+
 // Grow-only device buffer; synchronises `stream` before releasing an old allocation.
 inline void ensure_buffer(void** ptr, size_t* cap, size_t need, cudaStream_t stream) {
   if (*cap >= need && *ptr) return;

@@ -457,7 +457,7 @@ void words_advance(evb_rng_s* r, int64_t to, cudaStream_t st) {
   EVB_CUDA(cudaStreamSynchronize(st));
   if (to > r->n_words) {
     int one = 1;
-    EVB_CUDA(cudaMemcpy(r->d_overflow, &one, sizeof(int), cudaMemcpyHostToDevice));
+    EVB_CUDA(copy_h2d_now(r->d_overflow, &one, sizeof(int)));
   }
 }
 
@@ -675,7 +675,7 @@ int evb_pso_set_pbest(evb_pso s, const void* pbest_host, const void* pbest_fit_h
     const size_t es = s->dtype == EVB_F64 ? 8 : 4;
     EVB_CUDA(cudaDeviceSynchronize());
     EVB_CUDA(cudaMemcpy2D(s->pbest, s->ldb * es, pbest_host, s->D * es, s->D * es, s->P, cudaMemcpyHostToDevice));
-    EVB_CUDA(cudaMemcpy(s->pbest_fit, pbest_fit_host, es * s->P, cudaMemcpyHostToDevice));
+    EVB_CUDA(copy_h2d_now(s->pbest_fit, pbest_fit_host, es * s->P));
     s->prepared = 1;
   });
 }

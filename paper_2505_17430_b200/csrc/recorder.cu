@@ -250,7 +250,7 @@ int evb_param_trace_create(int dtype, int n_runs, int capacity, evb_param_trace*
       EVB_CUDA(cudaMalloc(&t->mu_f, es * size_t(n_runs) * capacity));
       EVB_CUDA(cudaMalloc(&t->mu_cr, es * size_t(n_runs) * capacity));
       EVB_CUDA(cudaMalloc(&t->count, sizeof(int) * n_runs));
-      EVB_CUDA(cudaMemset(t->count, 0, sizeof(int) * n_runs));
+      EVB_CUDA(memset_now(t->count, 0, sizeof(int) * n_runs));
     } catch (...) {
       cudaFree(t->gen);
       cudaFree(t->mu_f);
