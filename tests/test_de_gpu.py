@@ -126,14 +126,16 @@ def test_device_philox_matches_restatement():
         assert np.array_equal(philox_words(key, hi, 5, 257), O.philox_words(key, hi, 5, 257))
 
 
-@pytest.mark.parametrize("G", [40])
-def test_config2_shade_lockstep(dev, G):
-    P, D, key = 180, 100, 11
+@pytest.mark.parametrize("P,D,G", [(180, 100, 40), (1100, 20, 6)])
+def test_config2_shade_lockstep(dev, P, D, G):
+    # config 2 shape, and a population above one select-scan pass (1024: successes staged apart
+    # from the flags, SHADE memory sums over several chunks)
+    key = 11
     o, m = O.shift_rotation(11, D)
     cfg = preset_shade(0.11, P, 1.0)
     prob = evb.ProblemInstance.base(evb.BaseKind.ackley, o, m, 0.0)
     eng = DEEngine(cfg, P, D)
-    assert eng.archive_capacity == P and eng.p_count == 20
+    assert eng.archive_capacity == P and eng.p_count == (20 if P == 180 else 121)
     rng = Rng.philox(key)
     pop = torch.empty((P, D), dtype=torch.float64, device=dev)
     eng.init_population(pop, -100.0, 100.0, rng)
@@ -173,12 +175,19 @@ def test_config2_shade_lockstep(dev, G):
         if same.all():
             exact_gens += 1
             assert np.array_equal(eng.get_state()["archive"], st["archive"]), g
+        # the SHADE memory update (sequential success sums) on the GPU's own F / CR: equal up to
+        # the F / CR ulps above
+        gst = eng.get_state()
+        assert gst["write_index"] == st["write_index"], g
+        assert np.max(np.abs(gst["memory_f"] - st["memory_f"])) <= 1e-12, g
+        assert np.max(np.abs(gst["memory_cr"] - st["memory_cr"])) <= 1e-12, g
         # rows that differ must come from an F/CR ulp difference
         diff_rows = np.where(~same)[0]
         for i in diff_rows:
             assert dr["F"][i] != out["F"][i] or dr["CR"][i] != out["CR"][i], (g, i)
         assert np.max(np.abs(gpu_pop - st["pop"])) <= 1e-9
-    assert exact_gens >= G // 2, (exact_gens, flagged)
+    # (at P = 1100 nearly every generation has some row with an F / CR ulp difference)
+    assert exact_gens >= (G // 2 if P <= 256 else 0), (exact_gens, flagged)
 
 
 def test_large_population_properties(dev):
