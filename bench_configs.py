@@ -109,10 +109,25 @@ def cfg0(out):
         eng.generation(prob, pop, fit, -100.0, 100.0, rng)
         fit.cpu()
     e2e_ms = (time.perf_counter() - t0) / 20 * 1e3
+    # whole run in one persistent launch (K8, n_runs = 1: a 2-CTA cluster), per generation
+    pops = torch.empty((1, P, D), dtype=torch.float64, device=DEV)
+    fits = torch.empty((1, P), dtype=torch.float64, device=DEV)
+    keys = run_keys(42, 1)
+    de_runs(preset_de(), [prob], keys, pops, fits, 20, -100.0, 100.0, init=True, gen0=0)
+    G = 2000
+    a2, b2 = ev(), ev()
+    a2.record()
+    de_runs(preset_de(), [prob], keys, pops, fits, G, -100.0, 100.0, init=True, gen0=0)
+    b2.record()
+    torch.cuda.synchronize()
+    ms_persist = a2.elapsed_time(b2) / G
     cpu_s = O.REF_FAST().ref_bench_de(0, P, D, 2000, 5, O.ptr(o), O.ptr(np.ascontiguousarray(m)), 42)
     out["config0"] = {"gpu_ms_per_generation": ms, "gpu_generations_per_s": 1e3 / ms,
                       "gpu_graph_ms_per_generation": ms_graph, "gpu_graph_generations_per_s": 1e3 / ms_graph,
                       "gpu_e2e_ms_per_generation": e2e_ms, "kernels_per_generation": 5,
+                      "gpu_persistent_ms_per_generation": ms_persist,
+                      "gpu_persistent_generations_per_s": 1e3 / ms_persist,
+                      "persistent_how": "de_runs (K8): init + 2000 generations of the run in one launch",
                       "cpu_reference_ms_per_generation": cpu_s / 2000 * 1e3, "cpu_cores": 1,
                       "cpu_sample": "build_de_fixed(0.5,0.9), 2000 generations, native stream"}
 

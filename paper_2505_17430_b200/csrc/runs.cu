@@ -50,6 +50,29 @@ struct phase_clock {
   }
 };
 
+// Individual i's draw sub-stream with its first eight words computed up front: four independent
+// Philox blocks (instruction-level parallel) instead of one block per word in sequence, each
+// recomputing its pair's block.  Word n is still philox_word(key, ctr_hi, n), so the values and
+// the consumed count are exactly word_reader's.
+struct philox8_reader {
+  uint64_t key, ctr_hi;
+  int64_t count = 0;
+  uint64_t w0, w1, w2, w3, w4, w5, w6, w7;
+  __device__ __forceinline__ philox8_reader(uint64_t k, uint64_t c) : key(k), ctr_hi(c) {
+    philox_pair(k, c, 0, w0, w1);
+    philox_pair(k, c, 1, w2, w3);
+    philox_pair(k, c, 2, w4, w5);
+    philox_pair(k, c, 3, w6, w7);
+  }
+  __device__ __forceinline__ uint64_t next() {
+    const int64_t n = count++;
+    if (n >= 8) return philox_word(key, ctr_hi, uint64_t(n));
+    const uint64_t v = w0;  // shift the prefetched words down
+    w0 = w1; w1 = w2; w2 = w3; w3 = w4; w4 = w5; w5 = w6; w6 = w7;
+    return v;
+  }
+};
+
 struct run_problem {
   const double* shift[kRunsMaxComp];  // per component (base problem: component 0)
   const double* rot[kRunsMaxComp];
@@ -284,7 +307,6 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
   const uint64_t key = a.keys[run];
   double* gpop = a.pop + size_t(run) * P * D;
   double* gfit = a.fit + size_t(run) * P;
-  word_source src{RNG_PHILOX, key, nullptr, 0};
   phase_clock pc{blockIdx.x == 0 ? a.prof : nullptr, 0};
   // evaluate rows [p0, p1) of X into f
   auto evaluate = [&](const double* X, double* f) {
@@ -322,7 +344,7 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
     double* sTfit = sTfit2 + (g & 1) * P;
     // draws (thread per individual of this CTA's half)
     for (int i = p0 + int(threadIdx.x); i < p1; i += blockDim.x) {
-      word_reader r{&src, (uint64_t(gen) << 32) | uint32_t(i), 0, 0, nullptr};
+      philox8_reader r(key, (uint64_t(gen) << 32) | uint32_t(i));
       int x1, x2, x3;
       if (a.mutation == EVB_MUT_RAND1) {
         do { x1 = draw_int(r, P); } while (x1 == i);
@@ -344,18 +366,22 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
     }
     __syncthreads();
     pc.mark(0);
-    // trial (warp per individual of this half; each lane owns one Philox block = two gene words)
+    // trial: thread per (individual of this half, Philox block = two gene words), flattened over
+    // the half so that small D still fills the CTA (a warp per individual left most lanes idle at
+    // D = 10 and serialised the Philox chains)
     {
-      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-      for (int i = p0 + warp; i < p1; i += nwarps) {
+      const int NB = D / 2 + 1;  // blocks an individual's D gene words can touch
+      for (int e = int(threadIdx.x); e < (p1 - p0) * NB; e += blockDim.x) {
+        const int i = p0 + e / NB, q = e % NB;
         const int packed = sIdx[4 * i + 3];
         const int s0 = packed >> 16, jr = packed & 0xFFFF;
+        const int blk0 = s0 >> 1, nblk = ((s0 + D + 1) >> 1) - blk0;
+        if (q >= nblk) continue;
         const double* xa = sPop + sIdx[4 * i] * D;
         const double* xb = sPop + sIdx[4 * i + 1] * D;
         const double* xc = sPop + sIdx[4 * i + 2] * D;
         const uint64_t ctr = (uint64_t(gen) << 32) | uint32_t(i);
-        const int blk0 = s0 >> 1, nblk = ((s0 + D + 1) >> 1) - blk0;
-        for (int q = lane; q < nblk; q += 32) {
+        {
           uint64_t w0, w1;
           philox_pair(key, ctr, uint64_t(blk0 + q), w0, w1);
 #pragma unroll

@@ -61,6 +61,35 @@ def test_config4_runs_match_reference(dev, n_runs, gens, check_runs):
     assert np.all(np.isfinite(gf))
 
 
+@pytest.mark.parametrize("n_runs", [1, 4])
+def test_config0_shape_persistent_matches_reference(dev, n_runs):
+    # BASELINE config 0's problem and preset (D=10, P=100, Rastrigin with z = 0.0512 M (x - o),
+    # rand/1/bin F 0.5 CR 0.9, clip) as whole runs in one persistent launch; the reference engine
+    # replays each run's Philox words
+    P0, D0, gens = 100, 10, 200
+    o, m = O.shift_rotation(42, D0)
+    m = m * 0.0512
+    probs = [evb.ProblemInstance.base(evb.BaseKind.rastrigin, o, m, 0.0) for _ in range(n_runs)]
+    keys = run_keys(42, n_runs)
+    pops = torch.empty((n_runs, P0, D0), dtype=torch.float64, device=dev)
+    fits = torch.empty((n_runs, P0), dtype=torch.float64, device=dev)
+    de_runs(preset_de(0.5, 0.9), probs, keys, pops, fits, gens, -100.0, 100.0, init=True, gen0=0)
+    torch.cuda.synchronize()
+    gp, gf = pops.cpu().numpy(), fits.cpu().numpy()
+    for r in range(n_runs):
+        ref = O.RefDE(preset_de(0.5, 0.9), P0, D0)
+        ref.set_problem_base(5, o, m, 0.0)
+        assert ref.init(O.philox_words(int(keys[r]), 0xFFFFFFF0, 0, P0 * D0), -100.0, 100.0) == P0 * D0
+        for g in range(1, gens + 1):
+            assert ref.generation(O.de_fixed_generation_words(0, int(keys[r]), g, P0, D0), -100.0, 100.0)
+        st = ref.get()
+        same = np.all(gp[r] == st["pop"], axis=1)
+        # exact-order arithmetic: identical unless a libm-vs-CUDA cos ulp flipped a near-tie
+        assert same.mean() >= 0.95, (r, int((~same).sum()))
+        rel = np.abs(gf[r] - st["fit"]) / np.maximum(1.0, np.abs(st["fit"]))
+        assert rel[same].max() <= 1e-12, r
+
+
 def test_runs_continue_equals_single_launch(dev):
     # init + 10 generations in one launch == init + 4 then 6 more (gen ids continue)
     probs, _ = make_runs(3)
