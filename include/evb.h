@@ -135,7 +135,9 @@ EVB_API int evb_evaluate_batch_host(evb_problem p, evb_scratch s, const void* X_
                             int64_t ldx, void* out_host);
 /* One device population on several problems (same dimension and dtype): outs[k] (device,
  * n_points) receives problem k's fitness.  Two or three fp64 base problems with fused kinds run
- * as ONE launch whose stages carry X once for all problems; otherwise one launch per problem. */
+ * as ONE launch whose stages carry X once for all problems; otherwise one launch per problem.
+ * Replaces several problems::evaluate_batch calls on one population (problems/batch.hpp:243-278,
+ * e.g. a suite's problems at one generation's population); results equal one call per problem. */
 EVB_API int evb_evaluate_batch_problems(const evb_problem* problems, int n_problems, evb_scratch s, const void* X,
                                         int64_t n_points, int64_t ldx, void* const* outs, void* stream);
 
