@@ -29,6 +29,7 @@
 
 #include "evb_internal.cuh"
 #include "evb_math.cuh"
+#include "ptx.cuh"
 #include "rng.cuh"
 
 namespace evb {
@@ -159,6 +160,8 @@ struct de_dev {
 // fitness order (core/population.hpp:70-77): rank = #{j : f_j < f_i or (f_j == f_i and j < i)}
 template <typename T>
 __global__ void de_order_kernel(const de_dev<T> d) {
+  ptx::griddep_wait();  // PDL (launch_pdl): predecessor data first
+  ptx::griddep_launch_dependents();
   extern __shared__ __align__(16) uint8_t smem_raw[];
   T* sf = reinterpret_cast<T*>(smem_raw);
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -255,6 +258,8 @@ __device__ void draw_scalars(const de_dev<T>& d, int i, int arch_size, R& r) {
 
 template <typename T>
 __global__ void de_draw_philox_kernel(const de_dev<T> d) {
+  ptx::griddep_wait();  // PDL (launch_pdl): predecessor data first
+  ptx::griddep_launch_dependents();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= d.P) return;
   const int arch_size = *d.arch_size;
@@ -352,6 +357,8 @@ __device__ __forceinline__ T donor_gene(int mutation, T xij, T xaj, T xbj, T xcj
 
 template <typename T, int CX>
 __global__ void de_trial_kernel(const de_dev<T> d) {
+  ptx::griddep_wait();  // PDL (launch_pdl): predecessor data first
+  ptx::griddep_launch_dependents();
   const int i = blockIdx.x;
   const int D = d.D;
   const T Fi = d.F[i];
@@ -473,6 +480,8 @@ constexpr int kSelThreads = 1024;
 
 template <typename T>
 __global__ void __launch_bounds__(kSelThreads) de_select_scan_kernel(const de_dev<T> d) {
+  ptx::griddep_wait();  // PDL (launch_pdl): predecessor data first
+  ptx::griddep_launch_dependents();
   __shared__ int warp_sum[2][kSelThreads / 32];
   __shared__ int carry[2];
   // successes' (gain, F, CR) in success order, for the adapter update below
@@ -678,6 +687,8 @@ __global__ void __launch_bounds__(kSelThreads) de_select_scan_kernel(const de_de
 // K5b: replaced parent -> archive slot, trial -> population (std::swap(pop[i], trial)).
 template <typename T>
 __global__ void de_select_apply_kernel(const de_dev<T> d) {
+  ptx::griddep_wait();  // PDL (launch_pdl): predecessor data first
+  ptx::griddep_launch_dependents();
   const int i = blockIdx.x;
   if (i == 0 && threadIdx.x == 0) *d.gen_ptr += 1u;  // last reader of this generation's id is done
   if (!d.win[i]) return;
@@ -809,19 +820,21 @@ void generation_t(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, vo
   e->gen_P = e->P;
   if (e->cfg.mutation == EVB_MUT_TTPB1 || e->cfg.mutation == EVB_MUT_BEST1) {
     const int th = 256;
-    de_order_kernel<T><<<(e->P + th - 1) / th, th, th * sizeof(T), st>>>(d);
+    EVB_CUDA(launch_pdl(de_order_kernel<T>, dim3((e->P + th - 1) / th), dim3(th), th * sizeof(T), st, d));
     count_launch();
   }
   if (r->mode == RNG_PHILOX) {
-    de_draw_philox_kernel<T><<<(e->P + 127) / 128, 128, 0, st>>>(d);
+    EVB_CUDA(launch_pdl(de_draw_philox_kernel<T>, dim3((e->P + 127) / 128), dim3(128), 0, st, d));
   } else {
     de_draw_words_kernel<T><<<1, 32, 0, st>>>(d);
   }
   count_launch();
   {
     const int th = std::min(256, int(round_up((e->D + 2) / 2 + 1, 32)));
-    if (e->cfg.crossover == EVB_CX_EXPONENTIAL) de_trial_kernel<T, EVB_CX_EXPONENTIAL><<<e->P, th, 0, st>>>(d);
-    else de_trial_kernel<T, EVB_CX_BINOMIAL><<<e->P, th, 0, st>>>(d);
+    if (e->cfg.crossover == EVB_CX_EXPONENTIAL)
+      EVB_CUDA(launch_pdl(de_trial_kernel<T, EVB_CX_EXPONENTIAL>, dim3(e->P), dim3(th), 0, st, d));
+    else
+      EVB_CUDA(launch_pdl(de_trial_kernel<T, EVB_CX_BINOMIAL>, dim3(e->P), dim3(th), 0, st, d));
     count_launch();
     if (e->cfg.repair == EVB_REP_REINITIALIZE) {
       de_reinit_kernel<T><<<e->P, std::max(32, std::min(256, int(round_up(e->D, 32)))), 0, st>>>(d);
@@ -849,11 +862,11 @@ void generation_t(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, vo
     restart_monitor_kernel<T><<<1, 32, 0, st>>>(static_cast<const T*>(e->trial_fit), e->P, e->d_mon, e->mon_eps);
     count_launch();
   }
-  de_select_scan_kernel<T><<<1, kSelThreads, 0, st>>>(d);
+  EVB_CUDA(launch_pdl(de_select_scan_kernel<T>, dim3(1), dim3(kSelThreads), 0, st, d));
   count_launch();
   {
     const int th = std::min(256, int(round_up(e->D, 32)));
-    de_select_apply_kernel<T><<<e->P, th, 0, st>>>(d);
+    EVB_CUDA(launch_pdl(de_select_apply_kernel<T>, dim3(e->P), dim3(th), 0, st, d));
     count_launch();
   }
   EVB_CUDA(cudaGetLastError());

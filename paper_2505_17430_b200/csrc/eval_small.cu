@@ -81,6 +81,8 @@ __device__ __forceinline__ void stage_rows(T* __restrict__ dst, int S, const T* 
 
 template <typename T>
 __global__ void eval_small_kernel(const small_args<T> a) {
+  ptx::griddep_wait();  // PDL (launch_pdl): predecessor data first
+  ptx::griddep_launch_dependents();
   // layout: M^T (bulk copy, 16-byte padded) | s = x - o (PB x D) | z (PB x D) | mbarrier
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int D = a.D;
@@ -455,7 +457,7 @@ void dispatch_t(const eval_request& rq_in) {
       for (int o = 0; o < rq.n_out; ++o) { a.kinds[o] = rq.kinds[o]; a.biases[o] = rq.biases[o]; }
       a.out = static_cast<T*>(rq.out); a.ldo = rq.ldo; a.scalar_trig = rq.scalar_trig ? 1 : 0;
       set_smem_attr<T>(reinterpret_cast<const void*>(eval_small_kernel<T>), smem);
-      eval_small_kernel<T><<<blocks, threads, smem, rq.stream>>>(a);
+      EVB_CUDA(launch_pdl(eval_small_kernel<T>, dim3(blocks), dim3(threads), smem, rq.stream, a));
     }
     EVB_CUDA(cudaGetLastError());
     count_launch();

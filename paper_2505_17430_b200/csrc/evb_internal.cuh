@@ -186,6 +186,25 @@ inline cudaError_t copy_h2d_now(void* dst, const void* src, size_t n) {
   return e != cudaSuccess ? e : cudaStreamSynchronize(nullptr);
 }
 
+// Launch with programmatic stream serialisation (PDL): the kernel's launch overlaps the tail of
+// the previous kernel in the stream; the kernel itself must call ptx::griddep_wait() before
+// touching predecessor data (launch latency is most of a small generation's kernel time).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = grid;
+  lc.blockDim = block;
+  lc.dynamicSmemBytes = smem;
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  return cudaLaunchKernelEx(&lc, kernel, static_cast<KArgs>(args)...);
+}
+
 // Grow-only device buffer; synchronises `stream` before releasing an old allocation.
 inline void ensure_buffer(void** ptr, size_t* cap, size_t need, cudaStream_t stream) {
   if (*cap >= need && *ptr) return;

@@ -116,6 +116,14 @@ __device__ __forceinline__ double lds_f64(uint32_t addr) {
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
   return v;
 }
+// Programmatic dependent launch: a kernel launched with programmatic stream serialisation may
+// start while its predecessor drains; griddep_wait() blocks until the predecessor grid has
+// completed and its memory is visible (a no-op for a normal launch), so it goes before any
+// access to data a predecessor reads or writes.  griddep_launch_dependents() lets the next
+// kernel in the stream start launching now.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ double2 lds_f64x2(uint32_t addr) {
   double2 v;
   asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
