@@ -843,6 +843,9 @@ __global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
   __syncthreads();
   umma::fence_after();
   const uint32_t tmem = *tmem_slot;
+  // launched with PDL behind the split pre-pass: barrier init and TMEM allocation above overlap
+  // its tail; S_hi / S_lo (and the partials / tickets of earlier launches) only after it completed
+  ptx::griddep_wait();
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer ----------------
@@ -1218,7 +1221,7 @@ void launch_f32_umma(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUt
     attr = true;
   }
   dim3 grid((fp.P + C::BM - 1) / C::BM, (fp.D + BN - 1) / BN);
-  kern<<<grid, C::THREADS, C::SMEM, st>>>(a_hi, a_lo, b_hi, b_lo, fp);
+  EVB_CUDA(launch_pdl(kern, grid, dim3(C::THREADS), C::SMEM, st, a_hi, a_lo, b_hi, b_lo, fp));
   EVB_CUDA(cudaGetLastError());
   count_launch();
 }

@@ -106,6 +106,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 // split pre-pass: S = X - o (fp32, reference rounding), S_hi = rna_tf32(S), S_lo = S - S_hi
 __global__ void split_tf32_kernel(const float* __restrict__ X, int64_t ldx, const float* __restrict__ shift, int P,
                                   int D, float* __restrict__ hi, float* __restrict__ lo, int64_t lds) {
+  ptx::griddep_launch_dependents();  // the MMA kernel's prologue may overlap this pass (PDL)
   const int i = blockIdx.y;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < lds; k += gridDim.x * blockDim.x) {
     float h = 0.f, l = 0.f;
