@@ -578,6 +578,21 @@ __global__ void __launch_bounds__(f64m_cfg<NP>::THREADS, 1)
   const int mtile = p0.tiles_nfast ? blockIdx.y : blockIdx.x, ntile = p0.tiles_nfast ? blockIdx.x : blockIdx.y;
   const int m0 = mtile * C::BM, n0 = ntile * C::BN;
   const int KT = (p0.D + C::KB - 1) / C::KB;
+  // EVB_K1_TIMELINE=1 (tuning aid): CTA phase stamps (entry, first stage, mainloop end, exit)
+  unsigned long long* ts = p0.dbg_ts ? p0.dbg_ts + 8 * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
+  auto stamp = [&](int i) {
+    if (ts && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      ts[i] = t;
+    }
+  };
+  stamp(0);
+  if (ts && threadIdx.x == 0) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    ts[7] = sm;
+  }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -634,6 +649,7 @@ __global__ void __launch_bounds__(f64m_cfg<NP>::THREADS, 1)
   for (int kb = 0; kb < KT; ++kb) {
     const int s = kb % C::STAGES;
     ptx::mbar_wait(&full[s], (kb / C::STAGES) & 1);
+    if (kb == 0) stamp(1);
     const uint32_t sA = smem_base + s * C::STAGE_BYTES;
     const uint32_t sB = sA + C::A_BYTES + grp * C::B_BYTES;
     const uint32_t sO = sA + C::A_BYTES + NP * C::B_BYTES + grp * C::O_BYTES;
@@ -644,6 +660,7 @@ __global__ void __launch_bounds__(f64m_cfg<NP>::THREADS, 1)
 
   // every group has drained the ring: park each group's tile in its own region, then per group
   // the fused epilogue (named barrier 2 + g over the group's 128 threads)
+  stamp(2);
   ptx::named_bar_sync(1, C::NCW * 32);
   double* zt = reinterpret_cast<double*>(smem) + size_t(grp) * C::BM * C::LDT;
 #pragma unroll
@@ -656,6 +673,7 @@ __global__ void __launch_bounds__(f64m_cfg<NP>::THREADS, 1)
   const fused_params<double>& pg = grp == 0 ? p0 : (grp == 1 ? p1 : p2);
   tile_epilogue<double, C::BM, C::BN>(pg, zt, C::LDT, m0, n0, threadIdx.x - grp * C::WM * 32, C::WM * 32,
                                       last_flag + grp, mtile, ntile, 2 + grp);
+  stamp(4);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1556,7 +1574,28 @@ bool gemm_eval_multi(const eval_request* rqs, int np, const void* X, int64_t ldx
       EVB_CUDA(cudaFuncSetAttribute(eval_f64_dmma_multi_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
       attr = true;
     }
+    static const bool timeline = std::getenv("EVB_K1_TIMELINE") != nullptr;
+    unsigned long long* dts = nullptr;
+    const int nct = int(grid.x * grid.y);
+    if (timeline) {
+      EVB_CUDA(cudaMalloc(&dts, size_t(nct) * 64));
+      EVB_CUDA(cudaMemset(dts, 0, size_t(nct) * 64));
+      fp[0].dbg_ts = dts;
+    }
     eval_f64_dmma_multi_kernel<3><<<grid, C::THREADS, C::SMEM, st>>>(tmX, maps3, fp[0], fp[1], fp[2]);
+    if (timeline) {  // one synchronous launch, phase stamps appended to a CSV
+      EVB_CUDA(cudaStreamSynchronize(st));
+      std::vector<unsigned long long> h(size_t(nct) * 8);
+      EVB_CUDA(cudaMemcpy(h.data(), dts, h.size() * 8, cudaMemcpyDeviceToHost));
+      cudaFree(dts);
+      if (FILE* f = std::fopen("gpurun_out/k1m_ts.csv", "a")) {
+        for (int c = 0; c < nct; ++c)
+          std::fprintf(f, "%d,%llu,%llu,%llu,%llu,%llu\n", c, h[c * 8 + 0], h[c * 8 + 1], h[c * 8 + 2], h[c * 8 + 4],
+                       h[c * 8 + 7]);
+        std::fprintf(f, "end\n");
+        std::fclose(f);
+      }
+    }
   } else {
     using C = f64m_cfg<2>;
     static bool attr = false;
