@@ -264,7 +264,7 @@ __global__ void de_draw_philox_kernel(const de_dev<T> d) {
   if (i >= d.P) return;
   const int arch_size = *d.arch_size;
   const uint32_t gen = *d.gen_ptr;
-  word_reader r{&d.src, (uint64_t(gen) << 32) | uint32_t(i), 0, 0, d.overflow};
+  philox_prefetch_reader<5> r(d.src.key, (uint64_t(gen) << 32) | uint32_t(i));  // the PHILOX source
   draw_scalars<T>(d, i, arch_size, r);
   const int64_t xw = d.cfg.crossover == EVB_CX_BINOMIAL ? d.D : 0;  // gene uniforms follow the scalars
   d.woff[i] = r.count;

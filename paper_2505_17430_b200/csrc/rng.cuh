@@ -84,6 +84,29 @@ struct word_reader {
   }
 };
 
+// A Philox sub-stream with its first 2 * NB words computed up front: NB independent Philox blocks
+// (instruction-level parallel) instead of one block per word in sequence, each recomputing its
+// pair's block.  Word n is still philox_word(key, ctr_hi, n), so values and `count` are exactly
+// word_reader's for a PHILOX source.
+template <int NB>
+struct philox_prefetch_reader {
+  uint64_t key, ctr_hi;
+  int64_t count = 0;
+  uint64_t w[2 * NB];
+  __device__ __forceinline__ philox_prefetch_reader(uint64_t k, uint64_t c) : key(k), ctr_hi(c) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) philox_pair(k, c, uint64_t(b), w[2 * b], w[2 * b + 1]);
+  }
+  __device__ __forceinline__ uint64_t next() {
+    const int64_t n = count++;
+    if (n >= 2 * NB) return philox_word(key, ctr_hi, uint64_t(n));
+    const uint64_t v = w[0];  // shift the prefetched words down (registers, no dynamic index)
+#pragma unroll
+    for (int q = 0; q + 1 < 2 * NB; ++q) w[q] = w[q + 1];
+    return v;
+  }
+};
+
 __device__ __forceinline__ uint64_t word_at(const word_source& s, uint64_t ctr_hi, int64_t n, int* overflow) {
   if (s.mode == RNG_PHILOX) return philox_word(s.key, ctr_hi, uint64_t(n));
   if (n >= s.n_words) {

@@ -50,29 +50,6 @@ struct phase_clock {
   }
 };
 
-// Individual i's draw sub-stream with its first eight words computed up front: four independent
-// Philox blocks (instruction-level parallel) instead of one block per word in sequence, each
-// recomputing its pair's block.  Word n is still philox_word(key, ctr_hi, n), so the values and
-// the consumed count are exactly word_reader's.
-struct philox8_reader {
-  uint64_t key, ctr_hi;
-  int64_t count = 0;
-  uint64_t w0, w1, w2, w3, w4, w5, w6, w7;
-  __device__ __forceinline__ philox8_reader(uint64_t k, uint64_t c) : key(k), ctr_hi(c) {
-    philox_pair(k, c, 0, w0, w1);
-    philox_pair(k, c, 1, w2, w3);
-    philox_pair(k, c, 2, w4, w5);
-    philox_pair(k, c, 3, w6, w7);
-  }
-  __device__ __forceinline__ uint64_t next() {
-    const int64_t n = count++;
-    if (n >= 8) return philox_word(key, ctr_hi, uint64_t(n));
-    const uint64_t v = w0;  // shift the prefetched words down
-    w0 = w1; w1 = w2; w2 = w3; w3 = w4; w4 = w5; w5 = w6; w6 = w7;
-    return v;
-  }
-};
-
 struct run_problem {
   const double* shift[kRunsMaxComp];  // per component (base problem: component 0)
   const double* rot[kRunsMaxComp];
@@ -344,7 +321,7 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
     double* sTfit = sTfit2 + (g & 1) * P;
     // draws (thread per individual of this CTA's half)
     for (int i = p0 + int(threadIdx.x); i < p1; i += blockDim.x) {
-      philox8_reader r(key, (uint64_t(gen) << 32) | uint32_t(i));
+      philox_prefetch_reader<4> r(key, (uint64_t(gen) << 32) | uint32_t(i));
       int x1, x2, x3;
       if (a.mutation == EVB_MUT_RAND1) {
         do { x1 = draw_int(r, P); } while (x1 == i);
