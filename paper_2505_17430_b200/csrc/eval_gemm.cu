@@ -97,19 +97,22 @@ __device__ __forceinline__ float epi_cos<float>(float x) {
   return __cosf(r);
 }
 
-// cos(2 pi v) of the Rastrigin / Ackley terms.  fp64: the period is taken out exactly
+// cos(2 pi v) of the Rastrigin / Ackley terms.  fp64 fast form: the period is taken out exactly
 // (r = v - rint(v), rint by the 1.5 * 2^52 round-to-nearest trick: two adds, |r| <= 1/2) and
 // cos(2 pi r) is a degree-11 polynomial in r^2 (Chebyshev interpolation on [0, 1/4], fitted in
 // 50-digit arithmetic; max error 8e-16 over [-1/2, 1/2] evaluated in double) — 14 FP64 ops on
 // the DFMA pipe instead of the library cos's reduction.  It differs from the reference's
-// cos(fl(2 pi * v)) by the rounding of that product (|2 pi v| * 2^-53, ~1e-13 at |v| ~ 100)
-// plus ~1e-15: far inside the 1e-10 relative fitness tolerance of this tensor-core-order path.
-template <typename T>
+// cos(fl(2 pi * v)) by the rounding of that product, |2 pi v| * ~3.3e-16 (~2e-13 at |v| ~ 100),
+// plus ~1e-15.  That bound grows with |v|, so the fast form is only used while |v| < 2^16
+// (Ackley's mean-cosine error then stays < 2e-11 relative); callers take EXACT = true — the
+// reference's own expression through libm-grade cos — for any larger (or non-finite) argument.
+template <typename T, bool EXACT = false>
 __device__ __forceinline__ T epi_cos2pi(T v) { return epi_cos<T>(fop<T>::mul(two_pi_v<T>(), v)); }
 template <>
-__device__ __forceinline__ double epi_cos2pi<double>(double v) {
-  // |v| >= 2^51 (v a multiple of 1/2) takes rint; inf / NaN give NaN like cos
-  const double t = fabs(v) < 0x1p51 ? __dsub_rn(__dadd_rn(v, 0x1.8p52), 0x1.8p52) : rint(v);
+__device__ __forceinline__ double epi_cos2pi<double, true>(double v) { return cos(__dmul_rn(two_pi_v<double>(), v)); }
+template <>
+__device__ __forceinline__ double epi_cos2pi<double, false>(double v) {
+  const double t = __dsub_rn(__dadd_rn(v, 0x1.8p52), 0x1.8p52);  // rint(v) for |v| < 2^51
   const double r = __dsub_rn(v, t);
   const double u = __dmul_rn(r, r);
   double c = -0.0002900600501912893;
@@ -125,18 +128,23 @@ __device__ __forceinline__ double epi_cos2pi<double>(double v) {
   c = fma(c, u, -19.739208802178716);
   return fma(c, u, 1.0);
 }
-
+// arguments the fast form may not take (fp64 only): |v| >= 2^16, inf (NaN passes through it)
 template <typename T>
+__device__ __forceinline__ bool cos2pi_needs_exact(T v) {
+  return std::is_same<T, double>::value && fabs(double(v)) >= 65536.0;
+}
+
+template <typename T, bool EXACT = false>
 __device__ __forceinline__ T term_value(int term, T v, int col, const T* ell_w) {
   using F = fop<T>;
   switch (term) {
     case TERM_SQ: return F::mul(v, v);
     case TERM_WSQ: return elliptic_term<T>(ell_w[col], v);
     case TERM_RAST: {  // v*v - T(10) * cos(two_pi * v) + T(10)  (problems/batch.hpp:161)
-      const T c = epi_cos2pi<T>(v);
+      const T c = epi_cos2pi<T, EXACT>(v);
       return F::add(F::sub(F::mul(v, v), F::mul(T(10), c)), T(10));
     }
-    case TERM_COS: return epi_cos2pi<T>(v);
+    case TERM_COS: return epi_cos2pi<T, EXACT>(v);
     case TERM_TAIL: return col >= 1 ? F::mul(v, v) : T(0);
     case TERM_HEAD: return col == 0 ? v : T(0);
     case TERM_GCOS: return epi_cos<T>(F::div(v, F::sqrt_(T(col + 1))));
@@ -155,7 +163,8 @@ __device__ __forceinline__ T accumulate16(T acc, const T (&v)[16], int col0, int
   for (int q = 0; q < 16; ++q) {
     const int col = col0 + q;
     if (col < D) {
-      const T t = term_value<T>(TERM, v[q], col, ell_w);
+      const T t = cos2pi_needs_exact(v[q]) ? term_value<T, true>(TERM, v[q], col, ell_w)
+                                           : term_value<T, false>(TERM, v[q], col, ell_w);
       acc = prod ? fop<T>::mul(acc, t) : fop<T>::add(acc, t);
     }
   }
@@ -228,26 +237,48 @@ __device__ __forceinline__ void epilogue_rows(const fused_params<T>& p, const T*
     else cw[cc] = T(0);
   }
   const uint32_t zs = static_cast<uint32_t>(__cvta_generic_to_shared(zt));
+  constexpr bool has_cos2pi = std::is_same<T, double>::value && (TERM == TERM_RAST || TERM == TERM_COS);
   for (int r0 = 0; r0 < rpw; r0 += 8) {
     T s[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) s[q] = ident;
+    auto block = [&](auto exact_tag) {
+      constexpr bool EXACT = decltype(exact_tag)::value;
 #pragma unroll
-    for (int cc = 0; cc < CPL; ++cc) {
-      const int col = n0 + cl[cc];
+      for (int cc = 0; cc < CPL; ++cc) {
+        const int col = n0 + cl[cc];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int r = warp + (r0 + q) * nwarps;
-        const bool ok = cv[cc] && r0 + q < rpw && r < BM;
-        const T z = ptx::lds<T>(zs + uint32_t(((ok ? r : 0) * ldt + cl[cc]) * int(sizeof(T))));
-        T v;
-        if (TERM == TERM_WSQ) v = elliptic_term<T>(cw[cc], z);
-        else if (TERM == TERM_GCOS) v = epi_cos<T>(F::div(z, cw[cc]));
-        else v = term_value<T>(TERM, z, col, p.ell_w);
-        const T acc = prod ? F::mul(s[q], v) : F::add(s[q], v);
-        s[q] = ok ? acc : s[q];
+        for (int q = 0; q < 8; ++q) {
+          const int r = warp + (r0 + q) * nwarps;
+          const bool ok = cv[cc] && r0 + q < rpw && r < BM;
+          const T z = ptx::lds<T>(zs + uint32_t(((ok ? r : 0) * ldt + cl[cc]) * int(sizeof(T))));
+          T v;
+          if (TERM == TERM_WSQ) v = elliptic_term<T>(cw[cc], z);
+          else if (TERM == TERM_GCOS) v = epi_cos<T>(F::div(z, cw[cc]));
+          else v = term_value<T, EXACT>(TERM, z, col, p.ell_w);
+          const T acc = prod ? F::mul(s[q], v) : F::add(s[q], v);
+          s[q] = ok ? acc : s[q];
+        }
       }
+    };
+    // the fast cos(2 pi v) form covers |v| < 2^16; a warp whose 8-row group holds a larger (or
+    // non-finite) value evaluates that group with the reference's expression instead (uniform
+    // branch: the common path stays straight-line)
+    bool big = false;
+    if constexpr (has_cos2pi) {
+#pragma unroll
+      for (int cc = 0; cc < CPL; ++cc)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int r = warp + (r0 + q) * nwarps;
+          const bool ok = cv[cc] && r0 + q < rpw && r < BM;
+          const T z = ptx::lds<T>(zs + uint32_t(((ok ? r : 0) * ldt + cl[cc]) * int(sizeof(T))));
+          big = big || (ok && cos2pi_needs_exact(z));
+        }
+      big = __any_sync(0xffffffffu, big);
     }
+    if (big) block(std::true_type{});
+    else block(std::false_type{});
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       for (int off = 16; off > 0; off >>= 1) {

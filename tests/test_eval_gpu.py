@@ -354,3 +354,47 @@ def test_large_sizes_sampled(dev, n, dim):
     assert rel_err(out.cpu().numpy()[rows], ref) <= 1e-10
     del Xd
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("dim", [300, 1000])
+def test_gemm_path_extreme_inputs(dev, dim):
+    # the fused fp64 epilogue's fast cos(2 pi z) covers |z| < 2^16; larger and non-finite
+    # arguments take the reference's own expression (warp-uniform switch): rows scaled far out of
+    # the search domain, a NaN and an inf coordinate, against the C restatement — NaN / inf
+    # positions identical, finite values within the path's 1e-10
+    o, m = O.shift_rotation(7, dim)
+    X = O.population(8, 70, dim)
+    X[1] *= 1e3  # |z| beyond 2^16
+    X[40:47] *= 3e2  # a whole 8-row epilogue group (and neighbours) around 2^16
+    # far out (|z| ~ 1e7 .. 1e11): here the tensor-core summation order alone moves z by more than
+    # cos(2 pi z) can absorb (~1e-15 |z|), so only NaN / inf agreement and finiteness are checked
+    far = [2, 3]
+    X[2] *= 1e5
+    X[3] *= 1e9
+    X[5, 7] = np.nan
+    X[6, 11] = np.inf
+    X[9, 0] = -np.inf
+    kinds = [K.rastrigin, K.ackley, K.elliptic, K.griewank]
+    for kind in kinds:
+        p = evb.ProblemInstance.base(kind, o, m, 1.5)
+        got = gpu_eval(p, X, dev)
+        ref = O.eval_batch(int(kind), o, m, 1.5, X)
+        assert np.array_equal(np.isnan(got), np.isnan(ref)), kind
+        assert np.array_equal(np.isinf(got), np.isinf(ref)) and np.array_equal(got[np.isinf(ref)], ref[np.isinf(ref)])
+        fin = np.isfinite(ref)
+        fin[far] = False
+        assert rel_err(got[fin], ref[fin]) <= 1e-10, kind
+        assert np.all(np.isfinite(got[far]) == np.isfinite(ref[far])), kind
+    # the multi-problem launch (its own 64 x 56 tiling) on the same population
+    probs = [evb.ProblemInstance.base(k, o, m, 1.5) for k in kinds[:3]]
+    Xd = torch.from_numpy(X).to(dev)
+    outs = [torch.empty(X.shape[0], dtype=torch.float64, device=dev) for _ in probs]
+    evb.evaluate_batch_problems(probs, Xd, evb.EvalScratch(), outs)
+    torch.cuda.synchronize()
+    for kind, o_ in zip(kinds[:3], outs):
+        got = o_.cpu().numpy()
+        ref = O.eval_batch(int(kind), o, m, 1.5, X)
+        assert np.array_equal(np.isnan(got), np.isnan(ref)), kind
+        fin = np.isfinite(ref)
+        fin[far] = False
+        assert rel_err(got[fin], ref[fin]) <= 1e-10, kind
