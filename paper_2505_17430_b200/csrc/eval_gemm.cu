@@ -492,6 +492,10 @@ __global__ void __launch_bounds__(f64_cfg<BM, BN, WM, WN, STAGES>::THREADS, MINB
     ptx::fence_mbar_init();
   }
   __syncthreads();
+  // launched with PDL (launch_pdl): the prologue above overlaps the predecessor's tail; X, the
+  // partials and the tickets are touched only after it completed
+  ptx::griddep_wait();
+  ptx::griddep_launch_dependents();
 
   if (warp == C::NCW) {
     // ---------------- producer ----------------
@@ -1235,7 +1239,7 @@ void launch_f64(const CUtensorMap& tmX, const CUtensorMap& tmM, const fused_para
     attr = true;
   }
   dim3 grid((fp.P + BM - 1) / BM, (fp.D + BN - 1) / BN);
-  kern<<<grid, C::THREADS, C::SMEM, st>>>(tmX, tmM, fp);
+  EVB_CUDA(launch_pdl(kern, grid, dim3(C::THREADS), C::SMEM, st, tmX, tmM, fp));
   EVB_CUDA(cudaGetLastError());
   count_launch();
 }

@@ -23,6 +23,7 @@
 
 #include "evb_internal.cuh"
 #include "evb_math.cuh"
+#include "ptx.cuh"
 #include "rng.cuh"
 
 struct evb_pso_s {
@@ -59,6 +60,8 @@ __device__ __forceinline__ void argmin_merge(T& f, int& i, T f2, int i2) {
 // strict minimum == lexicographic (f, i) minimum); writes nb[i] = best for all i.
 template <typename T>
 __global__ void pso_gbest_kernel(const T* __restrict__ pf, int P, int* nb) {
+  ptx::griddep_wait();  // PDL (launch_pdl): predecessor data first
+  ptx::griddep_launch_dependents();
   __shared__ T sf[32];
   __shared__ int si[32];
   T bf = T(0);
@@ -94,6 +97,8 @@ __global__ void pso_gbest_kernel(const T* __restrict__ pf, int P, int* nb) {
 // ring of width one (pso/topology.hpp:44-54), offsets -1, 0, +1 in that order
 template <typename T>
 __global__ void pso_ring_kernel(const T* __restrict__ pf, int P, int* nb) {
+  ptx::griddep_wait();  // PDL (launch_pdl): predecessor data first
+  ptx::griddep_launch_dependents();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
   int best = -1;
@@ -169,6 +174,8 @@ __global__ void __launch_bounds__(256) pso_update_kernel(const pso_dev<T> d) {
 // 16-byte aligned.  Same arithmetic and draws as pso_update_kernel.
 template <typename T, int VEC>
 __global__ void __launch_bounds__(128) pso_update_vec_kernel(const pso_dev<T> d) {
+  ptx::griddep_wait();  // PDL (launch_pdl): predecessor data first
+  ptx::griddep_launch_dependents();
   using F = fop<T>;
   using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
   const int i = blockIdx.y;
@@ -332,6 +339,8 @@ __global__ void pso_spherical_kernel(const pso_dev<T> d) {
 template <typename T>
 __global__ void pso_pbest_kernel(const T* __restrict__ x, int64_t ldx, const T* __restrict__ fnew, T* fit, T* pb,
                                  int64_t ldb, T* pbf, int D, uint32_t* gen) {
+  ptx::griddep_wait();  // PDL (launch_pdl): predecessor data first
+  ptx::griddep_launch_dependents();
   const int i = blockIdx.x;
   if (i == 0 && threadIdx.x == 0) *gen += 1u;  // the update kernel (last reader) has finished
   const T f = fnew[i];
@@ -368,8 +377,8 @@ template <typename T>
 void generation_t(evb_pso_s* s, const device_problem* prob, evb_scratch_s* sc, void* X, int64_t ldx, void* V,
                   int64_t ldv, void* fit, double lb, double ub, evb_rng_s* r, cudaStream_t st) {
   const T* pf = static_cast<const T*>(s->pbest_fit);
-  if (s->topology == EVB_TOPO_GBEST) pso_gbest_kernel<T><<<1, 1024, 0, st>>>(pf, s->P, s->nb);
-  else pso_ring_kernel<T><<<(s->P + 255) / 256, 256, 0, st>>>(pf, s->P, s->nb);
+  if (s->topology == EVB_TOPO_GBEST) EVB_CUDA(launch_pdl(pso_gbest_kernel<T>, dim3(1), dim3(1024), 0, st, pf, s->P, s->nb));
+  else EVB_CUDA(launch_pdl(pso_ring_kernel<T>, dim3((s->P + 255) / 256), dim3(256), 0, st, pf, s->P, s->nb));
   count_launch();
   pso_dev<T> d{};
   d.P = s->P;
@@ -411,7 +420,7 @@ void generation_t(evb_pso_s* s, const device_problem* prob, evb_scratch_s* sc, v
                          (s->ldb * sizeof(T)) % 16 == 0;
     if (aligned) {
       dim3 grid(unsigned((s->D + 128 * VEC - 1) / (128 * VEC)), unsigned(s->P));
-      pso_update_vec_kernel<T, VEC><<<grid, 128, 0, st>>>(d);
+      EVB_CUDA(launch_pdl(pso_update_vec_kernel<T, VEC>, grid, dim3(128), 0, st, d));
     } else {
       dim3 grid((s->D + 255) / 256, s->P);
       pso_update_kernel<T><<<grid, 256, 0, st>>>(d);
@@ -435,9 +444,9 @@ void generation_t(evb_pso_s* s, const device_problem* prob, evb_scratch_s* sc, v
   rq.scalar_trig = true;
   eval_dispatch(rq);
   if (s->rec) recorder_observe(s->rec, s->rec_run, s->fit_new, s->P, st);  // particles in i (FE) order
-  pso_pbest_kernel<T><<<s->P, std::min(256, int(round_up(s->D, 32))), 0, st>>>(
-      static_cast<const T*>(X), ldx, static_cast<const T*>(s->fit_new), static_cast<T*>(fit),
-      static_cast<T*>(s->pbest), s->ldb, static_cast<T*>(s->pbest_fit), s->D, r->d_gen);
+  EVB_CUDA(launch_pdl(pso_pbest_kernel<T>, dim3(s->P), dim3(std::min(256, int(round_up(s->D, 32)))), 0, st,
+                      static_cast<const T*>(X), ldx, static_cast<const T*>(s->fit_new), static_cast<T*>(fit),
+                      static_cast<T*>(s->pbest), s->ldb, static_cast<T*>(s->pbest_fit), s->D, r->d_gen));
   count_launch();
   EVB_CUDA(cudaGetLastError());
   s->last_gen = r->gen;
