@@ -350,8 +350,14 @@ def run_evb(args, rank, world, local):
         # wall clock over `blocks` consecutive blocks of steps; the median block (a host-side
         # hiccup in one block — page-ins, another process — does not decide the figure); every
         # step of every block is a full host call with its copies and device sync
-        for _ in range(max(3, args.warmup // 2)):
+        # warm-up: at least W calls and 0.5 s of them — the host link comes out of its idle power
+        # state only under sustained traffic (the first ~0.1-0.2 s of calls after the device-side
+        # phases ran at up to 2x the steady per-call time, measured)
+        t_w = time.perf_counter()
+        n_w = 0
+        while n_w < max(3, args.warmup) or time.perf_counter() - t_w < 0.5:
             fn()
+            n_w += 1
         torch.cuda.synchronize()
         per = max(1, steps // blocks)
         times = []

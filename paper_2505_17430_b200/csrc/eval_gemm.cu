@@ -1517,21 +1517,25 @@ int multi_first_wave_rows(int np, int64_t n_points, int64_t dim) {
   if (np < 2 || np > 3) return 0;
   constexpr int BM = kMultiBM, BN = kMultiBN;
   const int64_t n_ntiles = (dim + BN - 1) / BN, n_mtiles = (n_points + BM - 1) / BM;
-  int dev = 0, sms = 0, per_sm = 0;
-  EVB_CUDA(cudaGetDevice(&dev));
-  EVB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  if (np == 3) {
-    EVB_CUDA(cudaFuncSetAttribute(eval_f64_dmma_multi_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  f64m_cfg<3>::SMEM));
-    EVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eval_f64_dmma_multi_kernel<3>,
-                                                           f64m_cfg<3>::THREADS, f64m_cfg<3>::SMEM));
-  } else {
-    EVB_CUDA(cudaFuncSetAttribute(eval_f64_dmma_multi_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  f64m_cfg<2>::SMEM));
-    EVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eval_f64_dmma_multi_kernel<2>,
-                                                           f64m_cfg<2>::THREADS, f64m_cfg<2>::SMEM));
+  // occupancy of the multi-problem kernel, queried once per NP (host cost of every host call)
+  static int per_sm_cache[4] = {0, 0, 0, 0};
+  const int sms = sm_count();
+  int per_sm = per_sm_cache[np];
+  if (per_sm == 0) {
+    if (np == 3) {
+      EVB_CUDA(cudaFuncSetAttribute(eval_f64_dmma_multi_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    f64m_cfg<3>::SMEM));
+      EVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eval_f64_dmma_multi_kernel<3>,
+                                                             f64m_cfg<3>::THREADS, f64m_cfg<3>::SMEM));
+    } else {
+      EVB_CUDA(cudaFuncSetAttribute(eval_f64_dmma_multi_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    f64m_cfg<2>::SMEM));
+      EVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eval_f64_dmma_multi_kernel<2>,
+                                                             f64m_cfg<2>::THREADS, f64m_cfg<2>::SMEM));
+    }
+    per_sm_cache[np] = per_sm = std::max(per_sm, 1);
   }
-  const int64_t wave = int64_t(sms) * std::max(per_sm, 1);
+  const int64_t wave = int64_t(sms) * per_sm;
   if (n_ntiles * n_mtiles <= wave) return 0;
   // row blocks the first wave covers completely (EVB_H2D_ROWS=ceil: also the partly covered one,
   // tuning aid); the first wave's few tiles of the next row block wait for the second group
