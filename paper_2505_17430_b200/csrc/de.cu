@@ -477,6 +477,7 @@ __global__ void de_reinit_kernel(const de_dev<T> d) {
 //   * SHADE / JADE sums stay sequential (one thread, successes staged in order) so the memory
 //     update rounds exactly like the reference's loops.
 constexpr int kSelThreads = 1024;
+constexpr int kOwnerSmem = 4096;
 
 template <typename T>
 __global__ void __launch_bounds__(kSelThreads) de_select_scan_kernel(const de_dev<T> d) {
@@ -490,7 +491,10 @@ __global__ void __launch_bounds__(kSelThreads) de_select_scan_kernel(const de_de
   const bool adapt = d.cfg.parameter == EVB_PAR_SHADE || d.cfg.parameter == EVB_PAR_JADE;
   // one pass-1 chunk: pass 1 stages the successes itself (no second trip through global memory)
   const bool staged_in_pass1 = adapt && d.P <= int(blockDim.x);
-  for (int s = tid; s < d.archive_cap; s += blockDim.x) d.owner[s] = -1;
+  // archive-slot owners (last writer wins): shared memory for archives up to kOwnerSmem slots
+  __shared__ int s_owner[kOwnerSmem];
+  int* owner = d.archive_cap <= kOwnerSmem ? s_owner : d.owner;
+  for (int s = tid; s < d.archive_cap; s += blockDim.x) owner[s] = -1;
   const int size0 = *d.arch_size;
   const int room = d.archive_cap - size0;
   const int64_t wpos = d.src.mode == RNG_WORDS ? *d.cursor : 0;
@@ -562,7 +566,7 @@ __global__ void __launch_bounds__(kSelThreads) de_select_scan_kernel(const de_de
           sl = uint_of(word_at(d.src, ctr_hi, d.src.mode == RNG_WORDS ? wpos + v : v, d.overflow), d.archive_cap);
         }
         d.arch_slot[i] = sl;  // provisional; resolved below
-        atomicMax(&d.owner[sl], q);
+        atomicMax(&owner[sl], q);
       }
     }
     __syncthreads();
@@ -578,7 +582,7 @@ __global__ void __launch_bounds__(kSelThreads) de_select_scan_kernel(const de_de
     const int i = base + tid;
     if (i < d.P && d.win[i] && d.archive_cap > 0) {
       const int sl = d.arch_slot[i];
-      if (d.owner[sl] != d.win[i] - 1) d.arch_slot[i] = -1;  // overwritten by a later push
+      if (owner[sl] != d.win[i] - 1) d.arch_slot[i] = -1;  // overwritten by a later push
     }
   }
   __syncthreads();
