@@ -11,16 +11,21 @@
 //   * consumer warps: the shift is applied while fragments are loaded from shared memory
 //     (x - o rounded in T exactly like problems/batch.hpp:50), then
 //       fp64: DMMA m8n8k4 tensor-core tiles (the only FP64 tensor route on sm_100a;
-//             tcgen05 has no f64 kind),
-//       fp32: FFMA register-tiled outer products (1xTF32 fails the 1e-4 tolerance);
+//             tcgen05 has no f64 kind), operands as conflict-free LDS.128 pairs
+//             (k order permuted inside each 16-deep slice, dmma_kslice);
+//       fp32: 3xTF32 on tcgen05 with TMEM accumulators (umma.cuh), or FFMA register-tiled
+//             outer products for discus / hybrids / compositions (1xTF32 fails the 1e-4
+//             tolerance);
 //   * epilogue: per-element transform terms (elliptic / rastrigin / ackley / sphere /
 //     bent-cigar / discus / griewank) are reduced per row inside the CTA, written as per-N-tile
 //     partials, and the last CTA of each row block (ticket counter) sums the partials in fixed
 //     N-tile order and applies the final formula + bias.  No float atomics: results are
 //     deterministic run to run.
+//   * several problems on one population (multi-problem K1): one CTA per tile holds a warp
+//     group per problem, the X slice is staged once for all of them.
 //   * z-store mode writes z in the reference's SoA layout (soa_z[i*ldz + b]) for the kinds
 //     whose epilogue needs neighbours or prefixes (rosenbrock, schwefel_1.2, schaffer F6,
-//     hybrids); eval_rows.cu finishes those.
+//     hybrids); eval_small.cu's row kernel finishes those.
 #include <cuda.h>
 #include <cuda_runtime.h>
 

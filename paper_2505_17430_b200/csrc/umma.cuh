@@ -8,14 +8,15 @@
 // transform (problems/batch.hpp:50) before the split (split pre-pass, HBM-bound, ~3 us);
 // M_hi / M_lo are split once when the problem is created.
 //
-// CTA (6 warps, one 128 x 64 output tile):
+// CTA (10 warps, one 128 x 64 output tile; launched with PDL behind the split pre-pass):
 //   warp 0  TMA producer: per 32-float K-slice, S_hi, S_lo (128 rows) and M_hi, M_lo (64 rows),
 //           SWIZZLE_128B, into a 4-stage mbarrier ring (48 KB per stage)
 //   warp 1  TMEM allocator + single-thread MMA issuer: 4 K-steps x 3 products of
 //           tcgen05.mma.cta_group::1.kind::tf32 (M=128, N=64, K=8) per stage; tcgen05.commit frees
 //           the stage and finally signals the epilogue
-//   warps 2-5 epilogue: tcgen05.ld 32x32b (each thread = one output row, 64 columns), transform
-//           terms, sequential row sum, N-tile partials + last-CTA finalisation (as K1).
+//   warps 2-9 epilogue: tcgen05.ld 32x32b, two warps per TMEM lane quarter (each thread = one
+//           output row, half of the 64 columns), transform terms, half-row sums meeting in shared
+//           memory, N-tile partials + last-CTA finalisation (as K1).
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
