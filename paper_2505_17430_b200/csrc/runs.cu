@@ -116,7 +116,21 @@ __device__ __forceinline__ void dot_rows(const double* __restrict__ m, const dou
     acc[q] = 0.0;
     sp[q] = sS + (i0 + (EXACT ? q : min(q, n - 1)) * G) * D;
   }
-  for (int k = 0; k < D; ++k) {
+  int k = 0;
+  if ((D & 1) == 0 && (reinterpret_cast<uintptr_t>(sS) & 15) == 0) {
+    // even D: each individual's (k, k+1) pair is one 16-byte word (LDS.128) — 10 instead of 18
+    // shared loads per pair of k; the adds stay in increasing k
+    for (; k < D; k += 2) {
+      const double mk0 = m[k], mk1 = m[k + 1];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const double2 sv = *reinterpret_cast<const double2*>(sp[q] + k);
+        acc[q] = __dadd_rn(acc[q], __dmul_rn(mk0, sv.x));
+        acc[q] = __dadd_rn(acc[q], __dmul_rn(mk1, sv.y));
+      }
+    }
+  }
+  for (; k < D; ++k) {
     const double mk = m[k];
 #pragma unroll
     for (int q = 0; q < Q; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(mk, sp[q][k]));
