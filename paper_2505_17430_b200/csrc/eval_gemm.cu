@@ -847,31 +847,43 @@ __global__ void __launch_bounds__(f64p_cfg<BM, BN, STAGES>::THREADS, 1)
 
 // ---------------------------------------------------------------------------------------
 // K2 on tcgen05 (see umma.cuh): 3xTF32, 128 x BN tile per CTA, accumulator in TMEM.
-template <int BN>
+// FUSE (BN = 64): the split pre-pass is folded in.  X tiles arrive by TMA in their own ring (XS
+// stages, same SWIZZLE_128B rows as S_hi / S_lo, so a 16-byte chunk keeps its position); the
+// eight epilogue warps, idle during the mainloop, form S = X - o, S_hi, S_lo straight into the
+// A/B stage (after the MMA released it) and release the X stage; the producer then loads only
+// M_hi / M_lo into the A/B ring.  L2 -> SM traffic per stage 48 -> 32 KB, no pre-pass launch.
+template <int BN, bool FUSE = false>
 struct umma_cfg {
   static constexpr int BM = 128;
   static constexpr int KB = 32;  // floats per K-slice (one 128-byte swizzle row)
   static constexpr int A_BYTES = BM * 128;
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // hi + lo of both operands
-  static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) < 4 ? (200 * 1024 / STAGE_BYTES) : 4;
+  static constexpr int XS = FUSE ? 4 : 0;                         // X ring (FUSE)
+  static constexpr int X_RING = XS * A_BYTES;
+  static constexpr int STAGES = FUSE ? 3 : ((200 * 1024 / STAGE_BYTES) < 4 ? (200 * 1024 / STAGE_BYTES) : 4);
   static constexpr int THREADS = 10 * 32;  // producer, MMA issuer, 8 epilogue warps
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // [0,BN): main, [BN,2BN): corrections
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + (2 * STAGES + 1) * 8 + 64;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + X_RING + 1024 + (3 * STAGES + 2 * XS + 1) * 8 + 64;
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
 };
 
-template <int BN>
-__global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
+template <int BN, bool FUSE>
+__global__ void __launch_bounds__(umma_cfg<BN, FUSE>::THREADS, 1)
     eval_f32_umma_kernel(const __grid_constant__ CUtensorMap tmShi, const __grid_constant__ CUtensorMap tmSlo,
                          const __grid_constant__ CUtensorMap tmMhi, const __grid_constant__ CUtensorMap tmMlo,
                          const fused_params<float> p) {
-  using C = umma_cfg<BN>;
+  // FUSE: tmShi maps X itself (tmSlo unused)
+  using C = umma_cfg<BN, FUSE>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint8_t* xring = smem + C::STAGES * C::STAGE_BYTES;  // FUSE: XS x (128 x 32 floats)
+  uint64_t* full = reinterpret_cast<uint64_t*>(xring + C::X_RING);
   uint64_t* empty = full + C::STAGES;
-  uint64_t* accfull = empty + C::STAGES;
+  uint64_t* aready = empty + C::STAGES;  // FUSE: the stage's S_hi / S_lo are formed
+  uint64_t* xfull = aready + C::STAGES;  // FUSE: X tile landed
+  uint64_t* xempty = xfull + C::XS;      // FUSE: X tile consumed by the split warps
+  uint64_t* accfull = xempty + C::XS;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accfull + 1);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
@@ -892,6 +904,11 @@ __global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
     for (int s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&aready[s], 8);
+    }
+    for (int s = 0; s < C::XS; ++s) {
+      ptx::mbar_init(&xfull[s], 1);
+      ptx::mbar_init(&xempty[s], 8);
     }
     ptx::mbar_init(accfull, 1);
     ptx::fence_mbar_init();
@@ -913,11 +930,21 @@ __global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
       ptx::prefetch_tma(&tmMlo);
       for (int kb = 0; kb < KT; ++kb) {
         const int s = kb % C::STAGES;
+        if constexpr (FUSE) {  // X tile into its own ring, as far ahead as the split warps allow
+          const int sx = kb % C::XS;
+          if (kb >= C::XS) ptx::mbar_wait(&xempty[sx], ((kb / C::XS) - 1) & 1);
+          ptx::mbar_arrive_expect_tx(&xfull[sx], C::A_BYTES);
+          ptx::tma_load_2d(xring + sx * C::A_BYTES, &tmShi, &xfull[sx], kb * C::KB, m0);
+        }
         if (kb >= C::STAGES) ptx::mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
         uint8_t* st = smem + s * C::STAGE_BYTES;
-        ptx::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
-        ptx::tma_load_2d(st, &tmShi, &full[s], kb * C::KB, m0);
-        ptx::tma_load_2d(st + C::A_BYTES, &tmSlo, &full[s], kb * C::KB, m0);
+        if constexpr (FUSE) {
+          ptx::mbar_arrive_expect_tx(&full[s], 2 * C::B_BYTES);
+        } else {
+          ptx::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
+          ptx::tma_load_2d(st, &tmShi, &full[s], kb * C::KB, m0);
+          ptx::tma_load_2d(st + C::A_BYTES, &tmSlo, &full[s], kb * C::KB, m0);
+        }
         ptx::tma_load_2d(st + 2 * C::A_BYTES, &tmMhi, &full[s], kb * C::KB, n0);
         ptx::tma_load_2d(st + 2 * C::A_BYTES + C::B_BYTES, &tmMlo, &full[s], kb * C::KB, n0);
       }
@@ -929,6 +956,7 @@ __global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
       for (int kb = 0; kb < KT; ++kb) {
         const int s = kb % C::STAGES;
         ptx::mbar_wait(&full[s], (kb / C::STAGES) & 1);
+        if constexpr (FUSE) ptx::mbar_wait(&aready[s], (kb / C::STAGES) & 1);
         if (kb == 0) stamp(1);
         umma::fence_after();
         const uint32_t sa_hi = base + s * C::STAGE_BYTES, sa_lo = sa_hi + C::A_BYTES;
@@ -957,6 +985,47 @@ __global__ void __launch_bounds__(umma_cfg<BN>::THREADS, 1)
     const int r = quarter * 32 + lane;
     const int row = m0 + r;
     const int etid = threadIdx.x - 64;  // 0..255
+    if constexpr (FUSE) {
+      // split of each X tile: S = X - o (fp32, reference rounding), S_hi = rna_tf32(S),
+      // S_lo = rna_tf32(S - S_hi) — the pre-pass's arithmetic — written into the A/B stage once
+      // the MMA has released it; chunk q of row q / 8 holds logical chunk (q & 7) ^ (row & 7)
+      // (columns >= D: X is zero-filled by TMA and o zero-padded, so S = 0).  The generic-proxy
+      // writes are fenced to the async proxy before the arrive.
+      for (int kb = 0; kb < KT; ++kb) {
+        const int s = kb % C::STAGES, sx = kb % C::XS;
+        ptx::mbar_wait(&xfull[sx], (kb / C::XS) & 1);
+        if (kb >= C::STAGES) ptx::mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
+        const float4* xs = reinterpret_cast<const float4*>(xring + sx * C::A_BYTES);
+        uint8_t* st = smem + s * C::STAGE_BYTES;
+        float4* hi = reinterpret_cast<float4*>(st);
+        float4* lo = reinterpret_cast<float4*>(st + C::A_BYTES);
+#pragma unroll
+        for (int u = 0; u < C::A_BYTES / 16 / 256; ++u) {
+          const int q = etid + u * 256;
+          const int rr = q >> 3, c = (q & 7) ^ (rr & 7);
+          const float4 x = xs[q];
+          const float4 o = __ldg(reinterpret_cast<const float4*>(p.shift + size_t(kb) * C::KB + c * 4));
+          auto split = [](float xv, float ov, float& hv, float& lv) {
+            const float sv = __fsub_rn(xv, ov);
+            hv = __uint_as_float(umma::cvt_rna_tf32(sv));
+            lv = __uint_as_float(umma::cvt_rna_tf32(__fsub_rn(sv, hv)));
+          };
+          float4 h, l;
+          split(x.x, o.x, h.x, l.x);
+          split(x.y, o.y, h.y, l.y);
+          split(x.z, o.z, h.z, l.z);
+          split(x.w, o.w, h.w, l.w);
+          hi[q] = h;
+          lo[q] = l;
+        }
+        ptx::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          ptx::mbar_arrive(&xempty[sx]);
+          ptx::mbar_arrive(&aready[s]);
+        }
+      }
+    }
     ptx::mbar_wait_sleep(accfull, 0);
     if (threadIdx.x == 64) stamp(3);
     umma::fence_after();
@@ -1268,11 +1337,11 @@ void launch_f64_persistent(const CUtensorMap& tmX, const CUtensorMap& tmM, const
   count_launch();
 }
 
-template <int BN>
+template <int BN, bool FUSE = false>
 void launch_f32_umma(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUtensorMap& b_hi, const CUtensorMap& b_lo,
                      const fused_params<float>& fp, cudaStream_t st) {
-  using C = umma_cfg<BN>;
-  auto kern = eval_f32_umma_kernel<BN>;
+  using C = umma_cfg<BN, FUSE>;
+  auto kern = eval_f32_umma_kernel<BN, FUSE>;
   static bool attr = false;
   if (!attr) {
     EVB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -1393,17 +1462,27 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
           pr->rot_lo = rlo;
         }
       }
-      const int64_t lds = round_up(D, 32);
-      ensure_buffer(&sc->s_hi, &sc->s_hi_bytes, size_t(lds) * P * sizeof(float), rq.stream);
-      ensure_buffer(&sc->s_lo, &sc->s_lo_bytes, size_t(lds) * P * sizeof(float), rq.stream);
-      split_tf32_kernel<<<dim3(unsigned((lds + 255) / 256), unsigned(P)), 256, 0, rq.stream>>>(
-          static_cast<const float*>(X), ldx, shift, P, D, static_cast<float*>(sc->s_hi), static_cast<float*>(sc->s_lo),
-          lds);
-      count_launch();
+      // UBN = 64 (the default): the split folded into the kernel (EVB_F32_FUSE=0 keeps the
+      // pre-pass, A/B); other widths (EVB_UMMA_BN, tuning) keep the pre-pass
+      static const char* fuse_env = std::getenv("EVB_F32_FUSE");
+      const bool fuse = UBN == 64 && !(fuse_env && std::string(fuse_env) == "0");
       CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
-      bool ok = make_tma_2d(&ta_hi, sc->s_hi, EVB_F32, uint64_t(lds), uint64_t(P), uint64_t(lds) * 4, 32, 128) &&
-                make_tma_2d(&ta_lo, sc->s_lo, EVB_F32, uint64_t(lds), uint64_t(P), uint64_t(lds) * 4, 32, 128) &&
-                make_tma_2d(&tb_hi, rhi, EVB_F32, uint64_t(ldm), uint64_t(D), uint64_t(ldm) * 4, 32, uint32_t(UBN)) &&
+      bool ok = true;
+      if (fuse) {
+        ok = make_tma_2d(&ta_hi, X, EVB_F32, uint64_t(D), uint64_t(P), uint64_t(ldx) * 4, 32, 128);
+        ta_lo = ta_hi;
+      } else {
+        const int64_t lds = round_up(D, 32);
+        ensure_buffer(&sc->s_hi, &sc->s_hi_bytes, size_t(lds) * P * sizeof(float), rq.stream);
+        ensure_buffer(&sc->s_lo, &sc->s_lo_bytes, size_t(lds) * P * sizeof(float), rq.stream);
+        split_tf32_kernel<<<dim3(unsigned((lds + 255) / 256), unsigned(P)), 256, 0, rq.stream>>>(
+            static_cast<const float*>(X), ldx, shift, P, D, static_cast<float*>(sc->s_hi),
+            static_cast<float*>(sc->s_lo), lds);
+        count_launch();
+        ok = make_tma_2d(&ta_hi, sc->s_hi, EVB_F32, uint64_t(lds), uint64_t(P), uint64_t(lds) * 4, 32, 128) &&
+             make_tma_2d(&ta_lo, sc->s_lo, EVB_F32, uint64_t(lds), uint64_t(P), uint64_t(lds) * 4, 32, 128);
+      }
+      ok = ok && make_tma_2d(&tb_hi, rhi, EVB_F32, uint64_t(ldm), uint64_t(D), uint64_t(ldm) * 4, 32, uint32_t(UBN)) &&
                 make_tma_2d(&tb_lo, rlo, EVB_F32, uint64_t(ldm), uint64_t(D), uint64_t(ldm) * 4, 32, uint32_t(UBN));
       if (!ok) throw runtime_error("gemm_eval: cannot encode the TMA descriptors of the tf32 split");
       fp.n_ntiles = (D + UBN - 1) / UBN;
@@ -1429,7 +1508,8 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
         EVB_CUDA(cudaMemset(d, 0, size_t(nct) * 8 * 8));
         fused_params<float> f2 = fp;
         f2.dbg_ts = d;
-        launch_f32_umma<64>(ta_hi, ta_lo, tb_hi, tb_lo, f2, rq.stream);
+        if (fuse) launch_f32_umma<64, true>(ta_hi, ta_lo, tb_hi, tb_lo, f2, rq.stream);
+        else launch_f32_umma<64>(ta_hi, ta_lo, tb_hi, tb_lo, f2, rq.stream);
         EVB_CUDA(cudaStreamSynchronize(rq.stream));
         std::vector<unsigned long long> h(size_t(nct) * 8);
         EVB_CUDA(cudaMemcpy(h.data(), d, h.size() * 8, cudaMemcpyDeviceToHost));
@@ -1443,6 +1523,7 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
         }
       } else if (UBN == 256) launch_f32_umma<256>(ta_hi, ta_lo, tb_hi, tb_lo, fp, rq.stream);
       else if (UBN == 128) launch_f32_umma<128>(ta_hi, ta_lo, tb_hi, tb_lo, fp, rq.stream);
+      else if (fuse) launch_f32_umma<64, true>(ta_hi, ta_lo, tb_hi, tb_lo, fp, rq.stream);
       else launch_f32_umma<64>(ta_hi, ta_lo, tb_hi, tb_lo, fp, rq.stream);
       if (!own_rot) {
         EVB_CUDA(cudaStreamSynchronize(rq.stream));
