@@ -5,16 +5,19 @@
 // split into a TF32-exact head and its remainder, a = a_hi + a_lo, and
 //     z = S_hi M_hi^T + S_hi M_lo^T + S_lo M_hi^T        (the a_lo b_lo term, ~2^-22, dropped)
 // accumulated in fp32 in TMEM.  S = X - o is rounded in fp32 exactly like the reference's
-// transform (problems/batch.hpp:50) before the split (split pre-pass, HBM-bound, ~3 us);
-// M_hi / M_lo are split once when the problem is created.
+// transform (problems/batch.hpp:50) before the split; M_hi / M_lo are split once when the
+// problem is created.  The S split is folded into the kernel at the default tile width (FUSE,
+// eval_gemm.cu); other widths run the split pre-pass below first.
 //
-// CTA (10 warps, one 128 x 64 output tile; launched with PDL behind the split pre-pass):
-//   warp 0  TMA producer: per 32-float K-slice, S_hi, S_lo (128 rows) and M_hi, M_lo (64 rows),
-//           SWIZZLE_128B, into a 4-stage mbarrier ring (48 KB per stage)
+// CTA (10 warps, one 128 x 64 output tile):
+//   warp 0  TMA producer: per 32-float K-slice, M_hi, M_lo (64 rows) into the A/B ring and X
+//           (128 rows) into its own ring (FUSE), or S_hi, S_lo, M_hi, M_lo into a 4-stage ring
+//           (pre-pass mode); SWIZZLE_128B, 48 KB A/B stages
 //   warp 1  TMEM allocator + single-thread MMA issuer: 4 K-steps x 3 products of
 //           tcgen05.mma.cta_group::1.kind::tf32 (M=128, N=64, K=8) per stage; tcgen05.commit frees
 //           the stage and finally signals the epilogue
-//   warps 2-9 epilogue: tcgen05.ld 32x32b, two warps per TMEM lane quarter (each thread = one
+//   warps 2-9 during the mainloop (FUSE): S_hi / S_lo of each X tile into the A/B stage;
+//           epilogue: tcgen05.ld 32x32b, two warps per TMEM lane quarter (each thread = one
 //           output row, half of the 64 columns), transform terms, half-row sums meeting in shared
 //           memory, N-tile partials + last-CTA finalisation (as K1).
 #pragma once
