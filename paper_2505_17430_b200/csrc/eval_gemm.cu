@@ -847,11 +847,11 @@ __global__ void __launch_bounds__(f64p_cfg<BM, BN, STAGES>::THREADS, 1)
 
 // ---------------------------------------------------------------------------------------
 // K2 on tcgen05 (see umma.cuh): 3xTF32, 128 x BN tile per CTA, accumulator in TMEM.
-// FUSE (BN = 64): the split pre-pass is folded in.  X tiles arrive by TMA in their own ring (XS
-// stages, same SWIZZLE_128B rows as S_hi / S_lo, so a 16-byte chunk keeps its position); the
-// eight epilogue warps, idle during the mainloop, form S = X - o, S_hi, S_lo straight into the
-// A/B stage (after the MMA released it) and release the X stage; the producer then loads only
-// M_hi / M_lo into the A/B ring.  L2 -> SM traffic per stage 48 -> 32 KB, no pre-pass launch.
+// FUSE (BN = 64): the split pre-pass is folded in.  The X tile arrives by TMA in the stage's
+// S_hi slot (same SWIZZLE_128B rows as S_hi / S_lo, so a 16-byte chunk keeps its position); the
+// eight epilogue warps, idle during the mainloop, form S = X - o, S_hi, S_lo in place (S_hi over
+// X, S_lo into its slot) and signal the MMA issuer.  L2 -> SM traffic per stage 48 -> 32 KB, no
+// pre-pass launch.
 template <int BN, bool FUSE = false>
 struct umma_cfg {
   static constexpr int BM = 128;
@@ -859,12 +859,10 @@ struct umma_cfg {
   static constexpr int A_BYTES = BM * 128;
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // hi + lo of both operands
-  static constexpr int XS = FUSE ? 4 : 0;                         // X ring (FUSE)
-  static constexpr int X_RING = XS * A_BYTES;
-  static constexpr int STAGES = FUSE ? 3 : ((200 * 1024 / STAGE_BYTES) < 4 ? (200 * 1024 / STAGE_BYTES) : 4);
+  static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) < 4 ? (200 * 1024 / STAGE_BYTES) : 4;
   static constexpr int THREADS = 10 * 32;  // producer, MMA issuer, 8 epilogue warps
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // [0,BN): main, [BN,2BN): corrections
-  static constexpr int SMEM = STAGES * STAGE_BYTES + X_RING + 1024 + (3 * STAGES + 2 * XS + 1) * 8 + 64;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + (3 * STAGES + 1) * 8 + 64;
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
 };
 
@@ -877,13 +875,10 @@ __global__ void __launch_bounds__(umma_cfg<BN, FUSE>::THREADS, 1)
   using C = umma_cfg<BN, FUSE>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
-  uint8_t* xring = smem + C::STAGES * C::STAGE_BYTES;  // FUSE: XS x (128 x 32 floats)
-  uint64_t* full = reinterpret_cast<uint64_t*>(xring + C::X_RING);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* aready = empty + C::STAGES;  // FUSE: the stage's S_hi / S_lo are formed
-  uint64_t* xfull = aready + C::STAGES;  // FUSE: X tile landed
-  uint64_t* xempty = xfull + C::XS;      // FUSE: X tile consumed by the split warps
-  uint64_t* accfull = xempty + C::XS;
+  uint64_t* accfull = aready + C::STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accfull + 1);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
@@ -906,10 +901,6 @@ __global__ void __launch_bounds__(umma_cfg<BN, FUSE>::THREADS, 1)
       ptx::mbar_init(&empty[s], 1);
       ptx::mbar_init(&aready[s], 8);
     }
-    for (int s = 0; s < C::XS; ++s) {
-      ptx::mbar_init(&xfull[s], 1);
-      ptx::mbar_init(&xempty[s], 8);
-    }
     ptx::mbar_init(accfull, 1);
     ptx::fence_mbar_init();
   }
@@ -930,16 +921,11 @@ __global__ void __launch_bounds__(umma_cfg<BN, FUSE>::THREADS, 1)
       ptx::prefetch_tma(&tmMlo);
       for (int kb = 0; kb < KT; ++kb) {
         const int s = kb % C::STAGES;
-        if constexpr (FUSE) {  // X tile into its own ring, as far ahead as the split warps allow
-          const int sx = kb % C::XS;
-          if (kb >= C::XS) ptx::mbar_wait(&xempty[sx], ((kb / C::XS) - 1) & 1);
-          ptx::mbar_arrive_expect_tx(&xfull[sx], C::A_BYTES);
-          ptx::tma_load_2d(xring + sx * C::A_BYTES, &tmShi, &xfull[sx], kb * C::KB, m0);
-        }
         if (kb >= C::STAGES) ptx::mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
         uint8_t* st = smem + s * C::STAGE_BYTES;
-        if constexpr (FUSE) {
-          ptx::mbar_arrive_expect_tx(&full[s], 2 * C::B_BYTES);
+        if constexpr (FUSE) {  // X into the A_hi slot (converted in place), M_hi / M_lo as usual
+          ptx::mbar_arrive_expect_tx(&full[s], C::A_BYTES + 2 * C::B_BYTES);
+          ptx::tma_load_2d(st, &tmShi, &full[s], kb * C::KB, m0);
         } else {
           ptx::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
           ptx::tma_load_2d(st, &tmShi, &full[s], kb * C::KB, m0);
@@ -987,16 +973,15 @@ __global__ void __launch_bounds__(umma_cfg<BN, FUSE>::THREADS, 1)
     const int etid = threadIdx.x - 64;  // 0..255
     if constexpr (FUSE) {
       // split of each X tile: S = X - o (fp32, reference rounding), S_hi = rna_tf32(S),
-      // S_lo = rna_tf32(S - S_hi) — the pre-pass's arithmetic — written into the A/B stage once
-      // the MMA has released it; chunk q of row q / 8 holds logical chunk (q & 7) ^ (row & 7)
-      // (columns >= D: X is zero-filled by TMA and o zero-padded, so S = 0).  The generic-proxy
-      // writes are fenced to the async proxy before the arrive.
+      // S_lo = rna_tf32(S - S_hi) — the pre-pass's arithmetic — in place in the stage; chunk q
+      // of row q / 8 holds logical chunk (q & 7) ^ (row & 7) (columns >= D: X is zero-filled by
+      // TMA and o zero-padded, so S = 0).  The generic-proxy writes are fenced to the async proxy
+      // before the arrive.
       for (int kb = 0; kb < KT; ++kb) {
-        const int s = kb % C::STAGES, sx = kb % C::XS;
-        ptx::mbar_wait(&xfull[sx], (kb / C::XS) & 1);
-        if (kb >= C::STAGES) ptx::mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
-        const float4* xs = reinterpret_cast<const float4*>(xring + sx * C::A_BYTES);
+        const int s = kb % C::STAGES;
+        ptx::mbar_wait(&full[s], (kb / C::STAGES) & 1);  // X (and M) landed
         uint8_t* st = smem + s * C::STAGE_BYTES;
+        const float4* xs = reinterpret_cast<const float4*>(st);  // each thread rewrites its own chunks
         float4* hi = reinterpret_cast<float4*>(st);
         float4* lo = reinterpret_cast<float4*>(st + C::A_BYTES);
 #pragma unroll
@@ -1020,10 +1005,7 @@ __global__ void __launch_bounds__(umma_cfg<BN, FUSE>::THREADS, 1)
         }
         ptx::fence_proxy_async();
         __syncwarp();
-        if (lane == 0) {
-          ptx::mbar_arrive(&xempty[sx]);
-          ptx::mbar_arrive(&aready[s]);
-        }
+        if (lane == 0) ptx::mbar_arrive(&aready[s]);
       }
     }
     ptx::mbar_wait_sleep(accfull, 0);

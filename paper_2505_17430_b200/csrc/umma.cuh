@@ -10,13 +10,13 @@
 // eval_gemm.cu); other widths run the split pre-pass below first.
 //
 // CTA (10 warps, one 128 x 64 output tile):
-//   warp 0  TMA producer: per 32-float K-slice, M_hi, M_lo (64 rows) into the A/B ring and X
-//           (128 rows) into its own ring (FUSE), or S_hi, S_lo, M_hi, M_lo into a 4-stage ring
-//           (pre-pass mode); SWIZZLE_128B, 48 KB A/B stages
+//   warp 0  TMA producer: per 32-float K-slice, X (128 rows, into the S_hi slot; FUSE) or
+//           S_hi, S_lo (pre-pass mode), and M_hi, M_lo (64 rows), SWIZZLE_128B, into a 4-stage
+//           mbarrier ring (48 KB per stage)
 //   warp 1  TMEM allocator + single-thread MMA issuer: 4 K-steps x 3 products of
 //           tcgen05.mma.cta_group::1.kind::tf32 (M=128, N=64, K=8) per stage; tcgen05.commit frees
 //           the stage and finally signals the epilogue
-//   warps 2-9 during the mainloop (FUSE): S_hi / S_lo of each X tile into the A/B stage;
+//   warps 2-9 during the mainloop (FUSE): S_hi / S_lo of each X tile, in place in the stage;
 //           epilogue: tcgen05.ld 32x32b, two warps per TMEM lane quarter (each thread = one
 //           output row, half of the 64 columns), transform terms, half-row sums meeting in shared
 //           memory, N-tile partials + last-CTA finalisation (as K1).
