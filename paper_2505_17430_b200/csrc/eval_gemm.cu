@@ -862,7 +862,7 @@ struct umma_cfg {
   static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) < 4 ? (200 * 1024 / STAGE_BYTES) : 4;
   static constexpr int THREADS = 10 * 32;  // producer, MMA issuer, 8 epilogue warps
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // [0,BN): main, [BN,2BN): corrections
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + (3 * STAGES + 1) * 8 + 64;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + (4 * STAGES + 1) * 8 + 64;
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
 };
 
@@ -878,7 +878,8 @@ __global__ void __launch_bounds__(umma_cfg<BN, FUSE>::THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* aready = empty + C::STAGES;  // FUSE: the stage's S_hi / S_lo are formed
-  uint64_t* accfull = aready + C::STAGES;
+  uint64_t* xfull = aready + C::STAGES;   // FUSE: the stage's X tile landed (M on `full`)
+  uint64_t* accfull = xfull + C::STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accfull + 1);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
@@ -900,6 +901,7 @@ __global__ void __launch_bounds__(umma_cfg<BN, FUSE>::THREADS, 1)
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
       ptx::mbar_init(&aready[s], 8);
+      ptx::mbar_init(&xfull[s], 1);
     }
     ptx::mbar_init(accfull, 1);
     ptx::fence_mbar_init();
@@ -923,9 +925,11 @@ __global__ void __launch_bounds__(umma_cfg<BN, FUSE>::THREADS, 1)
         const int s = kb % C::STAGES;
         if (kb >= C::STAGES) ptx::mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
         uint8_t* st = smem + s * C::STAGE_BYTES;
-        if constexpr (FUSE) {  // X into the A_hi slot (converted in place), M_hi / M_lo as usual
-          ptx::mbar_arrive_expect_tx(&full[s], C::A_BYTES + 2 * C::B_BYTES);
-          ptx::tma_load_2d(st, &tmShi, &full[s], kb * C::KB, m0);
+        if constexpr (FUSE) {  // X into the A_hi slot on its own barrier (the split starts as it
+                               // lands), M_hi / M_lo as usual
+          ptx::mbar_arrive_expect_tx(&xfull[s], C::A_BYTES);
+          ptx::tma_load_2d(st, &tmShi, &xfull[s], kb * C::KB, m0);
+          ptx::mbar_arrive_expect_tx(&full[s], 2 * C::B_BYTES);
         } else {
           ptx::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
           ptx::tma_load_2d(st, &tmShi, &full[s], kb * C::KB, m0);
@@ -979,7 +983,7 @@ __global__ void __launch_bounds__(umma_cfg<BN, FUSE>::THREADS, 1)
       // before the arrive.
       for (int kb = 0; kb < KT; ++kb) {
         const int s = kb % C::STAGES;
-        ptx::mbar_wait(&full[s], (kb / C::STAGES) & 1);  // X (and M) landed
+        ptx::mbar_wait(&xfull[s], (kb / C::STAGES) & 1);  // X landed
         uint8_t* st = smem + s * C::STAGE_BYTES;
         const float4* xs = reinterpret_cast<const float4*>(st);  // each thread rewrites its own chunks
         float4* hi = reinterpret_cast<float4*>(st);
@@ -992,8 +996,8 @@ __global__ void __launch_bounds__(umma_cfg<BN, FUSE>::THREADS, 1)
           const float4 o = __ldg(reinterpret_cast<const float4*>(p.shift + size_t(kb) * C::KB + c * 4));
           auto split = [](float xv, float ov, float& hv, float& lv) {
             const float sv = __fsub_rn(xv, ov);
-            hv = __uint_as_float(umma::cvt_rna_tf32(sv));
-            lv = __uint_as_float(umma::cvt_rna_tf32(__fsub_rn(sv, hv)));
+            hv = __uint_as_float(umma::rna_tf32_bits(sv));
+            lv = __uint_as_float(umma::rna_tf32_bits(__fsub_rn(sv, hv)));
           };
           float4 h, l;
           split(x.x, o.x, h.x, l.x);

@@ -35,6 +35,10 @@ __device__ __forceinline__ uint32_t cvt_rna_tf32(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return r;
 }
+// the same rounding on the integer pipe (round half away from zero on the magnitude: add half a
+// TF32 ulp to the bits, clear the 13 dropped bits; inf and NaN keep their class) — two integer
+// ops instead of a conversion, for the in-kernel split where the conversion rate bounds a stage
+__device__ __forceinline__ uint32_t rna_tf32_bits(float x) { return (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u; }
 
 // K-major SWIZZLE_128B shared-memory matrix descriptor (tcgen05 "smem descriptor"):
 // start address >> 4, LBO = 1 (unused for swizzled K-major), SBO = 1024 B (8 rows x 128 B),
