@@ -500,7 +500,8 @@ void host_eval(const evb_problem* probs, int n_prob, evb_scratch s, const void* 
     int n_chunks = 0;
     int64_t c0 = 0;
     // two gate groups: 6 column chunks each unless EVB_H2D_CHUNKS says otherwise (measured 270 vs 274 us)
-    const int max_chunks = rows_a > 0 ? std::min(chunks_env ? want : 6, kMaxGates / 2) : want;
+    // (at most 8 chunks per group: eval_request::kgate_end; two groups fill the 16 gate words)
+    const int max_chunks = std::min(rows_a > 0 ? (chunks_env ? want : 6) : want, 8);
     while (c0 < D) {
       int64_t w;
       if (n_chunks == max_chunks - 1) w = D - c0;
