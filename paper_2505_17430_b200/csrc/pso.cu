@@ -94,18 +94,30 @@ __global__ void pso_gbest_kernel(const T* __restrict__ pf, int P, int* nb) {
   for (int i = threadIdx.x; i < P; i += blockDim.x) nb[i] = best;
 }
 
-// ring of width one (pso/topology.hpp:44-54), offsets -1, 0, +1 in that order
+// ring of width one (pso/topology.hpp:44-54), offsets -1, 0, +1 in that order: each particle's
+// pbest fitness is loaded once; the left / right neighbours' values come from the adjacent lanes
+// (warp shuffles), global loads only at warp edges and where the ring wraps
 template <typename T>
 __global__ void pso_ring_kernel(const T* __restrict__ pf, int P, int* nb) {
   ptx::griddep_wait();  // PDL (launch_pdl): predecessor data first
   ptx::griddep_launch_dependents();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const T f = i < P ? pf[i] : T(0);
+  T fl = __shfl_up_sync(0xffffffffu, f, 1);
+  T fr = __shfl_down_sync(0xffffffffu, f, 1);
   if (i >= P) return;
-  int best = -1;
-  for (int off = -1; off <= 1; ++off) {
-    const int c = ((i + off) % P + P) % P;
-    if (best < 0 || pf[c] < pf[best] || (pf[c] == pf[best] && c < best)) best = c;
+  const int il = i == 0 ? P - 1 : i - 1, ir = i + 1 == P ? 0 : i + 1;
+  if (lane == 0 || il != i - 1) fl = pf[il];
+  if (lane == 31 || ir != i + 1) fr = pf[ir];
+  // lexicographic (fitness, index) minimum over the candidates in the reference's order
+  int best = il;
+  T bf = fl;
+  if (f < bf || (f == bf && i < best)) {
+    best = i;
+    bf = f;
   }
+  if (fr < bf || (fr == bf && ir < best)) best = ir;
   nb[i] = best;
 }
 

@@ -64,6 +64,13 @@ def test_config3_small(dev, topology, nd):
     run(dev, topology, nd, 64, 200, 6)
 
 
+@pytest.mark.parametrize("P", [1, 2, 33, 50])
+def test_ring_small_and_ragged_swarms(dev, P):
+    # ring neighbours from warp shuffles: swarms below / across a warp and not a multiple of 32
+    # (warp edges, the wrap of the ring, lanes past the swarm), against the reference driver
+    run(dev, "lbest_ring", np.float64, P, 12, 4)
+
+
 @pytest.mark.parametrize("topology", ["gbest", "lbest_ring"])
 def test_config3_full_size_fp64(dev, topology):
     # D=1000, pop 1024 (the config's full size) for two generations
