@@ -7,7 +7,8 @@
 // core/population.hpp:70-77 (stable fitness order).
 //
 // Per generation (one stream, no host sync):
-//   1. order     stable (fitness, index) ranks -> the first p_count entries      (ttpb/1, best/1)
+//   1. order     stable (fitness, index) ranks -> the first p_count entries (ttpb/1); best/1:
+//                the (fitness, index) argmin by warp-shuffle trees (de_best_kernel)
 //   2. draws     per-individual scalar draws: adapter (slot, F, CR), donor indices, jrand.
 //                PHILOX: thread per individual, each on its own sub-stream (gen<<32 | i).
 //                WORDS : one thread walks the caller's word list in the reference's exact order
@@ -158,6 +159,48 @@ struct de_dev {
 };
 
 // fitness order (core/population.hpp:70-77): rank = #{j : f_j < f_i or (f_j == f_i and j < i)}
+// best/1 (p_count = 1): order[0] = the first strict minimum, i.e. the lexicographic (fitness,
+// index) minimum — one block, strided scan + warp-shuffle and shared-memory argmin trees (O(P);
+// the rank kernel below is O(P^2) and serves the top-p of current-to-pbest)
+template <typename T>
+__global__ void __launch_bounds__(1024) de_best_kernel(const de_dev<T> d) {
+  ptx::griddep_wait();  // PDL (launch_pdl): predecessor data first
+  ptx::griddep_launch_dependents();
+  __shared__ T sf[32];
+  __shared__ int si[32];
+  auto merge = [](T& f, int& i, T f2, int i2) {  // (f2, i2) precedes (f, i)?
+    if (i2 >= 0 && (i < 0 || f2 < f || (!(f < f2) && !(f2 < f) && i2 < i))) {
+      f = f2;
+      i = i2;
+    }
+  };
+  T bf = T(0);
+  int bi = -1;
+  for (int i = threadIdx.x; i < d.P; i += blockDim.x) merge(bf, bi, d.fit[i], i);
+  for (int off = 16; off > 0; off >>= 1) {
+    const T of = __shfl_xor_sync(0xffffffffu, bf, off);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+    merge(bf, bi, of, oi);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+    sf[w] = bf;
+    si[w] = bi;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    bf = l < nw ? sf[l] : T(0);
+    bi = l < nw ? si[l] : -1;
+    for (int off = 16; off > 0; off >>= 1) {
+      const T of = __shfl_xor_sync(0xffffffffu, bf, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      merge(bf, bi, of, oi);
+    }
+    if (l == 0) d.order[0] = bi;
+  }
+}
+
 template <typename T>
 __global__ void de_order_kernel(const de_dev<T> d) {
   ptx::griddep_wait();  // PDL (launch_pdl): predecessor data first
@@ -822,7 +865,10 @@ void generation_t(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, vo
                   double lb, double ub, evb_rng_s* r, cudaStream_t st) {
   de_dev<T> d = make_dev<T>(e, pop, ldp, fit, lb, ub, r);
   e->gen_P = e->P;
-  if (e->cfg.mutation == EVB_MUT_TTPB1 || e->cfg.mutation == EVB_MUT_BEST1) {
+  if (e->cfg.mutation == EVB_MUT_BEST1) {
+    EVB_CUDA(launch_pdl(de_best_kernel<T>, dim3(1), dim3(1024), 0, st, d));
+    count_launch();
+  } else if (e->cfg.mutation == EVB_MUT_TTPB1) {
     const int th = 256;
     EVB_CUDA(launch_pdl(de_order_kernel<T>, dim3((e->P + th - 1) / th), dim3(th), th * sizeof(T), st, d));
     count_launch();
