@@ -333,6 +333,33 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
   for (int g = 0; g < a.G; ++g) {
     const uint32_t gen = g_first + uint32_t(g);
     double* sTfit = sTfit2 + (g & 1) * P;
+    // best/1: the first strict minimum of the population (the sequential scan's result: index 0
+    // when f[0] is NaN, else the (fitness, index) minimum over the non-NaN entries), by warp 0
+    // with a shuffle tree, once per generation for the whole CTA
+    __shared__ int s_best;
+    if (a.mutation != EVB_MUT_RAND1) {
+      if (threadIdx.x < 32) {
+        double bf = 0.0;
+        int bi = -1;
+        for (int q = int(threadIdx.x); q < P; q += 32) {
+          const double fq = sFit[q];
+          if (!isnan(fq) && (bi < 0 || fq < bf)) {  // strided: q increases, ties keep the lower
+            bf = fq;
+            bi = q;
+          }
+        }
+        for (int off = 16; off > 0; off >>= 1) {
+          const double of = __shfl_xor_sync(0xffffffffu, bf, off);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+          if (oi >= 0 && (bi < 0 || of < bf || (of == bf && oi < bi))) {
+            bf = of;
+            bi = oi;
+          }
+        }
+        if (threadIdx.x == 0) s_best = (isnan(sFit[0]) || bi < 0) ? 0 : bi;
+      }
+      __syncthreads();
+    }
     // draws (thread per individual of this CTA's half)
     for (int i = p0 + int(threadIdx.x); i < p1; i += blockDim.x) {
       philox_prefetch_reader<4> r(key, (uint64_t(gen) << 32) | uint32_t(i));
@@ -341,11 +368,8 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
         do { x1 = draw_int(r, P); } while (x1 == i);
         do { x2 = draw_int(r, P); } while (x2 == i || x2 == x1);
         do { x3 = draw_int(r, P); } while (x3 == i || x3 == x1 || x3 == x2);
-      } else {  // best/1: best = first strict minimum (fitness_order[0])
-        int best = 0;
-        for (int q = 1; q < P; ++q)
-          if (sFit[q] < sFit[best]) best = q;
-        x1 = best;
+      } else {  // best/1: best = first strict minimum (fitness_order[0]), s_best above
+        x1 = s_best;
         do { x2 = draw_int(r, P); } while (x2 == i);
         do { x3 = draw_int(r, P); } while (x3 == i || x3 == x2);
       }

@@ -90,6 +90,33 @@ def test_config0_shape_persistent_matches_reference(dev, n_runs):
         assert rel[same].max() <= 1e-12, r
 
 
+def test_best1_runs_match_reference(dev):
+    # best/1 in the persistent kernel: the generation's best comes from a warp-shuffle argmin
+    # (first strict minimum); the reference engine replays each run's Philox words.  Few
+    # generations: one libm-vs-CUDA cos ulp that changes the best member redirects every donor of
+    # every later generation (no flagged-row tolerance can absorb that cascade)
+    from paper_2505_17430_b200.de import DEConfig
+    P0, D0, gens, n_runs = 100, 10, 20, 2
+    cfg = DEConfig("best_1", "binomial", "clip", "fixed", f=0.5, cr=0.9)
+    o, m = O.shift_rotation(42, D0)
+    m = m * 0.0512
+    probs = [evb.ProblemInstance.base(evb.BaseKind.rastrigin, o, m, 0.0) for _ in range(n_runs)]
+    keys = run_keys(7, n_runs)
+    pops = torch.empty((n_runs, P0, D0), dtype=torch.float64, device=dev)
+    fits = torch.empty((n_runs, P0), dtype=torch.float64, device=dev)
+    de_runs(cfg, probs, keys, pops, fits, gens, -100.0, 100.0, init=True, gen0=0)
+    torch.cuda.synchronize()
+    gp = pops.cpu().numpy()
+    for r in range(n_runs):
+        ref = O.RefDE(cfg, P0, D0)
+        ref.set_problem_base(5, o, m, 0.0)
+        assert ref.init(O.philox_words(int(keys[r]), 0xFFFFFFF0, 0, P0 * D0), -100.0, 100.0) == P0 * D0
+        for g in range(1, gens + 1):
+            assert ref.generation(O.de_fixed_generation_words(1, int(keys[r]), g, P0, D0), -100.0, 100.0)
+        same = np.all(gp[r] == ref.get()["pop"], axis=1)
+        assert same.all(), (r, int((~same).sum()))
+
+
 def test_runs_continue_equals_single_launch(dev):
     # init + 10 generations in one launch == init + 4 then 6 more (gen ids continue)
     probs, _ = make_runs(3)
