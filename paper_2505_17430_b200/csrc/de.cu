@@ -215,11 +215,15 @@ __global__ void de_order_kernel(const de_dev<T> d) {
     sf[threadIdx.x] = j < d.P ? d.fit[j] : T(0);
     __syncthreads();
     const int n = min(int(blockDim.x), d.P - base);
+    // (fitness, index) order with NaN after every number (a strict weak order, so the ranks are
+    // a permutation and every order slot is written; NaN-free populations: the reference's
+    // stable sort by fitness)
+    auto less = [](T a, T b) { return a < b || (!isnan(a) && isnan(b)); };
     if (i < d.P)
       for (int q = 0; q < n; ++q) {
         const T fj = sf[q];
         const int jj = base + q;
-        rank += (fj < fi || (!(fi < fj) && !(fj < fi) && jj < i)) ? 1 : 0;
+        rank += (less(fj, fi) || (!less(fi, fj) && !less(fj, fi) && jj < i)) ? 1 : 0;
       }
     __syncthreads();
   }
