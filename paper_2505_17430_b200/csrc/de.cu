@@ -168,8 +168,10 @@ __global__ void __launch_bounds__(1024) de_best_kernel(const de_dev<T> d) {
   ptx::griddep_launch_dependents();
   __shared__ T sf[32];
   __shared__ int si[32];
-  auto merge = [](T& f, int& i, T f2, int i2) {  // (f2, i2) precedes (f, i)?
-    if (i2 >= 0 && (i < 0 || f2 < f || (!(f < f2) && !(f2 < f) && i2 < i))) {
+  // (f2, i2) precedes (f, i)?  The order kernel's (fitness, index) order, NaN after every number
+  auto less = [](T a, T b) { return a < b || (!isnan(a) && isnan(b)); };
+  auto merge = [&](T& f, int& i, T f2, int i2) {
+    if (i2 >= 0 && (i < 0 || less(f2, f) || (!less(f, f2) && i2 < i))) {
       f = f2;
       i = i2;
     }
