@@ -198,11 +198,16 @@ __global__ void __launch_bounds__(128) pso_update_vec_kernel(const pso_dev<T> d)
   const T* pr = d.pb + size_t(i) * d.ldb;
   const T* lr = d.pb + size_t(d.nb[i]) * d.ldb;
   T x[VEC], v[VEC], pb[VEC], lb_[VEC];
+  constexpr int NV = VEC * int(sizeof(T)) / 16;  // 16-byte vectors per array
   if (j0 + VEC <= d.D) {
-    *reinterpret_cast<V*>(x) = *reinterpret_cast<const V*>(xr + j0);
-    *reinterpret_cast<V*>(v) = *reinterpret_cast<const V*>(vr + j0);
-    *reinterpret_cast<V*>(pb) = __ldg(reinterpret_cast<const V*>(pr + j0));
-    *reinterpret_cast<V*>(lb_) = __ldg(reinterpret_cast<const V*>(lr + j0));
+#pragma unroll
+    for (int u = 0; u < NV; ++u) {
+      const int e = u * (16 / int(sizeof(T)));
+      *reinterpret_cast<V*>(x + e) = *reinterpret_cast<const V*>(xr + j0 + e);
+      *reinterpret_cast<V*>(v + e) = *reinterpret_cast<const V*>(vr + j0 + e);
+      *reinterpret_cast<V*>(pb + e) = __ldg(reinterpret_cast<const V*>(pr + j0 + e));
+      *reinterpret_cast<V*>(lb_ + e) = __ldg(reinterpret_cast<const V*>(lr + j0 + e));
+    }
   } else {
 #pragma unroll
     for (int q = 0; q < VEC; ++q) {
@@ -244,8 +249,12 @@ __global__ void __launch_bounds__(128) pso_update_vec_kernel(const pso_dev<T> d)
     v[q] = vv;
   }
   if (j0 + VEC <= d.D) {
-    *reinterpret_cast<V*>(xr + j0) = *reinterpret_cast<const V*>(x);
-    *reinterpret_cast<V*>(vr + j0) = *reinterpret_cast<const V*>(v);
+#pragma unroll
+    for (int u = 0; u < NV; ++u) {
+      const int e = u * (16 / int(sizeof(T)));
+      *reinterpret_cast<V*>(xr + j0 + e) = *reinterpret_cast<const V*>(x + e);
+      *reinterpret_cast<V*>(vr + j0 + e) = *reinterpret_cast<const V*>(v + e);
+    }
   } else {
 #pragma unroll
     for (int q = 0; q < VEC; ++q)
@@ -426,7 +435,9 @@ void generation_t(evb_pso_s* s, const device_problem* prob, evb_scratch_s* sc, v
     pso_spherical_kernel<T><<<s->P, threads, smem, st>>>(d);
     words_per_particle += 1;
   } else {
-    constexpr int VEC = sizeof(T) == 8 ? 2 : 4;
+    // four doubles / eight floats per thread: two 16-byte vectors per array and four or eight
+    // independent Philox chains in flight (measured 120 -> 115 us at P = 16384, D = 1000)
+    constexpr int VEC = sizeof(T) == 8 ? 4 : 8;
     const bool aligned = reinterpret_cast<uintptr_t>(X) % 16 == 0 && reinterpret_cast<uintptr_t>(V) % 16 == 0 &&
                          (ldx * sizeof(T)) % 16 == 0 && (ldv * sizeof(T)) % 16 == 0 &&
                          (s->ldb * sizeof(T)) % 16 == 0;
