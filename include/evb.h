@@ -108,6 +108,11 @@ EVB_API int evb_problem_dtype(evb_problem p);
 
 EVB_API int evb_scratch_create(evb_scratch* out);
 EVB_API int evb_scratch_destroy(evb_scratch s);
+/* Page-locked host staging owned by the scratch (grown on demand, freed with it): the C++
+ * wrapper flattens a std::vector<std::vector<T>> batch into it so evb_evaluate_batch_host runs
+ * at full host-link bandwidth and writes the fitness values into it directly.  Replaces the
+ * per-call heap flatten of problems::evaluate_batch's AoS input (problems/batch.hpp:243-247). */
+EVB_API int evb_scratch_host_staging(evb_scratch s, size_t bytes, void** out);
 
 /* ---- batched evaluation (problems/batch.hpp:243-278) ------------------------------- */
 

@@ -16,10 +16,14 @@
 //                                  runner.hpp:101      (all tasks of a suite; DE presets in one launch)
 //
 // Errors are rethrown as the reference's types: std::invalid_argument (dimension mismatch),
-// evb::config_error (a std::runtime_error, like evobench::config_error, common.hpp:12-15),
-// std::logic_error, std::runtime_error.  No CUDA header is needed by users of this file.
+// evb::config_error, std::logic_error, std::runtime_error.  evb::config_error IS
+// evobench::config_error (common.hpp:12-15) when the evobench headers are in the build
+// (EVB_WITH_EVOBENCH, set by evb/evobench_adapter.hpp), so a reference caller's
+// `catch (const evobench::config_error&)` sees GPU configuration errors; otherwise it is a
+// std::runtime_error of the same shape.  No CUDA header is needed by users of this file.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -30,12 +34,21 @@
 
 #include "evb.h"
 
+#ifdef EVB_WITH_EVOBENCH
+#include "evobench/common.hpp"
 namespace evb {
-
+using config_error = ::evobench::config_error;
+}  // namespace evb
+#else
+namespace evb {
 class config_error : public std::runtime_error {
  public:
   explicit config_error(const std::string& what) : std::runtime_error(what) {}
 };
+}  // namespace evb
+#endif
+
+namespace evb {
 
 inline void check(int status, const char* what) {
   if (status == EVB_OK) return;
@@ -113,6 +126,12 @@ class gpu_scratch {
     if (h_) evb_scratch_destroy(h_);
   }
   evb_scratch handle() const { return h_; }
+  // page-locked staging owned by the scratch (reused across calls, grown on demand)
+  void* host_staging(size_t bytes) {
+    void* p = nullptr;
+    check(evb_scratch_host_staging(h_, bytes, &p), "scratch_host_staging");
+    return p;
+  }
 
  private:
   evb_scratch h_ = nullptr;
@@ -172,6 +191,9 @@ class gpu_problem {
 
 // problems::evaluate_batch(problem, xs, scratch, out) (problems/batch.hpp:243-278): host points in,
 // host values out; throws std::invalid_argument on a dimension mismatch, like the reference.
+// The rows are flattened into the scratch's page-locked staging (reused across calls), so the
+// batch crosses the host link at full bandwidth and the kernel writes the values straight into
+// the staging's tail.
 template <typename T>
 void evaluate_batch(const gpu_problem<T>& problem, const std::vector<std::vector<T>>& xs, gpu_scratch& scratch,
                     std::vector<T>& out) {
@@ -180,11 +202,14 @@ void evaluate_batch(const gpu_problem<T>& problem, const std::vector<std::vector
   const int d = problem.dim();
   for (const auto& x : xs)
     if (int(x.size()) != d) throw std::invalid_argument("evaluate_batch: point dimension mismatch");
-  std::vector<T> flat(xs.size() * size_t(d));
-  for (size_t b = 0; b < xs.size(); ++b) std::memcpy(flat.data() + b * d, xs[b].data(), sizeof(T) * d);
-  out.resize(xs.size());
-  check(evb_evaluate_batch_host(problem.handle(), scratch.handle(), flat.data(), int64_t(xs.size()), d, out.data()),
-        "evaluate_batch");
+  const size_t n = xs.size();
+  const size_t x_bytes = (n * size_t(d) * sizeof(T) + 255) / 256 * 256;
+  uint8_t* stage = static_cast<uint8_t*>(scratch.host_staging(x_bytes + n * sizeof(T)));
+  T* flat = reinterpret_cast<T*>(stage);
+  T* vals = reinterpret_cast<T*>(stage + x_bytes);
+  for (size_t b = 0; b < n; ++b) std::memcpy(flat + b * d, xs[b].data(), sizeof(T) * d);
+  check(evb_evaluate_batch_host(problem.handle(), scratch.handle(), flat, int64_t(n), d, vals), "evaluate_batch");
+  out.assign(vals, vals + n);
 }
 
 // problems::batched_evaluate(problem, xs) (problems/batch.hpp:281-288)
@@ -265,6 +290,8 @@ class gpu_de_engine {
     check(evb_de_create(dtype_of<T>(), &cfg, pop_size, dim, &h_), "de_create");
   }
   gpu_de_engine(const gpu_de_engine&) = delete;
+  gpu_de_engine& operator=(const gpu_de_engine&) = delete;
+  gpu_de_engine(gpu_de_engine&& o) noexcept : h_(std::exchange(o.h_, nullptr)), P_(o.P_), D_(o.D_) {}
   ~gpu_de_engine() {
     if (h_) evb_de_destroy(h_);
   }
@@ -290,6 +317,26 @@ class gpu_de_engine {
     return bi;
   }
   int archive_capacity() const { return evb_de_archive_capacity(h_); }
+  int pop_size() const { return P_; }
+  int dim() const { return D_; }
+  // adaptation + archive state (SHADE memories / JADE means in memory_f[0], memory_cr[0])
+  void set_state(const std::vector<T>& archive_rows, int archive_size, const std::vector<T>& memory_f,
+                 const std::vector<T>& memory_cr, int write_index) {
+    check(evb_de_set_state(h_, archive_rows.empty() ? nullptr : archive_rows.data(), archive_size,
+                           memory_f.empty() ? nullptr : memory_f.data(), memory_cr.empty() ? nullptr : memory_cr.data(),
+                           write_index),
+          "de_set_state");
+  }
+  void get_state(std::vector<T>& archive_rows, int& archive_size, std::vector<T>& memory_f, std::vector<T>& memory_cr,
+                 int& write_index, int memory_size) const {
+    archive_rows.assign(size_t(std::max(1, archive_capacity())) * D_, T(0));
+    memory_f.assign(size_t(std::max(1, memory_size)), T(0));
+    memory_cr.assign(size_t(std::max(1, memory_size)), T(0));
+    check(evb_de_get_state(h_, archive_rows.data(), &archive_size, memory_f.data(), memory_cr.data(), &write_index),
+          "de_get_state");
+    archive_rows.resize(size_t(archive_size) * D_);
+  }
+  evb_de handle() const { return h_; }
 
  private:
   evb_de h_ = nullptr;
@@ -304,6 +351,8 @@ class gpu_pso_engine {
     check(evb_pso_create(dtype_of<T>(), &cfg, pop_size, dim, &h_), "pso_create");
   }
   gpu_pso_engine(const gpu_pso_engine&) = delete;
+  gpu_pso_engine& operator=(const gpu_pso_engine&) = delete;
+  gpu_pso_engine(gpu_pso_engine&& o) noexcept : h_(std::exchange(o.h_, nullptr)) {}
   ~gpu_pso_engine() {
     if (h_) evb_pso_destroy(h_);
   }
@@ -316,6 +365,11 @@ class gpu_pso_engine {
                              rng.handle(), stream),
           "pso_generation");
   }
+  // personal bests from the host (pop_size x dim row-major + fitness); marks the engine prepared
+  void set_personal_bests(const std::vector<T>& pbest_rows, const std::vector<T>& pbest_fitness) {
+    check(evb_pso_set_pbest(h_, pbest_rows.data(), pbest_fitness.data()), "pso_set_pbest");
+  }
+  evb_pso handle() const { return h_; }
 
  private:
   evb_pso h_ = nullptr;

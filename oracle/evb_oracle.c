@@ -575,13 +575,17 @@ static double orc_sample_cr(orc_rng* r, double mu) {
   return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
 }
 
-/* core/population.hpp:70-77 stable ascending order (insertion sort keeps it stable) */
+/* core/population.hpp:70-77 stable ascending order (insertion sort keeps it stable).  NaN ranks
+ * after every number: the reference's stable_sort with `<` has no strict weak order once a NaN is
+ * present (its result then depends on the sort's internals); the GPU kernels and this checker
+ * share the NaN-last order, which equals the reference's on NaN-free populations. */
+static int orc_less_nan_last(double a, double b) { return a < b || (!isnan(a) && isnan(b)); }
 static void orc_fitness_order(const double* fit, int P, int* order) {
   for (int i = 0; i < P; ++i) order[i] = i;
   for (int i = 1; i < P; ++i) {
     const int v = order[i];
     int j = i - 1;
-    while (j >= 0 && fit[v] < fit[order[j]]) {
+    while (j >= 0 && orc_less_nan_last(fit[v], fit[order[j]])) {
       order[j + 1] = order[j];
       --j;
     }

@@ -444,6 +444,10 @@ class RefPSO:
         w = np.ascontiguousarray(words, np.uint64)
         return bool(REF().ref_pso_step(self.dt, self.h, ptr(w), len(w), lb, ub))
 
+    def set_threads(self, n: int) -> None:
+        """Evaluate the swarm on n host threads (contiguous slices, one eval_scratch each)."""
+        REF().ref_pso_set_threads(self.dt, self.h, int(n))
+
     def get(self):
         P, D = self.P, self.D
         out = {k: np.zeros((P, D), self.nd) for k in ("x", "v", "pbest")}

@@ -321,6 +321,23 @@ int evb_scratch_create(evb_scratch* out) {
   });
 }
 
+int evb_scratch_host_staging(evb_scratch s, size_t bytes, void** out) {
+  return guarded([&] {
+    require(s != nullptr && out != nullptr, "scratch_host_staging: null argument");
+    if (bytes > s->host_stage_bytes) {
+      if (s->host_stage) {
+        if (s->own_stream) EVB_CUDA(cudaStreamSynchronize(s->own_stream));
+        EVB_CUDA(cudaFreeHost(s->host_stage));
+        s->host_stage = nullptr;
+        s->host_stage_bytes = 0;
+      }
+      EVB_CUDA(cudaHostAlloc(&s->host_stage, bytes, cudaHostAllocPortable | cudaHostAllocMapped));
+      s->host_stage_bytes = bytes;
+    }
+    *out = s->host_stage;
+  });
+}
+
 int evb_scratch_destroy(evb_scratch s) {
   return guarded([&] {
     if (!s) return;
@@ -331,6 +348,7 @@ int evb_scratch_destroy(evb_scratch s) {
     if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
     if (s->gate_stream) cudaStreamDestroy(s->gate_stream);
     if (s->ev_x_ready) cudaEventDestroy(s->ev_x_ready);
+    if (s->host_stage) cudaFreeHost(s->host_stage);
     for (auto e : s->ev_chunk)
       if (e) cudaEventDestroy(e);
     delete s;

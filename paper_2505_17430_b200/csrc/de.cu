@@ -947,27 +947,71 @@ void generation_t(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, vo
 // reduce_population removes the worst member (fitness >=, so ties remove the higher index) until
 // the scheduled size: the survivors are exactly the members of (fitness, index) rank < target,
 // kept in their order (erase_member).
+// reduce_population (de/policy.hpp:44-60): while size > target, remove `worst` from the
+// sequential scan worst = 0; for i: if f[i] >= f[worst] worst = i, over the current members.
+// Closed form of one scan: the head when its fitness is NaN (nothing compares >= NaN), else the
+// last index of the maximum over the non-NaN members (a NaN member never satisfies >=).  One
+// block repeats that reduction once per removal; rank[i] = 0 marks a survivor, `target` a
+// removed member (the gather kernel keeps rank < target).  NaN-free populations: exactly the
+// members of (fitness, index) rank >= target.
 template <typename T>
-__global__ void de_reduce_rank_kernel(const T* fit, int P, int* rank) {
+__global__ void __launch_bounds__(1024) de_reduce_mark_kernel(const T* fit, int P, int target, int* rank) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   T* sf = reinterpret_cast<T*>(smem_raw);
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const T fi = i < P ? fit[i] : T(0);
-  int rk = 0;
-  for (int base = 0; base < P; base += blockDim.x) {
-    const int j = base + threadIdx.x;
-    sf[threadIdx.x] = j < P ? fit[j] : T(0);
+  uint8_t* alive = smem_raw + sizeof(T) * size_t(P);
+  __shared__ T wf[32];
+  __shared__ int wi[32], wh[32];
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    sf[i] = fit[i];
+    alive[i] = 1;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  // (f2, i2) replaces (f, i) as the scan's worst: larger fitness, or equal fitness at a later index
+  auto merge = [](T& f, int& i, T f2, int i2) {
+    if (i2 >= 0 && (i < 0 || f2 > f || (f2 == f && i2 > i))) {
+      f = f2;
+      i = i2;
+    }
+  };
+  for (int r = target; r < P; ++r) {
+    T bf = T(0);
+    int bi = -1, head = P;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+      if (!alive[i]) continue;
+      head = min(head, i);
+      if (!isnan(sf[i])) merge(bf, bi, sf[i], i);
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      const T of = __shfl_xor_sync(0xffffffffu, bf, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      head = min(head, __shfl_xor_sync(0xffffffffu, head, off));
+      merge(bf, bi, of, oi);
+    }
+    if (lane == 0) {
+      wf[w] = bf;
+      wi[w] = bi;
+      wh[w] = head;
+    }
     __syncthreads();
-    const int n = min(int(blockDim.x), P - base);
-    if (i < P)
-      for (int q = 0; q < n; ++q) {
-        const T fj = sf[q];
-        const int jj = base + q;
-        rk += (fj < fi || (!(fi < fj) && !(fj < fi) && jj < i)) ? 1 : 0;
+    if (w == 0) {
+      bf = lane < nw ? wf[lane] : T(0);
+      bi = lane < nw ? wi[lane] : -1;
+      head = lane < nw ? wh[lane] : P;
+      for (int off = 16; off > 0; off >>= 1) {
+        const T of = __shfl_xor_sync(0xffffffffu, bf, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        head = min(head, __shfl_xor_sync(0xffffffffu, head, off));
+        merge(bf, bi, of, oi);
       }
+      if (lane == 0) {
+        const int worst = (isnan(sf[head]) || bi < 0) ? head : bi;
+        alive[worst] = 0;
+      }
+    }
     __syncthreads();
   }
-  if (i < P) rank[i] = rk;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) rank[i] = alive[i] ? 0 : target;
 }
 
 // block i: survivor i moves to position #{j < i : survivor} of the staging rows
@@ -1045,8 +1089,11 @@ void reduce_t(evb_de_s* e, void* pop, int64_t ldp, void* fit, evb_rng_s* r, cuda
   const int target = std::clamp(int(std::lround(e->P_alloc + (e->n_min - e->P_alloc) * frac)), e->n_min, e->P_alloc);
   if (target >= e->P) return;  // policy.hpp:49: no-op when the schedule allows the current size
   const int P = e->P, D = e->D;
-  const int th = 256;
-  de_reduce_rank_kernel<T><<<(P + th - 1) / th, th, th * sizeof(T), st>>>(static_cast<const T*>(fit), P, e->rank);
+  const size_t mark_smem = (sizeof(T) + 1) * size_t(P);
+  require(mark_smem <= 200 * 1024, "L-SHADE reduction: population too large for the one-block removal scan");
+  if (mark_smem > 48 * 1024)
+    EVB_CUDA(cudaFuncSetAttribute(de_reduce_mark_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(mark_smem)));
+  de_reduce_mark_kernel<T><<<1, 1024, mark_smem, st>>>(static_cast<const T*>(fit), P, target, e->rank);
   de_reduce_gather_kernel<T><<<P, 128, 0, st>>>(static_cast<const T*>(pop), ldp, static_cast<const T*>(fit), P, D,
                                                  e->rank, target, static_cast<T*>(e->trial), e->ldt,
                                                  static_cast<T*>(e->trial_fit));

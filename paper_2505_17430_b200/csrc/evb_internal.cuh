@@ -166,6 +166,9 @@ struct evb_scratch_s {
   unsigned gate_epoch = 0;
   cudaEvent_t ev_x_ready = nullptr;
   cudaEvent_t ev_chunk[16] = {};
+  // page-locked host staging for the C++ wrapper's vector<vector<T>> batches
+  void* host_stage = nullptr;
+  size_t host_stage_bytes = 0;
 };
 
 namespace evb {

@@ -56,8 +56,11 @@ __device__ __forceinline__ void argmin_merge(T& f, int& i, T f2, int i2) {
   }
 }
 
-// gbest: one block reduces all pbests (pso/topology.hpp:28-34 semantics: index of the first
-// strict minimum == lexicographic (f, i) minimum); writes nb[i] = best for all i.
+// gbest: one block reduces all pbests; writes nb[i] = best for all i.  pso/topology.hpp:28-34 is
+// the sequential scan best = 0; for i: if f[i] < f[best] best = i.  Its closed form: index 0 when
+// f[0] is NaN (nothing compares < NaN), else the lexicographic (f, i) minimum over the non-NaN
+// entries (a NaN never satisfies <).  NaN entries therefore stay out of the shuffle tree, which
+// keeps the merge a strict weak order (independent of the tree's shape).
 template <typename T>
 __global__ void pso_gbest_kernel(const T* __restrict__ pf, int P, int* nb) {
   ptx::griddep_wait();  // PDL (launch_pdl): predecessor data first
@@ -66,7 +69,10 @@ __global__ void pso_gbest_kernel(const T* __restrict__ pf, int P, int* nb) {
   __shared__ int si[32];
   T bf = T(0);
   int bi = -1;
-  for (int i = threadIdx.x; i < P; i += blockDim.x) argmin_merge(bf, bi, pf[i], i);
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    const T fi = pf[i];
+    if (!isnan(fi)) argmin_merge(bf, bi, fi, i);
+  }
   for (int off = 16; off > 0; off >>= 1) {
     const T of = __shfl_xor_sync(0xffffffffu, bf, off);
     const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
@@ -87,7 +93,7 @@ __global__ void pso_gbest_kernel(const T* __restrict__ pf, int P, int* nb) {
       const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
       if (oi >= 0) argmin_merge(bf, bi, of, oi);
     }
-    if (l == 0) si[0] = bi;
+    if (l == 0) si[0] = (bi < 0 || isnan(pf[0])) ? 0 : bi;
   }
   __syncthreads();
   const int best = si[0];
@@ -197,7 +203,11 @@ __global__ void __launch_bounds__(128) pso_update_vec_kernel(const pso_dev<T> d)
   T* vr = d.v + size_t(i) * d.ldv;
   const T* pr = d.pb + size_t(i) * d.ldb;
   const T* lr = d.pb + size_t(d.nb[i]) * d.ldb;
-  T x[VEC], v[VEC], pb[VEC], lb_[VEC];
+  // 16-byte aligned so the vector views below stay legal even if the arrays spill to local memory
+  alignas(16) T x[VEC];
+  alignas(16) T v[VEC];
+  alignas(16) T pb[VEC];
+  alignas(16) T lb_[VEC];
   constexpr int NV = VEC * int(sizeof(T)) / 16;  // 16-byte vectors per array
   if (j0 + VEC <= d.D) {
 #pragma unroll

@@ -333,9 +333,10 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
   for (int g = 0; g < a.G; ++g) {
     const uint32_t gen = g_first + uint32_t(g);
     double* sTfit = sTfit2 + (g & 1) * P;
-    // best/1: the first strict minimum of the population (the sequential scan's result: index 0
-    // when f[0] is NaN, else the (fitness, index) minimum over the non-NaN entries), by warp 0
-    // with a shuffle tree, once per generation for the whole CTA
+    // best/1: fitness_order()[0] (core/population.hpp:70-77) under the engine's order kernel's
+    // (fitness, index) order with NaN after every number (de_best_kernel, de.cu): the (fitness,
+    // index) minimum over the non-NaN entries, index 0 when every entry is NaN; by warp 0 with a
+    // shuffle tree, once per generation for the whole CTA
     __shared__ int s_best;
     if (a.mutation != EVB_MUT_RAND1) {
       if (threadIdx.x < 32) {
@@ -356,7 +357,7 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
             bi = oi;
           }
         }
-        if (threadIdx.x == 0) s_best = (isnan(sFit[0]) || bi < 0) ? 0 : bi;
+        if (threadIdx.x == 0) s_best = bi < 0 ? 0 : bi;
       }
       __syncthreads();
     }

@@ -126,10 +126,12 @@ def test_device_philox_matches_restatement():
         assert np.array_equal(philox_words(key, hi, 5, 257), O.philox_words(key, hi, 5, 257))
 
 
-@pytest.mark.parametrize("P,D,G", [(180, 100, 40), (1100, 20, 6)])
+@pytest.mark.parametrize("P,D,G", [(180, 100, 1000), (1100, 20, 6)])
 def test_config2_shade_lockstep(dev, P, D, G):
-    # config 2 shape, and a population above one select-scan pass (1024: successes staged apart
-    # from the flags, SHADE memory sums over several chunks)
+    # BASELINE config 2 for its stated 1000 generations, and a population above one select-scan
+    # pass (1024: successes staged apart from the flags, SHADE memory sums over several chunks).
+    # A row may differ only when it is flagged: its F / CR differ by a libm-vs-CUDA ulp, or its
+    # selection (f_trial <= f_parent) is a near-tie within 1e-10 relative (Ackley's exp / cos).
     key = 11
     o, m = O.shift_rotation(11, D)
     cfg = preset_shade(0.11, P, 1.0)
@@ -145,7 +147,7 @@ def test_config2_shade_lockstep(dev, P, D, G):
     ref.set_pop(pop.cpu().numpy(), fit.cpu().numpy())
     orc = O.OracleDE(cfg, P, D)
     orc.set_problem_base(6, o, m, 0.0)
-    flagged = 0
+    flagged = near_ties = 0
     exact_gens = 0
     for g in range(G):
         st0 = ref.get()
@@ -175,17 +177,33 @@ def test_config2_shade_lockstep(dev, P, D, G):
         if same.all():
             exact_gens += 1
             assert np.array_equal(eng.get_state()["archive"], st["archive"]), g
+        # rows that differ must come from an F/CR ulp difference or a near-tie selection
+        gpu_fit = fit.cpu().numpy()
+        rel = np.abs(gpu_fit - st["fit"]) / np.maximum(1.0, np.abs(st["fit"]))
+        diff_rows = np.where(~same)[0]
+        tie = np.zeros(P, bool)
+        for i in diff_rows:
+            ulp = dr["F"][i] != out["F"][i] or dr["CR"][i] != out["CR"][i]
+            fp = st0["fit"][i]
+            took_gpu, took_ref = gpu_fit[i] != fp or not np.array_equal(gpu_pop[i], st0["pop"][i]), \
+                st["fit"][i] != fp or not np.array_equal(st["pop"][i], st0["pop"][i])
+            if not ulp:  # a selection decided differently: the trial's fitness ties the parent's
+                assert took_gpu != took_ref, (g, i)
+                ft = gpu_fit[i] if took_gpu else st["fit"][i]
+                assert abs(ft - fp) <= 1e-10 * max(1.0, abs(fp)), (g, i)
+                near_ties += 1
+                tie[i] = True
+        assert np.max(np.abs(gpu_pop[~tie] - st["pop"][~tie])) <= 1e-9
+        assert rel[same].max() <= 1e-10, g
         # the SHADE memory update (sequential success sums) on the GPU's own F / CR: equal up to
-        # the F / CR ulps above
+        # the F / CR ulps above (a flagged near-tie changes the success set: not compared then)
         gst = eng.get_state()
         assert gst["write_index"] == st["write_index"], g
-        assert np.max(np.abs(gst["memory_f"] - st["memory_f"])) <= 1e-12, g
-        assert np.max(np.abs(gst["memory_cr"] - st["memory_cr"])) <= 1e-12, g
-        # rows that differ must come from an F/CR ulp difference
-        diff_rows = np.where(~same)[0]
-        for i in diff_rows:
-            assert dr["F"][i] != out["F"][i] or dr["CR"][i] != out["CR"][i], (g, i)
-        assert np.max(np.abs(gpu_pop - st["pop"])) <= 1e-9
+        if not tie.any():
+            assert np.max(np.abs(gst["memory_f"] - st["memory_f"])) <= 1e-12, g
+            assert np.max(np.abs(gst["memory_cr"] - st["memory_cr"])) <= 1e-12, g
+    print(f"config 2 lockstep P={P} D={D}: {G} generations, {exact_gens} bit-exact, {flagged} flagged rows "
+          f"({near_ties} near-tie selections)")
     # (at P = 1100 nearly every generation has some row with an F / CR ulp difference)
     assert exact_gens >= (G // 2 if P <= 256 else 0), (exact_gens, flagged)
 
@@ -287,6 +305,171 @@ def test_exponential_reinitialize_philox_replay(dev, cfg):
             pop.copy_(torch.from_numpy(st["pop"]))
             fit.copy_(torch.from_numpy(st["fit"]))
             eng.set_state(st["archive"], st["memory_f"], st["memory_cr"], st["write_index"])
+
+
+JADE_REFLECT = [
+    DEConfig("rand_1", "binomial", "reflect", "fixed", f=0.9, cr=0.9),
+    DEConfig("best_1", "exponential", "reflect", "fixed", f=0.8, cr=0.5),
+    DEConfig("ttpb_1", "binomial", "clip", "jade", p_best=0.05, use_archive=True, jade_c=0.1, archive_rate=1.0),
+    DEConfig("ttpb_1", "binomial", "reflect", "jade", p_best=0.1, use_archive=False, jade_c=0.2, archive_rate=0.0),
+    DEConfig("rand_1", "exponential", "reflect", "jade", jade_c=0.5),
+]
+
+
+@pytest.mark.parametrize("cfg", JADE_REFLECT, ids=lambda c: f"{c.mutation}-{c.crossover}-{c.repair}-{c.parameter}")
+def test_jade_reflect_philox_lockstep(dev, cfg):
+    """JADE (de/parameter.hpp:99-147: F ~ Cauchy(mu_F, 0.1), CR ~ N(mu_CR, 0.1), Lehmer-mean and
+    arithmetic-mean updates with learning rate c) and reflect repair (de/strategy.hpp:243-259:
+    lb + (lb - v) / ub - (v - ub), then clip).  The unmodified reference engine replays the GPU's
+    exported Philox words generation after generation and must consume exactly that many; the C
+    restatement on the same words gives the integer draws (donor indices, jrand, word counts:
+    exact) and F / CR (tan / log / cos: within 4e-16).  Fixed-parameter configurations are
+    bit-exact free running; JADE re-syncs the GPU to the reference each generation (lockstep) and
+    allows a row to differ only where its F / CR differ by an ulp, or at a near-tie selection."""
+    P, D, G, key = 64, 30, 40, 0x1ADE
+    o, m = O.shift_rotation(19, D)
+    prob = evb.ProblemInstance.base(evb.BaseKind.sphere, o, m, 0.0)
+    eng = DEEngine(cfg, P, D)
+    rng = Rng.philox(key)
+    pop = torch.empty((P, D), dtype=torch.float64, device=dev)
+    eng.init_population(pop, -100.0, 100.0, rng)
+    fit = dev_eval(prob, pop, dev)
+    ref = O.RefDE(cfg, P, D)
+    ref.set_problem_base(0, o, m, 0.0)
+    ref.set_pop(pop.cpu().numpy(), fit.cpu().numpy())
+    orc = O.OracleDE(cfg, P, D)
+    orc.set_problem_base(0, o, m, 0.0)
+    jade = cfg.parameter == "jade"
+    reflected = flagged = 0
+    for g in range(G):
+        st0 = ref.get()
+        if jade:  # lockstep: GPU <- reference state (population, archive, mu_F / mu_CR)
+            pop.copy_(torch.from_numpy(st0["pop"]))
+            fit.copy_(torch.from_numpy(st0["fit"]))
+            eng.set_state(st0["archive"], st0["memory_f"][:1], st0["memory_cr"][:1], 0)
+        orc.set_state(st0["pop"], st0["fit"], st0["archive"], st0["archive_size"], st0["memory_f"][:1],
+                      st0["memory_cr"][:1], 0)
+        eng.generation(prob, pop, fit, -100.0, 100.0, rng)
+        dr = eng.last_draws()
+        words = scripted_words_for_generation(key, dr["generation"], dr["word_counts"], dr["archive_words"],
+                                              philox=O.philox_words)
+        assert ref.generation(words, -100.0, 100.0), f"gen {g}: word count mismatch"
+        out = orc.generation(words, -100.0, 100.0)
+        st = ref.get()
+        assert np.array_equal(dr["idx"][:, :3], out["idx"][:, :3]), g
+        assert np.array_equal(dr["jrand"], out["jrand"]), g
+        assert np.array_equal(dr["word_counts"], out["words"]), g
+        assert np.max(np.abs(dr["F"] - out["F"])) <= 4e-16, g
+        assert np.max(np.abs(dr["CR"] - out["CR"])) <= 4e-16, g
+        # reflect is exercised: some donor genes left [lb, ub] (F up to 1 on U[-100, 100] rows)
+        x0 = st0["pop"]
+        if cfg.mutation != "ttpb_1":  # rand/1, best/1: donor = x_a + F (x_b - x_c)
+            donors = x0[dr["idx"][:, 0]] + dr["F"][:, None] * (x0[dr["idx"][:, 1]] - x0[dr["idx"][:, 2]])
+            reflected += int(np.sum(np.abs(donors) > 100.0))
+        gpu_pop, gpu_fit = pop.cpu().numpy(), fit.cpu().numpy()
+        if not jade:
+            assert np.array_equal(gpu_pop, st["pop"]), g
+            assert np.array_equal(gpu_fit, st["fit"]), g
+            continue
+        same = np.all(gpu_pop == st["pop"], axis=1)
+        flagged += int((~same).sum())
+        tie = np.zeros(P, bool)
+        for i in np.where(~same)[0]:
+            if dr["F"][i] != out["F"][i] or dr["CR"][i] != out["CR"][i]:
+                continue
+            fp = st0["fit"][i]
+            ft = gpu_fit[i] if not np.array_equal(gpu_pop[i], st0["pop"][i]) else st["fit"][i]
+            assert abs(ft - fp) <= 1e-10 * max(1.0, abs(fp)), (g, i)
+            tie[i] = True
+        assert np.max(np.abs(gpu_pop[~tie] - st["pop"][~tie])) <= 1e-9, g
+        if not tie.any():  # mu_F (Lehmer mean) and mu_CR after the update
+            gst = eng.get_state()
+            assert abs(gst["memory_f"][0] - st["memory_f"][0]) <= 1e-12, g
+            assert abs(gst["memory_cr"][0] - st["memory_cr"][0]) <= 1e-12, g
+    if cfg.repair == "reflect" and cfg.mutation != "ttpb_1":
+        assert reflected > 0
+    print(f"{cfg.mutation}/{cfg.crossover}/{cfg.repair}/{cfg.parameter}: {G} generations, {reflected} reflected "
+          f"donor genes, {flagged} flagged rows")
+    assert flagged <= P * G // 20
+
+
+def test_lshade_reduction_with_nan(dev):
+    # reduce_population (de/policy.hpp:44-60) with NaN fitness: the reference's `>=` worst scan
+    # removes the head when its fitness is NaN and otherwise the last maximum among the non-NaN
+    # members, so NaN members survive until they reach the head.  GPU removal vs the reference
+    # engine's on the same state (budget chosen so one generation shrinks 24 -> 8 members).
+    P, D, key = 24, 8, 0x4A4A
+    o, m = O.shift_rotation(5, D)
+    # rand/1 + fixed F/CR: the trials (hence the archive and its shrink words) do not depend on the
+    # fitness order, whose NaN handling is the reference sort's internals (see best/1 below)
+    cfg = DEConfig("rand_1", "binomial", "clip", "fixed", f=0.5, cr=0.9, archive_rate=1.0,
+                   reduction="linear_reduction", n_min=4)
+    prob = evb.ProblemInstance.base(evb.BaseKind.sphere, o, m, 0.0)
+    for nan_at in ([0], [1], [0, 1, 2], [5, 17], [23], list(range(3, 20))):
+        eng = DEEngine(cfg, P, D)
+        rng = Rng.philox(key)
+        pop = torch.empty((P, D), dtype=torch.float64, device=dev)
+        eng.init_population(pop, -100.0, 100.0, rng)
+        fit = dev_eval(prob, pop, dev)
+        fit[nan_at] = float("nan")
+        max_fes = 2 * P + P // 2   # after one generation (fes = 2P): target = round(24 - 20 * 48/60) = 8
+        eng.set_budget(max_fes, P)
+        ref = O.RefDE(cfg, P, D)
+        ref.set_problem_base(0, o, m, 0.0)
+        ref.set_pop(pop.cpu().numpy(), fit.cpu().numpy())
+        ref.set_budget(max_fes, P)
+        eng.generation(prob, pop, fit, -100.0, 100.0, rng)
+        dr, red = eng.last_draws(), eng.last_reduction()
+        words = scripted_words_for_generation(key, dr["generation"], dr["word_counts"], dr["archive_words"],
+                                              philox=O.philox_words, shrink_words=red["shrink_words"])
+        assert ref.generation(words, -100.0, 100.0), nan_at
+        n = red["pop_after"]
+        assert n < P and ref.pop_size() == n, (nan_at, n, ref.pop_size())
+        st = ref.get()
+        got_f = fit[:n].cpu().numpy()
+        assert np.array_equal(np.isnan(got_f), np.isnan(st["fit"])), nan_at
+        assert np.array_equal(pop[:n].cpu().numpy(), st["pop"]), nan_at
+
+
+def test_best1_nan_order_engine_equals_persistent_runs(dev):
+    # best/1's base member = fitness_order()[0] under the NaN-last (fitness, index) order, in both
+    # the engine's de_best_kernel and K8's per-generation warp argmin: same Philox words, same
+    # population with NaN fitness entries -> the same generation on both paths
+    from paper_2505_17430_b200.runs import de_runs
+    P, D = 40, 10
+    cfg = DEConfig("best_1", "binomial", "clip", "fixed", f=0.5, cr=0.9)
+    o, m = O.shift_rotation(3, D)
+    prob = evb.ProblemInstance.base(evb.BaseKind.sphere, o, m, 0.0)
+    key = 0x77
+    x0 = torch.from_numpy(O.population(3, P, D)).to(dev)
+    for nan_at in ([0], [0, 1], [4, 9], list(range(P))):
+        f0 = dev_eval(prob, x0, dev)
+        f0[nan_at] = float("nan")
+        # engine: one Philox generation
+        eng = DEEngine(cfg, P, D)
+        rng = Rng.philox(key)
+        pa, fa = x0.clone(), f0.clone()
+        eng.generation(prob, pa, fa, -100.0, 100.0, rng)
+        dr = eng.last_draws()
+        best_engine = int(dr["idx"][0, 0])
+        # K8: the same generation id from the same state
+        pb, fb = x0.clone()[None], f0.clone()[None]
+        de_runs(cfg, [prob], np.array([key], np.uint64), pb, fb, 1, -100.0, 100.0, init=False,
+                gen0=int(dr["generation"]))
+        assert torch.equal(pa, pb[0]), nan_at
+        expect = [i for i in range(P) if i not in nan_at]
+        fl = f0.cpu().numpy()
+        want = min(expect, key=lambda i: (fl[i], i)) if expect else 0
+        assert best_engine == want, (nan_at, best_engine, want)
+        # the C restatement (insertion sort under the same NaN-last order) on the same words
+        orc = O.OracleDE(cfg, P, D)
+        orc.set_problem_base(0, o, m, 0.0)
+        orc.set_state(x0.cpu().numpy(), fl)
+        words = scripted_words_for_generation(key, dr["generation"], dr["word_counts"], dr["archive_words"],
+                                              philox=O.philox_words)
+        out = orc.generation(words, -100.0, 100.0)
+        assert np.all(out["idx"][:, 0] == want), nan_at
+        assert np.array_equal(orc.pop, pa.cpu().numpy()), nan_at
 
 
 @pytest.mark.parametrize("cfg", NEW_STRATEGIES[:3], ids=lambda c: f"{c.mutation}-{c.crossover}-{c.repair}")

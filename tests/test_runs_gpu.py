@@ -39,8 +39,10 @@ def replay_reference(run, comps, key, gens):
     return ref.get()
 
 
-@pytest.mark.parametrize("n_runs,gens,check_runs", [(8, 30, 8), (64, 2000, 2)])
-def test_config4_runs_match_reference(dev, n_runs, gens, check_runs):
+def test_config4_free_running_short(dev):
+    # 8 runs x 30 generations in one launch, free running (no re-sync): exact-order arithmetic
+    # keeps the populations identical to the reference's replay
+    n_runs, gens = 8, 30
     probs, comps = make_runs(n_runs)
     keys = run_keys(64, n_runs)
     pops = torch.empty((n_runs, P, D), dtype=torch.float64, device=dev)
@@ -48,17 +50,78 @@ def test_config4_runs_match_reference(dev, n_runs, gens, check_runs):
     de_runs(preset_de(0.5, 0.9), probs, keys, pops, fits, gens, -100.0, 100.0, init=True, gen0=0)
     torch.cuda.synchronize()
     gp, gf = pops.cpu().numpy(), fits.cpu().numpy()
-    flagged = 0
-    for r in range(check_runs):
+    for r in range(n_runs):
         st = replay_reference(r, comps[r], keys[r], gens)
-        rel = np.abs(gf[r] - st["fit"]) / np.maximum(1.0, np.abs(st["fit"]))
-        same = np.all(gp[r] == st["pop"], axis=1)
-        flagged += int((~same).sum())
-        # exact-order arithmetic: populations identical unless a libm-vs-CUDA exp/cos ulp flipped a
-        # selection at a near-tie (flagged), fitness within 1e-10
-        assert rel.max() <= 1e-10 or (~same).sum() > 0, r
-        assert same.mean() >= 0.95, (r, int((~same).sum()))
-    assert np.all(np.isfinite(gf))
+        assert np.array_equal(gp[r], st["pop"]), r
+        assert np.max(np.abs(gf[r] - st["fit"]) / np.maximum(1.0, np.abs(st["fit"]))) <= 1e-10, r
+
+
+def test_config4_all_runs_lockstep(dev):
+    """BASELINE config 4 as stated: all 64 runs x 2000 generations, checked every generation.
+
+    Lockstep (SURVEY §7 hard part 3): before generation g the GPU state is set to the reference's
+    state after g-1; K8 runs generation g (init=False, gen0=g) while the unmodified reference
+    engine replays the same Philox words (experiment/runner.hpp:101-160 semantics per run).
+    Every row must be bit-identical, except a flagged near-tie: a selection (f_trial <= f_parent,
+    de/engine.hpp:36) decided differently with |f_trial - f_parent| <= 1e-10 max(1, |f_parent|)
+    (libm vs CUDA exp/cos ulps in the composition); the row then equals the parent on one side.
+    Fitness of every non-flagged row within 1e-10 relative."""
+    from concurrent.futures import ThreadPoolExecutor
+    import os
+
+    n_runs, gens, tol = 64, 2000, 1e-10
+    probs, comps = make_runs(n_runs)
+    keys = run_keys(64, n_runs)
+    cfg = preset_de(0.5, 0.9)
+    pops = torch.empty((n_runs, P, D), dtype=torch.float64, device=dev)
+    fits = torch.empty((n_runs, P), dtype=torch.float64, device=dev)
+    de_runs(cfg, probs, keys, pops, fits, 0, -100.0, 100.0, init=True, gen0=0)
+    refs = []
+    for r in range(n_runs):
+        s, m = comps[r]
+        ref = O.RefDE(cfg, P, D)
+        ref.set_problem_composition(O.CONFIG4_KINDS, s, m, O.CONFIG4_SIGMA, O.CONFIG4_LAMBDA, O.CONFIG4_BIAS, 0.0)
+        assert ref.init(O.philox_words(int(keys[r]), 0xFFFFFFF0, 0, P * D), -100.0, 100.0) == P * D
+        refs.append(ref)
+    states = [ref.get() for ref in refs]
+    gp, gf = pops.cpu().numpy(), fits.cpu().numpy()
+    for r in range(n_runs):
+        assert np.array_equal(gp[r], states[r]["pop"]), r
+        assert np.max(np.abs(gf[r] - states[r]["fit"]) / np.maximum(1.0, np.abs(states[r]["fit"]))) <= tol, r
+
+    def ref_step(r, g):
+        words = O.de_fixed_generation_words(0, int(keys[r]), g, P, D)
+        ok, trial_vals = refs[r].generation_trace(words, -100.0, 100.0)
+        assert ok, (r, g)
+        return trial_vals, refs[r].get()
+
+    flagged, checked_rows = [], 0
+    with ThreadPoolExecutor(max_workers=max(1, os.cpu_count() or 1)) as pool:
+        for g in range(1, gens + 1):
+            prev_pop = np.stack([st["pop"] for st in states])
+            prev_fit = np.stack([st["fit"] for st in states])
+            pops.copy_(torch.from_numpy(prev_pop))
+            fits.copy_(torch.from_numpy(prev_fit))
+            de_runs(cfg, probs, keys, pops, fits, 1, -100.0, 100.0, init=False, gen0=g)
+            futs = [pool.submit(ref_step, r, g) for r in range(n_runs)]
+            gp, gf = pops.cpu().numpy(), fits.cpu().numpy()
+            results = [f.result() for f in futs]
+            for r, (tv, st) in enumerate(results):
+                rp, rf = st["pop"], st["fit"]
+                same = np.all(gp[r] == rp, axis=1)
+                checked_rows += P
+                for i in np.where(~same)[0]:
+                    fp = prev_fit[r, i]
+                    near = abs(tv[i] - fp) <= tol * max(1.0, abs(fp))
+                    one_side_parent = np.array_equal(gp[r, i], prev_pop[r, i]) or np.array_equal(rp[i], prev_pop[r, i])
+                    assert near and one_side_parent, (r, g, i, tv[i], fp)
+                    flagged.append((r, g, i))
+                rel = np.abs(gf[r] - rf) / np.maximum(1.0, np.abs(rf))
+                assert rel[same].max() <= tol, (r, g)
+            states = [st for _, st in results]
+    print(f"config 4 lockstep: {n_runs} runs x {gens} generations, {checked_rows} rows checked, "
+          f"{len(flagged)} flagged near-tie selections: {flagged[:10]}")
+    assert len(flagged) <= checked_rows // 1000
 
 
 @pytest.mark.parametrize("n_runs", [1, 4])
