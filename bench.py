@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="evb", choices=["evb", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the other BASELINE configs (bench_configs.py)")
     return ap.parse_args()
 
 
@@ -126,7 +127,17 @@ def make_inputs():
     return o, m, X
 
 
-def cpu_baseline_reference(o, m, X, budget_s: float = 10.0):
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_baseline_reference(o, m, X, budget_s: float = 6.0):
     """The reference's own evaluate_batch (oracle/_ref, -O3 -march, all host threads)."""
     import numpy as np
 
@@ -158,6 +169,7 @@ def cpu_baseline_reference(o, m, X, budget_s: float = 10.0):
         "value": reps * 3 * n / el,
         "unit": UNIT,
         "cores": threads,
+        "cpu_model": cpu_model(),
         "kind": "reference",
         "sample": f"{reps} full config-1 steps (3 x evaluate_batch of {n} points, D={D}, fp64) in {el:.1f} s, "
                   f"batch split into {threads} contiguous slices; {L._evb_name}",
@@ -175,7 +187,7 @@ def run_reference(args, rank, world):
     o, m, X = make_inputs()
     L = O.REF_FAST()
     threads = os.cpu_count() or 1
-    sample = 128  # points per objective per step: a bounded sample of the 1024-point step
+    sample = P  # the full step: 3 x evaluate_batch over all 1024 points (same config as the GPU arm)
     jobs, keep = [], []
     for kind in KINDS:
         kid = {"elliptic": 1, "rastrigin": 5, "ackley": 6}[kind]
@@ -199,10 +211,11 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(CONFIG, reference_sample_points_per_objective=sample),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"3 x evaluate_batch of {sample} of the {P} points per step, {threads} threads, "
-                                   f"{L._evb_name} (reference headers, -O3 -march)"},
+        "config": CONFIG,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "cpu_model": cpu_model(), "kind": "reference",
+                         "sample": f"every step is the full config-1 step: 3 x evaluate_batch of all {P} points "
+                                   f"(D={D}, fp64), batch split into {threads} contiguous slices, one eval_scratch "
+                                   f"each; {L._evb_name} (reference headers, -O3 -march)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -372,6 +385,34 @@ def run_evb(args, rank, world, local):
     e2e_steps = max(200, args.steps)  # ~0.1 s of wall clock per arm
     e2e_s, e2e_blocks = wall(e2e_step, e2e_steps)
     per_call_s, _ = wall(per_call_step, e2e_steps)
+    # the reference-shaped C++ binding: run_handle::evaluate_batch -> evb::evaluate_batch(problem,
+    # vector<vector<double>>, scratch, out) (include/evb/evb.hpp), one call per objective, timed in C++
+    reference_shape = None
+    try:
+        R = ctypes.CDLL(str(ROOT / "paper_2505_17430_b200" / "libevb_refshape.so"))
+        R.evb_refshape_time.restype = ctypes.c_int
+        blocks = 5
+        us = (ctypes.c_double * blocks)()
+        vals = np.empty((3, P))
+        kinds_arr = (ctypes.c_int * 3)(*[int(k) for k in kinds])
+        mr = np.ascontiguousarray(m)
+        rc = R.evb_refshape_time(3, kinds_arr, D, P, ctypes.c_void_p(o.ctypes.data), ctypes.c_void_p(mr.ctypes.data),
+                                 ctypes.c_void_p(X.ctypes.data), ctypes.c_int(max(100, args.steps // 2)),
+                                 ctypes.c_int(blocks), ctypes.c_double(0.5), us,
+                                 ctypes.c_void_p(vals.ctypes.data))
+        if rc == 0:
+            step_us = pdist.max_over_ranks(statistics.median(list(us)), dist, dev)
+            reference_shape = {
+                "value": world * 3 * P / (step_us * 1e-6), "unit": UNIT, "us_per_step": step_us,
+                "us_per_step_blocks": list(us), "h2d_bytes_per_step": 3 * P * D * 8, "d2h_bytes_per_step": 3 * P * 8,
+                "how": "C++: 3 x evb::evaluate_batch(gpu_problem, const vector<vector<double>>& xs, gpu_scratch&, "
+                       "vector<double>& out) per step — the call run_handle<T>::evaluate_batch "
+                       "(experiment/runner.hpp:47-53) makes; heap rows flattened into the scratch's pinned "
+                       "staging, copied in, evaluated, values back into std::vector; wall clock, median of 5 blocks"}
+        else:
+            reference_shape = {"unavailable": f"evb_refshape_time returned {rc}"}
+    except OSError as exc:
+        reference_shape = {"unavailable": str(exc)}
     e2e = {"value": world * e2e_steps * 3 * P / e2e_s, "unit": UNIT, "h2d_bytes_per_step": P * D * 8,
            "d2h_bytes_per_step": 3 * P * 8,
            "how": "evb_evaluate_batch_host_many per step (C ABI): the step's population, pinned host memory, "
@@ -381,7 +422,8 @@ def run_evb(args, rank, world, local):
            "us_per_step_blocks": e2e_blocks,
            "per_call": {"value": world * e2e_steps * 3 * P / per_call_s, "unit": UNIT,
                         "h2d_bytes_per_step": 3 * P * D * 8,
-                        "how": "3 x evb_evaluate_batch_host (the population copied in once per objective)"}}
+                        "how": "3 x evb_evaluate_batch_host (the population copied in once per objective)"},
+           "reference_shape": reference_shape}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -397,6 +439,12 @@ def run_evb(args, rank, world, local):
             line["cpu_baseline"] = cpu_baseline_reference(o, m, X)
         except Exception as exc:  # the checker is test infrastructure; report, do not crash the bench
             line["cpu_baseline"] = {"value": None, "unavailable": str(exc)}
+    if rank == 0 and world == 1 and not args.no_configs:
+        # BASELINE configs 0, 2, 3, 4, fp32 config 1 and the L2-exceeding update kernels, each with
+        # its own unit, roofline and same-run reference CPU baseline (bench_configs.py)
+        import bench_configs
+
+        line["configs"] = bench_configs.run_all()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:

@@ -359,6 +359,12 @@ EVB_API int evb_evo_bench_de(int dtype, const evb_de_config* cfg, int pop_size, 
                              evb_param_trace ptrace, double* best_host, int flags, int* path_used,
                              void* stream);
 
+/* Per-phase device time of each later generation (CUDA events on the launching stream, between
+ * the generation's kernels): order/best, draws, trial, evaluation, selection scan, selection
+ * apply.  evb_de_phase_ms synchronises and returns the last generation's phase times. */
+EVB_API int evb_de_phase_timing(evb_de e, int enable);
+EVB_API int evb_de_phase_ms(evb_de e, float* ms, int cap, int* n);
+
 /* ---- PSO engine (pso/engine.hpp:33-153, pso/topology.hpp, pso/update.hpp) ------------------ */
 
 enum evb_pso_topology { EVB_TOPO_GBEST = 0 /* "gbest" */, EVB_TOPO_LBEST_RING = 1 /* "lbest_ring" */ };
@@ -396,6 +402,10 @@ EVB_API int evb_pso_optimize(evb_pso s, evb_problem objective, evb_scratch sc, v
 /* Report every evaluation (init inside optimize, each generation's particles in i order) to
  * recorder run `run`; r = NULL detaches. */
 EVB_API int evb_pso_attach_recorder(evb_pso s, evb_recorder r, int run);
+/* Per-phase device time (as evb_de_phase_timing): neighbourhood best, update, evaluation,
+ * personal best. */
+EVB_API int evb_pso_phase_timing(evb_pso s, int enable);
+EVB_API int evb_pso_phase_ms(evb_pso s, float* ms, int cap, int* n);
 
 /* evo_bench for the swarm presets (presets.hpp make_algorithm "pso" / "spso2011" / "cso"), same
  * task layout, Philox keys, recorder slots and best_host as evb_evo_bench_de; each task runs

@@ -51,6 +51,7 @@ struct de_conf {
 }  // namespace evb
 
 struct evb_de_s {
+  evb::phase_timer phases;  // order, draws, trial, evaluation, selection scan, selection apply
   int dtype = EVB_F64;
   int P = 0, D = 0;
   evb::de_conf cfg{};
@@ -871,6 +872,7 @@ void generation_t(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, vo
                   double lb, double ub, evb_rng_s* r, cudaStream_t st) {
   de_dev<T> d = make_dev<T>(e, pop, ldp, fit, lb, ub, r);
   e->gen_P = e->P;
+  e->phases.begin(st);
   if (e->cfg.mutation == EVB_MUT_BEST1) {
     EVB_CUDA(launch_pdl(de_best_kernel<T>, dim3(1), dim3(1024), 0, st, d));
     count_launch();
@@ -879,12 +881,14 @@ void generation_t(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, vo
     EVB_CUDA(launch_pdl(de_order_kernel<T>, dim3((e->P + th - 1) / th), dim3(th), th * sizeof(T), st, d));
     count_launch();
   }
+  e->phases.mark(st);
   if (r->mode == RNG_PHILOX) {
     EVB_CUDA(launch_pdl(de_draw_philox_kernel<T>, dim3((e->P + 127) / 128), dim3(128), 0, st, d));
   } else {
     de_draw_words_kernel<T><<<1, 32, 0, st>>>(d);
   }
   count_launch();
+  e->phases.mark(st);
   {
     const int th = std::min(256, int(round_up((e->D + 2) / 2 + 1, 32)));
     if (e->cfg.crossover == EVB_CX_EXPONENTIAL)
@@ -898,6 +902,7 @@ void generation_t(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, vo
     }
   }
   EVB_CUDA(cudaGetLastError());
+  e->phases.mark(st);
   // evaluate the trials with the scalar path's semantics (problem.evaluate via individual::evaluate)
   eval_request rq{};
   rq.prob = prob;
@@ -918,13 +923,16 @@ void generation_t(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, vo
     restart_monitor_kernel<T><<<1, 32, 0, st>>>(static_cast<const T*>(e->trial_fit), e->P, e->d_mon, e->mon_eps);
     count_launch();
   }
+  e->phases.mark(st);
   EVB_CUDA(launch_pdl(de_select_scan_kernel<T>, dim3(1), dim3(kSelThreads), 0, st, d));
   count_launch();
+  e->phases.mark(st);
   {
     const int th = std::min(256, int(round_up(e->D, 32)));
     EVB_CUDA(launch_pdl(de_select_apply_kernel<T>, dim3(e->P), dim3(th), 0, st, d));
     count_launch();
   }
+  e->phases.mark(st);
   EVB_CUDA(cudaGetLastError());
   e->fes += e->P;  // st.add_fes(1) per trial (de/engine.hpp:88)
   ++e->gen_count;
@@ -1387,7 +1395,23 @@ int evb_de_destroy(evb_de e) {
   return guarded([&] {
     if (!e) return;
     free_de(e);
+    e->phases.destroy();
     delete e;
+  });
+}
+
+int evb_de_phase_timing(evb_de e, int enable) {
+  return guarded([&] {
+    require(e != nullptr, "de: null handle");
+    e->phases.on = enable != 0;
+    e->phases.n = 0;
+  });
+}
+
+int evb_de_phase_ms(evb_de e, float* ms, int cap, int* n) {
+  return guarded([&] {
+    require(e != nullptr && ms != nullptr && n != nullptr, "de_phase_ms: null argument");
+    *n = e->phases.read(ms, cap);
   });
 }
 

@@ -303,6 +303,42 @@ void population_init(int dtype, int P, int D, void* pop, int64_t ldp, double lb,
 // device generation counter <- host mirror (after host-side Philox consumers such as init)
 void set_device_gen(evb_rng_s* r, cudaStream_t st);
 
+// Per-phase CUDA events on the launching stream (bench.py's per-kernel roofline timing): when on,
+// an engine records an event before its first kernel and after each phase of a generation;
+// elapsed(ev[k], ev[k+1]) is phase k's device time.  Off by default: the events sit between
+// kernels that otherwise overlap launch and prologue with the predecessor's tail (PDL).
+struct phase_timer {
+  static constexpr int kMax = 8;
+  cudaEvent_t ev[kMax] = {};
+  int n = 0;
+  bool on = false;
+  void mark(cudaStream_t st) {
+    if (!on || n >= kMax) return;
+    if (!ev[n]) cuda_check(cudaEventCreate(&ev[n]), "phase_timer event");
+    cuda_check(cudaEventRecord(ev[n], st), "phase_timer record");
+    ++n;
+  }
+  void begin(cudaStream_t st) {
+    n = 0;
+    mark(st);
+  }
+  // phase durations of the last generation (synchronises on its last event); returns the count
+  int read(float* ms, int cap) {
+    if (n < 2) return 0;
+    cuda_check(cudaEventSynchronize(ev[n - 1]), "phase_timer sync");
+    int k = 0;
+    for (; k + 1 < n && k < cap; ++k) cuda_check(cudaEventElapsedTime(&ms[k], ev[k], ev[k + 1]), "phase_timer");
+    return k;
+  }
+  void destroy() {
+    for (auto& e : ev)
+      if (e) {
+        cudaEventDestroy(e);
+        e = nullptr;
+      }
+  }
+};
+
 // Number of kernel launches issued by the last eval_dispatch on this thread (bench accounting).
 int last_launch_count();
 void count_launch(int n = 1);

@@ -27,6 +27,7 @@
 #include "rng.cuh"
 
 struct evb_pso_s {
+  evb::phase_timer phases;  // neighbourhood best, velocity/position update, evaluation, personal best
   int dtype = EVB_F64;
   int P = 0, D = 0;
   int topology = EVB_TOPO_GBEST;
@@ -408,9 +409,11 @@ template <typename T>
 void generation_t(evb_pso_s* s, const device_problem* prob, evb_scratch_s* sc, void* X, int64_t ldx, void* V,
                   int64_t ldv, void* fit, double lb, double ub, evb_rng_s* r, cudaStream_t st) {
   const T* pf = static_cast<const T*>(s->pbest_fit);
+  s->phases.begin(st);
   if (s->topology == EVB_TOPO_GBEST) EVB_CUDA(launch_pdl(pso_gbest_kernel<T>, dim3(1), dim3(1024), 0, st, pf, s->P, s->nb));
   else EVB_CUDA(launch_pdl(pso_ring_kernel<T>, dim3((s->P + 255) / 256), dim3(256), 0, st, pf, s->P, s->nb));
   count_launch();
+  s->phases.mark(st);
   pso_dev<T> d{};
   d.P = s->P;
   d.D = s->D;
@@ -462,6 +465,7 @@ void generation_t(evb_pso_s* s, const device_problem* prob, evb_scratch_s* sc, v
   count_launch();
   EVB_CUDA(cudaGetLastError());
   if (r->mode == RNG_WORDS) words_advance(r, d.base + int64_t(s->P) * words_per_particle, st);
+  s->phases.mark(st);
   eval_request rq{};
   rq.prob = prob;
   rq.scratch = sc;
@@ -477,10 +481,12 @@ void generation_t(evb_pso_s* s, const device_problem* prob, evb_scratch_s* sc, v
   rq.scalar_trig = true;
   eval_dispatch(rq);
   if (s->rec) recorder_observe(s->rec, s->rec_run, s->fit_new, s->P, st);  // particles in i (FE) order
+  s->phases.mark(st);
   EVB_CUDA(launch_pdl(pso_pbest_kernel<T>, dim3(s->P), dim3(std::min(256, int(round_up(s->D, 32)))), 0, st,
                       static_cast<const T*>(X), ldx, static_cast<const T*>(s->fit_new), static_cast<T*>(fit),
                       static_cast<T*>(s->pbest), s->ldb, static_cast<T*>(s->pbest_fit), s->D, r->d_gen));
   count_launch();
+  s->phases.mark(st);
   EVB_CUDA(cudaGetLastError());
   s->last_gen = r->gen;
   r->gen++;
@@ -558,7 +564,23 @@ int evb_pso_destroy(evb_pso s) {
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (s->eval_scratch) evb_scratch_destroy(s->eval_scratch);
+    s->phases.destroy();
     delete s;
+  });
+}
+
+int evb_pso_phase_timing(evb_pso s, int enable) {
+  return guarded([&] {
+    require(s != nullptr, "pso: null handle");
+    s->phases.on = enable != 0;
+    s->phases.n = 0;
+  });
+}
+
+int evb_pso_phase_ms(evb_pso s, float* ms, int cap, int* n) {
+  return guarded([&] {
+    require(s != nullptr && ms != nullptr && n != nullptr, "pso_phase_ms: null argument");
+    *n = s->phases.read(ms, cap);
   });
 }
 

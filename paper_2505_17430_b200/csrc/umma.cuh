@@ -111,6 +111,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 
 }  // namespace umma
 
+#ifndef EVB_UMMA_HELPERS_ONLY  // the split kernels live in eval_gemm.cu's translation unit
 // split pre-pass: S = X - o (fp32, reference rounding), S_hi = rna_tf32(S), S_lo = S - S_hi
 __global__ void split_tf32_kernel(const float* __restrict__ X, int64_t ldx, const float* __restrict__ shift, int P,
                                   int D, float* __restrict__ hi, float* __restrict__ lo, int64_t lds) {
@@ -140,5 +141,6 @@ __global__ void split_plain_kernel(const float* __restrict__ a, int64_t n, float
     lo[e] = __uint_as_float(umma::cvt_rna_tf32(__fsub_rn(x, h)));
   }
 }
+#endif  // EVB_UMMA_HELPERS_ONLY
 
 }  // namespace evb

@@ -119,6 +119,8 @@ def _sigs():
         "evb_de_get_state": (c_int, [vp, vp, P(c_int), vp, vp, P(c_int)]),
         "evb_de_set_state": (c_int, [vp, vp, c_int, vp, vp, c_int]),
         "evb_de_last_draws": (c_int, [vp, vp, P(i64), P(u32), vp, vp, vp, vp]),
+        "evb_de_phase_timing": (c_int, [vp, c_int]),
+        "evb_de_phase_ms": (c_int, [vp, vp, c_int, P(c_int)]),
     })
     _lib.lib()
     _SIGS = True
@@ -307,6 +309,19 @@ class DEEngine:
         check(_lib.lib().evb_de_set_state(self._h, ctypes.c_void_p(a.ctypes.data), a.shape[0],
                                           ctypes.c_void_p(mf.ctypes.data), ctypes.c_void_p(mc.ctypes.data),
                                           write_index), "de_set_state")
+
+    PHASES = ("order", "draws", "trial", "evaluate", "select_scan", "select_apply")
+
+    def phase_timing(self, enable: bool = True) -> None:
+        """Record CUDA events between the kernels of each later generation (bench accounting)."""
+        check(_lib.lib().evb_de_phase_timing(self._h, int(enable)), "de_phase_timing")
+
+    def phase_ms(self) -> dict:
+        """Device time of each phase of the last generation (ms), synchronising on it."""
+        ms = (ctypes.c_float * 8)()
+        n = ctypes.c_int()
+        check(_lib.lib().evb_de_phase_ms(self._h, ms, 8, ctypes.byref(n)), "de_phase_ms")
+        return dict(zip(self.PHASES, [float(ms[k]) for k in range(n.value)]))
 
     def last_draws(self):
         P = self.pop_size

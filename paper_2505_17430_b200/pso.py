@@ -74,6 +74,8 @@ def _sigs():
         "evb_pso_generation": (c_int, [vp, vp, vp, vp, i64, vp, i64, vp, c_double, c_double, vp, vp]),
         "evb_pso_init_uniform": (c_int, [vp, vp, i64, c_double, c_double, vp, vp]),
         "evb_pso_get": (c_int, [vp, vp, vp, vp, P(u32)]),
+        "evb_pso_phase_timing": (c_int, [vp, c_int]),
+        "evb_pso_phase_ms": (c_int, [vp, vp, c_int, P(c_int)]),
         "evb_pso_set_pbest": (c_int, [vp, vp, vp]),
         "evb_pso_optimize": (c_int, [vp, vp, vp, vp, i64, vp, i64, vp, c_double, c_double, i64, vp, P(c_int),
                                      P(c_double), P(c_int), vp]),
@@ -135,6 +137,19 @@ class PSOEngine:
         check(_lib.lib().evb_pso_attach_recorder(self._h, recorder.handle if recorder is not None else None, run),
               "pso_attach_recorder")
         self._recorder = recorder
+
+    PHASES = ("neighbors", "update", "evaluate", "personal_best")
+
+    def phase_timing(self, enable: bool = True) -> None:
+        """Record CUDA events between the kernels of each later generation (bench accounting)."""
+        check(_lib.lib().evb_pso_phase_timing(self._h, int(enable)), "pso_phase_timing")
+
+    def phase_ms(self) -> dict:
+        """Device time of each phase of the last generation (ms), synchronising on it."""
+        ms = (ctypes.c_float * 8)()
+        n = ctypes.c_int()
+        check(_lib.lib().evb_pso_phase_ms(self._h, ms, 8, ctypes.byref(n)), "pso_phase_ms")
+        return dict(zip(self.PHASES, [float(ms[k]) for k in range(n.value)]))
 
     def personal_bests(self):
         pb = np.zeros((self.pop_size, self.dim), self._np())
