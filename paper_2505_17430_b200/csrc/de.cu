@@ -74,6 +74,12 @@ struct evb_de_s {
   int* arch_slot = nullptr;   // P: archive slot written by i's push (-1: none / overwritten)
   int* owner = nullptr;       // archive_cap
   int* succ = nullptr;        // P success list (indices)
+  int* wlist = nullptr;       // P: winners in push order
+  int* d_npush = nullptr;     // [winners, successes] of the last generation
+  unsigned* d_epoch = nullptr;               // generation counter of the engine (apply kernel)
+  unsigned long long* d_owner64 = nullptr;   // archive_cap
+  unsigned long long* d_sel_agg = nullptr;   // ceil(P / kSelBlockItems)
+  unsigned* d_sel_sync = nullptr;            // 2
   void* archive = nullptr;    // archive_cap x ldt
   int* d_arch_size = nullptr;
   int* d_write_index = nullptr;
@@ -146,6 +152,13 @@ struct de_dev {
   int* arch_slot;
   int* owner;
   int* succ;
+  int* wlist;   // P: winners in push (i) order
+  int* n_push;  // [winners, successes, multi-CTA epoch tag] of the last generation
+  unsigned* epoch;                // engine generation counter (never reset; tags below)
+  unsigned long long* owner64;    // archive_cap: (epoch + 1) << 32 | last push index (multi-CTA)
+  unsigned long long* sel_agg;    // per selection CTA: (epoch + 1) << 32 | pushes << 16 | successes
+  unsigned* sel_sync;             // [ticket, done] of the multi-CTA selection
+  int sel_multi;                  // selection ran on de_select_multi_kernel
   T* archive;
   int* arch_size;
   int* write_index;
@@ -231,6 +244,61 @@ __global__ void de_order_kernel(const de_dev<T> d) {
     __syncthreads();
   }
   if (i < d.P && rank < d.p_count) d.order[rank] = i;
+}
+
+// Top-p order by sorting (current-to-pbest/1): one CTA bitonic-sorts (key(f), index) pairs in
+// shared memory, N = next power of two >= P (<= kSortMax), and writes the first p_count indices.
+// key() maps the (fitness, index) order of de_order_kernel onto unsigned integers: -0.0 and +0.0
+// are one key (the reference's `<` ties them), every NaN is the largest key (after +inf), and
+// equal keys fall back to the index, so the result is the stable sort the reference performs
+// (core/population.hpp:70-77) with NaN last.  Padding sorts after everything.
+constexpr int kSortMax = 16384;
+
+__device__ __forceinline__ unsigned long long order_key(double f) {
+  if (isnan(f)) return ~0ull;
+  unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(f == 0.0 ? 0.0 : f));
+  return (b >> 63) ? ~b : (b | (1ull << 63));
+}
+__device__ __forceinline__ unsigned long long order_key(float f) {
+  if (isnan(f)) return ~0ull;
+  unsigned b = __float_as_uint(f == 0.f ? 0.f : f);
+  return (b >> 31) ? (~b) & 0xFFFFFFFFu : (b | (1u << 31));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024) de_sort_order_kernel(const de_dev<T> d, int n_pow2) {
+  ptx::griddep_wait();  // PDL (launch_pdl): predecessor data first
+  ptx::griddep_launch_dependents();
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(smem_raw);
+  int* idx = reinterpret_cast<int*>(key + n_pow2);
+  for (int t = threadIdx.x; t < n_pow2; t += blockDim.x) {
+    const bool real = t < d.P;
+    key[t] = real ? order_key(d.fit[t]) : ~0ull;
+    idx[t] = real ? t : 0x7FFFFFFF;  // padding after every NaN
+  }
+  __syncthreads();
+  const int half = n_pow2 >> 1;
+  for (int k = 2; k <= n_pow2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < half; t += blockDim.x) {
+        const int lo = ((t & ~(j - 1)) << 1) | (t & (j - 1));  // pair (lo, lo + j)
+        const int hi = lo + j;
+        const bool up = (lo & k) == 0;
+        const unsigned long long ka = key[lo], kb = key[hi];
+        const int ia = idx[lo], ib = idx[hi];
+        const bool gt = ka > kb || (ka == kb && ia > ib);
+        if (gt == up) {
+          key[lo] = kb;
+          key[hi] = ka;
+          idx[lo] = ib;
+          idx[hi] = ia;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int r = threadIdx.x; r < d.p_count; r += blockDim.x) d.order[r] = idx[r];
 }
 
 // de/parameter.hpp:28-38
@@ -472,6 +540,195 @@ __global__ void de_trial_kernel(const de_dev<T> d) {
   }
 }
 
+// K4, vectorised (binomial crossover, PHILOX source, 16-byte aligned rows): one warp per
+// individual walks its row in chunks of W = 32 x VEC genes; lane l owns genes
+// [cW + VEC l, cW + VEC l + VEC) and moves them with one 16-byte load per donor row and one
+// 16-byte store.  Gene j's uniform is stream word s0 + j.  The Philox blocks a lane computes are
+// the pairs covering words [wb + cW + VEC l, +VEC) with wb = s0 rounded down to even, so for odd
+// s0 each gene takes the NEXT word: the lane's own words 1..VEC-1 and word 0 of lane l+1 (a
+// shuffle; lane 31 takes lane 0's word 0 of the next chunk).  One Philox block per word pair as
+// in the scalar kernel, plus up to two blocks per row (the windows run ahead).  Same arithmetic as de_trial_kernel per gene, so the trials are bit-identical.
+template <typename T>
+struct vec16;
+template <>
+struct vec16<double> {
+  using V = double2;
+  static constexpr int N = 2;
+  __device__ static void get(const V& v, double (&a)[2]) { a[0] = v.x; a[1] = v.y; }
+  __device__ static V make(const double (&a)[2]) { return make_double2(a[0], a[1]); }
+};
+template <>
+struct vec16<float> {
+  using V = float4;
+  static constexpr int N = 4;
+  __device__ static void get(const V& v, float (&a)[4]) { a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w; }
+  __device__ static V make(const float (&a)[4]) { return make_float4(a[0], a[1], a[2], a[3]); }
+};
+
+constexpr int kTrialVecWarps = 8;  // individuals per 256-thread block
+
+// 16-byte read-only load; HINT: L2 evict_last (the population is re-read as donors by other
+// individuals of the same launch, the trial rows stream out with evict-first stores)
+template <bool HINT>
+__device__ __forceinline__ double2 ld16(const double* p, uint64_t pol) {
+  if constexpr (HINT) {
+    double2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+  } else {
+    return __ldg(reinterpret_cast<const double2*>(p));
+  }
+}
+template <bool HINT>
+__device__ __forceinline__ float4 ld16(const float* p, uint64_t pol) {
+  if constexpr (HINT) {
+    float4 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    return v;
+  } else {
+    return __ldg(reinterpret_cast<const float4*>(p));
+  }
+}
+
+template <typename T, int MUT, int U, bool HINT = false>
+__global__ void __launch_bounds__(32 * kTrialVecWarps) de_trial_vec_kernel(const de_dev<T> d) {
+  ptx::griddep_wait();  // PDL (launch_pdl): predecessor data first
+  ptx::griddep_launch_dependents();
+  using VT = vec16<T>;
+  using V = typename VT::V;
+  constexpr int VEC = VT::N, W = 32 * VEC;
+  const int i = blockIdx.x * kTrialVecWarps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= d.P) return;  // warp-uniform
+  const int D = d.D;
+  const T Fi = d.F[i];
+  const int jr = d.jrand[i];
+  const int a = d.idx[4 * i + 0], b = d.idx[4 * i + 1], c = d.idx[4 * i + 2];
+  const T* xi = d.pop + size_t(i) * d.ldp;
+  const T* xa = d.pop + size_t(a) * d.ldp;
+  const T* xb = d.pop + size_t(b) * d.ldp;
+  const T* xc = (MUT == EVB_MUT_TTPB1 && c >= d.P) ? d.archive + size_t(c - d.P) * d.ldt : d.pop + size_t(c) * d.ldp;
+  T* out = d.trial + size_t(i) * d.ldt;
+  const uint64_t ctr_hi = (uint64_t(*d.gen_ptr) << 32) | uint32_t(i);
+  const T lb = d.lb, ub = d.ub;
+  const int repair = d.cfg.repair;
+  const double cr = double(d.CR[i]);
+  const int64_t s0 = d.woff[i];
+  const int sh = int(s0 & 1);
+  const int64_t blk0 = s0 >> 1;  // first Philox block of the row's window
+  const uint64_t key = d.src.key;
+  uint64_t pol = 0;
+  if constexpr (HINT) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  // take bits of the lane's VEC window words in chunk cc
+  auto window = [&](int cc, bool (&tb)[VEC]) {
+#pragma unroll
+    for (int k = 0; k < VEC / 2; ++k) {
+      uint64_t w0, w1;
+      philox_pair(key, ctr_hi, uint64_t(blk0 + int64_t(cc) * (W / 2) + lane * (VEC / 2) + k), w0, w1);
+      tb[2 * k] = u01_of(w0) < cr;
+      tb[2 * k + 1] = u01_of(w1) < cr;
+    }
+  };
+  const int nchunks = (D + W - 1) / W;
+  // U chunks per iteration.  Windows run ahead: at the top of an iteration the windows of its U
+  // chunks and of the chunk after them (the odd-s0 seam word) are known, so the take bits — and
+  // with them which target vectors are needed — are known before any load issues; the next U
+  // windows are computed while the loads are in flight.
+  bool win[U + 1][VEC];
+#pragma unroll
+  for (int u = 0; u <= U; ++u)
+    if (u <= nchunks) window(u, win[u]);
+  for (int c0 = 0; c0 < nchunks; c0 += U) {
+    bool take[U][VEC];
+    bool need[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (sh) {
+        const bool up = __shfl_down_sync(0xffffffffu, win[u][0], 1);
+        const bool wrap = __shfl_sync(0xffffffffu, win[u + 1][0], 0);
+#pragma unroll
+        for (int e = 0; e + 1 < VEC; ++e) take[u][e] = win[u][e + 1];
+        take[u][VEC - 1] = lane == 31 ? wrap : up;
+      } else {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) take[u][e] = win[u][e];
+      }
+      const int j0 = (c0 + u) * W + VEC * lane;
+      need[u] = MUT == EVB_MUT_TTPB1 || repair == EVB_REP_MIDPOINT_TARGET;
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        take[u][e] = take[u][e] || (j0 + e == jr);
+        need[u] = need[u] || !take[u][e];
+      }
+    }
+    V va[U], vb[U], vc[U], vi[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j0 = (c0 + u) * W + VEC * lane;
+      if (j0 + VEC <= D) {
+        va[u] = ld16<HINT>(xa + j0, pol);
+        vb[u] = ld16<HINT>(xb + j0, pol);
+        vc[u] = ld16<HINT>(xc + j0, pol);
+        if (need[u]) vi[u] = ld16<HINT>(xi + j0, pol);
+      }
+    }
+    // the next iteration's windows (chunks c0 + U + 1 .. c0 + 2U), overlapping the loads
+    bool nw[U][VEC];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (c0 + U + 1 + u <= nchunks) window(c0 + U + 1 + u, nw[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j0 = (c0 + u) * W + VEC * lane;
+      if (j0 + VEC <= D) {
+        T ta[VEC], tb_[VEC], tc[VEC], ti[VEC] = {}, v[VEC];
+        VT::get(va[u], ta);
+        VT::get(vb[u], tb_);
+        VT::get(vc[u], tc);
+        if (need[u]) VT::get(vi[u], ti);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          T x;
+          if (take[u][e]) x = donor_gene<T>(MUT, MUT == EVB_MUT_TTPB1 ? ti[e] : T(0), ta[e], tb_[e], tc[e], Fi);
+          else x = ti[e];
+          if (repair == EVB_REP_CLIP) {
+            if (x < lb) x = lb;
+            if (x > ub) x = ub;
+          } else if (repair != EVB_REP_REINITIALIZE) {
+            if (x < lb || x > ub) x = repair_gene<T>(repair, x, ti[e], lb, ub);
+          }
+          v[e] = x;
+        }
+        __stcs(reinterpret_cast<V*>(out + j0), VT::make(v));
+      } else if (j0 < D) {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          const int j = j0 + e;
+          if (j >= D) break;
+          T x;
+          if (take[u][e]) x = donor_gene<T>(MUT, MUT == EVB_MUT_TTPB1 ? xi[j] : T(0), xa[j], xb[j], xc[j], Fi);
+          else x = xi[j];
+          if (repair == EVB_REP_CLIP) {
+            if (x < lb) x = lb;
+            if (x > ub) x = ub;
+          } else if (repair != EVB_REP_REINITIALIZE) {
+            if (x < lb || x > ub) x = repair_gene<T>(repair, x, xi[j], lb, ub);
+          }
+          out[j] = x;
+        }
+      }
+    }
+    // shift the windows: the last known one moves to the front, the new ones follow
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) win[0][e] = win[U][e];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) win[u + 1][e] = nw[u][e];
+  }
+}
+
 // reinitialize repair (de/strategy.hpp:285-289), a second pass over the trial rows: every gene
 // still outside [lb, ub] takes T(uniform(lb, ub)); the words follow the crossover words in j
 // order, so each violating gene's word is its rank among the violations (block prefix count).
@@ -515,6 +772,10 @@ __global__ void de_reinit_kernel(const de_dev<T> d) {
   }
   if (threadIdx.x == 0 && d.src.mode == RNG_PHILOX) d.wcount[i] = r0 + running;
 }
+
+template <typename T>
+__device__ void adapter_update(const de_dev<T>& d, int n_succ, bool staged_in_pass1, double* st_g, double* st_f,
+                               double* st_c);
 
 // K5a: selection bookkeeping (de/engine.hpp:27-47, de/strategy.hpp:29-37, de/parameter.hpp:166-184)
 // in one CTA, parallel where the reference's sequential semantics allow it:
@@ -601,6 +862,7 @@ __global__ void __launch_bounds__(kSelThreads) de_select_scan_kernel(const de_de
     const int k = carry[1] + (wid > 0 ? warp_sum[1][wid - 1] : 0) + is - s;  // success index
     if (i < d.P) {
       d.win[i] = w ? q + 1 : 0;  // winner flag carrying its push index
+      if (w) d.wlist[q] = i;
       if (s) d.succ[k] = i;
       if (s && staged_in_pass1) {
         st_g[k] = gain;
@@ -637,16 +899,26 @@ __global__ void __launch_bounds__(kSelThreads) de_select_scan_kernel(const de_de
   }
   __syncthreads();
   if (tid == 0) {
+    d.n_push[0] = n_push;
+    d.n_push[1] = n_succ;
     const int new_size = min(d.archive_cap, size0 + n_push);
     const int64_t nv = d.archive_cap > 0 ? max(0, n_push - room) : 0;
     *d.arch_size = new_size;
     *d.arch_words = nv;
     if (d.src.mode == RNG_WORDS) *d.cursor = wpos + nv;
   }
-  // adapter update: the sums stay sequential in success order (the reference's loops), but the
-  // successes' (gain, F, CR) are first staged into shared memory by the whole block — one thread
-  // chasing succ[s] -> fit[i] through global memory paid the L2 latency per success
   if (n_succ == 0 || !adapt) return;
+  adapter_update<T>(d, n_succ, staged_in_pass1, st_g, st_f, st_c);
+}
+
+// SHADE / JADE memory update from the generation's successes (de/parameter.hpp:107-120, 166-184):
+// the sums stay sequential in success order (the reference's loops), but the successes' (gain, F,
+// CR) are first staged into shared memory by the whole block — one thread chasing succ[s] ->
+// fit[i] through global memory paid the L2 latency per success.  st_* hold blockDim.x doubles.
+template <typename T>
+__device__ void adapter_update(const de_dev<T>& d, int n_succ, bool staged_in_pass1, double* st_g, double* st_f,
+                               double* st_c) {
+  const int tid = threadIdx.x;
   __shared__ double acc_s[4];
   auto stage = [&](int base) {
     const int s = base + tid;
@@ -738,24 +1010,245 @@ __global__ void __launch_bounds__(kSelThreads) de_select_scan_kernel(const de_de
   }
 }
 
-// K5b: replaced parent -> archive slot, trial -> population (std::swap(pop[i], trial)).
+// K5a for large populations (P > kSelSingleMax): the same bookkeeping over many CTAs.  Each CTA
+// takes kSelBlockItems consecutive individuals in ticket order (atomic ticket = virtual block id,
+// so every lower id is already running), publishes its (pushes, successes) aggregate tagged with
+// the generation's epoch, and sums the aggregates of all lower ids (decoupled look-back; a lower
+// id publishes before it waits on anything, so the spin always ends).  Archive-slot owners are
+// 64-bit (epoch << 32 | push index) maxima, so a later generation needs no reset; the apply
+// kernel resolves last-writer-wins against them.  The CTA that finishes last writes the archive
+// size / victim-word count / cursor and resets the tickets.  Adaptive adapters then run
+// de_adapt_kernel (one CTA, the sequential sums).
+constexpr int kSelSingleMax = 2048;
+constexpr int kSelBlockThreads = 256;
+constexpr int kSelPerThread = 4;
+constexpr int kSelBlockItems = kSelBlockThreads * kSelPerThread;
+
 template <typename T>
-__global__ void de_select_apply_kernel(const de_dev<T> d) {
+__global__ void __launch_bounds__(kSelBlockThreads) de_select_multi_kernel(const de_dev<T> d) {
   ptx::griddep_wait();  // PDL (launch_pdl): predecessor data first
   ptx::griddep_launch_dependents();
-  const int i = blockIdx.x;
-  if (i == 0 && threadIdx.x == 0) *d.gen_ptr += 1u;  // last reader of this generation's id is done
-  if (!d.win[i]) return;
-  const int sl = d.arch_slot[i];
-  T* x = d.pop + size_t(i) * d.ldp;
-  const T* t = d.trial + size_t(i) * d.ldt;
-  T* a = sl >= 0 ? d.archive + size_t(sl) * d.ldt : nullptr;
-  for (int j = threadIdx.x; j < d.D; j += blockDim.x) {
-    const T old = x[j];
-    if (a) a[j] = old;
-    x[j] = t[j];
+  __shared__ int s_vb, s_last;
+  __shared__ int warp_sum[2][kSelBlockThreads / 32];
+  __shared__ int s_prefix[2];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) s_vb = int(atomicAdd(&d.sel_sync[0], 1u));
+  __syncthreads();
+  const int vb = s_vb;
+  const unsigned tag = *d.epoch + 1u;
+  const int size0 = *d.arch_size;
+  const int room = d.archive_cap - size0;
+  const int64_t wpos = d.src.mode == RNG_WORDS ? *d.cursor : 0;
+  const uint64_t ctr_hi = (uint64_t(*d.gen_ptr) << 32) | kSubArchive;
+  const int i0 = vb * kSelBlockItems + tid * kSelPerThread;
+  T ftv[kSelPerThread], fpv[kSelPerThread];
+#pragma unroll
+  for (int u = 0; u < kSelPerThread; ++u)
+    if (i0 + u < d.P) {
+      ftv[u] = d.trial_fit[i0 + u];
+      fpv[u] = d.fit[i0 + u];
+    }
+  int wbits = 0, sbits = 0;
+#pragma unroll
+  for (int u = 0; u < kSelPerThread; ++u)
+    if (i0 + u < d.P) {
+      const int w_ = (ftv[u] <= fpv[u]) ? 1 : 0;
+      wbits |= w_ << u;
+      sbits |= ((w_ && fop<T>::sub(fpv[u], ftv[u]) > T(0)) ? 1 : 0) << u;
+    }
+  const int w = __popc(wbits), s = __popc(sbits);
+  int iw = w, is = s;
+  for (int off = 1; off < 32; off <<= 1) {
+    const int a = __shfl_up_sync(0xffffffffu, iw, off), b = __shfl_up_sync(0xffffffffu, is, off);
+    if (lane >= off) {
+      iw += a;
+      is += b;
+    }
   }
-  if (threadIdx.x == 0) d.fit[i] = d.trial_fit[i];
+  if (lane == 31) {
+    warp_sum[0][wid] = iw;
+    warp_sum[1][wid] = is;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    constexpr int nw = kSelBlockThreads / 32;
+    int a = lane < nw ? warp_sum[0][lane] : 0, b = lane < nw ? warp_sum[1][lane] : 0;
+    for (int off = 1; off < 32; off <<= 1) {
+      const int x = __shfl_up_sync(0xffffffffu, a, off), y = __shfl_up_sync(0xffffffffu, b, off);
+      if (lane >= off) {
+        a += x;
+        b += y;
+      }
+    }
+    if (lane < nw) {
+      warp_sum[0][lane] = a;
+      warp_sum[1][lane] = b;
+    }
+    // publish this CTA's aggregate, then sum every lower id's (spin until tagged this generation)
+    const int tw = __shfl_sync(0xffffffffu, a, nw - 1), ts = __shfl_sync(0xffffffffu, b, nw - 1);
+    if (lane == 0) {
+      const unsigned long long agg = (static_cast<unsigned long long>(tag) << 32) | (unsigned(tw) << 16) | unsigned(ts);
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(d.sel_agg + vb), "l"(agg) : "memory");
+    }
+    int pw = 0, ps = 0;
+    for (int j = lane; j < vb; j += 32) {
+      unsigned long long v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(d.sel_agg + j) : "memory");
+      } while (unsigned(v >> 32) != tag);
+      pw += int((v >> 16) & 0xFFFFu);
+      ps += int(v & 0xFFFFu);
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      pw += __shfl_xor_sync(0xffffffffu, pw, off);
+      ps += __shfl_xor_sync(0xffffffffu, ps, off);
+    }
+    if (lane == 0) {
+      s_prefix[0] = pw;
+      s_prefix[1] = ps;
+    }
+  }
+  __syncthreads();
+  const int q0 = s_prefix[0] + (wid > 0 ? warp_sum[0][wid - 1] : 0) + iw - w;
+  const int k0 = s_prefix[1] + (wid > 0 ? warp_sum[1][wid - 1] : 0) + is - s;
+#pragma unroll
+  for (int u = 0; u < kSelPerThread; ++u) {
+    const int i = i0 + u;
+    if (i >= d.P) continue;
+    const int wu = (wbits >> u) & 1, su = (sbits >> u) & 1;
+    const int q = q0 + __popc(wbits & ((1 << u) - 1));
+    const int k = k0 + __popc(sbits & ((1 << u) - 1));
+    d.win[i] = wu ? q + 1 : 0;
+    if (wu) d.wlist[q] = i;
+    if (su) d.succ[k] = i;
+    int sl = -1;
+    if (wu && d.archive_cap > 0) {
+      if (q < room) {
+        sl = size0 + q;
+      } else {
+        const int64_t v = q - room;
+        sl = uint_of(word_at(d.src, ctr_hi, d.src.mode == RNG_WORDS ? wpos + v : v, d.overflow), d.archive_cap);
+      }
+      atomicMax(d.owner64 + sl, (static_cast<unsigned long long>(tag) << 32) | unsigned(q));
+    }
+    d.arch_slot[i] = sl;  // provisional; the apply kernel resolves overwritten pushes
+  }
+  // the last CTA to finish: totals, archive size, victim words, cursor; tickets back to 0
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const unsigned done = atomicAdd(&d.sel_sync[1], 1u);
+    s_last = done == gridDim.x - 1 ? 1 : 0;
+  }
+  __syncthreads();
+  if (s_last && tid == 0) {
+    __threadfence();
+    int tw = 0, ts = 0;  // all aggregates are published (every CTA counted itself done)
+    for (int j = 0; j < int(gridDim.x); ++j) {
+      const unsigned long long a = __ldcg(d.sel_agg + j);
+      tw += int((a >> 16) & 0xFFFFu);
+      ts += int(a & 0xFFFFu);
+    }
+    d.n_push[0] = tw;
+    d.n_push[1] = ts;
+    d.n_push[2] = int(tag);
+    *d.epoch = tag;  // the next generation tags with tag + 1 (read by every CTA before this point)
+    const int new_size = min(d.archive_cap, size0 + tw);
+    const int64_t nv = d.archive_cap > 0 ? max(0, tw - room) : 0;
+    *d.arch_size = new_size;
+    *d.arch_words = nv;
+    if (d.src.mode == RNG_WORDS) *d.cursor = wpos + nv;
+    d.sel_sync[0] = 0u;
+    d.sel_sync[1] = 0u;
+  }
+}
+
+// adaptive adapters after de_select_multi_kernel: the SHADE / JADE update over the success list
+template <typename T>
+__global__ void __launch_bounds__(kSelThreads) de_adapt_kernel(const de_dev<T> d) {
+  ptx::griddep_wait();  // PDL (launch_pdl): predecessor data first
+  ptx::griddep_launch_dependents();
+  __shared__ double st_g[kSelThreads], st_f[kSelThreads], st_c[kSelThreads];
+  const int n_succ = d.n_push[1];
+  if (n_succ == 0) return;
+  adapter_update<T>(d, n_succ, false, st_g, st_f, st_c);
+}
+
+// K5b: replaced parent -> archive slot, trial -> population (std::swap(pop[i], trial)), one warp
+// per winner over the scan's push list (a generation late in a run replaces few rows: no block per
+// individual), 16-byte moves where the rows allow, four in flight per lane.
+template <typename T>
+__global__ void __launch_bounds__(256) de_select_apply_kernel(const de_dev<T> d, int vec, int list) {
+  ptx::griddep_wait();  // PDL (launch_pdl): predecessor data first
+  ptx::griddep_launch_dependents();
+  if (list && blockIdx.x == 0 && threadIdx.x == 0) *d.gen_ptr += 1u;  // last reader of this generation's id is done
+  using VT = vec16<T>;
+  using V = typename VT::V;
+  constexpr int VEC = VT::N;
+  if (!list) {  // one block per individual (small populations: the shortest dependent chain)
+    const int i = blockIdx.x;
+    if (i == 0 && threadIdx.x == 0) *d.gen_ptr += 1u;
+    if (!d.win[i]) return;
+    const int sl = d.arch_slot[i];
+    T* x = d.pop + size_t(i) * d.ldp;
+    const T* t = d.trial + size_t(i) * d.ldt;
+    T* a = sl >= 0 ? d.archive + size_t(sl) * d.ldt : nullptr;
+    for (int j = threadIdx.x; j < d.D; j += blockDim.x) {
+      const T old = x[j];
+      if (a) a[j] = old;
+      x[j] = t[j];
+    }
+    if (threadIdx.x == 0) d.fit[i] = d.trial_fit[i];
+    return;
+  }
+  // list: walk the scan's push list, one warp per winner (few winners late in a run)
+  const int n = *d.n_push;
+  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+  for (int q = blockIdx.x * wpb + (threadIdx.x >> 5); q < n; q += gridDim.x * wpb) {
+    const int i = d.wlist[q];
+    int sl = d.arch_slot[i];
+    if (d.sel_multi && sl >= 0 &&  // a later push won the slot (tag: the multi-CTA selection's epoch)
+        d.owner64[sl] != ((static_cast<unsigned long long>(unsigned(d.n_push[2])) << 32) | unsigned(q))) {
+      sl = -1;
+      if ((threadIdx.x & 31) == 0) d.arch_slot[i] = -1;
+    }
+    T* x = d.pop + size_t(i) * d.ldp;
+    const T* t = d.trial + size_t(i) * d.ldt;
+    T* a = sl >= 0 ? d.archive + size_t(sl) * d.ldt : nullptr;
+    int j0 = 0;
+    if (vec) {
+      const int nv = d.D / VEC;  // whole vectors
+      V* xv = reinterpret_cast<V*>(x);
+      const V* tv = reinterpret_cast<const V*>(t);
+      V* av = reinterpret_cast<V*>(a);
+      int k = lane;
+      for (; k + 96 < nv; k += 128) {
+        V o[4], tt[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          o[u] = xv[k + 32 * u];
+          tt[u] = tv[k + 32 * u];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (a) av[k + 32 * u] = o[u];
+          xv[k + 32 * u] = tt[u];
+        }
+      }
+      for (; k < nv; k += 32) {
+        const V o = xv[k], tt = tv[k];
+        if (a) av[k] = o;
+        xv[k] = tt;
+      }
+      j0 = nv * VEC;
+    }
+    for (int j = j0 + lane; j < d.D; j += 32) {
+      const T old = x[j];
+      if (a) a[j] = old;
+      x[j] = t[j];
+    }
+    if (lane == 0) d.fit[i] = d.trial_fit[i];
+  }
 }
 
 // init_population (core/population.hpp:88-98): P*D uniforms, individual-major
@@ -799,6 +1292,13 @@ de_dev<T> make_dev(evb_de_s* e, void* pop, int64_t ldp, void* fit, double lb, do
   d.arch_slot = e->arch_slot;
   d.owner = e->owner;
   d.succ = e->succ;
+  d.wlist = e->wlist;
+  d.n_push = e->d_npush;
+  d.epoch = e->d_epoch;
+  d.owner64 = e->d_owner64;
+  d.sel_agg = e->d_sel_agg;
+  d.sel_sync = e->d_sel_sync;
+  d.sel_multi = (e->P > kSelSingleMax || std::getenv("EVB_DE_SELECT_MULTI") != nullptr) ? 1 : 0;
   d.archive = static_cast<T*>(e->archive);
   d.arch_size = e->d_arch_size;
   d.write_index = e->d_write_index;
@@ -867,6 +1367,16 @@ __global__ void param_trace_kernel(const T* mem_f, const T* mem_cr, int H, int s
 template <typename T>
 void reduce_t(evb_de_s* e, void* pop, int64_t ldp, void* fit, evb_rng_s* r, cudaStream_t st);
 
+int sm_count_cached() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    EVB_CUDA(cudaGetDevice(&dev));
+    EVB_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
 template <typename T>
 void generation_t(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, void* pop, int64_t ldp, void* fit,
                   double lb, double ub, evb_rng_s* r, cudaStream_t st) {
@@ -877,8 +1387,24 @@ void generation_t(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, vo
     EVB_CUDA(launch_pdl(de_best_kernel<T>, dim3(1), dim3(1024), 0, st, d));
     count_launch();
   } else if (e->cfg.mutation == EVB_MUT_TTPB1) {
-    const int th = 256;
-    EVB_CUDA(launch_pdl(de_order_kernel<T>, dim3((e->P + th - 1) / th), dim3(th), th * sizeof(T), st, d));
+    if (e->P <= kSortMax && std::getenv("EVB_DE_ORDER_RANK") == nullptr) {
+      int n2 = 1;
+      while (n2 < e->P) n2 <<= 1;
+      const size_t smem = size_t(n2) * (sizeof(unsigned long long) + sizeof(int));
+      static bool attr = false;
+      if (!attr) {  // up to 192 KB of (key, index) pairs
+        EVB_CUDA(cudaFuncSetAttribute(de_sort_order_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(size_t(kSortMax) * 12)));
+        EVB_CUDA(cudaFuncSetAttribute(de_sort_order_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(size_t(kSortMax) * 12)));
+        attr = true;
+      }
+      EVB_CUDA(launch_pdl(de_sort_order_kernel<T>, dim3(1), dim3(std::min(1024, std::max(32, n2 / 2))), smem, st, d,
+                          n2));
+    } else {
+      const int th = 256;
+      EVB_CUDA(launch_pdl(de_order_kernel<T>, dim3((e->P + th - 1) / th), dim3(th), th * sizeof(T), st, d));
+    }
     count_launch();
   }
   e->phases.mark(st);
@@ -891,7 +1417,28 @@ void generation_t(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, vo
   e->phases.mark(st);
   {
     const int th = std::min(256, int(round_up((e->D + 2) / 2 + 1, 32)));
-    if (e->cfg.crossover == EVB_CX_EXPONENTIAL)
+    // warp per individual with 16-byte rows where the rows allow it (the population and the
+    // archive / trial rows, which the engine pitches to 16 bytes)
+    // (small populations keep the block-per-individual kernel: one Philox block per thread and
+    // no run-ahead windows, the shorter dependent chain when the whole generation is latency)
+    const bool vec = r->mode == RNG_PHILOX && e->cfg.crossover == EVB_CX_BINOMIAL &&
+                     (int64_t(e->P) * e->D >= (int64_t(1) << 18) || std::getenv("EVB_DE_TRIAL_VEC") != nullptr) &&
+                     (ldp * int64_t(sizeof(T))) % 16 == 0 && reinterpret_cast<uintptr_t>(pop) % 16 == 0 &&
+                     std::getenv("EVB_DE_TRIAL_SCALAR") == nullptr;
+    if (vec) {
+      const dim3 g((e->P + kTrialVecWarps - 1) / kTrialVecWarps), bl(32 * kTrialVecWarps);
+      const int variant = std::getenv("EVB_DE_TRIAL_VARIANT") ? std::atoi(std::getenv("EVB_DE_TRIAL_VARIANT")) : 0;
+      if (e->cfg.mutation == EVB_MUT_TTPB1)
+        EVB_CUDA(launch_pdl(variant == 1   ? de_trial_vec_kernel<T, EVB_MUT_TTPB1, 1, true>
+                            : variant == 2 ? de_trial_vec_kernel<T, EVB_MUT_TTPB1, 2, false>
+                                           : de_trial_vec_kernel<T, EVB_MUT_TTPB1, 1, false>,
+                            g, bl, 0, st, d));
+      else
+        EVB_CUDA(launch_pdl(variant == 1   ? de_trial_vec_kernel<T, EVB_MUT_RAND1, 1, true>
+                            : variant == 2 ? de_trial_vec_kernel<T, EVB_MUT_RAND1, 2, false>
+                                           : de_trial_vec_kernel<T, EVB_MUT_RAND1, 1, false>,
+                            g, bl, 0, st, d));
+    } else if (e->cfg.crossover == EVB_CX_EXPONENTIAL)
       EVB_CUDA(launch_pdl(de_trial_kernel<T, EVB_CX_EXPONENTIAL>, dim3(e->P), dim3(th), 0, st, d));
     else
       EVB_CUDA(launch_pdl(de_trial_kernel<T, EVB_CX_BINOMIAL>, dim3(e->P), dim3(th), 0, st, d));
@@ -924,12 +1471,28 @@ void generation_t(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, vo
     count_launch();
   }
   e->phases.mark(st);
-  EVB_CUDA(launch_pdl(de_select_scan_kernel<T>, dim3(1), dim3(kSelThreads), 0, st, d));
-  count_launch();
+  if (d.sel_multi) {
+    const int blocks = (e->P + kSelBlockItems - 1) / kSelBlockItems;
+    EVB_CUDA(launch_pdl(de_select_multi_kernel<T>, dim3(blocks), dim3(kSelBlockThreads), 0, st, d));
+    count_launch();
+    if (e->cfg.parameter == EVB_PAR_SHADE || e->cfg.parameter == EVB_PAR_JADE) {
+      EVB_CUDA(launch_pdl(de_adapt_kernel<T>, dim3(1), dim3(kSelThreads), 0, st, d));
+      count_launch();
+    }
+  } else {
+    EVB_CUDA(launch_pdl(de_select_scan_kernel<T>, dim3(1), dim3(kSelThreads), 0, st, d));
+    count_launch();
+  }
   e->phases.mark(st);
   {
-    const int th = std::min(256, int(round_up(e->D, 32)));
-    EVB_CUDA(launch_pdl(de_select_apply_kernel<T>, dim3(e->P), dim3(th), 0, st, d));
+    const int vec = (ldp * int64_t(sizeof(T))) % 16 == 0 && reinterpret_cast<uintptr_t>(pop) % 16 == 0 ? 1 : 0;
+    const int blocks = std::max(1, std::min((e->P + 7) / 8, 4 * sm_count_cached()));
+    if (d.sel_multi) {
+      EVB_CUDA(launch_pdl(de_select_apply_kernel<T>, dim3(blocks), dim3(256), 0, st, d, vec, 1));
+    } else {
+      const int th = std::min(256, int(round_up(e->D, 32)));
+      EVB_CUDA(launch_pdl(de_select_apply_kernel<T>, dim3(e->P), dim3(th), 0, st, d, vec, 0));
+    }
     count_launch();
   }
   e->phases.mark(st);
@@ -1185,7 +1748,8 @@ void free_de(evb_de_s* e) {
   if (e->graph) cudaGraphExecDestroy(e->graph);
   if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
   void* ptrs[] = {e->trial, e->trial_fit, e->F, e->CR, e->slot, e->idx, e->jrand, e->xlen, e->rword, e->woff, e->wcount, e->order,
-                  e->win, e->arch_slot, e->owner, e->succ, e->archive, e->d_arch_size, e->d_write_index,
+                  e->win, e->arch_slot, e->owner, e->succ, e->wlist, e->d_npush, e->d_epoch, e->d_owner64, e->d_sel_agg,
+                  e->d_sel_sync, e->archive, e->d_arch_size, e->d_write_index,
                   e->d_arch_words, e->mem_f, e->mem_cr, e->rank, e->d_shrink_words, e->d_mon};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -1370,6 +1934,12 @@ int evb_de_create(int dtype, const evb_de_config* c, int pop_size, int dim, evb_
       e->arch_slot = static_cast<int*>(dalloc<int>(pop_size));
       e->owner = static_cast<int*>(dalloc<int>(std::max(1, e->archive_cap)));
       e->succ = static_cast<int*>(dalloc<int>(pop_size));
+      e->wlist = static_cast<int*>(dalloc<int>(pop_size));
+      e->d_npush = static_cast<int*>(dalloc<int>(3));
+      e->d_epoch = static_cast<unsigned*>(dalloc<unsigned>(1));
+      e->d_owner64 = static_cast<unsigned long long*>(dalloc<unsigned long long>(std::max(1, e->archive_cap)));
+      e->d_sel_agg = static_cast<unsigned long long*>(dalloc<unsigned long long>((pop_size + 1023) / 1024));
+      e->d_sel_sync = static_cast<unsigned*>(dalloc<unsigned>(2));
       EVB_CUDA(cudaMalloc(&e->archive, bytes(size_t(std::max(1, e->archive_cap)) * e->ldt)));
       EVB_CUDA(memset_now(e->archive, 0, bytes(size_t(std::max(1, e->archive_cap)) * e->ldt)));
       e->d_arch_size = static_cast<int*>(dalloc<int>(1));

@@ -126,10 +126,11 @@ def test_device_philox_matches_restatement():
         assert np.array_equal(philox_words(key, hi, 5, 257), O.philox_words(key, hi, 5, 257))
 
 
-@pytest.mark.parametrize("P,D,G", [(180, 100, 1000), (1100, 20, 6)])
+@pytest.mark.parametrize("P,D,G", [(180, 100, 1000), (1100, 20, 6), (2500, 20, 4)])
 def test_config2_shade_lockstep(dev, P, D, G):
-    # BASELINE config 2 for its stated 1000 generations, and a population above one select-scan
-    # pass (1024: successes staged apart from the flags, SHADE memory sums over several chunks).
+    # BASELINE config 2 for its stated 1000 generations, a population above one select-scan
+    # pass (1024: successes staged apart from the flags, SHADE memory sums over several chunks),
+    # and one above the single-CTA selection (2048: multi-CTA look-back scan + adapter kernel).
     # A row may differ only when it is flagged: its F / CR differ by a libm-vs-CUDA ulp, or its
     # selection (f_trial <= f_parent) is a near-tie within 1e-10 relative (Ackley's exp / cos).
     key = 11
@@ -137,7 +138,7 @@ def test_config2_shade_lockstep(dev, P, D, G):
     cfg = preset_shade(0.11, P, 1.0)
     prob = evb.ProblemInstance.base(evb.BaseKind.ackley, o, m, 0.0)
     eng = DEEngine(cfg, P, D)
-    assert eng.archive_capacity == P and eng.p_count == (20 if P == 180 else 121)
+    assert eng.archive_capacity == P and eng.p_count == {180: 20, 1100: 121, 2500: 275}[P]
     rng = Rng.philox(key)
     pop = torch.empty((P, D), dtype=torch.float64, device=dev)
     eng.init_population(pop, -100.0, 100.0, rng)
@@ -576,3 +577,111 @@ def test_restart_lshade_matches_reference(dev, stagnation, budget):
     assert got["evaluations"] == ref["evaluations"]
     assert abs(got["best_fitness"] - ref["best_fitness"]) <= 1e-10 * max(1.0, abs(ref["best_fitness"]))
     assert not rng.state()["overflow"]
+
+
+VEC_CASES = [
+    (DEConfig("rand_1", "binomial", "clip", "fixed", f=0.5, cr=0.9), 64, 1000),
+    (DEConfig("rand_1", "binomial", "midpoint_target", "fixed", f=0.9, cr=0.5), 40, 65),
+    (DEConfig("best_1", "binomial", "reflect", "fixed", f=0.8, cr=0.7), 33, 130),
+    (DEConfig("rand_1", "binomial", "reinitialize", "fixed", f=0.9, cr=0.9), 50, 7),
+    (DEConfig("ttpb_1", "binomial", "midpoint_target", "shade", p_best=0.11, use_archive=True, memory_size=20,
+              archive_rate=1.0), 180, 100),
+    (DEConfig("ttpb_1", "binomial", "clip", "jade", p_best=0.05, use_archive=True, jade_c=0.1, archive_rate=1.0),
+     2100, 33),
+    (DEConfig("rand_1", "binomial", "clip", "fixed", f=0.5, cr=0.9), 16, 1),
+]
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32], ids=["f64", "f32"])
+@pytest.mark.parametrize("cfg,P,D", VEC_CASES, ids=lambda v: str(v) if isinstance(v, int) else
+                         (f"{v.mutation}-{v.repair}-{v.parameter}" if isinstance(v, DEConfig) else None))
+def test_trial_vector_kernel_equals_scalar(dev, monkeypatch, cfg, P, D, dtype):
+    """K4's warp-per-individual 16-byte kernel (odd and even gene-word offsets, row tails, the
+    Philox word shuffle at the lane-31 seam) against the block-per-individual scalar kernel: the
+    same generations from the same state, populations / fitness / archive / memories bit-identical;
+    P = 2100 also runs the multi-item selection scan (> 1024 individuals)."""
+    from paper_2505_17430_b200.de import EVB_F32, EVB_F64
+
+    o, m = O.shift_rotation(3, D)
+    et = EVB_F64 if dtype == torch.float64 else EVB_F32
+    prob = evb.ProblemInstance.base(evb.BaseKind.rastrigin, o, m, 0.0, dtype=et)
+    runs = []
+    for scalar in (False, True):
+        if scalar:
+            monkeypatch.setenv("EVB_DE_TRIAL_SCALAR", "1")
+            monkeypatch.delenv("EVB_DE_TRIAL_VEC", raising=False)
+        else:
+            monkeypatch.delenv("EVB_DE_TRIAL_SCALAR", raising=False)
+            monkeypatch.setenv("EVB_DE_TRIAL_VEC", "1")
+        eng = DEEngine(cfg, P, D, et)
+        rng = Rng.philox(0xBEEF)
+        pop = torch.empty((P, D), dtype=dtype, device=dev)
+        eng.init_population(pop, -100.0, 100.0, rng)
+        fit = dev_eval(prob, pop, dev)
+        for _ in range(12):
+            eng.generation(prob, pop, fit, -100.0, 100.0, rng)
+        torch.cuda.synchronize()
+        runs.append((pop.cpu().numpy(), fit.cpu().numpy(), eng.get_state(), eng.last_draws()["word_counts"]))
+    (p0, f0, s0, w0), (p1, f1, s1, w1) = runs
+    assert np.array_equal(p0, p1)
+    assert np.array_equal(f0, f1, equal_nan=True)
+    assert np.array_equal(w0, w1)
+    assert s0["archive_size"] == s1["archive_size"]
+    assert np.array_equal(s0["archive"], s1["archive"])
+    assert np.array_equal(s0["memory_f"], s1["memory_f"]) and np.array_equal(s0["memory_cr"], s1["memory_cr"])
+
+
+SEL_CASES = [
+    (preset_shade(0.11, 180, 1.0), 180, 20, "ackley"),
+    (DEConfig("ttpb_1", "binomial", "clip", "jade", p_best=0.05, use_archive=True, jade_c=0.1, archive_rate=0.5),
+     700, 16, "sphere"),
+    (DEConfig("rand_1", "binomial", "clip", "fixed", f=0.5, cr=0.9), 3000, 8, "sphere"),
+]
+
+
+@pytest.mark.parametrize("cfg,P,D,kind", SEL_CASES, ids=lambda v: str(v) if not isinstance(v, DEConfig) else v.parameter)
+def test_multi_cta_selection_and_sort_order_equal_single(dev, monkeypatch, cfg, P, D, kind):
+    """The multi-CTA selection (decoupled look-back over ticketed CTAs, epoch-tagged archive
+    owners resolved in the apply kernel, adapter kernel) and the bitonic top-p order against the
+    single-CTA scan and the O(P^2) rank kernel: populations, fitness, archive and adapter
+    memories bit-identical over 15 generations.  The population carries ties, -0.0 / +0.0 and NaN
+    fitness (a clipped sphere at the bound: many equal values; NaN rows are never replaced)."""
+    o, m = O.shift_rotation(5, D)
+    prob = evb.ProblemInstance.base(getattr(evb.BaseKind, kind), o, m, 0.0)
+    init = None
+    runs = []
+    for fast in (True, False):
+        for k in ("EVB_DE_SELECT_MULTI", "EVB_DE_ORDER_RANK"):
+            monkeypatch.delenv(k, raising=False)
+        if fast:
+            monkeypatch.setenv("EVB_DE_SELECT_MULTI", "1")
+        else:
+            monkeypatch.setenv("EVB_DE_ORDER_RANK", "1")
+        eng = DEEngine(cfg, P, D)
+        rng = Rng.philox(0x5E1)
+        pop = torch.empty((P, D), dtype=torch.float64, device=dev)
+        if init is None:
+            eng.init_population(pop, -100.0, 100.0, rng)
+            fit = dev_eval(prob, pop, dev)
+            f = fit.cpu().numpy()
+            f[3] = np.nan
+            f[7] = -0.0
+            f[8] = 0.0
+            f[10:14] = f[20]  # ties
+            init = (pop.clone(), torch.from_numpy(f).to(dev), rng.state()["generation"])
+        else:
+            rng.set_generation(init[2])
+        pop.copy_(init[0])
+        fit = init[1].clone()
+        for _ in range(15):
+            eng.generation(prob, pop, fit, -100.0, 100.0, rng)
+        torch.cuda.synchronize()
+        runs.append((pop.cpu().numpy(), fit.cpu().numpy(), eng.get_state(), eng.last_draws()))
+    (p0, f0, s0, d0), (p1, f1, s1, d1) = runs
+    assert np.array_equal(d0["idx"], d1["idx"])
+    assert np.array_equal(p0, p1)
+    assert np.array_equal(f0, f1, equal_nan=True)
+    assert s0["archive_size"] == s1["archive_size"]
+    assert np.array_equal(s0["archive"], s1["archive"])
+    assert np.array_equal(s0["memory_f"], s1["memory_f"]) and np.array_equal(s0["memory_cr"], s1["memory_cr"])
+    assert s0["write_index"] == s1["write_index"]
