@@ -117,21 +117,7 @@ template <>
 __device__ __forceinline__ double epi_cos2pi<double, true>(double v) { return cos(__dmul_rn(two_pi_v<double>(), v)); }
 template <>
 __device__ __forceinline__ double epi_cos2pi<double, false>(double v) {
-  const double t = __dsub_rn(__dadd_rn(v, 0x1.8p52), 0x1.8p52);  // rint(v) for |v| < 2^51
-  const double r = __dsub_rn(v, t);
-  const double u = __dmul_rn(r, r);
-  double c = -0.0002900600501912893;
-  c = fma(c, u, 0.003758590561310354);
-  c = fma(c, u, -0.03637490036340231);
-  c = fma(c, u, 0.28200407958316315);
-  c = fma(c, u, -1.7143904138098518);
-  c = fma(c, u, 7.903536340077173);
-  c = fma(c, u, -26.42625678121189);
-  c = fma(c, u, 60.24464137178173);
-  c = fma(c, u, -85.45681720669127);
-  c = fma(c, u, 64.93939402266825);
-  c = fma(c, u, -19.739208802178716);
-  return fma(c, u, 1.0);
+  return cos2pi_fast(v);
 }
 // arguments the fast form may not take (fp64 only): |v| >= 2^16, inf (NaN passes through it)
 template <typename T>

@@ -25,6 +25,7 @@
 
 #include "evb_internal.cuh"
 #include "evb_math.cuh"
+#include "ptx.cuh"
 #include "rng.cuh"
 #include "recorder.cuh"
 
@@ -83,6 +84,8 @@ struct runs_args {
   int split;             // CTAs per run (1, or a 2-CTA cluster that splits every evaluation)
   int resident;          // all rotations / shifts of a run staged in shared memory once
   int n_mat;             // max components over the runs (resident slots)
+  int tc;                // tensor-core (DMMA) dots with resident operands
+  int tc_epi;            // tc: warp-parallel distance / base-value sums and the fast cos(2 pi z)
 };
 
 __device__ __forceinline__ double clip_or_mid(double v, double target, double lb, double ub, int repair) {
@@ -140,14 +143,78 @@ __device__ __forceinline__ void dot_rows(const double* __restrict__ m, const dou
     if (EXACT || q < n) sZ[(i0 + q * G) * D + r] = acc[q];
 }
 
+// K3 on the FP64 tensor core: z[i][r] = sum_k s[i][k] M[r][k] for the R rows of sS by DMMA
+// m8n8k4 (the survey's K3; problems/instance.hpp:60-76, 116-174 per component).  sS is RP x KS and
+// M is NP8 x KS (RP, NP8 = multiples of 8; KS = round_up(D, 8) with KS % 16 == 8, so a quarter
+// warp's 16-byte fragment loads hit 8 distinct 16-byte bank groups); pad rows / columns hold zeros.
+// Inside each 8-deep k slice lane (g, t) feeds k = 2t at the first step and 2t + 1 at the second
+// (one LDS.128 per operand per two steps; A and B use the same k permutation).  Warp task = 8 rows
+// x 16 columns (one A fragment, two B fragments).  The accumulation order differs from the
+// reference's sequential one (fitness within ~1e-15 relative; selections equal except flagged
+// near-ties).
+__device__ __forceinline__ void dmma_rows(const double* __restrict__ sS, const double* __restrict__ sM, int R, int D,
+                                          int KS, double* __restrict__ sZ) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int mt = (R + 7) >> 3, nt = (D + 15) >> 4;
+  for (int task = warp; task < mt * nt; task += nwarps) {
+    const int m0 = (task / nt) << 3, n0 = (task % nt) << 4;
+    const bool two = n0 + 8 < D;  // warp-uniform
+    double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+    const double* pa = sS + (m0 + g) * KS + 2 * t;
+    const double* pb = sM + (n0 + g) * KS + 2 * t;
+    if (two) {
+      const double* pb1 = pb + 8 * KS;
+#pragma unroll 4
+      for (int k0 = 0; k0 < KS; k0 += 8) {
+        const double2 a = *reinterpret_cast<const double2*>(pa + k0);
+        const double2 b0 = *reinterpret_cast<const double2*>(pb + k0);
+        const double2 b1 = *reinterpret_cast<const double2*>(pb1 + k0);
+        ptx::dmma_8x8x4(c00, c01, a.x, b0.x);
+        ptx::dmma_8x8x4(c10, c11, a.x, b1.x);
+        ptx::dmma_8x8x4(c00, c01, a.y, b0.y);
+        ptx::dmma_8x8x4(c10, c11, a.y, b1.y);
+      }
+    } else {
+#pragma unroll 4
+      for (int k0 = 0; k0 < KS; k0 += 8) {
+        const double2 a = *reinterpret_cast<const double2*>(pa + k0);
+        const double2 b0 = *reinterpret_cast<const double2*>(pb + k0);
+        ptx::dmma_8x8x4(c00, c01, a.x, b0.x);
+        ptx::dmma_8x8x4(c00, c01, a.y, b0.y);
+      }
+    }
+    const int row = m0 + g;
+    if (row < R) {
+      const int c0 = n0 + 2 * t;
+      if (c0 < D) sZ[row * D + c0] = c00;
+      if (c0 + 1 < D) sZ[row * D + c0 + 1] = c01;
+      if (two) {
+        if (c0 + 8 < D) sZ[row * D + c0 + 8] = c10;
+        if (c0 + 9 < D) sZ[row * D + c0 + 9] = c11;
+      }
+    }
+  }
+}
+
+// tensor-core layout of the resident operands (dmma_rows)
+__host__ __device__ __forceinline__ int tc_ks(int D) {
+  const int k = (D + 7) / 8 * 8;
+  return (k % 16 == 8) ? k : k + 8;
+}
+__host__ __device__ __forceinline__ int round8(int v) { return (v + 7) / 8 * 8; }
+
+// KS > 0: tensor-core dots (dmma_rows; resident operands in the tc layout, sS stride KS with
+// zero pads), else exact-order dots (dot_rows; M stride S, sS stride D)
 __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int D, int S, double* sMbase,
                               double* sZ, double* sS, double* sObase, double* sFk, double* sDist, double* f,
-                              bool resident, phase_clock& pc) {
+                              bool resident, int KS, int fast_epi, phase_clock& pc) {
   const int ncomp = pr.n_comp > 0 ? pr.n_comp : 1;
+  const int SS = KS > 0 ? KS : D;  // row stride of sS
   for (int c = 0; c < ncomp; ++c) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
     // resident: every component's M and o were staged once at kernel start
-    double* sM = resident ? sMbase + size_t(c) * D * S : sMbase;
+    double* sM = resident ? sMbase + size_t(c) * (KS > 0 ? size_t(round8(D)) * KS : size_t(D) * S) : sMbase;
     double* sO = resident ? sObase + size_t(c) * D : sObase;
     if (!resident) {
       for (int r = warp; r < D; r += nwarps)
@@ -155,24 +222,61 @@ __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int
       for (int e = threadIdx.x; e < D; e += blockDim.x) sO[e] = pr.shift[c][e];
       __syncthreads();
     }
-    for (int i = warp; i < P; i += nwarps)
-      for (int k = lane; k < D; k += 32) sS[i * D + k] = __dsub_rn(X[i * D + k], sO[k]);
+    if (KS > 0) {  // all RP x KS entries: the pads are zero for the tensor-core tiles
+      const int RP = round8(P);
+      for (int e = threadIdx.x; e < RP * KS; e += blockDim.x) {
+        const int i = e / KS, k = e - i * KS;
+        sS[e] = (i < P && k < D) ? __dsub_rn(X[i * D + k], sO[k]) : 0.0;
+      }
+    } else {
+      for (int i = warp; i < P; i += nwarps)
+        for (int k = lane; k < D; k += 32) sS[i * D + k] = __dsub_rn(X[i * D + k], sO[k]);
+    }
     __syncthreads();
     pc.mark(2);
     {
-      // dist^2 in double (problems/instance.hpp:127-134): one sequential chain per individual
-      if (pr.n_comp > 0)
+      // dist^2 in double (problems/instance.hpp:127-134): one sequential chain per individual;
+      // the tensor-core path (a tolerance path already) takes a warp per individual and a
+      // shuffle tree (the weights it feeds are relative: ~1e-16)
+      if (pr.n_comp > 0 && KS > 0 && fast_epi) {
+        // two levels: thread (i, q) sums the 8 elements [8q, 8q + 8) of row i, then thread i sums
+        // its row's partials (sFk as scratch: its slots are written after this)
+        const int nq = (D + 7) >> 3;
+        double* part = sZ;  // R x nq partials (sZ is written by the dots below)
+        for (int e = threadIdx.x; e < P * nq; e += blockDim.x) {
+          const int i = e / nq, q = e - i * nq;
+          const double* si = sS + i * SS + 8 * q;
+          double d2 = 0.0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (8 * q + j < D) d2 = fma(si[j], si[j], d2);
+          part[e] = d2;
+        }
+        __syncthreads();
         for (int i = threadIdx.x; i < P; i += blockDim.x) {
           double d2 = 0.0;
-          const double* si = sS + i * D;
+          for (int q = 0; q < nq; ++q) d2 += part[i * nq + q];
+          sDist[i * kRunsMaxComp + c] = d2;
+        }
+        __syncthreads();
+      } else if (pr.n_comp > 0)
+        for (int i = threadIdx.x; i < P; i += blockDim.x) {
+          double d2 = 0.0;
+          const double* si = sS + i * SS;
           for (int j = 0; j < D; ++j) d2 = __dadd_rn(d2, __dmul_rn(si[j], si[j]));
           sDist[i * kRunsMaxComp + c] = d2;
         }
+      if (pc.acc) {  // profiling only: separate the distance chains from the dots
+        __syncthreads();
+        pc.mark(9);
+      }
       // thread t owns row r = t % D for individual group g = t / D (G groups): individuals g,
       // g + G, ... — rows over consecutive lanes (odd stride: conflict-free), every chain real
       const int G = max(1, int(blockDim.x) / D);
       const int t = int(threadIdx.x);
-      if (t < G * D) {
+      if (KS > 0) {
+        dmma_rows(sS, sM, P, D, KS, sZ);
+      } else if (t < G * D) {
         const int r = t % D, g = t / D;
         const double* m = sM + r * S;
         for (int i0 = g; i0 < P; i0 += 8 * G) {
@@ -193,7 +297,16 @@ __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int
       continue;
     }
     const int kind = pr.kind[c];
-    if (kind_has_pre(kind)) {  // transcendental terms in parallel over all P*D elements (into sS)
+    if (KS > 0 && fast_epi && (kind == EVB_RASTRIGIN || kind == EVB_ACKLEY)) {
+      // tensor-core path: the transcendental terms with cos2pi_fast (the reference's formulas),
+      // element-parallel into sS; the sequential sums below are the reference's order
+      for (int e = threadIdx.x; e < P * D; e += blockDim.x) {
+        const double v = sZ[e];
+        const double cz = cos2pi_fast_ok(v) ? cos2pi_fast(v) : cos(__dmul_rn(two_pi_v<double>(), v));
+        sS[e] = kind == EVB_ACKLEY ? cz : __dadd_rn(__dsub_rn(__dmul_rn(v, v), __dmul_rn(10.0, cz)), 10.0);
+      }
+      __syncthreads();
+    } else if (kind_has_pre(kind)) {  // transcendental terms in parallel over all P*D elements (into sS)
       for (int e = threadIdx.x; e < P * D; e += blockDim.x) {
         const int i = e / D, k = e - i * D;
         const double* zr = sZ + i * D;
@@ -213,40 +326,72 @@ __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int
     __syncthreads();
     pc.mark(5);
   }
+  // the per-component raw weights (1/d) exp(-d^2 / (2 D sigma^2)) are independent: one thread per
+  // (individual, component) into sS (free after the last component), bit-identical to the
+  // per-individual loop; the normalisation below stays per individual
+  double* sWraw = sS;  // R x 4 fits in sS when D >= 4
+  const bool par_w = pr.n_comp > 0 && D >= kRunsMaxComp;
+  if (par_w) {
+    for (int e = threadIdx.x; e < P * pr.n_comp; e += blockDim.x) {
+      const int i = e / pr.n_comp, k = e - i * pr.n_comp;
+      const double dk = sDist[i * kRunsMaxComp + k];
+      sWraw[i * kRunsMaxComp + k] =
+          dk == 0.0 ? -1.0
+                    : __dmul_rn(__ddiv_rn(1.0, __dsqrt_rn(dk)),
+                                exp(__ddiv_rn(-dk, __dmul_rn(__dmul_rn(__dmul_rn(2.0, double(D)), pr.sigma[k]), pr.sigma[k]))));
+    }
+    __syncthreads();
+  }
   for (int i = threadIdx.x; i < P; i += blockDim.x) {
     if (pr.n_comp == 0) {
       f[i] = __dadd_rn(sFk[i * kRunsMaxComp], pr.bias);
       continue;
     }
-    // weights exactly as problems/instance.hpp:135-171
+    // weights exactly as problems/instance.hpp:135-171 (loops over the fixed kRunsMaxComp slots,
+    // unrolled, so w[] stays in registers)
     const double* dist = sDist + i * kRunsMaxComp;
+    const int nc = pr.n_comp;
     double w[kRunsMaxComp];
     int zero_count = 0;
-    for (int k = 0; k < pr.n_comp; ++k) {
-      if (dist[k] == 0.0) {
-        ++zero_count;
-        w[k] = -1.0;
+#pragma unroll
+    for (int k = 0; k < kRunsMaxComp; ++k) {
+      w[k] = 0.0;
+      if (k >= nc) continue;
+      if (par_w) {
+        w[k] = sWraw[i * kRunsMaxComp + k];
       } else {
-        w[k] = __dmul_rn(__ddiv_rn(1.0, __dsqrt_rn(dist[k])),
-                         exp(__ddiv_rn(-dist[k], __dmul_rn(__dmul_rn(__dmul_rn(2.0, double(D)), pr.sigma[k]), pr.sigma[k]))));
+        const double dk = dist[k];
+        w[k] = dk == 0.0 ? -1.0
+                         : __dmul_rn(__ddiv_rn(1.0, __dsqrt_rn(dk)),
+                                     exp(__ddiv_rn(-dk, __dmul_rn(__dmul_rn(__dmul_rn(2.0, double(D)), pr.sigma[k]),
+                                                                  pr.sigma[k]))));
       }
+      if (w[k] < 0.0) ++zero_count;
     }
     double wsum = 0.0;
     if (zero_count > 0) {
-      for (int k = 0; k < pr.n_comp; ++k) w[k] = w[k] < 0.0 ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < kRunsMaxComp; ++k)
+        if (k < nc) w[k] = w[k] < 0.0 ? 1.0 : 0.0;
       wsum = double(zero_count);
     } else {
-      for (int k = 0; k < pr.n_comp; ++k) wsum = __dadd_rn(wsum, w[k]);
+#pragma unroll
+      for (int k = 0; k < kRunsMaxComp; ++k)
+        if (k < nc) wsum = __dadd_rn(wsum, w[k]);
       if (wsum == 0.0) {
         int nearest = 0;
-        for (int k = 1; k < pr.n_comp; ++k)
+        for (int k = 1; k < nc; ++k)
           if (dist[k] < dist[nearest]) nearest = k;
-        w[nearest] = 1.0;
+#pragma unroll
+        for (int k = 0; k < kRunsMaxComp; ++k)
+          if (k == nearest) w[k] = 1.0;
         wsum = 1.0;
       }
     }
     double value = 0.0;
-    for (int k = 0; k < pr.n_comp; ++k) {
+#pragma unroll
+    for (int k = 0; k < kRunsMaxComp; ++k) {
+      if (k >= nc) continue;
       const double wk = __ddiv_rn(w[k], wsum);
       if (wk == 0.0) continue;
       value = __dadd_rn(value, __dmul_rn(wk, __dadd_rn(__dmul_rn(pr.lambda[k], sFk[i * kRunsMaxComp + k]), pr.cbias[k])));
@@ -273,24 +418,41 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
   const int p1 = a.split == 2 ? min(P, p0 + half) : P;
   const int R = p1 - p0 > 0 ? (a.split == 2 ? half : P) : 1;  // rows this CTA evaluates
   const int NM = a.resident ? a.n_mat : 1;     // rotation / shift slots
+  const int KS = a.tc ? tc_ks(D) : 0;          // tensor-core dots: operand row stride
+  const size_t m_len = a.tc ? size_t(round8(D)) * KS : size_t(D) * S;  // one rotation
+  const size_t s_len = a.tc ? size_t(round8(R)) * KS : size_t(R) * D;  // x - o
+  auto even = [](size_t n) { return (n + 1) & ~size_t(1); };           // 16-byte sections
   double* sPop = sm;                           // P x D
-  double* sTrial = sPop + P * D;               // P x D
-  double* sM = sTrial + P * D;                 // NM x D x S
-  double* sZ = sM + size_t(NM) * D * S;        // R x D
-  double* sS = sZ + R * D;                     // R x D  (x - o of the current component)
-  double* sO = sS + R * D;                     // NM x D
+  double* sTrial = sPop + even(size_t(P) * D); // P x D
+  double* sM = sTrial + even(size_t(P) * D);   // NM rotations
+  double* sZ = sM + even(NM * m_len);          // R x D
+  double* sS = sZ + even(size_t(R) * D);       // x - o of the current component (tc: RP x KS)
+  double* sO = sS + even(s_len);               // NM x D
   double* sFit = sO + NM * D;                  // P
   double* sTfit2 = sFit + P;                   // 2 x P (generation parity)
   double* sFk = sTfit2 + 2 * P;                // R x 4
   double* sDist = sFk + R * kRunsMaxComp;      // R x 4
   int* sIdx = reinterpret_cast<int*>(sDist + R * kRunsMaxComp);  // P x 4 (a, b, c, word offset)
-  const run_problem pr = a.probs[run];
+  // the run's problem descriptor in shared memory (a local-memory copy lived in L1, which the
+  // ~200 KB shared-memory carve-out leaves nearly empty: every field access missed to L2)
+  __shared__ run_problem s_pr;
+  for (int e = threadIdx.x; e < int(sizeof(run_problem) / 4); e += blockDim.x)
+    reinterpret_cast<int*>(&s_pr)[e] = reinterpret_cast<const int*>(a.probs + run)[e];
+  __syncthreads();
+  const run_problem& pr = s_pr;
   if (a.resident) {  // stage every component's rotation and shift once for all generations
     const int nc = pr.n_comp > 0 ? pr.n_comp : 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
     for (int c = 0; c < nc; ++c) {
-      for (int r = warp; r < D; r += nwarps)
-        for (int k = lane; k < D; k += 32) sM[(size_t(c) * D + r) * S + k] = pr.rot[c][r * pr.ld + k];
+      if (a.tc) {  // round8(D) x KS, zero pads
+        const int NP8 = round8(D);
+        for (int r = warp; r < NP8; r += nwarps)
+          for (int k = lane; k < KS; k += 32)
+            sM[c * m_len + size_t(r) * KS + k] = (r < D && k < D) ? pr.rot[c][r * pr.ld + k] : 0.0;
+      } else {
+        for (int r = warp; r < D; r += nwarps)
+          for (int k = lane; k < D; k += 32) sM[(size_t(c) * D + r) * S + k] = pr.rot[c][r * pr.ld + k];
+      }
       for (int e = threadIdx.x; e < D; e += blockDim.x) sO[c * D + e] = pr.shift[c][e];
     }
     __syncthreads();
@@ -301,7 +463,7 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
   phase_clock pc{blockIdx.x == 0 ? a.prof : nullptr, 0};
   // evaluate rows [p0, p1) of X into f
   auto evaluate = [&](const double* X, double* f) {
-    runs_evaluate(pr, X + size_t(p0) * D, p1 - p0, D, S, sM, sZ, sS, sO, sFk, sDist, f + p0, a.resident != 0, pc);
+    runs_evaluate(pr, X + size_t(p0) * D, p1 - p0, D, S, sM, sZ, sS, sO, sFk, sDist, f + p0, a.resident != 0, KS, a.tc_epi, pc);
   };
   // (split) publish this CTA's rows [p0, p1) of the given arrays into the peer's copies
   auto publish = [&](double* rows, int row_len) {
@@ -447,11 +609,14 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
   if (a.split == 2) cg::this_cluster().sync();  // no CTA leaves while its peer may still write into it
 }
 
-size_t runs_smem(int P, int D, int split = 1, int n_mat = 1) {
+size_t runs_smem(int P, int D, int split = 1, int n_mat = 1, int tc = 0) {
   const int S = (D % 2 == 1) ? D : D + 1;
   const size_t R = split == 2 ? size_t((P + 1) / 2) : size_t(P);
-  return sizeof(double) * (size_t(2) * P * D + size_t(n_mat) * D * S + 2 * R * D + size_t(n_mat) * D + 3 * P +
-                           2 * R * kRunsMaxComp) +
+  auto even = [](size_t n) { return (n + 1) & ~size_t(1); };
+  const size_t m_len = tc ? size_t(round8(D)) * tc_ks(D) : size_t(D) * S;
+  const size_t s_len = tc ? size_t(round8(int(R))) * tc_ks(D) : R * D;
+  return sizeof(double) * (2 * even(size_t(P) * D) + even(size_t(n_mat) * m_len) + even(R * D) + even(s_len) +
+                           size_t(n_mat) * D + 3 * P + 2 * R * kRunsMaxComp) +
          sizeof(int) * 4 * P + 64;
 }
 
@@ -579,7 +744,14 @@ extern "C" int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int 
     for (const run_problem& q : rp) a.n_mat = std::max(a.n_mat, std::max(1, q.n_comp));
     static const char* res_env = std::getenv("EVB_RUNS_RESIDENT");
     a.resident = (!res_env || std::atoi(res_env) != 0) && runs_smem(pop_size, dim, a.split, a.n_mat) <= 227 * 1024;
-    const size_t smem = runs_smem(pop_size, dim, a.split, a.resident ? a.n_mat : 1);
+    // DMMA dots (K3) for the resident layout when it fits and D is large enough for the tiles to
+    // pay (EVB_RUNS_TC=0|1 overrides); small D keeps the exact-order dots
+    static const char* tc_env = std::getenv("EVB_RUNS_TC");
+    a.tc = a.resident && runs_smem(pop_size, dim, a.split, a.n_mat, 1) <= 227 * 1024 &&
+           (tc_env ? std::atoi(tc_env) != 0 : dim >= 32);
+    static const char* epi_env = std::getenv("EVB_RUNS_TC_EPI");
+    a.tc_epi = a.tc && (epi_env ? std::atoi(epi_env) != 0 : 1);
+    const size_t smem = runs_smem(pop_size, dim, a.split, a.resident ? a.n_mat : 1, a.tc);
     require(smem <= 227 * 1024, "de_runs: run state does not fit in shared memory");
     EVB_CUDA(cudaFuncSetAttribute(de_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     static const bool prof = std::getenv("EVB_RUNS_PROFILE") != nullptr;
@@ -615,9 +787,9 @@ extern "C" int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int 
       unsigned long long h[16];
       EVB_CUDA(cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost));
       cudaFree(dprof);
-      const char* names[] = {"draws", "trial", "x-o", "dist+dot", "pre", "base", "weights", "exchange", "select"};
+      const char* names[] = {"draws", "trial", "x-o", "dot", "pre", "base", "weights", "exchange", "select", "dist"};
       std::string line = "[evb runs] cycles/generation:";
-      for (int k = 0; k < 9; ++k) line += std::string(" ") + names[k] + "=" + std::to_string(h[k] / std::max(1, generations));
+      for (int k = 0; k < 10; ++k) line += std::string(" ") + names[k] + "=" + std::to_string(h[k] / std::max(1, generations));
       std::fprintf(stderr, "%s\n", line.c_str());
     }
     cudaFree(dprobs);
