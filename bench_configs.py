@@ -39,7 +39,8 @@ from paper_2505_17430_b200.pso import PSOEngine, config3 as pso_config3  # noqa:
 from paper_2505_17430_b200.runs import de_runs, run_keys  # noqa: E402
 
 DEV = torch.device("cuda:0")
-K2_TILE_N = 64  # N of the fp32 kernel's tcgen05.mma tiles (eval_gemm.cu eval_f32_umma_kernel)
+K2_TILE_N = 128  # N of the fp32 kernel's tcgen05.mma tiles (eval_gemm.cu eval_f32_umma_sk_kernel)
+K2_KERNEL = "eval_f32_umma_sk_kernel"
 
 
 def hbm_peak():
@@ -237,11 +238,12 @@ def config1_fp32():
     return {
         "metric": "objective evals/sec (D=1000, pop 1024, fp32)", "value": 3 * P / (step_ms * 1e-3),
         "unit": "evals/s", "ms_per_batch": batch_ms,
-        "how": "3 x evaluate_batch fp32 per step (eval_f32_umma_kernel: tcgen05 kind::tf32, 3xTF32 split, "
-               "TMEM accumulators); CUDA events per launch; L2 flushed between steps",
+        "how": "3 x evaluate_batch fp32 per step (eval_f32_umma_sk_kernel: tcgen05 kind::tf32 128x128 tiles, "
+               "3xTF32 split in-kernel, TMEM accumulators, K halves as a 2-CTA cluster exchanging z over DSMEM, "
+               "M pairs multicasting the rotation slices); CUDA events per launch; L2 flushed between steps",
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s (fp32-equivalent)",
-                     "frac": achieved / peak, "traffic": dram_traffic("eval_f32_umma_kernel"),
-                     "kernel": "eval_f32_umma_kernel",
+                     "frac": achieved / peak, "traffic": dram_traffic(K2_KERNEL),
+                     "kernel": K2_KERNEL,
                      "peak_source": f"in-run tcgen05.mma kind::tf32 probe at N={K2_TILE_N}: {tf32:.1f} TFLOP/s, "
                                     f"divided by 3 (3xTF32: three tensor-core products per fp32 product); "
                                     f"at N=256 the probe reads {tf32_256:.1f}",

@@ -84,6 +84,7 @@ struct fused_params {
   int kgate_rows;   // > 0: rows >= kgate_rows wait on the second gate group kgate[kgate_n + c]
   int tiles_nfast;  // multi kernel: blockIdx.x walks column tiles (row blocks form the waves)
   unsigned long long* dbg_ts;  // EVB_K1_TIMELINE=1 (tuning aid): per-CTA globaltimer phase stamps
+  int dbg_skip;  // EVB_K2_SKIP (tuning aid, wrong results): bit 0 = no S split, bit 1 = no MMAs
 };
 
 // cosine of the fused epilogue: library cos for fp64.  fp32 (a tolerance path: 3xTF32 / FFMA
@@ -1099,6 +1100,335 @@ __global__ void __launch_bounds__(umma_cfg<BN, FUSE>::THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------------------
+// K2 on tcgen05, split-K (the default fp32 tensor-core path).  128 x BN output tile per CTA with
+// BN = 128 (N = 128 MMAs run at the tensor core's full rate; N = 64 reached ~60% of it), and the
+// K range split over gridDim.z CTAs so that the config-1 grid (8 x 8 tiles x 2 halves = 128 CTAs)
+// fills the SMs.  Per 32-float K slice: TMA brings X (128 rows, into the S_hi slot, own barrier)
+// and M_hi / M_lo (BN rows); the 8 epilogue warps split X into S_hi / S_lo in place (as the
+// FUSE kernel above) while the single MMA thread issues 4 K-steps x 3 products.  After the
+// mainloop each CTA holds z_k = main + corrections of its K half in TMEM.  The two K halves of a
+// tile form a 2-CTA cluster and split the epilogue by columns: each CTA sends its z_k of the
+// peer's 64 columns into the peer's receive buffer (DSMEM), one cluster barrier, then adds the
+// received half to its own (z = z_0 + z_1: fp add is commutative, the same in both CTAs) and runs
+// the usual epilogue on its 64 columns (terms, per-row channel sums, column-block partials,
+// last-CTA finalisation).  Deterministic, no float atomics.
+template <int BN>
+struct umma_sk_cfg {
+  static constexpr int BM = 128;
+  static constexpr int KB = 32;                   // floats per K slice (one 128-byte swizzle row)
+  static constexpr int X_BYTES = BM * 128;        // one X slice (TMA), split in place into S_hi
+  static constexpr int A_BYTES = 2 * BM * 128;    // S_hi (over X) + S_lo
+  static constexpr int B_BYTES = 2 * BN * 128;    // M_hi + M_lo of one slice (TMA, multicast pair)
+  // A and B rings apart, so X slices (and their split) run up to NA slices ahead of the MMAs
+  static constexpr int NA = 4, NB = (BN == 128 ? 3 : 2);
+  static constexpr int A_OFF = 0, B_OFF = NA * A_BYTES, O_OFF = B_OFF + NB * B_BYTES;
+  static constexpr int RING_BYTES = O_OFF + NA * KB * 4;  // + the shift slice of each A stage
+  static constexpr int NBAR = 3 * NA + 2 * NB + 1;
+  static constexpr int THREADS = 11 * 32;  // X producer, MMA, 8 split / epilogue warps, B producer
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int RECV_BYTES = BM * (BN / 2) * 4;  // the peer's z_k of the owned columns (A ring)
+  static constexpr int SMEM = RING_BYTES + 1024 + NBAR * 8 + 64;
+  static_assert(RECV_BYTES + 8192 <= NA * A_BYTES, "receive buffer + epilogue scratch in the drained A ring");
+  static_assert(SMEM <= 227 * 1024, "shared memory");
+};
+
+template <int BN>
+__global__ void __launch_bounds__(umma_sk_cfg<BN>::THREADS, 1)
+    eval_f32_umma_sk_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmMhi,
+                            const __grid_constant__ CUtensorMap tmMlo, const fused_params<float> p) {
+  using C = umma_sk_cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
+  uint64_t* xfull = reinterpret_cast<uint64_t*>(smem + C::RING_BYTES);  // X + shift slice landed
+  uint64_t* afull = xfull + C::NA;                                      // S_hi / S_lo formed
+  uint64_t* aempty = afull + C::NA;                                     // the MMAs read the stage
+  uint64_t* bfull = aempty + C::NA;
+  uint64_t* bempty = bfull + C::NB;
+  uint64_t* accfull = bempty + C::NB;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accfull + 1);
+  int* flags = reinterpret_cast<int*>(tmem_slot + 1);  // [1]: last column block of the row block
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * C::BM, n0 = blockIdx.y * BN;
+  const int KT_all = (p.D + C::KB - 1) / C::KB;
+  const int nsk = gridDim.z, kz = blockIdx.z;
+  // cluster (2 along M) x (gridDim.z along K): rank = mx + 2 kz.  The M pair shares every B slice
+  // (each CTA loads half of its rows and multicasts it to both); the K pair exchanges z halves.
+  const unsigned crank = ptx::cluster_ctarank();
+  const unsigned mx = crank & 1u;
+  const uint16_t pair_mask = uint16_t(3u << (crank & ~1u));
+  const int kb0 = int((int64_t(KT_all) * kz) / nsk), kb1 = int((int64_t(KT_all) * (kz + 1)) / nsk);
+  const int KT = kb1 - kb0;
+  unsigned long long* ts =
+      p.dbg_ts ? p.dbg_ts + 8 * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) : nullptr;
+  auto stamp = [&](int i) {  // EVB_K1_TIMELINE=1 (tuning aid)
+    if (ts) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      ts[i] = t;
+    }
+  };
+  if (threadIdx.x == 0) stamp(0);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::NA; ++s) {
+      ptx::mbar_init(&xfull[s], 1);
+      ptx::mbar_init(&afull[s], 8);
+      ptx::mbar_init(&aempty[s], 1);
+    }
+    for (int s = 0; s < C::NB; ++s) {
+      ptx::mbar_init(&bfull[s], 1);
+      ptx::mbar_init(&bempty[s], 2);  // both CTAs of the M pair consumed the slot
+    }
+    ptx::mbar_init(accfull, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) umma::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  umma::fence_before();
+  ptx::cluster_sync_all();  // every CTA's barriers exist before the first multicast / remote commit
+  umma::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  ptx::griddep_wait();  // PDL: barrier init and TMEM allocation overlap the predecessor's tail
+  ptx::griddep_launch_dependents();
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- X producer: X slice + its 32 shift values ----------------
+      ptx::prefetch_tma(&tmX);
+      for (int kb = 0; kb < KT; ++kb) {
+        const int s = kb % C::NA;
+        if (kb >= C::NA) ptx::mbar_wait(&aempty[s], ((kb / C::NA) - 1) & 1);
+        ptx::mbar_arrive_expect_tx(&xfull[s], C::X_BYTES + C::KB * 4);
+        ptx::tma_load_2d(smem + C::A_OFF + s * C::A_BYTES, &tmX, &xfull[s], (kb0 + kb) * C::KB, m0);
+        ptx::bulk_load(smem + C::O_OFF + s * C::KB * 4, p.shift + size_t(kb0 + kb) * C::KB, C::KB * 4, &xfull[s]);
+      }
+    }
+  } else if (warp == 10) {
+    if (lane == 0) {  // ---------------- B producer (M_hi, M_lo) ----------------
+      ptx::prefetch_tma(&tmMhi);
+      ptx::prefetch_tma(&tmMlo);
+      for (int kb = 0; kb < KT; ++kb) {
+        const int s = kb % C::NB;
+        if (kb >= C::NB) ptx::mbar_wait(&bempty[s], ((kb / C::NB) - 1) & 1);
+        uint8_t* st = smem + C::B_OFF + s * C::B_BYTES + mx * (BN / 2) * 128;  // this CTA's half of the rows
+        ptx::mbar_arrive_expect_tx(&bfull[s], C::B_BYTES);  // both halves land here
+        ptx::tma_load_2d_mc(st, &tmMhi, &bfull[s], (kb0 + kb) * C::KB, n0 + int(mx) * (BN / 2), pair_mask);
+        ptx::tma_load_2d_mc(st + C::B_BYTES / 2, &tmMlo, &bfull[s], (kb0 + kb) * C::KB, n0 + int(mx) * (BN / 2),
+                            pair_mask);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- single-thread MMA issuer ----------------
+      constexpr uint32_t idesc = umma::idesc_tf32(C::BM, BN);
+      const uint32_t base = ptx::smem_u32(smem);
+      const uint32_t tcorr = tmem + BN;
+      for (int kb = 0; kb < KT; ++kb) {
+        const int sa = kb % C::NA, sb = kb % C::NB;
+        ptx::mbar_wait(&afull[sa], (kb / C::NA) & 1);
+        ptx::mbar_wait(&bfull[sb], (kb / C::NB) & 1);
+        if (kb == 0) stamp(1);
+        umma::fence_after();
+        const uint32_t sa_hi = base + C::A_OFF + sa * C::A_BYTES, sa_lo = sa_hi + C::A_BYTES / 2;
+        const uint32_t sb_hi = base + C::B_OFF + sb * C::B_BYTES, sb_lo = sb_hi + C::B_BYTES / 2;
+#pragma unroll
+        for (int k = 0; k < C::KB / 8; ++k) {
+          if (p.dbg_skip & 2) break;
+          const uint32_t off = k * 32;
+          const uint32_t acc0 = (kb | k) ? 1u : 0u;
+          umma::mma_tf32(tmem, umma::smem_desc(sa_hi + off), umma::smem_desc(sb_hi + off), idesc, acc0);
+          umma::mma_tf32(tcorr, umma::smem_desc(sa_lo + off), umma::smem_desc(sb_hi + off), idesc, acc0);
+          umma::mma_tf32(tcorr, umma::smem_desc(sa_hi + off), umma::smem_desc(sb_lo + off), idesc, 1u);
+        }
+        umma::commit(&aempty[sa]);
+        umma::commit_mc(&bempty[sb], pair_mask);  // the slot is freed in both CTAs of the M pair
+      }
+      umma::commit(accfull);
+    }
+  } else {
+    // ---------------- split / epilogue warps 2..9 ----------------
+    const int ew = warp - 2, half = ew >> 2;
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const int row = m0 + r;
+    const int etid = threadIdx.x - 64;
+    // S = X - o, S_hi = rna_tf32(S) over X, S_lo = rna_tf32(S - S_hi) into the stage's lo half
+    // (same SWIZZLE_128B positions: chunk q of row q / 8 holds logical chunk (q & 7) ^ (row & 7))
+    for (int kb = 0; kb < KT; ++kb) {
+      const int sa = kb % C::NA;
+      ptx::mbar_wait(&xfull[sa], (kb / C::NA) & 1);
+      float4* hi = reinterpret_cast<float4*>(smem + C::A_OFF + sa * C::A_BYTES);
+      float4* lo = reinterpret_cast<float4*>(smem + C::A_OFF + sa * C::A_BYTES + C::A_BYTES / 2);
+      const float4* osl = reinterpret_cast<const float4*>(smem + C::O_OFF + sa * C::KB * 4);
+      if (!(p.dbg_skip & 1)) {
+#pragma unroll
+        for (int u = 0; u < C::X_BYTES / 16 / 256; ++u) {
+          const int q = etid + u * 256;
+          const int rr = q >> 3, c = (q & 7) ^ (rr & 7);
+          const float4 x = hi[q];
+          const float4 o = osl[c];
+          auto split = [](float xq, float oq, float& hq, float& lq) {
+            const float sq = __fsub_rn(xq, oq);
+            hq = __uint_as_float(umma::rna_tf32_bits(sq));
+            lq = __uint_as_float(umma::rna_tf32_bits(__fsub_rn(sq, hq)));
+          };
+          float4 h, l;
+          split(x.x, o.x, h.x, l.x);
+          split(x.y, o.y, h.y, l.y);
+          split(x.z, o.z, h.z, l.z);
+          split(x.w, o.w, h.w, l.w);
+          hi[q] = h;
+          lo[q] = l;
+        }
+        ptx::fence_proxy_async();
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&afull[sa]);
+    }
+    ptx::mbar_wait_sleep(accfull, 0);
+    if (etid == 0) stamp(3);
+    umma::fence_after();
+    // Column ownership: with the K range split over a 2-CTA cluster (blockIdx.z = cluster rank),
+    // CTA kz finalises columns [kz * BN/2, (kz + 1) * BN/2) of the tile.  Each epilogue thread
+    // (TMEM lane quarter = 32 rows, column half h) sends its z_k of the other CTA's columns into
+    // the peer's receive buffer (DSMEM, 16-byte chunks XOR-swizzled by row), one cluster barrier,
+    // then adds the peer's z_k to its own for the columns it owns (z = z_0 + z_1).
+    const int OWN = BN / nsk;           // columns this CTA finalises
+    const int TW = OWN / 2;             // per thread (two threads per row)
+    const int own0 = kz * OWN;          // first owned column of the tile
+    const uint32_t tbase = tmem + (uint32_t(quarter * 32) << 16);
+    auto load16 = [&](int col, float (&v)[16]) {  // this CTA's z_k, tile columns [col, col + 16)
+      uint32_t a[16], b[16];
+      umma::tmem_ld16_raw(tbase + col, a);
+      umma::tmem_ld16_raw(tbase + BN + col, b);
+      umma::tmem_wait_ld();
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = __fadd_rn(__uint_as_float(a[q]), __uint_as_float(b[q]));
+    };
+    float* recv = reinterpret_cast<float*>(smem + C::A_OFF);  // [BM][BN/2] in the drained A ring (nsk == 2)
+    auto rchunk = [&](int rr, int ch16) { return rr * (BN / 2) + 4 * ((ch16 & ~7) | ((ch16 & 7) ^ (rr & 7))); };
+    if (nsk > 1) {
+      ptx::cluster_sync_all();  // both CTAs past their mainloops: the peer's A ring is drained
+      const int snd0 = (1 - kz) * OWN + half * TW;  // tile columns sent to the peer
+      const uint32_t peer = ptx::mapa(ptx::smem_u32(recv), crank ^ 2u);  // the other K half
+#pragma unroll 1
+      for (int c0 = 0; c0 < TW; c0 += 16) {
+        float v[16];
+        load16(snd0 + c0, v);
+#pragma unroll
+        for (int q = 0; q < 16; q += 4) {
+          const int ch16 = (half * TW + c0 + q) >> 2;  // 16-byte chunk in the peer's [BN/2] row
+          ptx::st_cluster_v4(peer + 4u * uint32_t(rchunk(r, ch16)), v[q], v[q + 1], v[q + 2], v[q + 3]);
+        }
+      }
+    }
+    if (nsk > 1) ptx::cluster_sync_all();  // every thread of both CTAs (warps 0-1 join below)
+    auto loadz = [&](int c0, float (&v)[16]) {  // z of owned columns [own0 + half*TW + c0, +16)
+      load16(own0 + half * TW + c0, v);
+      if (nsk > 1) {
+#pragma unroll
+        for (int q = 0; q < 16; q += 4) {
+          const float4 w = *reinterpret_cast<const float4*>(recv + rchunk(r, (half * TW + c0 + q) >> 2));
+          v[q] = __fadd_rn(v[q], w.x);
+          v[q + 1] = __fadd_rn(v[q + 1], w.y);
+          v[q + 2] = __fadd_rn(v[q + 2], w.z);
+          v[q + 3] = __fadd_rn(v[q + 3], w.w);
+        }
+      }
+    };
+    if (p.zbuf) {
+#pragma unroll 1
+      for (int c0 = 0; c0 < TW; c0 += 16) {
+        float v[16];
+        loadz(c0, v);
+        const int cb = n0 + own0 + half * TW + c0;
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          if (row < p.P && cb + q < p.D) p.zbuf[size_t(cb + q) * p.ldz + row] = v[q];
+      }
+    } else {
+      float* xs = reinterpret_cast<float*>(smem + C::A_OFF + C::RECV_BYTES);  // drained A ring: [half][ch][row]
+      for (int ch = 0; ch < p.n_ch; ++ch) {
+        const int term = p.ch_term[ch];
+        float acc = term_is_product(term) ? 1.f : 0.f;
+#pragma unroll 1
+        for (int c0 = 0; c0 < TW; c0 += 16) {
+          float v[16];
+          loadz(c0, v);
+          acc = accumulate16_rt<float>(term, acc, v, n0 + own0 + half * TW + c0, p.D, p.ell_w);
+        }
+        xs[(half * kMaxCh + ch) * C::BM + r] = acc;
+      }
+      ptx::named_bar_sync(1, 256);
+      const int pt = blockIdx.y * nsk + kz;  // partial slot of this CTA's column block
+      if (half == 0 && row < p.P)
+        for (int ch = 0; ch < p.n_ch; ++ch) {
+          const float a0 = xs[ch * C::BM + r], a1 = xs[(kMaxCh + ch) * C::BM + r];
+          const float v = term_is_product(p.ch_term[ch]) ? __fmul_rn(a0, a1) : __fadd_rn(a0, a1);
+          p.partial[(size_t(ch) * p.n_ntiles + pt) * p.P + row] = v;
+        }
+      ptx::named_bar_sync(1, 256);
+      if (etid == 0) {
+        stamp(4);
+        __threadfence();
+        const unsigned ticket = atomicAdd(&p.counters[blockIdx.x], 1u);
+        const int last = (ticket == unsigned(p.n_ntiles - 1)) ? 1 : 0;
+        if (last) __threadfence();
+        flags[1] = last;
+      }
+      ptx::named_bar_sync(1, 256);
+      if (flags[1]) {
+        auto chain = [&](int ch, int rw) {
+          const bool prod = term_is_product(p.ch_term[ch]);
+          const float* src = p.partial + size_t(ch) * p.n_ntiles * p.P + rw;
+          float v = __ldcg(src);
+          for (int t0 = 1; t0 < p.n_ntiles; t0 += 8) {
+            float x[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (t0 + q < p.n_ntiles) x[q] = __ldcg(src + size_t(t0 + q) * p.P);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (t0 + q < p.n_ntiles) v = prod ? __fmul_rn(v, x[q]) : __fadd_rn(v, x[q]);
+          }
+          return v;
+        };
+        const bool par = p.n_ch > 1 && p.n_ch * C::BM <= 256;
+        if (par) {
+          const int ch = etid / C::BM, rr = etid % C::BM;
+          if (ch < p.n_ch && m0 + rr < p.P) xs[ch * C::BM + rr] = chain(ch, m0 + rr);
+          ptx::named_bar_sync(1, 256);
+        }
+        if (etid < C::BM && m0 + etid < p.P) {
+          float chv[kMaxCh];
+          for (int ch = 0; ch < p.n_ch; ++ch) chv[ch] = par ? xs[ch * C::BM + etid] : chain(ch, m0 + etid);
+          for (int o = 0; o < p.n_out; ++o) {
+            const float s0 = chv[p.out_ch0[o]];
+            const float s1 = p.out_ch1[o] >= 0 ? chv[p.out_ch1[o]] : 0.f;
+            p.out[o * p.ldo + m0 + etid] = finalize<float>(p.out_kind[o], s0, s1, p.D, float(p.out_bias[o]));
+          }
+        }
+        if (etid == 0) p.counters[blockIdx.x] = 0u;
+      }
+    }
+  }
+  if ((warp < 2 || warp == 10) && nsk > 1) {  // the producer / MMA warps join both exchange barriers
+    ptx::cluster_sync_all();
+    ptx::cluster_sync_all();
+  }
+  // no CTA leaves while its M partner may still multicast into it or commit to its barriers
+  ptx::cluster_sync_all();
+  umma::fence_before();
+  __syncthreads();
+  if (threadIdx.x == 64) {
+    stamp(5);
+    if (ts) {
+      ts[6] = flags[1];
+      ts[7] = 1;
+    }
+  }
+  if (warp == 1) umma::tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
+// ---------------------------------------------------------------------------------------
 // K2: FP32 FFMA kernel.  Each consumer thread owns an 8x8 register tile; rows and columns
 // are interleaved with stride 8 (rows ty + 8*i, cols tx + 8*j) so the float4 fragment loads
 // of a warp hit 8 distinct 16-byte swizzle chunks (conflict free).
@@ -1325,6 +1655,37 @@ void launch_f32_umma(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUt
   count_launch();
 }
 
+template <int BN>
+void launch_f32_umma_sk(const CUtensorMap& tx, const CUtensorMap& b_hi, const CUtensorMap& b_lo,
+                        const fused_params<float>& fp, int splitk, cudaStream_t st) {
+  using C = umma_sk_cfg<BN>;
+  auto kern = eval_f32_umma_sk_kernel<BN>;
+  static bool attr = false;
+  if (!attr) {
+    EVB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  const int mt = (fp.P + C::BM - 1) / C::BM;
+  dim3 grid((mt + 1) & ~1, (fp.D + BN - 1) / BN, splitk);  // M pairs (a padding tile computes zeros)
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = grid;
+  lc.blockDim = dim3(C::THREADS);
+  lc.dynamicSmemBytes = C::SMEM;
+  lc.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;  // the K halves of a tile form one cluster
+  at[1].val.clusterDim.x = 2;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = unsigned(splitk);
+  lc.attrs = at;
+  lc.numAttrs = 2;
+  EVB_CUDA(cudaLaunchKernelEx(&lc, kern, tx, b_hi, b_lo, fp));
+  EVB_CUDA(cudaGetLastError());
+  count_launch();
+}
+
 template <int BM, int BN>
 void launch_f32(const CUtensorMap& tmX, const CUtensorMap& tmM, const fused_params<float>& fp, cudaStream_t st) {
   using C = f32_cfg<BM, BN, kStages32>;
@@ -1414,7 +1775,9 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
     if (umma32) {
       // ---- fp32 on tcgen05: 3xTF32, 128 x UBN tiles ----
       static const char* ubn_env = std::getenv("EVB_UMMA_BN");
-      const int UBN = ubn_env ? std::atoi(ubn_env) : 64;
+      // default: the split-K kernel with 128 x 128 tiles (EVB_UMMA_BN=64 / 128 / 256 selects the
+      // single-K-range kernels)
+      const int UBN = ubn_env ? std::atoi(ubn_env) : 0;
       device_problem* pr = const_cast<device_problem*>(rq.prob);
       const bool own_rot = rotation == pr->rotation;  // composition components pass their own rotation
       const int64_t mel = int64_t(D) * ldm;
@@ -1440,6 +1803,63 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
       const bool fuse = UBN == 64 && !(fuse_env && std::string(fuse_env) == "0");
       CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
       bool ok = true;
+      if (UBN == 0) {
+        constexpr int SBN = 128;
+        const int n_mtiles = ((P + 127) / 128 + 1) & ~1, n_nt = (D + SBN - 1) / SBN;  // M pairs
+        const int n_tiles = n_mtiles * n_nt;
+        // K halves when the tiles alone leave SMs idle and each half keeps >= 8 K slices
+        static const char* sk_env = std::getenv("EVB_UMMA_SPLITK");
+        int splitk = (n_tiles * 2 <= sm_count() && (D + 31) / 32 >= 16) ? 2 : 1;
+        if (sk_env) splitk = std::max(1, std::min(2, std::atoi(sk_env)));
+        ok = make_tma_2d(&ta_hi, X, EVB_F32, uint64_t(D), uint64_t(P), uint64_t(ldx) * 4, 32, 128) &&
+             make_tma_2d(&tb_hi, rhi, EVB_F32, uint64_t(ldm), uint64_t(D), uint64_t(ldm) * 4, 32, SBN / 2) &&
+             make_tma_2d(&tb_lo, rlo, EVB_F32, uint64_t(ldm), uint64_t(D), uint64_t(ldm) * 4, 32, SBN / 2);
+        if (!ok) throw runtime_error("gemm_eval: cannot encode the TMA descriptors of the tf32 split");
+        fp.n_ntiles = n_nt * splitk;  // column blocks of BN / splitk, one partial each
+        if (!zstore) {
+          ensure_buffer(&sc->partial, &sc->partial_bytes, size_t(fp.n_ch) * fp.n_ntiles * P * sizeof(T), rq.stream);
+          if (sc->counters_n < size_t(n_mtiles)) {
+            size_t cap = sc->counters_n * sizeof(unsigned);
+            void* ptr = sc->counters;
+            ensure_buffer(&ptr, &cap, size_t(n_mtiles) * sizeof(unsigned), rq.stream);
+            sc->counters = static_cast<unsigned*>(ptr);
+            sc->counters_n = cap / sizeof(unsigned);
+            EVB_CUDA(cudaMemsetAsync(sc->counters, 0, cap, rq.stream));
+          }
+          fp.partial = static_cast<T*>(sc->partial);
+          fp.counters = sc->counters;
+        }
+        static const bool timeline = std::getenv("EVB_K1_TIMELINE") != nullptr;
+        if (timeline) {  // one synchronous launch, per-CTA phase stamps appended to a CSV
+          const int nct = n_tiles * splitk;
+          unsigned long long* d = nullptr;
+          EVB_CUDA(cudaMalloc(&d, size_t(nct) * 8 * 8));
+          EVB_CUDA(cudaMemset(d, 0, size_t(nct) * 8 * 8));
+          fused_params<float> f2 = fp;
+          f2.dbg_ts = d;
+          f2.dbg_skip = std::getenv("EVB_K2_SKIP") ? std::atoi(std::getenv("EVB_K2_SKIP")) : 0;
+          launch_f32_umma_sk<SBN>(ta_hi, tb_hi, tb_lo, f2, splitk, rq.stream);
+          EVB_CUDA(cudaStreamSynchronize(rq.stream));
+          std::vector<unsigned long long> h(size_t(nct) * 8);
+          EVB_CUDA(cudaMemcpy(h.data(), d, h.size() * 8, cudaMemcpyDeviceToHost));
+          cudaFree(d);
+          if (FILE* f = std::fopen("gpurun_out/k2_ts.csv", "a")) {
+            for (int c = 0; c < nct; ++c)
+              std::fprintf(f, "%d,%llu,%llu,%llu,%llu,%llu,%llu,%llu\n", c, h[c * 8 + 0], h[c * 8 + 1], h[c * 8 + 3],
+                           h[c * 8 + 4], h[c * 8 + 5], h[c * 8 + 6], h[c * 8 + 7]);
+            std::fprintf(f, "end\n");
+            std::fclose(f);
+          }
+        } else {
+          launch_f32_umma_sk<SBN>(ta_hi, tb_hi, tb_lo, fp, splitk, rq.stream);
+        }
+        if (!own_rot) {
+          EVB_CUDA(cudaStreamSynchronize(rq.stream));
+          cudaFree(rhi);
+          cudaFree(rlo);
+        }
+        return;
+      }
       if (fuse) {
         ok = make_tma_2d(&ta_hi, X, EVB_F32, uint64_t(D), uint64_t(P), uint64_t(ldx) * 4, 32, 128);
         ta_lo = ta_hi;

@@ -73,6 +73,14 @@ __device__ __forceinline__ void commit(uint64_t* bar) {
                    ptx::smem_u32(bar))
                : "memory");
 }
+// commit arriving on the barrier at `bar`'s offset in every CTA of `mask` (operands multicast
+// into several CTAs are freed only when all their consumers' MMAs are done)
+__device__ __forceinline__ void commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   ptx::smem_u32(bar)),
+               "h"(mask)
+               : "memory");
+}
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
