@@ -21,9 +21,13 @@
 //   6. apply     block per replaced individual: parent -> archive slot, trial -> population.
 // Arithmetic uses explicitly rounded intrinsics (no FMA contraction), so with the same draws the
 // trial vectors are bit-identical to the reference's.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
 #include <limits>
 #include <cmath>
 #include <vector>
@@ -80,6 +84,7 @@ struct evb_de_s {
   unsigned long long* d_owner64 = nullptr;   // archive_cap
   unsigned long long* d_sel_agg = nullptr;   // ceil(P / kSelBlockItems)
   unsigned* d_sel_sync = nullptr;            // 2
+  double* d_srec = nullptr;                  // 3 x P: persistent generations' success records
   void* archive = nullptr;    // archive_cap x ldt
   int* d_arch_size = nullptr;
   int* d_write_index = nullptr;
@@ -1364,6 +1369,467 @@ __global__ void param_trace_kernel(const T* mem_f, const T* mem_cr, int H, int s
   *count = n + 1;
 }
 
+// ---- persistent generations (K8 for one engine run: BASELINE config 2) ------------------------
+// A whole sequence of generations of one engine in ONE launch: a cluster of NC CTAs, CTA c owns
+// individuals [c Q, c Q + Q).  Per generation, with the engine's own arithmetic and Philox words:
+//   A  fitness of every member (L2) -> (fitness, index) ranks, NaN last: top-p order (ttpb/1) or
+//      the best member (best/1), redundantly in every CTA; adapter memories staged (L2 -> smem)
+//   B  draws of the owned individuals (draw_scalars: the engine's sub-streams and word counts)
+//   C  trial genes (binomial word per gene, donor rows of population / archive read through L2)
+//   D  evaluation of the owned trials exactly as eval_small_kernel (M^T resident in shared memory,
+//      sequential k with separate mul and add, base_value_pre): bit-identical to the engine
+//   E  selection flags; each CTA's (pushes, successes) counts into every CTA (DSMEM)
+//      -- cluster barrier --
+//   F  push / success indices from the counts prefix; archive slots (victim words of the archive
+//      sub-stream); last-writer-wins by 64-bit (epoch << 32 | push) maxima; success records
+//      (gain, F, CR) in success order
+//      -- cluster barrier --
+//   G  owners replace parents (parent row -> its archive slot if it still owns it, trial -> the
+//      population); CTA 0: archive size, victim-word count, SHADE / JADE memory update with the
+//      reference's sequential sums (de/parameter.hpp:107-120, 166-184)
+//      -- cluster barrier --
+// Data other CTAs wrote during the launch is read with ld.global.cg (L2; the L1s are not coherent).
+// Results are bit-identical to the same number of evb_de_generation calls.
+template <typename T>
+struct de_run_args {
+  de_dev<T> d;
+  const T* shift;
+  const T* rot_t;  // M^T dense, D x D (device_problem::rot_t)
+  const T* ell_w;
+  int kind;
+  double bias;
+  int G;
+  int Q;       // individuals per CTA
+  double* srec;  // 3 x P: success (gain, F, CR) in success order
+  unsigned long long* prof;  // EVB_DE_PERSIST_PROFILE: CTA 0's clock64 per phase (tuning aid)
+};
+
+constexpr int kRunThreads = 512;
+
+template <typename T>
+__device__ __forceinline__ T ldcg(const T* p) { return __ldcg(p); }
+
+template <typename T>
+__global__ void __launch_bounds__(kRunThreads, 1) de_run_kernel(const de_run_args<T> a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const de_dev<T>& d = a.d;
+  const int NC = int(gridDim.x), c = int(blockIdx.x);
+  const int P = d.P, D = d.D, Q = a.Q;
+  const int i0 = c * Q, i1 = min(P, i0 + Q), nq = max(0, i1 - i0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
+  const int H = max(1, d.cfg.memory_size);
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const uint32_t mt_bytes = uint32_t((size_t(D) * D * sizeof(T) + 15) / 16 * 16);
+  T* sMT = reinterpret_cast<T*>(smem_raw);                                     // D x D (M^T)
+  T* sS = reinterpret_cast<T*>(smem_raw + mt_bytes);                            // Q x D: x - o / pre terms
+  T* sZ = sS + size_t(Q) * D;                                                   // Q x D
+  T* sT = sZ + size_t(Q) * D;                                                   // Q x D: owned trials
+  T* sR = sT + size_t(Q) * D;                                                   // Q x 4 x D: target + donor rows
+  T* sFit = sR + 4 * size_t(Q) * D;                                             // P
+  T* sMemF = sFit + P;                                                          // H
+  T* sMemC = sMemF + H;                                                         // H
+  T* sTf = sMemC + H;                                                           // Q
+  T* sQf = sTf + Q;                                                             // Q x 2: F, CR
+  double* sG = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sQf + 2 * Q) + 15) & ~uintptr_t(15));  // 3 x P
+  int NP2 = 1;
+  while (NP2 < P) NP2 <<= 1;
+  unsigned long long* sKey = reinterpret_cast<unsigned long long*>(sG + 3 * P);  // P order keys
+  int* sIdx = reinterpret_cast<int*>(sKey + P);  // NP2 order slots + P rank counters
+  int* sCnt = sIdx + NP2 + P;                    // NC x 2
+  int* sQi = sCnt + 2 * NC;                      // Q x 8: donors, jrand, first gene word
+  uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<uintptr_t>(sCnt + 2 * NC + 2) & ~uintptr_t(7)) + 1;
+  __shared__ int s_misc[4];  // [0] archive size at the generation start
+
+  if (tid == 0) {
+    ptx::mbar_init(bar, 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {  // M^T once for the whole launch
+    ptx::mbar_arrive_expect_tx(bar, mt_bytes);
+    ptx::bulk_load(sMT, a.rot_t, mt_bytes, bar);
+  }
+  ptx::mbar_wait(bar, 0);
+  const uint32_t gen0 = *d.gen_ptr;
+  const unsigned E0 = *d.epoch;
+  const bool ttpb = d.cfg.mutation == EVB_MUT_TTPB1, best = d.cfg.mutation == EVB_MUT_BEST1;
+  const bool adapt = d.cfg.parameter == EVB_PAR_SHADE || d.cfg.parameter == EVB_PAR_JADE;
+  cl.sync();  // every CTA's shared memory exists before the first DSMEM write
+  long long t_last = clock64();
+  auto mark = [&](int k) {  // phase boundary (after a barrier): CTA 0 thread 0 accumulates cycles
+    if (a.prof && c == 0 && tid == 0) {
+      const long long t = clock64();
+      a.prof[k] += (unsigned long long)(t - t_last);
+      t_last = t;
+    }
+  };
+
+  for (int g = 0; g < a.G; ++g) {
+    const uint32_t gen = gen0 + uint32_t(g);
+    const unsigned tag = E0 + unsigned(g) + 1u;
+    // ---- A: fitness, order, adapter memories, archive size ----
+    for (int t = tid; t < P; t += nthr) sFit[t] = ldcg(d.fit + t);
+    if (adapt)
+      for (int t = tid; t < H; t += nthr) {
+        sMemF[t] = ldcg(d.mem_f + t);
+        sMemC[t] = ldcg(d.mem_cr + t);
+      }
+    if (tid == 0) s_misc[0] = ldcg(d.arch_size);
+    __syncthreads();
+    if (ttpb || best) {  // (fitness, index) ranks, NaN last, over all threads: thread (i, chunk)
+      // counts the members of its j chunk that precede i on order_key (integer shared atomics)
+      const int nch = max(1, min(8, nthr / P));
+      for (int t = tid; t < P; t += nthr) {
+        sIdx[NP2 + t] = 0;  // rank counters (after the order slots)
+        sKey[t] = order_key(sFit[t]);
+      }
+      __syncthreads();
+      for (int t = tid; t < P * nch; t += nthr) {
+        const int ch = t / P, i = t - ch * P;
+        const int j0 = (P * ch) / nch, j1 = (P * (ch + 1)) / nch;
+        const unsigned long long ki = sKey[i];
+        int cnt = 0;
+#pragma unroll 4
+        for (int j = j0; j < j1; ++j) {
+          const unsigned long long kj = sKey[j];
+          cnt += (kj < ki || (kj == ki && j < i)) ? 1 : 0;
+        }
+        if (cnt) atomicAdd(&sIdx[NP2 + i], cnt);
+      }
+      __syncthreads();
+      for (int i = tid; i < P; i += nthr) {
+        const int rk = sIdx[NP2 + i];
+        if (rk < d.p_count) sIdx[rk] = i;
+      }
+      __syncthreads();
+    }
+    mark(0);
+    const int arch_size = s_misc[0];
+    // ---- B: draws of the owned individuals ----
+    if (tid < nq) {
+      de_dev<T> dl = d;
+      dl.order = sIdx;  // sorted: the first p_count entries are the order
+      dl.mem_f = sMemF;
+      dl.mem_cr = sMemC;
+      const int i = i0 + tid;
+      philox_prefetch_reader<5> r(d.src.key, (uint64_t(gen) << 32) | uint32_t(i));
+      draw_scalars<T>(dl, i, arch_size, r);
+      d.woff[i] = r.count;
+      d.rword[i] = r.count + D;
+      d.wcount[i] = r.count + D;
+      // the same values for this CTA's later phases from shared memory (no L2 round trip)
+      sQi[8 * tid + 0] = d.idx[4 * i + 0];
+      sQi[8 * tid + 1] = d.idx[4 * i + 1];
+      sQi[8 * tid + 2] = d.idx[4 * i + 2];
+      sQi[8 * tid + 3] = d.jrand[i];
+      sQi[8 * tid + 4] = int(r.count);
+      sQf[2 * tid] = d.F[i];
+      sQf[2 * tid + 1] = d.CR[i];
+    }
+    __syncthreads();
+    mark(1);
+    // ---- C: trial genes (binomial, de_trial_kernel's arithmetic) ----
+    // the owned individuals' target and donor rows (population or archive, L2) into shared memory
+    // with every load of the CTA in flight at once, then thread per (individual, Philox block)
+    for (int rt0 = 2 * warp; rt0 < nq * 4; rt0 += 2 * (nthr / 32)) {  // warp per 2 rows, all loads in flight
+      const T* rows[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int rt = min(rt0 + h, nq * 4 - 1);
+        const int q = rt >> 2, w = rt & 3;
+        const int src = w == 0 ? i0 + q : sQi[8 * q + (w - 1)];
+        rows[h] = (w == 3 && ttpb && src >= P) ? d.archive + size_t(src - P) * d.ldt : d.pop + size_t(src) * d.ldp;
+      }
+      constexpr int NL = 4;  // loads per lane per row (D <= 128 in one pass)
+      for (int j0 = 0; j0 < D; j0 += 32 * NL) {
+        T v[2][NL];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int u = 0; u < NL; ++u) {
+            const int j = j0 + lane + 32 * u;
+            v[h][u] = j < D ? ldcg(rows[h] + j) : T(0);
+          }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int u = 0; u < NL; ++u) {
+            const int j = j0 + lane + 32 * u;
+            if (j < D && rt0 + h < nq * 4) sR[size_t(rt0 + h) * D + j] = v[h][u];
+          }
+      }
+    }
+    __syncthreads();
+    {
+      const int NB = D / 2 + 1;
+      for (int e = tid; e < nq * NB; e += nthr) {
+        const int q = e / NB, b = e - q * NB;
+        const int i = i0 + q;
+        const int64_t s0 = sQi[8 * q + 4];
+        const int64_t blk0 = s0 >> 1;
+        const int64_t nblk = ((s0 + D + 1) >> 1) - blk0;
+        if (b >= nblk) continue;
+        const T Fi = sQf[2 * q];
+        const double cr = double(sQf[2 * q + 1]);
+        const int jr = sQi[8 * q + 3];
+        const T* xi = sR + q * 4 * D;
+        const T* xa = xi + D;
+        const T* xb = xa + D;
+        const T* xc = xb + D;
+        uint64_t w0, w1;
+        philox_pair(d.src.key, (uint64_t(gen) << 32) | uint32_t(i), uint64_t(blk0 + b), w0, w1);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t j64 = 2 * (blk0 + b) + h - s0;
+          if (j64 < 0 || j64 >= D) continue;
+          const int j = int(j64);
+          const T xij = xi[j];
+          T v;
+          if (u01_of(h ? w1 : w0) < cr || j == jr)
+            v = donor_gene<T>(d.cfg.mutation, xij, xa[j], xb[j], xc[j], Fi);
+          else
+            v = xij;
+          if (d.cfg.repair == EVB_REP_CLIP) {
+            if (v < d.lb) v = d.lb;
+            if (v > d.ub) v = d.ub;
+          } else if (v < d.lb || v > d.ub) {
+            v = repair_gene<T>(d.cfg.repair, v, xij, d.lb, d.ub);
+          }
+          sT[q * D + j] = v;
+          sS[q * D + j] = fop<T>::sub(v, a.shift[j]);  // x - o for the evaluation (eval_small's rounding)
+        }
+      }
+    }
+    __syncthreads();
+    mark(2);
+    // ---- D: evaluation, eval_small_kernel's order ----
+    mark(8);
+    {  // thread = (row r, a group of up to QG owned individuals): M^T[k][r] is loaded once per k for
+       // all of them, s[q][k .. k+1] are 16-byte broadcasts; every chain keeps the reference's
+       // sequential k order (separate mul and add)
+      constexpr int QG = 4;
+      const int ngr = (nq + QG - 1) / QG;
+      for (int t = tid; t < D * ngr; t += nthr) {
+        const int r = t % D, gq = t / D;
+        const int q0 = gq * QG;
+        const int nv = min(QG, nq - q0);
+        const T* mcol = sMT + r;
+        T acc[QG];
+        const T* sv[QG];
+#pragma unroll
+        for (int u = 0; u < QG; ++u) {
+          acc[u] = T(0);
+          sv[u] = sS + (q0 + min(u, nv - 1)) * D;
+        }
+        int k = 0;
+        if constexpr (sizeof(T) == 8) {
+          if ((D & 1) == 0)
+            for (; k + 2 <= D; k += 2) {
+              const T m0 = mcol[k * D], m1 = mcol[(k + 1) * D];
+#pragma unroll
+              for (int u = 0; u < QG; ++u) {
+                const double2 x = *reinterpret_cast<const double2*>(sv[u] + k);
+                acc[u] = fop<T>::add(acc[u], fop<T>::mul(m0, x.x));
+                acc[u] = fop<T>::add(acc[u], fop<T>::mul(m1, x.y));
+              }
+            }
+        }
+        for (; k < D; ++k) {
+          const T mk = mcol[k * D];
+#pragma unroll
+          for (int u = 0; u < QG; ++u) acc[u] = fop<T>::add(acc[u], fop<T>::mul(mk, sv[u][k]));
+        }
+#pragma unroll
+        for (int u = 0; u < QG; ++u)
+          if (u < nv) sZ[(q0 + u) * D + r] = acc[u];
+      }
+    }
+    __syncthreads();
+    mark(9);
+    if (kind_has_pre(a.kind)) {
+      const int dq = nthr / D, dj = nthr - dq * D;
+      int q = tid / D, j = tid - q * D;  // (q, j) of element e = tid, advanced by nthr without division
+      for (; q < nq;) {
+        const T* zr = sZ + q * D;
+        auto z = [&](int qq) { return zr[qq]; };
+        sS[q * D + j] = base_pre_term<T, false>(a.kind, D, z, j);
+        q += dq;
+        j += dj;
+        if (j >= D) {
+          j -= D;
+          ++q;
+        }
+      }
+      __syncthreads();
+    }
+    mark(10);
+    if (tid < nq) {
+      const T* zrow = sZ + tid * D;
+      const T* pe = sS + tid * D;
+      auto z = [&](int qq) { return zrow[qq]; };
+      auto pre = [&](int qq) { return pe[qq]; };
+      const T v = fop<T>::add(base_value_pre<T, false>(a.kind, D, z, pre, a.ell_w), T(a.bias));
+      sTf[tid] = v;
+      d.trial_fit[i0 + tid] = v;
+    }
+    __syncthreads();
+    mark(3);
+    // ---- E: selection flags, counts to every CTA ----
+    int wq = 0, sq = 0;  // warp 0: lane q's flags
+    unsigned wmask = 0, smask = 0;
+    if (warp == 0) {
+      if (lane < nq) {
+        const T ft = sTf[lane], fp = sFit[i0 + lane];
+        wq = (ft <= fp) ? 1 : 0;
+        sq = (wq && fop<T>::sub(fp, ft) > T(0)) ? 1 : 0;
+      }
+      wmask = __ballot_sync(0xffffffffu, wq);
+      smask = __ballot_sync(0xffffffffu, sq);
+      if (lane < NC) {
+        int* dst = cl.map_shared_rank(sCnt, lane);
+        dst[2 * c] = __popc(wmask);
+        dst[2 * c + 1] = __popc(smask);
+      }
+    }
+    cl.sync();
+    mark(4);
+    // ---- F: indices, archive slots, owners, success records ----
+    if (warp == 0) {
+      int pw = 0, ps = 0, tw = 0, ts = 0;
+      for (int k = 0; k < NC; ++k) {
+        const int a0 = sCnt[2 * k], a1 = sCnt[2 * k + 1];
+        if (k < c) {
+          pw += a0;
+          ps += a1;
+        }
+        tw += a0;
+        ts += a1;
+      }
+      const int size0 = arch_size, room = d.archive_cap - size0;
+      if (lane < nq) {
+        const int i = i0 + lane;
+        const int q = pw + __popc(wmask & ((1u << lane) - 1u));
+        const int k = ps + __popc(smask & ((1u << lane) - 1u));
+        d.win[i] = wq ? q + 1 : 0;
+        int sl = -1;
+        if (wq && d.archive_cap > 0) {
+          if (q < room) {
+            sl = size0 + q;
+          } else {
+            const uint64_t ctr_hi = (uint64_t(gen) << 32) | kSubArchive;
+            sl = uint_of(word_at(d.src, ctr_hi, int64_t(q - room), d.overflow), d.archive_cap);
+          }
+          atomicMax(d.owner64 + sl, (static_cast<unsigned long long>(tag) << 32) | unsigned(q));
+        }
+        d.arch_slot[i] = sl;
+        if (sq) {
+          d.succ[k] = i;
+          a.srec[k] = double(fop<T>::sub(sFit[i], sTf[lane]));
+          a.srec[P + k] = double(sQf[2 * lane]);
+          a.srec[2 * P + k] = double(sQf[2 * lane + 1]);
+        }
+      }
+      if (c == 0 && lane == 0) {
+        s_misc[1] = tw;
+        s_misc[2] = ts;
+      }
+    }
+    cl.sync();
+    mark(5);
+    // ---- G: replacements (owners), archive / adapter bookkeeping (CTA 0) ----
+    for (int q = warp; q < nq; q += nthr / 32) {
+      const int i = i0 + q;
+      const int wv = d.win[i];
+      if (!wv) continue;
+      int sl = d.arch_slot[i];
+      if (sl >= 0 && __ldcg(d.owner64 + sl) != ((static_cast<unsigned long long>(tag) << 32) | unsigned(wv - 1))) {
+        sl = -1;  // overwritten by a later push (members_[victim] = genome, in push order)
+        if (lane == 0) d.arch_slot[i] = -1;
+      }
+      T* x = d.pop + size_t(i) * d.ldp;
+      T* arow = sl >= 0 ? d.archive + size_t(sl) * d.ldt : nullptr;
+      for (int j = lane; j < D; j += 32) {
+        const T old = ldcg(x + j);
+        if (arow) arow[j] = old;
+        x[j] = sT[q * D + j];
+      }
+      if (lane == 0) d.fit[i] = sTf[q];
+    }
+    if (c == 0) {
+      const int n_push = s_misc[1], n_succ = s_misc[2];
+      if (tid == 0) {
+        const int size0 = arch_size, room = d.archive_cap - size0;
+        *d.arch_size = min(d.archive_cap, size0 + n_push);
+        *d.arch_words = d.archive_cap > 0 ? max(0, n_push - room) : 0;
+        d.n_push[0] = n_push;
+        d.n_push[1] = n_succ;
+      }
+      if (adapt && n_succ > 0) {
+        for (int k = tid; k < n_succ; k += nthr) {
+          sG[k] = __ldcg(a.srec + k);
+          sG[P + k] = __ldcg(a.srec + P + k);
+          sG[2 * P + k] = __ldcg(a.srec + 2 * P + k);
+        }
+        __syncthreads();
+        const double* gv = sG;
+        const double* fv = sG + P;
+        const double* cv = sG + 2 * P;
+        if (d.cfg.parameter == EVB_PAR_SHADE) {  // de/parameter.hpp:166-184 (adapter_update's roundings)
+          double gain_sum = 0.0;
+          if (tid == 0)
+            for (int k = 0; k < n_succ; ++k) gain_sum = __dadd_rn(gain_sum, gv[k]);
+          __shared__ double s_gsum;
+          if (tid == 0) s_gsum = gain_sum;
+          __syncthreads();
+          gain_sum = s_gsum;
+          // per-success products by their own threads, in place (w = gain / sum; (w f) f, w f, w cr)
+          double* wnum = sG;
+          for (int k = tid; k < n_succ; k += nthr) {
+            const double w = __ddiv_rn(gv[k], gain_sum);
+            const double wf = __dmul_rn(w, fv[k]);
+            wnum[k] = __dmul_rn(wf, fv[k]);
+            wnum[P + k] = wf;
+            wnum[2 * P + k] = __dmul_rn(w, cv[k]);
+          }
+          __syncthreads();
+          if (tid == 0) {
+            double f_num = 0.0, f_den = 0.0, cr_acc = 0.0;
+            for (int k = 0; k < n_succ; ++k) {
+              f_num = __dadd_rn(f_num, wnum[k]);
+              f_den = __dadd_rn(f_den, wnum[P + k]);
+              cr_acc = __dadd_rn(cr_acc, wnum[2 * P + k]);
+            }
+            const int kw = *d.write_index;
+            d.mem_f[kw] = T(__ddiv_rn(f_num, f_den));
+            d.mem_cr[kw] = T(cr_acc);
+            *d.write_index = (kw + 1) % d.cfg.memory_size;
+          }
+        } else if (tid == 0) {  // JADE, de/parameter.hpp:107-120
+          double num = 0.0, den = 0.0, crm = 0.0;
+          for (int k = 0; k < n_succ; ++k) {
+            num = __dadd_rn(num, __dmul_rn(fv[k], fv[k]));
+            den = __dadd_rn(den, fv[k]);
+            crm = __dadd_rn(crm, cv[k]);
+          }
+          const double lehmer = __ddiv_rn(num, den);
+          crm = __ddiv_rn(crm, double(n_succ));
+          const double cc = double(T(d.cfg.jade_c));
+          d.mem_f[0] = T(__dadd_rn(__dmul_rn(__dsub_rn(1.0, cc), double(sMemF[0])), __dmul_rn(cc, lehmer)));
+          d.mem_cr[0] = T(__dadd_rn(__dmul_rn(__dsub_rn(1.0, cc), double(sMemC[0])), __dmul_rn(cc, crm)));
+        }
+      }
+    }
+    mark(6);
+    cl.sync();
+    mark(7);
+  }
+  if (c == 0 && tid == 0) {
+    *d.gen_ptr = gen0 + uint32_t(a.G);
+    *d.epoch = E0 + unsigned(a.G);
+  }
+}
+
 template <typename T>
 void reduce_t(evb_de_s* e, void* pop, int64_t ldp, void* fit, evb_rng_s* r, cudaStream_t st);
 
@@ -1711,6 +2177,101 @@ void init_population_t(int P, int D, void* pop, int64_t ldp, double lb, double u
 
 }  // namespace
 
+// n generations in one persistent cluster launch when the configuration allows it (PHILOX words,
+// binomial crossover, clip / reflect / midpoint repair, fixed population, a base problem the
+// small-D kernel evaluates, no per-generation observers, P <= 16 x 32); false: not eligible.
+template <typename T>
+bool run_generations_t(evb_de_s* e, const device_problem* prob, void* pop, int64_t ldp, void* fit, double lb,
+                       double ub, evb_rng_s* r, int n, cudaStream_t st) {
+  static const char* env = std::getenv("EVB_DE_PERSIST");
+  if (env && std::atoi(env) == 0) return false;
+  if (r->mode != RNG_PHILOX || e->cfg.crossover != EVB_CX_BINOMIAL || e->cfg.repair == EVB_REP_REINITIALIZE) return false;
+  if (e->reduction || e->rec || e->ptrace || e->mon_on) return false;
+  if (prob->spec != SPEC_BASE || !prob->rot_t || !eval_small_path(*prob)) return false;
+  const int P = e->P, D = e->D;
+  static int max_nc = [] {
+    int v = 8;
+    if (cudaFuncSetAttribute(de_run_kernel<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) v = 16;
+    cudaGetLastError();
+    return v;
+  }();
+  const int NC = std::min(max_nc, std::max(1, (P + 7) / 8));
+  const int Q = (P + NC - 1) / NC;
+  if (Q > 32) return false;
+  const int H = std::max(1, e->cfg.memory_size);
+  const size_t mt_bytes = (size_t(D) * D * sizeof(T) + 15) / 16 * 16;
+  auto smem_for = [&](int q, int nc) {
+    size_t np2 = 1;
+    while (np2 < size_t(P)) np2 <<= 1;
+    return mt_bytes + (7 * size_t(q) * D + P + 2 * H + 3 * q + 1) * sizeof(T) + 16 + 4 * size_t(P) * 8 +
+           (np2 + P + 2 * nc + 8 * q + 2) * sizeof(int) + 64;
+  };
+  if (smem_for(Q, NC) > 200 * 1024) return false;
+  de_run_args<T> a{};
+  a.d = make_dev<T>(e, pop, ldp, fit, lb, ub, r);
+  a.shift = static_cast<const T*>(prob->shift);
+  a.rot_t = static_cast<const T*>(prob->rot_t);
+  a.ell_w = static_cast<const T*>(prob->ell_w);
+  a.kind = prob->kind;
+  a.bias = prob->bias;
+  a.G = n;
+  a.Q = Q;
+  a.srec = e->d_srec;
+  EVB_CUDA(cudaFuncSetAttribute(de_run_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  cudaLaunchConfig_t lc{};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.blockDim = dim3(kRunThreads);
+  lc.stream = st;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  int nc = NC;
+  for (;;) {  // a cluster this size must fit on one GPC with this shared memory
+    at[0].val.clusterDim.x = unsigned(nc);
+    lc.gridDim = dim3(nc);
+    lc.dynamicSmemBytes = smem_for((P + nc - 1) / nc, nc);
+    if (lc.dynamicSmemBytes > 200 * 1024) return false;
+    int active = 0;
+    if (cudaOccupancyMaxActiveClusters(&active, de_run_kernel<T>, &lc) == cudaSuccess && active >= 1) break;
+    cudaGetLastError();
+    if (nc == 1) return false;
+    nc = std::max(1, nc / 2);
+    if ((P + nc - 1) / nc > 32) return false;
+  }
+  a.Q = (P + nc - 1) / nc;
+  static const bool prof = std::getenv("EVB_DE_PERSIST_PROFILE") != nullptr;
+  if (prof) {
+    EVB_CUDA(cudaMalloc(&a.prof, 16 * sizeof(unsigned long long)));
+    EVB_CUDA(cudaMemset(a.prof, 0, 16 * sizeof(unsigned long long)));
+  }
+  EVB_CUDA(cudaLaunchKernelEx(&lc, de_run_kernel<T>, a));
+  count_launch();
+  if (prof) {
+    unsigned long long h[16];
+    EVB_CUDA(cudaMemcpy(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost));
+    cudaFree(a.prof);
+    const char* names[] = {"order", "draws", "trial", "eval-base", "select+B1", "slots+B2", "apply+adapt", "B3",
+                           "x-o", "dots", "pre"};
+    std::string line = "[evb de_run] NC=" + std::to_string(nc) + " cycles/generation:";
+    for (int k = 0; k < 11; ++k) line += std::string(" ") + names[k] + "=" + std::to_string(h[k] / std::max(1, n));
+    std::fprintf(stderr, "%s\n", line.c_str());
+  }
+  e->gen_P = P;
+  e->last_gen = r->gen + uint32_t(n - 1);
+  r->gen += uint32_t(n);
+  e->fes += int64_t(n) * P;
+  e->gen_count += n;
+  return true;
+}
+
+bool run_generations(evb_de_s* e, const device_problem* prob, void* pop, int64_t ldp, void* fit, double lb, double ub,
+                     evb_rng_s* r, int n, cudaStream_t st) {
+  return e->dtype == EVB_F64 ? run_generations_t<double>(e, prob, pop, ldp, fit, lb, ub, r, n, st)
+                             : run_generations_t<float>(e, prob, pop, ldp, fit, lb, ub, r, n, st);
+}
+
 void de_generation(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, void* pop, int64_t ldp, void* fit,
                    double lb, double ub, evb_rng_s* r, cudaStream_t st) {
   if (e->dtype == EVB_F64) generation_t<double>(e, prob, sc, pop, ldp, fit, lb, ub, r, st);
@@ -1749,7 +2310,7 @@ void free_de(evb_de_s* e) {
   if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
   void* ptrs[] = {e->trial, e->trial_fit, e->F, e->CR, e->slot, e->idx, e->jrand, e->xlen, e->rword, e->woff, e->wcount, e->order,
                   e->win, e->arch_slot, e->owner, e->succ, e->wlist, e->d_npush, e->d_epoch, e->d_owner64, e->d_sel_agg,
-                  e->d_sel_sync, e->archive, e->d_arch_size, e->d_write_index,
+                  e->d_sel_sync, e->d_srec, e->archive, e->d_arch_size, e->d_write_index,
                   e->d_arch_words, e->mem_f, e->mem_cr, e->rank, e->d_shrink_words, e->d_mon};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -1940,6 +2501,7 @@ int evb_de_create(int dtype, const evb_de_config* c, int pop_size, int dim, evb_
       e->d_owner64 = static_cast<unsigned long long*>(dalloc<unsigned long long>(std::max(1, e->archive_cap)));
       e->d_sel_agg = static_cast<unsigned long long*>(dalloc<unsigned long long>((pop_size + 1023) / 1024));
       e->d_sel_sync = static_cast<unsigned*>(dalloc<unsigned>(2));
+      e->d_srec = static_cast<double*>(dalloc<double>(3 * size_t(pop_size)));
       EVB_CUDA(cudaMalloc(&e->archive, bytes(size_t(std::max(1, e->archive_cap)) * e->ldt)));
       EVB_CUDA(memset_now(e->archive, 0, bytes(size_t(std::max(1, e->archive_cap)) * e->ldt)));
       e->d_arch_size = static_cast<int*>(dalloc<int>(1));
@@ -2054,6 +2616,8 @@ int evb_de_generations(evb_de e, evb_problem objective, evb_scratch s, void* pop
       throw config_error("de_generations: linear population reduction needs a budget (evb_de_set_budget)");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     evb_scratch_s* sc = s ? s : e->eval_scratch;
+    // one persistent cluster launch for all n generations where the configuration allows
+    if (run_generations(e, &objective->p, pop, ldp, fitness, lb, ub, rng, n, st)) return;
     if (e->reduction || e->ptrace) {  // size changes / per-generation trace arguments: no graph replay
       for (int g = 0; g < n; ++g) de_generation(e, &objective->p, sc, pop, ldp, fitness, lb, ub, rng, st);
       return;

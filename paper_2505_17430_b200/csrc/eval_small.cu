@@ -534,6 +534,13 @@ bool multi_eligible(const eval_request* rqs, int np) {
   return true;
 }
 
+// the small-D kernel (exact order) evaluates this base / hybrid problem (the persistent DE
+// generations reproduce its arithmetic, de.cu)
+bool eval_small_path(const device_problem& p) {
+  return p.spec != SPEC_COMPOSITION && (p.dtype == EVB_F64 ? small_fits<double>(p.dim, false)
+                                                           : small_fits<float>(p.dim, false));
+}
+
 void eval_dispatch(const eval_request& rq) {
   if (rq.n == 0) return;
   if (rq.prob->dtype == EVB_F64) dispatch_t<double>(rq);

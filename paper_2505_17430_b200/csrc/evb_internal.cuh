@@ -264,6 +264,7 @@ constexpr int kMaxGates = 16;
 int multi_first_wave_rows(int np, int64_t n_points, int64_t dim);
 
 void eval_dispatch(const eval_request& rq);
+bool eval_small_path(const device_problem& p);
 // true when eval_dispatch runs the request on the fused fp64 GEMM, whose producer honours kgate
 bool gate_eligible(const eval_request& rq);
 // several base problems (same D, fp64, fused kinds) on one device X in one multi-problem K1

@@ -685,3 +685,72 @@ def test_multi_cta_selection_and_sort_order_equal_single(dev, monkeypatch, cfg, 
     assert np.array_equal(s0["archive"], s1["archive"])
     assert np.array_equal(s0["memory_f"], s1["memory_f"]) and np.array_equal(s0["memory_cr"], s1["memory_cr"])
     assert s0["write_index"] == s1["write_index"]
+
+
+PERSIST_CASES = [
+    (preset_shade(0.11, 180, 1.0), 180, 100, "ackley", torch.float64),
+    (preset_shade(0.11, 50, 1.0), 60, 30, "rastrigin", torch.float32),
+    (DEConfig("ttpb_1", "binomial", "clip", "jade", p_best=0.05, use_archive=True, jade_c=0.1, archive_rate=1.0),
+     100, 20, "elliptic", torch.float64),
+    (DEConfig("rand_1", "binomial", "clip", "fixed", f=0.5, cr=0.9), 100, 10, "rastrigin", torch.float64),
+    (DEConfig("best_1", "binomial", "reflect", "fixed", f=0.8, cr=0.7), 33, 50, "sphere", torch.float64),
+]
+
+
+@pytest.mark.parametrize("cfg,P,D,kind,dtype", PERSIST_CASES,
+                         ids=lambda v: f"{v.mutation}-{v.parameter}" if isinstance(v, DEConfig) else str(v))
+def test_persistent_generations_equal_per_generation(dev, monkeypatch, cfg, P, D, kind, dtype):
+    """evb_de_generations' persistent cluster launch (all generations in one kernel, the engine's
+    draws / trial / exact-order evaluation / selection / archive / adapter update per CTA and
+    across the cluster) against the same generations run one evb_de_generation at a time:
+    populations, fitness, archive, adapter memories and every exported draw bit-identical, both
+    for 40 generations in one launch and generation by generation (launches of one)."""
+    from paper_2505_17430_b200.de import EVB_F32, EVB_F64
+
+    o, m = O.shift_rotation(9, D)
+    et = EVB_F64 if dtype == torch.float64 else EVB_F32
+    prob = evb.ProblemInstance.base(getattr(evb.BaseKind, kind), o, m, 0.0, dtype=et)
+    G = 40
+
+    def start():
+        eng = DEEngine(cfg, P, D, et)
+        rng = Rng.philox(0xC0FFEE)
+        pop = torch.empty((P, D), dtype=dtype, device=dev)
+        eng.init_population(pop, -100.0, 100.0, rng)
+        fit = dev_eval(prob, pop, dev)
+        return eng, rng, pop, fit
+
+    def state(eng, pop, fit):
+        torch.cuda.synchronize()
+        return pop.cpu().numpy(), fit.cpu().numpy(), eng.get_state()
+
+    # reference: one generation per call (multi-kernel path)
+    e0, r0, p0, f0 = start()
+    per_gen = []
+    for _ in range(G):
+        e0.generation(prob, p0, f0, -100.0, 100.0, r0)
+        dr = e0.last_draws()
+        per_gen.append((dr["word_counts"].copy(), dr["idx"].copy(), dr["archive_words"]))
+    ref = state(e0, p0, f0)
+    # persistent: all G generations in one launch
+    e1, r1, p1, f1 = start()
+    e1.generations(prob, p1, f1, -100.0, 100.0, r1, G)
+    got = state(e1, p1, f1)
+    # persistent, one generation per launch: the exported draws of every generation
+    e2, r2, p2, f2 = start()
+    for g in range(G):
+        e2.generations(prob, p2, f2, -100.0, 100.0, r2, 1)
+        dr = e2.last_draws()
+        assert np.array_equal(dr["word_counts"], per_gen[g][0]), g
+        assert np.array_equal(dr["idx"], per_gen[g][1]), g
+        assert dr["archive_words"] == per_gen[g][2], g
+    got1 = state(e2, p2, f2)
+    assert r1.state()["generation"] == r0.state()["generation"] == r2.state()["generation"]
+    for st in (got, got1):
+        assert np.array_equal(st[0], ref[0])
+        assert np.array_equal(st[1], ref[1], equal_nan=True)
+        assert st[2]["archive_size"] == ref[2]["archive_size"]
+        assert np.array_equal(st[2]["archive"], ref[2]["archive"])
+        assert np.array_equal(st[2]["memory_f"], ref[2]["memory_f"])
+        assert np.array_equal(st[2]["memory_cr"], ref[2]["memory_cr"])
+        assert st[2]["write_index"] == ref[2]["write_index"]
