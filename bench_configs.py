@@ -158,21 +158,44 @@ def config0():
         torch.cuda.current_stream().synchronize()
         gen[0] += 1
 
-    e2e_s = wall_median(host_generation, 500)
+    e2e_k8_s = wall_median(host_generation, 500)
+    # the same through the engine (de_engine::generation's shape): state from pinned host memory,
+    # evb_de_generations(1) (the persistent cluster kernel), state back; wall clock with the copies
+    eng_h = DEEngine(preset_de(), P, D)
+    rng_h = Rng.philox(42)
+    state_d = torch.empty(P * D + P, dtype=torch.float64, device=DEV)  # [population | fitness]: one copy each way
+    pop_h = state_d[:P * D].view(P, D)
+    fit_h = state_d[P * D:]
+    eng_h.init_population(pop_h, -100.0, 100.0, rng_h)
+    evb.evaluate_batch(prob, pop_h, evb.EvalScratch(), fit_h)
+    state_h = state_d.cpu().pin_memory()
+    cur = torch.cuda.current_stream()
+
+    def host_generation_engine():
+        state_d.copy_(state_h, non_blocking=True)
+        eng_h.generations(prob, pop_h, fit_h, -100.0, 100.0, rng_h, 1)
+        state_h.copy_(state_d, non_blocking=True)
+        cur.synchronize()
+
+    e2e_s = wall_median(host_generation_engine, 500)
     cpu_s = O.REF_FAST().ref_bench_de(0, P, D, 2000, 5, O.ptr(o), O.ptr(np.ascontiguousarray(m)), 42)
     cpu_gps = 2000 / cpu_s
     return {
         "metric": "generations/s (one DE generation: mutate, cross, repair, evaluate, select)",
         "value": 1e3 / graph_ms, "unit": "generations/s",
-        "how": "DEEngine.generations: first generation eager, then a CUDA graph of one generation replayed "
-               "(5 kernels with PDL); device time per generation",
-        "us_per_generation": {"graph": graph_ms * 1e3, "eager": eager_ms * 1e3, "persistent_k8": persist_ms * 1e3},
+        "how": "DEEngine.generations(1000): all generations in one persistent cluster launch (de_run_kernel); "
+               "device time per generation ('eager': one evb_de_generation call per generation, 5 kernels)",
+        "us_per_generation": {"engine_persistent": graph_ms * 1e3, "eager": eager_ms * 1e3,
+                              "persistent_k8": persist_ms * 1e3},
         "persistent_k8": {"value": 1e3 / persist_ms, "unit": "generations/s",
                           "how": "de_runs: init + 2000 generations of the run in one launch"},
         "e2e": {"value": 1.0 / e2e_s, "unit": "generations/s", "us_per_generation": e2e_s * 1e6,
                 "h2d_bytes_per_step": P * D * 8 + P * 8, "d2h_bytes_per_step": P * D * 8 + P * 8,
-                "how": "population + fitness from pinned host memory, one K8 generation, back to the host; "
-                       "wall clock incl. copies and sync, median of 5 blocks"},
+                "how": "population + fitness (one pinned buffer, one copy each way) from host memory, one engine generation "
+                       "(DEEngine.generations(1): the persistent cluster kernel), back to the host; wall clock incl. "
+                       "copies and sync, median of 5 blocks",
+                "k8": {"value": 1.0 / e2e_k8_s, "unit": "generations/s", "us_per_generation": e2e_k8_s * 1e6,
+                       "how": "the same step through de_runs (K8, one generation)"}},
         "roofline": {"bound": "latency", "note": "about 20 KFLOP and 80 KB per generation (SURVEY §8(d)): "
                                                   "launch and dependency latency, no throughput roofline"},
         "cpu_baseline": cpu_baseline(cpu_gps, "generations/s", 1,
@@ -291,10 +314,13 @@ def config2():
     return {
         "metric": "generations/s (config 2, 1000 generations)", "value": G / (ms * 1e-3), "unit": "generations/s",
         "ms_1000_generations": ms, "best_fitness": float(fit.min()),
-        "how": "DEEngine.generations over 1000 generations (CUDA graph of one generation, PDL), device time",
-        "us_per_phase": ph,
-        "roofline": {"bound": "latency", "note": "population 144 KB, L2-resident; per-phase device times above "
-                                                  "(events between kernels) show where a generation goes"},
+        "how": "DEEngine.generations over 1000 generations: all of them in one persistent cluster launch "
+               "(de_run_kernel, 16 CTAs), device time",
+        "eager_us_per_phase": ph,
+        "roofline": {"bound": "latency", "note": "population 144 KB, L2-resident; one cluster runs the whole run: "
+                                                  "cluster barriers, serial per-individual draws and exact-order "
+                                                  "dots bound a generation (DESIGN.md); eager_us_per_phase: the "
+                                                  "per-generation multi-kernel path's phases (events between kernels)"},
         "cpu_baseline": cpu_baseline(G / cpu_s, "generations/s", 1,
                                      "build_shade(0.11, 180, 1.0), the full 1000 generations on its native stream, "
                                      "1 thread (a single run has no reference parallelism)"),
@@ -463,15 +489,16 @@ def hbm_update():
             out["frac_dram"] = out["gbps_dram"] / hbm
         return out
 
-    res["de_trial_kernel"] = rec("de_trial_kernel", ph["trial"], trial_alg,
+    res["de_trial_vec_kernel"] = rec("de_trial_vec_kernel", ph["trial"], trial_alg,
                                  f"5*s*P*D algorithmic; compulsory DRAM 2*s*P*D = {trial_min / 1e6:.0f} MB "
                                  f"(donor rows hit L2)")
-    res["de_trial_kernel"]["frac_compulsory"] = trial_min / (ph["trial"] * 1e-3) / 1e9 / hbm
+    res["de_trial_vec_kernel"]["frac_compulsory"] = trial_min / (ph["trial"] * 1e-3) / 1e9 / hbm
     winners = statistics.median(wins)  # rows replaced (fitness changed) per generation
     res["de_select_apply_kernel"] = rec("de_select_apply_kernel", ph["select_apply"], int(3 * s * winners * D),
                                         f"s*D*(trial read + parent read + write) per winner; {winners:.0f} of {P} "
                                         f"trials won (median of the timed generations)")
-    res["de_select_scan_kernel"] = {"us": ph["select_scan"] * 1e3, "note": "flags, prefix sums, archive slots"}
+    res["de_select_multi_kernel"] = {"us": ph["select_scan"] * 1e3,
+                                     "note": "flags, look-back prefix sums over ticketed CTAs, archive slots"}
     res["de_phase_us"] = {k: v * 1e3 for k, v in ph.items()}
     # PSO update (config 3's rule) at the same size
     eng2 = PSOEngine(pso_config3("gbest"), P, D)

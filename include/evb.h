@@ -311,7 +311,8 @@ EVB_API int evb_de_last_draws(evb_de e, int64_t* word_counts, int64_t* archive_w
  * gen0+1 ...); otherwise continue from the given populations (ids gen0 ...).  Supports the `de`
  * preset family: rand_1 / best_1, binomial, clip / midpoint_target, fixed F, CR, no archive;
  * the run state must fit in shared memory (else use evb_de_generation per run).  rec (may be
- * NULL): run r's evaluations are recorded into recorder run r, in FE order. */
+ * NULL): run r's evaluations are recorded into recorder run r, in FE order.  Asynchronous on
+ * `stream` (the call returns once the launch is queued). */
 EVB_API int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int pop_size, int dim,
                         const evb_problem* problems, const uint64_t* keys, int generations, double lb,
                         double ub, void* pops, void* fits, int init, uint32_t gen0, evb_recorder rec,

@@ -294,6 +294,9 @@ int evb_problem_create_composition(int dtype, int dim, int n_comp, const int* ki
       p.comp_sigma = static_cast<double*>(upload(sigma, sizeof(double) * n_comp));
       p.comp_lambda = static_cast<double*>(upload(lambda, sizeof(double) * n_comp));
       p.comp_bias = static_cast<double*>(upload(comp_bias, sizeof(double) * n_comp));
+      p.h_comp_sigma.assign(sigma, sigma + n_comp);
+      p.h_comp_lambda.assign(lambda, lambda + n_comp);
+      p.h_comp_bias.assign(comp_bias, comp_bias + n_comp);
     } catch (...) {
       free_problem(p);
       delete h;

@@ -85,6 +85,8 @@ struct evb_de_s {
   unsigned long long* d_sel_agg = nullptr;   // ceil(P / kSelBlockItems)
   unsigned* d_sel_sync = nullptr;            // 2
   double* d_srec = nullptr;                  // 3 x P: persistent generations' success records
+  int run_nc = -1;                           // persistent generations: cluster size chosen (0: none fits)
+  size_t run_smem = 0;
   void* archive = nullptr;    // archive_cap x ldt
   int* d_arch_size = nullptr;
   int* d_write_index = nullptr;
@@ -2217,7 +2219,11 @@ bool run_generations_t(evb_de_s* e, const device_problem* prob, void* pop, int64
   a.G = n;
   a.Q = Q;
   a.srec = e->d_srec;
-  EVB_CUDA(cudaFuncSetAttribute(de_run_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  static bool attr = [] {
+    EVB_CUDA(cudaFuncSetAttribute(de_run_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    return true;
+  }();
+  (void)attr;
   cudaLaunchConfig_t lc{};
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -2228,18 +2234,30 @@ bool run_generations_t(evb_de_s* e, const device_problem* prob, void* pop, int64
   lc.attrs = at;
   lc.numAttrs = 1;
   int nc = NC;
-  for (;;) {  // a cluster this size must fit on one GPC with this shared memory
-    at[0].val.clusterDim.x = unsigned(nc);
-    lc.gridDim = dim3(nc);
-    lc.dynamicSmemBytes = smem_for((P + nc - 1) / nc, nc);
-    if (lc.dynamicSmemBytes > 200 * 1024) return false;
-    int active = 0;
-    if (cudaOccupancyMaxActiveClusters(&active, de_run_kernel<T>, &lc) == cudaSuccess && active >= 1) break;
-    cudaGetLastError();
-    if (nc == 1) return false;
-    nc = std::max(1, nc / 2);
-    if ((P + nc - 1) / nc > 32) return false;
+  if (e->run_nc < 0) {  // once per engine: the largest cluster that fits one GPC with its shared memory
+    e->run_nc = 0;
+    for (;;) {
+      at[0].val.clusterDim.x = unsigned(nc);
+      lc.gridDim = dim3(nc);
+      lc.dynamicSmemBytes = smem_for((P + nc - 1) / nc, nc);
+      if (lc.dynamicSmemBytes > 200 * 1024) break;
+      int active = 0;
+      if (cudaOccupancyMaxActiveClusters(&active, de_run_kernel<T>, &lc) == cudaSuccess && active >= 1) {
+        e->run_nc = nc;
+        e->run_smem = lc.dynamicSmemBytes;
+        break;
+      }
+      cudaGetLastError();
+      if (nc == 1) break;
+      nc = std::max(1, nc / 2);
+      if ((P + nc - 1) / nc > 32) break;
+    }
   }
+  if (e->run_nc <= 0) return false;
+  nc = e->run_nc;
+  at[0].val.clusterDim.x = unsigned(nc);
+  lc.gridDim = dim3(nc);
+  lc.dynamicSmemBytes = e->run_smem;
   a.Q = (P + nc - 1) / nc;
   static const bool prof = std::getenv("EVB_DE_PERSIST_PROFILE") != nullptr;
   if (prof) {

@@ -85,6 +85,8 @@ struct fused_params {
   int tiles_nfast;  // multi kernel: blockIdx.x walks column tiles (row blocks form the waves)
   unsigned long long* dbg_ts;  // EVB_K1_TIMELINE=1 (tuning aid): per-CTA globaltimer phase stamps
   int dbg_skip;  // EVB_K2_SKIP (tuning aid, wrong results): bit 0 = no S split, bit 1 = no MMAs
+  int b_early;   // split-K fp32: the rotation split predates this launch, its first B slices may
+                 // load before griddep_wait (they do not depend on the preceding kernel)
 };
 
 // cosine of the fused epilogue: library cos for fp64.  fp32 (a tolerance path: 3xTF32 / FFMA
@@ -1188,6 +1190,20 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN>::THREADS, 1)
   ptx::cluster_sync_all();  // every CTA's barriers exist before the first multicast / remote commit
   umma::fence_after();
   const uint32_t tmem = *tmem_slot;
+  // B producer: with PDL the first B slices (the problem's immutable rotation split) may load
+  // while the predecessor still runs; everything else waits for it
+  const int b_pre = p.b_early ? min(KT, C::NB) : 0;
+  if (warp == 10 && lane == 0) {
+    ptx::prefetch_tma(&tmMhi);
+    ptx::prefetch_tma(&tmMlo);
+    for (int kb = 0; kb < b_pre; ++kb) {
+      uint8_t* st = smem + C::B_OFF + kb * C::B_BYTES + mx * (BN / 2) * 128;
+      ptx::mbar_arrive_expect_tx(&bfull[kb], C::B_BYTES);
+      ptx::tma_load_2d_mc(st, &tmMhi, &bfull[kb], (kb0 + kb) * C::KB, n0 + int(mx) * (BN / 2), pair_mask);
+      ptx::tma_load_2d_mc(st + C::B_BYTES / 2, &tmMlo, &bfull[kb], (kb0 + kb) * C::KB, n0 + int(mx) * (BN / 2),
+                          pair_mask);
+    }
+  }
   ptx::griddep_wait();  // PDL: barrier init and TMEM allocation overlap the predecessor's tail
   ptx::griddep_launch_dependents();
 
@@ -1204,9 +1220,7 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN>::THREADS, 1)
     }
   } else if (warp == 10) {
     if (lane == 0) {  // ---------------- B producer (M_hi, M_lo) ----------------
-      ptx::prefetch_tma(&tmMhi);
-      ptx::prefetch_tma(&tmMlo);
-      for (int kb = 0; kb < KT; ++kb) {
+      for (int kb = b_pre; kb < KT; ++kb) {
         const int s = kb % C::NB;
         if (kb >= C::NB) ptx::mbar_wait(&bempty[s], ((kb / C::NB) - 1) & 1);
         uint8_t* st = smem + C::B_OFF + s * C::B_BYTES + mx * (BN / 2) * 128;  // this CTA's half of the rows
@@ -1783,7 +1797,9 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
       const int64_t mel = int64_t(D) * ldm;
       void* rhi = nullptr;
       void* rlo = nullptr;
-      if (own_rot && pr->rot_hi) {
+      const bool split_cached = own_rot && pr->rot_hi;
+      fp.b_early = split_cached ? 1 : 0;
+      if (split_cached) {
         rhi = pr->rot_hi;
         rlo = pr->rot_lo;
       } else {

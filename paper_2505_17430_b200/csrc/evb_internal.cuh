@@ -96,7 +96,8 @@ struct device_problem {
   // composition (problems/instance.hpp:33-41, 116-174)
   int n_comp = 0;
   int* comp_kinds = nullptr;
-  std::vector<int> h_comp_kinds;  // host copy (no device->host read on the evaluation path)
+  std::vector<int> h_comp_kinds;  // host copies (no device->host read on the evaluation path)
+  std::vector<double> h_comp_sigma, h_comp_lambda, h_comp_bias;
   void* comp_shift = nullptr;  // n_comp x ld
   void* comp_rot = nullptr;    // n_comp x dim x ld
   double* comp_sigma = nullptr;

@@ -157,7 +157,9 @@ int evb_evo_bench_de(int dtype, const evb_de_config* cfg, int pop_size, int dim,
       const int rc = evb_de_runs(dtype, cfg, tasks, P, D, task_problem.data(), keys.data(), gens, lb, ub, pops, fits,
                                  1, 0u, rec, stream);
       cudaError_t e = cudaSuccess;
-      if (rc == EVB_OK) e = cudaMemcpy(fit_host.data(), fits, fit_host.size(), cudaMemcpyDeviceToHost);
+      if (rc == EVB_OK) e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));  // de_runs is asynchronous
+      if (rc == EVB_OK && e == cudaSuccess)
+        e = cudaMemcpy(fit_host.data(), fits, fit_host.size(), cudaMemcpyDeviceToHost);
       cudaFree(pops);
       cudaFree(fits);
       check_status(rc);

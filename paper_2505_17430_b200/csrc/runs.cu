@@ -682,12 +682,10 @@ extern "C" int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int 
         q.kind[0] = p.kind;
       } else {
         q.n_comp = p.n_comp;
-        std::vector<int> kinds(p.n_comp);
-        std::vector<double> sg(p.n_comp), la(p.n_comp), cb(p.n_comp);
-        EVB_CUDA(cudaMemcpy(kinds.data(), p.comp_kinds, sizeof(int) * p.n_comp, cudaMemcpyDeviceToHost));
-        EVB_CUDA(cudaMemcpy(sg.data(), p.comp_sigma, sizeof(double) * p.n_comp, cudaMemcpyDeviceToHost));
-        EVB_CUDA(cudaMemcpy(la.data(), p.comp_lambda, sizeof(double) * p.n_comp, cudaMemcpyDeviceToHost));
-        EVB_CUDA(cudaMemcpy(cb.data(), p.comp_bias, sizeof(double) * p.n_comp, cudaMemcpyDeviceToHost));
+        const std::vector<int>& kinds = p.h_comp_kinds;  // host copies made at creation
+        const std::vector<double>& sg = p.h_comp_sigma;
+        const std::vector<double>& la = p.h_comp_lambda;
+        const std::vector<double>& cb = p.h_comp_bias;
         for (int c = 0; c < p.n_comp; ++c) {
           q.shift[c] = static_cast<const double*>(p.comp_shift) + size_t(c) * p.ld;
           q.rot[c] = static_cast<const double*>(p.comp_rot) + size_t(c) * dim * p.ld;
@@ -699,10 +697,28 @@ extern "C" int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int 
       }
     }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    run_problem* dprobs = nullptr;
-    uint64_t* dkeys = nullptr;
-    EVB_CUDA(cudaMalloc(&dprobs, sizeof(run_problem) * n_runs));
-    EVB_CUDA(cudaMalloc(&dkeys, sizeof(uint64_t) * n_runs));
+    // the run table and keys in a per-thread device buffer reused across calls (a call on another
+    // stream first waits for the previous launch that read it)
+    struct table_cache {
+      void* buf = nullptr;
+      size_t cap = 0;
+      cudaEvent_t done = nullptr;
+    };
+    static thread_local table_cache tc_;
+    const size_t tbytes = (sizeof(run_problem) * n_runs + 15) / 16 * 16 + sizeof(uint64_t) * n_runs;
+    if (!tc_.done) EVB_CUDA(cudaEventCreateWithFlags(&tc_.done, cudaEventDisableTiming));
+    EVB_CUDA(cudaStreamWaitEvent(st, tc_.done, 0));
+    if (tc_.cap < tbytes) {
+      EVB_CUDA(cudaEventSynchronize(tc_.done));
+      if (tc_.buf) EVB_CUDA(cudaFree(tc_.buf));
+      tc_.buf = nullptr;
+      tc_.cap = 0;
+      EVB_CUDA(cudaMalloc(&tc_.buf, tbytes));
+      tc_.cap = tbytes;
+    }
+    run_problem* dprobs = static_cast<run_problem*>(tc_.buf);
+    uint64_t* dkeys = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(tc_.buf) +
+                                                  (sizeof(run_problem) * n_runs + 15) / 16 * 16);
     EVB_CUDA(cudaMemcpyAsync(dprobs, rp.data(), sizeof(run_problem) * n_runs, cudaMemcpyHostToDevice, st));
     EVB_CUDA(cudaMemcpyAsync(dkeys, keys, sizeof(uint64_t) * n_runs, cudaMemcpyHostToDevice, st));
     runs_args a{};
@@ -753,7 +769,11 @@ extern "C" int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int 
     a.tc_epi = a.tc && (epi_env ? std::atoi(epi_env) != 0 : 1);
     const size_t smem = runs_smem(pop_size, dim, a.split, a.resident ? a.n_mat : 1, a.tc);
     require(smem <= 227 * 1024, "de_runs: run state does not fit in shared memory");
-    EVB_CUDA(cudaFuncSetAttribute(de_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    static thread_local size_t smem_set = 0;
+    if (smem > smem_set) {
+      EVB_CUDA(cudaFuncSetAttribute(de_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      smem_set = smem;
+    }
     static const bool prof = std::getenv("EVB_RUNS_PROFILE") != nullptr;
     unsigned long long* dprof = nullptr;
     if (prof) {
@@ -782,8 +802,9 @@ extern "C" int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int 
     }
     count_launch();
     if (err == cudaSuccess) err = cudaGetLastError();
-    EVB_CUDA(cudaStreamSynchronize(st));
+    EVB_CUDA(cudaEventRecord(tc_.done, st));  // the run table may be rewritten once this launch is done
     if (dprof) {
+      EVB_CUDA(cudaStreamSynchronize(st));
       unsigned long long h[16];
       EVB_CUDA(cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost));
       cudaFree(dprof);
@@ -792,8 +813,6 @@ extern "C" int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int 
       for (int k = 0; k < 10; ++k) line += std::string(" ") + names[k] + "=" + std::to_string(h[k] / std::max(1, generations));
       std::fprintf(stderr, "%s\n", line.c_str());
     }
-    cudaFree(dprobs);
-    cudaFree(dkeys);
     EVB_CUDA(err);
   });
 }

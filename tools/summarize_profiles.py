@@ -27,6 +27,10 @@ METRICS = [
     "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
     "lts__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+    "sm__ops_path_tensor_op_utchmma_src_tf32_dst_fp32_sparsity_off.sum.pct_of_peak_sustained_elapsed",
+    "sm__ops_path_tensor_op_utchmma_src_tf32_dst_fp32_sparsity_off.sum.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_op_utchmma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
 ]
 
 
@@ -64,9 +68,9 @@ def main():
                "kernels": {}}
     traffic = {}
     for name, rep in (("eval_f64_multi", "eval_multi.ncu-rep"), ("eval_f64_dmma", "eval_f64.ncu-rep"),
-                      ("eval_f32_ffma", "eval_f32.ncu-rep"),
+                      ("eval_f32_umma_sk", "eval_f32.ncu-rep"),
                       ("de_runs", "runs.ncu-rep"), ("updates", "updates.ncu-rep"),
-                      ("updates", "pso_update.ncu-rep")):
+                      ("updates", "pso_update.ncu-rep"), ("de_run", "de_run.ncu-rep")):
         p = SRC / rep
         if not p.exists():
             continue
@@ -88,10 +92,16 @@ def main():
                 e["algorithmic_flop"] = 3 * 2.0 * 1000 * 1000 * 1024
                 e["achieved_TFLOPs_under_ncu"] = e["algorithmic_flop"] / (dur * 1e-6) / 1e12
                 traffic["eval_f64_dmma_multi_kernel"] = rd + wr
+            if name == "eval_f32_umma_sk":
+                e["algorithmic_flop"] = 2.0 * 1000 * 1000 * 1024
+                e["achieved_TFLOPs_under_ncu"] = e["algorithmic_flop"] / (dur * 1e-6) / 1e12
+                traffic["eval_f32_umma_sk_kernel"] = rd + wr
             if "pso_update" in kn:
+                traffic["pso_update_vec_kernel"] = rd + wr
                 e["algorithmic_bytes"] = 5 * 8 * 16384 * 1000
                 e["algorithmic_GBps"] = e["algorithmic_bytes"] / (dur * 1e-6) / 1e9
             if "de_trial" in kn:
+                traffic["de_trial_vec_kernel"] = rd + wr
                 e["algorithmic_bytes"] = 5 * 8 * 16384 * 1000
                 e["algorithmic_GBps"] = e["algorithmic_bytes"] / (dur * 1e-6) / 1e9
             key = f"{name}:{kn[:90]}"
@@ -101,15 +111,17 @@ def main():
                 i += 1
             summary["kernels"][key] = e
     (DST / f"ncu_summary_{tag}.json").write_text(json.dumps(summary, indent=1))
-    (DST / "traffic.json").write_text(json.dumps(traffic, indent=1))
+    old = json.loads((DST / "traffic.json").read_text()) if (DST / "traffic.json").exists() else {}
+    old.update(traffic)
+    (DST / "traffic.json").write_text(json.dumps(old, indent=1))
     lc = SRC / "bench_launches.csv"
     if lc.exists():
         shutil.copy(lc, DST / f"bench_launches_{tag}.csv")
-    for name in ("eval_multi", "eval_f64", "eval_f32", "runs", "updates", "pso_update"):
+    for name in ("eval_multi", "eval_f64", "eval_f32", "runs", "updates", "pso_update", "de_run"):
         rep = SRC / f"{name}.ncu-rep"
         if rep.exists():
             shutil.copy(rep, DST / f"{name}_{tag}.ncu-rep")
-    for f in ("hbm_plain.json", "bench_plain.log"):
+    for f in ("hbm_plain.json", "bench_plain.log", "de_run_plain.log", "runs_plain.log"):
         if (SRC / f).exists():
             shutil.copy(SRC / f, DST / f"{Path(f).stem}_{tag}{Path(f).suffix}")
     print(json.dumps(summary, indent=1)[:6000])
