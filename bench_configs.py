@@ -178,6 +178,30 @@ def config0():
         cur.synchronize()
 
     e2e_s = wall_median(host_generation_engine, 500)
+    # the reference caller's shape in C++: de_engine state in host memory, one generation per call
+    # through evb_de_generations_host (libevb_refshape.so, no Python in the loop)
+    cxx = None
+    try:
+        import ctypes
+
+        R = ctypes.CDLL(str(ROOT / "paper_2505_17430_b200" / "libevb_refshape.so"))
+        R.evb_refshape_time_de.restype = ctypes.c_int
+        hp3 = state_h[:P * D].numpy().reshape(P, D).copy()
+        hf3 = state_h[P * D:].numpy().copy()
+        us = (ctypes.c_double * 5)()
+        mr = np.ascontiguousarray(m)
+        rc = R.evb_refshape_time_de(D, P, ctypes.c_void_p(o.ctypes.data), ctypes.c_void_p(mr.ctypes.data),
+                                    ctypes.c_void_p(hp3.ctypes.data), ctypes.c_void_p(hf3.ctypes.data),
+                                    ctypes.c_uint64(42), 2000, 5, ctypes.c_double(0.3), us)
+        if rc == 0:
+            u = statistics.median(list(us))
+            cxx = {"value": 1e6 / u, "unit": "generations/s", "us_per_generation": u,
+                   "h2d_bytes_per_step": P * D * 8 + P * 8, "d2h_bytes_per_step": P * D * 8 + P * 8,
+                   "how": "C++ over the C ABI: evb_de_generations_host(engine, problem, host pop, host fitness, 1) "
+                          "per generation (one copy in, the persistent kernel, one copy out, synchronous); wall clock, "
+                          "median of 5 blocks"}
+    except OSError as exc:
+        cxx = {"unavailable": str(exc)}
     cpu_s = O.REF_FAST().ref_bench_de(0, P, D, 2000, 5, O.ptr(o), O.ptr(np.ascontiguousarray(m)), 42)
     cpu_gps = 2000 / cpu_s
     return {
@@ -195,7 +219,8 @@ def config0():
                        "(DEEngine.generations(1): the persistent cluster kernel), back to the host; wall clock incl. "
                        "copies and sync, median of 5 blocks",
                 "k8": {"value": 1.0 / e2e_k8_s, "unit": "generations/s", "us_per_generation": e2e_k8_s * 1e6,
-                       "how": "the same step through de_runs (K8, one generation)"}},
+                       "how": "the same step through de_runs (K8, one generation)"},
+                "cxx_host_state": cxx},
         "roofline": {"bound": "latency", "note": "about 20 KFLOP and 80 KB per generation (SURVEY §8(d)): "
                                                   "launch and dependency latency, no throughput roofline"},
         "cpu_baseline": cpu_baseline(cpu_gps, "generations/s", 1,

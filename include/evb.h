@@ -258,6 +258,12 @@ EVB_API int evb_de_generation(evb_de e, evb_problem objective, evb_scratch s, vo
  * device-resident), removing per-kernel launch overhead for small populations. */
 EVB_API int evb_de_generations(evb_de e, evb_problem objective, evb_scratch s, void* pop, int64_t ldp,
                                void* fitness, double lb, double ub, evb_rng rng, int n, void* stream);
+/* n generations on a HOST-resident population / fitness (row stride ldp elements), the shape of the
+ * reference's de_engine (whose population lives on the host): one copy in, evb_de_generations on
+ * the engine's own stream, one copy out; returns when the host arrays hold the result.  Fixed
+ * population size only. */
+EVB_API int evb_de_generations_host(evb_de e, evb_problem objective, evb_scratch s, void* pop_host, int64_t ldp,
+                                    void* fitness_host, double lb, double ub, evb_rng rng, int n);
 /* init_population (core/population.hpp:88-98) from the rng. */
 EVB_API int evb_de_init_population(evb_de e, void* pop, int64_t ldp, double lb, double ub, evb_rng rng,
                                    void* stream);

@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 #include <string>
 #include <limits>
@@ -86,6 +87,11 @@ struct evb_de_s {
   unsigned* d_sel_sync = nullptr;            // 2
   double* d_srec = nullptr;                  // 3 x P: persistent generations' success records
   int run_nc = -1;                           // persistent generations: cluster size chosen (0: none fits)
+  // host-state generations (evb_de_generations_host): packed device [population | fitness], its
+  // page-locked staging and the engine's own stream
+  void* hs_dev = nullptr;
+  void* hs_pinned = nullptr;
+  cudaStream_t hs_stream = nullptr;
   size_t run_smem = 0;
   void* archive = nullptr;    // archive_cap x ldt
   int* d_arch_size = nullptr;
@@ -2197,7 +2203,9 @@ bool run_generations_t(evb_de_s* e, const device_problem* prob, void* pop, int64
     cudaGetLastError();
     return v;
   }();
-  const int NC = std::min(max_nc, std::max(1, (P + 7) / 8));
+  static const char* nc_env = std::getenv("EVB_DE_PERSIST_NC");  // tuning override
+  const int NC = nc_env ? std::min(max_nc, std::max((P + 31) / 32, std::atoi(nc_env)))
+                        : std::min(max_nc, std::max(1, (P + 7) / 8));
   const int Q = (P + NC - 1) / NC;
   if (Q > 32) return false;
   const int H = std::max(1, e->cfg.memory_size);
@@ -2326,6 +2334,9 @@ void* dalloc(size_t n) {
 void free_de(evb_de_s* e) {
   if (e->graph) cudaGraphExecDestroy(e->graph);
   if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
+  if (e->hs_dev) cudaFree(e->hs_dev);
+  if (e->hs_pinned) cudaFreeHost(e->hs_pinned);
+  if (e->hs_stream) cudaStreamDestroy(e->hs_stream);
   void* ptrs[] = {e->trial, e->trial_fit, e->F, e->CR, e->slot, e->idx, e->jrand, e->xlen, e->rword, e->woff, e->wcount, e->order,
                   e->win, e->arch_slot, e->owner, e->succ, e->wlist, e->d_npush, e->d_epoch, e->d_owner64, e->d_sel_agg,
                   e->d_sel_sync, e->d_srec, e->archive, e->d_arch_size, e->d_write_index,
@@ -2687,6 +2698,51 @@ int evb_de_generations(evb_de e, evb_problem objective, evb_scratch s, void* pop
       ++e->gen_count;
       count_launch(e->g_kernels);
     }
+  });
+}
+
+// n generations on a host-resident population (the reference's engine keeps its population on
+// the host): the rows go into the engine's page-locked staging, cross the host link as one copy
+// with the fitness, run as evb_de_generations (one persistent launch where eligible), and come
+// back the same way; synchronous, like de_engine::generation.
+int evb_de_generations_host(evb_de e, evb_problem objective, evb_scratch s, void* pop_host, int64_t ldp,
+                            void* fitness_host, double lb, double ub, evb_rng rng, int n) {
+  const int rc0 = guarded([&] {
+    require(e && objective && rng && pop_host && fitness_host, "de_generations_host: null argument");
+    require(n >= 0, "de_generations_host: negative count");
+    if (ldp < e->D) throw invalid_argument("de_generations_host: ldp < dim");
+    require(e->reduction == 0, "de_generations_host: linear population reduction changes the population size");
+    const size_t es = e->dtype == EVB_F64 ? 8 : 4;
+    const size_t row = es * size_t(e->D), bytes = es * (size_t(e->P) * e->D + e->P);
+    if (!e->hs_dev) {
+      EVB_CUDA(cudaMalloc(&e->hs_dev, bytes));
+      EVB_CUDA(cudaHostAlloc(&e->hs_pinned, bytes, cudaHostAllocPortable));
+      EVB_CUDA(cudaStreamCreateWithFlags(&e->hs_stream, cudaStreamNonBlocking));
+    }
+    uint8_t* hp = static_cast<uint8_t*>(e->hs_pinned);
+    const uint8_t* src = static_cast<const uint8_t*>(pop_host);
+    if (size_t(ldp) * es == row) std::memcpy(hp, src, row * e->P);
+    else
+      for (int i = 0; i < e->P; ++i) std::memcpy(hp + row * i, src + size_t(ldp) * es * i, row);
+    std::memcpy(hp + row * e->P, fitness_host, es * e->P);
+    EVB_CUDA(cudaMemcpyAsync(e->hs_dev, hp, bytes, cudaMemcpyHostToDevice, e->hs_stream));
+  });
+  if (rc0 != EVB_OK) return rc0;
+  const size_t es = e->dtype == EVB_F64 ? 8 : 4;
+  uint8_t* dv = static_cast<uint8_t*>(e->hs_dev);
+  const int rc = evb_de_generations(e, objective, s, dv, e->D, dv + es * size_t(e->P) * e->D, lb, ub, rng, n,
+                                    e->hs_stream);
+  if (rc != EVB_OK) return rc;
+  return guarded([&] {
+    const size_t row = es * size_t(e->D), bytes = es * (size_t(e->P) * e->D + e->P);
+    EVB_CUDA(cudaMemcpyAsync(e->hs_pinned, e->hs_dev, bytes, cudaMemcpyDeviceToHost, e->hs_stream));
+    EVB_CUDA(cudaStreamSynchronize(e->hs_stream));
+    const uint8_t* hp = static_cast<const uint8_t*>(e->hs_pinned);
+    uint8_t* dst = static_cast<uint8_t*>(pop_host);
+    if (size_t(ldp) * es == row) std::memcpy(dst, hp, row * e->P);
+    else
+      for (int i = 0; i < e->P; ++i) std::memcpy(dst + size_t(ldp) * es * i, hp + row * i, row);
+    std::memcpy(fitness_host, hp + row * e->P, es * e->P);
   });
 }
 

@@ -55,3 +55,51 @@ int evb_refshape_time(int n_kinds, const int* kinds, int dim, int n_points, cons
     return -1;
   }
 }
+
+// BASELINE config 0 as the reference's caller runs it: the population and fitness live in host
+// memory (de_engine's state), one DE generation per call (de_engine::generation), here
+// evb_de_generations_host(…, 1) — one copy in, the persistent cluster kernel, one copy out.
+// preset `de` (rand/1/bin, F 0.5, CR 0.9, clip), Rastrigin on the given (pre-scaled) rotation.
+extern "C" __attribute__((visibility("default"))) int evb_refshape_time_de(int dim, int pop_size, const double* shift,
+                                                                           const double* rotation, double* pop,
+                                                                           double* fit, uint64_t key, int steps,
+                                                                           int blocks, double warm_s,
+                                                                           double* us_per_step);
+
+int evb_refshape_time_de(int dim, int pop_size, const double* shift, const double* rotation, double* pop, double* fit,
+                         uint64_t key, int steps, int blocks, double warm_s, double* us_per_step) {
+  evb_problem prob = nullptr;
+  evb_de eng = nullptr;
+  evb_rng rng = nullptr;
+  int rc = evb_problem_create_base(EVB_F64, dim, EVB_RASTRIGIN, shift, rotation, 0.0, &prob);
+  evb_de_config cfg{};
+  cfg.mutation = EVB_MUT_RAND1;
+  cfg.crossover = EVB_CX_BINOMIAL;
+  cfg.repair = EVB_REP_CLIP;
+  cfg.parameter = EVB_PAR_FIXED;
+  cfg.f = 0.5;
+  cfg.cr = 0.9;
+  cfg.memory_size = 1;
+  if (rc == EVB_OK) rc = evb_de_create(EVB_F64, &cfg, pop_size, dim, &eng);
+  if (rc == EVB_OK) rc = evb_rng_create_philox(key, &rng);
+  auto step = [&] { return evb_de_generations_host(eng, prob, nullptr, pop, dim, fit, -100.0, 100.0, rng, 1); };
+  using clk = std::chrono::steady_clock;
+  if (rc == EVB_OK) {
+    const auto t_w = clk::now();
+    int n_w = 0;
+    while (rc == EVB_OK && (n_w < 3 || std::chrono::duration<double>(clk::now() - t_w).count() < warm_s)) {
+      rc = step();
+      ++n_w;
+    }
+  }
+  const int per = std::max(1, steps / std::max(1, blocks));
+  for (int b = 0; b < blocks && rc == EVB_OK; ++b) {
+    const auto t0 = clk::now();
+    for (int s = 0; s < per && rc == EVB_OK; ++s) rc = step();
+    us_per_step[b] = std::chrono::duration<double, std::micro>(clk::now() - t0).count() / per;
+  }
+  if (rng) evb_rng_destroy(rng);
+  if (eng) evb_de_destroy(eng);
+  if (prob) evb_problem_destroy(prob);
+  return rc == EVB_OK ? 0 : -1;
+}

@@ -114,6 +114,7 @@ def _sigs():
         "evb_de_generation": (c_int, [vp, vp, vp, vp, i64, vp, c_double, c_double, vp, vp]),
         "evb_de_init_population": (c_int, [vp, vp, i64, c_double, c_double, vp, vp]),
         "evb_de_generations": (c_int, [vp, vp, vp, vp, i64, vp, c_double, c_double, vp, c_int, vp]),
+        "evb_de_generations_host": (c_int, [vp, vp, vp, vp, i64, vp, c_double, c_double, vp, c_int]),
         "evb_de_optimize": (c_int, [vp, vp, vp, vp, i64, vp, c_double, c_double, i64, vp, P(c_int), P(c_double),
                                     P(c_int), vp]),
         "evb_de_get_state": (c_int, [vp, vp, P(c_int), vp, vp, P(c_int)]),
@@ -227,6 +228,19 @@ class DEEngine:
         p, ld, f = self._pop(pop, fitness)
         check(_lib.lib().evb_de_generations(self._h, problem.handle, scratch.handle if scratch else None, p, ld, f,
                                             lb, ub, rng.handle, n, _stream_ptr(stream)), "de_generations")
+
+    def generations_host(self, problem: ProblemInstance, pop: np.ndarray, fitness: np.ndarray, lb: float, ub: float,
+                         rng: Rng, n: int, scratch: EvalScratch | None = None) -> None:
+        """n generations on a host (numpy) population / fitness, updated in place: the reference's
+        de_engine shape (one copy in, evb_de_generations, one copy out; synchronous)."""
+        nd = self._np()
+        if pop.dtype != nd or fitness.dtype != nd or pop.ndim != 2 or pop.shape[1] != self.dim \
+                or pop.shape[0] != self.pop_size or not pop.flags["C_CONTIGUOUS"] or not fitness.flags["C_CONTIGUOUS"]:
+            raise ConfigError("de: host population must be a C-contiguous (pop_size, dim) array of the engine dtype")
+        check(_lib.lib().evb_de_generations_host(self._h, problem.handle, scratch.handle if scratch else None,
+                                                 ctypes.c_void_p(pop.ctypes.data), pop.shape[1],
+                                                 ctypes.c_void_p(fitness.ctypes.data), lb, ub, rng.handle, n),
+              "de_generations_host")
 
     @property
     def current_pop_size(self) -> int:

@@ -754,3 +754,31 @@ def test_persistent_generations_equal_per_generation(dev, monkeypatch, cfg, P, D
         assert np.array_equal(st[2]["memory_f"], ref[2]["memory_f"])
         assert np.array_equal(st[2]["memory_cr"], ref[2]["memory_cr"])
         assert st[2]["write_index"] == ref[2]["write_index"]
+
+
+def test_generations_host_state_equals_device(dev):
+    """evb_de_generations_host (population / fitness in host memory, the reference engine's shape)
+    against evb_de_generations on device tensors: identical state after 1 + 25 generations."""
+    P, D = 100, 10
+    o, m = O.shift_rotation(42, D)
+    prob = evb.ProblemInstance.base(evb.BaseKind.rastrigin, o, m * 0.0512, 0.0)
+    cfg = preset_de(0.5, 0.9)
+    res = []
+    for host in (False, True):
+        eng = DEEngine(cfg, P, D)
+        rng = Rng.philox(42)
+        pop = torch.empty((P, D), dtype=torch.float64, device=dev)
+        eng.init_population(pop, -100.0, 100.0, rng)
+        fit = dev_eval(prob, pop, dev)
+        if host:
+            hp, hf = pop.cpu().numpy().copy(), fit.cpu().numpy().copy()
+            eng.generations_host(prob, hp, hf, -100.0, 100.0, rng, 1)
+            eng.generations_host(prob, hp, hf, -100.0, 100.0, rng, 25)
+            res.append((hp, hf))
+        else:
+            eng.generations(prob, pop, fit, -100.0, 100.0, rng, 1)
+            eng.generations(prob, pop, fit, -100.0, 100.0, rng, 25)
+            torch.cuda.synchronize()
+            res.append((pop.cpu().numpy(), fit.cpu().numpy()))
+    assert np.array_equal(res[0][0], res[1][0])
+    assert np.array_equal(res[0][1], res[1][1])
