@@ -718,6 +718,10 @@ def test_persistent_generations_equal_per_generation(dev, monkeypatch, cfg, P, D
         pop = torch.empty((P, D), dtype=dtype, device=dev)
         eng.init_population(pop, -100.0, 100.0, rng)
         fit = dev_eval(prob, pop, dev)
+        fit[5] = float("nan")  # a member that is never replaced and ranks after every number
+        fit[7:10] = fit[11]    # ties in the (fitness, index) order
+        fit[12] = -0.0
+        fit[13] = 0.0
         return eng, rng, pop, fit
 
     def state(eng, pop, fit):
