@@ -1485,6 +1485,7 @@ __global__ void __launch_bounds__(kRunThreads, 1) de_run_kernel(const de_run_arg
       }
     if (tid == 0) s_misc[0] = ldcg(d.arch_size);
     __syncthreads();
+    mark(11);
     if (ttpb || best) {  // (fitness, index) ranks, NaN last, over all threads: thread (i, chunk)
       // counts the members of its j chunk that precede i on order_key (integer shared atomics)
       const int nch = max(1, min(8, nthr / P));
@@ -2282,10 +2283,10 @@ bool run_generations_t(evb_de_s* e, const device_problem* prob, void* pop, int64
     unsigned long long h[16];
     EVB_CUDA(cudaMemcpy(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost));
     cudaFree(a.prof);
-    const char* names[] = {"order", "draws", "trial", "eval-base", "select+B1", "slots+B2", "apply+adapt", "B3",
-                           "x-o", "dots", "pre"};
+    const char* names[] = {"ranks", "draws", "trial", "eval-base", "select+B1", "slots+B2", "apply+adapt", "B3",
+                           "x-o", "dots", "pre", "loads"};
     std::string line = "[evb de_run] NC=" + std::to_string(nc) + " cycles/generation:";
-    for (int k = 0; k < 11; ++k) line += std::string(" ") + names[k] + "=" + std::to_string(h[k] / std::max(1, n));
+    for (int k = 0; k < 12; ++k) line += std::string(" ") + names[k] + "=" + std::to_string(h[k] / std::max(1, n));
     std::fprintf(stderr, "%s\n", line.c_str());
   }
   e->gen_P = P;

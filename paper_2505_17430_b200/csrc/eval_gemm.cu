@@ -1114,39 +1114,52 @@ __global__ void __launch_bounds__(umma_cfg<BN, FUSE>::THREADS, 1)
 // received half to its own (z = z_0 + z_1: fp add is commutative, the same in both CTAs) and runs
 // the usual epilogue on its 64 columns (terms, per-row channel sums, column-block partials,
 // last-CTA finalisation).  Deterministic, no float atomics.
-template <int BN>
+template <int BN, bool ATMEM>
 struct umma_sk_cfg {
   static constexpr int BM = 128;
   static constexpr int KB = 32;                   // floats per K slice (one 128-byte swizzle row)
-  static constexpr int X_BYTES = BM * 128;        // one X slice (TMA), split in place into S_hi
-  static constexpr int A_BYTES = 2 * BM * 128;    // S_hi (over X) + S_lo
+  static constexpr int X_BYTES = BM * 128;        // one X slice (TMA)
   static constexpr int B_BYTES = 2 * BN * 128;    // M_hi + M_lo of one slice (TMA, multicast pair)
-  // A and B rings apart, so X slices (and their split) run up to NA slices ahead of the MMAs
-  static constexpr int NA = 4, NB = (BN == 128 ? 3 : 2);
-  static constexpr int A_OFF = 0, B_OFF = NA * A_BYTES, O_OFF = B_OFF + NB * B_BYTES;
-  static constexpr int RING_BYTES = O_OFF + NA * KB * 4;  // + the shift slice of each A stage
-  static constexpr int NBAR = 3 * NA + 2 * NB + 1;
+  // ATMEM: S_hi / S_lo go to TMEM (the MMA's A operand from TMEM: shared memory then feeds only B,
+  //        which a 128 x 128 x 8 tf32 MMA otherwise reads at the full 128 B/clk with A);
+  //        X ring NX x 16 KB, A ring NA x (32 + 32) TMEM columns, B ring NB x 32 KB
+  // else:  S_hi over X and S_lo in shared memory: A ring NA x 32 KB
+  static constexpr int NX = ATMEM ? 4 : 0;
+  static constexpr int NA = 4;
+  static constexpr int NB = ATMEM ? 4 : (BN == 128 ? 3 : 2);
+  static constexpr int A_BYTES = ATMEM ? 0 : 2 * BM * 128;
+  static constexpr int X_OFF = 0;
+  static constexpr int A_OFF = NX * X_BYTES;
+  static constexpr int B_OFF = A_OFF + NA * A_BYTES;
+  static constexpr int O_OFF = B_OFF + NB * B_BYTES;
+  static constexpr int NSLOT = ATMEM ? NX : NA;  // stages carrying an X slice + its shift values
+  static constexpr int RING_BYTES = O_OFF + NSLOT * KB * 4;
+  static constexpr int NBAR = NSLOT + 2 * NA + 2 * NB + NX + 1;
   static constexpr int THREADS = 11 * 32;  // X producer, MMA, 8 split / epilogue warps, B producer
-  static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int RECV_BYTES = BM * (BN / 2) * 4;  // the peer's z_k of the owned columns (A ring)
+  static constexpr int TMEM_COLS = ATMEM ? 512 : 2 * BN;
+  static constexpr uint32_t TA = 2 * BN;  // first A column (ATMEM)
+  static constexpr int RECV_BYTES = BM * (BN / 2) * 4;  // the peer's z_k of the owned columns
   static constexpr int SMEM = RING_BYTES + 1024 + NBAR * 8 + 64;
-  static_assert(RECV_BYTES + 8192 <= NA * A_BYTES, "receive buffer + epilogue scratch in the drained A ring");
+  static_assert(!ATMEM || TA + NA * 2 * KB <= 512, "TMEM columns");
+  static_assert(RECV_BYTES + 8192 <= (ATMEM ? NX * X_BYTES + NB * B_BYTES : NA * A_BYTES),
+                "receive buffer + epilogue scratch in the drained rings");
   static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
-template <int BN>
-__global__ void __launch_bounds__(umma_sk_cfg<BN>::THREADS, 1)
+template <int BN, bool ATMEM>
+__global__ void __launch_bounds__(umma_sk_cfg<BN, ATMEM>::THREADS, 1)
     eval_f32_umma_sk_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmMhi,
                             const __grid_constant__ CUtensorMap tmMlo, const fused_params<float> p) {
-  using C = umma_sk_cfg<BN>;
+  using C = umma_sk_cfg<BN, ATMEM>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   uint64_t* xfull = reinterpret_cast<uint64_t*>(smem + C::RING_BYTES);  // X + shift slice landed
-  uint64_t* afull = xfull + C::NA;                                      // S_hi / S_lo formed
-  uint64_t* aempty = afull + C::NA;                                     // the MMAs read the stage
+  uint64_t* afull = xfull + C::NSLOT;                                   // S_hi / S_lo formed
+  uint64_t* aempty = afull + C::NA;                                     // the MMAs read the A stage
   uint64_t* bfull = aempty + C::NA;
   uint64_t* bempty = bfull + C::NB;
-  uint64_t* accfull = bempty + C::NB;
+  uint64_t* xempty = bempty + C::NB;  // ATMEM: the split warps read the X slot
+  uint64_t* accfull = xempty + C::NX;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accfull + 1);
   int* flags = reinterpret_cast<int*>(tmem_slot + 1);  // [1]: last column block of the row block
 
@@ -1173,8 +1186,9 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN>::THREADS, 1)
   if (threadIdx.x == 0) stamp(0);
 
   if (threadIdx.x == 0) {
+    for (int s = 0; s < C::NSLOT; ++s) ptx::mbar_init(&xfull[s], 1);
+    for (int s = 0; s < C::NX; ++s) ptx::mbar_init(&xempty[s], 8);
     for (int s = 0; s < C::NA; ++s) {
-      ptx::mbar_init(&xfull[s], 1);
       ptx::mbar_init(&afull[s], 8);
       ptx::mbar_init(&aempty[s], 1);
     }
@@ -1211,10 +1225,14 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN>::THREADS, 1)
     if (lane == 0) {  // ---------------- X producer: X slice + its 32 shift values ----------------
       ptx::prefetch_tma(&tmX);
       for (int kb = 0; kb < KT; ++kb) {
-        const int s = kb % C::NA;
-        if (kb >= C::NA) ptx::mbar_wait(&aempty[s], ((kb / C::NA) - 1) & 1);
+        const int s = kb % C::NSLOT;
+        if (kb >= C::NSLOT) {
+          if constexpr (ATMEM) ptx::mbar_wait(&xempty[s], ((kb / C::NSLOT) - 1) & 1);
+          else ptx::mbar_wait(&aempty[s], ((kb / C::NSLOT) - 1) & 1);
+        }
+        uint8_t* dst = ATMEM ? smem + C::X_OFF + s * C::X_BYTES : smem + C::A_OFF + s * C::A_BYTES;
         ptx::mbar_arrive_expect_tx(&xfull[s], C::X_BYTES + C::KB * 4);
-        ptx::tma_load_2d(smem + C::A_OFF + s * C::A_BYTES, &tmX, &xfull[s], (kb0 + kb) * C::KB, m0);
+        ptx::tma_load_2d(dst, &tmX, &xfull[s], (kb0 + kb) * C::KB, m0);
         ptx::bulk_load(smem + C::O_OFF + s * C::KB * 4, p.shift + size_t(kb0 + kb) * C::KB, C::KB * 4, &xfull[s]);
       }
     }
@@ -1241,16 +1259,29 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN>::THREADS, 1)
         ptx::mbar_wait(&bfull[sb], (kb / C::NB) & 1);
         if (kb == 0) stamp(1);
         umma::fence_after();
-        const uint32_t sa_hi = base + C::A_OFF + sa * C::A_BYTES, sa_lo = sa_hi + C::A_BYTES / 2;
         const uint32_t sb_hi = base + C::B_OFF + sb * C::B_BYTES, sb_lo = sb_hi + C::B_BYTES / 2;
+        if constexpr (ATMEM) {
+          const uint32_t ta_hi = tmem + C::TA + uint32_t(sa) * 2 * C::KB, ta_lo = ta_hi + C::KB;
 #pragma unroll
-        for (int k = 0; k < C::KB / 8; ++k) {
-          if (p.dbg_skip & 2) break;
-          const uint32_t off = k * 32;
-          const uint32_t acc0 = (kb | k) ? 1u : 0u;
-          umma::mma_tf32(tmem, umma::smem_desc(sa_hi + off), umma::smem_desc(sb_hi + off), idesc, acc0);
-          umma::mma_tf32(tcorr, umma::smem_desc(sa_lo + off), umma::smem_desc(sb_hi + off), idesc, acc0);
-          umma::mma_tf32(tcorr, umma::smem_desc(sa_hi + off), umma::smem_desc(sb_lo + off), idesc, 1u);
+          for (int k = 0; k < C::KB / 8; ++k) {
+            if (p.dbg_skip & 2) break;
+            const uint32_t off = k * 32, col = k * 8;
+            const uint32_t acc0 = (kb | k) ? 1u : 0u;
+            umma::mma_tf32_ts(tmem, ta_hi + col, umma::smem_desc(sb_hi + off), idesc, acc0);
+            umma::mma_tf32_ts(tcorr, ta_lo + col, umma::smem_desc(sb_hi + off), idesc, acc0);
+            umma::mma_tf32_ts(tcorr, ta_hi + col, umma::smem_desc(sb_lo + off), idesc, 1u);
+          }
+        } else {
+          const uint32_t sa_hi = base + C::A_OFF + sa * C::A_BYTES, sa_lo = sa_hi + C::A_BYTES / 2;
+#pragma unroll
+          for (int k = 0; k < C::KB / 8; ++k) {
+            if (p.dbg_skip & 2) break;
+            const uint32_t off = k * 32;
+            const uint32_t acc0 = (kb | k) ? 1u : 0u;
+            umma::mma_tf32(tmem, umma::smem_desc(sa_hi + off), umma::smem_desc(sb_hi + off), idesc, acc0);
+            umma::mma_tf32(tcorr, umma::smem_desc(sa_lo + off), umma::smem_desc(sb_hi + off), idesc, acc0);
+            umma::mma_tf32(tcorr, umma::smem_desc(sa_hi + off), umma::smem_desc(sb_lo + off), idesc, 1u);
+          }
         }
         umma::commit(&aempty[sa]);
         umma::commit_mc(&bempty[sb], pair_mask);  // the slot is freed in both CTAs of the M pair
@@ -1264,38 +1295,82 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN>::THREADS, 1)
     const int r = quarter * 32 + lane;
     const int row = m0 + r;
     const int etid = threadIdx.x - 64;
-    // S = X - o, S_hi = rna_tf32(S) over X, S_lo = rna_tf32(S - S_hi) into the stage's lo half
-    // (same SWIZZLE_128B positions: chunk q of row q / 8 holds logical chunk (q & 7) ^ (row & 7))
-    for (int kb = 0; kb < KT; ++kb) {
-      const int sa = kb % C::NA;
-      ptx::mbar_wait(&xfull[sa], (kb / C::NA) & 1);
-      float4* hi = reinterpret_cast<float4*>(smem + C::A_OFF + sa * C::A_BYTES);
-      float4* lo = reinterpret_cast<float4*>(smem + C::A_OFF + sa * C::A_BYTES + C::A_BYTES / 2);
-      const float4* osl = reinterpret_cast<const float4*>(smem + C::O_OFF + sa * C::KB * 4);
-      if (!(p.dbg_skip & 1)) {
+    auto split = [](float xq, float oq, uint32_t& hq, uint32_t& lq) {
+      const float sq = __fsub_rn(xq, oq);
+      hq = umma::rna_tf32_bits(sq);
+      lq = umma::rna_tf32_bits(__fsub_rn(sq, __uint_as_float(hq)));
+    };
+    if constexpr (ATMEM) {
+      // thread = row r (its TMEM lane), columns [16 half, 16 half + 16) of each slice: S from the
+      // swizzled X slot (logical chunk c of row r at physical chunk c ^ (r & 7)) into registers,
+      // the X slot released, S_hi / S_lo to the stage's TMEM columns
+      const uint32_t tlane = tmem + (uint32_t(quarter * 32) << 16);
+      for (int kb = 0; kb < KT; ++kb) {
+        const int sx = kb % C::NX, sa = kb % C::NA;
+        ptx::mbar_wait(&xfull[sx], (kb / C::NX) & 1);
+        const float4* xs = reinterpret_cast<const float4*>(smem + C::X_OFF + sx * C::X_BYTES) + r * 8;
+        const float4* osl = reinterpret_cast<const float4*>(smem + C::O_OFF + sx * C::KB * 4);
+        float4 xv[4], ov[4];
 #pragma unroll
-        for (int u = 0; u < C::X_BYTES / 16 / 256; ++u) {
-          const int q = etid + u * 256;
-          const int rr = q >> 3, c = (q & 7) ^ (rr & 7);
-          const float4 x = hi[q];
-          const float4 o = osl[c];
-          auto split = [](float xq, float oq, float& hq, float& lq) {
-            const float sq = __fsub_rn(xq, oq);
-            hq = __uint_as_float(umma::rna_tf32_bits(sq));
-            lq = __uint_as_float(umma::rna_tf32_bits(__fsub_rn(sq, hq)));
-          };
-          float4 h, l;
-          split(x.x, o.x, h.x, l.x);
-          split(x.y, o.y, h.y, l.y);
-          split(x.z, o.z, h.z, l.z);
-          split(x.w, o.w, h.w, l.w);
-          hi[q] = h;
-          lo[q] = l;
+        for (int u = 0; u < 4; ++u) {
+          const int c = 4 * half + u;
+          xv[u] = xs[c ^ (r & 7)];
+          ov[u] = osl[c];
         }
-        ptx::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&xempty[sx]);  // the X slot is free once read
+        uint32_t hv[16], lv[16];
+        if (!(p.dbg_skip & 1)) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            split(xv[u].x, ov[u].x, hv[4 * u + 0], lv[4 * u + 0]);
+            split(xv[u].y, ov[u].y, hv[4 * u + 1], lv[4 * u + 1]);
+            split(xv[u].z, ov[u].z, hv[4 * u + 2], lv[4 * u + 2]);
+            split(xv[u].w, ov[u].w, hv[4 * u + 3], lv[4 * u + 3]);
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) hv[q] = lv[q] = 0u;
+        }
+        if (kb >= C::NA) ptx::mbar_wait(&aempty[sa], ((kb / C::NA) - 1) & 1);  // the MMAs read this A stage
+        umma::fence_after();
+        const uint32_t ta = tlane + C::TA + uint32_t(sa) * 2 * C::KB + uint32_t(16 * half);
+        umma::tmem_st16(ta, hv);
+        umma::tmem_st16(ta + C::KB, lv);
+        umma::tmem_wait_st();
+        umma::fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&afull[sa]);
       }
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&afull[sa]);
+    } else {
+      // S = X - o, S_hi = rna_tf32(S) over X, S_lo = rna_tf32(S - S_hi) into the stage's lo half
+      // (same SWIZZLE_128B positions: chunk q of row q / 8 holds logical chunk (q & 7) ^ (row & 7))
+      for (int kb = 0; kb < KT; ++kb) {
+        const int sa = kb % C::NA;
+        ptx::mbar_wait(&xfull[sa], (kb / C::NA) & 1);
+        float4* hi = reinterpret_cast<float4*>(smem + C::A_OFF + sa * C::A_BYTES);
+        float4* lo = reinterpret_cast<float4*>(smem + C::A_OFF + sa * C::A_BYTES + C::A_BYTES / 2);
+        const float4* osl = reinterpret_cast<const float4*>(smem + C::O_OFF + sa * C::KB * 4);
+        if (!(p.dbg_skip & 1)) {
+#pragma unroll
+          for (int u = 0; u < C::X_BYTES / 16 / 256; ++u) {
+            const int q = etid + u * 256;
+            const int rr = q >> 3, c = (q & 7) ^ (rr & 7);
+            const float4 x = hi[q];
+            const float4 o = osl[c];
+            uint32_t h[4], l[4];
+            split(x.x, o.x, h[0], l[0]);
+            split(x.y, o.y, h[1], l[1]);
+            split(x.z, o.z, h[2], l[2]);
+            split(x.w, o.w, h[3], l[3]);
+            hi[q] = make_float4(__uint_as_float(h[0]), __uint_as_float(h[1]), __uint_as_float(h[2]), __uint_as_float(h[3]));
+            lo[q] = make_float4(__uint_as_float(l[0]), __uint_as_float(l[1]), __uint_as_float(l[2]), __uint_as_float(l[3]));
+          }
+          ptx::fence_proxy_async();
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&afull[sa]);
+      }
     }
     ptx::mbar_wait_sleep(accfull, 0);
     if (etid == 0) stamp(3);
@@ -1317,10 +1392,10 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN>::THREADS, 1)
 #pragma unroll
       for (int q = 0; q < 16; ++q) v[q] = __fadd_rn(__uint_as_float(a[q]), __uint_as_float(b[q]));
     };
-    float* recv = reinterpret_cast<float*>(smem + C::A_OFF);  // [BM][BN/2] in the drained A ring (nsk == 2)
+    float* recv = reinterpret_cast<float*>(smem);  // [BM][BN/2] in the drained rings (nsk == 2)
     auto rchunk = [&](int rr, int ch16) { return rr * (BN / 2) + 4 * ((ch16 & ~7) | ((ch16 & 7) ^ (rr & 7))); };
     if (nsk > 1) {
-      ptx::cluster_sync_all();  // both CTAs past their mainloops: the peer's A ring is drained
+      ptx::cluster_sync_all();  // both CTAs past their mainloops: the peer's rings are drained
       const int snd0 = (1 - kz) * OWN + half * TW;  // tile columns sent to the peer
       const uint32_t peer = ptx::mapa(ptx::smem_u32(recv), crank ^ 2u);  // the other K half
 #pragma unroll 1
@@ -1359,7 +1434,7 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN>::THREADS, 1)
           if (row < p.P && cb + q < p.D) p.zbuf[size_t(cb + q) * p.ldz + row] = v[q];
       }
     } else {
-      float* xs = reinterpret_cast<float*>(smem + C::A_OFF + C::RECV_BYTES);  // drained A ring: [half][ch][row]
+      float* xs = reinterpret_cast<float*>(smem + C::RECV_BYTES);  // drained rings: [half][ch][row]
       for (int ch = 0; ch < p.n_ch; ++ch) {
         const int term = p.ch_term[ch];
         float acc = term_is_product(term) ? 1.f : 0.f;
@@ -1669,11 +1744,11 @@ void launch_f32_umma(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUt
   count_launch();
 }
 
-template <int BN>
+template <int BN, bool ATMEM>
 void launch_f32_umma_sk(const CUtensorMap& tx, const CUtensorMap& b_hi, const CUtensorMap& b_lo,
                         const fused_params<float>& fp, int splitk, cudaStream_t st) {
-  using C = umma_sk_cfg<BN>;
-  auto kern = eval_f32_umma_sk_kernel<BN>;
+  using C = umma_sk_cfg<BN, ATMEM>;
+  auto kern = eval_f32_umma_sk_kernel<BN, ATMEM>;
   static bool attr = false;
   if (!attr) {
     EVB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -1689,7 +1764,7 @@ void launch_f32_umma_sk(const CUtensorMap& tx, const CUtensorMap& b_hi, const CU
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
-  at[1].id = cudaLaunchAttributeClusterDimension;  // the K halves of a tile form one cluster
+  at[1].id = cudaLaunchAttributeClusterDimension;  // M pairs x the K halves of a tile
   at[1].val.clusterDim.x = 2;
   at[1].val.clusterDim.y = 1;
   at[1].val.clusterDim.z = unsigned(splitk);
@@ -1845,6 +1920,11 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
           fp.partial = static_cast<T*>(sc->partial);
           fp.counters = sc->counters;
         }
+        // EVB_UMMA_ATMEM=1: S_hi / S_lo as the MMA's A operand in TMEM (shared memory then feeds only
+        // B).  Correct, but measured equal (22.9 vs 23.0 us per config-1 launch): the N = 128 tf32 MMAs
+        // are not bound by shared-memory bandwidth but by a fixed per-instruction cost (~30 cycles,
+        // from the probe's N = 64 / 256 rates), so the default keeps the operands in shared memory.
+        static const bool atmem = std::getenv("EVB_UMMA_ATMEM") && std::atoi(std::getenv("EVB_UMMA_ATMEM")) == 1;
         static const bool timeline = std::getenv("EVB_K1_TIMELINE") != nullptr;
         if (timeline) {  // one synchronous launch, per-CTA phase stamps appended to a CSV
           const int nct = n_tiles * splitk;
@@ -1854,7 +1934,8 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
           fused_params<float> f2 = fp;
           f2.dbg_ts = d;
           f2.dbg_skip = std::getenv("EVB_K2_SKIP") ? std::atoi(std::getenv("EVB_K2_SKIP")) : 0;
-          launch_f32_umma_sk<SBN>(ta_hi, tb_hi, tb_lo, f2, splitk, rq.stream);
+          if (atmem) launch_f32_umma_sk<SBN, true>(ta_hi, tb_hi, tb_lo, f2, splitk, rq.stream);
+          else launch_f32_umma_sk<SBN, false>(ta_hi, tb_hi, tb_lo, f2, splitk, rq.stream);
           EVB_CUDA(cudaStreamSynchronize(rq.stream));
           std::vector<unsigned long long> h(size_t(nct) * 8);
           EVB_CUDA(cudaMemcpy(h.data(), d, h.size() * 8, cudaMemcpyDeviceToHost));
@@ -1867,7 +1948,8 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
             std::fclose(f);
           }
         } else {
-          launch_f32_umma_sk<SBN>(ta_hi, tb_hi, tb_lo, fp, splitk, rq.stream);
+          if (atmem) launch_f32_umma_sk<SBN, true>(ta_hi, tb_hi, tb_lo, fp, splitk, rq.stream);
+          else launch_f32_umma_sk<SBN, false>(ta_hi, tb_hi, tb_lo, fp, splitk, rq.stream);
         }
         if (!own_rot) {
           EVB_CUDA(cudaStreamSynchronize(rq.stream));

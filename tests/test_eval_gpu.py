@@ -398,3 +398,39 @@ def test_gemm_path_extreme_inputs(dev, dim):
         fin = np.isfinite(ref)
         fin[far] = False
         assert rel_err(got[fin], ref[fin]) <= 1e-10, kind
+
+
+@pytest.mark.parametrize("kind", [1, 5, 6])
+def test_f32_tensor_core_a_in_tmem_variant(kind):
+    """The split-K fp32 kernel with S_hi / S_lo as the MMA's A operand in TMEM (EVB_UMMA_ATMEM=1,
+    tcgen05.mma with [a-tmem]; the switch is read once per process, hence the subprocess) against
+    the restatement at config 1's size (1e-4 relative)."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    from pathlib import Path
+
+    D, P = 1000, 1024
+    o, m = O.shift_rotation(7, D)
+    X = O.population(7, P, D)
+    ref = O.eval_batch(kind, o, m, 0.0, X)
+    code = f"""
+import sys; sys.path.insert(0, '.'); sys.path.insert(0, 'oracle')
+import numpy as np, torch, oracle as O, paper_2505_17430_b200 as evb
+o, m = O.shift_rotation(7, {D}); X = O.population(7, {P}, {D})
+p = evb.ProblemInstance.base({kind}, o.astype(np.float32), m.astype(np.float32), 0.0, dtype=evb.EVB_F32)
+out = torch.empty({P}, dtype=torch.float32, device='cuda')
+evb.evaluate_batch(p, torch.from_numpy(X.astype(np.float32)).cuda(), evb.EvalScratch(), out)
+np.save(sys.argv[1], out.cpu().numpy())
+"""
+    with tempfile.TemporaryDirectory() as td:
+        f = str(Path(td) / "v.npy")
+        root = Path(__file__).resolve().parents[1]
+        env = dict(os.environ, EVB_UMMA_ATMEM="1")
+        r = subprocess.run([sys.executable, "-c", code, f], cwd=str(root), capture_output=True, text=True, timeout=300,
+                           env=env)
+        assert r.returncode == 0, r.stderr[-2000:]
+        got = np.load(f).astype(np.float64)
+    err = np.max(np.abs(got - ref) / np.maximum(1.0, np.abs(ref)))
+    assert err <= 1e-4, err
