@@ -158,7 +158,8 @@ __device__ __forceinline__ void dmma_rows(const double* __restrict__ sS, const d
   const int g = lane >> 2, t = lane & 3;
   const int mt = (R + 7) >> 3, nt = (D + 15) >> 4;
   for (int task = warp; task < mt * nt; task += nwarps) {
-    const int m0 = (task / nt) << 3, n0 = (task % nt) << 4;
+    // m fastest: the narrow last column tile's tasks spread over the SM sub-partitions (warp % 4)
+    const int m0 = (task % mt) << 3, n0 = (task / mt) << 4;
     const bool two = n0 + 8 < D;  // warp-uniform
     double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
     const double* pa = sS + (m0 + g) * KS + 2 * t;
@@ -208,8 +209,15 @@ __host__ __device__ __forceinline__ int round8(int v) { return (v + 7) / 8 * 8; 
 // zero pads), else exact-order dots (dot_rows; M stride S, sS stride D)
 __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int D, int S, double* sMbase,
                               double* sZ, double* sS, double* sObase, double* sFk, double* sDist, double* f,
-                              bool resident, int KS, int fast_epi, phase_clock& pc) {
+                              bool resident, int KS, int fast_epi, double* part, phase_clock& pc) {
   const int ncomp = pr.n_comp > 0 ? pr.n_comp : 1;
+  // fast tensor-core epilogue (KS > 0 && fast_epi): x - o and the distance partials in one pass,
+  // base-value sums in two levels (8-element chunks, then per individual); part holds
+  // R x nqK distance partials and 2 x R x nqD base partials
+  const bool fast = KS > 0 && fast_epi;
+  const int nqK = KS > 0 ? KS / 8 : 0, nqD = (D + 7) / 8;
+  double* part_d = part;
+  double* part_b = part ? part + size_t(round8(P)) * nqK : nullptr;
   const int SS = KS > 0 ? KS : D;  // row stride of sS
   for (int c = 0; c < ncomp; ++c) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
@@ -222,7 +230,23 @@ __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int
       for (int e = threadIdx.x; e < D; e += blockDim.x) sO[e] = pr.shift[c][e];
       __syncthreads();
     }
-    if (KS > 0) {  // all RP x KS entries: the pads are zero for the tensor-core tiles
+    if (fast) {  // thread = (row, 8-wide chunk): s = x - o with zero pads, and the chunk's dist^2
+      const int RP = round8(P);
+      for (int e = threadIdx.x; e < RP * nqK; e += blockDim.x) {
+        const int i = e / nqK, q = e - i * nqK;
+        double sv[8], d2 = 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int k = 8 * q + j;
+          sv[j] = (i < P && k < D) ? __dsub_rn(X[i * D + k], sO[k]) : 0.0;
+          d2 = fma(sv[j], sv[j], d2);
+        }
+        double2* dst = reinterpret_cast<double2*>(sS + size_t(i) * KS + 8 * q);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dst[j] = make_double2(sv[2 * j], sv[2 * j + 1]);
+        part_d[e] = d2;
+      }
+    } else if (KS > 0) {  // all RP x KS entries: the pads are zero for the tensor-core tiles
       const int RP = round8(P);
       for (int e = threadIdx.x; e < RP * KS; e += blockDim.x) {
         const int i = e / KS, k = e - i * KS;
@@ -238,27 +262,8 @@ __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int
       // dist^2 in double (problems/instance.hpp:127-134): one sequential chain per individual;
       // the tensor-core path (a tolerance path already) takes a warp per individual and a
       // shuffle tree (the weights it feeds are relative: ~1e-16)
-      if (pr.n_comp > 0 && KS > 0 && fast_epi) {
-        // two levels: thread (i, q) sums the 8 elements [8q, 8q + 8) of row i, then thread i sums
-        // its row's partials (sFk as scratch: its slots are written after this)
-        const int nq = (D + 7) >> 3;
-        double* part = sZ;  // R x nq partials (sZ is written by the dots below)
-        for (int e = threadIdx.x; e < P * nq; e += blockDim.x) {
-          const int i = e / nq, q = e - i * nq;
-          const double* si = sS + i * SS + 8 * q;
-          double d2 = 0.0;
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (8 * q + j < D) d2 = fma(si[j], si[j], d2);
-          part[e] = d2;
-        }
-        __syncthreads();
-        for (int i = threadIdx.x; i < P; i += blockDim.x) {
-          double d2 = 0.0;
-          for (int q = 0; q < nq; ++q) d2 += part[i * nq + q];
-          sDist[i * kRunsMaxComp + c] = d2;
-        }
-        __syncthreads();
+      if (fast) {
+        // the distance partials were formed with x - o; summed with the base values below
       } else if (pr.n_comp > 0)
         for (int i = threadIdx.x; i < P; i += blockDim.x) {
           double d2 = 0.0;
@@ -316,12 +321,59 @@ __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int
       __syncthreads();
     }
     pc.mark(4);
-    for (int i = threadIdx.x; i < P; i += blockDim.x) {
-      const double* zr = sZ + i * D;
-      const double* pe = sS + i * D;
-      auto z = [&](int q) { return zr[q]; };
-      auto pre = [&](int q) { return pe[q]; };
-      sFk[i * kRunsMaxComp + c] = base_value_pre<double, false>(kind, D, z, pre, pr.ell_w);
+    if (fast && (kind == EVB_RASTRIGIN || kind == EVB_ACKLEY || kind == EVB_ELLIPTIC || kind == EVB_SPHERE)) {
+      // chunk sums (thread = (individual, 8 elements)), then per individual; the distance partials
+      // of this component are summed here too (problems/instance.hpp:127-134 up to order)
+      for (int e = threadIdx.x; e < P * nqD; e += blockDim.x) {
+        const int i = e / nqD, q = e - i * nqD;
+        double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int k = 8 * q + j;
+          if (k >= D) break;
+          const double v = sZ[i * D + k];
+          if (kind == EVB_RASTRIGIN) {
+            s1 += sS[i * D + k];
+          } else if (kind == EVB_ACKLEY) {
+            s1 = fma(v, v, s1);
+            s2 += sS[i * D + k];
+          } else if (kind == EVB_ELLIPTIC) {
+            s1 += __dmul_rn(__dmul_rn(pr.ell_w[k], v), v);
+          } else {
+            s1 = fma(v, v, s1);
+          }
+        }
+        part_b[e] = s1;
+        part_b[size_t(P) * nqD + e] = s2;
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        double s1 = 0.0, s2 = 0.0;
+        for (int q = 0; q < nqD; ++q) {
+          s1 += part_b[i * nqD + q];
+          s2 += part_b[size_t(P) * nqD + i * nqD + q];
+        }
+        sFk[i * kRunsMaxComp + c] = kind == EVB_ACKLEY ? ackley_final<double>(s1, s2, D) : s1;
+        if (pr.n_comp > 0) {
+          double d2 = 0.0;
+          for (int q = 0; q < nqK; ++q) d2 += part_d[i * nqK + q];
+          sDist[i * kRunsMaxComp + c] = d2;
+        }
+      }
+    } else {
+      if (fast && pr.n_comp > 0)  // distance partials of a component without the fast base sums
+        for (int i = threadIdx.x; i < P; i += blockDim.x) {
+          double d2 = 0.0;
+          for (int q = 0; q < nqK; ++q) d2 += part_d[i * nqK + q];
+          sDist[i * kRunsMaxComp + c] = d2;
+        }
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const double* zr = sZ + i * D;
+        const double* pe = sS + i * D;
+        auto z = [&](int q) { return zr[q]; };
+        auto pre = [&](int q) { return pe[q]; };
+        sFk[i * kRunsMaxComp + c] = base_value_pre<double, false>(kind, D, z, pre, pr.ell_w);
+      }
     }
     __syncthreads();
     pc.mark(5);
@@ -428,11 +480,13 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
   double* sZ = sM + even(NM * m_len);          // R x D
   double* sS = sZ + even(size_t(R) * D);       // x - o of the current component (tc: RP x KS)
   double* sO = sS + even(s_len);               // NM x D
+  const size_t part_len = (a.tc && a.tc_epi) ? size_t(round8(R)) * (tc_ks(D) / 8) + 2 * size_t(R) * ((D + 7) / 8) : 0;
   double* sFit = sO + NM * D;                  // P
   double* sTfit2 = sFit + P;                   // 2 x P (generation parity)
   double* sFk = sTfit2 + 2 * P;                // R x 4
   double* sDist = sFk + R * kRunsMaxComp;      // R x 4
-  int* sIdx = reinterpret_cast<int*>(sDist + R * kRunsMaxComp);  // P x 4 (a, b, c, word offset)
+  double* sPart = sDist + R * kRunsMaxComp;    // fast epilogue partials (part_len)
+  int* sIdx = reinterpret_cast<int*>(sPart + part_len);  // P x 4 (a, b, c, word offset)
   // the run's problem descriptor in shared memory (a local-memory copy lived in L1, which the
   // ~200 KB shared-memory carve-out leaves nearly empty: every field access missed to L2)
   __shared__ run_problem s_pr;
@@ -463,7 +517,7 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
   phase_clock pc{blockIdx.x == 0 ? a.prof : nullptr, 0};
   // evaluate rows [p0, p1) of X into f
   auto evaluate = [&](const double* X, double* f) {
-    runs_evaluate(pr, X + size_t(p0) * D, p1 - p0, D, S, sM, sZ, sS, sO, sFk, sDist, f + p0, a.resident != 0, KS, a.tc_epi, pc);
+    runs_evaluate(pr, X + size_t(p0) * D, p1 - p0, D, S, sM, sZ, sS, sO, sFk, sDist, f + p0, a.resident != 0, KS, a.tc_epi, sPart, pc);
   };
   // (split) publish this CTA's rows [p0, p1) of the given arrays into the peer's copies
   auto publish = [&](double* rows, int row_len) {
@@ -615,8 +669,9 @@ size_t runs_smem(int P, int D, int split = 1, int n_mat = 1, int tc = 0) {
   auto even = [](size_t n) { return (n + 1) & ~size_t(1); };
   const size_t m_len = tc ? size_t(round8(D)) * tc_ks(D) : size_t(D) * S;
   const size_t s_len = tc ? size_t(round8(int(R))) * tc_ks(D) : R * D;
+  const size_t part_len = tc ? size_t(round8(int(R))) * (tc_ks(D) / 8) + 2 * R * ((D + 7) / 8) : 0;
   return sizeof(double) * (2 * even(size_t(P) * D) + even(size_t(n_mat) * m_len) + even(R * D) + even(s_len) +
-                           size_t(n_mat) * D + 3 * P + 2 * R * kRunsMaxComp) +
+                           size_t(n_mat) * D + 3 * P + 2 * R * kRunsMaxComp + part_len) +
          sizeof(int) * 4 * P + 64;
 }
 
