@@ -36,18 +36,24 @@ constexpr int kRunsMaxComp = 4;
 
 // EVB_RUNS_PROFILE=1: CTA 0's thread 0 accumulates clock64() per phase (the phases end at block
 // barriers, so its clock marks the phase boundary) — a tuning aid, off by default.
+// The profiling build is a separate instantiation (PROF): without it the marks compile to
+// nothing (a runtime null check kept the struct in local memory, and every thread's check was an
+// L1-missing load on the phase boundaries).
+template <bool PROF>
 struct phase_clock {
   unsigned long long* acc;  // null: off
   long long last;
   __device__ __forceinline__ void start() {
-    if (acc && threadIdx.x == 0) last = clock64();
+    if constexpr (PROF)
+      if (acc && threadIdx.x == 0) last = clock64();
   }
   __device__ __forceinline__ void mark(int k) {
-    if (acc && threadIdx.x == 0) {
-      const long long t = clock64();
-      acc[k] += (unsigned long long)(t - last);
-      last = t;
-    }
+    if constexpr (PROF)
+      if (acc && threadIdx.x == 0) {
+        const long long t = clock64();
+        acc[k] += (unsigned long long)(t - last);
+        last = t;
+      }
   }
 };
 
@@ -207,9 +213,10 @@ __host__ __device__ __forceinline__ int round8(int v) { return (v + 7) / 8 * 8; 
 
 // KS > 0: tensor-core dots (dmma_rows; resident operands in the tc layout, sS stride KS with
 // zero pads), else exact-order dots (dot_rows; M stride S, sS stride D)
+template <bool PROF>
 __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int D, int S, double* sMbase,
                               double* sZ, double* sS, double* sObase, double* sFk, double* sDist, double* f,
-                              bool resident, int KS, int fast_epi, double* part, phase_clock& pc) {
+                              bool resident, int KS, int fast_epi, double* part, phase_clock<PROF>& pc) {
   const int ncomp = pr.n_comp > 0 ? pr.n_comp : 1;
   // fast tensor-core epilogue (KS > 0 && fast_epi): x - o and the distance partials in one pass,
   // base-value sums in two levels (8-element chunks, then per individual); part holds
@@ -271,7 +278,7 @@ __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int
           for (int j = 0; j < D; ++j) d2 = __dadd_rn(d2, __dmul_rn(si[j], si[j]));
           sDist[i * kRunsMaxComp + c] = d2;
         }
-      if (pc.acc) {  // profiling only: separate the distance chains from the dots
+      if constexpr (PROF) {  // profiling only: separate the distance chains from the dots
         __syncthreads();
         pc.mark(9);
       }
@@ -305,6 +312,7 @@ __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int
     if (KS > 0 && fast_epi && (kind == EVB_RASTRIGIN || kind == EVB_ACKLEY)) {
       // tensor-core path: the transcendental terms with cos2pi_fast (the reference's formulas),
       // element-parallel into sS; the sequential sums below are the reference's order
+#pragma unroll 2
       for (int e = threadIdx.x; e < P * D; e += blockDim.x) {
         const double v = sZ[e];
         const double cz = cos2pi_fast_ok(v) ? cos2pi_fast(v) : cos(__dmul_rn(two_pi_v<double>(), v));
@@ -459,6 +467,7 @@ __device__ void runs_evaluate(const run_problem& pr, const double* X, int P, int
 // half of the individuals; the halves of the fitness vector are exchanged through distributed
 // shared memory.  The trial fitness is double-buffered by generation parity, so one cluster
 // barrier per generation suffices (a CTA can only write the buffer its peer reads next).
+template <bool PROF>
 __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) double sm[];
@@ -486,13 +495,20 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
   double* sFk = sTfit2 + 2 * P;                // R x 4
   double* sDist = sFk + R * kRunsMaxComp;      // R x 4
   double* sPart = sDist + R * kRunsMaxComp;    // fast epilogue partials (part_len)
-  int* sIdx = reinterpret_cast<int*>(sPart + part_len);  // P x 4 (a, b, c, word offset)
+  double* sEw = sPart + part_len;              // D: elliptic weights (the problem's, staged once)
+  int* sIdx = reinterpret_cast<int*>(sEw + D);  // P x 4 (a, b, c, word offset)
   // the run's problem descriptor in shared memory (a local-memory copy lived in L1, which the
   // ~200 KB shared-memory carve-out leaves nearly empty: every field access missed to L2)
   __shared__ run_problem s_pr;
   for (int e = threadIdx.x; e < int(sizeof(run_problem) / 4); e += blockDim.x)
     reinterpret_cast<int*>(&s_pr)[e] = reinterpret_cast<const int*>(a.probs + run)[e];
   __syncthreads();
+  if (s_pr.ell_w) {  // elliptic weights from shared memory (L1 is nearly all carve-out)
+    for (int e = threadIdx.x; e < D; e += blockDim.x) sEw[e] = s_pr.ell_w[e];
+    __syncthreads();
+    if (threadIdx.x == 0) s_pr.ell_w = sEw;
+    __syncthreads();
+  }
   const run_problem& pr = s_pr;
   if (a.resident) {  // stage every component's rotation and shift once for all generations
     const int nc = pr.n_comp > 0 ? pr.n_comp : 1;
@@ -514,10 +530,10 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
   const uint64_t key = a.keys[run];
   double* gpop = a.pop + size_t(run) * P * D;
   double* gfit = a.fit + size_t(run) * P;
-  phase_clock pc{blockIdx.x == 0 ? a.prof : nullptr, 0};
+  phase_clock<PROF> pc{blockIdx.x == 0 ? a.prof : nullptr, 0};
   // evaluate rows [p0, p1) of X into f
   auto evaluate = [&](const double* X, double* f) {
-    runs_evaluate(pr, X + size_t(p0) * D, p1 - p0, D, S, sM, sZ, sS, sO, sFk, sDist, f + p0, a.resident != 0, KS, a.tc_epi, sPart, pc);
+    runs_evaluate<PROF>(pr, X + size_t(p0) * D, p1 - p0, D, S, sM, sZ, sS, sO, sFk, sDist, f + p0, a.resident != 0, KS, a.tc_epi, sPart, pc);
   };
   // (split) publish this CTA's rows [p0, p1) of the given arrays into the peer's copies
   auto publish = [&](double* rows, int row_len) {
@@ -671,7 +687,7 @@ size_t runs_smem(int P, int D, int split = 1, int n_mat = 1, int tc = 0) {
   const size_t s_len = tc ? size_t(round8(int(R))) * tc_ks(D) : R * D;
   const size_t part_len = tc ? size_t(round8(int(R))) * (tc_ks(D) / 8) + 2 * R * ((D + 7) / 8) : 0;
   return sizeof(double) * (2 * even(size_t(P) * D) + even(size_t(n_mat) * m_len) + even(R * D) + even(s_len) +
-                           size_t(n_mat) * D + 3 * P + 2 * R * kRunsMaxComp + part_len) +
+                           size_t(n_mat) * D + 3 * P + 2 * R * kRunsMaxComp + part_len + D) +
          sizeof(int) * 4 * P + 64;
 }
 
@@ -826,7 +842,8 @@ extern "C" int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int 
     require(smem <= 227 * 1024, "de_runs: run state does not fit in shared memory");
     static thread_local size_t smem_set = 0;
     if (smem > smem_set) {
-      EVB_CUDA(cudaFuncSetAttribute(de_runs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      EVB_CUDA(cudaFuncSetAttribute(de_runs_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      EVB_CUDA(cudaFuncSetAttribute(de_runs_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       smem_set = smem;
     }
     static const bool prof = std::getenv("EVB_RUNS_PROFILE") != nullptr;
@@ -850,9 +867,10 @@ extern "C" int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int 
       attr[0].val.clusterDim.z = 1;
       lc.attrs = attr;
       lc.numAttrs = 1;
-      err = cudaLaunchKernelEx(&lc, de_runs_kernel, a);
+      err = cudaLaunchKernelEx(&lc, dprof ? de_runs_kernel<true> : de_runs_kernel<false>, a);
     } else {
-      de_runs_kernel<<<n_runs, 512, smem, st>>>(a);
+      if (dprof) de_runs_kernel<true><<<n_runs, 512, smem, st>>>(a);
+      else de_runs_kernel<false><<<n_runs, 512, smem, st>>>(a);
       err = cudaGetLastError();
     }
     count_launch();
