@@ -286,6 +286,77 @@ __device__ __forceinline__ void epilogue_rows(const fused_params<T>& p, const T*
   }
 }
 
+// Ackley's two channels (sum of squares, sum of cos(2 pi z)) in ONE pass over the parked tile: one
+// shared-memory read per element and both shuffle trees per 8-row block (two separate passes made
+// the Ackley group the slowest of a multi-problem CTA's epilogues).  Same terms and orders as
+// epilogue_rows<TERM_SQ> + epilogue_rows<TERM_COS>.
+template <typename T, int BM, int BN>
+__device__ __forceinline__ void epilogue_rows_sqcos(const fused_params<T>& p, const T* zt, int ldt, int m0, int n0,
+                                                    int warp, int lane, int nwarps, int rpw, int ch, int ntile) {
+  using F = fop<T>;
+  constexpr int CPL = (BN + 31) / 32;
+  int cl[CPL];
+  bool cv[CPL];
+#pragma unroll
+  for (int cc = 0; cc < CPL; ++cc) {
+    const int c = lane + 32 * cc;
+    cv[cc] = c < BN && n0 + c < p.D;
+    cl[cc] = cv[cc] ? c : 0;
+  }
+  const uint32_t zs = static_cast<uint32_t>(__cvta_generic_to_shared(zt));
+  for (int r0 = 0; r0 < rpw; r0 += 8) {
+    T sa[8], sb[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) sa[q] = sb[q] = T(0);
+    auto block = [&](auto exact_tag) {
+      constexpr bool EXACT = decltype(exact_tag)::value;
+#pragma unroll
+      for (int cc = 0; cc < CPL; ++cc) {
+        const int col = n0 + cl[cc];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int r = warp + (r0 + q) * nwarps;
+          const bool ok = cv[cc] && r0 + q < rpw && r < BM;
+          const T z = ptx::lds<T>(zs + uint32_t(((ok ? r : 0) * ldt + cl[cc]) * int(sizeof(T))));
+          const T va = term_value<T, EXACT>(TERM_SQ, z, col, p.ell_w);
+          const T vb = term_value<T, EXACT>(TERM_COS, z, col, p.ell_w);
+          const T a1 = F::add(sa[q], va), b1 = F::add(sb[q], vb);
+          sa[q] = ok ? a1 : sa[q];
+          sb[q] = ok ? b1 : sb[q];
+        }
+      }
+    };
+    bool big = false;
+    if constexpr (std::is_same<T, double>::value) {
+#pragma unroll
+      for (int cc = 0; cc < CPL; ++cc)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int r = warp + (r0 + q) * nwarps;
+          const bool ok = cv[cc] && r0 + q < rpw && r < BM;
+          const T z = ptx::lds<T>(zs + uint32_t(((ok ? r : 0) * ldt + cl[cc]) * int(sizeof(T))));
+          big = big || (ok && cos2pi_needs_exact(z));
+        }
+      big = __any_sync(0xffffffffu, big);
+    }
+    if (big) block(std::true_type{});
+    else block(std::false_type{});
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      for (int off = 16; off > 0; off >>= 1) {
+        sa[q] = F::add(sa[q], __shfl_xor_sync(0xffffffffu, sa[q], off));
+        sb[q] = F::add(sb[q], __shfl_xor_sync(0xffffffffu, sb[q], off));
+      }
+      const int r = warp + (r0 + q) * nwarps;
+      const int row = m0 + r;
+      if (lane == 0 && r0 + q < rpw && r < BM && row < p.P) {
+        p.partial[(size_t(ch) * p.n_ntiles + ntile) * p.P + row] = sa[q];
+        p.partial[(size_t(ch + 1) * p.n_ntiles + ntile) * p.P + row] = sb[q];
+      }
+    }
+  }
+}
+
 template <typename T, int BM, int BN>
 __device__ void tile_epilogue(const fused_params<T>& p, const T* zt, int ldt, int m0, int n0, int tid, int nthreads,
                               int* last_flag, int mtile, int ntile, int bar_id) {
@@ -308,6 +379,11 @@ __device__ void tile_epilogue(const fused_params<T>& p, const T* zt, int ldt, in
   // are independent (ILP) instead of one row at a time.
   const int rpw = (BM + nwarps - 1) / nwarps;
   for (int ch = 0; ch < p.n_ch; ++ch) {
+    if (p.ch_term[ch] == TERM_SQ && ch + 1 < p.n_ch && p.ch_term[ch + 1] == TERM_COS) {  // Ackley's pair
+      epilogue_rows_sqcos<T, BM, BN>(p, zt, ldt, m0, n0, warp, lane, nwarps, rpw, ch, ntile);
+      ++ch;
+      continue;
+    }
     switch (p.ch_term[ch]) {  // one specialised loop nest per term (no per-element switch)
       case TERM_SQ: epilogue_rows<TERM_SQ, T, BM, BN>(p, zt, ldt, m0, n0, warp, lane, nwarps, rpw, ch, ntile); break;
       case TERM_WSQ: epilogue_rows<TERM_WSQ, T, BM, BN>(p, zt, ldt, m0, n0, warp, lane, nwarps, rpw, ch, ntile); break;
