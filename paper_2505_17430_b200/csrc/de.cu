@@ -333,12 +333,12 @@ __device__ double sample_crossover_rate(R& r, double mu) {
 }
 
 // Scalar draws of individual i in the reference's order (de/engine.hpp:88-92):
-// adapter sample, mutation indices, crossover jrand.  Returns via the de_dev arrays.
+// adapter sample, mutation indices, crossover jrand.  Returns via the de_dev arrays.  Split in two
+// so that the persistent generations can draw the adapter sample (which needs no order) while
+// the rest of the CTA ranks the population.
 template <typename T, typename R>
-__device__ void draw_scalars(const de_dev<T>& d, int i, int arch_size, R& r) {
-  // adapter
-  T F, CR;
-  int slot = -1;
+__device__ __forceinline__ void draw_adapter(const de_dev<T>& d, R& r, T& F, T& CR, int& slot) {
+  slot = -1;
   if (d.cfg.parameter == EVB_PAR_SHADE) {
     slot = draw_int(r, d.cfg.memory_size);
     F = T(sample_scale_factor(r, double(d.mem_f[slot])));
@@ -350,7 +350,10 @@ __device__ void draw_scalars(const de_dev<T>& d, int i, int arch_size, R& r) {
     F = T(d.cfg.f);
     CR = T(d.cfg.cr);
   }
-  // mutation
+}
+
+template <typename T, typename R>
+__device__ __forceinline__ void draw_mutation(const de_dev<T>& d, int i, int arch_size, R& r, T F, T CR, int slot) {
   const int ps = d.P;
   int a = 0, b = 0, c = 0;
   if (d.cfg.mutation == EVB_MUT_RAND1) {  // de/strategy.hpp:84-86
@@ -385,6 +388,14 @@ __device__ void draw_scalars(const de_dev<T>& d, int i, int arch_size, R& r) {
   d.idx[4 * i + 1] = b;
   d.idx[4 * i + 2] = c;
   d.jrand[i] = jr;
+}
+
+template <typename T, typename R>
+__device__ void draw_scalars(const de_dev<T>& d, int i, int arch_size, R& r) {
+  T F, CR;
+  int slot;
+  draw_adapter<T>(d, r, F, CR, slot);
+  draw_mutation<T>(d, i, arch_size, r, F, CR, slot);
 }
 
 template <typename T>
@@ -1477,24 +1488,44 @@ __global__ void __launch_bounds__(kRunThreads, 1) de_run_kernel(const de_run_arg
     const uint32_t gen = gen0 + uint32_t(g);
     const unsigned tag = E0 + unsigned(g) + 1u;
     // ---- A: fitness, order, adapter memories, archive size ----
-    for (int t = tid; t < P; t += nthr) sFit[t] = ldcg(d.fit + t);
-    if (adapt)
-      for (int t = tid; t < H; t += nthr) {
-        sMemF[t] = ldcg(d.mem_f + t);
-        sMemC[t] = ldcg(d.mem_cr + t);
-      }
-    if (tid == 0) s_misc[0] = ldcg(d.arch_size);
-    __syncthreads();
+    // (read from L2 once; later generations get them pushed into every CTA's copy over DSMEM by
+    // the CTA that changed them, phase G)
+    if (g == 0) {
+      for (int t = tid; t < P; t += nthr) sFit[t] = ldcg(d.fit + t);
+      if (adapt)
+        for (int t = tid; t < H; t += nthr) {
+          sMemF[t] = ldcg(d.mem_f + t);
+          sMemC[t] = ldcg(d.mem_cr + t);
+        }
+      if (tid == 0) s_misc[0] = ldcg(d.arch_size);
+      __syncthreads();
+    }
     mark(11);
-    if (ttpb || best) {  // (fitness, index) ranks, NaN last, over all threads: thread (i, chunk)
-      // counts the members of its j chunk that precede i on order_key (integer shared atomics)
-      const int nch = max(1, min(8, nthr / P));
-      for (int t = tid; t < P; t += nthr) {
+    // the last warp draws the owned individuals' adapter samples (they need no order) while the
+    // other warps rank the population (named barrier 1 over them); then the mutation draws
+    const int dw = (nthr >> 5) - 1;  // draw warp
+    de_dev<T> dl = d;
+    dl.order = sIdx;  // sorted: the first p_count entries are the order
+    dl.mem_f = sMemF;
+    dl.mem_cr = sMemC;
+    philox_prefetch_reader<5> rd;
+    T dF = T(0), dCR = T(0);
+    int dslot = -1;
+    if (warp == dw) {
+      if (lane < nq) {
+        rd.reset(d.src.key, (uint64_t(gen) << 32) | uint32_t(i0 + lane));
+        draw_adapter<T>(dl, rd, dF, dCR, dslot);
+      }
+    } else if (ttpb || best) {  // (fitness, index) ranks, NaN last: thread (i, chunk) counts the
+      // members of its j chunk that precede i on order_key (integer shared atomics)
+      const int nr = nthr - 32;
+      const int nch = max(1, min(8, nr / P));
+      for (int t = tid; t < P; t += nr) {
         sIdx[NP2 + t] = 0;  // rank counters (after the order slots)
         sKey[t] = order_key(sFit[t]);
       }
-      __syncthreads();
-      for (int t = tid; t < P * nch; t += nthr) {
+      ptx::named_bar_sync(1, nr);
+      for (int t = tid; t < P * nch; t += nr) {
         const int ch = t / P, i = t - ch * P;
         const int j0 = (P * ch) / nch, j1 = (P * (ch + 1)) / nch;
         const unsigned long long ki = sKey[i];
@@ -1506,35 +1537,30 @@ __global__ void __launch_bounds__(kRunThreads, 1) de_run_kernel(const de_run_arg
         }
         if (cnt) atomicAdd(&sIdx[NP2 + i], cnt);
       }
-      __syncthreads();
-      for (int i = tid; i < P; i += nthr) {
+      ptx::named_bar_sync(1, nr);
+      for (int i = tid; i < P; i += nr) {
         const int rk = sIdx[NP2 + i];
         if (rk < d.p_count) sIdx[rk] = i;
       }
-      __syncthreads();
     }
+    __syncthreads();
     mark(0);
     const int arch_size = s_misc[0];
-    // ---- B: draws of the owned individuals ----
-    if (tid < nq) {
-      de_dev<T> dl = d;
-      dl.order = sIdx;  // sorted: the first p_count entries are the order
-      dl.mem_f = sMemF;
-      dl.mem_cr = sMemC;
-      const int i = i0 + tid;
-      philox_prefetch_reader<5> r(d.src.key, (uint64_t(gen) << 32) | uint32_t(i));
-      draw_scalars<T>(dl, i, arch_size, r);
-      d.woff[i] = r.count;
-      d.rword[i] = r.count + D;
-      d.wcount[i] = r.count + D;
+    // ---- B: the rest of the owned individuals' draws ----
+    if (warp == dw && lane < nq) {
+      const int i = i0 + lane;
+      draw_mutation<T>(dl, i, arch_size, rd, dF, dCR, dslot);
+      d.woff[i] = rd.count;
+      d.rword[i] = rd.count + D;
+      d.wcount[i] = rd.count + D;
       // the same values for this CTA's later phases from shared memory (no L2 round trip)
-      sQi[8 * tid + 0] = d.idx[4 * i + 0];
-      sQi[8 * tid + 1] = d.idx[4 * i + 1];
-      sQi[8 * tid + 2] = d.idx[4 * i + 2];
-      sQi[8 * tid + 3] = d.jrand[i];
-      sQi[8 * tid + 4] = int(r.count);
-      sQf[2 * tid] = d.F[i];
-      sQf[2 * tid + 1] = d.CR[i];
+      sQi[8 * lane + 0] = d.idx[4 * i + 0];
+      sQi[8 * lane + 1] = d.idx[4 * i + 1];
+      sQi[8 * lane + 2] = d.idx[4 * i + 2];
+      sQi[8 * lane + 3] = d.jrand[i];
+      sQi[8 * lane + 4] = int(rd.count);
+      sQf[2 * lane] = dF;
+      sQf[2 * lane + 1] = dCR;
     }
     __syncthreads();
     mark(1);
@@ -1764,9 +1790,11 @@ __global__ void __launch_bounds__(kRunThreads, 1) de_run_kernel(const de_run_arg
         x[j] = sT[q * D + j];
       }
       if (lane == 0) d.fit[i] = sTf[q];
+      if (lane < NC) *cl.map_shared_rank(sFit + i, lane) = sTf[q];  // every CTA's copy
     }
     if (c == 0) {
       const int n_push = s_misc[1], n_succ = s_misc[2];
+      if (tid < NC) *cl.map_shared_rank(&s_misc[0], tid) = min(d.archive_cap, arch_size + n_push);
       if (tid == 0) {
         const int size0 = arch_size, room = d.archive_cap - size0;
         *d.arch_size = min(d.archive_cap, size0 + n_push);
@@ -1810,9 +1838,14 @@ __global__ void __launch_bounds__(kRunThreads, 1) de_run_kernel(const de_run_arg
               cr_acc = __dadd_rn(cr_acc, wnum[2 * P + k]);
             }
             const int kw = *d.write_index;
-            d.mem_f[kw] = T(__ddiv_rn(f_num, f_den));
-            d.mem_cr[kw] = T(cr_acc);
+            const T nf = T(__ddiv_rn(f_num, f_den)), nc = T(cr_acc);
+            d.mem_f[kw] = nf;
+            d.mem_cr[kw] = nc;
             *d.write_index = (kw + 1) % d.cfg.memory_size;
+            for (int k = 0; k < NC; ++k) {  // every CTA's copy
+              *cl.map_shared_rank(sMemF + kw, k) = nf;
+              *cl.map_shared_rank(sMemC + kw, k) = nc;
+            }
           }
         } else if (tid == 0) {  // JADE, de/parameter.hpp:107-120
           double num = 0.0, den = 0.0, crm = 0.0;
@@ -1824,8 +1857,14 @@ __global__ void __launch_bounds__(kRunThreads, 1) de_run_kernel(const de_run_arg
           const double lehmer = __ddiv_rn(num, den);
           crm = __ddiv_rn(crm, double(n_succ));
           const double cc = double(T(d.cfg.jade_c));
-          d.mem_f[0] = T(__dadd_rn(__dmul_rn(__dsub_rn(1.0, cc), double(sMemF[0])), __dmul_rn(cc, lehmer)));
-          d.mem_cr[0] = T(__dadd_rn(__dmul_rn(__dsub_rn(1.0, cc), double(sMemC[0])), __dmul_rn(cc, crm)));
+          const T nf = T(__dadd_rn(__dmul_rn(__dsub_rn(1.0, cc), double(sMemF[0])), __dmul_rn(cc, lehmer)));
+          const T nc = T(__dadd_rn(__dmul_rn(__dsub_rn(1.0, cc), double(sMemC[0])), __dmul_rn(cc, crm)));
+          d.mem_f[0] = nf;
+          d.mem_cr[0] = nc;
+          for (int k = 0; k < NC; ++k) {  // every CTA's copy
+            *cl.map_shared_rank(sMemF, k) = nf;
+            *cl.map_shared_rank(sMemC, k) = nc;
+          }
         }
       }
     }

@@ -93,7 +93,12 @@ struct philox_prefetch_reader {
   uint64_t key, ctr_hi;
   int64_t count = 0;
   uint64_t w[2 * NB];
-  __device__ __forceinline__ philox_prefetch_reader(uint64_t k, uint64_t c) : key(k), ctr_hi(c) {
+  __device__ __forceinline__ philox_prefetch_reader(uint64_t k, uint64_t c) { reset(k, c); }
+  __device__ __forceinline__ philox_prefetch_reader() : key(0), ctr_hi(0) {}  // reset() before use
+  __device__ __forceinline__ void reset(uint64_t k, uint64_t c) {
+    key = k;
+    ctr_hi = c;
+    count = 0;
 #pragma unroll
     for (int b = 0; b < NB; ++b) philox_pair(k, c, uint64_t(b), w[2 * b], w[2 * b + 1]);
   }
