@@ -1457,7 +1457,7 @@ __global__ void __launch_bounds__(kRunThreads, 1) de_run_kernel(const de_run_arg
   int* sIdx = reinterpret_cast<int*>(sKey + P);  // NP2 order slots + P rank counters
   int* sCnt = sIdx + NP2 + P;                    // NC x 2
   int* sQi = sCnt + 2 * NC;                      // Q x 8: donors, jrand, first gene word
-  uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<uintptr_t>(sCnt + 2 * NC + 2) & ~uintptr_t(7)) + 1;
+  uint64_t* bar = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(sQi + 8 * Q) + 7) & ~uintptr_t(7));  // 2
   __shared__ int s_misc[4];  // [0] archive size at the generation start
 
   if (tid == 0) {
@@ -2258,7 +2258,7 @@ bool run_generations_t(evb_de_s* e, const device_problem* prob, void* pop, int64
     size_t np2 = 1;
     while (np2 < size_t(P)) np2 <<= 1;
     return mt_bytes + (7 * size_t(q) * D + P + 2 * H + 3 * q + 1) * sizeof(T) + 16 + 4 * size_t(P) * 8 +
-           (np2 + P + 2 * nc + 8 * q + 2) * sizeof(int) + 64;
+           (np2 + P + 2 * nc + 8 * q) * sizeof(int) + 8 + 2 * 8 + 64;
   };
   if (smem_for(Q, NC) > 200 * 1024) return false;
   de_run_args<T> a{};
