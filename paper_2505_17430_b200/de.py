@@ -235,10 +235,11 @@ class DEEngine:
         de_engine shape (one copy in, evb_de_generations, one copy out; synchronous)."""
         nd = self._np()
         if pop.dtype != nd or fitness.dtype != nd or pop.ndim != 2 or pop.shape[1] != self.dim \
-                or pop.shape[0] != self.pop_size or not pop.flags["C_CONTIGUOUS"] or not fitness.flags["C_CONTIGUOUS"]:
-            raise ConfigError("de: host population must be a C-contiguous (pop_size, dim) array of the engine dtype")
+                or pop.shape[0] != self.pop_size or pop.strides[1] != pop.itemsize \
+                or pop.strides[0] % pop.itemsize or not fitness.flags["C_CONTIGUOUS"]:
+            raise ConfigError("de: host population must be a row-major (pop_size, dim) array of the engine dtype")
         check(_lib.lib().evb_de_generations_host(self._h, problem.handle, scratch.handle if scratch else None,
-                                                 ctypes.c_void_p(pop.ctypes.data), pop.shape[1],
+                                                 ctypes.c_void_p(pop.ctypes.data), pop.strides[0] // pop.itemsize,
                                                  ctypes.c_void_p(fitness.ctypes.data), lb, ub, rng.handle, n),
               "de_generations_host")
 

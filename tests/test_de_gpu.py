@@ -775,10 +775,14 @@ def test_generations_host_state_equals_device(dev):
         eng.init_population(pop, -100.0, 100.0, rng)
         fit = dev_eval(prob, pop, dev)
         if host:
-            hp, hf = pop.cpu().numpy().copy(), fit.cpu().numpy().copy()
+            # rows with a padded stride (ldp = D + 3) in host memory
+            big = np.full((P, D + 3), -7.0)
+            big[:, :D] = pop.cpu().numpy()
+            hp, hf = big[:, :D], fit.cpu().numpy().copy()
             eng.generations_host(prob, hp, hf, -100.0, 100.0, rng, 1)
             eng.generations_host(prob, hp, hf, -100.0, 100.0, rng, 25)
-            res.append((hp, hf))
+            assert np.all(big[:, D:] == -7.0)  # the padding is untouched
+            res.append((hp.copy(), hf))
         else:
             eng.generations(prob, pop, fit, -100.0, 100.0, rng, 1)
             eng.generations(prob, pop, fit, -100.0, 100.0, rng, 25)
