@@ -1486,6 +1486,7 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN, ATMEM>::THREADS, 1)
       }
     }
     if (nsk > 1) ptx::cluster_sync_all();  // every thread of both CTAs (warps 0-1 join below)
+    if (etid == 0) stamp(2);  // the K halves exchanged
     auto loadz = [&](int c0, float (&v)[16]) {  // z of owned columns [own0 + half*TW + c0, +16)
       load16(own0 + half * TW + c0, v);
       if (nsk > 1) {
@@ -1557,6 +1558,31 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN, ATMEM>::THREADS, 1)
           return v;
         };
         const bool par = p.n_ch > 1 && p.n_ch * C::BM <= 256;
+        // one channel: two threads per row each sum half of the column-block partials (in order),
+        // one L2 round of loads instead of two; the halves add in fixed order
+        const bool split2 = p.n_ch == 1 && p.n_ntiles >= 4;
+        if (split2) {
+          const int h2 = etid / C::BM, rr = etid % C::BM, rw = m0 + rr;
+          const int nh = (p.n_ntiles + 1) / 2, t_lo = h2 * nh, t_hi = min(p.n_ntiles, t_lo + nh);
+          if (rw < p.P) {
+            const bool prod = term_is_product(p.ch_term[0]);
+            const float* src = p.partial + rw;
+            float x[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              if (t_lo + q < t_hi) x[q] = __ldcg(src + size_t(t_lo + q) * p.P);
+            float v = x[0];
+#pragma unroll
+            for (int q = 1; q < 16; ++q)
+              if (t_lo + q < t_hi) v = prod ? __fmul_rn(v, x[q]) : __fadd_rn(v, x[q]);
+            for (int t = t_lo + 16; t < t_hi; ++t) {  // more than 32 column blocks
+              const float y = __ldcg(src + size_t(t) * p.P);
+              v = prod ? __fmul_rn(v, y) : __fadd_rn(v, y);
+            }
+            xs[h2 * C::BM + rr] = v;
+          }
+          ptx::named_bar_sync(1, 256);
+        }
         if (par) {
           const int ch = etid / C::BM, rr = etid % C::BM;
           if (ch < p.n_ch && m0 + rr < p.P) xs[ch * C::BM + rr] = chain(ch, m0 + rr);
@@ -1564,7 +1590,12 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN, ATMEM>::THREADS, 1)
         }
         if (etid < C::BM && m0 + etid < p.P) {
           float chv[kMaxCh];
-          for (int ch = 0; ch < p.n_ch; ++ch) chv[ch] = par ? xs[ch * C::BM + etid] : chain(ch, m0 + etid);
+          if (split2) {
+            const float a0 = xs[etid], a1 = xs[C::BM + etid];
+            chv[0] = term_is_product(p.ch_term[0]) ? __fmul_rn(a0, a1) : __fadd_rn(a0, a1);
+          } else {
+            for (int ch = 0; ch < p.n_ch; ++ch) chv[ch] = par ? xs[ch * C::BM + etid] : chain(ch, m0 + etid);
+          }
           for (int o = 0; o < p.n_out; ++o) {
             const float s0 = chv[p.out_ch0[o]];
             const float s1 = p.out_ch1[o] >= 0 ? chv[p.out_ch1[o]] : 0.f;
@@ -2019,7 +2050,7 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
           if (FILE* f = std::fopen("gpurun_out/k2_ts.csv", "a")) {
             for (int c = 0; c < nct; ++c)
               std::fprintf(f, "%d,%llu,%llu,%llu,%llu,%llu,%llu,%llu\n", c, h[c * 8 + 0], h[c * 8 + 1], h[c * 8 + 3],
-                           h[c * 8 + 4], h[c * 8 + 5], h[c * 8 + 6], h[c * 8 + 7]);
+                           h[c * 8 + 4], h[c * 8 + 5], h[c * 8 + 6], h[c * 8 + 2]);
             std::fprintf(f, "end\n");
             std::fclose(f);
           }

@@ -1,6 +1,7 @@
 """Per-CTA phase timeline of the split-K fp32 tcgen05 kernel (EVB_K1_TIMELINE=1 hook): entry,
 first stage consumed by the MMA issuer, accumulator complete, partials written / z parked, exit.
-Columns: c, start, first, accfull, terms, end, last-N-tile flag, last-K-half flag.  Tuning aid."""
+Columns: c, start, first, accfull, partials written, end, last-column-block flag, exchange done.
+Tuning aid."""
 import os
 import sys
 from pathlib import Path
@@ -39,7 +40,8 @@ for r in runs[2:]:
     def q(v):
         return f"{np.min(v) / 1e3:.1f}/{np.median(v) / 1e3:.1f}/{np.max(v) / 1e3:.1f}" if len(v) else "-"
 
-    lk = a[:, 7] == 1
+    ex = a[:, 7] > 0  # the K halves exchanged (split-K launches)
+    xt = np.where(ex, a[:, 7], a[:, 3])
     print(f"{kind.name}: start {q(a[:, 1] - t0)} | first stage {q(a[:, 2] - a[:, 1])} | mainloop {q(a[:, 3] - a[:, 2])}"
-          f" | accfull->park/terms (first half) {q((a[:, 5] - a[:, 3])[~lk])} | accfull->partials (last) "
-          f"{q((a[:, 4] - a[:, 3])[lk])} | combine {q((a[:, 5] - a[:, 4])[a[:, 6] == 1])} | end {np.max(a[:, 5] - t0) / 1e3:.1f} us")
+          f" | exchange {q(xt - a[:, 3])} | terms+partials {q(a[:, 4] - xt)} | combine {q((a[:, 5] - a[:, 4])[a[:, 6] == 1])}"
+          f" | end {np.max(a[:, 5] - t0) / 1e3:.1f} us")
