@@ -514,10 +514,11 @@ def hbm_update():
             out["frac_dram"] = out["gbps_dram"] / hbm
         return out
 
-    res["de_trial_vec_kernel"] = rec("de_trial_vec_kernel", ph["trial"], trial_alg,
-                                 f"5*s*P*D algorithmic; compulsory DRAM 2*s*P*D = {trial_min / 1e6:.0f} MB "
-                                 f"(donor rows hit L2)")
-    res["de_trial_vec_kernel"]["frac_compulsory"] = trial_min / (ph["trial"] * 1e-3) / 1e9 / hbm
+    res["de_trial_stage_kernel"] = rec("de_trial_stage_kernel", ph["trial"], trial_alg,
+                                       f"5*s*P*D algorithmic; compulsory DRAM 2*s*P*D = {trial_min / 1e6:.0f} MB "
+                                       f"(donor rows hit L2); rows staged by cp.async through a 3-stage "
+                                       f"per-warp shared-memory ring")
+    res["de_trial_stage_kernel"]["frac_compulsory"] = trial_min / (ph["trial"] * 1e-3) / 1e9 / hbm
     winners = statistics.median(wins)  # rows replaced (fitness changed) per generation
     res["de_select_apply_kernel"] = rec("de_select_apply_kernel", ph["select_apply"], int(3 * s * winners * D),
                                         f"s*D*(trial read + parent read + write) per winner; {winners:.0f} of {P} "

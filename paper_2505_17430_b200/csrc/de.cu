@@ -180,6 +180,7 @@ struct de_dev {
   T* mem_cr;
   T lb, ub;
   word_source src;
+  philox_keys pk;  // src.key's round keys (PHILOX)
   uint32_t* gen_ptr;  // device generation counter (incremented by the apply kernel)
   int64_t* cursor;
   int* overflow;
@@ -591,31 +592,34 @@ struct vec16<float> {
 
 constexpr int kTrialVecWarps = 8;  // individuals per 256-thread block
 
-// 16-byte read-only load; HINT: L2 evict_last (the population is re-read as donors by other
-// individuals of the same launch, the trial rows stream out with evict-first stores)
-template <bool HINT>
-__device__ __forceinline__ double2 ld16(const double* p, uint64_t pol) {
-  if constexpr (HINT) {
-    double2 v;
-    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
-    return v;
-  } else {
-    return __ldg(reinterpret_cast<const double2*>(p));
+// Take bits of one lane's VEC window words: bit e = (u01(word e) < CR).  u01(w) = (w >> 11) 2^-53
+// (core/rng.hpp:81-83) is compared with CR as an integer: (w >> 11) < ceil(CR 2^53) exactly (the
+// scaling by 2^53 is exact, the left side is an integer), i.e. w <= lim with
+// lim = ((ceil(CR 2^53) - 1) << 11) | 0x7FF; CR <= 0 (or NaN) never takes (`none`).
+struct take_rule {
+  uint64_t lim;
+  bool none;
+  __device__ explicit take_rule(double cr) {
+    const double t = ceil(cr * 0x1.0p53);
+    none = !(t >= 1.0);
+    const uint64_t ti = t >= 0x1.0p53 ? (uint64_t(1) << 53) : uint64_t(none ? 1.0 : t);
+    lim = ((ti - 1) << 11) | 0x7FFu;
   }
-}
-template <bool HINT>
-__device__ __forceinline__ float4 ld16(const float* p, uint64_t pol) {
-  if constexpr (HINT) {
-    float4 v;
-    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
-    return v;
-  } else {
-    return __ldg(reinterpret_cast<const float4*>(p));
-  }
-}
+  __device__ __forceinline__ uint32_t bit(uint64_t w) const { return (!none && w <= lim) ? 1u : 0u; }
+};
 
-template <typename T, int MUT, int U, bool HINT = false, int MINB = 1>
+// Warp-per-individual trial kernel (binomial crossover, PHILOX words, 16-byte aligned rows).
+// The grid is (individual blocks) x (column blocks); a warp walks chunks [cb0, cb1) of its row,
+// W = 32 x VEC genes per chunk, lane l owning genes [cW + VEC l, +VEC) with one 16-byte load per
+// donor row and one 16-byte evict-first store.  Gene j's uniform is stream word s0 + j: lane l
+// computes the Philox blocks of words [wb + cW + VEC l, +VEC), wb = s0 rounded down to even, as a
+// VEC-bit take mask; for odd s0 every gene takes the NEXT word (mask >> 1, the top bit from lane
+// l + 1's bit 0 by shuffle, lane 31 from lane 0 of the next chunk's mask).  The masks run two
+// chunks ahead, so the loads of a chunk issue before its successor's Philox work.  CLIP: the
+// clip repair inlined (the configs' repair); otherwise the runtime repair switch.  Per gene the
+// arithmetic is de_trial_kernel's (explicitly rounded donor, same repair), so the trials are
+// bit-identical to it.
+template <typename T, int MUT, bool CLIP, int MINB>
 __global__ void __launch_bounds__(32 * kTrialVecWarps, MINB) de_trial_vec_kernel(const de_dev<T> d) {
   ptx::griddep_wait();  // PDL (launch_pdl): predecessor data first
   ptx::griddep_launch_dependents();
@@ -626,130 +630,223 @@ __global__ void __launch_bounds__(32 * kTrialVecWarps, MINB) de_trial_vec_kernel
   const int lane = threadIdx.x & 31;
   if (i >= d.P) return;  // warp-uniform
   const int D = d.D;
+  const int nchunks = (D + W - 1) / W;
+  // column block blockIdx.y: chunks [cb0, cb1).  At large P the population exceeds L2; the grid
+  // walks individuals fastest within a column block, so the donor rows' slices of the block in
+  // flight (P x block width) stay L2-resident and each is fetched from HBM about once.
+  const int cpb = (nchunks + int(gridDim.y) - 1) / int(gridDim.y);
+  const int cb0 = int(blockIdx.y) * cpb, cb1 = min(nchunks, cb0 + cpb);
   const T Fi = d.F[i];
   const int jr = d.jrand[i];
   const int a = d.idx[4 * i + 0], b = d.idx[4 * i + 1], c = d.idx[4 * i + 2];
-  const T* xi = d.pop + size_t(i) * d.ldp;
-  const T* xa = d.pop + size_t(a) * d.ldp;
-  const T* xb = d.pop + size_t(b) * d.ldp;
-  const T* xc = (MUT == EVB_MUT_TTPB1 && c >= d.P) ? d.archive + size_t(c - d.P) * d.ldt : d.pop + size_t(c) * d.ldp;
-  T* out = d.trial + size_t(i) * d.ldt;
+  const T* __restrict__ xi = d.pop + size_t(i) * d.ldp;
+  const T* __restrict__ xa = d.pop + size_t(a) * d.ldp;
+  const T* __restrict__ xb = d.pop + size_t(b) * d.ldp;
+  const T* __restrict__ xc =
+      (MUT == EVB_MUT_TTPB1 && c >= d.P) ? d.archive + size_t(c - d.P) * d.ldt : d.pop + size_t(c) * d.ldp;
+  T* __restrict__ out = d.trial + size_t(i) * d.ldt;
   const uint64_t ctr_hi = (uint64_t(*d.gen_ptr) << 32) | uint32_t(i);
   const T lb = d.lb, ub = d.ub;
   const int repair = d.cfg.repair;
-  const double cr = double(d.CR[i]);
+  const take_rule rule(double(d.CR[i]));
   const int64_t s0 = d.woff[i];
-  const int sh = int(s0 & 1);
-  const int64_t blk0 = s0 >> 1;  // first Philox block of the row's window
-  const uint64_t key = d.src.key;
-  uint64_t pol = 0;
-  if constexpr (HINT) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  // take bits of the lane's VEC window words in chunk cc
-  auto window = [&](int cc, bool (&tb)[VEC]) {
+  const bool odd = (s0 & 1) != 0;
+  const uint64_t blk0 = uint64_t(s0 >> 1) + uint64_t(lane * (VEC / 2));  // this lane's first block
+  constexpr uint32_t FULL = (1u << VEC) - 1u;
+  auto window = [&](int cc) -> uint32_t {  // the lane's VEC take bits of chunk cc (words wb + ...)
+    uint32_t m = 0;
 #pragma unroll
     for (int k = 0; k < VEC / 2; ++k) {
-      uint64_t w0, w1;
-      philox_pair(key, ctr_hi, uint64_t(blk0 + int64_t(cc) * (W / 2) + lane * (VEC / 2) + k), w0, w1);
-      tb[2 * k] = u01_of(w0) < cr;
-      tb[2 * k + 1] = u01_of(w1) < cr;
+      const uint64_t blk = blk0 + uint64_t(cc) * (W / 2) + uint64_t(k);
+      uint32_t cw[4] = {uint32_t(blk), uint32_t(blk >> 32), uint32_t(ctr_hi), uint32_t(ctr_hi >> 32)};
+      philox4x32_10_rk(cw, d.pk);
+      m |= rule.bit((uint64_t(cw[1]) << 32) | cw[0]) << (2 * k);
+      m |= rule.bit((uint64_t(cw[3]) << 32) | cw[2]) << (2 * k + 1);
     }
+    return m;
   };
-  const int nchunks = (D + W - 1) / W;
-  // U chunks per iteration.  Windows run ahead: at the top of an iteration the windows of its U
-  // chunks and of the chunk after them (the odd-s0 seam word) are known, so the take bits — and
-  // with them which target vectors are needed — are known before any load issues; the next U
-  // windows are computed while the loads are in flight.
-  bool win[U + 1][VEC];
-#pragma unroll
-  for (int u = 0; u <= U; ++u)
-    if (u <= nchunks) window(u, win[u]);
-  for (int c0 = 0; c0 < nchunks; c0 += U) {
-    bool take[U][VEC];
-    bool need[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (sh) {
-        const bool up = __shfl_down_sync(0xffffffffu, win[u][0], 1);
-        const bool wrap = __shfl_sync(0xffffffffu, win[u + 1][0], 0);
-#pragma unroll
-        for (int e = 0; e + 1 < VEC; ++e) take[u][e] = win[u][e + 1];
-        take[u][VEC - 1] = lane == 31 ? wrap : up;
-      } else {
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) take[u][e] = win[u][e];
-      }
-      const int j0 = (c0 + u) * W + VEC * lane;
-      need[u] = MUT == EVB_MUT_TTPB1 || repair == EVB_REP_MIDPOINT_TARGET;
+  uint32_t w0 = window(cb0);
+  uint32_t w1 = cb0 + 1 <= nchunks ? window(cb0 + 1) : 0u;
+  for (int cc = cb0; cc < cb1; ++cc) {
+    uint32_t take = w0;
+    if (odd) {
+      const uint32_t up = __shfl_down_sync(0xffffffffu, w0, 1) & 1u;
+      const uint32_t wrap = __shfl_sync(0xffffffffu, w1, 0) & 1u;
+      take = (w0 >> 1) | ((lane == 31 ? wrap : up) << (VEC - 1));
+    }
+    const int j0 = cc * W + VEC * lane;
+    if (unsigned(jr - j0) < unsigned(VEC)) take |= 1u << (jr - j0);
+    const bool full = j0 + VEC <= D;
+    const bool need = MUT == EVB_MUT_TTPB1 || repair == EVB_REP_MIDPOINT_TARGET || take != FULL;
+    V va, vb, vc, vi;
+    if (full) {
+      va = __ldg(reinterpret_cast<const V*>(xa + j0));
+      vb = __ldg(reinterpret_cast<const V*>(xb + j0));
+      vc = __ldg(reinterpret_cast<const V*>(xc + j0));
+      if (need) vi = __ldg(reinterpret_cast<const V*>(xi + j0));
+    }
+    // the window after next (overlaps the loads)
+    const uint32_t w2 = cc + 2 <= min(nchunks, cb1) ? window(cc + 2) : 0u;
+    if (full) {
+      T ta[VEC], tb_[VEC], tc[VEC], ti[VEC] = {}, v[VEC];
+      VT::get(va, ta);
+      VT::get(vb, tb_);
+      VT::get(vc, tc);
+      if (need) VT::get(vi, ti);
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
-        take[u][e] = take[u][e] || (j0 + e == jr);
-        need[u] = need[u] || !take[u][e];
-      }
-    }
-    V va[U], vb[U], vc[U], vi[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j0 = (c0 + u) * W + VEC * lane;
-      if (j0 + VEC <= D) {
-        va[u] = ld16<HINT>(xa + j0, pol);
-        vb[u] = ld16<HINT>(xb + j0, pol);
-        vc[u] = ld16<HINT>(xc + j0, pol);
-        if (need[u]) vi[u] = ld16<HINT>(xi + j0, pol);
-      }
-    }
-    // the next iteration's windows (chunks c0 + U + 1 .. c0 + 2U), overlapping the loads
-    bool nw[U][VEC];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (c0 + U + 1 + u <= nchunks) window(c0 + U + 1 + u, nw[u]);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j0 = (c0 + u) * W + VEC * lane;
-      if (j0 + VEC <= D) {
-        T ta[VEC], tb_[VEC], tc[VEC], ti[VEC] = {}, v[VEC];
-        VT::get(va[u], ta);
-        VT::get(vb[u], tb_);
-        VT::get(vc[u], tc);
-        if (need[u]) VT::get(vi[u], ti);
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) {
-          T x;
-          if (take[u][e]) x = donor_gene<T>(MUT, MUT == EVB_MUT_TTPB1 ? ti[e] : T(0), ta[e], tb_[e], tc[e], Fi);
-          else x = ti[e];
-          if (repair == EVB_REP_CLIP) {
-            if (x < lb) x = lb;
-            if (x > ub) x = ub;
-          } else if (repair != EVB_REP_REINITIALIZE) {
-            if (x < lb || x > ub) x = repair_gene<T>(repair, x, ti[e], lb, ub);
-          }
-          v[e] = x;
+        T x = ((take >> e) & 1u) ? donor_gene<T>(MUT, MUT == EVB_MUT_TTPB1 ? ti[e] : T(0), ta[e], tb_[e], tc[e], Fi)
+                                 : ti[e];
+        if (CLIP) {
+          if (x < lb) x = lb;
+          if (x > ub) x = ub;
+        } else if (repair == EVB_REP_CLIP) {
+          if (x < lb) x = lb;
+          if (x > ub) x = ub;
+        } else if (repair != EVB_REP_REINITIALIZE) {
+          if (x < lb || x > ub) x = repair_gene<T>(repair, x, ti[e], lb, ub);
         }
+        v[e] = x;
+      }
+      __stcs(reinterpret_cast<V*>(out + j0), VT::make(v));
+    } else if (j0 < D) {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        const int j = j0 + e;
+        if (j >= D) break;
+        T x;
+        if ((take >> e) & 1u) x = donor_gene<T>(MUT, MUT == EVB_MUT_TTPB1 ? xi[j] : T(0), xa[j], xb[j], xc[j], Fi);
+        else x = xi[j];
+        if (CLIP || repair == EVB_REP_CLIP) {
+          if (x < lb) x = lb;
+          if (x > ub) x = ub;
+        } else if (repair != EVB_REP_REINITIALIZE) {
+          if (x < lb || x > ub) x = repair_gene<T>(repair, x, xi[j], lb, ub);
+        }
+        out[j] = x;
+      }
+    }
+    w0 = w1;
+    w1 = w2;
+  }
+}
+
+// The trial kernel with the rows staged through shared memory (the HBM regime, P x D beyond L2):
+// same warp-per-individual mapping, chunks, column blocks, take masks and per-gene arithmetic as
+// de_trial_vec_kernel (bit-identical trials), but every lane moves its 16 bytes of the four rows
+// (target, a, b, c) with cp.async (LDGSTS: no registers held while in flight) into a per-warp
+// ring of S chunk stages, S - 1 chunks ahead of the one it computes, so a warp keeps
+// (S - 1) x 2 KB of loads outstanding instead of one chunk's 2 KB in registers.  A lane reads back
+// only what it copied itself, so cp.async.wait_group alone orders it (no barrier).  Bulk copies
+// (TMA, one per 512-byte row chunk) measured slower: ~30 cycles of the SM's copy engine per op.
+template <typename T, int MUT, bool CLIP, int S, int MINB>
+__global__ void __launch_bounds__(32 * kTrialVecWarps, MINB) de_trial_stage_kernel(const de_dev<T> d) {
+  using VT = vec16<T>;
+  using V = typename VT::V;
+  constexpr int VEC = VT::N, W = 32 * VEC;
+  constexpr int STAGEB = 4 * 512;  // target, a, b, c: 512 bytes each
+  extern __shared__ __align__(128) uint8_t tsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t ring = ptx::smem_u32(tsm + size_t(warp) * S * STAGEB) + uint32_t(lane) * 16u;
+  const int i = blockIdx.x * kTrialVecWarps + warp;
+  ptx::griddep_wait();  // PDL (launch_pdl): predecessor data first
+  ptx::griddep_launch_dependents();
+  if (i >= d.P) return;  // warp-uniform
+  const int D = d.D;
+  const int nchunks = (D + W - 1) / W;
+  const int cpb = (nchunks + int(gridDim.y) - 1) / int(gridDim.y);
+  const int cb0 = int(blockIdx.y) * cpb, cb1 = min(nchunks, cb0 + cpb);
+  const int a = d.idx[4 * i + 0], b = d.idx[4 * i + 1], c = d.idx[4 * i + 2];
+  const T* xi = d.pop + size_t(i) * d.ldp + VEC * lane;
+  const T* xa = d.pop + size_t(a) * d.ldp + VEC * lane;
+  const T* xb = d.pop + size_t(b) * d.ldp + VEC * lane;
+  const T* xc = ((MUT == EVB_MUT_TTPB1 && c >= d.P) ? d.archive + size_t(c - d.P) * d.ldt
+                                                    : d.pop + size_t(c) * d.ldp) + VEC * lane;
+  // this lane's 16 bytes of chunk cc of the four rows (rows are pitched to 16 bytes, so a vector
+  // starting before D stays inside the row)
+  auto copy = [&](int cc) {
+    if (cc < cb1 && cc * W + VEC * lane < D) {
+      const uint32_t st = ring + uint32_t((cc - cb0) % S) * STAGEB;
+      const size_t off = size_t(cc) * W;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st), "l"(xi + off) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st + 512u), "l"(xa + off) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st + 1024u), "l"(xb + off) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st + 1536u), "l"(xc + off) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");  // one group per chunk, empty or not
+  };
+#pragma unroll
+  for (int k = 0; k < S - 1; ++k) copy(cb0 + k);
+  const T Fi = d.F[i];
+  const int jr = d.jrand[i];
+  T* __restrict__ out = d.trial + size_t(i) * d.ldt;
+  const uint64_t ctr_hi = (uint64_t(*d.gen_ptr) << 32) | uint32_t(i);
+  const T lb = d.lb, ub = d.ub;
+  const int repair = d.cfg.repair;
+  const take_rule rule(double(d.CR[i]));
+  const int64_t s0 = d.woff[i];
+  const bool odd = (s0 & 1) != 0;
+  const uint64_t blk0 = uint64_t(s0 >> 1) + uint64_t(lane * (VEC / 2));
+  auto window = [&](int cc) -> uint32_t {
+    uint32_t m = 0;
+#pragma unroll
+    for (int k = 0; k < VEC / 2; ++k) {
+      const uint64_t blk = blk0 + uint64_t(cc) * (W / 2) + uint64_t(k);
+      uint32_t cw[4] = {uint32_t(blk), uint32_t(blk >> 32), uint32_t(ctr_hi), uint32_t(ctr_hi >> 32)};
+      philox4x32_10_rk(cw, d.pk);
+      m |= rule.bit((uint64_t(cw[1]) << 32) | cw[0]) << (2 * k);
+      m |= rule.bit((uint64_t(cw[3]) << 32) | cw[2]) << (2 * k + 1);
+    }
+    return m;
+  };
+  uint32_t w0 = window(cb0);
+  for (int cc = cb0; cc < cb1; ++cc) {
+    copy(cc + S - 1);  // into the stage chunk cc - 1 used (this lane read it last iteration)
+    const uint32_t w1 = (odd && cc + 1 <= nchunks) ? window(cc + 1) : 0u;
+    uint32_t take = w0;
+    if (odd) {
+      const uint32_t up = __shfl_down_sync(0xffffffffu, w0, 1) & 1u;
+      const uint32_t wrap = __shfl_sync(0xffffffffu, w1, 0) & 1u;
+      take = (w0 >> 1) | ((lane == 31 ? wrap : up) << (VEC - 1));
+    }
+    const int j0 = cc * W + VEC * lane;
+    if (unsigned(jr - j0) < unsigned(VEC)) take |= 1u << (jr - j0);
+    asm volatile("cp.async.wait_group %0;" ::"n"(S - 1) : "memory");  // chunk cc's group landed
+    const uint32_t st = ring + uint32_t((cc - cb0) % S) * STAGEB;
+    if (j0 < D) {
+      T ti[VEC], ta[VEC], tb_[VEC], tc[VEC], v[VEC];
+      if constexpr (sizeof(T) == 8) {
+        const double2 q0 = ptx::lds_f64x2(st), q1 = ptx::lds_f64x2(st + 512u), q2 = ptx::lds_f64x2(st + 1024u),
+                      q3 = ptx::lds_f64x2(st + 1536u);
+        ti[0] = q0.x; ti[1] = q0.y; ta[0] = q1.x; ta[1] = q1.y;
+        tb_[0] = q2.x; tb_[1] = q2.y; tc[0] = q3.x; tc[1] = q3.y;
+      } else {
+        const float4 q0 = ptx::lds_f32x4(st), q1 = ptx::lds_f32x4(st + 512u), q2 = ptx::lds_f32x4(st + 1024u),
+                     q3 = ptx::lds_f32x4(st + 1536u);
+        VT::get(q0, ti); VT::get(q1, ta); VT::get(q2, tb_); VT::get(q3, tc);
+      }
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        T x = ((take >> e) & 1u) ? donor_gene<T>(MUT, MUT == EVB_MUT_TTPB1 ? ti[e] : T(0), ta[e], tb_[e], tc[e], Fi)
+                                 : ti[e];
+        if (CLIP || repair == EVB_REP_CLIP) {
+          if (x < lb) x = lb;
+          if (x > ub) x = ub;
+        } else if (repair != EVB_REP_REINITIALIZE) {
+          if (x < lb || x > ub) x = repair_gene<T>(repair, x, ti[e], lb, ub);
+        }
+        v[e] = x;
+      }
+      if (j0 + VEC <= D) {
         __stcs(reinterpret_cast<V*>(out + j0), VT::make(v));
-      } else if (j0 < D) {
+      } else {
 #pragma unroll
-        for (int e = 0; e < VEC; ++e) {
-          const int j = j0 + e;
-          if (j >= D) break;
-          T x;
-          if (take[u][e]) x = donor_gene<T>(MUT, MUT == EVB_MUT_TTPB1 ? xi[j] : T(0), xa[j], xb[j], xc[j], Fi);
-          else x = xi[j];
-          if (repair == EVB_REP_CLIP) {
-            if (x < lb) x = lb;
-            if (x > ub) x = ub;
-          } else if (repair != EVB_REP_REINITIALIZE) {
-            if (x < lb || x > ub) x = repair_gene<T>(repair, x, xi[j], lb, ub);
-          }
-          out[j] = x;
-        }
+        for (int e = 0; e < VEC; ++e)
+          if (j0 + e < D) out[j0 + e] = v[e];
       }
     }
-    // shift the windows: the last known one moves to the front, the new ones follow
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) win[0][e] = win[U][e];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) win[u + 1][e] = nw[u][e];
+    w0 = w1;
+    if (!odd && cc + 1 < cb1) w0 = window(cc + 1);
   }
 }
 
@@ -1333,6 +1430,7 @@ de_dev<T> make_dev(evb_de_s* e, void* pop, int64_t ldp, void* fit, double lb, do
   d.ub = T(ub);
   d.src.mode = r->mode;
   d.src.key = r->key;
+  d.pk = philox_keys(r->key);
   d.src.words = r->d_words;
   d.src.n_words = r->n_words;
   d.gen_ptr = r->d_gen;
@@ -1940,22 +2038,49 @@ void generation_t(evb_de_s* e, const device_problem* prob, evb_scratch_s* sc, vo
                      (ldp * int64_t(sizeof(T))) % 16 == 0 && reinterpret_cast<uintptr_t>(pop) % 16 == 0 &&
                      std::getenv("EVB_DE_TRIAL_SCALAR") == nullptr;
     if (vec) {
-      const dim3 g((e->P + kTrialVecWarps - 1) / kTrialVecWarps), bl(32 * kTrialVecWarps);
-      // (EVB_DE_TRIAL_VARIANT, tuning: 1 = L2 evict_last loads, 2 = two chunks per iteration,
-      // 0 = no register cap; default: <= 51 registers for 5 blocks per SM, measured 6% faster)
-      const int variant = std::getenv("EVB_DE_TRIAL_VARIANT") ? std::atoi(std::getenv("EVB_DE_TRIAL_VARIANT")) : 3;
-      if (e->cfg.mutation == EVB_MUT_TTPB1)
-        EVB_CUDA(launch_pdl(variant == 1   ? de_trial_vec_kernel<T, EVB_MUT_TTPB1, 1, true>
-                            : variant == 2 ? de_trial_vec_kernel<T, EVB_MUT_TTPB1, 2, false>
-                            : variant == 0 ? de_trial_vec_kernel<T, EVB_MUT_TTPB1, 1, false>
-                                           : de_trial_vec_kernel<T, EVB_MUT_TTPB1, 1, false, 5>,
-                            g, bl, 0, st, d));
-      else
-        EVB_CUDA(launch_pdl(variant == 1   ? de_trial_vec_kernel<T, EVB_MUT_RAND1, 1, true>
-                            : variant == 2 ? de_trial_vec_kernel<T, EVB_MUT_RAND1, 2, false>
-                            : variant == 0 ? de_trial_vec_kernel<T, EVB_MUT_RAND1, 1, false>
-                                           : de_trial_vec_kernel<T, EVB_MUT_RAND1, 1, false, 5>,
-                            g, bl, 0, st, d));
+      // column blocks (EVB_DE_TRIAL_COLBLOCKS: rows split into that many blocks of whole 512-byte
+      // chunks, grid.y; default whole rows)
+      const int wchunk = 32 * (16 / int(sizeof(T)));
+      const int nchunks = (e->D + wchunk - 1) / wchunk;
+      const int64_t pop_bytes = int64_t(e->P) * ldp * int64_t(sizeof(T));
+      // (measured with the staged kernel at P = 16384, D = 1000: whole rows 71.7 us, 4 blocks 78.9 us;
+      // the L2 saving is real — DRAM reads 290 -> 136 MB — but the extra per-block windows cost more)
+      int ncb = 1;
+      if (const char* s = std::getenv("EVB_DE_TRIAL_COLBLOCKS")) ncb = std::max(1, std::atoi(s));
+      ncb = std::min(ncb, nchunks);
+      ncb = (nchunks + (nchunks + ncb - 1) / ncb - 1) / ((nchunks + ncb - 1) / ncb);  // no empty block
+      const dim3 g((e->P + kTrialVecWarps - 1) / kTrialVecWarps, ncb), bl(32 * kTrialVecWarps);
+      // (EVB_DE_TRIAL_MINB, tuning: resident blocks per SM the register cap targets)
+      const int minb = std::getenv("EVB_DE_TRIAL_MINB") ? std::atoi(std::getenv("EVB_DE_TRIAL_MINB")) : 4;
+      const bool clip = e->cfg.repair == EVB_REP_CLIP;
+#define EVB_TRIAL_VEC(MUT, CLIP)                                                                          \
+  (minb >= 6 ? de_trial_vec_kernel<T, MUT, CLIP, 6>                                                      \
+             : minb == 5 ? de_trial_vec_kernel<T, MUT, CLIP, 5> : de_trial_vec_kernel<T, MUT, CLIP, 4>)
+      auto kern = e->cfg.mutation == EVB_MUT_TTPB1 ? (clip ? EVB_TRIAL_VEC(EVB_MUT_TTPB1, true)
+                                                           : EVB_TRIAL_VEC(EVB_MUT_TTPB1, false))
+                                                   : (clip ? EVB_TRIAL_VEC(EVB_MUT_RAND1, true)
+                                                           : EVB_TRIAL_VEC(EVB_MUT_RAND1, false));
+#undef EVB_TRIAL_VEC
+      // rows staged through shared memory where the population exceeds ~40 MB
+      // (EVB_DE_TRIAL_STAGE=0/1 overrides; EVB_DE_TRIAL_STAGES = ring depth 2..4)
+      bool staged = pop_bytes > (int64_t(40) << 20);
+      if (const char* s = std::getenv("EVB_DE_TRIAL_STAGE")) staged = std::atoi(s) != 0;
+      if (staged) {
+        const int ns = std::getenv("EVB_DE_TRIAL_STAGES") ? std::atoi(std::getenv("EVB_DE_TRIAL_STAGES")) : 3;
+#define EVB_TRIAL_STG(MUT, CLIP)                                                                      \
+  (ns <= 2 ? de_trial_stage_kernel<T, MUT, CLIP, 2, 4>                                                 \
+           : ns == 3 ? de_trial_stage_kernel<T, MUT, CLIP, 3, 4> : de_trial_stage_kernel<T, MUT, CLIP, 4, 3>)
+        auto ks = e->cfg.mutation == EVB_MUT_TTPB1 ? (clip ? EVB_TRIAL_STG(EVB_MUT_TTPB1, true)
+                                                           : EVB_TRIAL_STG(EVB_MUT_TTPB1, false))
+                                                   : (clip ? EVB_TRIAL_STG(EVB_MUT_RAND1, true)
+                                                           : EVB_TRIAL_STG(EVB_MUT_RAND1, false));
+#undef EVB_TRIAL_STG
+        const size_t smem = size_t(kTrialVecWarps) * std::max(2, std::min(4, ns)) * 2048;
+        EVB_CUDA(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        EVB_CUDA(launch_pdl(ks, g, bl, smem, st, d));
+      } else {
+        EVB_CUDA(launch_pdl(kern, g, bl, 0, st, d));
+      }
     } else if (e->cfg.crossover == EVB_CX_EXPONENTIAL)
       EVB_CUDA(launch_pdl(de_trial_kernel<T, EVB_CX_EXPONENTIAL>, dim3(e->P), dim3(th), 0, st, d));
     else

@@ -41,6 +41,43 @@ __host__ __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k
   }
 }
 
+// Philox4x32-10 with the 20 round keys precomputed (host side, once per source): kernels that
+// draw many blocks take them from their parameter bank instead of re-deriving the key schedule
+// per block, and the 32x32 -> 64 products are single mul.wide instructions.  Same values as
+// philox4x32_10.
+struct philox_keys {
+  uint32_t rk[20];
+  __host__ __device__ philox_keys(uint64_t key = 0) {
+    uint32_t k0 = uint32_t(key), k1 = uint32_t(key >> 32);
+    for (int r = 0; r < 10; ++r) {
+      rk[2 * r] = k0;
+      rk[2 * r + 1] = k1;
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+  }
+};
+
+__device__ __forceinline__ uint64_t mul_wide_u32(uint32_t a, uint32_t b) {
+  uint64_t p;
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(a), "r"(b));
+  return p;
+}
+
+__device__ __forceinline__ void philox4x32_10_rk(uint32_t c[4], const philox_keys& ks) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = mul_wide_u32(c[0], 0xD2511F53u);
+    const uint64_t p1 = mul_wide_u32(c[2], 0xCD9E8D57u);
+    const uint32_t n0 = uint32_t(p1 >> 32) ^ c[1] ^ ks.rk[2 * r];
+    const uint32_t n2 = uint32_t(p0 >> 32) ^ c[3] ^ ks.rk[2 * r + 1];
+    c[1] = uint32_t(p1);
+    c[3] = uint32_t(p0);
+    c[0] = n0;
+    c[2] = n2;
+  }
+}
+
 __host__ __device__ __forceinline__ uint64_t philox_word(uint64_t key, uint64_t ctr_hi, uint64_t n) {
   const uint64_t blk = n >> 1;
   uint32_t c[4] = {uint32_t(blk), uint32_t(blk >> 32), uint32_t(ctr_hi), uint32_t(ctr_hi >> 32)};

@@ -600,6 +600,27 @@ def test_trial_vector_kernel_equals_scalar(dev, monkeypatch, cfg, P, D, dtype):
     Philox word shuffle at the lane-31 seam) against the block-per-individual scalar kernel: the
     same generations from the same state, populations / fitness / archive / memories bit-identical;
     P = 2100 also runs the multi-item selection scan (> 1024 individuals)."""
+    _trial_vector_vs_scalar(dev, monkeypatch, cfg, P, D, dtype)
+
+
+@pytest.mark.parametrize("stages", ["0", "2", "3", "4"], ids=["regs", "stage2", "stage3", "stage4"])
+@pytest.mark.parametrize("colblocks", ["1", "2", "3", "5"])
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32], ids=["f64", "f32"])
+@pytest.mark.parametrize("case", [0, 1, 2, 3, 4, 5])
+def test_trial_vector_kernel_column_blocks(dev, monkeypatch, case, dtype, colblocks, stages):
+    """The large-P layouts of the vector kernel forced at small sizes: rows split into column
+    blocks (grid.y, keeping the donor slices L2-resident) and rows staged by cp.async through a
+    per-warp shared-memory ring (de_trial_stage_kernel, cp.async, 2-4 stages): bit-identical to the scalar kernel,
+    including seam words at block edges, blocks holding the row tail, odd D (16-byte-rounded copies)
+    and archive donors."""
+    cfg, P, D = VEC_CASES[case]
+    monkeypatch.setenv("EVB_DE_TRIAL_COLBLOCKS", colblocks)
+    monkeypatch.setenv("EVB_DE_TRIAL_STAGE", "0" if stages == "0" else "1")
+    monkeypatch.setenv("EVB_DE_TRIAL_STAGES", stages)
+    _trial_vector_vs_scalar(dev, monkeypatch, cfg, P, D, dtype)
+
+
+def _trial_vector_vs_scalar(dev, monkeypatch, cfg, P, D, dtype):
     from paper_2505_17430_b200.de import EVB_F32, EVB_F64
 
     o, m = O.shift_rotation(3, D)

@@ -101,7 +101,7 @@ def main():
                 e["algorithmic_bytes"] = 5 * 8 * 16384 * 1000
                 e["algorithmic_GBps"] = e["algorithmic_bytes"] / (dur * 1e-6) / 1e9
             if "de_trial" in kn:
-                traffic["de_trial_vec_kernel"] = rd + wr
+                traffic["de_trial_stage_kernel"] = rd + wr
                 e["algorithmic_bytes"] = 5 * 8 * 16384 * 1000
                 e["algorithmic_GBps"] = e["algorithmic_bytes"] / (dur * 1e-6) / 1e9
             key = f"{name}:{kn[:90]}"
