@@ -679,6 +679,433 @@ __global__ void __launch_bounds__(512) de_runs_kernel(const runs_args a) {
   if (a.split == 2) cg::this_cluster().sync();  // no CTA leaves while its peer may still write into it
 }
 
+// ---- fused variant (config 4's shape) -------------------------------------------------------
+// For runs whose components are all sphere / elliptic / Rastrigin / Ackley (base problem or
+// composition, D >= 32) the generation needs five block barriers instead of ~20:
+//   draws | trial | contraction + terms | values | selection + exchange
+// - the trial rows of this CTA's half live in the tensor-core layout (R8 x KS, zero pads); the
+//   A fragment is formed as x - o while it is loaded (rounded like transform_input's diff,
+//   problems/instance.hpp:66-67), so no s = x - o copy exists and the three components'
+//   contractions are ONE phase of (component, row tile, column tile) warp tasks;
+// - each task keeps its 8 x 16 accumulators in registers, applies the component's per-element
+//   term there (cos2pi_fast for Rastrigin / Ackley), reduces over the quad and writes one
+//   partial per (row, column tile, channel); the column-tile-0 task also forms the row's
+//   ||x - o||^2 from the A fragments it loads anyway;
+// - values: four adjacent lanes per individual (lane k = component k) sum the partials, form the
+//   base value and the raw weight, exchange them by shuffles and lane 0 normalises exactly as
+//   problems/instance.hpp:135-171;
+// - selection writes a winner's row into this CTA's and the peer's population copy; the two
+//   cluster barriers are split into arrive / wait (arrive after the trial phase = "my reads of
+//   the population are done", wait before the remote writes; arrive after them, wait at the top
+//   of the next generation), so neither CTA idles at a cluster barrier unless its peer is late.
+// Tolerance path like the tensor-core path above (fitness ~1e-15 relative, selections equal
+// except flagged near-ties).
+__host__ __device__ __forceinline__ bool fused_kind(int k) {
+  return k == EVB_SPHERE || k == EVB_ELLIPTIC || k == EVB_RASTRIGIN || k == EVB_ACKLEY;
+}
+
+struct fused_layout {
+  int R, R8, KS, D8, NT, NM;
+  size_t pop, tr, m, o, fit, partb, partd, ew, idx, bytes;  // offsets in doubles (idx too)
+};
+__host__ __device__ inline fused_layout fused_make_layout(int P, int D, int split, int n_mat) {
+  fused_layout L;
+  auto even = [](size_t n) { return (n + 1) & ~size_t(1); };
+  L.R = split == 2 ? (P + 1) / 2 : P;
+  L.R8 = round8(L.R);
+  L.KS = tc_ks(D);
+  L.D8 = round8(D);
+  L.NT = (D + 15) / 16;
+  L.NM = n_mat;
+  size_t off = 0;
+  L.pop = off;   off += even(size_t(P) * D);
+  L.tr = off;    off += size_t(L.R8) * L.KS;
+  L.m = off;     off += size_t(n_mat) * L.D8 * L.KS;
+  L.o = off;     off += size_t(n_mat) * L.KS;
+  L.fit = off;   off += even(3 * size_t(P));
+  L.partb = off; off += even(size_t(n_mat) * 2 * L.R8 * L.NT);
+  L.partd = off; off += even(size_t(n_mat) * L.R8);
+  L.ew = off;    off += size_t(L.KS);
+  L.idx = off;   off += even(size_t(P) * 4) / 2;  // 4 ints per individual
+  L.bytes = off * sizeof(double);
+  return L;
+}
+
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+
+// contraction + terms for the rows of sTr (rows < nrows are real): partials into sPartB / sPartD
+__device__ __forceinline__ void fused_contract(const run_problem& pr, const fused_layout& L, int D, int nrows,
+                                               const double* __restrict__ sTr, const double* __restrict__ sM,
+                                               const double* __restrict__ sO, const double* __restrict__ sEw,
+                                               double* __restrict__ sPartB, double* __restrict__ sPartD) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int nc = pr.n_comp > 0 ? pr.n_comp : 1;
+  const int mt = L.R8 >> 3, KS = L.KS;
+  const size_t m_len = size_t(L.D8) * KS;
+  const int ntasks = nc * mt * L.NT;
+  for (int task = warp; task < ntasks; task += nwarps) {
+    // column tile slowest (the narrow last tile's short tasks come last), row tile fastest
+    const int mi = task % mt;
+    const int rest = task / mt;
+    const int c = rest % nc, ni = rest / nc;
+    const int m0 = mi << 3, n0 = ni << 4;
+    const bool two = n0 + 8 < D;  // warp-uniform
+    double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0, d2 = 0.0;
+    const double* pa = sTr + (m0 + g) * KS + 2 * t;
+    const double* po = sO + c * KS + 2 * t;
+    const double* pb = sM + c * m_len + size_t(n0 + g) * KS + 2 * t;
+    if (two) {
+      const double* pb1 = pb + 8 * KS;
+#pragma unroll 7
+      for (int k0 = 0; k0 < KS; k0 += 8) {
+        const double2 x = *reinterpret_cast<const double2*>(pa + k0);
+        const double2 o = *reinterpret_cast<const double2*>(po + k0);
+        const double2 b0 = *reinterpret_cast<const double2*>(pb + k0);
+        const double2 b1 = *reinterpret_cast<const double2*>(pb1 + k0);
+        const double ax = __dsub_rn(x.x, o.x), ay = __dsub_rn(x.y, o.y);
+        ptx::dmma_8x8x4(c00, c01, ax, b0.x);
+        ptx::dmma_8x8x4(c10, c11, ax, b1.x);
+        ptx::dmma_8x8x4(c00, c01, ay, b0.y);
+        ptx::dmma_8x8x4(c10, c11, ay, b1.y);
+        if (ni == 0) d2 = fma(ay, ay, fma(ax, ax, d2));
+      }
+    } else {
+#pragma unroll 7
+      for (int k0 = 0; k0 < KS; k0 += 8) {
+        const double2 x = *reinterpret_cast<const double2*>(pa + k0);
+        const double2 o = *reinterpret_cast<const double2*>(po + k0);
+        const double2 b0 = *reinterpret_cast<const double2*>(pb + k0);
+        const double ax = __dsub_rn(x.x, o.x), ay = __dsub_rn(x.y, o.y);
+        ptx::dmma_8x8x4(c00, c01, ax, b0.x);
+        ptx::dmma_8x8x4(c00, c01, ay, b0.y);
+        if (ni == 0) d2 = fma(ay, ay, fma(ax, ax, d2));
+      }
+    }
+    // per-element terms on the accumulators (problems/batch.hpp:96-183 per kind)
+    const int kind = pr.kind[c];
+    double s1 = 0.0, s2 = 0.0;
+    auto term = [&](double v, int col) {
+      if (col >= D) return;
+      if (kind == EVB_ELLIPTIC) {
+        s1 += __dmul_rn(__dmul_rn(sEw[col], v), v);
+      } else if (kind == EVB_SPHERE) {
+        s1 = fma(v, v, s1);
+      } else {
+        const double cz = cos2pi_fast_ok(v) ? cos2pi_fast(v) : cos(__dmul_rn(two_pi_v<double>(), v));
+        if (kind == EVB_ACKLEY) {
+          s1 = fma(v, v, s1);
+          s2 += cz;
+        } else {
+          s1 += __dadd_rn(__dsub_rn(__dmul_rn(v, v), __dmul_rn(10.0, cz)), 10.0);
+        }
+      }
+    };
+    const int col = n0 + 2 * t;
+    term(c00, col);
+    term(c01, col + 1);
+    if (two) {
+      term(c10, col + 8);
+      term(c11, col + 9);
+    }
+    s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
+    if (kind == EVB_ACKLEY) {
+      s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, 2);
+    }
+    if (ni == 0) {
+      d2 += __shfl_xor_sync(0xffffffffu, d2, 1);
+      d2 += __shfl_xor_sync(0xffffffffu, d2, 2);
+    }
+    const int row = m0 + g;
+    if (t == 0 && row < nrows) {
+      sPartB[(size_t(c) * 2 * L.R8 + row) * L.NT + ni] = s1;
+      sPartB[(size_t(c) * 2 * L.R8 + L.R8 + row) * L.NT + ni] = s2;
+      if (ni == 0) sPartD[c * L.R8 + row] = d2;
+    }
+  }
+}
+
+// values of the nrows individuals from the partials: f[i], i < nrows
+__device__ __forceinline__ void fused_values(const run_problem& pr, const fused_layout& L, int D, int nrows,
+                                             const double* __restrict__ sPartB, const double* __restrict__ sPartD,
+                                             double* __restrict__ f) {
+  const int nc = pr.n_comp > 0 ? pr.n_comp : 1;
+  const int lane = threadIdx.x & 31;
+  const int bound = (nrows * kRunsMaxComp + 31) & ~31;  // whole warps: the quad exchanges use shuffles
+  for (int e = threadIdx.x; e < bound; e += blockDim.x) {
+    const int i = e >> 2, k = e & 3;
+    const bool live = i < nrows && k < nc;
+    double fk = 0.0, dk = 0.0, wr = 0.0;
+    if (live) {
+      double s1 = 0.0, s2 = 0.0;
+      const double* p1 = sPartB + (size_t(k) * 2 * L.R8 + i) * L.NT;
+      const double* p2 = p1 + size_t(L.R8) * L.NT;
+      for (int q = 0; q < L.NT; ++q) {
+        s1 += p1[q];
+        s2 += p2[q];
+      }
+      fk = pr.kind[k] == EVB_ACKLEY ? ackley_final<double>(s1, s2, D) : s1;
+      if (pr.n_comp > 0) {
+        dk = sPartD[k * L.R8 + i];
+        wr = dk == 0.0 ? -1.0
+                       : __dmul_rn(__ddiv_rn(1.0, __dsqrt_rn(dk)),
+                                   exp(__ddiv_rn(-dk, __dmul_rn(__dmul_rn(__dmul_rn(2.0, double(D)), pr.sigma[k]), pr.sigma[k]))));
+      }
+    }
+    double w[kRunsMaxComp], fks[kRunsMaxComp], dist[kRunsMaxComp];
+#pragma unroll
+    for (int q = 0; q < kRunsMaxComp; ++q) {
+      const int src = (lane & ~3) + q;
+      w[q] = __shfl_sync(0xffffffffu, wr, src);
+      fks[q] = __shfl_sync(0xffffffffu, fk, src);
+      dist[q] = __shfl_sync(0xffffffffu, dk, src);
+    }
+    if (k != 0 || i >= nrows) continue;
+    if (pr.n_comp == 0) {
+      f[i] = __dadd_rn(fks[0], pr.bias);
+      continue;
+    }
+    // weights exactly as problems/instance.hpp:135-171
+    int zero_count = 0;
+#pragma unroll
+    for (int q = 0; q < kRunsMaxComp; ++q)
+      if (q < nc && w[q] < 0.0) ++zero_count;
+    double wsum = 0.0;
+    if (zero_count > 0) {
+#pragma unroll
+      for (int q = 0; q < kRunsMaxComp; ++q)
+        if (q < nc) w[q] = w[q] < 0.0 ? 1.0 : 0.0;
+      wsum = double(zero_count);
+    } else {
+#pragma unroll
+      for (int q = 0; q < kRunsMaxComp; ++q)
+        if (q < nc) wsum = __dadd_rn(wsum, w[q]);
+      if (wsum == 0.0) {
+        int nearest = 0;
+        double dn = dist[0];
+#pragma unroll
+        for (int q = 1; q < kRunsMaxComp; ++q)
+          if (q < nc && dist[q] < dn) {
+            dn = dist[q];
+            nearest = q;
+          }
+#pragma unroll
+        for (int q = 0; q < kRunsMaxComp; ++q)
+          if (q == nearest) w[q] = 1.0;
+        wsum = 1.0;
+      }
+    }
+    double value = 0.0;
+#pragma unroll
+    for (int q = 0; q < kRunsMaxComp; ++q) {
+      if (q >= nc) continue;
+      const double wq = __ddiv_rn(w[q], wsum);
+      if (wq == 0.0) continue;
+      value = __dadd_rn(value, __dmul_rn(wq, __dadd_rn(__dmul_rn(pr.lambda[q], fks[q]), pr.cbias[q])));
+    }
+    f[i] = __dadd_rn(value, pr.bias);
+  }
+}
+
+template <bool PROF>
+__global__ void __launch_bounds__(512) de_runs_fused_kernel(const runs_args a) {
+  namespace cg = cooperative_groups;
+  extern __shared__ __align__(16) double sm[];
+  const int P = a.P, D = a.D;
+  const bool split = a.split == 2;
+  const int run = blockIdx.x / a.split;
+  const int rank = split ? int(cg::this_cluster().block_rank()) : 0;
+  const fused_layout L = fused_make_layout(P, D, a.split, a.n_mat);
+  const int p0 = split ? rank * L.R : 0;
+  const int p1 = split ? min(P, p0 + L.R) : P;
+  const int nrows = p1 - p0;
+  const int KS = L.KS;
+  double* sPop = sm + L.pop;
+  double* sTr = sm + L.tr;
+  double* sM = sm + L.m;
+  double* sO = sm + L.o;
+  double* sFit = sm + L.fit;
+  double* sTfit2 = sFit + P;
+  double* sPartB = sm + L.partb;
+  double* sPartD = sm + L.partd;
+  double* sEw = sm + L.ew;
+  int* sIdx = reinterpret_cast<int*>(sm + L.idx);
+  __shared__ run_problem s_pr;
+  for (int e = threadIdx.x; e < int(sizeof(run_problem) / 4); e += blockDim.x)
+    reinterpret_cast<int*>(&s_pr)[e] = reinterpret_cast<const int*>(a.probs + run)[e];
+  __syncthreads();
+  const run_problem& pr = s_pr;
+  {  // resident operands in the tensor-core layout (zero pads), trial pads zero once
+    const int nc = pr.n_comp > 0 ? pr.n_comp : 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    const size_t m_len = size_t(L.D8) * KS;
+    for (int c = 0; c < nc; ++c) {
+      for (int r = warp; r < L.D8; r += nwarps)
+        for (int k = lane; k < KS; k += 32)
+          sM[c * m_len + size_t(r) * KS + k] = (r < D && k < D) ? pr.rot[c][r * pr.ld + k] : 0.0;
+      for (int e = threadIdx.x; e < KS; e += blockDim.x) sO[c * KS + e] = e < D ? pr.shift[c][e] : 0.0;
+    }
+    for (int e = threadIdx.x; e < KS; e += blockDim.x) sEw[e] = (pr.ell_w && e < D) ? pr.ell_w[e] : 0.0;
+    for (int e = threadIdx.x; e < L.R8 * KS; e += blockDim.x) sTr[e] = 0.0;
+  }
+  __syncthreads();
+  const uint64_t key = a.keys[run];
+  double* gpop = a.pop + size_t(run) * P * D;
+  double* gfit = a.fit + size_t(run) * P;
+  phase_clock<PROF> pc{blockIdx.x == 0 ? a.prof : nullptr, 0};
+  cg::cluster_group cl = cg::this_cluster();
+  double* peerPop = split ? cl.map_shared_rank(sPop, rank ^ 1) : nullptr;
+  double* peerFit = split ? cl.map_shared_rank(sFit, rank ^ 1) : nullptr;
+  if (split) cl.sync();  // the peer's shared memory exists from here on
+
+  if (a.init) {  // init_population (core/population.hpp:88-98), sub-stream kSubInit of gen0
+    const uint64_t ctr = (uint64_t(a.gen0) << 32) | kSubInit;
+    for (int e = threadIdx.x; e < P * D; e += blockDim.x)
+      sPop[e] = __dadd_rn(a.lb, __dmul_rn(__dsub_rn(a.ub, a.lb), u01_of(philox_word(key, ctr, uint64_t(e)))));
+    __syncthreads();
+    for (int e = threadIdx.x; e < nrows * D; e += blockDim.x) {
+      const int i = e / D, j = e - i * D;
+      sTr[i * KS + j] = sPop[(p0 + i) * D + j];
+    }
+    __syncthreads();
+    fused_contract(pr, L, D, nrows, sTr, sM, sO, sEw, sPartB, sPartD);
+    __syncthreads();
+    fused_values(pr, L, D, nrows, sPartB, sPartD, sFit + p0);
+    __syncthreads();
+    if (split) {
+      for (int i = p0 + int(threadIdx.x); i < p1; i += blockDim.x) peerFit[i] = sFit[i];
+      cl.sync();
+    }
+    if (a.rec_on && rank == 0 && threadIdx.x == 0) rec_observe_seq<double>(a.rec, run, sFit, P);
+  } else {
+    for (int e = threadIdx.x; e < P * D; e += blockDim.x) sPop[e] = gpop[e];
+    for (int i = threadIdx.x; i < P; i += blockDim.x) sFit[i] = gfit[i];
+    __syncthreads();
+  }
+  const uint32_t g_first = a.gen0 + (a.init ? 1u : 0u);
+  pc.start();
+  for (int g = 0; g < a.G; ++g) {
+    const uint32_t gen = g_first + uint32_t(g);
+    double* sTfit = sTfit2 + (g & 1) * P;
+    __shared__ int s_best;
+    if (a.mutation != EVB_MUT_RAND1) {  // best/1: as de_runs_kernel
+      if (threadIdx.x < 32) {
+        double bf = 0.0;
+        int bi = -1;
+        for (int q = int(threadIdx.x); q < P; q += 32) {
+          const double fq = sFit[q];
+          if (!isnan(fq) && (bi < 0 || fq < bf)) {
+            bf = fq;
+            bi = q;
+          }
+        }
+        for (int off = 16; off > 0; off >>= 1) {
+          const double of = __shfl_xor_sync(0xffffffffu, bf, off);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+          if (oi >= 0 && (bi < 0 || of < bf || (of == bf && oi < bi))) {
+            bf = of;
+            bi = oi;
+          }
+        }
+        if (threadIdx.x == 0) s_best = bi < 0 ? 0 : bi;
+      }
+      __syncthreads();
+    }
+    for (int i = p0 + int(threadIdx.x); i < p1; i += blockDim.x) {  // draws (de/strategy.hpp:84-86, 187)
+      philox_prefetch_reader<4> r(key, (uint64_t(gen) << 32) | uint32_t(i));
+      int x1, x2, x3;
+      if (a.mutation == EVB_MUT_RAND1) {
+        do { x1 = draw_int(r, P); } while (x1 == i);
+        do { x2 = draw_int(r, P); } while (x2 == i || x2 == x1);
+        do { x3 = draw_int(r, P); } while (x3 == i || x3 == x1 || x3 == x2);
+      } else {
+        x1 = s_best;
+        do { x2 = draw_int(r, P); } while (x2 == i);
+        do { x3 = draw_int(r, P); } while (x3 == i || x3 == x2);
+      }
+      const int jr = draw_int(r, D);
+      sIdx[4 * i + 0] = x1;
+      sIdx[4 * i + 1] = x2;
+      sIdx[4 * i + 2] = x3;
+      sIdx[4 * i + 3] = (int(r.count) << 16) | jr;
+    }
+    __syncthreads();
+    pc.mark(0);
+    {  // trial rows of this half into the tensor-core layout
+      const int NB = D / 2 + 1;
+      for (int e = int(threadIdx.x); e < nrows * NB; e += blockDim.x) {
+        const int il = e / NB, q = e - il * NB, i = p0 + il;
+        const int packed = sIdx[4 * i + 3];
+        const int s0 = packed >> 16, jr = packed & 0xFFFF;
+        const int blk0 = s0 >> 1, nblk = ((s0 + D + 1) >> 1) - blk0;
+        if (q >= nblk) continue;
+        const double* xa = sPop + sIdx[4 * i] * D;
+        const double* xb = sPop + sIdx[4 * i + 1] * D;
+        const double* xc = sPop + sIdx[4 * i + 2] * D;
+        uint64_t w0, w1;
+        philox_pair(key, (uint64_t(gen) << 32) | uint32_t(i), uint64_t(blk0 + q), w0, w1);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int j = 2 * (blk0 + q) + h - s0;
+          if (j < 0 || j >= D) continue;
+          const double u = u01_of(h ? w1 : w0);
+          const double xi = sPop[i * D + j];
+          double v = xi;
+          if (u < a.CR || j == jr) v = __dadd_rn(xa[j], __dmul_rn(a.F, __dsub_rn(xb[j], xc[j])));
+          sTr[il * KS + j] = clip_or_mid(v, xi, a.lb, a.ub, a.repair);
+        }
+      }
+    }
+    __syncthreads();
+    if (split) cluster_arrive();  // this CTA's reads of the population / fitness copies are done
+    pc.mark(1);
+    fused_contract(pr, L, D, nrows, sTr, sM, sO, sEw, sPartB, sPartD);
+    __syncthreads();
+    pc.mark(3);
+    fused_values(pr, L, D, nrows, sPartB, sPartD, sTfit + p0);
+    __syncthreads();
+    pc.mark(6);
+    if (split) cluster_wait();  // the peer's reads are done too: its copies may be written
+    pc.mark(7);
+    {  // selection on this half (de/engine.hpp:36), winners into both copies
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+      for (int i = p0 + warp; i < p1; i += nwarps) {
+        const double ft = sTfit[i];
+        if (split && lane == 0) cl.map_shared_rank(sTfit, rank ^ 1)[i] = ft;
+        if (ft <= sFit[i]) {
+          const double* src = sTr + (i - p0) * KS;
+          for (int j = lane; j < D; j += 32) {
+            const double v = src[j];
+            sPop[i * D + j] = v;
+            if (split) peerPop[i * D + j] = v;
+          }
+          __syncwarp();
+          if (lane == 0) {
+            sFit[i] = ft;
+            if (split) peerFit[i] = ft;
+          }
+        }
+      }
+    }
+    if (split) {
+      cluster_arrive();
+      cluster_wait();
+    } else {
+      __syncthreads();
+    }
+    pc.mark(8);
+    if (a.rec_on && rank == 0 && threadIdx.x == 0) rec_observe_seq<double>(a.rec, run, sTfit, P);  // trials, i order
+  }
+  if (rank == 0) {
+    for (int e = threadIdx.x; e < P * D; e += blockDim.x) gpop[e] = sPop[e];
+    for (int i = threadIdx.x; i < P; i += blockDim.x) gfit[i] = sFit[i];
+  }
+  if (split) cl.sync();  // no CTA leaves while its peer may still write into it
+}
+
 size_t runs_smem(int P, int D, int split = 1, int n_mat = 1, int tc = 0) {
   const int S = (D % 2 == 1) ? D : D + 1;
   const size_t R = split == 2 ? size_t((P + 1) / 2) : size_t(P);
@@ -838,12 +1265,25 @@ extern "C" int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int 
            (tc_env ? std::atoi(tc_env) != 0 : dim >= 32);
     static const char* epi_env = std::getenv("EVB_RUNS_TC_EPI");
     a.tc_epi = a.tc && (epi_env ? std::atoi(epi_env) != 0 : 1);
-    const size_t smem = runs_smem(pop_size, dim, a.split, a.resident ? a.n_mat : 1, a.tc);
+    // fused generation (contraction + terms in registers, five barriers): every run a base or
+    // composition problem over sphere / elliptic / Rastrigin / Ackley (EVB_RUNS_FUSED=0: off)
+    static const char* fused_env = std::getenv("EVB_RUNS_FUSED");
+    bool fused = a.tc && a.tc_epi && (!fused_env || std::atoi(fused_env) != 0) &&
+                 fused_make_layout(pop_size, dim, a.split, a.n_mat).bytes + 64 <= 227 * 1024;
+    for (const run_problem& q : rp) {
+      if (q.hybrid) fused = false;
+      for (int c = 0; c < std::max(1, q.n_comp); ++c)
+        if (!fused_kind(q.kind[c])) fused = false;
+    }
+    const size_t smem = fused ? fused_make_layout(pop_size, dim, a.split, a.n_mat).bytes + 64
+                              : runs_smem(pop_size, dim, a.split, a.resident ? a.n_mat : 1, a.tc);
     require(smem <= 227 * 1024, "de_runs: run state does not fit in shared memory");
     static thread_local size_t smem_set = 0;
     if (smem > smem_set) {
       EVB_CUDA(cudaFuncSetAttribute(de_runs_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       EVB_CUDA(cudaFuncSetAttribute(de_runs_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      EVB_CUDA(cudaFuncSetAttribute(de_runs_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      EVB_CUDA(cudaFuncSetAttribute(de_runs_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       smem_set = smem;
     }
     static const bool prof = std::getenv("EVB_RUNS_PROFILE") != nullptr;
@@ -867,10 +1307,17 @@ extern "C" int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int 
       attr[0].val.clusterDim.z = 1;
       lc.attrs = attr;
       lc.numAttrs = 1;
-      err = cudaLaunchKernelEx(&lc, dprof ? de_runs_kernel<true> : de_runs_kernel<false>, a);
+      auto kern = fused ? (dprof ? de_runs_fused_kernel<true> : de_runs_fused_kernel<false>)
+                        : (dprof ? de_runs_kernel<true> : de_runs_kernel<false>);
+      err = cudaLaunchKernelEx(&lc, kern, a);
     } else {
-      if (dprof) de_runs_kernel<true><<<n_runs, 512, smem, st>>>(a);
-      else de_runs_kernel<false><<<n_runs, 512, smem, st>>>(a);
+      if (fused) {
+        if (dprof) de_runs_fused_kernel<true><<<n_runs, 512, smem, st>>>(a);
+        else de_runs_fused_kernel<false><<<n_runs, 512, smem, st>>>(a);
+      } else {
+        if (dprof) de_runs_kernel<true><<<n_runs, 512, smem, st>>>(a);
+        else de_runs_kernel<false><<<n_runs, 512, smem, st>>>(a);
+      }
       err = cudaGetLastError();
     }
     count_launch();
