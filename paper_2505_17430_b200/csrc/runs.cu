@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -74,7 +75,24 @@ struct run_problem {
   const double* hyb_w;
 };
 
+// crossover test u01(w) < CR as an integer compare (de.cu take_rule): u01(w) = (w >> 11) 2^-53
+// (core/rng.hpp:81-83), so u01(w) < CR <=> (w >> 11) < ceil(CR 2^53) <=> w <= lim; CR <= 0 never
+struct take_rule_host {
+  uint64_t lim;
+  int none;
+  static take_rule_host make(double cr) {
+    take_rule_host r;
+    const double t = std::ceil(cr * 0x1.0p53);
+    r.none = !(t >= 1.0);
+    const uint64_t ti = t >= 0x1.0p53 ? (uint64_t(1) << 53) : uint64_t(r.none ? 1.0 : t);
+    r.lim = ((ti - 1) << 11) | 0x7FFu;
+    return r;
+  }
+  __device__ __forceinline__ bool bit(uint64_t w) const { return !none && w <= lim; }
+};
+
 struct runs_args {
+  take_rule_host take;
   int P, D, G, ld;
   int mutation, repair;
   double F, CR, lb, ub;
@@ -745,11 +763,14 @@ __device__ __forceinline__ void fused_contract(const run_problem& pr, const fuse
   const int mt = L.R8 >> 3, KS = L.KS;
   const size_t m_len = size_t(L.D8) * KS;
   const int ntasks = nc * mt * L.NT;
+  const float inv_mt = 1.0f / float(mt), inv_nc = 1.0f / float(nc);
   for (int task = warp; task < ntasks; task += nwarps) {
     // column tile slowest (the narrow last tile's short tasks come last), row tile fastest
-    const int mi = task % mt;
-    const int rest = task / mt;
-    const int c = rest % nc, ni = rest / nc;
+    // (small non-negative ints: the float quotient of (n + 0.5) is exact after truncation)
+    const int rest = int((float(task) + 0.5f) * inv_mt);
+    const int mi = task - rest * mt;
+    const int ni = int((float(rest) + 0.5f) * inv_nc);
+    const int c = rest - ni * nc;
     const int m0 = mi << 3, n0 = ni << 4;
     const bool two = n0 + 8 < D;  // warp-uniform
     double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0, d2 = 0.0;
@@ -783,31 +804,43 @@ __device__ __forceinline__ void fused_contract(const run_problem& pr, const fuse
         if (ni == 0) d2 = fma(ay, ay, fma(ax, ax, d2));
       }
     }
-    // per-element terms on the accumulators (problems/batch.hpp:96-183 per kind)
+    // per-element terms on the accumulators (problems/batch.hpp:96-183 per kind); the four
+    // elements of a lane are evaluated side by side (one warp-uniform switch on the kind, no
+    // per-element branches), so their polynomial chains overlap
     const int kind = pr.kind[c];
-    double s1 = 0.0, s2 = 0.0;
-    auto term = [&](double v, int col) {
-      if (col >= D) return;
-      if (kind == EVB_ELLIPTIC) {
-        s1 += __dmul_rn(__dmul_rn(sEw[col], v), v);
-      } else if (kind == EVB_SPHERE) {
-        s1 = fma(v, v, s1);
-      } else {
-        const double cz = cos2pi_fast_ok(v) ? cos2pi_fast(v) : cos(__dmul_rn(two_pi_v<double>(), v));
-        if (kind == EVB_ACKLEY) {
-          s1 = fma(v, v, s1);
-          s2 += cz;
-        } else {
-          s1 += __dadd_rn(__dsub_rn(__dmul_rn(v, v), __dmul_rn(10.0, cz)), 10.0);
-        }
-      }
-    };
     const int col = n0 + 2 * t;
-    term(c00, col);
-    term(c01, col + 1);
-    if (two) {
-      term(c10, col + 8);
-      term(c11, col + 9);
+    const bool v0 = col < D, v1 = col + 1 < D, v2 = two && col + 8 < D, v3 = two && col + 9 < D;
+    double s1, s2 = 0.0;
+    if (kind == EVB_ELLIPTIC) {
+      const double w0 = v0 ? sEw[col] : 0.0, w1 = v1 ? sEw[col + 1] : 0.0;
+      const double w2 = v2 ? sEw[col + 8] : 0.0, w3 = v3 ? sEw[col + 9] : 0.0;
+      s1 = (__dmul_rn(__dmul_rn(w0, c00), c00) + __dmul_rn(__dmul_rn(w1, c01), c01)) +
+           (__dmul_rn(__dmul_rn(w2, c10), c10) + __dmul_rn(__dmul_rn(w3, c11), c11));
+    } else if (kind == EVB_SPHERE) {
+      s1 = fma(c11, c11, fma(c10, c10, fma(c01, c01, c00 * c00)));  // pad columns hold exact zeros
+    } else {
+      double z0, z1, z2, z3;
+      if (cos2pi_fast_ok(c00) && cos2pi_fast_ok(c01) && cos2pi_fast_ok(c10) && cos2pi_fast_ok(c11)) {
+        z0 = cos2pi_fast(c00);
+        z1 = cos2pi_fast(c01);
+        z2 = cos2pi_fast(c10);
+        z3 = cos2pi_fast(c11);
+      } else {  // out of the fast form's range (or not finite): the reference's expression
+        z0 = cos(__dmul_rn(two_pi_v<double>(), c00));
+        z1 = cos(__dmul_rn(two_pi_v<double>(), c01));
+        z2 = cos(__dmul_rn(two_pi_v<double>(), c10));
+        z3 = cos(__dmul_rn(two_pi_v<double>(), c11));
+      }
+      if (kind == EVB_ACKLEY) {
+        s1 = fma(c11, c11, fma(c10, c10, fma(c01, c01, c00 * c00)));
+        s2 = ((v0 ? z0 : 0.0) + (v1 ? z1 : 0.0)) + ((v2 ? z2 : 0.0) + (v3 ? z3 : 0.0));
+      } else {
+        const double r0 = __dadd_rn(__dsub_rn(__dmul_rn(c00, c00), __dmul_rn(10.0, z0)), 10.0);
+        const double r1 = __dadd_rn(__dsub_rn(__dmul_rn(c01, c01), __dmul_rn(10.0, z1)), 10.0);
+        const double r2 = __dadd_rn(__dsub_rn(__dmul_rn(c10, c10), __dmul_rn(10.0, z2)), 10.0);
+        const double r3 = __dadd_rn(__dsub_rn(__dmul_rn(c11, c11), __dmul_rn(10.0, z3)), 10.0);
+        s1 = ((v0 ? r0 : 0.0) + (v1 ? r1 : 0.0)) + ((v2 ? r2 : 0.0) + (v3 ? r3 : 0.0));
+      }
     }
     s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
     s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
@@ -986,11 +1019,38 @@ __global__ void __launch_bounds__(512) de_runs_fused_kernel(const runs_args a) {
     __syncthreads();
   }
   const uint32_t g_first = a.gen0 + (a.init ? 1u : 0u);
+  const bool rand1 = a.mutation == EVB_MUT_RAND1;
+  __shared__ int s_best;
+  // individual i's scalar draws of generation gen (de/strategy.hpp:84-86, 187) into sIdx
+  auto draw_individual = [&](int i, uint32_t gen) {
+    philox_prefetch_reader<4> r(key, (uint64_t(gen) << 32) | uint32_t(i));
+    int x1, x2, x3;
+    if (rand1) {
+      do { x1 = draw_int(r, P); } while (x1 == i);
+      do { x2 = draw_int(r, P); } while (x2 == i || x2 == x1);
+      do { x3 = draw_int(r, P); } while (x3 == i || x3 == x1 || x3 == x2);
+    } else {  // best/1: best = first strict minimum (fitness_order[0]), s_best
+      x1 = s_best;
+      do { x2 = draw_int(r, P); } while (x2 == i);
+      do { x3 = draw_int(r, P); } while (x3 == i || x3 == x2);
+    }
+    const int jr = draw_int(r, D);
+    sIdx[4 * i + 0] = x1;
+    sIdx[4 * i + 1] = x2;
+    sIdx[4 * i + 2] = x3;
+    sIdx[4 * i + 3] = (int(r.count) << 16) | jr;  // gene words start after the scalar words
+  };
+  // rand/1 draws depend on (key, generation, individual) only: generation g + 1's are made by
+  // the upper warps while the lower ones form generation g's values (the first ones here)
+  if (rand1 && a.G > 0) {
+    for (int i = p0 + int(threadIdx.x); i < p1; i += blockDim.x) draw_individual(i, g_first);
+    __syncthreads();
+  }
+  const take_rule_host take = a.take;
   pc.start();
   for (int g = 0; g < a.G; ++g) {
     const uint32_t gen = g_first + uint32_t(g);
     double* sTfit = sTfit2 + (g & 1) * P;
-    __shared__ int s_best;
     if (a.mutation != EVB_MUT_RAND1) {  // best/1: as de_runs_kernel
       if (threadIdx.x < 32) {
         double bf = 0.0;
@@ -1014,30 +1074,16 @@ __global__ void __launch_bounds__(512) de_runs_fused_kernel(const runs_args a) {
       }
       __syncthreads();
     }
-    for (int i = p0 + int(threadIdx.x); i < p1; i += blockDim.x) {  // draws (de/strategy.hpp:84-86, 187)
-      philox_prefetch_reader<4> r(key, (uint64_t(gen) << 32) | uint32_t(i));
-      int x1, x2, x3;
-      if (a.mutation == EVB_MUT_RAND1) {
-        do { x1 = draw_int(r, P); } while (x1 == i);
-        do { x2 = draw_int(r, P); } while (x2 == i || x2 == x1);
-        do { x3 = draw_int(r, P); } while (x3 == i || x3 == x1 || x3 == x2);
-      } else {
-        x1 = s_best;
-        do { x2 = draw_int(r, P); } while (x2 == i);
-        do { x3 = draw_int(r, P); } while (x3 == i || x3 == x2);
-      }
-      const int jr = draw_int(r, D);
-      sIdx[4 * i + 0] = x1;
-      sIdx[4 * i + 1] = x2;
-      sIdx[4 * i + 2] = x3;
-      sIdx[4 * i + 3] = (int(r.count) << 16) | jr;
+    if (!rand1) {
+      for (int i = p0 + int(threadIdx.x); i < p1; i += blockDim.x) draw_individual(i, gen);
+      __syncthreads();
     }
-    __syncthreads();
     pc.mark(0);
     {  // trial rows of this half into the tensor-core layout
       const int NB = D / 2 + 1;
+      const float inv_nb = 1.0f / float(NB);
       for (int e = int(threadIdx.x); e < nrows * NB; e += blockDim.x) {
-        const int il = e / NB, q = e - il * NB, i = p0 + il;
+        const int il = int((float(e) + 0.5f) * inv_nb), q = e - il * NB, i = p0 + il;
         const int packed = sIdx[4 * i + 3];
         const int s0 = packed >> 16, jr = packed & 0xFFFF;
         const int blk0 = s0 >> 1, nblk = ((s0 + D + 1) >> 1) - blk0;
@@ -1051,10 +1097,9 @@ __global__ void __launch_bounds__(512) de_runs_fused_kernel(const runs_args a) {
         for (int h = 0; h < 2; ++h) {
           const int j = 2 * (blk0 + q) + h - s0;
           if (j < 0 || j >= D) continue;
-          const double u = u01_of(h ? w1 : w0);
           const double xi = sPop[i * D + j];
           double v = xi;
-          if (u < a.CR || j == jr) v = __dadd_rn(xa[j], __dmul_rn(a.F, __dsub_rn(xb[j], xc[j])));
+          if (take.bit(h ? w1 : w0) || j == jr) v = __dadd_rn(xa[j], __dmul_rn(a.F, __dsub_rn(xb[j], xc[j])));
           sTr[il * KS + j] = clip_or_mid(v, xi, a.lb, a.ub, a.repair);
         }
       }
@@ -1066,6 +1111,10 @@ __global__ void __launch_bounds__(512) de_runs_fused_kernel(const runs_args a) {
     __syncthreads();
     pc.mark(3);
     fused_values(pr, L, D, nrows, sPartB, sPartD, sTfit + p0);
+    if (rand1 && g + 1 < a.G && threadIdx.x >= 256) {  // warps 8-15: individual il = 8 lane + (warp - 8)
+      for (int il = 8 * int(threadIdx.x & 31) + (int(threadIdx.x >> 5) - 8); il < nrows; il += 256)
+        draw_individual(p0 + il, gen + 1);
+    }
     __syncthreads();
     pc.mark(6);
     if (split) cluster_wait();  // the peer's reads are done too: its copies may be written
@@ -1227,6 +1276,7 @@ extern "C" int evb_de_runs(int dtype, const evb_de_config* cfg, int n_runs, int 
     a.repair = cfg->repair;
     a.F = cfg->f;
     a.CR = cfg->cr;
+    a.take = take_rule_host::make(cfg->cr);
     a.lb = lb;
     a.ub = ub;
     a.probs = dprobs;
