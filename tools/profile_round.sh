@@ -18,7 +18,7 @@ ncu --set full --clock-control none --import-source on -k regex:eval_f32_umma_sk
     python tools/prof_eval.py f32 5 4 > $OUT/eval32_ncu.log 2>&1
 # HBM update kernels at P=16384, D=1000 (L2-exceeding)
 python bench_configs.py --only hbm_update > $OUT/hbm_plain.json 2>&1 &&
-ncu --set full --clock-control none --import-source on -k regex:"de_trial_vec|de_select_multi|de_select_apply" -s 3 -c 3 \
+ncu --set full --clock-control none --import-source on -k regex:"de_trial|de_select_multi|de_select_apply" -s 3 -c 3 \
     -o $OUT/updates python bench_configs.py --only hbm_update > $OUT/updates_ncu.log 2>&1
 ncu --set full --clock-control none -k regex:pso_update -s 1 -c 1 -o $OUT/pso_update \
     python bench_configs.py --only hbm_update > $OUT/pso_ncu.log 2>&1
