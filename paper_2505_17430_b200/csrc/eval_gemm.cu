@@ -507,6 +507,37 @@ __device__ __forceinline__ void dmma_kslice(double (&acc)[TM][TN][2], uint32_t s
           ptx::dmma_8x8x4(acc[i][j][0], acc[i][j][1], h ? a[pp][i].y : a[pp][i].x, h ? b[pp][j].y : b[pp][j].x);
 }
 
+// The same slice for tall warp tiles (TM = 4: 112 accumulator registers): one operand pair at a
+// time, A fragments of the pair held, B fragments streamed per 8-column block one block ahead, so
+// only TM + 2 fragments are live beside the accumulators.
+template <int TM, int TN>
+__device__ __forceinline__ void dmma_kslice_stream(double (&acc)[TM][TN][2], uint32_t sA, uint32_t sB, uint32_t sO,
+                                                   int rA, int rB, int g, int t) {
+#pragma unroll
+  for (int pp = 0; pp < 2; ++pp) {
+    const int ch = 2 * t + pp;
+    const uint32_t col = uint32_t((ch ^ g) << 4);  // rows rA + 8 i + g and rB + 8 j + g: (r & 7) == g
+    const double2 o = ptx::lds_f64x2(sO + (4 * t + 2 * pp) * 8);
+    double2 a[TM];
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const double2 x = ptx::lds_f64x2(sA + (rA + i * 8 + g) * 128 + col);
+      a[i] = make_double2(__dsub_rn(x.x, o.x), __dsub_rn(x.y, o.y));
+    }
+    double2 b = ptx::lds_f64x2(sB + (rB + g) * 128 + col);
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      double2 bn = b;
+      if (j + 1 < TN) bn = ptx::lds_f64x2(sB + (rB + (j + 1) * 8 + g) * 128 + col);
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int i = 0; i < TM; ++i) ptx::dmma_8x8x4(acc[i][j][0], acc[i][j][1], h ? a[i].y : a[i].x, h ? b.y : b.x);
+      b = bn;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // K1: FP64 DMMA kernel
 template <int BM, int BN, int WM, int WN, int STAGES>
@@ -645,13 +676,20 @@ __global__ void __launch_bounds__(f64_cfg<BM, BN, WM, WN, STAGES>::THREADS, MINB
 // its own parked tile, with its own partials / tickets.
 constexpr int kMultiBM = 64, kMultiBN = 56, kMultiStages = 6;
 
-template <int NP>
+// BM_ = 128 (one-wave variant): 32 x 56 warp tiles (112 accumulator registers per thread), a
+// 5-stage ring; at config 1 its 8 x 18 = 144 CTAs are ONE wave on 148 SMs instead of 148 + 140.
+template <int NP, int BM_ = kMultiBM>
 struct f64m_cfg {
-  static constexpr int BM = kMultiBM, BN = kMultiBN, KB = 16, STAGES = kMultiStages;
-  static constexpr int WM = 4;  // MMA warps per group (16 x 56 warp tiles)
+  static constexpr int BM = BM_, BN = kMultiBN, KB = 16, STAGES = BM_ == 64 ? kMultiStages : 5;
+  static constexpr int WM = 4;  // MMA warps per group (16 x 56 or 32 x 56 warp tiles)
   static constexpr int NCW = NP * WM;
-  static constexpr int THREADS = (NCW + 1) * 32;
-  static constexpr int TM = 2, TN = 7;
+  // BM_ = 64: a separate TMA producer warp.  BM_ = 128: no 13th warp (a 4th warp on one SM
+  // sub-partition would cap every thread at 128 registers; 12 warps may take 168) — lane 0 of
+  // warp 0 refills the ring, LOOKAHEAD slices ahead of the slice it computes.
+  static constexpr bool PRODUCER_WARP = BM_ == 64;
+  static constexpr int LOOKAHEAD = STAGES - 2;
+  static constexpr int THREADS = (NCW + (PRODUCER_WARP ? 1 : 0)) * 32;
+  static constexpr int TM = BM / WM / 8, TN = 7;
   static constexpr int A_BYTES = BM * 128;
   static constexpr int B_BYTES = BN * 128;
   static constexpr int O_BYTES = 128;
@@ -666,13 +704,13 @@ struct multi_maps {
   CUtensorMap m[NP];
 };
 
-template <int NP>
-__global__ void __launch_bounds__(f64m_cfg<NP>::THREADS, 1)
+template <int NP, int BM_ = kMultiBM>
+__global__ void __launch_bounds__(f64m_cfg<NP, BM_>::THREADS, 1)
     eval_f64_dmma_multi_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ multi_maps<NP> tmM,
                                const __grid_constant__ fused_params<double> p0,
                                const __grid_constant__ fused_params<double> p1,
                                const __grid_constant__ fused_params<double> p2) {
-  using C = f64m_cfg<NP>;
+  using C = f64m_cfg<NP, BM_>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
@@ -708,42 +746,49 @@ __global__ void __launch_bounds__(f64m_cfg<NP>::THREADS, 1)
   }
   __syncthreads();
 
-  if (warp == C::NCW) {
-    // ---------------- producer: X once, then each problem's rotation tile and shift slice ----
-    if (lane == 0) {
-      ptx::prefetch_tma(&tmX);
-      for (int g = 0; g < NP; ++g) ptx::prefetch_tma(&tmM.m[g]);
-      int chunk = 0, chunk_end = 0;
-      for (int kb = 0; kb < KT; ++kb) {
-        const int s = kb % C::STAGES;
-        if (kb >= C::STAGES) ptx::mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
-        if (p0.kgate) {
-          const int gbase = (p0.kgate_rows > 0 && m0 >= p0.kgate_rows) ? p0.kgate_n : 0;
-          while (kb * C::KB >= chunk_end) {
-            ptx::wait_gate(p0.kgate + gbase + chunk, p0.kgate_epoch);
-            chunk_end = chunk + 1 < p0.kgate_n ? p0.kgate_end[chunk] : 1 << 30;
-            ++chunk;
-          }
-        }
-        uint8_t* st = smem + s * C::STAGE_BYTES;
-        ptx::mbar_arrive_expect_tx(&full[s], C::A_BYTES + NP * (C::B_BYTES + C::O_BYTES));
-        ptx::tma_load_2d(st, &tmX, &full[s], kb * C::KB, m0);
-#pragma unroll
-        for (int g = 0; g < NP; ++g) {
-          const fused_params<double>& pg = g == 0 ? p0 : (g == 1 ? p1 : p2);
-          ptx::tma_load_2d(st + C::A_BYTES + g * C::B_BYTES, &tmM.m[g], &full[s], kb * C::KB, n0);
-          ptx::bulk_load(st + C::A_BYTES + NP * C::B_BYTES + g * C::O_BYTES, pg.shift + size_t(kb) * C::KB, C::O_BYTES,
-                         &full[s]);
-        }
+  // producer step: slice kb into its stage — X once, then each problem's rotation tile and shift slice
+  int chunk = 0, chunk_end = 0;
+  auto produce = [&](int kb) {
+    const int s = kb % C::STAGES;
+    if (kb >= C::STAGES) ptx::mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
+    if (p0.kgate) {
+      const int gbase = (p0.kgate_rows > 0 && m0 >= p0.kgate_rows) ? p0.kgate_n : 0;
+      while (kb * C::KB >= chunk_end) {
+        ptx::wait_gate(p0.kgate + gbase + chunk, p0.kgate_epoch);
+        chunk_end = chunk + 1 < p0.kgate_n ? p0.kgate_end[chunk] : 1 << 30;
+        ++chunk;
       }
     }
-    return;
+    uint8_t* st = smem + s * C::STAGE_BYTES;
+    ptx::mbar_arrive_expect_tx(&full[s], C::A_BYTES + NP * (C::B_BYTES + C::O_BYTES));
+    ptx::tma_load_2d(st, &tmX, &full[s], kb * C::KB, m0);
+#pragma unroll
+    for (int g = 0; g < NP; ++g) {
+      const fused_params<double>& pg = g == 0 ? p0 : (g == 1 ? p1 : p2);
+      ptx::tma_load_2d(st + C::A_BYTES + g * C::B_BYTES, &tmM.m[g], &full[s], kb * C::KB, n0);
+      ptx::bulk_load(st + C::A_BYTES + NP * C::B_BYTES + g * C::O_BYTES, pg.shift + size_t(kb) * C::KB, C::O_BYTES,
+                     &full[s]);
+    }
+  };
+  if constexpr (C::PRODUCER_WARP) {
+    if (warp == C::NCW) {
+      if (lane == 0) {
+        ptx::prefetch_tma(&tmX);
+        for (int g = 0; g < NP; ++g) ptx::prefetch_tma(&tmM.m[g]);
+        for (int kb = 0; kb < KT; ++kb) produce(kb);
+      }
+      return;
+    }
+  } else if (threadIdx.x == 0) {
+    ptx::prefetch_tma(&tmX);
+    for (int g = 0; g < NP; ++g) ptx::prefetch_tma(&tmM.m[g]);
+    for (int kb = 0; kb < C::LOOKAHEAD && kb < KT; ++kb) produce(kb);
   }
 
   // ---------------- consumers: group g = warp / 4 computes problem g ----------------
   const int grp = warp / C::WM, wg = warp % C::WM;
   const int g8 = lane >> 2, t = lane & 3;
-  const int rA = wg * 16;
+  const int rA = wg * (C::BM / C::WM);
   double acc[C::TM][C::TN][2];
 #pragma unroll
   for (int i = 0; i < C::TM; ++i)
@@ -753,12 +798,17 @@ __global__ void __launch_bounds__(f64m_cfg<NP>::THREADS, 1)
   const uint32_t smem_base = ptx::smem_u32(smem);
   for (int kb = 0; kb < KT; ++kb) {
     const int s = kb % C::STAGES;
+    if constexpr (!C::PRODUCER_WARP) {  // refill the stage every warp left two slices ago
+      if (threadIdx.x == 0 && kb + C::LOOKAHEAD < KT) produce(kb + C::LOOKAHEAD);
+      __syncwarp();
+    }
     ptx::mbar_wait(&full[s], (kb / C::STAGES) & 1);
     if (kb == 0) stamp(1);
     const uint32_t sA = smem_base + s * C::STAGE_BYTES;
     const uint32_t sB = sA + C::A_BYTES + grp * C::B_BYTES;
     const uint32_t sO = sA + C::A_BYTES + NP * C::B_BYTES + grp * C::O_BYTES;
-    dmma_kslice<C::TM, C::TN>(acc, sA, sB, sO, rA, 0, g8, t);
+    if constexpr (C::TM > 2) dmma_kslice_stream<C::TM, C::TN>(acc, sA, sB, sO, rA, 0, g8, t);
+    else dmma_kslice<C::TM, C::TN>(acc, sA, sB, sO, rA, 0, g8, t);
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(&empty[s]);
   }
@@ -2196,8 +2246,20 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
   }
 }
 
+// Row-block height of the multi-problem kernel: 64 by default.  EVB_K1M_BM=128 selects the
+// one-wave variant (NP = 3; config 1: 144 CTAs of 128 x 56 x 3 instead of 148 + 140 of 64 x 56 x 3).
+// Measured equal on the device (216.2 vs 215.6 us, results bit-identical): the single wave saves one
+// CTA turnover and one first stage, but its epilogue is twice as long and nothing overlaps it
+// either; from host buffers it is slower (every CTA needs every column chunk: 320 vs 263 us).
+int multi_bm(int np, int64_t, int64_t) {
+  if (np != 3) return kMultiBM;
+  static const char* env = std::getenv("EVB_K1M_BM");
+  return env && std::atoi(env) == 128 ? 128 : kMultiBM;
+}
+
 int multi_first_wave_rows(int np, int64_t n_points, int64_t dim) {
   if (np < 2 || np > 3) return 0;
+  if (multi_bm(np, n_points, dim) == 128) return 0;  // one wave: every CTA needs all columns
   constexpr int BM = kMultiBM, BN = kMultiBN;
   const int64_t n_ntiles = (dim + BN - 1) / BN, n_mtiles = (n_points + BM - 1) / BM;
   // occupancy of the multi-problem kernel, queried once per NP (host cost of every host call)
@@ -2237,7 +2299,8 @@ bool gemm_eval_multi(const eval_request* rqs, int np, const void* X, int64_t ldx
   fused_params<double> fp[3]{};
   multi_maps<3> maps3{};
   multi_maps<2> maps2{};
-  constexpr int BM = kMultiBM, BN = kMultiBN;
+  constexpr int BN = kMultiBN;
+  const int BM = multi_bm(np, P, D);
   const int n_ntiles = (D + BN - 1) / BN, n_mtiles = (P + BM - 1) / BM;
   CUtensorMap tmX;
   if (!make_tma_2d(&tmX, X, EVB_F64, uint64_t(D), uint64_t(P), uint64_t(ldx) * 8, 16, BM)) return false;
@@ -2289,7 +2352,16 @@ bool gemm_eval_multi(const eval_request* rqs, int np, const void* X, int64_t ldx
   const bool nfast = rqs[0].kgate && rqs[0].kgate_rows > 0;
   fp[0].tiles_nfast = nfast ? 1 : 0;
   dim3 grid(nfast ? n_ntiles : n_mtiles, nfast ? n_mtiles : n_ntiles);
-  if (np == 3) {
+  if (np == 3 && BM == 128) {
+    using C = f64m_cfg<3, 128>;
+    static bool attr = false;
+    if (!attr) {
+      EVB_CUDA(cudaFuncSetAttribute(eval_f64_dmma_multi_kernel<3, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    C::SMEM));
+      attr = true;
+    }
+    eval_f64_dmma_multi_kernel<3, 128><<<grid, C::THREADS, C::SMEM, st>>>(tmX, maps3, fp[0], fp[1], fp[2]);
+  } else if (np == 3) {
     using C = f64m_cfg<3>;
     static bool attr = false;
     if (!attr) {

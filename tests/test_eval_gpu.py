@@ -434,3 +434,43 @@ np.save(sys.argv[1], out.cpu().numpy())
         got = np.load(f).astype(np.float64)
     err = np.max(np.abs(got - ref) / np.maximum(1.0, np.abs(ref)))
     assert err <= 1e-4, err
+
+
+def test_multi_problem_one_wave_variant_bit_identical():
+    """The multi-problem K1 with 128-row blocks (EVB_K1M_BM=128: config 1 as one wave of 144 CTAs,
+    32 x 56 warp tiles, ring refilled by warp 0; the switch is read once per process, hence the
+    subprocesses) returns the same bits as the default 64-row kernel, device and host buffers,
+    at config 1 and at a ragged size."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    from pathlib import Path
+
+    code = """
+import sys; sys.path.insert(0, '.'); sys.path.insert(0, 'oracle')
+import numpy as np, torch, oracle as O, paper_2505_17430_b200 as evb
+res = []
+for (P, D) in ((1024, 1000), (333, 217)):
+    o, m = O.shift_rotation(7, D); Xh = O.population(7, P, D)
+    kinds = [evb.BaseKind.elliptic, evb.BaseKind.rastrigin, evb.BaseKind.ackley]
+    probs = [evb.ProblemInstance.base(k, o, m, 0.0) for k in kinds]
+    outs = [torch.empty(P, dtype=torch.float64, device='cuda') for _ in kinds]
+    sc = evb.EvalScratch()
+    evb.evaluate_batch_problems(probs, torch.from_numpy(Xh).cuda(), sc, outs)
+    torch.cuda.synchronize()
+    res.append(np.stack([t.cpu().numpy() for t in outs]).ravel())
+    res.append(np.concatenate(evb.batched_evaluate_many(probs, Xh, sc)))
+np.save(sys.argv[1], np.concatenate(res))
+"""
+    root = Path(__file__).resolve().parents[1]
+    got = {}
+    with tempfile.TemporaryDirectory() as td:
+        for bm in ("64", "128"):
+            f = str(Path(td) / f"v{bm}.npy")
+            r = subprocess.run([sys.executable, "-c", code, f], cwd=str(root), capture_output=True, text=True,
+                               timeout=300, env=dict(os.environ, EVB_K1M_BM=bm))
+            assert r.returncode == 0, r.stderr[-2000:]
+            got[bm] = np.load(f)
+    assert np.array_equal(got["64"].view(np.uint64), got["128"].view(np.uint64))
+    assert np.all(np.isfinite(got["128"]))
