@@ -1542,25 +1542,37 @@ __global__ void __launch_bounds__(kRunThreads, 1) de_run_kernel(const de_run_arg
   T* sS = reinterpret_cast<T*>(smem_raw + mt_bytes);                            // Q x D: x - o / pre terms
   T* sZ = sS + size_t(Q) * D;                                                   // Q x D
   T* sT = sZ + size_t(Q) * D;                                                   // Q x D: owned trials
-  T* sR = sT + size_t(Q) * D;                                                   // Q x 4 x D: target + donor rows
-  T* sFit = sR + 4 * size_t(Q) * D;                                             // P
+  T* sFit = sT + size_t(Q) * D;                                                 // P
   T* sMemF = sFit + P;                                                          // H
   T* sMemC = sMemF + H;                                                         // H
   T* sTf = sMemC + H;                                                           // Q
   T* sQf = sTf + Q;                                                             // Q x 2: F, CR
-  double* sG = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sQf + 2 * Q) + 15) & ~uintptr_t(15));  // 3 x P
+  T* sAll = sQf + 2 * Q;                                                        // 3 x P: every trial's fitness, F, CR
+  double* sG = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sAll + 3 * P) + 15) & ~uintptr_t(15));  // 3 x P
   int NP2 = 1;
   while (NP2 < P) NP2 <<= 1;
   unsigned long long* sKey = reinterpret_cast<unsigned long long*>(sG + 3 * P);  // P order keys
   int* sIdx = reinterpret_cast<int*>(sKey + P);  // NP2 order slots + P rank counters
-  int* sCnt = sIdx + NP2 + P;                    // NC x 2
-  int* sQi = sCnt + 2 * NC;                      // Q x 8: donors, jrand, first gene word
+  int* sOwner = sIdx + NP2 + P;                  // archive_cap: last push index per archive slot
+  int* sWC = sOwner + d.archive_cap;             // 2 x 32: per-warp (pushes, successes)
+  int* sWin = sWC + 64;                          // Q x 2: owned individual won, its archive slot
+  int* sQi = sWin + 2 * Q;                       // Q x 8: donors, jrand, first gene word
   uint64_t* bar = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(sQi + 8 * Q) + 7) & ~uintptr_t(7));  // 2
-  __shared__ int s_misc[4];  // [0] archive size at the generation start
+  __shared__ int s_misc[4];  // [0] archive size at the generation start, [3] SHADE write index
+  // adapter transcendentals of the NEXT generation, computed while the dots run (see `speculate`):
+  // per owned individual kSpec Cauchy tangents, then kSpec normal offsets
+  constexpr int kSpec = 3;
+  __shared__ double s_pre[32 * 2 * kSpec];
+  constexpr int kVict = 256;
+  __shared__ int sVict[kVict];        // archive slots of the generation's first victim words
+  __shared__ unsigned long long s_K;  // order key of last generation's p_count-th member
+  __shared__ int s_nc;                // candidate counter of the rank phase
 
   if (tid == 0) {
     ptx::mbar_init(bar, 1);
     ptx::fence_mbar_init();
+    s_K = ~0ull;
+    s_nc = 0;
   }
   __syncthreads();
   if (tid == 0) {  // M^T once for the whole launch
@@ -1572,6 +1584,43 @@ __global__ void __launch_bounds__(kRunThreads, 1) de_run_kernel(const de_run_arg
   const unsigned E0 = *d.epoch;
   const bool ttpb = d.cfg.mutation == EVB_MUT_TTPB1, best = d.cfg.mutation == EVB_MUT_BEST1;
   const bool adapt = d.cfg.parameter == EVB_PAR_SHADE || d.cfg.parameter == EVB_PAR_JADE;
+  const bool shade = d.cfg.parameter == EVB_PAR_SHADE;
+  const int dw = (nthr >> 5) - 1;  // draw warp: lane q draws owned individual q
+  philox_prefetch_reader<5> rd;    // lane q's reader of the current generation (reset one generation ahead)
+  // The adapter draws (de/parameter.hpp:28-43) cost a tan, a log and a cos per individual, but
+  // only `mu + 0.1 * tan(..)` and `mu + (0.1 rr) cos(..)` depend on the memories.  The memory-
+  // independent factors of generation gen_n are computed here, off the critical path (threads
+  // that have no dot products to do), for the first kSpec Cauchy attempts: attempt k reads word
+  // b0 + k, and if it is the accepted one the normal reads words b0 + k + 1, b0 + k + 2.  The
+  // draw warp then only adds, compares and skips words; an individual whose first kSpec attempts
+  // all fail (p ~ 2.5e-4 at mu = 0.5) falls back to the sequential draws.  Same operations and
+  // roundings as draw_cauchy / draw_normal (rng.cuh), so F, CR and the word counts are identical.
+  auto speculate = [&](uint32_t gen_n) {
+    const int b0 = shade ? 1 : 0;
+    if (warp == dw) {
+      if (lane < nq) rd.reset(d.src.key, (uint64_t(gen_n) << 32) | uint32_t(i0 + lane));
+    } else if (warp == dw - 1 || warp == dw - 4 || warp == dw - 5) {
+      // (three warps of the two SM sub-partitions that hold the fewest dot-product warps)
+      const int wl = warp == dw - 5 ? 0 : (warp == dw - 4 ? 1 : 2);
+      for (int e = wl * 32 + lane; e < 2 * kSpec * nq; e += 96) {
+        const int q = e / (2 * kSpec), r = e - q * 2 * kSpec;
+        const uint64_t ctr = (uint64_t(gen_n) << 32) | uint32_t(i0 + q);
+        double v;
+        if (r < kSpec) {
+          const double u = u01pos_of(philox_word(d.src.key, ctr, uint64_t(b0 + r)));
+          v = tan(__dmul_rn(3.14159265358979323846, __dsub_rn(u, 0.5)));
+        } else {
+          const int k = r - kSpec;
+          const double u1 = u01pos_of(philox_word(d.src.key, ctr, uint64_t(b0 + k + 1)));
+          const double u2 = u01_of(philox_word(d.src.key, ctr, uint64_t(b0 + k + 2)));
+          const double rr = __dsqrt_rn(__dmul_rn(-2.0, log(u1)));
+          v = __dmul_rn(__dmul_rn(0.1, rr), cos(__dmul_rn(2.0 * 3.14159265358979323846, u2)));
+        }
+        s_pre[e] = v;
+      }
+    }
+  };
+  if (adapt) speculate(gen0);
   cl.sync();  // every CTA's shared memory exists before the first DSMEM write
   long long t_last = clock64();
   auto mark = [&](int k) {  // phase boundary (after a barrier): CTA 0 thread 0 accumulates cycles
@@ -1584,7 +1633,6 @@ __global__ void __launch_bounds__(kRunThreads, 1) de_run_kernel(const de_run_arg
 
   for (int g = 0; g < a.G; ++g) {
     const uint32_t gen = gen0 + uint32_t(g);
-    const unsigned tag = E0 + unsigned(g) + 1u;
     // ---- A: fitness, order, adapter memories, archive size ----
     // (read from L2 once; later generations get them pushed into every CTA's copy over DSMEM by
     // the CTA that changed them, phase G)
@@ -1595,132 +1643,197 @@ __global__ void __launch_bounds__(kRunThreads, 1) de_run_kernel(const de_run_arg
           sMemF[t] = ldcg(d.mem_f + t);
           sMemC[t] = ldcg(d.mem_cr + t);
         }
-      if (tid == 0) s_misc[0] = ldcg(d.arch_size);
+      if (tid == 0) {
+        s_misc[0] = ldcg(d.arch_size);
+        s_misc[3] = adapt ? ldcg(d.write_index) : 0;
+      }
       __syncthreads();
     }
     mark(11);
-    // the last warp draws the owned individuals' adapter samples (they need no order) while the
-    // other warps rank the population (named barrier 1 over them); then the mutation draws
-    const int dw = (nthr >> 5) - 1;  // draw warp
+    // the last warp draws for the owned individuals (adapter sample, mutation indices, jrand:
+    // draw_scalars' order and word counts) while the other warps rank the population (named
+    // barrier 1 over them); a donor picked by rank (best/1, current-to-pbest) is kept as a rank
+    // and resolved once the order exists
     de_dev<T> dl = d;
-    dl.order = sIdx;  // sorted: the first p_count entries are the order
     dl.mem_f = sMemF;
     dl.mem_cr = sMemC;
-    philox_prefetch_reader<5> rd;
+    const int arch_size = s_misc[0];
     T dF = T(0), dCR = T(0);
-    int dslot = -1;
+    int dslot = -1, da = 0, db = 0, dc = 0, djr = 0;
     if (warp == dw) {
       if (lane < nq) {
-        rd.reset(d.src.key, (uint64_t(gen) << 32) | uint32_t(i0 + lane));
-        draw_adapter<T>(dl, rd, dF, dCR, dslot);
+        const int i = i0 + lane;
+        if (adapt) {  // finish the speculated draws: sample_scale_factor / sample_crossover_rate
+          if (shade) dslot = draw_int(rd, d.cfg.memory_size);
+          const double muf = double(sMemF[shade ? dslot : 0]), muc = double(sMemC[shade ? dslot : 0]);
+          const double* pre = s_pre + lane * 2 * kSpec;
+          double f = 0.0;
+          int k = 0;
+          bool ok = false;
+          for (; k < kSpec; ++k) {
+            rd.next();  // the attempt's word
+            f = __dadd_rn(muf, __dmul_rn(0.1, pre[k]));
+            if (f > 0.0) {
+              ok = true;
+              break;
+            }
+          }
+          if (!ok)
+            for (int attempt = kSpec; attempt < 100; ++attempt) {
+              f = draw_cauchy(rd, muf, 0.1);
+              if (f > 0.0) break;
+            }
+          if (f <= 0.0) f = 0.1;
+          dF = T(fmin(f, 1.0));
+          double v;
+          if (ok) {
+            rd.next();
+            rd.next();
+            v = __dadd_rn(muc, pre[kSpec + k]);
+          } else {
+            v = draw_normal(rd, muc, 0.1);
+          }
+          dCR = T(v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v));
+        } else {
+          rd.reset(d.src.key, (uint64_t(gen) << 32) | uint32_t(i));
+          draw_adapter<T>(dl, rd, dF, dCR, dslot);
+        }
+        // draw_mutation's draws (de/strategy.hpp:84-86, 107-110, 143-152, 187); da is a rank for
+        // best/1 and current-to-pbest
+        if (best) {
+          da = 0;
+          do { db = draw_int(rd, P); } while (db == i);
+          do { dc = draw_int(rd, P); } while (dc == i || dc == db);
+        } else if (ttpb) {
+          da = draw_int(rd, d.p_count);
+          do { db = draw_int(rd, P); } while (db == i);
+          const int pool = P + (d.cfg.use_archive ? arch_size : 0);
+          do { dc = draw_int(rd, pool); } while (dc == i || dc == db);
+        } else {
+          do { da = draw_int(rd, P); } while (da == i);
+          do { db = draw_int(rd, P); } while (db == i || db == da);
+          do { dc = draw_int(rd, P); } while (dc == i || dc == da || dc == db);
+        }
+        djr = draw_int(rd, D);
+        sQi[8 * lane + 0] = da;
+        sQi[8 * lane + 1] = db;
+        sQi[8 * lane + 2] = dc;
+        sQi[8 * lane + 3] = djr;
+        sQi[8 * lane + 4] = int(rd.count);
+        sQf[2 * lane] = dF;
+        sQf[2 * lane + 1] = dCR;
       }
-    } else if (ttpb || best) {  // (fitness, index) ranks, NaN last: thread (i, chunk) counts the
-      // members of its j chunk that precede i on order_key (integer shared atomics)
+    } else if (ttpb || best) {
+      // (fitness, index) ranks, NaN last.  Only the first p_count ranks are needed, and a member's
+      // key never increases inside the launch (a trial replaces its parent only when it is <=), so
+      // the key K of last generation's p_count-th member bounds this generation's: the candidates
+      // {key <= K} hold every member that precedes any of them, and ranks among the candidates are
+      // ranks in the population.  Generation 0 ranks everybody.  Thread (candidate, chunk) counts
+      // the candidates of its chunk that precede it on order_key (integer shared atomics).
       const int nr = nthr - 32;
-      const int nch = max(1, min(8, nr / P));
+      int* sCand = reinterpret_cast<int*>(sG);  // the success records' space is free until phase G
+      const bool narrow = g > 0;
+      const unsigned long long K = s_K;
       for (int t = tid; t < P; t += nr) {
         sIdx[NP2 + t] = 0;  // rank counters (after the order slots)
-        sKey[t] = order_key(sFit[t]);
+        const unsigned long long key = order_key(sFit[t]);
+        sKey[t] = key;
+        if (!narrow || key <= K) sCand[atomicAdd(&s_nc, 1)] = t;
       }
       ptx::named_bar_sync(1, nr);
-      for (int t = tid; t < P * nch; t += nr) {
-        const int ch = t / P, i = t - ch * P;
-        const int j0 = (P * ch) / nch, j1 = (P * (ch + 1)) / nch;
+      const int C = s_nc;
+      const int nch = max(1, min(8, nr / C));
+      for (int t = tid; t < C * nch; t += nr) {
+        const int ch = t / C, ci = t - ch * C;
+        const int j0 = (C * ch) / nch, j1 = (C * (ch + 1)) / nch;
+        const int i = sCand[ci];
         const unsigned long long ki = sKey[i];
         int cnt = 0;
 #pragma unroll 4
-        for (int j = j0; j < j1; ++j) {
+        for (int cj = j0; cj < j1; ++cj) {
+          const int j = sCand[cj];
           const unsigned long long kj = sKey[j];
           cnt += (kj < ki || (kj == ki && j < i)) ? 1 : 0;
         }
         if (cnt) atomicAdd(&sIdx[NP2 + i], cnt);
       }
       ptx::named_bar_sync(1, nr);
-      for (int i = tid; i < P; i += nr) {
+      for (int ci = tid; ci < C; ci += nr) {
+        const int i = sCand[ci];
         const int rk = sIdx[NP2 + i];
         if (rk < d.p_count) sIdx[rk] = i;
+      }
+      ptx::named_bar_sync(1, nr);
+      if (tid == 0) {
+        s_K = sKey[sIdx[d.p_count - 1]];
+        s_nc = 0;
       }
     }
     __syncthreads();
     mark(0);
-    const int arch_size = s_misc[0];
-    // ---- B: the rest of the owned individuals' draws ----
+    // ---- B: donors picked by rank, the engine's exported draws ----
+    const bool a_by_rank = ttpb || best;
     if (warp == dw && lane < nq) {
       const int i = i0 + lane;
-      draw_mutation<T>(dl, i, arch_size, rd, dF, dCR, dslot);
+      d.F[i] = dF;
+      d.CR[i] = dCR;
+      d.slot[i] = dslot;
+      d.idx[4 * i + 0] = a_by_rank ? sIdx[da] : da;
+      d.idx[4 * i + 1] = db;
+      d.idx[4 * i + 2] = dc;
+      d.jrand[i] = djr;
       d.woff[i] = rd.count;
       d.rword[i] = rd.count + D;
       d.wcount[i] = rd.count + D;
-      // the same values for this CTA's later phases from shared memory (no L2 round trip)
-      sQi[8 * lane + 0] = d.idx[4 * i + 0];
-      sQi[8 * lane + 1] = d.idx[4 * i + 1];
-      sQi[8 * lane + 2] = d.idx[4 * i + 2];
-      sQi[8 * lane + 3] = d.jrand[i];
-      sQi[8 * lane + 4] = int(rd.count);
-      sQf[2 * lane] = dF;
-      sQf[2 * lane + 1] = dCR;
     }
-    __syncthreads();
     mark(1);
     // ---- C: trial genes (binomial, de_trial_kernel's arithmetic) ----
-    // the owned individuals' target and donor rows (population or archive, L2) into shared memory
-    // with every load of the CTA in flight at once, then thread per (individual, Philox block)
-    for (int rt0 = 2 * warp; rt0 < nq * 4; rt0 += 2 * (nthr / 32)) {  // warp per 2 rows, all loads in flight
-      const T* rows[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int rt = min(rt0 + h, nq * 4 - 1);
-        const int q = rt >> 2, w = rt & 3;
-        const int src = w == 0 ? i0 + q : sQi[8 * q + (w - 1)];
-        rows[h] = (w == 3 && ttpb && src >= P) ? d.archive + size_t(src - P) * d.ldt : d.pop + size_t(src) * d.ldp;
-      }
-      constexpr int NL = 4;  // loads per lane per row (D <= 128 in one pass)
-      for (int j0 = 0; j0 < D; j0 += 32 * NL) {
-        T v[2][NL];
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int u = 0; u < NL; ++u) {
-            const int j = j0 + lane + 32 * u;
-            v[h][u] = j < D ? ldcg(rows[h] + j) : T(0);
-          }
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int u = 0; u < NL; ++u) {
-            const int j = j0 + lane + 32 * u;
-            if (j < D && rt0 + h < nq * 4) sR[size_t(rt0 + h) * D + j] = v[h][u];
-          }
-      }
-    }
-    __syncthreads();
+    // thread = (owned individual, two Philox blocks = four gene words): its target / donor genes
+    // come straight from L2 (every load of the CTA in flight at once) while the words are computed
     {
-      const int NB = D / 2 + 1;
-      for (int e = tid; e < nq * NB; e += nthr) {
-        const int q = e / NB, b = e - q * NB;
+      const int NB = D / 2 + 1;      // blocks covering D gene words at any offset parity
+      const int NB2 = (NB + 1) / 2;  // two blocks per thread
+      for (int e = tid; e < nq * NB2; e += nthr) {
+        const int q = e / NB2, b2 = e - q * NB2;
         const int i = i0 + q;
         const int64_t s0 = sQi[8 * q + 4];
         const int64_t blk0 = s0 >> 1;
         const int64_t nblk = ((s0 + D + 1) >> 1) - blk0;
-        if (b >= nblk) continue;
+        const int ic = sQi[8 * q + 2];
+        const T* xi = d.pop + size_t(i) * d.ldp;
+        const int ia = a_by_rank ? sIdx[sQi[8 * q + 0]] : sQi[8 * q + 0];
+        const T* xa = d.pop + size_t(ia) * d.ldp;
+        const T* xb = d.pop + size_t(sQi[8 * q + 1]) * d.ldp;
+        const T* xc = (ttpb && ic >= P) ? d.archive + size_t(ic - P) * d.ldt : d.pop + size_t(ic) * d.ldp;
+        int jj[4];
+        T gi[4], ga[4], gb[4], gc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t b = 2 * b2 + (u >> 1);
+          const int64_t j64 = 2 * (blk0 + b) + (u & 1) - s0;
+          const bool valid = b < nblk && j64 >= 0 && j64 < D;
+          jj[u] = valid ? int(j64) : -1;
+          const int j = valid ? int(j64) : 0;
+          gi[u] = ldcg(xi + j);
+          ga[u] = ldcg(xa + j);
+          gb[u] = ldcg(xb + j);
+          gc[u] = ldcg(xc + j);
+        }
         const T Fi = sQf[2 * q];
         const double cr = double(sQf[2 * q + 1]);
         const int jr = sQi[8 * q + 3];
-        const T* xi = sR + q * 4 * D;
-        const T* xa = xi + D;
-        const T* xb = xa + D;
-        const T* xc = xb + D;
-        uint64_t w0, w1;
-        philox_pair(d.src.key, (uint64_t(gen) << 32) | uint32_t(i), uint64_t(blk0 + b), w0, w1);
+        uint64_t w[4];
+        const uint64_t ctr = (uint64_t(gen) << 32) | uint32_t(i);
+        philox_pair(d.src.key, ctr, uint64_t(blk0 + 2 * b2), w[0], w[1]);
+        philox_pair(d.src.key, ctr, uint64_t(blk0 + 2 * b2 + 1), w[2], w[3]);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int64_t j64 = 2 * (blk0 + b) + h - s0;
-          if (j64 < 0 || j64 >= D) continue;
-          const int j = int(j64);
-          const T xij = xi[j];
+        for (int u = 0; u < 4; ++u) {
+          const int j = jj[u];
+          if (j < 0) continue;
+          const T xij = gi[u];
           T v;
-          if (u01_of(h ? w1 : w0) < cr || j == jr)
-            v = donor_gene<T>(d.cfg.mutation, xij, xa[j], xb[j], xc[j], Fi);
+          if (u01_of(w[u]) < cr || j == jr)
+            v = donor_gene<T>(d.cfg.mutation, xij, ga[u], gb[u], gc[u], Fi);
           else
             v = xij;
           if (d.cfg.repair == EVB_REP_CLIP) {
@@ -1738,6 +1851,7 @@ __global__ void __launch_bounds__(kRunThreads, 1) de_run_kernel(const de_run_arg
     mark(2);
     // ---- D: evaluation, eval_small_kernel's order ----
     mark(8);
+    if (adapt && g + 1 < a.G) speculate(gen + 1u);  // warps with no (or the fewest) dot products
     {  // thread = (row r, a group of up to QG owned individuals): M^T[k][r] is loaded once per k for
        // all of them, s[q][k .. k+1] are 16-byte broadcasts; every chain keeps the reference's
        // sequential k order (separate mul and add)
@@ -1797,7 +1911,32 @@ __global__ void __launch_bounds__(kRunThreads, 1) de_run_kernel(const de_run_arg
       __syncthreads();
     }
     mark(10);
-    if (tid < nq) {
+    // base values: one thread per owned individual runs the reference's sequential sums; Ackley's
+    // two sums (squares, cosines) are independent chains and take two adjacent lanes.
+    if (a.kind == EVB_ACKLEY && 2 * nq <= 32) {
+      if (warp == 0) {
+        const int q = min(lane >> 1, max(nq - 1, 0)), role = lane & 1;
+        const T* src = (role ? sS : sZ) + q * D;
+        T acc = T(0);
+        int j = 0;
+        for (; j + 8 <= D; j += 8) {  // loads and squares ahead of the sequential adds
+          T v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = src[j + u];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = role ? v[u] : fop<T>::mul(v[u], v[u]);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc = fop<T>::add(acc, v[u]);
+        }
+        for (; j < D; ++j) acc = fop<T>::add(acc, role ? src[j] : fop<T>::mul(src[j], src[j]));
+        const T other = __shfl_xor_sync(0xffffffffu, acc, 1);
+        if (!role && (lane >> 1) < nq) {
+          const T v = fop<T>::add(ackley_final<T>(acc, other, D), T(a.bias));
+          sTf[q] = v;
+          d.trial_fit[i0 + q] = v;
+        }
+      }
+    } else if (tid < nq) {
       const T* zrow = sZ + tid * D;
       const T* pe = sS + tid * D;
       auto z = [&](int qq) { return zrow[qq]; };
@@ -1808,161 +1947,165 @@ __global__ void __launch_bounds__(kRunThreads, 1) de_run_kernel(const de_run_arg
     }
     __syncthreads();
     mark(3);
-    // ---- E: selection flags, counts to every CTA ----
-    int wq = 0, sq = 0;  // warp 0: lane q's flags
-    unsigned wmask = 0, smask = 0;
-    if (warp == 0) {
-      if (lane < nq) {
-        const T ft = sTf[lane], fp = sFit[i0 + lane];
-        wq = (ft <= fp) ? 1 : 0;
-        sq = (wq && fop<T>::sub(fp, ft) > T(0)) ? 1 : 0;
-      }
-      wmask = __ballot_sync(0xffffffffu, wq);
-      smask = __ballot_sync(0xffffffffu, sq);
-      if (lane < NC) {
-        int* dst = cl.map_shared_rank(sCnt, lane);
-        dst[2 * c] = __popc(wmask);
-        dst[2 * c + 1] = __popc(smask);
-      }
+    // ---- E: trial fitness, F, CR of the owned individuals into every CTA's copy (DSMEM) ----
+    for (int e = tid; e < nq * NC; e += nthr) {
+      const int q = e / NC, dst = e - q * NC;
+      T* all = cl.map_shared_rank(sAll, dst);
+      all[i0 + q] = sTf[q];
+      all[P + i0 + q] = sQf[2 * q];
+      all[2 * P + i0 + q] = sQf[2 * q + 1];
     }
-    cl.sync();
+    // cluster barrier split into arrive / wait: the archive sub-stream's first victim words
+    // (needed once the archive is full: de/strategy.hpp:33-36) are computed while the other
+    // CTAs' values arrive
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    {
+      const int room0 = d.archive_cap - arch_size;
+      if (d.archive_cap > 0 && room0 < P && d.src.mode == RNG_PHILOX)
+        for (int t = tid; t < min(P - max(room0, 0), kVict); t += nthr)
+          sVict[t] = uint_of(philox_word(d.src.key, (uint64_t(gen) << 32) | kSubArchive, uint64_t(t)), d.archive_cap);
+    }
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    __syncthreads();
     mark(4);
-    // ---- F: indices, archive slots, owners, success records ----
-    if (warp == 0) {
-      int pw = 0, ps = 0, tw = 0, ts = 0;
-      for (int k = 0; k < NC; ++k) {
-        const int a0 = sCnt[2 * k], a1 = sCnt[2 * k + 1];
-        if (k < c) {
-          pw += a0;
-          ps += a1;
-        }
-        tw += a0;
-        ts += a1;
-      }
-      const int size0 = arch_size, room = d.archive_cap - size0;
-      if (lane < nq) {
-        const int i = i0 + lane;
-        const int q = pw + __popc(wmask & ((1u << lane) - 1u));
-        const int k = ps + __popc(smask & ((1u << lane) - 1u));
-        d.win[i] = wq ? q + 1 : 0;
-        int sl = -1;
-        if (wq && d.archive_cap > 0) {
-          if (q < room) {
-            sl = size0 + q;
-          } else {
-            const uint64_t ctr_hi = (uint64_t(gen) << 32) | kSubArchive;
-            sl = uint_of(word_at(d.src, ctr_hi, int64_t(q - room), d.overflow), d.archive_cap);
-          }
-          atomicMax(d.owner64 + sl, (static_cast<unsigned long long>(tag) << 32) | unsigned(q));
-        }
-        d.arch_slot[i] = sl;
-        if (sq) {
-          d.succ[k] = i;
-          a.srec[k] = double(fop<T>::sub(sFit[i], sTf[lane]));
-          a.srec[P + k] = double(sQf[2 * lane]);
-          a.srec[2 * P + k] = double(sQf[2 * lane + 1]);
-        }
-      }
-      if (c == 0 && lane == 0) {
-        s_misc[1] = tw;
-        s_misc[2] = ts;
-      }
+    // ---- F: every CTA resolves the whole selection in its own shared memory ----
+    // thread = individual: win / success flags (de/engine.hpp:27-47), push and success indices by
+    // index-order prefix sums, archive slots (de/strategy.hpp:29-37: free slots first, then the
+    // archive sub-stream's victim words), the last push into a slot wins it (shared atomicMax),
+    // success records (gain, F, CR) in success order.  Same values in every CTA, no exchange.
+    const int size0 = arch_size, room = d.archive_cap - size0;
+    bool wq = false, sq = false;
+    T ft = T(0), fp = T(0);
+    if (tid < P) {
+      ft = sAll[tid];
+      fp = sFit[tid];
+      wq = ft <= fp;
+      sq = wq && fop<T>::sub(fp, ft) > T(0);
     }
-    cl.sync();
+    for (int t = tid; t < d.archive_cap; t += nthr) sOwner[t] = -1;
+    const unsigned wmask = __ballot_sync(0xffffffffu, wq), smask = __ballot_sync(0xffffffffu, sq);
+    if (lane == 0) {
+      sWC[2 * warp] = __popc(wmask);
+      sWC[2 * warp + 1] = __popc(smask);
+    }
+    __syncthreads();
+    int pw = 0, ps = 0, tw = 0, ts = 0;
+    for (int k = 0; k < (nthr >> 5); ++k) {
+      const int a0 = sWC[2 * k], a1 = sWC[2 * k + 1];
+      if (k < warp) {
+        pw += a0;
+        ps += a1;
+      }
+      tw += a0;
+      ts += a1;
+    }
+    const int qidx = pw + __popc(wmask & ((1u << lane) - 1u));
+    const int kidx = ps + __popc(smask & ((1u << lane) - 1u));
+    int sl = -1;
+    if (wq && d.archive_cap > 0) {
+      if (qidx < room) {
+        sl = size0 + qidx;
+      } else {
+        const int n = qidx - max(room, 0);
+        const uint64_t ctr_hi = (uint64_t(gen) << 32) | kSubArchive;
+        sl = n < kVict ? sVict[n] : uint_of(word_at(d.src, ctr_hi, int64_t(n), d.overflow), d.archive_cap);
+      }
+      atomicMax(&sOwner[sl], qidx);
+    }
+    if (sq) {
+      sG[kidx] = double(fop<T>::sub(fp, ft));
+      sG[P + kidx] = double(sAll[P + tid]);
+      sG[2 * P + kidx] = double(sAll[2 * P + tid]);
+    }
+    if (tid >= i0 && tid < i1) sWin[2 * (tid - i0)] = wq ? 1 : 0;
+    __syncthreads();
     mark(5);
-    // ---- G: replacements (owners), archive / adapter bookkeeping (CTA 0) ----
-    for (int q = warp; q < nq; q += nthr / 32) {
-      const int i = i0 + q;
-      const int wv = d.win[i];
-      if (!wv) continue;
-      int sl = d.arch_slot[i];
-      if (sl >= 0 && __ldcg(d.owner64 + sl) != ((static_cast<unsigned long long>(tag) << 32) | unsigned(wv - 1))) {
-        sl = -1;  // overwritten by a later push (members_[victim] = genome, in push order)
-        if (lane == 0) d.arch_slot[i] = -1;
+    if (wq) {  // (tid < P)
+      sFit[tid] = ft;
+      if (tid >= i0 && tid < i1) {
+        // overwritten by a later push: members_[victim] = genome, in push order
+        sWin[2 * (tid - i0) + 1] = (sl >= 0 && sOwner[sl] == qidx) ? sl : -1;
+        d.fit[tid] = ft;
       }
-      T* x = d.pop + size_t(i) * d.ldp;
-      T* arow = sl >= 0 ? d.archive + size_t(sl) * d.ldt : nullptr;
-      for (int j = lane; j < D; j += 32) {
-        const T old = ldcg(x + j);
-        if (arow) arow[j] = old;
-        x[j] = sT[q * D + j];
-      }
-      if (lane == 0) d.fit[i] = sTf[q];
-      if (lane < NC) *cl.map_shared_rank(sFit + i, lane) = sTf[q];  // every CTA's copy
     }
-    if (c == 0) {
-      const int n_push = s_misc[1], n_succ = s_misc[2];
-      if (tid < NC) *cl.map_shared_rank(&s_misc[0], tid) = min(d.archive_cap, arch_size + n_push);
-      if (tid == 0) {
-        const int size0 = arch_size, room = d.archive_cap - size0;
-        *d.arch_size = min(d.archive_cap, size0 + n_push);
-        *d.arch_words = d.archive_cap > 0 ? max(0, n_push - room) : 0;
-        d.n_push[0] = n_push;
-        d.n_push[1] = n_succ;
-      }
-      if (adapt && n_succ > 0) {
-        for (int k = tid; k < n_succ; k += nthr) {
-          sG[k] = __ldcg(a.srec + k);
-          sG[P + k] = __ldcg(a.srec + P + k);
-          sG[2 * P + k] = __ldcg(a.srec + 2 * P + k);
+    if (tid == 0) s_misc[0] = min(d.archive_cap, size0 + tw);  // the next generation's archive size
+    __syncthreads();
+    // ---- G: the owned winners' rows; the adapter memories (last warp, every CTA the same) ----
+    if (warp != dw || !adapt) {
+      const int nw = (nthr >> 5) - (adapt ? 1 : 0);
+      for (int q = warp; q < nq; q += nw) {
+        if (!sWin[2 * q]) continue;
+        const int i = i0 + q;
+        const int wsl = sWin[2 * q + 1];
+        T* x = d.pop + size_t(i) * d.ldp;
+        T* arow = wsl >= 0 ? d.archive + size_t(wsl) * d.ldt : nullptr;
+        for (int j = lane; j < D; j += 32) {
+          if (arow) arow[j] = ldcg(x + j);
+          x[j] = sT[q * D + j];
         }
-        __syncthreads();
-        const double* gv = sG;
-        const double* fv = sG + P;
-        const double* cv = sG + 2 * P;
-        if (d.cfg.parameter == EVB_PAR_SHADE) {  // de/parameter.hpp:166-184 (adapter_update's roundings)
-          double gain_sum = 0.0;
-          if (tid == 0)
-            for (int k = 0; k < n_succ; ++k) gain_sum = __dadd_rn(gain_sum, gv[k]);
-          __shared__ double s_gsum;
-          if (tid == 0) s_gsum = gain_sum;
-          __syncthreads();
-          gain_sum = s_gsum;
-          // per-success products by their own threads, in place (w = gain / sum; (w f) f, w f, w cr)
-          double* wnum = sG;
-          for (int k = tid; k < n_succ; k += nthr) {
-            const double w = __ddiv_rn(gv[k], gain_sum);
-            const double wf = __dmul_rn(w, fv[k]);
-            wnum[k] = __dmul_rn(wf, fv[k]);
-            wnum[P + k] = wf;
-            wnum[2 * P + k] = __dmul_rn(w, cv[k]);
-          }
-          __syncthreads();
-          if (tid == 0) {
-            double f_num = 0.0, f_den = 0.0, cr_acc = 0.0;
-            for (int k = 0; k < n_succ; ++k) {
-              f_num = __dadd_rn(f_num, wnum[k]);
-              f_den = __dadd_rn(f_den, wnum[P + k]);
-              cr_acc = __dadd_rn(cr_acc, wnum[2 * P + k]);
-            }
-            const int kw = *d.write_index;
-            const T nf = T(__ddiv_rn(f_num, f_den)), nc = T(cr_acc);
+      }
+      if (c == 0 && tid == 0) {
+        *d.arch_size = min(d.archive_cap, size0 + tw);
+        *d.arch_words = d.archive_cap > 0 ? max(0, tw - room) : 0;
+        d.n_push[0] = tw;
+        d.n_push[1] = ts;
+      }
+    } else if (ts > 0) {
+      // de/parameter.hpp:166-184 (SHADE, adapter_update's roundings) / :107-120 (JADE): the
+      // reference's sequential sums, one chain per lane where the chains are independent
+      const int n_succ = ts;
+      const double* gv = sG;
+      const double* fv = sG + P;
+      const double* cv = sG + 2 * P;
+      if (shade) {
+        double gain_sum = 0.0;
+        if (lane == 0)
+          for (int k = 0; k < n_succ; ++k) gain_sum = __dadd_rn(gain_sum, gv[k]);
+        gain_sum = __shfl_sync(0xffffffffu, gain_sum, 0);
+        // per-success products by their own lanes, in place (w = gain / sum; (w f) f, w f, w cr)
+        double* wnum = sG;
+        for (int k = lane; k < n_succ; k += 32) {
+          const double w = __ddiv_rn(gv[k], gain_sum);
+          const double wf = __dmul_rn(w, fv[k]);
+          wnum[k] = __dmul_rn(wf, fv[k]);
+          wnum[P + k] = wf;
+          wnum[2 * P + k] = __dmul_rn(w, cv[k]);
+        }
+        __syncwarp();
+        double acc = 0.0;  // lane 0: f_num, lane 1: f_den, lane 2: cr
+        if (lane < 3)
+          for (int k = 0; k < n_succ; ++k) acc = __dadd_rn(acc, wnum[lane * P + k]);
+        const double f_num = __shfl_sync(0xffffffffu, acc, 0), f_den = __shfl_sync(0xffffffffu, acc, 1);
+        const double cr_acc = __shfl_sync(0xffffffffu, acc, 2);
+        if (lane == 0) {
+          const int kw = s_misc[3];
+          const T nf = T(__ddiv_rn(f_num, f_den)), nc = T(cr_acc);
+          sMemF[kw] = nf;
+          sMemC[kw] = nc;
+          s_misc[3] = (kw + 1) % d.cfg.memory_size;
+          if (c == 0) {
             d.mem_f[kw] = nf;
             d.mem_cr[kw] = nc;
             *d.write_index = (kw + 1) % d.cfg.memory_size;
-            for (int k = 0; k < NC; ++k) {  // every CTA's copy
-              *cl.map_shared_rank(sMemF + kw, k) = nf;
-              *cl.map_shared_rank(sMemC + kw, k) = nc;
-            }
           }
-        } else if (tid == 0) {  // JADE, de/parameter.hpp:107-120
-          double num = 0.0, den = 0.0, crm = 0.0;
-          for (int k = 0; k < n_succ; ++k) {
-            num = __dadd_rn(num, __dmul_rn(fv[k], fv[k]));
-            den = __dadd_rn(den, fv[k]);
-            crm = __dadd_rn(crm, cv[k]);
-          }
-          const double lehmer = __ddiv_rn(num, den);
-          crm = __ddiv_rn(crm, double(n_succ));
-          const double cc = double(T(d.cfg.jade_c));
-          const T nf = T(__dadd_rn(__dmul_rn(__dsub_rn(1.0, cc), double(sMemF[0])), __dmul_rn(cc, lehmer)));
-          const T nc = T(__dadd_rn(__dmul_rn(__dsub_rn(1.0, cc), double(sMemC[0])), __dmul_rn(cc, crm)));
+        }
+      } else if (lane == 0) {
+        double num = 0.0, den = 0.0, crm = 0.0;
+        for (int k = 0; k < n_succ; ++k) {
+          num = __dadd_rn(num, __dmul_rn(fv[k], fv[k]));
+          den = __dadd_rn(den, fv[k]);
+          crm = __dadd_rn(crm, cv[k]);
+        }
+        const double lehmer = __ddiv_rn(num, den);
+        crm = __ddiv_rn(crm, double(n_succ));
+        const double cc = double(T(d.cfg.jade_c));
+        const T nf = T(__dadd_rn(__dmul_rn(__dsub_rn(1.0, cc), double(sMemF[0])), __dmul_rn(cc, lehmer)));
+        const T nc = T(__dadd_rn(__dmul_rn(__dsub_rn(1.0, cc), double(sMemC[0])), __dmul_rn(cc, crm)));
+        sMemF[0] = nf;
+        sMemC[0] = nc;
+        if (c == 0) {
           d.mem_f[0] = nf;
           d.mem_cr[0] = nc;
-          for (int k = 0; k < NC; ++k) {  // every CTA's copy
-            *cl.map_shared_rank(sMemF, k) = nf;
-            *cl.map_shared_rank(sMemC, k) = nc;
-          }
         }
       }
     }
@@ -2382,8 +2525,9 @@ bool run_generations_t(evb_de_s* e, const device_problem* prob, void* pop, int64
   auto smem_for = [&](int q, int nc) {
     size_t np2 = 1;
     while (np2 < size_t(P)) np2 <<= 1;
-    return mt_bytes + (7 * size_t(q) * D + P + 2 * H + 3 * q + 1) * sizeof(T) + 16 + 4 * size_t(P) * 8 +
-           (np2 + P + 2 * nc + 8 * q) * sizeof(int) + 8 + 2 * 8 + 64;
+    (void)nc;
+    return mt_bytes + (3 * size_t(q) * D + 4 * size_t(P) + 2 * H + 3 * q + 1) * sizeof(T) + 16 + 4 * size_t(P) * 8 +
+           (np2 + P + size_t(std::max(0, e->archive_cap)) + 64 + 10 * q) * sizeof(int) + 8 + 2 * 8 + 64;
   };
   if (smem_for(Q, NC) > 200 * 1024) return false;
   de_run_args<T> a{};
