@@ -106,7 +106,7 @@ void fill_weights(device_problem& p) {
 
 void free_problem(device_problem& p) {
   void* ptrs[] = {p.shift, p.rotation, p.ell_w, p.hyb_w, p.perm, p.sub_kinds, p.chunk_sizes, p.comp_kinds,
-                  p.comp_shift, p.comp_rot, p.comp_sigma, p.comp_lambda, p.comp_bias, p.rot_hi, p.rot_lo, p.rot_t};
+                  p.comp_shift, p.comp_rot, p.comp_sigma, p.comp_lambda, p.comp_bias, p.rot_hi, p.rot_lo, p.rot_hi16, p.rot_lo16, p.rot_t};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -123,7 +123,10 @@ bool make_tma_2d(CUtensorMap* map, const void* base, int dtype, uint64_t inner_e
   const cuuint64_t strides[1] = {row_stride_bytes};
   const cuuint32_t box[2] = {box_inner, box_outer};
   const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = enc(map, dtype == EVB_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+  const CUtensorMapDataType dt = dtype == EVB_F64   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
+                                 : dtype == kTmaF16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                    : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  const CUresult r = enc(map, dt, 2,
                          const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

@@ -1240,11 +1240,19 @@ __global__ void __launch_bounds__(umma_cfg<BN, FUSE>::THREADS, 1)
 // received half to its own (z = z_0 + z_1: fp add is commutative, the same in both CTAs) and runs
 // the usual epilogue on its 64 columns (terms, per-row channel sums, column-block partials,
 // last-CTA finalisation).  Deterministic, no float atomics.
-template <int BN, bool ATMEM>
+// F16 (the default, "3xFP16"): the same split with fp16 heads and remainders (11 significant bits
+// each, like TF32; the rotation scaled by 2^8 so its remainders stay normal) and kind::f16 MMAs,
+// K = 16 per instruction at the tf32 instruction's cost: half the MMA time and half the rotation
+// bytes.  A K slice is then 64 elements: X lands as two 32-float boxes (32 KB, the whole A stage);
+// thread (row, box) forms its row's [S_hi k 0..31 | S_lo k 0..31] in place (it only overwrites what
+// it has read), so box b serves K steps 2b, 2b + 1 with hi at byte offsets 0 / 32 and lo at 64 / 96
+// of the 128-byte swizzle row.
+template <int BN, bool ATMEM, bool F16 = false>
 struct umma_sk_cfg {
+  static_assert(!(ATMEM && F16), "the fp16 split keeps its operands in shared memory");
   static constexpr int BM = 128;
-  static constexpr int KB = 32;                   // floats per K slice (one 128-byte swizzle row)
-  static constexpr int X_BYTES = BM * 128;        // one X slice (TMA)
+  static constexpr int KB = F16 ? 64 : 32;        // elements per K slice
+  static constexpr int X_BYTES = BM * KB * 4;     // one X slice (TMA; F16: two 32-float boxes)
   static constexpr int B_BYTES = 2 * BN * 128;    // M_hi + M_lo of one slice (TMA, multicast pair)
   // ATMEM: S_hi / S_lo go to TMEM (the MMA's A operand from TMEM: shared memory then feeds only B,
   //        which a 128 x 128 x 8 tf32 MMA otherwise reads at the full 128 B/clk with A);
@@ -1272,11 +1280,11 @@ struct umma_sk_cfg {
   static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
-template <int BN, bool ATMEM>
-__global__ void __launch_bounds__(umma_sk_cfg<BN, ATMEM>::THREADS, 1)
+template <int BN, bool ATMEM, bool F16 = false>
+__global__ void __launch_bounds__(umma_sk_cfg<BN, ATMEM, F16>::THREADS, 1)
     eval_f32_umma_sk_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmMhi,
                             const __grid_constant__ CUtensorMap tmMlo, const fused_params<float> p) {
-  using C = umma_sk_cfg<BN, ATMEM>;
+  using C = umma_sk_cfg<BN, ATMEM, F16>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   uint64_t* xfull = reinterpret_cast<uint64_t*>(smem + C::RING_BYTES);  // X + shift slice landed
@@ -1359,6 +1367,7 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN, ATMEM>::THREADS, 1)
         uint8_t* dst = ATMEM ? smem + C::X_OFF + s * C::X_BYTES : smem + C::A_OFF + s * C::A_BYTES;
         ptx::mbar_arrive_expect_tx(&xfull[s], C::X_BYTES + C::KB * 4);
         ptx::tma_load_2d(dst, &tmX, &xfull[s], (kb0 + kb) * C::KB, m0);
+        if constexpr (F16) ptx::tma_load_2d(dst + C::BM * 128, &tmX, &xfull[s], (kb0 + kb) * C::KB + 32, m0);
         ptx::bulk_load(smem + C::O_OFF + s * C::KB * 4, p.shift + size_t(kb0 + kb) * C::KB, C::KB * 4, &xfull[s]);
       }
     }
@@ -1396,6 +1405,19 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN, ATMEM>::THREADS, 1)
             umma::mma_tf32_ts(tmem, ta_hi + col, umma::smem_desc(sb_hi + off), idesc, acc0);
             umma::mma_tf32_ts(tcorr, ta_lo + col, umma::smem_desc(sb_hi + off), idesc, acc0);
             umma::mma_tf32_ts(tcorr, ta_hi + col, umma::smem_desc(sb_lo + off), idesc, 1u);
+          }
+        } else if constexpr (F16) {
+          constexpr uint32_t idesc16 = umma::idesc_f16(C::BM, BN);
+          const uint32_t sa0 = base + C::A_OFF + sa * C::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < C::KB / 16; ++k) {
+            if (p.dbg_skip & 2) break;
+            const uint32_t a_hi = sa0 + (k >> 1) * (C::BM * 128) + (k & 1) * 32, a_lo = a_hi + 64;
+            const uint32_t off = k * 32;
+            const uint32_t acc0 = (kb | k) ? 1u : 0u;
+            umma::mma_f16(tmem, umma::smem_desc(a_hi), umma::smem_desc(sb_hi + off), idesc16, acc0);
+            umma::mma_f16(tcorr, umma::smem_desc(a_lo), umma::smem_desc(sb_hi + off), idesc16, acc0);
+            umma::mma_f16(tcorr, umma::smem_desc(a_hi), umma::smem_desc(sb_lo + off), idesc16, 1u);
           }
         } else {
           const uint32_t sa_hi = base + C::A_OFF + sa * C::A_BYTES, sa_lo = sa_hi + C::A_BYTES / 2;
@@ -1468,6 +1490,45 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN, ATMEM>::THREADS, 1)
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&afull[sa]);
       }
+    } else if constexpr (F16) {
+      // thread = (row rr, box b): the row's 32 floats of the box (logical 16-byte chunk f at physical
+      // f ^ (rr & 7): the 8 rows of a quarter warp hit 8 distinct chunks) into registers, then
+      // [S_hi | S_lo] as 4 + 4 chunks of 8 halves back into the same 128 bytes
+      const int b = etid >> 7, rr = etid & 127;
+      for (int kb = 0; kb < KT; ++kb) {
+        const int sa = kb % C::NA;
+        ptx::mbar_wait(&xfull[sa], (kb / C::NA) & 1);
+        uint4* rowp = reinterpret_cast<uint4*>(smem + C::A_OFF + sa * C::A_BYTES + b * (C::BM * 128) + rr * 128);
+        const float4* osl = reinterpret_cast<const float4*>(smem + C::O_OFF + sa * C::KB * 4) + 8 * b;
+        if (!(p.dbg_skip & 1)) {
+          float4 xv[8];
+#pragma unroll
+          for (int f = 0; f < 8; ++f) xv[f] = *reinterpret_cast<const float4*>(rowp + (f ^ (rr & 7)));
+          uint32_t hw[16], lw[16];  // 2 halves per word
+#pragma unroll
+          for (int f = 0; f < 8; ++f) {
+            const float4 o = osl[f];
+            const float s0 = __fsub_rn(xv[f].x, o.x), s1 = __fsub_rn(xv[f].y, o.y);
+            const float s2 = __fsub_rn(xv[f].z, o.z), s3 = __fsub_rn(xv[f].w, o.w);
+            const __half2 h01 = __floats2half2_rn(s0, s1), h23 = __floats2half2_rn(s2, s3);
+            const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+            const __half2 l01 = __floats2half2_rn(__fsub_rn(s0, f01.x), __fsub_rn(s1, f01.y));
+            const __half2 l23 = __floats2half2_rn(__fsub_rn(s2, f23.x), __fsub_rn(s3, f23.y));
+            hw[2 * f] = *reinterpret_cast<const uint32_t*>(&h01);
+            hw[2 * f + 1] = *reinterpret_cast<const uint32_t*>(&h23);
+            lw[2 * f] = *reinterpret_cast<const uint32_t*>(&l01);
+            lw[2 * f + 1] = *reinterpret_cast<const uint32_t*>(&l23);
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            rowp[j ^ (rr & 7)] = make_uint4(hw[4 * j], hw[4 * j + 1], hw[4 * j + 2], hw[4 * j + 3]);
+            rowp[(4 + j) ^ (rr & 7)] = make_uint4(lw[4 * j], lw[4 * j + 1], lw[4 * j + 2], lw[4 * j + 3]);
+          }
+          ptx::fence_proxy_async();
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&afull[sa]);
+      }
     } else {
       // S = X - o, S_hi = rna_tf32(S) over X, S_lo = rna_tf32(S - S_hi) into the stage's lo half
       // (same SWIZZLE_128B positions: chunk q of row q / 8 holds logical chunk (q & 7) ^ (row & 7))
@@ -1515,8 +1576,13 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN, ATMEM>::THREADS, 1)
       umma::tmem_ld16_raw(tbase + col, a);
       umma::tmem_ld16_raw(tbase + BN + col, b);
       umma::tmem_wait_ld();
+      // (F16: the rotation was scaled by 2^8 for the split; the power of two comes off exactly)
+      constexpr float zs = F16 ? 1.f / kF16Scale : 1.f;
 #pragma unroll
-      for (int q = 0; q < 16; ++q) v[q] = __fadd_rn(__uint_as_float(a[q]), __uint_as_float(b[q]));
+      for (int q = 0; q < 16; ++q) {
+        const float zq = __fadd_rn(__uint_as_float(a[q]), __uint_as_float(b[q]));
+        v[q] = F16 ? __fmul_rn(zq, zs) : zq;
+      }
     };
     float* recv = reinterpret_cast<float*>(smem);  // [BM][BN/2] in the drained rings (nsk == 2)
     auto rchunk = [&](int rr, int ch16) { return rr * (BN / 2) + 4 * ((ch16 & ~7) | ((ch16 & 7) ^ (rr & 7))); };
@@ -1901,11 +1967,11 @@ void launch_f32_umma(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUt
   count_launch();
 }
 
-template <int BN, bool ATMEM>
+template <int BN, bool ATMEM, bool F16 = false>
 void launch_f32_umma_sk(const CUtensorMap& tx, const CUtensorMap& b_hi, const CUtensorMap& b_lo,
                         const fused_params<float>& fp, int splitk, cudaStream_t st) {
-  using C = umma_sk_cfg<BN, ATMEM>;
-  auto kern = eval_f32_umma_sk_kernel<BN, ATMEM>;
+  using C = umma_sk_cfg<BN, ATMEM, F16>;
+  auto kern = eval_f32_umma_sk_kernel<BN, ATMEM, F16>;
   static bool attr = false;
   if (!attr) {
     EVB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -2029,9 +2095,15 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
       const int64_t mel = int64_t(D) * ldm;
       void* rhi = nullptr;
       void* rlo = nullptr;
-      const bool split_cached = own_rot && pr->rot_hi;
+      // EVB_F32_MMA=tf32 keeps the 3xTF32 MMAs; the default is the fp16 split (3xFP16, kind::f16)
+      static const bool f16 = !(std::getenv("EVB_F32_MMA") && std::string(std::getenv("EVB_F32_MMA")) == "tf32");
+      static const bool atmem_env = std::getenv("EVB_UMMA_ATMEM") && std::atoi(std::getenv("EVB_UMMA_ATMEM")) == 1;
+      const bool use16 = f16 && !atmem_env && UBN == 0;
+      const bool split_cached = own_rot && (use16 ? pr->rot_hi16 != nullptr : pr->rot_hi != nullptr);
       fp.b_early = split_cached ? 1 : 0;
-      if (split_cached) {
+      if (use16) {
+        // (the fp16 split is built below)
+      } else if (split_cached) {
         rhi = pr->rot_hi;
         rlo = pr->rot_lo;
       } else {
@@ -2059,10 +2131,32 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
         static const char* sk_env = std::getenv("EVB_UMMA_SPLITK");
         int splitk = (n_tiles * 2 <= sm_count() && (D + 31) / 32 >= 16) ? 2 : 1;
         if (sk_env) splitk = std::max(1, std::min(2, std::atoi(sk_env)));
-        ok = make_tma_2d(&ta_hi, X, EVB_F32, uint64_t(D), uint64_t(P), uint64_t(ldx) * 4, 32, 128) &&
-             make_tma_2d(&tb_hi, rhi, EVB_F32, uint64_t(ldm), uint64_t(D), uint64_t(ldm) * 4, 32, SBN / 2) &&
-             make_tma_2d(&tb_lo, rlo, EVB_F32, uint64_t(ldm), uint64_t(D), uint64_t(ldm) * 4, 32, SBN / 2);
-        if (!ok) throw runtime_error("gemm_eval: cannot encode the TMA descriptors of the tf32 split");
+        void* r16h = nullptr;
+        void* r16l = nullptr;
+        if (use16) {
+          if (own_rot && pr->rot_hi16) {
+            r16h = pr->rot_hi16;
+            r16l = pr->rot_lo16;
+          } else {
+            EVB_CUDA(cudaMalloc(&r16h, mel * sizeof(__half)));
+            EVB_CUDA(cudaMalloc(&r16l, mel * sizeof(__half)));
+            split_f16_kernel<<<int(std::min<int64_t>(2048, (mel + 255) / 256)), 256, 0, rq.stream>>>(
+                static_cast<const float*>(rotation), mel, static_cast<__half*>(r16h), static_cast<__half*>(r16l));
+            count_launch();
+            if (own_rot) {
+              pr->rot_hi16 = r16h;
+              pr->rot_lo16 = r16l;
+            }
+          }
+        }
+        ok = make_tma_2d(&ta_hi, X, EVB_F32, uint64_t(D), uint64_t(P), uint64_t(ldx) * 4, 32, 128);
+        if (use16)
+          ok = ok && make_tma_2d(&tb_hi, r16h, kTmaF16, uint64_t(ldm), uint64_t(D), uint64_t(ldm) * 2, 64, SBN / 2) &&
+               make_tma_2d(&tb_lo, r16l, kTmaF16, uint64_t(ldm), uint64_t(D), uint64_t(ldm) * 2, 64, SBN / 2);
+        else
+          ok = ok && make_tma_2d(&tb_hi, rhi, EVB_F32, uint64_t(ldm), uint64_t(D), uint64_t(ldm) * 4, 32, SBN / 2) &&
+               make_tma_2d(&tb_lo, rlo, EVB_F32, uint64_t(ldm), uint64_t(D), uint64_t(ldm) * 4, 32, SBN / 2);
+        if (!ok) throw runtime_error("gemm_eval: cannot encode the TMA descriptors of the tensor-core split");
         fp.n_ntiles = n_nt * splitk;  // column blocks of BN / splitk, one partial each
         if (!zstore) {
           ensure_buffer(&sc->partial, &sc->partial_bytes, size_t(fp.n_ch) * fp.n_ntiles * P * sizeof(T), rq.stream);
@@ -2091,7 +2185,8 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
           fused_params<float> f2 = fp;
           f2.dbg_ts = d;
           f2.dbg_skip = std::getenv("EVB_K2_SKIP") ? std::atoi(std::getenv("EVB_K2_SKIP")) : 0;
-          if (atmem) launch_f32_umma_sk<SBN, true>(ta_hi, tb_hi, tb_lo, f2, splitk, rq.stream);
+          if (use16) launch_f32_umma_sk<SBN, false, true>(ta_hi, tb_hi, tb_lo, f2, splitk, rq.stream);
+          else if (atmem) launch_f32_umma_sk<SBN, true>(ta_hi, tb_hi, tb_lo, f2, splitk, rq.stream);
           else launch_f32_umma_sk<SBN, false>(ta_hi, tb_hi, tb_lo, f2, splitk, rq.stream);
           EVB_CUDA(cudaStreamSynchronize(rq.stream));
           std::vector<unsigned long long> h(size_t(nct) * 8);
@@ -2105,13 +2200,16 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
             std::fclose(f);
           }
         } else {
-          if (atmem) launch_f32_umma_sk<SBN, true>(ta_hi, tb_hi, tb_lo, fp, splitk, rq.stream);
+          if (use16) launch_f32_umma_sk<SBN, false, true>(ta_hi, tb_hi, tb_lo, fp, splitk, rq.stream);
+          else if (atmem) launch_f32_umma_sk<SBN, true>(ta_hi, tb_hi, tb_lo, fp, splitk, rq.stream);
           else launch_f32_umma_sk<SBN, false>(ta_hi, tb_hi, tb_lo, fp, splitk, rq.stream);
         }
         if (!own_rot) {
           EVB_CUDA(cudaStreamSynchronize(rq.stream));
-          cudaFree(rhi);
-          cudaFree(rlo);
+          if (rhi) cudaFree(rhi);
+          if (rlo) cudaFree(rlo);
+          if (r16h) cudaFree(r16h);
+          if (r16l) cudaFree(r16l);
         }
         return;
       }

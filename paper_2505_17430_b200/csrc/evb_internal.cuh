@@ -111,6 +111,8 @@ struct device_problem {
   // fp32 tensor-core path: TF32 head / remainder split of the rotation (made on first use)
   void* rot_hi = nullptr;
   void* rot_lo = nullptr;
+  void* rot_hi16 = nullptr;  // fp16 split of 2^8 * rotation (the 3xFP16 kernel), built on first use
+  void* rot_lo16 = nullptr;
 };
 
 }  // namespace evb
@@ -224,6 +226,7 @@ inline void ensure_buffer(void** ptr, size_t* cap, size_t need, cudaStream_t str
 }
 
 // TMA descriptor helpers (driver entry point fetched through the runtime; no -lcuda).
+constexpr int kTmaF16 = 100;  // make_tma_2d dtype: fp16 elements (beside EVB_F32 / EVB_F64)
 bool make_tma_2d(CUtensorMap* map, const void* base, int dtype, uint64_t inner_elems,
                  uint64_t outer_rows, uint64_t row_stride_bytes, uint32_t box_inner,
                  uint32_t box_outer);

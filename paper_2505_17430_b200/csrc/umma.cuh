@@ -22,6 +22,7 @@
 //           memory, N-tile partials + last-CTA finalisation (as K1).
 #pragma once
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "ptx.cuh"
@@ -56,6 +57,20 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
 // instruction descriptor, kind::tf32: D f32, A/B tf32, both K-major, N >> 3, M >> 4
 constexpr uint32_t idesc_tf32(int M, int N) {
   return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+}
+
+// instruction descriptor, kind::f16: D f32, A/B f16 (format 0), both K-major; K = 16 per instruction
+constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -170,6 +185,19 @@ __global__ void split_plain_kernel(const float* __restrict__ a, int64_t n, float
     const float h = __uint_as_float(umma::cvt_rna_tf32(x));
     hi[e] = h;
     lo[e] = __uint_as_float(umma::cvt_rna_tf32(__fsub_rn(x, h)));
+  }
+}
+// fp16 split of the rotation for the 3xFP16 kernel: a' = kF16Scale * a (a power of two: exact, and
+// it lifts the remainder of typical entries out of fp16's subnormal range), hi = fp16(a'),
+// lo = fp16(a' - hi): 22 significant bits, as the TF32 split
+constexpr float kF16Scale = 256.f;
+__global__ void split_f16_kernel(const float* __restrict__ a, int64_t n, __half* __restrict__ hi,
+                                 __half* __restrict__ lo) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+    const float x = __fmul_rn(a[e], kF16Scale);
+    const __half h = __float2half_rn(x);
+    hi[e] = h;
+    lo[e] = __float2half_rn(__fsub_rn(x, __half2float(h)));
   }
 }
 #endif  // EVB_UMMA_HELPERS_ONLY

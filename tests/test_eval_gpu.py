@@ -400,11 +400,13 @@ def test_gemm_path_extreme_inputs(dev, dim):
         assert rel_err(got[fin], ref[fin]) <= 1e-10, kind
 
 
+@pytest.mark.parametrize("variant", [{"EVB_UMMA_ATMEM": "1"}, {"EVB_F32_MMA": "tf32"}])
 @pytest.mark.parametrize("kind", [1, 5, 6])
-def test_f32_tensor_core_a_in_tmem_variant(kind):
-    """The split-K fp32 kernel with S_hi / S_lo as the MMA's A operand in TMEM (EVB_UMMA_ATMEM=1,
-    tcgen05.mma with [a-tmem]; the switch is read once per process, hence the subprocess) against
-    the restatement at config 1's size (1e-4 relative)."""
+def test_f32_tensor_core_variants(kind, variant):
+    """The split-K fp32 kernel's selectable variants against the restatement at config 1's size
+    (1e-4 relative): S_hi / S_lo as the MMA's A operand in TMEM (EVB_UMMA_ATMEM=1, tcgen05.mma with
+    [a-tmem], 3xTF32), and the 3xTF32 shared-memory kernel (EVB_F32_MMA=tf32; the default is the
+    fp16 split, 3xFP16).  The switches are read once per process, hence the subprocess."""
     import os
     import subprocess
     import sys
@@ -427,7 +429,7 @@ np.save(sys.argv[1], out.cpu().numpy())
     with tempfile.TemporaryDirectory() as td:
         f = str(Path(td) / "v.npy")
         root = Path(__file__).resolve().parents[1]
-        env = dict(os.environ, EVB_UMMA_ATMEM="1")
+        env = dict(os.environ, **variant)
         r = subprocess.run([sys.executable, "-c", code, f], cwd=str(root), capture_output=True, text=True, timeout=300,
                            env=env)
         assert r.returncode == 0, r.stderr[-2000:]
