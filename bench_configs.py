@@ -5,7 +5,7 @@ workload and thread count of every CPU figure are stated in its `sample`).  benc
 ``run_all()`` into its JSON line under ``configs``; run standalone it prints the same object.
 
   config0        DE rand/1/bin one generation, D=10, pop 100 (latency; graph / persistent / e2e)
-  config1_fp32   batched evaluation fp32, D=1000, pop 1024 (tcgen05 3xTF32)
+  config1_fp32   batched evaluation fp32, D=1000, pop 1024 (tcgen05 3xFP16)
   config2        SHADE (ttpb/1, archive, midpoint), D=100, pop 180, 1000 generations, Ackley
   config3        synchronous PSO gbest / ring, fp64 / fp32, D=1000, pop 1024, 500 iterations
   config4        64 DE runs x 2000 generations, D=50, pop 100, 3-component composition, one launch
@@ -261,8 +261,8 @@ def config1_fp32():
     step_ms = batch_ms * len(kinds)
     flop = 2.0 * D * D * P
     achieved = flop / (batch_ms * 1e-3) / 1e12
-    tf32 = _lib.probe_umma_tf32_tflops(K2_TILE_N)
-    tf32_256 = _lib.probe_umma_tf32_tflops(256)
+    tf32 = _lib.probe_umma_f16_tflops(K2_TILE_N)  # the kernel's MMAs are kind::f16 (3xFP16 split)
+    tf32_256 = _lib.probe_umma_f16_tflops(256)
     peak = tf32 / 3.0
     # CPU: the reference's float evaluate_batch (fast_cos) for the three objectives, all threads
     L = O.REF_FAST()
@@ -286,14 +286,15 @@ def config1_fp32():
     return {
         "metric": "objective evals/sec (D=1000, pop 1024, fp32)", "value": 3 * P / (step_ms * 1e-3),
         "unit": "evals/s", "ms_per_batch": batch_ms,
-        "how": "3 x evaluate_batch fp32 per step (eval_f32_umma_sk_kernel: tcgen05 kind::tf32 128x128 tiles, "
-               "3xTF32 split in-kernel, TMEM accumulators, K halves as a 2-CTA cluster exchanging z over DSMEM, "
+        "how": "3 x evaluate_batch fp32 per step (eval_f32_umma_sk_kernel: tcgen05 kind::f16 128x128 tiles, "
+               "3xFP16 split in-kernel (fp16 head + remainder of S = X - o and of 2^8 M: 22 significant bits), "
+               "TMEM accumulators, K halves as a 2-CTA cluster exchanging z over DSMEM, "
                "M pairs multicasting the rotation slices); CUDA events per launch; L2 flushed between steps",
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s (fp32-equivalent)",
                      "frac": achieved / peak, "traffic": dram_traffic(K2_KERNEL),
                      "kernel": K2_KERNEL,
-                     "peak_source": f"in-run tcgen05.mma kind::tf32 probe at N={K2_TILE_N}: {tf32:.1f} TFLOP/s, "
-                                    f"divided by 3 (3xTF32: three tensor-core products per fp32 product); "
+                     "peak_source": f"in-run tcgen05.mma kind::f16 probe at N={K2_TILE_N}: {tf32:.1f} TFLOP/s, "
+                                    f"divided by 3 (3xFP16: three tensor-core products per fp32 product); "
                                     f"at N=256 the probe reads {tf32_256:.1f}",
                      "algorithmic": f"2*D^2*P = {flop:.4g} flop per launch (x3 on the tensor core)",
                      "tensor_pipe_frac": 3 * achieved / tf32},
@@ -358,7 +359,7 @@ def config3():
     o, m = O.shift_rotation(13, D)
     hbm, _ = hbm_peak()
     peak64 = _lib.probe_peak_tflops(0)
-    tf32 = _lib.probe_umma_tf32_tflops(K2_TILE_N)
+    tf32 = _lib.probe_umma_f16_tflops(K2_TILE_N)  # fp32 evaluation: kind::f16 MMAs (3xFP16)
     res = {"metric": "iterations/s (500 iterations, D=1000, pop 1024)", "unit": "iterations/s", "variants": {}}
     for nd, dt, tdt in ((np.float64, evb.EVB_F64, torch.float64), (np.float32, evb.EVB_F32, torch.float32)):
         prob = evb.ProblemInstance.base(evb.BaseKind.elliptic, o.astype(nd), m.astype(nd), 0.0, dtype=dt)

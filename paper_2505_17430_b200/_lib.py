@@ -104,6 +104,7 @@ def lib() -> ctypes.CDLL:
         "evb_launch_count": (c_int, []),
         "evb_probe_peak_tflops": (c_int, [c_int, c_int, P(c_double)]),
         "evb_probe_umma_tf32_tflops": (c_int, [c_int, P(c_double)]),
+        "evb_probe_umma_f16_tflops": (c_int, [c_int, P(c_double)]),
         "evb_scratch_host_staging": (c_int, [c_void_p, ctypes.c_size_t, P(c_void_p)]),
     }
     for name, (res, args) in sig.items():
@@ -152,6 +153,13 @@ def probe_peak_tflops(which: int = 0, iters: int = 20000) -> float:
     """Measured FP64 DMMA (which=0) or FP32 FFMA (which=1) throughput of this GPU, TFLOP/s."""
     v = ctypes.c_double()
     check(lib().evb_probe_peak_tflops(which, iters, ctypes.byref(v)), "evb_probe_peak_tflops")
+    return float(v.value)
+
+
+def probe_umma_f16_tflops(n: int = 256) -> float:
+    """Measured dense tcgen05.mma kind::f16 throughput (M=128, N=n, K=16) of this GPU, TFLOP/s."""
+    v = ctypes.c_double()
+    check(lib().evb_probe_umma_f16_tflops(n, ctypes.byref(v)), "evb_probe_umma_f16_tflops")
     return float(v.value)
 
 

@@ -44,7 +44,8 @@ __global__ void __launch_bounds__(512) ffma_peak_kernel(float* out, int iters) {
 
 // tcgen05.mma kind::tf32 issue rate: one CTA per SM, one thread issues `iters` M=128 x N x K=8
 // MMAs into one TMEM accumulator from a zeroed SWIZZLE_128B tile (tools/umma_probe.cu's kernel)
-__global__ void __launch_bounds__(128) umma_tf32_peak_kernel(int iters, int N) {
+template <bool F16>
+__global__ void __launch_bounds__(128) umma_peak_kernel(int iters, int N) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar;
@@ -61,11 +62,13 @@ __global__ void __launch_bounds__(128) umma_tf32_peak_kernel(int iters, int N) {
   evb::umma::fence_after();
   const uint32_t tm = tslot;
   if (threadIdx.x == 0) {
-    const uint32_t idesc = evb::umma::idesc_tf32(128, N);
+    const uint32_t idesc = F16 ? evb::umma::idesc_f16(128, N) : evb::umma::idesc_tf32(128, N);
     const uint32_t a = evb::ptx::smem_u32(sm), b = evb::ptx::smem_u32(sm + 16384);
-    for (int i = 0; i < iters; ++i)
-      evb::umma::mma_tf32(tm, evb::umma::smem_desc(a + (i & 3) * 32), evb::umma::smem_desc(b + (i & 3) * 32), idesc,
-                          uint32_t(i));
+    for (int i = 0; i < iters; ++i) {
+      const uint64_t da = evb::umma::smem_desc(a + (i & 3) * 32), db = evb::umma::smem_desc(b + (i & 3) * 32);
+      if (F16) evb::umma::mma_f16(tm, da, db, idesc, uint32_t(i));  // K = 16 halves per instruction
+      else evb::umma::mma_tf32(tm, da, db, idesc, uint32_t(i));     // K = 8
+    }
     evb::umma::commit(&bar);
     evb::ptx::mbar_wait(&bar, 0);
   }
@@ -78,16 +81,25 @@ __global__ void __launch_bounds__(128) umma_tf32_peak_kernel(int iters, int N) {
 
 extern "C" EVB_API int evb_probe_peak_tflops(int which, int iters, double* tflops);
 extern "C" EVB_API int evb_probe_umma_tf32_tflops(int n, double* tflops);
+extern "C" EVB_API int evb_probe_umma_f16_tflops(int n, double* tflops);
 
-// dense kind::tf32 tcgen05 throughput at tile width n (64, 128 or 256): best of 3 timed launches
-extern "C" int evb_probe_umma_tf32_tflops(int n, double* tflops) {
+namespace {
+int probe_umma(bool f16, int n, double* tflops);
+}
+// dense kind::tf32 / kind::f16 tcgen05 throughput at tile width n (64, 128 or 256): best of 3 timed launches
+extern "C" int evb_probe_umma_tf32_tflops(int n, double* tflops) { return probe_umma(false, n, tflops); }
+extern "C" int evb_probe_umma_f16_tflops(int n, double* tflops) { return probe_umma(true, n, tflops); }
+
+namespace {
+int probe_umma(bool f16, int n, double* tflops) {
   try {
     if (!(n == 64 || n == 128 || n == 256)) return EVB_ERR_INVALID_ARGUMENT;
     int dev = 0, sms = 0;
     EVB_CUDA(cudaGetDevice(&dev));
     EVB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int smem = 65 * 1024;
-    EVB_CUDA(cudaFuncSetAttribute(umma_tf32_peak_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    EVB_CUDA(cudaFuncSetAttribute(umma_peak_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    EVB_CUDA(cudaFuncSetAttribute(umma_peak_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int iters = 4096;
     cudaEvent_t e0, e1;
     EVB_CUDA(cudaEventCreate(&e0));
@@ -95,14 +107,15 @@ extern "C" int evb_probe_umma_tf32_tflops(int n, double* tflops) {
     float best = 1e30f;
     for (int r = 0; r < 4; ++r) {
       EVB_CUDA(cudaEventRecord(e0));
-      umma_tf32_peak_kernel<<<sms, 128, smem>>>(iters, n);
+      if (f16) umma_peak_kernel<true><<<sms, 128, smem>>>(iters, n);
+      else umma_peak_kernel<false><<<sms, 128, smem>>>(iters, n);
       EVB_CUDA(cudaEventRecord(e1));
       EVB_CUDA(cudaEventSynchronize(e1));
       float ms = 0;
       EVB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
       if (r > 0 && ms < best) best = ms;
     }
-    *tflops = 2.0 * 128 * n * 8 * double(iters) * sms / (double(best) * 1e-3) / 1e12;
+    *tflops = 2.0 * 128 * n * (f16 ? 16 : 8) * double(iters) * sms / (double(best) * 1e-3) / 1e12;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     return EVB_OK;
@@ -110,6 +123,7 @@ extern "C" int evb_probe_umma_tf32_tflops(int n, double* tflops) {
     return EVB_ERR_RUNTIME;
   }
 }
+}  // namespace
 
 // which: 0 = FP64 DMMA m8n8k4, 1 = FP32 FFMA.  Best of 3 timed launches after a warm-up.
 extern "C" int evb_probe_peak_tflops(int which, int iters, double* tflops) {
