@@ -1788,11 +1788,13 @@ __global__ void __launch_bounds__(kRunThreads, 1) de_run_kernel(const de_run_arg
     }
     mark(1);
     // ---- C: trial genes (binomial, de_trial_kernel's arithmetic) ----
-    // thread = (owned individual, two Philox blocks = four gene words): its target / donor genes
-    // come straight from L2 (every load of the CTA in flight at once) while the words are computed
-    {
-      const int NB = D / 2 + 1;      // blocks covering D gene words at any offset parity
-      const int NB2 = (NB + 1) / 2;  // two blocks per thread
+    // thread = (owned individual, NBT Philox blocks = 2 NBT gene words): its target / donor genes
+    // come straight from L2 (every load of the CTA in flight at once) while the words are computed.
+    // One block per thread while the CTA has a thread per block (the shorter chain), else two.
+    auto trial = [&](auto nbt_tag) {
+      constexpr int NBT = decltype(nbt_tag)::value, NG = 2 * NBT;
+      const int NB = D / 2 + 1;              // blocks covering D gene words at any offset parity
+      const int NB2 = (NB + NBT - 1) / NBT;  // threads per individual
       for (int e = tid; e < nq * NB2; e += nthr) {
         const int q = e / NB2, b2 = e - q * NB2;
         const int i = i0 + q;
@@ -1800,16 +1802,16 @@ __global__ void __launch_bounds__(kRunThreads, 1) de_run_kernel(const de_run_arg
         const int64_t blk0 = s0 >> 1;
         const int64_t nblk = ((s0 + D + 1) >> 1) - blk0;
         const int ic = sQi[8 * q + 2];
-        const T* xi = d.pop + size_t(i) * d.ldp;
         const int ia = a_by_rank ? sIdx[sQi[8 * q + 0]] : sQi[8 * q + 0];
+        const T* xi = d.pop + size_t(i) * d.ldp;
         const T* xa = d.pop + size_t(ia) * d.ldp;
         const T* xb = d.pop + size_t(sQi[8 * q + 1]) * d.ldp;
         const T* xc = (ttpb && ic >= P) ? d.archive + size_t(ic - P) * d.ldt : d.pop + size_t(ic) * d.ldp;
-        int jj[4];
-        T gi[4], ga[4], gb[4], gc[4];
+        int jj[NG];
+        T gi[NG], ga[NG], gb[NG], gc[NG];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int64_t b = 2 * b2 + (u >> 1);
+        for (int u = 0; u < NG; ++u) {
+          const int64_t b = NBT * b2 + (u >> 1);
           const int64_t j64 = 2 * (blk0 + b) + (u & 1) - s0;
           const bool valid = b < nblk && j64 >= 0 && j64 < D;
           jj[u] = valid ? int(j64) : -1;
@@ -1822,12 +1824,13 @@ __global__ void __launch_bounds__(kRunThreads, 1) de_run_kernel(const de_run_arg
         const T Fi = sQf[2 * q];
         const double cr = double(sQf[2 * q + 1]);
         const int jr = sQi[8 * q + 3];
-        uint64_t w[4];
+        uint64_t w[NG];
         const uint64_t ctr = (uint64_t(gen) << 32) | uint32_t(i);
-        philox_pair(d.src.key, ctr, uint64_t(blk0 + 2 * b2), w[0], w[1]);
-        philox_pair(d.src.key, ctr, uint64_t(blk0 + 2 * b2 + 1), w[2], w[3]);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < NBT; ++u)
+          philox_pair(d.src.key, ctr, uint64_t(blk0 + NBT * b2 + u), w[2 * u], w[2 * u + 1]);
+#pragma unroll
+        for (int u = 0; u < NG; ++u) {
           const int j = jj[u];
           if (j < 0) continue;
           const T xij = gi[u];
@@ -1846,7 +1849,9 @@ __global__ void __launch_bounds__(kRunThreads, 1) de_run_kernel(const de_run_arg
           sS[q * D + j] = fop<T>::sub(v, a.shift[j]);  // x - o for the evaluation (eval_small's rounding)
         }
       }
-    }
+    };
+    if (nq * (D / 2 + 1) <= nthr) trial(std::integral_constant<int, 1>{});
+    else trial(std::integral_constant<int, 2>{});
     __syncthreads();
     mark(2);
     // ---- D: evaluation, eval_small_kernel's order ----
@@ -1959,14 +1964,13 @@ __global__ void __launch_bounds__(kRunThreads, 1) de_run_kernel(const de_run_arg
     // (needed once the archive is full: de/strategy.hpp:33-36) are computed while the other
     // CTAs' values arrive
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-    {
-      const int room0 = d.archive_cap - arch_size;
-      if (d.archive_cap > 0 && room0 < P && d.src.mode == RNG_PHILOX)
-        for (int t = tid; t < min(P - max(room0, 0), kVict); t += nthr)
-          sVict[t] = uint_of(philox_word(d.src.key, (uint64_t(gen) << 32) | kSubArchive, uint64_t(t)), d.archive_cap);
-    }
+    const int room0 = d.archive_cap - arch_size;
+    const bool victims = d.archive_cap > 0 && room0 < P && d.src.mode == RNG_PHILOX;  // CTA-uniform
+    if (victims)
+      for (int t = tid; t < min(P - max(room0, 0), kVict); t += nthr)
+        sVict[t] = uint_of(philox_word(d.src.key, (uint64_t(gen) << 32) | kSubArchive, uint64_t(t)), d.archive_cap);
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-    __syncthreads();
+    if (victims) __syncthreads();
     mark(4);
     // ---- F: every CTA resolves the whole selection in its own shared memory ----
     // thread = individual: win / success flags (de/engine.hpp:27-47), push and success indices by
@@ -1984,13 +1988,13 @@ __global__ void __launch_bounds__(kRunThreads, 1) de_run_kernel(const de_run_arg
     }
     for (int t = tid; t < d.archive_cap; t += nthr) sOwner[t] = -1;
     const unsigned wmask = __ballot_sync(0xffffffffu, wq), smask = __ballot_sync(0xffffffffu, sq);
-    if (lane == 0) {
+    if (lane == 0 && warp * 32 < P) {
       sWC[2 * warp] = __popc(wmask);
       sWC[2 * warp + 1] = __popc(smask);
     }
     __syncthreads();
     int pw = 0, ps = 0, tw = 0, ts = 0;
-    for (int k = 0; k < (nthr >> 5); ++k) {
+    for (int k = 0; k < (P + 31) / 32; ++k) {  // the warps that hold individuals
       const int a0 = sWC[2 * k], a1 = sWC[2 * k + 1];
       if (k < warp) {
         pw += a0;
@@ -2008,7 +2012,7 @@ __global__ void __launch_bounds__(kRunThreads, 1) de_run_kernel(const de_run_arg
       } else {
         const int n = qidx - max(room, 0);
         const uint64_t ctr_hi = (uint64_t(gen) << 32) | kSubArchive;
-        sl = n < kVict ? sVict[n] : uint_of(word_at(d.src, ctr_hi, int64_t(n), d.overflow), d.archive_cap);
+        sl = (victims && n < kVict) ? sVict[n] : uint_of(word_at(d.src, ctr_hi, int64_t(n), d.overflow), d.archive_cap);
       }
       atomicMax(&sOwner[sl], qidx);
     }
