@@ -37,7 +37,9 @@ struct evb_pso_s {
   void* pbest = nullptr;      // P x ldb
   void* pbest_fit = nullptr;  // P
   void* fit_new = nullptr;    // P (evaluation of the moved swarm)
-  int* nb = nullptr;          // P
+  int* nb = nullptr;          // P: neighbourhood bests used by the last generation
+  int* nb_next = nullptr;     // P: the next generation's, written by the personal-best kernel
+  int nb_valid = 0;           // nb_next matches pbest_fit (cleared by every other writer of pbest_fit)
   int prepared = 0;
   uint32_t last_gen = 0;
   evb_scratch_s* eval_scratch = nullptr;
@@ -383,6 +385,82 @@ __global__ void pso_pbest_kernel(const T* __restrict__ x, int64_t ldx, const T* 
   if (threadIdx.x == 0) pbf[i] = f;
 }
 
+// Personal bests after the evaluation AND the next generation's neighbourhood bests in one launch
+// (the generation boundary costs one dependent launch less).  Block i refreshes particle i exactly
+// as pso_pbest_kernel; the neighbourhood minima need every particle's refreshed pbest fitness,
+// which block i forms itself as pfn(j) = fnew[j] < pbf[j] ? fnew[j] : pbf[j] — the same value
+// whether block j has stored its pbf[j] yet or not (old pbf: the refresh rule; new pbf: it equals
+// fnew[j] or was left alone), so no grid-wide ordering is needed.  Ring: block i's thread 0, the
+// candidates and ties of pso_ring_kernel.  gbest: block 0 scans all particles with
+// pso_gbest_kernel's rule (index 0 when pfn(0) is NaN, else the (fitness, index) minimum over the
+// non-NaN entries) and writes every nb entry.
+template <typename T>
+__global__ void pso_pbest_nb_kernel(const T* __restrict__ x, int64_t ldx, const T* __restrict__ fnew, T* fit, T* pb,
+                                    int64_t ldb, T* pbf, int D, int P, int topology, int* nb, uint32_t* gen) {
+  ptx::griddep_wait();  // PDL (launch_pdl): predecessor data first
+  ptx::griddep_launch_dependents();
+  const int i = blockIdx.x;
+  if (i == 0 && threadIdx.x == 0) *gen += 1u;  // the update kernel (last reader) has finished
+  auto pfn = [&](int j) {
+    const T f = fnew[j], q = __ldcg(pbf + j);
+    return f < q ? f : q;
+  };
+  __shared__ T sf[32];
+  __shared__ int si[32];
+  if (topology == EVB_TOPO_GBEST) {
+    if (i == 0) {
+      T bf = T(0);
+      int bi = -1;
+      for (int j = threadIdx.x; j < P; j += blockDim.x) {
+        const T fj = pfn(j);
+        if (!isnan(fj)) argmin_merge(bf, bi, fj, j);
+      }
+      for (int off = 16; off > 0; off >>= 1) {
+        const T of = __shfl_xor_sync(0xffffffffu, bf, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        if (oi >= 0) argmin_merge(bf, bi, of, oi);
+      }
+      const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+      if (l == 0) {
+        sf[w] = bf;
+        si[w] = bi;
+      }
+      __syncthreads();
+      if (w == 0) {
+        const int nw = (blockDim.x + 31) >> 5;
+        bf = l < nw ? sf[l] : T(0);
+        bi = l < nw ? si[l] : -1;
+        for (int off = 16; off > 0; off >>= 1) {
+          const T of = __shfl_xor_sync(0xffffffffu, bf, off);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+          if (oi >= 0) argmin_merge(bf, bi, of, oi);
+        }
+        if (l == 0) si[0] = (bi < 0 || isnan(pfn(0))) ? 0 : bi;
+      }
+      __syncthreads();
+      const int best = si[0];
+      for (int j = threadIdx.x; j < P; j += blockDim.x) nb[j] = best;
+    }
+  } else if (threadIdx.x == 0) {
+    const int il = i == 0 ? P - 1 : i - 1, ir = i + 1 == P ? 0 : i + 1;
+    const T fl = pfn(il), f0 = pfn(i), fr = pfn(ir);
+    int best = il;
+    T bf = fl;
+    if (f0 < bf || (f0 == bf && i < best)) {
+      best = i;
+      bf = f0;
+    }
+    if (fr < bf || (fr == bf && ir < best)) best = ir;
+    nb[i] = best;
+  }
+  const T f = fnew[i];
+  if (threadIdx.x == 0) fit[i] = f;
+  if (!(f < pbf[i])) return;  // (block-uniform: pbf[i] is written by this block only, below)
+  for (int j = threadIdx.x; j < D; j += blockDim.x) pb[size_t(i) * ldb + j] = x[size_t(i) * ldx + j];
+  __syncthreads();
+  if (threadIdx.x == 0) pbf[i] = f;
+}
+
 template <typename T>
 __global__ void copy_rows_kernel(const T* src, int64_t lds, T* dst, int64_t ldd, int D) {
   const int i = blockIdx.x;
@@ -410,9 +488,18 @@ void generation_t(evb_pso_s* s, const device_problem* prob, evb_scratch_s* sc, v
                   int64_t ldv, void* fit, double lb, double ub, evb_rng_s* r, cudaStream_t st) {
   const T* pf = static_cast<const T*>(s->pbest_fit);
   s->phases.begin(st);
-  if (s->topology == EVB_TOPO_GBEST) EVB_CUDA(launch_pdl(pso_gbest_kernel<T>, dim3(1), dim3(1024), 0, st, pf, s->P, s->nb));
-  else EVB_CUDA(launch_pdl(pso_ring_kernel<T>, dim3((s->P + 255) / 256), dim3(256), 0, st, pf, s->P, s->nb));
-  count_launch();
+  // the last generation's personal-best kernel already formed this generation's neighbourhood
+  // bests (EVB_PSO_FUSE_NB=0 keeps the separate kernels, A/B)
+  static const bool fuse_nb = !(std::getenv("EVB_PSO_FUSE_NB") && std::atoi(std::getenv("EVB_PSO_FUSE_NB")) == 0);
+  if (fuse_nb && s->nb_valid) {
+    std::swap(s->nb, s->nb_next);
+  } else {
+    if (s->topology == EVB_TOPO_GBEST)
+      EVB_CUDA(launch_pdl(pso_gbest_kernel<T>, dim3(1), dim3(1024), 0, st, pf, s->P, s->nb));
+    else EVB_CUDA(launch_pdl(pso_ring_kernel<T>, dim3((s->P + 255) / 256), dim3(256), 0, st, pf, s->P, s->nb));
+    count_launch();
+  }
+  s->nb_valid = 0;
   s->phases.mark(st);
   pso_dev<T> d{};
   d.P = s->P;
@@ -482,9 +569,17 @@ void generation_t(evb_pso_s* s, const device_problem* prob, evb_scratch_s* sc, v
   eval_dispatch(rq);
   if (s->rec) recorder_observe(s->rec, s->rec_run, s->fit_new, s->P, st);  // particles in i (FE) order
   s->phases.mark(st);
-  EVB_CUDA(launch_pdl(pso_pbest_kernel<T>, dim3(s->P), dim3(std::min(256, int(round_up(s->D, 32)))), 0, st,
-                      static_cast<const T*>(X), ldx, static_cast<const T*>(s->fit_new), static_cast<T*>(fit),
-                      static_cast<T*>(s->pbest), s->ldb, static_cast<T*>(s->pbest_fit), s->D, r->d_gen));
+  if (fuse_nb) {
+    EVB_CUDA(launch_pdl(pso_pbest_nb_kernel<T>, dim3(s->P), dim3(std::min(256, int(round_up(s->D, 32)))), 0, st,
+                        static_cast<const T*>(X), ldx, static_cast<const T*>(s->fit_new), static_cast<T*>(fit),
+                        static_cast<T*>(s->pbest), s->ldb, static_cast<T*>(s->pbest_fit), s->D, s->P, s->topology,
+                        s->nb_next, r->d_gen));
+    s->nb_valid = 1;
+  } else {
+    EVB_CUDA(launch_pdl(pso_pbest_kernel<T>, dim3(s->P), dim3(std::min(256, int(round_up(s->D, 32)))), 0, st,
+                        static_cast<const T*>(X), ldx, static_cast<const T*>(s->fit_new), static_cast<T*>(fit),
+                        static_cast<T*>(s->pbest), s->ldb, static_cast<T*>(s->pbest_fit), s->D, r->d_gen));
+  }
   count_launch();
   s->phases.mark(st);
   EVB_CUDA(cudaGetLastError());
@@ -545,9 +640,10 @@ int evb_pso_create(int dtype, const evb_pso_config* c, int pop_size, int dim, ev
       EVB_CUDA(cudaMalloc(&s->pbest_fit, es * pop_size));
       EVB_CUDA(cudaMalloc(&s->fit_new, es * pop_size));
       EVB_CUDA(cudaMalloc(&s->nb, sizeof(int) * pop_size));
+      EVB_CUDA(cudaMalloc(&s->nb_next, sizeof(int) * pop_size));
       require(evb_scratch_create(&s->eval_scratch) == EVB_OK, "pso: scratch allocation failed");
     } catch (...) {
-      void* ptrs[] = {s->pbest, s->pbest_fit, s->fit_new, s->nb};
+      void* ptrs[] = {s->pbest, s->pbest_fit, s->fit_new, s->nb, s->nb_next};
       for (void* p : ptrs)
         if (p) cudaFree(p);
       delete s;
@@ -560,7 +656,7 @@ int evb_pso_create(int dtype, const evb_pso_config* c, int pop_size, int dim, ev
 int evb_pso_destroy(evb_pso s) {
   return guarded([&] {
     if (!s) return;
-    void* ptrs[] = {s->pbest, s->pbest_fit, s->fit_new, s->nb};
+    void* ptrs[] = {s->pbest, s->pbest_fit, s->fit_new, s->nb, s->nb_next};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (s->eval_scratch) evb_scratch_destroy(s->eval_scratch);
@@ -599,6 +695,7 @@ int evb_pso_prepare(evb_pso s, const void* X, int64_t ldx, const void* fitness, 
                                                     s->ldb, s->D);
     count_launch();
     EVB_CUDA(cudaMemcpyAsync(s->pbest_fit, fitness, es * s->P, cudaMemcpyDeviceToDevice, st));
+    s->nb_valid = 0;
     s->prepared = 1;
   });
 }
@@ -670,6 +767,7 @@ int evb_pso_optimize(evb_pso s, evb_problem objective, evb_scratch sc, void* X, 
                                                     s->ldb, s->D);
     count_launch();
     EVB_CUDA(cudaMemcpyAsync(s->pbest_fit, fitness, es * s->P, cudaMemcpyDeviceToDevice, st));
+    s->nb_valid = 0;
     s->prepared = 1;
     int64_t fes = s->P;
     int gens = 0;
@@ -740,6 +838,7 @@ int evb_pso_set_pbest(evb_pso s, const void* pbest_host, const void* pbest_fit_h
     EVB_CUDA(cudaDeviceSynchronize());
     EVB_CUDA(cudaMemcpy2D(s->pbest, s->ldb * es, pbest_host, s->D * es, s->D * es, s->P, cudaMemcpyHostToDevice));
     EVB_CUDA(copy_h2d_now(s->pbest_fit, pbest_fit_host, es * s->P));
+    s->nb_valid = 0;
     s->prepared = 1;
   });
 }
