@@ -347,7 +347,8 @@ int evb_scratch_host_staging(evb_scratch s, size_t bytes, void** out) {
 int evb_scratch_destroy(evb_scratch s) {
   return guarded([&] {
     if (!s) return;
-    void* ptrs[] = {s->partial, s->counters, s->zbuf, s->xpad, s->dx, s->dout, s->acc, s->s_hi, s->s_lo, s->gate};
+    void* ptrs[] = {s->partial, s->counters, s->zbuf, s->xpad, s->dx,  s->dout,
+                    s->acc,     s->s_hi,    s->s_lo, s->gate, s->row_bad};
     for (void* q : ptrs)
       if (q) cudaFree(q);
     if (s->own_stream) cudaStreamDestroy(s->own_stream);

@@ -85,6 +85,13 @@ struct fused_params {
   int tiles_nfast;  // multi kernel: blockIdx.x walks column tiles (row blocks form the waves)
   unsigned long long* dbg_ts;  // EVB_K1_TIMELINE=1 (tuning aid): per-CTA globaltimer phase stamps
   int dbg_skip;  // EVB_K2_SKIP (tuning aid, wrong results): bit 0 = no S split, bit 1 = no MMAs
+  // 3xFP16 range guard: rows with a non-finite or too large |x - o| are flagged by the split warps
+  // and recomputed in fp32 (the reference's mul / add order) by the row block's last CTA
+  int* row_bad;     // [P], zero between launches
+  const T* Xrows;   // the population (row pitch ldxr) and the unsplit rotation (row pitch ldm)
+  int64_t ldxr;
+  const T* rot;
+  int64_t ldm;
   int b_early;   // split-K fp32: the rotation split predates this launch, its first B slices may
                  // load before griddep_wait (they do not depend on the preceding kernel)
 };
@@ -1227,6 +1234,58 @@ __global__ void __launch_bounds__(umma_cfg<BN, FUSE>::THREADS, 1)
   if (warp == 1) umma::tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
+// 3xFP16 range guard, the rare path (kept out of line: the kernel's common path stays compact):
+// rows of row block m0 whose flag is set are recomputed by the 256 epilogue threads — z in fp32
+// with the reference's separate mul and add in k order (problems/batch.hpp:40-82), the channel
+// terms per 16-column chunk, the chunks combined in order, the usual final formula — and their
+// flags re-armed.  `scratch` holds a row of s, a row of z and the chunk partials.
+template <int BM>
+__device__ __noinline__ void f16_fixup_rows(const fused_params<float>& p, uint8_t* scratch, int m0, int etid) {
+
+  const int D = p.D, nchunk = (D + 15) / 16;
+  float* sS = reinterpret_cast<float*>(scratch);
+  float* sZ = sS + ((D + 3) & ~3);
+  float* sP = sZ + ((D + 3) & ~3);  // [n_ch][nchunk]
+  for (int rr2 = 0; rr2 < BM && m0 + rr2 < p.P; ++rr2) {
+    const int rw = m0 + rr2;
+    if (!__ldcg(p.row_bad + rw)) continue;  // the same word for every thread
+    for (int k = etid; k < D; k += 256) sS[k] = __fsub_rn(p.Xrows[size_t(rw) * p.ldxr + k], p.shift[k]);
+    ptx::named_bar_sync(1, 256);
+    for (int j = etid; j < D; j += 256) {
+      const float* mr = p.rot + size_t(j) * p.ldm;
+      float acc = 0.f;
+      for (int k = 0; k < D; ++k) acc = __fadd_rn(acc, __fmul_rn(mr[k], sS[k]));
+      sZ[j] = acc;
+    }
+    ptx::named_bar_sync(1, 256);
+    for (int e = etid; e < p.n_ch * nchunk; e += 256) {
+      const int ch = e / nchunk, c = e - ch * nchunk;
+      float v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = 16 * c + q < D ? sZ[16 * c + q] : 0.f;
+      const int term = p.ch_term[ch];
+      sP[e] = accumulate16_rt<float>(term, term_is_product(term) ? 1.f : 0.f, v, 16 * c, D, p.ell_w);
+    }
+    ptx::named_bar_sync(1, 256);
+    if (etid == 0) {
+      float chv[kMaxCh];
+      for (int ch = 0; ch < p.n_ch; ++ch) {
+        const bool prod = term_is_product(p.ch_term[ch]);
+        float v = sP[ch * nchunk];
+        for (int c = 1; c < nchunk; ++c) v = prod ? __fmul_rn(v, sP[ch * nchunk + c]) : __fadd_rn(v, sP[ch * nchunk + c]);
+        chv[ch] = v;
+      }
+      for (int o = 0; o < p.n_out; ++o) {
+        const float s0 = chv[p.out_ch0[o]];
+        const float s1 = p.out_ch1[o] >= 0 ? chv[p.out_ch1[o]] : 0.f;
+        p.out[o * p.ldo + rw] = finalize<float>(p.out_kind[o], s0, s1, D, float(p.out_bias[o]));
+      }
+      p.row_bad[rw] = 0;  // re-arm for the next launch
+    }
+    ptx::named_bar_sync(1, 256);
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // K2 on tcgen05, split-K (the default fp32 tensor-core path).  128 x BN output tile per CTA with
 // BN = 128 (N = 128 MMAs run at the tensor core's full rate; N = 64 reached ~60% of it), and the
@@ -1283,7 +1342,7 @@ struct umma_sk_cfg {
 template <int BN, bool ATMEM, bool F16 = false>
 __global__ void __launch_bounds__(umma_sk_cfg<BN, ATMEM, F16>::THREADS, 1)
     eval_f32_umma_sk_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmMhi,
-                            const __grid_constant__ CUtensorMap tmMlo, const fused_params<float> p) {
+                            const __grid_constant__ CUtensorMap tmMlo, const __grid_constant__ fused_params<float> p) {
   using C = umma_sk_cfg<BN, ATMEM, F16>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (static_cast<unsigned>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
@@ -1516,6 +1575,7 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN, ATMEM, F16>::THREADS, 1)
             const __half2 l23 = __floats2half2_rn(__fsub_rn(s2, f23.x), __fsub_rn(s3, f23.y));
             hw[2 * f] = *reinterpret_cast<const uint32_t*>(&h01);
             hw[2 * f + 1] = *reinterpret_cast<const uint32_t*>(&h23);
+
             lw[2 * f] = *reinterpret_cast<const uint32_t*>(&l01);
             lw[2 * f + 1] = *reinterpret_cast<const uint32_t*>(&l23);
           }
@@ -1639,22 +1699,36 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN, ATMEM, F16>::THREADS, 1)
         }
         xs[(half * kMaxCh + ch) * C::BM + r] = acc;
       }
+      if (etid == 0) flags[2] = 0;  // a flagged row in this CTA (3xFP16 range guard)
       ptx::named_bar_sync(1, 256);
       const int pt = blockIdx.y * nsk + kz;  // partial slot of this CTA's column block
-      if (half == 0 && row < p.P)
+      if (half == 0 && row < p.P) {
+        // 3xFP16 range guard: a coordinate whose fp16 head is inf / NaN (|x - o| >= 65520, or not
+        // finite) makes every z of its row non-finite, hence a non-finite channel sum here; such rows
+        // (and rows whose sums overflow anyway) are flagged for the last CTA's fp32 recomputation
+        bool nonfinite = false;
         for (int ch = 0; ch < p.n_ch; ++ch) {
           const float a0 = xs[ch * C::BM + r], a1 = xs[(kMaxCh + ch) * C::BM + r];
           const float v = term_is_product(p.ch_term[ch]) ? __fmul_rn(a0, a1) : __fadd_rn(a0, a1);
           p.partial[(size_t(ch) * p.n_ntiles + pt) * p.P + row] = v;
+          nonfinite = nonfinite || !(fabsf(v) <= 3.4e38f);
         }
+        if (F16 && nonfinite) {  // before the ticket's barrier and fence
+          p.row_bad[row] = 1;
+          flags[2] = 1;
+        }
+      }
       ptx::named_bar_sync(1, 256);
       if (etid == 0) {
         stamp(4);
         __threadfence();
-        const unsigned ticket = atomicAdd(&p.counters[blockIdx.x], 1u);
-        const int last = (ticket == unsigned(p.n_ntiles - 1)) ? 1 : 0;
+        // the ticket's high half counts the CTAs that flagged a row, so the last CTA of the row
+        // block learns "any flagged row" from the value the atomic returns (no extra round trip)
+        const unsigned ticket = atomicAdd(&p.counters[blockIdx.x], 1u + (unsigned(flags[2]) << 16));
+        const int last = ((ticket & 0xFFFFu) == unsigned(p.n_ntiles - 1)) ? 1 : 0;
         if (last) __threadfence();
         flags[1] = last;
+        if (ticket >> 16) flags[2] = 1;
       }
       ptx::named_bar_sync(1, 256);
       if (flags[1]) {
@@ -1719,6 +1793,12 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN, ATMEM, F16>::THREADS, 1)
           }
         }
         if (etid == 0) p.counters[blockIdx.x] = 0u;
+        if constexpr (F16) {
+          // rows the split warps flagged (any CTA of the row block, either K half): z in fp32 with
+          // the reference's separate mul and add in k order (problems/batch.hpp:40-82), the
+          // channel terms per 16-column chunk, chunks combined in order, the usual final formula
+          if (flags[2]) f16_fixup_rows<C::BM>(p, smem + C::RECV_BYTES + 8192, m0, etid);  // (published with flags[1])
+        }
       }
     }
   }
@@ -2098,7 +2178,11 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
       // EVB_F32_MMA=tf32 keeps the 3xTF32 MMAs; the default is the fp16 split (3xFP16, kind::f16)
       static const bool f16 = !(std::getenv("EVB_F32_MMA") && std::string(std::getenv("EVB_F32_MMA")) == "tf32");
       static const bool atmem_env = std::getenv("EVB_UMMA_ATMEM") && std::atoi(std::getenv("EVB_UMMA_ATMEM")) == 1;
-      const bool use16 = f16 && !atmem_env && UBN == 0;
+      static thread_local bool force_tf32 = false;  // set for the re-dispatch after a failed range check
+      // (z-store launches and very long rows keep 3xTF32: the range guard's fp32 fix-up lives in the
+      // fused epilogue and stages a row of s and z in the drained rings)
+      const bool use16 = f16 && !atmem_env && UBN == 0 && !force_tf32 && !(own_rot && pr->f16_unsafe) && !zstore &&
+                         D <= 8192;
       const bool split_cached = own_rot && (use16 ? pr->rot_hi16 != nullptr : pr->rot_hi != nullptr);
       fp.b_early = split_cached ? 1 : 0;
       if (use16) {
@@ -2134,16 +2218,52 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
         void* r16h = nullptr;
         void* r16l = nullptr;
         if (use16) {
+          // flagged-row buffer (zero between launches: the last CTA of a row block re-arms it)
+          if (sc->row_bad_n < size_t(P)) {
+            size_t cap = sc->row_bad_n * sizeof(int);
+            void* ptr = sc->row_bad;
+            ensure_buffer(&ptr, &cap, size_t(P) * sizeof(int), rq.stream);
+            sc->row_bad = static_cast<int*>(ptr);
+            sc->row_bad_n = cap / sizeof(int);
+            EVB_CUDA(cudaMemsetAsync(sc->row_bad, 0, cap, rq.stream));
+          }
+          fp.row_bad = sc->row_bad;
+          fp.Xrows = static_cast<const float*>(X);
+          fp.ldxr = ldx;
+          fp.rot = static_cast<const float*>(rotation);
+          fp.ldm = ldm;
           if (own_rot && pr->rot_hi16) {
             r16h = pr->rot_hi16;
             r16l = pr->rot_lo16;
           } else {
             EVB_CUDA(cudaMalloc(&r16h, mel * sizeof(__half)));
             EVB_CUDA(cudaMalloc(&r16l, mel * sizeof(__half)));
+            // (one synchronous range check per problem: a rotation whose 2^8-scaled entries leave
+            // fp16's range keeps the 3xTF32 kernel)
+            EVB_CUDA(cudaMemsetAsync(sc->row_bad, 0, sizeof(int), rq.stream));
             split_f16_kernel<<<int(std::min<int64_t>(2048, (mel + 255) / 256)), 256, 0, rq.stream>>>(
-                static_cast<const float*>(rotation), mel, static_cast<__half*>(r16h), static_cast<__half*>(r16l));
+                static_cast<const float*>(rotation), mel, static_cast<__half*>(r16h), static_cast<__half*>(r16l),
+                sc->row_bad);
             count_launch();
-            if (own_rot) {
+            int oor = 0;
+            EVB_CUDA(cudaMemcpyAsync(&oor, sc->row_bad, sizeof(int), cudaMemcpyDeviceToHost, rq.stream));
+            EVB_CUDA(cudaStreamSynchronize(rq.stream));
+            if (oor) {
+              EVB_CUDA(cudaMemsetAsync(sc->row_bad, 0, sizeof(int), rq.stream));
+              cudaFree(r16h);
+              cudaFree(r16l);
+              r16h = r16l = nullptr;
+              if (own_rot) pr->f16_unsafe = true;
+              force_tf32 = true;  // this call again, on the 3xTF32 kernel
+              try {
+                gemm_eval<T>(rq, X, ldx, zstore, zbuf, ldz, shift, rotation, ldm, P, D);
+              } catch (...) {
+                force_tf32 = false;
+                throw;
+              }
+              force_tf32 = false;
+              return;
+            } else if (own_rot) {
               pr->rot_hi16 = r16h;
               pr->rot_lo16 = r16l;
             }

@@ -113,6 +113,7 @@ struct device_problem {
   void* rot_lo = nullptr;
   void* rot_hi16 = nullptr;  // fp16 split of 2^8 * rotation (the 3xFP16 kernel), built on first use
   void* rot_lo16 = nullptr;
+  bool f16_unsafe = false;   // the scaled rotation leaves fp16's range: this problem stays on 3xTF32
 };
 
 }  // namespace evb
@@ -154,6 +155,10 @@ struct evb_scratch_s {
   // composition: value accumulators (double) per point
   double* acc = nullptr;
   size_t acc_bytes = 0;
+  // fp32 3xFP16 path: rows whose S = X - o leaves fp16's range (recomputed in fp32 by the row
+  // block's last CTA); zero between launches
+  int* row_bad = nullptr;
+  size_t row_bad_n = 0;
   // fp32 tensor-core path: TF32 split of S = X - o
   void* s_hi = nullptr;
   size_t s_hi_bytes = 0;

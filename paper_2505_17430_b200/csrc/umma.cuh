@@ -191,14 +191,18 @@ __global__ void split_plain_kernel(const float* __restrict__ a, int64_t n, float
 // it lifts the remainder of typical entries out of fp16's subnormal range), hi = fp16(a'),
 // lo = fp16(a' - hi): 22 significant bits, as the TF32 split
 constexpr float kF16Scale = 256.f;
+constexpr float kF16SafeMax = 65000.f;  // |value| up to here has a finite fp16 head
 __global__ void split_f16_kernel(const float* __restrict__ a, int64_t n, __half* __restrict__ hi,
-                                 __half* __restrict__ lo) {
+                                 __half* __restrict__ lo, int* __restrict__ out_of_range) {
+  bool bad = false;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
     const float x = __fmul_rn(a[e], kF16Scale);
+    bad = bad || !(fabsf(x) <= kF16SafeMax);  // also NaN
     const __half h = __float2half_rn(x);
     hi[e] = h;
     lo[e] = __float2half_rn(__fsub_rn(x, __half2float(h)));
   }
+  if (bad) *out_of_range = 1;
 }
 #endif  // EVB_UMMA_HELPERS_ONLY
 

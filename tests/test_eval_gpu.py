@@ -476,3 +476,50 @@ np.save(sys.argv[1], np.concatenate(res))
             got[bm] = np.load(f)
     assert np.array_equal(got["64"].view(np.uint64), got["128"].view(np.uint64))
     assert np.all(np.isfinite(got["128"]))
+
+
+@pytest.mark.parametrize("dim", [300, 1000])
+def test_f32_tensor_core_range_guard(dev, dim):
+    """The 3xFP16 kernel's fp16 heads hold |x - o| < 65504.  Rows beyond that (or with a NaN / inf
+    coordinate) are flagged by the split warps and recomputed in fp32 by the row block's last CTA:
+    rows scaled 1e3 and 1e5 out of the search domain, a NaN and two inf coordinates, next to
+    ordinary rows, against the fp64 restatement of the same float inputs (1e-4 relative, NaN / inf
+    positions identical); a second launch on the same scratch (flags re-armed) with ordinary rows
+    only; and a rotation whose scaled entries leave fp16's range (the problem stays on 3xTF32)."""
+    o, m = O.shift_rotation(7, dim)
+    X = O.population(8, 200, dim).astype(np.float32)
+    X[1] *= 1e3
+    X[130] *= 1e5
+    X[5, 7] = np.nan
+    X[6, 11] = np.inf
+    X[199, 0] = -np.inf
+    o32, m32 = o.astype(np.float32), m.astype(np.float32)
+    sc = evb.EvalScratch()
+    for kind in (K.elliptic, K.rastrigin, K.ackley, K.sphere):
+        p = evb.ProblemInstance.base(kind, o32, m32, 1.5, dtype=evb.EVB_F32)
+        for Xc in (X, O.population(9, 200, dim).astype(np.float32)):
+            out = torch.empty(Xc.shape[0], dtype=torch.float32, device=dev)
+            evb.evaluate_batch(p, torch.from_numpy(Xc).to(dev), sc, out)
+            torch.cuda.synchronize()
+            got = out.cpu().numpy().astype(np.float64)
+            with np.errstate(all="ignore"):
+                ref = O.eval_batch(int(kind), o32.astype(np.float64), m32.astype(np.float64), 1.5, Xc.astype(np.float64))
+            assert np.array_equal(np.isnan(got), np.isnan(ref)), kind
+            assert np.array_equal(np.isinf(got), np.isinf(ref)), kind
+            fin = np.isfinite(ref)
+            if kind == K.ackley and Xc is X:
+                # far out the float spacing of z (~0.01 at 1e5) exceeds the period of cos(2 pi z):
+                # the cosine sum of those rows is noise in any fp32 evaluation, only finiteness holds
+                assert np.all(np.isfinite(got[[1, 130]]))
+                fin[[1, 130]] = False
+            assert rel_err(got[fin], ref[fin]) <= 1e-4, (kind, rel_err(got[fin], ref[fin]))
+    # rotation entries of 1e3: 2^8 * 1e3 is not an fp16 number
+    big = (m * 1e3).astype(np.float32)
+    p = evb.ProblemInstance.base(K.elliptic, o32, big, 0.0, dtype=evb.EVB_F32)
+    Xc = O.population(9, 200, dim).astype(np.float32)
+    out = torch.empty(200, dtype=torch.float32, device=dev)
+    for _ in range(2):
+        evb.evaluate_batch(p, torch.from_numpy(Xc).to(dev), sc, out)
+    torch.cuda.synchronize()
+    ref = O.eval_batch(int(K.elliptic), o32.astype(np.float64), big.astype(np.float64), 0.0, Xc.astype(np.float64))
+    assert rel_err(out.cpu().numpy().astype(np.float64), ref) <= 1e-4
