@@ -1327,7 +1327,11 @@ struct umma_sk_cfg {
   static constexpr int O_OFF = B_OFF + NB * B_BYTES;
   static constexpr int NSLOT = ATMEM ? NX : NA;  // stages carrying an X slice + its shift values
   static constexpr int RING_BYTES = O_OFF + NSLOT * KB * 4;
-  static constexpr int NBAR = NSLOT + 2 * NA + 2 * NB + NX + 1;
+  static constexpr int NBAR = NSLOT + 2 * NA + 2 * NB + NX + 3;
+  // K halves exchange z by point-to-point mbarriers instead of two cluster-wide barriers: the
+  // receive buffer is exactly A stage 0, which its owner's MMAs leave several slices before its
+  // mainloop ends (P2P; the TMEM-operand variant keeps the cluster barriers)
+  static constexpr bool P2P = !ATMEM;
   static constexpr int THREADS = 11 * 32;  // X producer, MMA, 8 split / epilogue warps, B producer
   static constexpr int TMEM_COLS = ATMEM ? 512 : 2 * BN;
   static constexpr uint32_t TA = 2 * BN;  // first A column (ATMEM)
@@ -1353,7 +1357,9 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN, ATMEM, F16>::THREADS, 1)
   uint64_t* bempty = bfull + C::NB;
   uint64_t* xempty = bempty + C::NB;  // ATMEM: the split warps read the X slot
   uint64_t* accfull = xempty + C::NX;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accfull + 1);
+  uint64_t* peer_free = accfull + 1;  // the K peer's MMAs have left its A stage 0 (= its receive buffer)
+  uint64_t* recv_full = accfull + 2;  // the K peer's 256 epilogue threads delivered their z halves
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accfull + 3);
   int* flags = reinterpret_cast<int*>(tmem_slot + 1);  // [1]: last column block of the row block
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1390,6 +1396,8 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN, ATMEM, F16>::THREADS, 1)
       ptx::mbar_init(&bempty[s], 2);  // both CTAs of the M pair consumed the slot
     }
     ptx::mbar_init(accfull, 1);
+    ptx::mbar_init(peer_free, 1);
+    ptx::mbar_init(recv_full, 256);
     ptx::fence_mbar_init();
   }
   if (warp == 1) umma::tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -1492,6 +1500,8 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN, ATMEM, F16>::THREADS, 1)
         }
         umma::commit(&aempty[sa]);
         umma::commit_mc(&bempty[sb], pair_mask);  // the slot is freed in both CTAs of the M pair
+        // A stage 0 is read for the last time by slice kb: tell the K peer it may deliver
+        if (C::P2P && nsk > 1 && sa == 0 && kb + C::NA >= KT) umma::commit_mc(peer_free, uint16_t(1u << (crank ^ 2u)));
       }
       umma::commit(accfull);
     }
@@ -1647,7 +1657,8 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN, ATMEM, F16>::THREADS, 1)
     float* recv = reinterpret_cast<float*>(smem);  // [BM][BN/2] in the drained rings (nsk == 2)
     auto rchunk = [&](int rr, int ch16) { return rr * (BN / 2) + 4 * ((ch16 & ~7) | ((ch16 & 7) ^ (rr & 7))); };
     if (nsk > 1) {
-      ptx::cluster_sync_all();  // both CTAs past their mainloops: the peer's rings are drained
+      if constexpr (C::P2P) ptx::mbar_wait_cluster(peer_free, 0);  // the peer's stage 0 is free
+      else ptx::cluster_sync_all();  // both CTAs past their mainloops: the peer's rings are drained
       const int snd0 = (1 - kz) * OWN + half * TW;  // tile columns sent to the peer
       const uint32_t peer = ptx::mapa(ptx::smem_u32(recv), crank ^ 2u);  // the other K half
 #pragma unroll 1
@@ -1661,7 +1672,15 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN, ATMEM, F16>::THREADS, 1)
         }
       }
     }
-    if (nsk > 1) ptx::cluster_sync_all();  // every thread of both CTAs (warps 0-1 join below)
+    if (nsk > 1) {
+      if constexpr (C::P2P) {
+        // every sender releases its stores on the peer's barrier; then wait for the peer's 256
+        ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(recv_full), crank ^ 2u));
+        ptx::mbar_wait_cluster(recv_full, 0);
+      } else {
+        ptx::cluster_sync_all();  // every thread of both CTAs (warps 0-1 join below)
+      }
+    }
     if (etid == 0) stamp(2);  // the K halves exchanged
     auto loadz = [&](int c0, float (&v)[16]) {  // z of owned columns [own0 + half*TW + c0, +16)
       load16(own0 + half * TW + c0, v);
@@ -1802,7 +1821,7 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN, ATMEM, F16>::THREADS, 1)
       }
     }
   }
-  if ((warp < 2 || warp == 10) && nsk > 1) {  // the producer / MMA warps join both exchange barriers
+  if (!C::P2P && (warp < 2 || warp == 10) && nsk > 1) {  // the producer / MMA warps join both exchange barriers
     ptx::cluster_sync_all();
     ptx::cluster_sync_all();
   }
