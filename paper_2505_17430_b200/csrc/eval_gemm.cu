@@ -13,7 +13,8 @@
 //       fp64: DMMA m8n8k4 tensor-core tiles (the only FP64 tensor route on sm_100a;
 //             tcgen05 has no f64 kind), operands as conflict-free LDS.128 pairs
 //             (k order permuted inside each 16-deep slice, dmma_kslice);
-//       fp32: 3xTF32 on tcgen05 with TMEM accumulators (umma.cuh), or FFMA register-tiled
+//       fp32: a three-product split (3xFP16 by default, 3xTF32 selectable) on tcgen05 with TMEM
+//       accumulators (umma.cuh), or FFMA register-tiled
 //             outer products for discus / hybrids / compositions (1xTF32 fails the 1e-4
 //             tolerance);
 //   * epilogue: per-element transform terms (elliptic / rastrigin / ackley / sphere /
@@ -2174,7 +2175,7 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
     BM = 64;
     BN = 128;
   }
-  // fp32 tensor-core path (3xTF32, main product and corrections in separate TMEM accumulators):
+  // fp32 tensor-core path (3xFP16 / 3xTF32, main product and corrections in separate TMEM accumulators):
   // measured fitness error <= 1e-5 relative for every base kind except discus, whose value is
   // dominated by 1e6 * z0^2 and amplifies the tensor-core accumulation error to ~1e-4; discus,
   // hybrids (chunks may be discus) and compositions stay on the FFMA kernel.
@@ -2184,7 +2185,7 @@ void gemm_eval(const eval_request& rq, const void* X, int64_t ldx, bool zstore, 
   if (force32) umma32 = std::string(force32) == "umma" && !std::is_same<T, double>::value;
   if constexpr (!std::is_same<T, double>::value) {
     if (umma32) {
-      // ---- fp32 on tcgen05: 3xTF32, 128 x UBN tiles ----
+      // ---- fp32 on tcgen05: three-product split, 128 x UBN tiles ----
       static const char* ubn_env = std::getenv("EVB_UMMA_BN");
       // default: the split-K kernel with 128 x 128 tiles (EVB_UMMA_BN=64 / 128 / 256 selects the
       // single-K-range kernels)
