@@ -411,9 +411,18 @@ __global__ void pso_pbest_nb_kernel(const T* __restrict__ x, int64_t ldx, const 
     if (i == 0) {
       T bf = T(0);
       int bi = -1;
-      for (int j = threadIdx.x; j < P; j += blockDim.x) {
-        const T fj = pfn(j);
-        if (!isnan(fj)) argmin_merge(bf, bi, fj, j);
+      for (int j0 = threadIdx.x; j0 < P; j0 += 4 * blockDim.x) {  // four particles' loads in flight
+        T fj[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = j0 + u * blockDim.x;
+          fj[u] = j < P ? pfn(j) : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = j0 + u * blockDim.x;
+          if (j < P && !isnan(fj[u])) argmin_merge(bf, bi, fj[u], j);
+        }
       }
       for (int off = 16; off > 0; off >>= 1) {
         const T of = __shfl_xor_sync(0xffffffffu, bf, off);
