@@ -104,10 +104,15 @@ struct fused_params {
 // config-1 fp32 batch, measured).
 template <typename T>
 __device__ __forceinline__ T epi_cos(T x) { return trig<T, true>::cos_(x); }
+// (out of line: inlined, the compiler predicates this double-precision polynomial into every
+// element's straight-line code — ~2 us of FP64 pipe per config-1 fp32 Rastrigin epilogue)
+__device__ __noinline__ float epi_cos_far(float x) { return trig<float, true>::cos_(x); }
 template <>
 __device__ __forceinline__ float epi_cos<float>(float x) {
-  if (!(fabsf(x) < 1.0e5f)) return trig<float, true>::cos_(x);
-  const float k = rintf(x * 0.159154943091895336f);
+  if (!(fabsf(x) < 1.0e5f)) return epi_cos_far(x);
+  // rint by the 1.5 * 2^23 trick (|x / 2 pi| < 2^22 here): two full-rate adds instead of a
+  // quarter-rate FRND
+  const float k = __fadd_rn(__fadd_rn(x * 0.159154943091895336f, 12582912.f), -12582912.f);
   float r = fmaf(-k, 6.28125f, x);
   r = fmaf(-k, 1.93530717958647692e-3f, r);
   return __cosf(r);
