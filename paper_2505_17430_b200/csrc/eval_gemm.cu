@@ -1713,7 +1713,29 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN, ATMEM, F16>::THREADS, 1)
       }
     } else {
       float* xs = reinterpret_cast<float*>(smem + C::RECV_BYTES);  // drained rings: [half][ch][row]
-      for (int ch = 0; ch < p.n_ch; ++ch) {
+      // two-channel kinds (Ackley, Griewank, bent cigar): both channels in one pass over z (one
+      // TMEM / receive-buffer read per chunk instead of one per channel)
+      const bool pair = p.n_ch == 2;
+      if (pair) {
+        const int t0 = p.ch_term[0], t1 = p.ch_term[1];
+        float a0 = term_is_product(t0) ? 1.f : 0.f, a1 = term_is_product(t1) ? 1.f : 0.f;
+#pragma unroll 1
+        for (int c0 = 0; c0 < TW; c0 += 16) {
+          float v[16];
+          loadz(c0, v);
+          const int col0 = n0 + own0 + half * TW + c0;
+          if (t0 == TERM_SQ && t1 == TERM_COS) {  // Ackley: no per-chunk switch (CTA-uniform branch)
+            a0 = accumulate16<TERM_SQ>(a0, v, col0, p.D, p.ell_w);
+            a1 = accumulate16<TERM_COS>(a1, v, col0, p.D, p.ell_w);
+          } else {
+            a0 = accumulate16_rt<float>(t0, a0, v, col0, p.D, p.ell_w);
+            a1 = accumulate16_rt<float>(t1, a1, v, col0, p.D, p.ell_w);
+          }
+        }
+        xs[(half * kMaxCh + 0) * C::BM + r] = a0;
+        xs[(half * kMaxCh + 1) * C::BM + r] = a1;
+      }
+      for (int ch = 0; ch < (pair ? 0 : p.n_ch); ++ch) {
         const int term = p.ch_term[ch];
         float acc = term_is_product(term) ? 1.f : 0.f;
 #pragma unroll 1
