@@ -1779,18 +1779,18 @@ __global__ void __launch_bounds__(umma_sk_cfg<BN, ATMEM, F16>::THREADS, 1)
       }
       ptx::named_bar_sync(1, 256);
       if (flags[1]) {
-        auto chain = [&](int ch, int rw) {
+        auto chain = [&](int ch, int rw) {  // column blocks in order, sixteen loads per L2 round
           const bool prod = term_is_product(p.ch_term[ch]);
           const float* src = p.partial + size_t(ch) * p.n_ntiles * p.P + rw;
-          float v = __ldcg(src);
-          for (int t0 = 1; t0 < p.n_ntiles; t0 += 8) {
-            float x[8];
+          float v = prod ? 1.f : 0.f;
+          for (int t0 = 0; t0 < p.n_ntiles; t0 += 16) {
+            float x[16];
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
+            for (int q = 0; q < 16; ++q)
               if (t0 + q < p.n_ntiles) x[q] = __ldcg(src + size_t(t0 + q) * p.P);
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-              if (t0 + q < p.n_ntiles) v = prod ? __fmul_rn(v, x[q]) : __fadd_rn(v, x[q]);
+            for (int q = 0; q < 16; ++q)
+              if (t0 + q < p.n_ntiles) v = (t0 + q == 0) ? x[q] : (prod ? __fmul_rn(v, x[q]) : __fadd_rn(v, x[q]));
           }
           return v;
         };
