@@ -107,15 +107,19 @@ __device__ __forceinline__ T epi_cos(T x) { return trig<T, true>::cos_(x); }
 // (out of line: inlined, the compiler predicates this double-precision polynomial into every
 // element's straight-line code — ~2 us of FP64 pipe per config-1 fp32 Rastrigin epilogue)
 __device__ __noinline__ float epi_cos_far(float x) { return trig<float, true>::cos_(x); }
-template <>
-__device__ __forceinline__ float epi_cos<float>(float x) {
-  if (!(fabsf(x) < 1.0e5f)) return epi_cos_far(x);
+// |x| < 1e5 (the caller's promise: no test here, so sixteen of these stay one straight-line block)
+__device__ __forceinline__ float epi_cos_near(float x) {
   // rint by the 1.5 * 2^23 trick (|x / 2 pi| < 2^22 here): two full-rate adds instead of a
   // quarter-rate FRND
   const float k = __fadd_rn(__fadd_rn(x * 0.159154943091895336f, 12582912.f), -12582912.f);
   float r = fmaf(-k, 6.28125f, x);
   r = fmaf(-k, 1.93530717958647692e-3f, r);
   return __cosf(r);
+}
+template <>
+__device__ __forceinline__ float epi_cos<float>(float x) {
+  if (!(fabsf(x) < 1.0e5f)) return epi_cos_far(x);
+  return epi_cos_near(x);
 }
 
 // cos(2 pi v) of the Rastrigin / Ackley terms.  fp64 fast form: the period is taken out exactly
@@ -135,10 +139,19 @@ template <>
 __device__ __forceinline__ double epi_cos2pi<double, false>(double v) {
   return cos2pi_fast(v);
 }
-// arguments the fast form may not take (fp64 only): |v| >= 2^16, inf (NaN passes through it)
+// fp32: EXACT = false promises |v| < 15000 (|2 pi v| < 1e5) and skips the per-element range test —
+// a branch per element splits the unrolled epilogue into one basic block per element and
+// serialises the sixteen cosine chains (~1.3 us per config-1 Rastrigin launch)
+template <>
+__device__ __forceinline__ float epi_cos2pi<float, false>(float v) {
+  return epi_cos_near(__fmul_rn(two_pi_v<float>(), v));
+}
+// arguments the fast forms may not take: fp64 |v| >= 2^16 or inf (NaN passes through the fast form);
+// fp32 |v| >= 15000 or not finite
 template <typename T>
 __device__ __forceinline__ bool cos2pi_needs_exact(T v) {
-  return std::is_same<T, double>::value && fabs(double(v)) >= 65536.0;
+  if (std::is_same<T, double>::value) return fabs(double(v)) >= 65536.0;
+  return !(fabsf(float(v)) < 15000.f);
 }
 
 template <typename T, bool EXACT = false>
@@ -166,16 +179,41 @@ __device__ __forceinline__ bool term_is_product(int term) { return term == TERM_
 template <int TERM, typename T>
 __device__ __forceinline__ T accumulate16(T acc, const T (&v)[16], int col0, int D, const T* ell_w) {
   constexpr bool prod = TERM == TERM_GCOS;
+  constexpr bool has_cos2pi = TERM == TERM_RAST || TERM == TERM_COS;
+  // one range test for the sixteen values (no per-element branch): the exact forms for all of
+  // them if any needs it, else the fast forms as one straight-line block
+  if constexpr (has_cos2pi) {
+    bool far = false;
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    const int col = col0 + q;
-    if (col < D) {
-      const T t = cos2pi_needs_exact(v[q]) ? term_value<T, true>(TERM, v[q], col, ell_w)
-                                           : term_value<T, false>(TERM, v[q], col, ell_w);
-      acc = prod ? fop<T>::mul(acc, t) : fop<T>::add(acc, t);
+    for (int q = 0; q < 16; ++q) far = far || (col0 + q < D && cos2pi_needs_exact(v[q]));
+    if (far) {  // (unrolled: a loop over q, or passing v by reference, would move v to local memory)
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int col = col0 + q;
+        if (col < D) acc = fop<T>::add(acc, term_value<T, true>(TERM, v[q], col, ell_w));
+      }
+      return acc;
     }
+    // straight-line: the cosine chains of the sixteen values overlap
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int col = col0 + q;
+      const T t = term_value<T, false>(TERM, v[q], col < D ? col : 0, ell_w);
+      const T a1 = fop<T>::add(acc, t);
+      acc = col < D ? a1 : acc;
+    }
+    return acc;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int col = col0 + q;
+      if (col < D) {
+        const T t = term_value<T, false>(TERM, v[q], col, ell_w);
+        acc = prod ? fop<T>::mul(acc, t) : fop<T>::add(acc, t);
+      }
+    }
+    return acc;
   }
-  return acc;
 }
 template <typename T>
 __device__ __forceinline__ T accumulate16_rt(int term, T acc, const T (&v)[16], int col0, int D, const T* ell_w) {
@@ -244,7 +282,7 @@ __device__ __forceinline__ void epilogue_rows(const fused_params<T>& p, const T*
     else cw[cc] = T(0);
   }
   const uint32_t zs = static_cast<uint32_t>(__cvta_generic_to_shared(zt));
-  constexpr bool has_cos2pi = std::is_same<T, double>::value && (TERM == TERM_RAST || TERM == TERM_COS);
+  constexpr bool has_cos2pi = TERM == TERM_RAST || TERM == TERM_COS;
   for (int r0 = 0; r0 < rpw; r0 += 8) {
     T s[8];
 #pragma unroll
@@ -340,7 +378,7 @@ __device__ __forceinline__ void epilogue_rows_sqcos(const fused_params<T>& p, co
       }
     };
     bool big = false;
-    if constexpr (std::is_same<T, double>::value) {
+    {
 #pragma unroll
       for (int cc = 0; cc < CPL; ++cc)
 #pragma unroll
